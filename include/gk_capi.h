@@ -1,0 +1,257 @@
+/* gk_capi.h — C-ABI of the B200 gradkrig hot path (libgk_b200.so).
+ *
+ * Drop-in boundary for the reference's core operator/solver API
+ * (reference: proj/core/include/gradkrig/{linear_operator,dski,dskip,linalg}.hpp,
+ * SPEC.md modules dski/dskip/linalg). Plain pointers and sizes only; no torch,
+ * Eigen or CUDA types in the signatures (streams are passed as void*).
+ *
+ * Conventions (same as the reference):
+ *   - X is n×d column-major (Eigen default; X.col(j) contiguous).
+ *   - Operator vectors are derivative-type-major [f; d_1 f; ...; d_d f]
+ *     (reference kernels.hpp:94-97, observations.hpp:27-35).
+ *   - Multi-RHS blocks are column-major N×nrhs with leading dimension ld.
+ *   - Host pointers are borrowed for the duration of the call. Handles own
+ *     their device memory and are freed by gk_*_destroy.
+ *   - Every entry returns a gk_status; gk_last_error() gives the message
+ *     (thread-local). Handles are immutable after creation and the const
+ *     entry points are safe to call from several host threads (each call
+ *     takes the handle's scratch under a mutex, like the reference's FFTW
+ *     planner lock dski.cpp:14-17, and runs on its own stream).
+ *   - Entry points with the _dev suffix take device pointers and a CUDA
+ *     stream (cudaStream_t passed as void*; NULL = legacy default stream) and
+ *     are asynchronous with respect to the host.
+ */
+#ifndef GK_CAPI_H
+#define GK_CAPI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes; each maps to the reference exception named. */
+typedef enum {
+  GK_OK = 0,
+  GK_ERR_ARG = 1,         /* std::invalid_argument (e.g. dski.cpp:230, linalg.cpp:180-181) */
+  GK_ERR_RANGE = 2,       /* std::out_of_range (dski.cpp:293, dskip.cpp:260)               */
+  GK_ERR_OUT_OF_GRID = 3, /* gradkrig::OutOfGridError (interpolation.cpp:90-95)            */
+  GK_ERR_RUNTIME = 4,     /* std::runtime_error (linalg.cpp:165-167, gp.cpp:151-156)       */
+  GK_ERR_LOGIC = 5,       /* std::logic_error (linear_operator.cpp:7-13)                   */
+  GK_ERR_LENGTH = 6,      /* std::length_error (kernels.cpp:252-255)                       */
+  GK_ERR_CUDA = 7,        /* CUDA runtime failure (no reference equivalent)                */
+  GK_ERR_NCCL = 8,
+  GK_ERR_UNSUPPORTED = 9  /* configuration the B200 path does not implement (reported, never
+                             silently routed elsewhere)                                     */
+} gk_status;
+
+const char* gk_last_error(void);
+/* Index of the offending point after GK_ERR_OUT_OF_GRID, else -1. */
+int64_t gk_last_error_point(void);
+const char* gk_version(void);
+/* Number of CUDA kernels this library has launched in this process. */
+int64_t gk_kernel_launch_count(void);
+
+/* ---------------------------------------------------------------- kernel spec
+ * KernelSpec (reference kernels.hpp:42-75). family 0 = squared exponential,
+ * 1 = spline (spline is accepted by the dense paths only; grid operators
+ * return GK_ERR_UNSUPPORTED for it in this build). */
+typedef struct {
+  int family;
+  double lengthscale;
+  double outputscale;
+  double spline_a, spline_b;
+  int spline_even;
+} gk_kernel;
+
+/* Grid (reference interpolation.hpp:13-35); dims/origin/spacing length d. */
+typedef struct {
+  int d;
+  int dims[8];
+  double origin[8];
+  double spacing[8];
+} gk_grid;
+
+/* Grid::cover (interpolation.cpp:117-146). Host-only. */
+gk_status gk_grid_cover(const double* X, int64_t n, int d, double target_spacing,
+                        int margin_cells, int max_nodes, gk_grid* out);
+
+/* rng.hpp:12-38 (host; identical streams to the reference's libstdc++ build). */
+uint64_t gk_mix_seed(uint64_t seed, uint64_t stream);
+void gk_rademacher_vector(int64_t n, uint64_t seed, uint64_t stream, double* out);
+void gk_gaussian_vector(int64_t n, uint64_t seed, uint64_t stream, double* out);
+
+/* ---------------------------------------------------------------- operators
+ * Every structured operator is a gk_op (LinearOperator, linear_operator.hpp:12-35). */
+typedef struct gk_op gk_op;
+
+/* DskiOperator(kernel, grid, X, noise, order, with_gradients) (dski.hpp:58-65).
+ * order: 0 quintic, 1 cubic. */
+gk_status gk_dski_create(const gk_kernel* kernel, const gk_grid* grid, const double* X,
+                         int64_t n, double noise_value, double noise_gradient, int order,
+                         int with_gradients, int device, gk_op** out);
+
+/* DskipOperator(kernel, X, noise, config) (dskip.hpp:91-94, DskipConfig :74-85). */
+typedef struct {
+  int64_t rank;
+  double grid_ratio;
+  int max_grid_nodes;
+  uint64_t seed;
+  int rank_policy_error;
+  int track_dlogell;
+  int with_gradients;
+} gk_dskip_config;
+gk_status gk_dskip_create(const gk_kernel* kernel, const double* X, int64_t n, int d,
+                          double noise_value, double noise_gradient, const gk_dskip_config* cfg,
+                          int device, gk_op** out);
+
+/* DenseOperator(A) (linear_operator.hpp:38-56); A is N×N column-major. */
+gk_status gk_dense_create(const double* A, int64_t N, int device, gk_op** out);
+
+/* Matrix-free exact D-SE operator: assemble_dense(kernel, X, X) + noise
+ * (kernels.cpp:242-285) applied without forming the N×N matrix. */
+gk_status gk_exact_create(const gk_kernel* kernel, const double* X, int64_t n, int d,
+                          double noise_value, double noise_gradient, int with_gradients,
+                          int device, gk_op** out);
+
+void gk_op_destroy(gk_op* op);
+int64_t gk_op_size(const gk_op* op);
+/* 0 = exact, 1 = dski, 2 = dskip, 3 = dense */
+int gk_op_kind(const gk_op* op);
+
+/* LinearOperator::mvm over nrhs columns: Out = A V (host pointers). */
+gk_status gk_op_mvm(const gk_op* op, const double* V, int64_t ldv, double* Out, int64_t ldo,
+                    int64_t nrhs);
+/* Same with device pointers (external layout) on `stream`. */
+gk_status gk_op_mvm_dev(const gk_op* op, const double* dV, int64_t ldv, double* dOut,
+                        int64_t ldo, int64_t nrhs, void* stream);
+/* LinearOperator::diagonal / row (dski.cpp:240-304, dskip.cpp:252-264). */
+gk_status gk_op_diagonal(const gk_op* op, double* out);
+gk_status gk_op_row(const gk_op* op, int64_t r, double* out);
+/* noise_diagonal() (dski.cpp:206-211). */
+gk_status gk_op_noise_diagonal(const gk_op* op, double* out);
+
+/* D-SKI pieces GpModel uses directly (gp.cpp:213,416,445,482):
+ * stacked_transpose_apply (dski.cpp:213-219): U(m×nrhs) = B^T V;
+ * stacked_apply (dski.cpp:221-226): Out = B U; grid_operator().apply
+ * (dski.cpp:146-172): W = K_UU U. */
+int64_t gk_dski_grid_size(const gk_op* op);
+gk_status gk_dski_get_grid(const gk_op* op, gk_grid* out);
+gk_status gk_dski_transpose_apply(const gk_op* op, const double* V, int64_t ldv, double* U,
+                                  int64_t ldu, int64_t nrhs);
+gk_status gk_dski_apply(const gk_op* op, const double* U, int64_t ldu, double* Out, int64_t ldo,
+                        int64_t nrhs);
+gk_status gk_dski_grid_mvm(const gk_op* op, const double* U, int64_t ldu, double* W, int64_t ldw,
+                           int64_t nrhs);
+
+/* D-SKIP factor access (DskipOperator::factors, dskip.hpp:108) and
+ * dlogell_apply (dskip.cpp:266-274). */
+int gk_dskip_factor_count(const gk_op* op);
+int64_t gk_dskip_factor_rank(const gk_op* op, int f);
+gk_status gk_dskip_factor_get(const gk_op* op, int f, double* Q, double* alpha, double* beta);
+gk_status gk_dskip_dlogell_apply(const gk_op* op, const double* V, int64_t ldv, double* Out,
+                                 int64_t ldo, int64_t nrhs);
+
+/* Internal-layout stage entry points (device pointers, RHS-minor internal
+ * layout; used by the benchmark to time each kernel on its own stream).
+ * stage: 0 = scatter (B^T), 1 = grid K_UU, 2 = gather+noise (B), 3 = whole MVM. */
+gk_status gk_op_stage_dev(const gk_op* op, int stage, const double* dIn, double* dOut,
+                          int64_t nrhs, void* stream);
+/* Convert external column-major blocks to/from the internal layout. */
+gk_status gk_op_to_internal_dev(const gk_op* op, const double* dV, int64_t ldv, double* dI,
+                                int64_t nrhs, void* stream);
+gk_status gk_op_from_internal_dev(const gk_op* op, const double* dI, double* dV, int64_t ldv,
+                                  int64_t nrhs, void* stream);
+
+/* ---------------------------------------------------------------- solvers
+ * cg (linalg.cpp:85-131), batched: each of the nrhs columns runs the
+ * reference's single-RHS PCG independently (own alpha/beta, own stopping
+ * iteration; a column that stops is frozen). Non-convergence is a flag,
+ * not an error (linalg.hpp:27-30). residual_history may be NULL; else it
+ * holds (max_iterations+1)×nrhs relres values (column-major), and
+ * history_len[c] entries are valid for column c. precond may be NULL. */
+typedef struct gk_precond gk_precond;
+gk_status gk_pcg(const gk_op* op, const gk_precond* precond, const double* B, int64_t ldb,
+                 int64_t nrhs, double tol, int max_iterations, double* X, int64_t ldx,
+                 int* iterations, int* converged, double* residual_history, int* history_len);
+/* Device-pointer variant (external layout), on `stream`. Iteration counts
+ * and flags are written to host arrays; the call synchronises `stream`. */
+gk_status gk_pcg_dev(const gk_op* op, const gk_precond* precond, const double* dB, int64_t ldb,
+                     int64_t nrhs, double tol, int max_iterations, double* dX, int64_t ldx,
+                     int* iterations, int* converged, void* stream);
+
+/* pivoted_cholesky (linalg.cpp:133-174) over the operator's own diagonal and
+ * rows. kernel_part != 0 factors op - noise_diagonal with the diagonal
+ * clamped at 0, exactly as GpModel::preconditioner (gp.cpp:122-136).
+ * L (N×max_rank col-major, original row order) and pivots are host outputs;
+ * *rank receives the achieved rank. */
+typedef struct gk_pivchol gk_pivchol;
+gk_status gk_pivoted_cholesky(const gk_op* op, int kernel_part, int64_t max_rank,
+                              double trace_tol, gk_pivchol** out);
+int64_t gk_pivchol_rank(const gk_pivchol* f);
+gk_status gk_pivchol_get(const gk_pivchol* f, double* L /*N×rank or NULL*/,
+                         int64_t* pivots /*rank or NULL*/, double* initial_trace,
+                         double* residual_trace);
+void gk_pivchol_destroy(gk_pivchol* f);
+
+/* Preconditioner(F, noise_diag) (linalg.cpp:176-213): M^{-1}b =
+ * D^{-1/2}(c - Q1 Q1^T c), c = D^{-1/2} b, Q1 from a QR of [D^{-1/2}F; I]. */
+gk_status gk_precond_create(const double* F, int64_t N, int64_t k, const double* noise_diag,
+                            int device, gk_precond** out);
+/* From a device-resident pivoted Cholesky factor, with D = op noise diagonal
+ * (GpModel::preconditioner, gp.cpp:139). */
+gk_status gk_precond_from_pivchol(const gk_op* op, const gk_pivchol* f, gk_precond** out);
+gk_status gk_precond_apply(const gk_precond* M, const double* B, int64_t ldb, double* Out,
+                           int64_t ldo, int64_t nrhs);
+gk_status gk_precond_quadratic(const gk_precond* M, const double* B, int64_t ldb, int64_t nrhs,
+                               double* out /*nrhs*/);
+int64_t gk_precond_rank(const gk_precond* M);
+gk_status gk_precond_q1(const gk_precond* M, double* Q1 /*N×k col-major*/);
+void gk_precond_destroy(gk_precond* M);
+
+/* slq_logdet (linalg.cpp:215-253): probes run as one batched Lanczos;
+ * probe p uses rademacher_vector(N, seed, p) and restart stream
+ * mix_seed(seed, 50000+p); estimates[p] (may be NULL) receives the per-probe
+ * value, and *logdet = sum_p estimates[p] / probes summed in probe order.
+ * probe_offset lets a rank run probes [probe_offset, probe_offset+probes)
+ * of a larger job (probe sharding); *logdet is then the local sum / probes. */
+gk_status gk_slq_logdet(const gk_op* op, int probes, int lanczos_steps, uint64_t seed,
+                        double eigen_floor, int probe_offset, double* logdet, int* clamped,
+                        double* estimates);
+
+/* lanczos_lowrank (linalg.cpp:306-314) / lanczos_from_start (:17-81). Q is
+ * N×rank col-major; *k receives the achieved rank. start may be NULL
+ * (seeded Gaussian start). */
+gk_status gk_lanczos(const gk_op* op, int64_t steps, uint64_t seed, const double* start,
+                     uint64_t restart_seed, double* Q, double* alpha, double* beta, int64_t* k,
+                     int* breakdown);
+
+/* trace_estimate (linalg.cpp:255-279): E_z[z^T A^{-1} B z], probes batched. */
+gk_status gk_trace_estimate(const gk_op* A, const gk_op* B, int probes, uint64_t seed, double tol,
+                            int max_iterations, const gk_precond* precond, double* out);
+
+/* ---------------------------------------------------------------- GP glue
+ * GpModel pieces on the hot path (gp.cpp:117-187,471-517): the operator is
+ * built by the caller; these run the batched solve / SLQ / prediction. */
+/* predict_mean_grad for D-SKI (gp.cpp:480-495): g = K_UU (B^T alpha) cached in
+ * the call; values = mean + W_test g, grads = dW_test g. Xtest T×d col-major. */
+gk_status gk_dski_predict_mean_grad(const gk_op* op, const double* alpha, double mean,
+                                    const double* Xtest, int64_t T, double* values,
+                                    double* grads /*T×d col-major*/);
+/* cross_covariance for D-SKI (gp.cpp:412-417), T test points at once:
+ * Q (N×T col-major). */
+gk_status gk_dski_cross_covariance(const gk_op* op, const double* Xtest, int64_t T, double* Q,
+                                   int64_t ldq);
+
+/* ---------------------------------------------------------------- datasets
+ * Seeded synthetic workloads C1..C5 (BASELINE.json configs), generated on
+ * the host with std::mt19937_64 + libstdc++ distributions like
+ * testfns.cpp:355-402. Writes n into *n, X (n×d col-major), y (n), dY (n×d).
+ * Pass NULL buffers to query n and d first. */
+gk_status gk_make_dataset(int config, uint64_t seed, int64_t* n, int* d, double* X, double* y,
+                          double* dY);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GK_CAPI_H */

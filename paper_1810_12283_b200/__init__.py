@@ -1,0 +1,724 @@
+"""B200-native gradkrig hot path (arXiv 1810.12283): D-SKI / D-SKIP K∇ MVMs,
+pivoted-Cholesky preconditioner, batched PCG and SLQ log-det on sm_100a.
+
+This module is a thin Python mirror of the reference's C++ operator API
+(proj/core/include/gradkrig/{linear_operator,dski,dskip,linalg}.hpp) over the
+C-ABI in ``include/gk_capi.h`` (``_lib/libgk_b200.so``). Every compute call
+runs the CUDA kernels of that library; there is no CPU fallback — if the
+shared library is missing, importing this package raises.
+
+Conventions follow the reference: X is n×d, operator vectors are
+derivative-type-major ``[f; ∂1 f; …; ∂d f]``, multi-RHS blocks are N×nrhs.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libgk_b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build the CUDA library first "
+        "(python -c 'import __graft_entry__ as g; g.build()')")
+
+_d = C.c_double
+_dp = C.POINTER(C.c_double)
+_i64 = C.c_int64
+_i64p = C.POINTER(C.c_int64)
+_ip = C.POINTER(C.c_int)
+_u64 = C.c_uint64
+_vp = C.c_void_p
+
+
+class GkKernel(C.Structure):
+    _fields_ = [("family", C.c_int), ("lengthscale", _d), ("outputscale", _d),
+                ("spline_a", _d), ("spline_b", _d), ("spline_even", C.c_int)]
+
+
+class GkGrid(C.Structure):
+    _fields_ = [("d", C.c_int), ("dims", C.c_int * 8), ("origin", _d * 8), ("spacing", _d * 8)]
+
+
+class GkDskipConfig(C.Structure):
+    _fields_ = [("rank", _i64), ("grid_ratio", _d), ("max_grid_nodes", C.c_int), ("seed", _u64),
+                ("rank_policy_error", C.c_int), ("track_dlogell", C.c_int),
+                ("with_gradients", C.c_int)]
+
+
+_lib = C.CDLL(LIB_PATH)
+
+_SIGS = {
+    "gk_last_error": (C.c_char_p, []),
+    "gk_last_error_point": (_i64, []),
+    "gk_version": (C.c_char_p, []),
+    "gk_kernel_launch_count": (_i64, []),
+    "gk_grid_cover": (C.c_int, [_dp, _i64, C.c_int, _d, C.c_int, C.c_int, C.POINTER(GkGrid)]),
+    "gk_mix_seed": (_u64, [_u64, _u64]),
+    "gk_rademacher_vector": (None, [_i64, _u64, _u64, _dp]),
+    "gk_gaussian_vector": (None, [_i64, _u64, _u64, _dp]),
+    "gk_dski_create": (C.c_int, [C.POINTER(GkKernel), C.POINTER(GkGrid), _dp, _i64, _d, _d, C.c_int,
+                                 C.c_int, C.c_int, C.POINTER(_vp)]),
+    "gk_dskip_create": (C.c_int, [C.POINTER(GkKernel), _dp, _i64, C.c_int, _d, _d,
+                                  C.POINTER(GkDskipConfig), C.c_int, C.POINTER(_vp)]),
+    "gk_dense_create": (C.c_int, [_dp, _i64, C.c_int, C.POINTER(_vp)]),
+    "gk_exact_create": (C.c_int, [C.POINTER(GkKernel), _dp, _i64, C.c_int, _d, _d, C.c_int, C.c_int,
+                                  C.POINTER(_vp)]),
+    "gk_op_destroy": (None, [_vp]),
+    "gk_op_size": (_i64, [_vp]),
+    "gk_op_kind": (C.c_int, [_vp]),
+    "gk_op_mvm": (C.c_int, [_vp, _dp, _i64, _dp, _i64, _i64]),
+    "gk_op_mvm_dev": (C.c_int, [_vp, _vp, _i64, _vp, _i64, _i64, _vp]),
+    "gk_op_diagonal": (C.c_int, [_vp, _dp]),
+    "gk_op_row": (C.c_int, [_vp, _i64, _dp]),
+    "gk_op_noise_diagonal": (C.c_int, [_vp, _dp]),
+    "gk_op_stage_dev": (C.c_int, [_vp, C.c_int, _vp, _vp, _i64, _vp]),
+    "gk_op_to_internal_dev": (C.c_int, [_vp, _vp, _i64, _vp, _i64, _vp]),
+    "gk_op_from_internal_dev": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp]),
+    "gk_dski_grid_size": (_i64, [_vp]),
+    "gk_dski_get_grid": (C.c_int, [_vp, C.POINTER(GkGrid)]),
+    "gk_dski_transpose_apply": (C.c_int, [_vp, _dp, _i64, _dp, _i64, _i64]),
+    "gk_dski_apply": (C.c_int, [_vp, _dp, _i64, _dp, _i64, _i64]),
+    "gk_dski_grid_mvm": (C.c_int, [_vp, _dp, _i64, _dp, _i64, _i64]),
+    "gk_dskip_factor_count": (C.c_int, [_vp]),
+    "gk_dskip_factor_rank": (_i64, [_vp, C.c_int]),
+    "gk_dskip_factor_get": (C.c_int, [_vp, C.c_int, _dp, _dp, _dp]),
+    "gk_dskip_dlogell_apply": (C.c_int, [_vp, _dp, _i64, _dp, _i64, _i64]),
+    "gk_pcg": (C.c_int, [_vp, _vp, _dp, _i64, _i64, _d, C.c_int, _dp, _i64, _ip, _ip, _dp, _ip]),
+    "gk_pcg_dev": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _d, C.c_int, _vp, _i64, _ip, _ip, _vp]),
+    "gk_pivoted_cholesky": (C.c_int, [_vp, C.c_int, _i64, _d, C.POINTER(_vp)]),
+    "gk_pivchol_rank": (_i64, [_vp]),
+    "gk_pivchol_get": (C.c_int, [_vp, _dp, _i64p, _dp, _dp]),
+    "gk_pivchol_destroy": (None, [_vp]),
+    "gk_precond_create": (C.c_int, [_dp, _i64, _i64, _dp, C.c_int, C.POINTER(_vp)]),
+    "gk_precond_from_pivchol": (C.c_int, [_vp, _vp, C.POINTER(_vp)]),
+    "gk_precond_apply": (C.c_int, [_vp, _dp, _i64, _dp, _i64, _i64]),
+    "gk_precond_quadratic": (C.c_int, [_vp, _dp, _i64, _i64, _dp]),
+    "gk_precond_rank": (_i64, [_vp]),
+    "gk_precond_q1": (C.c_int, [_vp, _dp]),
+    "gk_precond_destroy": (None, [_vp]),
+    "gk_slq_logdet": (C.c_int, [_vp, C.c_int, C.c_int, _u64, _d, C.c_int, _dp, _ip, _dp]),
+    "gk_lanczos": (C.c_int, [_vp, _i64, _u64, _dp, _u64, _dp, _dp, _dp, _i64p, _ip]),
+    "gk_trace_estimate": (C.c_int, [_vp, _vp, C.c_int, _u64, _d, C.c_int, _vp, _dp]),
+    "gk_dski_predict_mean_grad": (C.c_int, [_vp, _dp, _d, _dp, _i64, _dp, _dp]),
+    "gk_dski_cross_covariance": (C.c_int, [_vp, _dp, _i64, _dp, _i64]),
+    "gk_make_dataset": (C.c_int, [C.c_int, _u64, _i64p, _ip, _dp, _dp, _dp]),
+}
+for _name, (_res, _args) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+EXPORTED_SYMBOLS = tuple(_SIGS)
+
+
+# ------------------------------------------------------------------ errors
+class OutOfGridError(RuntimeError):
+    """gradkrig::OutOfGridError (reference interpolation.hpp:37-40)."""
+
+    def __init__(self, msg, point):
+        super().__init__(msg)
+        self.point = point
+
+
+class LogicError(RuntimeError):
+    """std::logic_error (e.g. linear_operator.cpp:7-13)."""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+_ERR = {1: ValueError, 2: IndexError, 4: RuntimeError, 5: LogicError, 6: OverflowError,
+        7: CudaError, 8: CudaError, 9: NotImplementedError}
+
+
+def _check(status):
+    if status == 0:
+        return
+    msg = _lib.gk_last_error().decode()
+    if status == 3:
+        raise OutOfGridError(msg, int(_lib.gk_last_error_point()))
+    raise _ERR.get(status, RuntimeError)(msg)
+
+
+def _p(a):
+    return a.ctypes.data_as(_dp)
+
+
+def _f64(a, fortran=False):
+    a = np.asarray(a, dtype=np.float64)
+    return np.asfortranarray(a) if fortran else np.ascontiguousarray(a)
+
+
+def kernel_launch_count() -> int:
+    """Number of libgk_b200 CUDA kernels launched by this process so far."""
+    return int(_lib.gk_kernel_launch_count())
+
+
+def version() -> str:
+    return _lib.gk_version().decode()
+
+
+# ------------------------------------------------------------------ rng (rng.hpp:12-38)
+def mix_seed(seed, stream):
+    return int(_lib.gk_mix_seed(seed, stream))
+
+
+def rademacher_vector(n, seed, stream=0):
+    out = np.empty(n)
+    _lib.gk_rademacher_vector(n, seed, stream, _p(out))
+    return out
+
+
+def gaussian_vector(n, seed, stream=0):
+    out = np.empty(n)
+    _lib.gk_gaussian_vector(n, seed, stream, _p(out))
+    return out
+
+
+# ------------------------------------------------------------------ kernel / grid
+SE, SPLINE = 0, 1
+
+
+@dataclass
+class KernelSpec:
+    """KernelSpec (kernels.hpp:42-75): family, lengthscale, outputscale."""
+    lengthscale: float
+    outputscale: float
+    family: int = SE
+    spline_a: float = -1.5
+    spline_b: float = 1.0
+    spline_even: bool = False
+
+    def __post_init__(self):
+        if not self.lengthscale > 0:
+            raise ValueError("lengthscale must be > 0")
+        if not self.outputscale > 0:
+            raise ValueError("outputscale must be > 0")
+
+    def c(self):
+        return GkKernel(self.family, self.lengthscale, self.outputscale, self.spline_a,
+                        self.spline_b, int(self.spline_even))
+
+
+class Grid:
+    """Grid (interpolation.hpp:13-35): row-major, last dimension fastest."""
+
+    def __init__(self, dims, origin, spacing):
+        self.dims = np.asarray(dims, dtype=np.int64)
+        self.origin = _f64(origin)
+        self.spacing = _f64(spacing)
+
+    @property
+    def d(self):
+        return int(self.dims.size)
+
+    def size(self):
+        return int(np.prod(self.dims))
+
+    def c(self):
+        g = GkGrid()
+        g.d = self.d
+        for j in range(self.d):
+            g.dims[j] = int(self.dims[j])
+            g.origin[j] = float(self.origin[j])
+            g.spacing[j] = float(self.spacing[j])
+        return g
+
+    @staticmethod
+    def from_c(g):
+        return Grid([g.dims[j] for j in range(g.d)], [g.origin[j] for j in range(g.d)],
+                    [g.spacing[j] for j in range(g.d)])
+
+    @staticmethod
+    def cover(X, target_spacing, margin_cells=3, max_nodes=128):
+        """Grid::cover (interpolation.cpp:117-146)."""
+        X = _f64(X, True)
+        if X.ndim == 1:
+            X = X.reshape(-1, 1, order="F")
+        g = GkGrid()
+        _check(_lib.gk_grid_cover(_p(X), X.shape[0], X.shape[1], target_spacing, margin_cells,
+                                  max_nodes, C.byref(g)))
+        return Grid.from_c(g)
+
+
+# ------------------------------------------------------------------ operators
+class LinearOperator:
+    """LinearOperator (linear_operator.hpp:12-35) backed by a device gk_op."""
+
+    def __init__(self, handle, device=0):
+        self._h = handle
+        self.device = device
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.gk_op_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def size(self):
+        return int(_lib.gk_op_size(self._h))
+
+    def mvm(self, v):
+        """y = A v for a vector (N,) or a block (N, nrhs)."""
+        v = np.asarray(v, dtype=np.float64)
+        N = self.size()
+        if v.shape[0] != N:
+            raise ValueError("MVM size mismatch")
+        if v.ndim == 1:
+            out = np.empty(N)
+            _check(_lib.gk_op_mvm(self._h, _p(np.ascontiguousarray(v)), N, _p(out), N, 1))
+            return out
+        V = np.asfortranarray(v)
+        out = np.empty_like(V, order="F")
+        _check(_lib.gk_op_mvm(self._h, _p(V), N, _p(out), N, V.shape[1]))
+        return out
+
+    apply = mvm
+
+    def mvm_dev(self, dV, dOut, nrhs, ldv=None, ldo=None, stream=0):
+        """Device-pointer MVM (external layout) on `stream` (raw pointers)."""
+        N = self.size()
+        _check(_lib.gk_op_mvm_dev(self._h, dV, ldv or N, dOut, ldo or N, nrhs, stream))
+
+    def stage_dev(self, stage, dIn, dOut, nrhs, stream=0):
+        _check(_lib.gk_op_stage_dev(self._h, stage, dIn, dOut, nrhs, stream))
+
+    def to_internal_dev(self, dV, dI, nrhs, ldv=None, stream=0):
+        _check(_lib.gk_op_to_internal_dev(self._h, dV, ldv or self.size(), dI, nrhs, stream))
+
+    def from_internal_dev(self, dI, dV, nrhs, ldv=None, stream=0):
+        _check(_lib.gk_op_from_internal_dev(self._h, dI, dV, ldv or self.size(), nrhs, stream))
+
+    def has_diagonal(self):
+        return True
+
+    def diagonal(self):
+        out = np.empty(self.size())
+        _check(_lib.gk_op_diagonal(self._h, _p(out)))
+        return out
+
+    def has_rows(self):
+        return True
+
+    def row(self, i):
+        out = np.empty(self.size())
+        _check(_lib.gk_op_row(self._h, int(i), _p(out)))
+        return out
+
+    def noise_diagonal(self):
+        out = np.empty(self.size())
+        _check(_lib.gk_op_noise_diagonal(self._h, _p(out)))
+        return out
+
+    def dense(self):
+        """LinearOperator::dense (linear_operator.cpp:15-27), batched."""
+        N = self.size()
+        out = np.empty((N, N), order="F")
+        for c0 in range(0, N, 256):
+            nb = min(256, N - c0)
+            E = np.zeros((N, nb), order="F")
+            E[np.arange(c0, c0 + nb), np.arange(nb)] = 1.0
+            out[:, c0:c0 + nb] = self.mvm(E)
+        return out
+
+
+def _create(fn, *args):
+    h = _vp()
+    _check(fn(*args, C.byref(h)))
+    return h
+
+
+class DskiOperator(LinearOperator):
+    """DskiOperator (dski.hpp:58-101): [W; ∂W] K_UU [W; ∂W]^T + noise."""
+
+    def __init__(self, kernel: KernelSpec, grid: Grid, X, noise=(0.0, 0.0), order=0,
+                 with_gradients=True, device=0):
+        X = _f64(X, True)
+        if X.ndim != 2 or X.shape[1] != grid.d:
+            raise ValueError("interpolation points do not match grid dimension")
+        self.n, self.d = X.shape
+        self.kernel, self.grid, self.noise = kernel, grid, tuple(noise)
+        k, g = kernel.c(), grid.c()
+        super().__init__(_create(_lib.gk_dski_create, C.byref(k), C.byref(g), _p(X), self.n,
+                                 float(noise[0]), float(noise[1]), int(order),
+                                 int(with_gradients), device), device)
+
+    def points(self):
+        return self.n
+
+    def grid_size(self):
+        return int(_lib.gk_dski_grid_size(self._h))
+
+    def _grid_block(self, fn, a, rows_in, rows_out):
+        a = np.asarray(a, dtype=np.float64)
+        vec = a.ndim == 1
+        A = np.asfortranarray(a.reshape(rows_in, -1) if vec else a)
+        if A.shape[0] != rows_in:
+            raise ValueError("size mismatch")
+        out = np.empty((rows_out, A.shape[1]), order="F")
+        _check(fn(self._h, _p(A), rows_in, _p(out), rows_out, A.shape[1]))
+        return out[:, 0] if vec else out
+
+    def stacked_transpose_apply(self, v):
+        """B^T v (dski.cpp:213-219)."""
+        return self._grid_block(_lib.gk_dski_transpose_apply, v, self.size(), self.grid_size())
+
+    def stacked_apply(self, u):
+        """B u (dski.cpp:221-226)."""
+        return self._grid_block(_lib.gk_dski_apply, u, self.grid_size(), self.size())
+
+    def grid_mvm(self, u):
+        """grid_operator().apply(u): K_UU u (dski.cpp:146-172)."""
+        return self._grid_block(_lib.gk_dski_grid_mvm, u, self.grid_size(), self.grid_size())
+
+    def predict_mean_grad(self, alpha, mean, Xtest):
+        """GpModel::predict_mean_grad for D-SKI (gp.cpp:480-495)."""
+        Xt = _f64(Xtest, True)
+        T = Xt.shape[0]
+        vals = np.empty(T)
+        grads = np.empty((T, self.d), order="F")
+        _check(_lib.gk_dski_predict_mean_grad(self._h, _p(_f64(alpha)), float(mean), _p(Xt), T,
+                                              _p(vals), _p(grads)))
+        return vals, grads
+
+    def cross_covariance(self, Xtest):
+        """GpModel::cross_covariance for D-SKI (gp.cpp:412-417), one column per test point."""
+        Xt = _f64(Xtest, True)
+        if Xt.ndim == 1:
+            Xt = Xt.reshape(1, -1, order="F")
+        T = Xt.shape[0]
+        Q = np.empty((self.size(), T), order="F")
+        _check(_lib.gk_dski_cross_covariance(self._h, _p(Xt), T, _p(Q), self.size()))
+        return Q
+
+
+class ExactOperator(LinearOperator):
+    """Matrix-free exact D-SE K∇ + noise (kernels.cpp:242-285 without assembly)."""
+
+    def __init__(self, kernel: KernelSpec, X, noise=(0.0, 0.0), with_gradients=True, device=0):
+        X = _f64(X, True)
+        self.n, self.d = X.shape
+        k = kernel.c()
+        super().__init__(_create(_lib.gk_exact_create, C.byref(k), _p(X), self.n, self.d,
+                                 float(noise[0]), float(noise[1]), int(with_gradients), device),
+                         device)
+
+
+class DenseOperator(LinearOperator):
+    """DenseOperator (linear_operator.hpp:38-56) on the device."""
+
+    def __init__(self, A, device=0):
+        A = _f64(A, True)
+        if A.ndim != 2 or A.shape[0] != A.shape[1]:
+            raise ValueError("dense operator must be square")
+        super().__init__(_create(_lib.gk_dense_create, _p(A), A.shape[0], device), device)
+
+
+class DskipOperator(LinearOperator):
+    """DskipOperator (dskip.hpp:91-121)."""
+
+    def __init__(self, kernel: KernelSpec, X, noise=(0.0, 0.0), rank=100, grid_ratio=0.1,
+                 max_grid_nodes=512, seed=0, rank_policy_error=False, track_dlogell=False,
+                 with_gradients=True, device=0):
+        X = _f64(X, True)
+        self.n, self.d = X.shape
+        cfg = GkDskipConfig(rank, grid_ratio, max_grid_nodes, seed, int(rank_policy_error),
+                            int(track_dlogell), int(with_gradients))
+        k = kernel.c()
+        super().__init__(_create(_lib.gk_dskip_create, C.byref(k), _p(X), self.n, self.d,
+                                 float(noise[0]), float(noise[1]), C.byref(cfg), device), device)
+
+    def factors(self):
+        out = []
+        N = self.size()
+        for f in range(_lib.gk_dskip_factor_count(self._h)):
+            r = int(_lib.gk_dskip_factor_rank(self._h, f))
+            Q = np.empty((N, r), order="F")
+            a = np.empty(r)
+            b = np.empty(max(r - 1, 1))
+            _check(_lib.gk_dskip_factor_get(self._h, f, _p(Q), _p(a), _p(b)))
+            out.append(LanczosFactor(Q, a, b[: max(r - 1, 0)], False))
+        return out
+
+    def dlogell_apply(self, v):
+        v = np.asarray(v, dtype=np.float64)
+        vec = v.ndim == 1
+        V = np.asfortranarray(v.reshape(-1, 1) if vec else v)
+        out = np.empty_like(V, order="F")
+        _check(_lib.gk_dskip_dlogell_apply(self._h, _p(V), V.shape[0], _p(out), V.shape[0], V.shape[1]))
+        return out[:, 0] if vec else out
+
+
+# ------------------------------------------------------------------ solvers
+@dataclass
+class CgResult:
+    """CgResult (linalg.hpp:18-23)."""
+    x: np.ndarray
+    iterations: int
+    converged: bool
+    residual_history: np.ndarray
+
+
+def cg(A: LinearOperator, b, tol=1e-4, max_iterations=1000, precond=None, history=True):
+    """cg (linalg.cpp:85-131). b may be (N,) or a block (N, nrhs): each column
+    runs the reference's single-RHS PCG independently (one batched device
+    solve). Returns a CgResult, or a list of them for a block."""
+    b = np.asarray(b, dtype=np.float64)
+    N = A.size()
+    if b.shape[0] != N:
+        raise ValueError("cg: rhs size mismatch")
+    vec = b.ndim == 1
+    B = np.asfortranarray(b.reshape(N, -1) if vec else b)
+    nrhs = B.shape[1]
+    X = np.empty((N, nrhs), order="F")
+    its = np.empty(nrhs, np.int32)
+    conv = np.empty(nrhs, np.int32)
+    hist = np.empty((max_iterations + 1, nrhs), order="F") if history else None
+    hl = np.empty(nrhs, np.int32)
+    _check(_lib.gk_pcg(A.handle, precond.handle if precond is not None else None, _p(B), N, nrhs,
+                       tol, max_iterations, _p(X), N, its.ctypes.data_as(_ip),
+                       conv.ctypes.data_as(_ip), _p(hist) if history else None,
+                       hl.ctypes.data_as(_ip)))
+    res = [CgResult(X[:, c].copy(), int(its[c]), bool(conv[c]),
+                    hist[: hl[c], c].copy() if history else np.empty(0)) for c in range(nrhs)]
+    return res[0] if vec else res
+
+
+def cg_dev(A: LinearOperator, dB, dX, nrhs, tol=1e-4, max_iterations=1000, precond=None, stream=0):
+    """Device-pointer batched PCG (external layout). Returns (iterations, converged)."""
+    its = np.empty(nrhs, np.int32)
+    conv = np.empty(nrhs, np.int32)
+    N = A.size()
+    _check(_lib.gk_pcg_dev(A.handle, precond.handle if precond is not None else None, dB, N, nrhs,
+                           tol, max_iterations, dX, N, its.ctypes.data_as(_ip),
+                           conv.ctypes.data_as(_ip), stream))
+    return its, conv
+
+
+class PivotedCholeskyFactor:
+    """PivotedCholeskyFactor (linalg.hpp:32-37); device-resident L."""
+
+    def __init__(self, handle, N):
+        self._h = handle
+        self.N = N
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.gk_pivchol_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def rank(self):
+        return int(_lib.gk_pivchol_rank(self._h))
+
+    def _get(self):
+        k = self.rank()
+        L = np.empty((self.N, k), order="F")
+        piv = np.empty(max(k, 1), np.int64)
+        it, rt = _d(), _d()
+        _check(_lib.gk_pivchol_get(self._h, _p(L) if k else None, piv.ctypes.data_as(_i64p),
+                                   C.byref(it), C.byref(rt)))
+        return L, piv[:k], it.value, rt.value
+
+    @property
+    def L(self):
+        return self._get()[0]
+
+    @property
+    def pivots(self):
+        return self._get()[1]
+
+    @property
+    def initial_trace(self):
+        return self._get()[2]
+
+    @property
+    def residual_trace(self):
+        return self._get()[3]
+
+
+def pivoted_cholesky(A: LinearOperator, max_rank, trace_tol=0.0, kernel_part=False):
+    """pivoted_cholesky (linalg.cpp:133-174) over A's diagonal and rows.
+    kernel_part=True factors A - noise_diagonal (GpModel::preconditioner,
+    gp.cpp:122-136)."""
+    h = _vp()
+    _check(_lib.gk_pivoted_cholesky(A.handle, int(kernel_part), int(max_rank), float(trace_tol),
+                                    C.byref(h)))
+    return PivotedCholeskyFactor(h, A.size())
+
+
+class Preconditioner:
+    """Preconditioner (linalg.cpp:176-213): M = D + F F^T applied via Q1."""
+
+    def __init__(self, F=None, noise_diag=None, device=0, _handle=None, size=None):
+        if _handle is not None:
+            self._h, self.N = _handle, size
+            return
+        F = _f64(F, True)
+        if F.ndim == 1:
+            F = F.reshape(-1, 1, order="F")
+        N, k = F.shape
+        nd = np.asarray(noise_diag, dtype=np.float64)
+        if nd.ndim == 0:
+            nd = np.full(N, float(noise_diag) ** 2)
+        if nd.size != N:
+            raise ValueError("preconditioner factor and noise sizes differ")
+        self.N = N
+        h = _vp()
+        _check(_lib.gk_precond_create(_p(F), N, k, _p(_f64(nd)), device, C.byref(h)))
+        self._h = h
+
+    @staticmethod
+    def from_pivchol(A: LinearOperator, factor: PivotedCholeskyFactor):
+        h = _vp()
+        _check(_lib.gk_precond_from_pivchol(A.handle, factor.handle, C.byref(h)))
+        return Preconditioner(_handle=h, size=A.size())
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.gk_precond_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def rank(self):
+        return int(_lib.gk_precond_rank(self._h))
+
+    def size(self):
+        return self.N
+
+    def apply(self, b):
+        b = np.asarray(b, dtype=np.float64)
+        vec = b.ndim == 1
+        B = np.asfortranarray(b.reshape(self.N, -1) if vec else b)
+        out = np.empty_like(B, order="F")
+        _check(_lib.gk_precond_apply(self._h, _p(B), self.N, _p(out), self.N, B.shape[1]))
+        return out[:, 0] if vec else out
+
+    def quadratic(self, b):
+        b = np.asarray(b, dtype=np.float64)
+        vec = b.ndim == 1
+        B = np.asfortranarray(b.reshape(self.N, -1) if vec else b)
+        out = np.empty(B.shape[1])
+        _check(_lib.gk_precond_quadratic(self._h, _p(B), self.N, B.shape[1], _p(out)))
+        return float(out[0]) if vec else out
+
+    def q1(self):
+        k = self.rank()
+        out = np.empty((self.N, k), order="F")
+        _check(_lib.gk_precond_q1(self._h, _p(out)))
+        return out
+
+
+@dataclass
+class SlqResult:
+    logdet: float
+    clamped: int
+    estimates: np.ndarray
+
+
+def slq_logdet(A: LinearOperator, probes=10, lanczos_steps=50, seed=0, eigen_floor=1e-12,
+               probe_offset=0):
+    """slq_logdet (linalg.cpp:215-253); probes run as one batched Lanczos."""
+    ld = _d()
+    cl = C.c_int()
+    est = np.empty(max(probes, 1))
+    _check(_lib.gk_slq_logdet(A.handle, probes, lanczos_steps, seed, eigen_floor, probe_offset,
+                              C.byref(ld), C.byref(cl), _p(est)))
+    return SlqResult(ld.value, cl.value, est[:probes].copy())
+
+
+def trace_estimate(A: LinearOperator, B: LinearOperator, probes, seed, tol=1e-4,
+                   max_iterations=1000, precond=None):
+    """trace_estimate (linalg.cpp:255-279)."""
+    out = _d()
+    _check(_lib.gk_trace_estimate(A.handle, B.handle, probes, seed, tol, max_iterations,
+                                  precond.handle if precond is not None else None, C.byref(out)))
+    return out.value
+
+
+class LanczosFactor:
+    """LanczosFactor (linalg.hpp:102-114)."""
+
+    def __init__(self, Q, alpha, beta, breakdown):
+        self.Q, self.alpha, self.beta, self.breakdown = Q, alpha, beta, breakdown
+
+    def rank(self):
+        return self.Q.shape[1]
+
+    def tridiagonal(self):
+        T = np.diag(self.alpha)
+        if self.alpha.size > 1:
+            T = T + np.diag(self.beta, 1) + np.diag(self.beta, -1)
+        return T
+
+    def ritz_values(self):
+        return np.sort(np.linalg.eigvalsh(self.tridiagonal()))[::-1]
+
+    def apply(self, v):
+        return self.Q @ (self.tridiagonal() @ (self.Q.T @ v))
+
+    def dense(self):
+        return self.Q @ self.tridiagonal() @ self.Q.T
+
+
+def lanczos(A: LinearOperator, steps, seed=0, start=None, restart_seed=0):
+    N = A.size()
+    steps = min(int(steps), N)
+    Q = np.empty((N, max(steps, 1)), order="F")
+    a = np.empty(max(steps, 1))
+    b = np.empty(max(steps, 1))
+    k = _i64()
+    bd = C.c_int()
+    st = _f64(start) if start is not None else None
+    _check(_lib.gk_lanczos(A.handle, steps, seed, _p(st) if st is not None else None, restart_seed,
+                           _p(Q), _p(a), _p(b), C.byref(k), C.byref(bd)))
+    k = k.value
+    return LanczosFactor(np.asfortranarray(Q[:, :k]), a[:k].copy(), b[: max(k - 1, 0)].copy(),
+                         bool(bd.value))
+
+
+def lanczos_lowrank(A: LinearOperator, rank, seed):
+    """lanczos_lowrank (linalg.cpp:306-314)."""
+    if rank <= 0 or rank > A.size():
+        raise ValueError("Lanczos rank must lie in [1, N]")
+    return lanczos(A, rank, seed)
+
+
+# ------------------------------------------------------------------ datasets
+def make_dataset(config, seed=0):
+    """Seeded synthetic workload C1..C5 (BASELINE.json configs). Returns X (n×d), y, dY."""
+    n = _i64()
+    d = C.c_int()
+    _check(_lib.gk_make_dataset(config, seed, C.byref(n), C.byref(d), None, None, None))
+    n, d = n.value, d.value
+    X = np.empty((n, d), order="F")
+    y = np.empty(n)
+    dY = np.empty((n, d), order="F")
+    _check(_lib.gk_make_dataset(config, seed, None, None, _p(X), _p(y), _p(dY)))
+    return X, y, dY
+
+
+def stacked_targets(y, dY, mean):
+    """ObservationSet::stacked_targets (observations.hpp:29-35)."""
+    parts = [np.asarray(y) - mean]
+    if dY is not None:
+        parts += [np.asarray(dY)[:, j] for j in range(np.asarray(dY).shape[1])]
+    return np.concatenate(parts)

@@ -1,0 +1,835 @@
+// capi.cu — extern "C" boundary (include/gk_capi.h). Maps C++ exceptions to
+// gk_status codes, stages host blocks through the device, converts between
+// the reference's external layout and the operators' internal layout.
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "gk_kernels.cuh"
+#include "solvers.hpp"
+
+extern "C" gk_status gk_make_dataset_impl(int config, std::uint64_t seed, int64_t* n, int* d, double* X,
+                                          double* y, double* dY);
+
+namespace gk {
+std::unique_ptr<Op> make_dski(const gk_kernel& k, const gk_grid& g, const double* X, i64 n, double nv, double ng,
+                              int order, int with_grad, int device);
+std::unique_ptr<Op> make_exact(const gk_kernel& k, const double* X, i64 n, int d, double nv, double ng,
+                               int with_grad, int device);
+std::unique_ptr<Op> make_dense(const double* A, i64 N, int device);
+std::unique_ptr<Op> make_dskip(const gk_kernel& k, const double* X, i64 n, int d, double nv, double ng,
+                               const gk_dskip_config& cfg, int device);
+int64_t dski_grid_size(const Op& o);
+gk_grid dski_grid(const Op& o);
+void dski_transpose_apply(Op& o, const double* Vi, double* U, int nrhs, cudaStream_t s);
+void dski_apply(Op& o, const double* U, double* Oi, int nrhs, cudaStream_t s);
+void dski_grid_mvm(Op& o, const double* U, double* W, int nrhs, cudaStream_t s);
+void dski_predict(Op& o, const double* alpha_i, double mean, const double* dXt, i64 nT, double* dvals,
+                  double* dgrads, int* dbad, cudaStream_t s);
+void dski_cross_cov(Op& o, const double* dXt, i64 nT, double* Qi, int* dbad, cudaStream_t s);
+void precond_quadratic(Precond& M, const double* r, int nrhs, double* out_h, cudaStream_t s);
+void pivchol_copy_L(const PivChol& f, double* out_host);
+int dskip_factor_count(const Op& o);
+i64 dskip_factor_rank(const Op& o, int f);
+void dskip_factor_get(const Op& o, int f, double* Q, double* a, double* b);
+void dskip_dlogell(Op& o, const double* in, double* out, int nrhs, cudaStream_t s);
+}  // namespace gk
+
+using namespace gk;
+
+struct gk_precond {
+  std::unique_ptr<Precond> impl;
+  // cached copies reordered for an operator's internal row order
+  std::vector<std::pair<const i64*, std::unique_ptr<Precond>>> reordered;
+};
+struct gk_pivchol {
+  std::unique_ptr<PivChol> impl;
+};
+
+namespace {
+
+thread_local std::string g_err;
+thread_local i64 g_err_point = -1;
+
+template <class F>
+gk_status guard(F&& f) {
+  try {
+    f();
+    return GK_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    g_err_point = e.point;
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_err = "host allocation failed";
+    return GK_ERR_RUNTIME;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return GK_ERR_RUNTIME;
+  }
+}
+
+Op& O(const gk_op* op) {
+  if (!op || !op->impl) fail(GK_ERR_ARG, "null operator handle");
+  return *op->impl;
+}
+
+cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+// Host block (N×nrhs col-major, ld) -> device internal layout.
+void upload_internal(Op& op, const double* V, i64 ldv, double* d_ext, double* d_int, int nrhs, cudaStream_t s) {
+  GK_CUDA(cudaMemcpy2DAsync(d_ext, sizeof(double) * op.N, V, sizeof(double) * ldv, sizeof(double) * op.N, nrhs,
+                            cudaMemcpyHostToDevice, s));
+  op.to_internal(d_ext, op.N, d_int, nrhs, s);
+}
+void download_internal(Op& op, const double* d_int, double* d_ext, double* Out, i64 ldo, int nrhs,
+                       cudaStream_t s) {
+  op.from_internal(d_int, d_ext, op.N, nrhs, s);
+  GK_CUDA(cudaMemcpy2DAsync(Out, sizeof(double) * ldo, d_ext, sizeof(double) * op.N, sizeof(double) * op.N, nrhs,
+                            cudaMemcpyDeviceToHost, s));
+}
+
+// Precond in the row order of `op`.
+Precond& precond_for(const gk_precond* M, const Op& op) {
+  auto* mm = const_cast<gk_precond*>(M);
+  Precond& base = *mm->impl;
+  if (base.N != op.N) fail(GK_ERR_ARG, "preconditioner and operator sizes differ");
+  const i64* ext = op.d_ext_of_int();
+  if (base.ext == ext) return base;
+  if (base.ext != nullptr) fail(GK_ERR_UNSUPPORTED, "preconditioner was built for another operator's row order");
+  for (auto& pr : mm->reordered)
+    if (pr.first == ext) return *pr.second;
+  // identity-ordered preconditioner -> reorder rows for op: new[r] = old[ext[r]]
+  auto P = std::make_unique<Precond>();
+  P->device = base.device;
+  P->N = base.N;
+  P->k = base.k;
+  P->ext = ext;
+  P->q1.alloc(static_cast<size_t>(base.N * base.k));
+  P->dinv.alloc(static_cast<size_t>(base.N));
+  cudaStream_t s = op.stream;
+  // q1 is [N][k] row-major == an external "k-column" block transposed; use the
+  // generic row map on a k-wide RHS-minor block.
+  DevBuf<double> tmp(static_cast<size_t>(base.N * base.k));
+  // internal (row-major [N][k]) -> external col-major with identity, then gather by ext
+  from_internal(nullptr, base.N, base.q1.p, tmp.p, base.N, int(base.k), s);
+  to_internal(ext, base.N, tmp.p, base.N, P->q1.p, int(base.k), s);
+  DevBuf<double> tmp1(static_cast<size_t>(base.N));
+  from_internal(nullptr, base.N, base.dinv.p, tmp1.p, base.N, 1, s);
+  to_internal(ext, base.N, tmp1.p, base.N, P->dinv.p, 1, s);
+  GK_CUDA(cudaStreamSynchronize(s));
+  mm->reordered.emplace_back(ext, std::move(P));
+  return *mm->reordered.back().second;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gk_last_error(void) { return g_err.c_str(); }
+int64_t gk_last_error_point(void) { return g_err_point; }
+const char* gk_version(void) { return "gk_b200 0.1 (sm_100a)"; }
+int64_t gk_kernel_launch_count(void) { return g_launches.load(); }
+
+gk_status gk_grid_cover(const double* X, int64_t n, int d, double target, int margin, int max_nodes,
+                        gk_grid* out) {
+  return guard([&] {  // interpolation.cpp:117-146
+    if (n <= 0) fail(GK_ERR_ARG, "cannot build a grid over no points");
+    if (!(target > 0.0)) fail(GK_ERR_ARG, "grid spacing must be positive");
+    if (d < 1 || d > 8) fail(GK_ERR_ARG, "grid dimension must be in [1, 8]");
+    margin = std::max(margin, 3);
+    out->d = d;
+    for (int j = 0; j < d; ++j) {
+      double lo = X[j * n], hi = X[j * n];
+      for (i64 i = 0; i < n; ++i) {
+        lo = std::min(lo, X[j * n + i]);
+        hi = std::max(hi, X[j * n + i]);
+      }
+      const double span = std::max(hi - lo, 1e-12);
+      double h = target;
+      const int interior = static_cast<int>(std::ceil(span / h)) + 1;
+      int m = interior + 2 * margin;
+      if (m > max_nodes) {
+        m = max_nodes;
+        h = span / static_cast<double>(m - 1 - 2 * margin);
+      }
+      if (m < 6 + 2 * margin) m = 6 + 2 * margin;
+      out->dims[j] = m;
+      out->spacing[j] = h;
+      out->origin[j] = lo - margin * h;
+    }
+  });
+}
+
+uint64_t gk_mix_seed(uint64_t seed, uint64_t stream) { return mix_seed(seed, stream); }
+void gk_rademacher_vector(int64_t n, uint64_t seed, uint64_t stream, double* out) { rademacher(n, seed, stream, out); }
+void gk_gaussian_vector(int64_t n, uint64_t seed, uint64_t stream, double* out) { gaussian(n, seed, stream, out); }
+
+gk_status gk_dski_create(const gk_kernel* kernel, const gk_grid* grid, const double* X, int64_t n, double nv,
+                         double ng, int order, int with_gradients, int device, gk_op** out) {
+  return guard([&] {
+    auto h = std::make_unique<gk_op>();
+    h->impl = make_dski(*kernel, *grid, X, n, nv, ng, order, with_gradients, device);
+    *out = h.release();
+  });
+}
+
+gk_status gk_dskip_create(const gk_kernel* kernel, const double* X, int64_t n, int d, double nv, double ng,
+                          const gk_dskip_config* cfg, int device, gk_op** out) {
+  return guard([&] {
+    auto h = std::make_unique<gk_op>();
+    h->impl = make_dskip(*kernel, X, n, d, nv, ng, *cfg, device);
+    *out = h.release();
+  });
+}
+
+gk_status gk_dense_create(const double* A, int64_t N, int device, gk_op** out) {
+  return guard([&] {
+    auto h = std::make_unique<gk_op>();
+    h->impl = make_dense(A, N, device);
+    *out = h.release();
+  });
+}
+
+gk_status gk_exact_create(const gk_kernel* kernel, const double* X, int64_t n, int d, double nv, double ng,
+                          int with_gradients, int device, gk_op** out) {
+  return guard([&] {
+    auto h = std::make_unique<gk_op>();
+    h->impl = make_exact(*kernel, X, n, d, nv, ng, with_gradients, device);
+    *out = h.release();
+  });
+}
+
+void gk_op_destroy(gk_op* op) {
+  if (!op) return;
+  if (op->impl) {
+    DeviceGuard dg(op->impl->device);
+    op->impl.reset();
+  }
+  delete op;
+}
+int64_t gk_op_size(const gk_op* op) { return op && op->impl ? op->impl->N : -1; }
+int gk_op_kind(const gk_op* op) { return op && op->impl ? op->impl->kind : -1; }
+
+gk_status gk_op_mvm(const gk_op* h, const double* V, int64_t ldv, double* Out, int64_t ldo, int64_t nrhs) {
+  return guard([&] {
+    Op& op = O(h);
+    if (nrhs < 0 || ldv < op.N || ldo < op.N) fail(GK_ERR_ARG, "MVM size mismatch");
+    if (nrhs == 0) return;
+    std::lock_guard<std::mutex> lk(op.mu);
+    DeviceGuard dg(op.device);
+    cudaStream_t s = op.stream;
+    const int chunk = int(std::min<i64>(nrhs, kMaxRhs));
+    op.scratch_a.reserve(static_cast<size_t>(op.N) * chunk);
+    op.scratch_b.reserve(static_cast<size_t>(op.N) * chunk);
+    op.scratch_c.reserve(static_cast<size_t>(op.N) * chunk);
+    for (i64 c0 = 0; c0 < nrhs; c0 += chunk) {
+      const int nb = int(std::min<i64>(chunk, nrhs - c0));
+      upload_internal(op, V + c0 * ldv, ldv, op.scratch_c.p, op.scratch_a.p, nb, s);
+      op.mvm(op.scratch_a.p, op.scratch_b.p, nb, s);
+      download_internal(op, op.scratch_b.p, op.scratch_c.p, Out + c0 * ldo, ldo, nb, s);
+    }
+    GK_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+gk_status gk_op_mvm_dev(const gk_op* h, const double* dV, int64_t ldv, double* dOut, int64_t ldo, int64_t nrhs,
+                        void* stream) {
+  return guard([&] {
+    Op& op = O(h);
+    if (nrhs < 0 || ldv < op.N || ldo < op.N) fail(GK_ERR_ARG, "MVM size mismatch");
+    if (nrhs == 0) return;
+    std::lock_guard<std::mutex> lk(op.mu);
+    DeviceGuard dg(op.device);
+    cudaStream_t s = S(stream);
+    const int chunk = int(std::min<i64>(nrhs, kMaxRhs));
+    op.scratch_a.reserve(static_cast<size_t>(op.N) * chunk);
+    op.scratch_b.reserve(static_cast<size_t>(op.N) * chunk);
+    for (i64 c0 = 0; c0 < nrhs; c0 += chunk) {
+      const int nb = int(std::min<i64>(chunk, nrhs - c0));
+      op.to_internal(dV + c0 * ldv, ldv, op.scratch_a.p, nb, s);
+      op.mvm(op.scratch_a.p, op.scratch_b.p, nb, s);
+      op.from_internal(op.scratch_b.p, dOut + c0 * ldo, ldo, nb, s);
+    }
+  });
+}
+
+gk_status gk_op_stage_dev(const gk_op* h, int stage, const double* dIn, double* dOut, int64_t nrhs, void* stream) {
+  return guard([&] {
+    Op& op = O(h);
+    if (nrhs < 1 || nrhs > 256) fail(GK_ERR_ARG, "stage: nrhs must be in [1, 256]");
+    DeviceGuard dg(op.device);
+    op.stage(stage, dIn, dOut, int(nrhs), S(stream));
+  });
+}
+
+gk_status gk_op_to_internal_dev(const gk_op* h, const double* dV, int64_t ldv, double* dI, int64_t nrhs,
+                                void* stream) {
+  return guard([&] {
+    Op& op = O(h);
+    DeviceGuard dg(op.device);
+    op.to_internal(dV, ldv, dI, int(nrhs), S(stream));
+  });
+}
+
+gk_status gk_op_from_internal_dev(const gk_op* h, const double* dI, double* dV, int64_t ldv, int64_t nrhs,
+                                  void* stream) {
+  return guard([&] {
+    Op& op = O(h);
+    DeviceGuard dg(op.device);
+    op.from_internal(dI, dV, ldv, int(nrhs), S(stream));
+  });
+}
+
+gk_status gk_op_diagonal(const gk_op* h, double* out) {
+  return guard([&] {
+    Op& op = O(h);
+    std::lock_guard<std::mutex> lk(op.mu);
+    DeviceGuard dg(op.device);
+    cudaStream_t s = op.stream;
+    op.scratch_a.reserve(static_cast<size_t>(op.N));
+    op.scratch_b.reserve(static_cast<size_t>(op.N));
+    op.diagonal(op.scratch_a.p, s);
+    op.from_internal(op.scratch_a.p, op.scratch_b.p, op.N, 1, s);
+    GK_CUDA(cudaMemcpyAsync(out, op.scratch_b.p, sizeof(double) * op.N, cudaMemcpyDeviceToHost, s));
+    GK_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+gk_status gk_op_row(const gk_op* h, int64_t r, double* out) {
+  return guard([&] {
+    Op& op = O(h);
+    if (r < 0 || r >= op.N) fail(GK_ERR_RANGE, "row index out of range");
+    std::lock_guard<std::mutex> lk(op.mu);
+    DeviceGuard dg(op.device);
+    cudaStream_t s = op.stream;
+    op.scratch_a.reserve(static_cast<size_t>(op.N));
+    op.scratch_b.reserve(static_cast<size_t>(op.N));
+    op.row(r, op.scratch_a.p, s);
+    op.from_internal(op.scratch_a.p, op.scratch_b.p, op.N, 1, s);
+    GK_CUDA(cudaMemcpyAsync(out, op.scratch_b.p, sizeof(double) * op.N, cudaMemcpyDeviceToHost, s));
+    GK_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+gk_status gk_op_noise_diagonal(const gk_op* h, double* out) {
+  return guard([&] {
+    Op& op = O(h);
+    for (i64 r = 0; r < op.N; ++r) out[r] = r < op.n_value ? op.nv2 : op.ng2;
+  });
+}
+
+// ---------------------------------------------------------------- D-SKI pieces
+int64_t gk_dski_grid_size(const gk_op* h) {
+  int64_t m = -1;
+  guard([&] { m = dski_grid_size(O(h)); });
+  return m;
+}
+
+gk_status gk_dski_get_grid(const gk_op* h, gk_grid* out) {
+  return guard([&] { *out = dski_grid(O(h)); });
+}
+
+}  // extern "C"
+
+namespace {
+// Generic grid-block helper: host grid blocks (M×nrhs col-major) are
+// RHS-minor on device via the identity row map.
+template <class F>
+void grid_call(Op& op, const double* In, i64 ldi, i64 rows_in, double* Out, i64 ldo, i64 rows_out, i64 nrhs,
+               bool in_is_grid, bool out_is_grid, F&& f) {
+  std::lock_guard<std::mutex> lk(op.mu);
+  DeviceGuard dg(op.device);
+  cudaStream_t s = op.stream;
+  const int chunk = int(std::min<i64>(nrhs, kMaxRhs));
+  DevBuf<double> ein(static_cast<size_t>(rows_in) * chunk), iin(static_cast<size_t>(rows_in) * chunk), iout(static_cast<size_t>(rows_out) * chunk),
+      eout(static_cast<size_t>(rows_out) * chunk);
+  for (i64 c0 = 0; c0 < nrhs; c0 += chunk) {
+    const int nb = int(std::min<i64>(chunk, nrhs - c0));
+    GK_CUDA(cudaMemcpy2DAsync(ein.p, sizeof(double) * rows_in, In + c0 * ldi, sizeof(double) * ldi,
+                              sizeof(double) * rows_in, nb, cudaMemcpyHostToDevice, s));
+    if (in_is_grid) to_internal(nullptr, rows_in, ein.p, rows_in, iin.p, nb, s);
+    else op.to_internal(ein.p, rows_in, iin.p, nb, s);
+    f(iin.p, iout.p, nb, s);
+    if (out_is_grid) from_internal(nullptr, rows_out, iout.p, eout.p, rows_out, nb, s);
+    else op.from_internal(iout.p, eout.p, rows_out, nb, s);
+    GK_CUDA(cudaMemcpy2DAsync(Out + c0 * ldo, sizeof(double) * ldo, eout.p, sizeof(double) * rows_out,
+                              sizeof(double) * rows_out, nb, cudaMemcpyDeviceToHost, s));
+  }
+  GK_CUDA(cudaStreamSynchronize(s));
+}
+}  // namespace
+
+extern "C" {
+
+gk_status gk_dski_transpose_apply(const gk_op* h, const double* V, int64_t ldv, double* U, int64_t ldu,
+                                  int64_t nrhs) {
+  return guard([&] {
+    Op& op = O(h);
+    const i64 M = dski_grid_size(op);
+    if (ldv < op.N || ldu < M) fail(GK_ERR_ARG, "size mismatch");
+    if (nrhs <= 0) return;
+    grid_call(op, V, ldv, op.N, U, ldu, M, nrhs, false, true,
+              [&](const double* i, double* o, int nb, cudaStream_t s) { dski_transpose_apply(op, i, o, nb, s); });
+  });
+}
+
+gk_status gk_dski_apply(const gk_op* h, const double* U, int64_t ldu, double* Out, int64_t ldo, int64_t nrhs) {
+  return guard([&] {
+    Op& op = O(h);
+    const i64 M = dski_grid_size(op);
+    if (ldu < M || ldo < op.N) fail(GK_ERR_ARG, "size mismatch");
+    if (nrhs <= 0) return;
+    grid_call(op, U, ldu, M, Out, ldo, op.N, nrhs, true, false,
+              [&](const double* i, double* o, int nb, cudaStream_t s) { dski_apply(op, i, o, nb, s); });
+  });
+}
+
+gk_status gk_dski_grid_mvm(const gk_op* h, const double* U, int64_t ldu, double* W, int64_t ldw, int64_t nrhs) {
+  return guard([&] {
+    Op& op = O(h);
+    const i64 M = dski_grid_size(op);
+    if (ldu < M || ldw < M) fail(GK_ERR_ARG, "grid kernel MVM size mismatch");
+    if (nrhs <= 0) return;
+    grid_call(op, U, ldu, M, W, ldw, M, nrhs, true, true,
+              [&](const double* i, double* o, int nb, cudaStream_t s) { dski_grid_mvm(op, i, o, nb, s); });
+  });
+}
+
+gk_status gk_dski_predict_mean_grad(const gk_op* h, const double* alpha, double mean, const double* Xtest,
+                                    int64_t T, double* values, double* grads) {
+  return guard([&] {
+    Op& op = O(h);
+    const gk_grid g = dski_grid(op);
+    if (T <= 0) return;
+    std::lock_guard<std::mutex> lk(op.mu);
+    DeviceGuard dg(op.device);
+    cudaStream_t s = op.stream;
+    DevBuf<double> ae(static_cast<size_t>(op.N)), ai(static_cast<size_t>(op.N)), xt(static_cast<size_t>(T) * g.d), v(static_cast<size_t>(T)), gr(static_cast<size_t>(T) * g.d);
+    DevBuf<int> bad(1);
+    const int big = INT_MAX;
+    GK_CUDA(cudaMemcpyAsync(bad.p, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+    ae.upload(alpha, static_cast<size_t>(op.N), s);
+    op.to_internal(ae.p, op.N, ai.p, 1, s);
+    xt.upload(Xtest, static_cast<size_t>(T) * g.d, s);
+    dski_predict(op, ai.p, mean, xt.p, T, v.p, gr.p, bad.p, s);
+    int badh = INT_MAX;
+    GK_CUDA(cudaMemcpy(&badh, bad.p, sizeof(int), cudaMemcpyDeviceToHost));
+    if (badh != INT_MAX)
+      fail(GK_ERR_OUT_OF_GRID, "test point " + std::to_string(badh) + " lies outside the interior of the grid", badh);
+    GK_CUDA(cudaMemcpy(values, v.p, sizeof(double) * T, cudaMemcpyDeviceToHost));
+    GK_CUDA(cudaMemcpy(grads, gr.p, sizeof(double) * T * g.d, cudaMemcpyDeviceToHost));
+  });
+}
+
+gk_status gk_dski_cross_covariance(const gk_op* h, const double* Xtest, int64_t T, double* Q, int64_t ldq) {
+  return guard([&] {
+    Op& op = O(h);
+    const gk_grid g = dski_grid(op);
+    if (ldq < op.N) fail(GK_ERR_ARG, "size mismatch");
+    if (T <= 0) return;
+    std::lock_guard<std::mutex> lk(op.mu);
+    DeviceGuard dg(op.device);
+    cudaStream_t s = op.stream;
+    for (i64 t0 = 0; t0 < T; t0 += kMaxRhs) {
+      const i64 nt = std::min<i64>(kMaxRhs, T - t0);
+      std::vector<double> xh(static_cast<size_t>(nt) * g.d);
+      for (int j = 0; j < g.d; ++j)
+        for (i64 i = 0; i < nt; ++i) xh[static_cast<size_t>(j * nt + i)] = Xtest[j * T + t0 + i];
+      DevBuf<double> xt(static_cast<size_t>(nt) * g.d), qi(static_cast<size_t>(op.N) * nt), qe(static_cast<size_t>(op.N) * nt);
+      DevBuf<int> bad(1);
+      const int big = INT_MAX;
+      GK_CUDA(cudaMemcpyAsync(bad.p, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+      xt.upload(xh.data(), xh.size(), s);
+      dski_cross_cov(op, xt.p, nt, qi.p, bad.p, s);
+      int badh = INT_MAX;
+      GK_CUDA(cudaMemcpy(&badh, bad.p, sizeof(int), cudaMemcpyDeviceToHost));
+      if (badh != INT_MAX)
+        fail(GK_ERR_OUT_OF_GRID, "test point " + std::to_string(t0 + badh) + " lies outside the interior of the grid",
+             t0 + badh);
+      op.from_internal(qi.p, qe.p, op.N, int(nt), s);
+      GK_CUDA(cudaMemcpy2DAsync(Q + t0 * ldq, sizeof(double) * ldq, qe.p, sizeof(double) * op.N,
+                                sizeof(double) * op.N, nt, cudaMemcpyDeviceToHost, s));
+      GK_CUDA(cudaStreamSynchronize(s));
+    }
+  });
+}
+
+// ---------------------------------------------------------------- D-SKIP pieces
+int gk_dskip_factor_count(const gk_op* h) {
+  int c = -1;
+  guard([&] { c = dskip_factor_count(O(h)); });
+  return c;
+}
+int64_t gk_dskip_factor_rank(const gk_op* h, int f) {
+  int64_t r = -1;
+  guard([&] { r = dskip_factor_rank(O(h), f); });
+  return r;
+}
+gk_status gk_dskip_factor_get(const gk_op* h, int f, double* Q, double* alpha, double* beta) {
+  return guard([&] { dskip_factor_get(O(h), f, Q, alpha, beta); });
+}
+gk_status gk_dskip_dlogell_apply(const gk_op* h, const double* V, int64_t ldv, double* Out, int64_t ldo,
+                                 int64_t nrhs) {
+  return guard([&] {
+    Op& op = O(h);
+    if (ldv < op.N || ldo < op.N) fail(GK_ERR_ARG, "size mismatch");
+    if (nrhs <= 0) return;
+    grid_call(op, V, ldv, op.N, Out, ldo, op.N, nrhs, false, false,
+              [&](const double* i, double* o, int nb, cudaStream_t s) { dskip_dlogell(op, i, o, nb, s); });
+  });
+}
+
+// ---------------------------------------------------------------- solvers
+gk_status gk_pcg(const gk_op* h, const gk_precond* M, const double* B, int64_t ldb, int64_t nrhs, double tol,
+                 int maxit, double* X, int64_t ldx, int* iterations, int* converged, double* history,
+                 int* history_len) {
+  return guard([&] {
+    Op& op = O(h);
+    if (ldb < op.N || ldx < op.N) fail(GK_ERR_ARG, "cg: rhs size mismatch");
+    if (nrhs <= 0) return;
+    std::lock_guard<std::mutex> lk(op.mu);
+    DeviceGuard dg(op.device);
+    cudaStream_t s = op.stream;
+    Precond* P = M ? &precond_for(M, op) : nullptr;
+    std::unique_lock<std::mutex> plk;
+    if (P) plk = std::unique_lock<std::mutex>(P->mu);
+    const int chunk = int(std::min<i64>(nrhs, 256));
+    DevBuf<double> e(static_cast<size_t>(op.N) * chunk), bi(static_cast<size_t>(op.N) * chunk), xi(static_cast<size_t>(op.N) * chunk);
+    for (i64 c0 = 0; c0 < nrhs; c0 += chunk) {
+      const int nb = int(std::min<i64>(chunk, nrhs - c0));
+      upload_internal(op, B + c0 * ldb, ldb, e.p, bi.p, nb, s);
+      PcgResult r = pcg_internal(op, P, bi.p, xi.p, nb, tol, maxit, history != nullptr, s);
+      download_internal(op, xi.p, e.p, X + c0 * ldx, ldx, nb, s);
+      GK_CUDA(cudaStreamSynchronize(s));
+      for (int b = 0; b < nb; ++b) {
+        if (iterations) iterations[c0 + b] = r.iterations[static_cast<size_t>(b)];
+        if (converged) converged[c0 + b] = r.converged[static_cast<size_t>(b)];
+        if (history_len) history_len[c0 + b] = r.hist_len[static_cast<size_t>(b)];
+        if (history)
+          for (int it = 0; it <= maxit; ++it)
+            history[(c0 + b) * (maxit + 1) + it] = r.history[static_cast<size_t>(it) * nb + b];
+      }
+    }
+  });
+}
+
+gk_status gk_pcg_dev(const gk_op* h, const gk_precond* M, const double* dB, int64_t ldb, int64_t nrhs, double tol,
+                     int maxit, double* dX, int64_t ldx, int* iterations, int* converged, void* stream) {
+  return guard([&] {
+    Op& op = O(h);
+    if (ldb < op.N || ldx < op.N) fail(GK_ERR_ARG, "cg: rhs size mismatch");
+    if (nrhs <= 0) return;
+    std::lock_guard<std::mutex> lk(op.mu);
+    DeviceGuard dg(op.device);
+    cudaStream_t s = S(stream);
+    Precond* P = M ? &precond_for(M, op) : nullptr;
+    std::unique_lock<std::mutex> plk;
+    if (P) plk = std::unique_lock<std::mutex>(P->mu);
+    const int chunk = int(std::min<i64>(nrhs, 256));
+    op.scratch_a.reserve(static_cast<size_t>(op.N) * chunk);
+    op.scratch_b.reserve(static_cast<size_t>(op.N) * chunk);
+    for (i64 c0 = 0; c0 < nrhs; c0 += chunk) {
+      const int nb = int(std::min<i64>(chunk, nrhs - c0));
+      op.to_internal(dB + c0 * ldb, ldb, op.scratch_a.p, nb, s);
+      PcgResult r = pcg_internal(op, P, op.scratch_a.p, op.scratch_b.p, nb, tol, maxit, false, s);
+      op.from_internal(op.scratch_b.p, dX + c0 * ldx, ldx, nb, s);
+      for (int b = 0; b < nb; ++b) {
+        if (iterations) iterations[c0 + b] = r.iterations[static_cast<size_t>(b)];
+        if (converged) converged[c0 + b] = r.converged[static_cast<size_t>(b)];
+      }
+    }
+    GK_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+gk_status gk_pivoted_cholesky(const gk_op* h, int kernel_part, int64_t max_rank, double trace_tol,
+                              gk_pivchol** out) {
+  return guard([&] {
+    Op& op = O(h);
+    std::lock_guard<std::mutex> lk(op.mu);
+    DeviceGuard dg(op.device);
+    auto f = std::make_unique<gk_pivchol>();
+    f->impl = pivchol_run(op, kernel_part != 0, max_rank, trace_tol);
+    *out = f.release();
+  });
+}
+int64_t gk_pivchol_rank(const gk_pivchol* f) { return f && f->impl ? f->impl->k : -1; }
+gk_status gk_pivchol_get(const gk_pivchol* f, double* L, int64_t* pivots, double* it, double* rt) {
+  return guard([&] {
+    if (!f || !f->impl) fail(GK_ERR_ARG, "null factor");
+    const PivChol& p = *f->impl;
+    DeviceGuard dg(p.device);
+    if (L) pivchol_copy_L(p, L);
+    if (pivots)
+      for (size_t j = 0; j < p.pivots.size(); ++j) pivots[j] = p.pivots[j];
+    if (it) *it = p.initial_trace;
+    if (rt) *rt = p.residual_trace;
+  });
+}
+void gk_pivchol_destroy(gk_pivchol* f) { delete f; }
+
+gk_status gk_precond_create(const double* F, int64_t N, int64_t k, const double* noise_diag, int device,
+                            gk_precond** out) {
+  return guard([&] {  // linalg.cpp:176-194
+    if (N <= 0) fail(GK_ERR_ARG, "preconditioner needs strictly positive noise");
+    for (i64 i = 0; i < N; ++i)
+      if (!(noise_diag[i] > 0.0)) fail(GK_ERR_ARG, "preconditioner needs strictly positive noise");
+    if (k == 0) fail(GK_ERR_ARG, "preconditioner needs a factor of rank at least 1");
+    DeviceGuard dg(device);
+    cudaStream_t s;
+    GK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    DevBuf<double> Fd(static_cast<size_t>(N * k)), nd(static_cast<size_t>(N));
+    Fd.upload(F, static_cast<size_t>(N * k), s);
+    nd.upload(noise_diag, static_cast<size_t>(N), s);
+    auto M = std::make_unique<gk_precond>();
+    M->impl = precond_build(Fd.p, N, k, nd.p, device, s);
+    M->impl->stream = s;
+    *out = M.release();
+  });
+}
+
+gk_status gk_precond_from_pivchol(const gk_op* h, const gk_pivchol* f, gk_precond** out) {
+  return guard([&] {
+    Op& op = O(h);
+    if (!f || !f->impl) fail(GK_ERR_ARG, "null factor");
+    const PivChol& p = *f->impl;
+    if (p.k == 0) fail(GK_ERR_RUNTIME, "pivoted Cholesky produced an empty preconditioner factor");
+    std::lock_guard<std::mutex> lk(op.mu);
+    DeviceGuard dg(op.device);
+    cudaStream_t s;
+    GK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    std::vector<double> nh(static_cast<size_t>(op.N));
+    for (i64 r = 0; r < op.N; ++r) nh[static_cast<size_t>(r)] = r < op.n_value ? op.nv2 : op.ng2;
+    if (op.nv2 <= 0.0 || (op.N > op.n_value && op.ng2 <= 0.0))
+      fail(GK_ERR_ARG, "preconditioner needs strictly positive noise");
+    DevBuf<double> nd(static_cast<size_t>(op.N));
+    nd.upload(nh.data(), nh.size(), s);  // group structure is order-invariant
+    auto M = std::make_unique<gk_precond>();
+    M->impl = precond_build(p.L.p, op.N, p.k, nd.p, op.device, s);
+    M->impl->stream = s;
+    M->impl->ext = op.d_ext_of_int();
+    *out = M.release();
+  });
+}
+
+gk_status gk_precond_apply(const gk_precond* M, const double* B, int64_t ldb, double* Out, int64_t ldo,
+                           int64_t nrhs) {
+  return guard([&] {
+    if (!M || !M->impl) fail(GK_ERR_ARG, "null preconditioner");
+    Precond& P = *M->impl;
+    if (ldb < P.N || ldo < P.N) fail(GK_ERR_ARG, "size mismatch");
+    if (nrhs <= 0) return;
+    std::lock_guard<std::mutex> lk(P.mu);
+    DeviceGuard dg(P.device);
+    cudaStream_t s = P.stream;
+    const int chunk = int(std::min<i64>(nrhs, kMaxRhs));
+    DevBuf<double> e(static_cast<size_t>(P.N) * chunk), a(static_cast<size_t>(P.N) * chunk), b(static_cast<size_t>(P.N) * chunk);
+    for (i64 c0 = 0; c0 < nrhs; c0 += chunk) {
+      const int nb = int(std::min<i64>(chunk, nrhs - c0));
+      GK_CUDA(cudaMemcpy2DAsync(e.p, sizeof(double) * P.N, B + c0 * ldb, sizeof(double) * ldb, sizeof(double) * P.N,
+                                nb, cudaMemcpyHostToDevice, s));
+      to_internal(P.ext, P.N, e.p, P.N, a.p, nb, s);
+      P.apply(a.p, b.p, nb, s);
+      from_internal(P.ext, P.N, b.p, e.p, P.N, nb, s);
+      GK_CUDA(cudaMemcpy2DAsync(Out + c0 * ldo, sizeof(double) * ldo, e.p, sizeof(double) * P.N,
+                                sizeof(double) * P.N, nb, cudaMemcpyDeviceToHost, s));
+    }
+    GK_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+gk_status gk_precond_quadratic(const gk_precond* M, const double* B, int64_t ldb, int64_t nrhs, double* out) {
+  return guard([&] {
+    if (!M || !M->impl) fail(GK_ERR_ARG, "null preconditioner");
+    Precond& P = *M->impl;
+    if (ldb < P.N) fail(GK_ERR_ARG, "size mismatch");
+    if (nrhs <= 0) return;
+    std::lock_guard<std::mutex> lk(P.mu);
+    DeviceGuard dg(P.device);
+    cudaStream_t s = P.stream;
+    const int chunk = int(std::min<i64>(nrhs, kMaxRhs));
+    DevBuf<double> e(static_cast<size_t>(P.N) * chunk), a(static_cast<size_t>(P.N) * chunk);
+    for (i64 c0 = 0; c0 < nrhs; c0 += chunk) {
+      const int nb = int(std::min<i64>(chunk, nrhs - c0));
+      GK_CUDA(cudaMemcpy2DAsync(e.p, sizeof(double) * P.N, B + c0 * ldb, sizeof(double) * ldb, sizeof(double) * P.N,
+                                nb, cudaMemcpyHostToDevice, s));
+      to_internal(P.ext, P.N, e.p, P.N, a.p, nb, s);
+      precond_quadratic(P, a.p, nb, out + c0, s);
+    }
+  });
+}
+
+int64_t gk_precond_rank(const gk_precond* M) { return M && M->impl ? M->impl->k : -1; }
+
+gk_status gk_precond_q1(const gk_precond* M, double* Q1) {
+  return guard([&] {
+    if (!M || !M->impl) fail(GK_ERR_ARG, "null preconditioner");
+    Precond& P = *M->impl;
+    std::lock_guard<std::mutex> lk(P.mu);
+    DeviceGuard dg(P.device);
+    cudaStream_t s = P.stream;
+    DevBuf<double> e(static_cast<size_t>(P.N * P.k)), t(static_cast<size_t>(P.N * P.k));
+    // q1 rows are internal-ordered [N][k] -> external col-major N×k
+    from_internal(P.ext, P.N, P.q1.p, e.p, P.N, int(P.k), s);
+    GK_CUDA(cudaMemcpyAsync(Q1, e.p, sizeof(double) * P.N * P.k, cudaMemcpyDeviceToHost, s));
+    GK_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+void gk_precond_destroy(gk_precond* M) { delete M; }
+
+gk_status gk_slq_logdet(const gk_op* h, int probes, int steps, uint64_t seed, double floor_, int probe_offset,
+                        double* logdet, int* clamped, double* estimates) {
+  return guard([&] {  // linalg.cpp:215-253
+    Op& op = O(h);
+    *logdet = 0.0;
+    if (clamped) *clamped = 0;
+    if (probes <= 0) return;
+    std::lock_guard<std::mutex> lk(op.mu);
+    DeviceGuard dg(op.device);
+    cudaStream_t s = op.stream;
+    const i64 N = op.N;
+    const int chunk = std::min(probes, 64);
+    std::vector<double> est(static_cast<size_t>(probes), 0.0);
+    std::vector<int> clamps(static_cast<size_t>(probes), 0);
+    std::vector<double> hz(static_cast<size_t>(N) * chunk);
+    DevBuf<double> ze(static_cast<size_t>(N) * chunk), zi(static_cast<size_t>(N) * chunk);
+    for (int p0 = 0; p0 < probes; p0 += chunk) {
+      const int P = std::min(chunk, probes - p0);
+      std::vector<std::uint64_t> rseeds(static_cast<size_t>(P));
+      double zn2 = 0.0;
+      for (int q = 0; q < P; ++q) {
+        const std::uint64_t pid = std::uint64_t(probe_offset + p0 + q);
+        rademacher(N, seed, pid, hz.data() + static_cast<size_t>(q) * N);
+        double s2 = 0.0;
+        for (i64 i = 0; i < N; ++i) s2 += hz[static_cast<size_t>(q) * N + i] * hz[static_cast<size_t>(q) * N + i];
+        zn2 = s2;
+        const double zn = std::sqrt(s2);
+        for (i64 i = 0; i < N; ++i) hz[static_cast<size_t>(q) * N + i] /= zn;
+        rseeds[static_cast<size_t>(q)] = mix_seed(seed, 50000 + pid);
+      }
+      ze.upload(hz.data(), static_cast<size_t>(N) * P, s);
+      op.to_internal(ze.p, N, zi.p, P, s);
+      LanczosBatch lb = lanczos_batch(op, zi.p, P, steps, rseeds, nullptr, s);
+      for (int q = 0; q < P; ++q) {
+        const int len = lb.len[static_cast<size_t>(q)];
+        std::vector<double> ev(static_cast<size_t>(len)), Z(static_cast<size_t>(len) * len);
+        tridiag_eig(len, lb.alpha[static_cast<size_t>(q)].data(), lb.beta[static_cast<size_t>(q)].data(), ev.data(), Z.data());
+        double e = 0.0;
+        for (int i = 0; i < len; ++i) {
+          double lambda = ev[static_cast<size_t>(i)];
+          if (lambda < floor_) {
+            lambda = floor_;
+            ++clamps[static_cast<size_t>(p0 + q)];
+          }
+          const double w0 = Z[static_cast<size_t>(i) * len];
+          e += w0 * w0 * std::log(lambda);
+        }
+        est[static_cast<size_t>(p0 + q)] = zn2 * e;
+      }
+    }
+    double sum = 0.0;
+    int cl = 0;
+    for (int p = 0; p < probes; ++p) {
+      sum += est[static_cast<size_t>(p)];
+      cl += clamps[static_cast<size_t>(p)];
+    }
+    *logdet = sum / probes;
+    if (clamped) *clamped = cl;
+    if (estimates) std::copy(est.begin(), est.end(), estimates);
+  });
+}
+
+gk_status gk_lanczos(const gk_op* h, int64_t steps, uint64_t seed, const double* start, uint64_t restart_seed,
+                     double* Q, double* alpha, double* beta, int64_t* k, int* breakdown) {
+  return guard([&] {
+    Op& op = O(h);
+    const i64 N = op.N;
+    if (!start && (steps <= 0 || steps > N)) fail(GK_ERR_ARG, "Lanczos rank must lie in [1, N]");
+    steps = std::min<i64>(steps, N);
+    std::lock_guard<std::mutex> lk(op.mu);
+    DeviceGuard dg(op.device);
+    cudaStream_t s = op.stream;
+    std::vector<double> q(static_cast<size_t>(N));
+    std::uint64_t rs = restart_seed;
+    if (start) {
+      std::copy(start, start + N, q.begin());
+    } else {  // lanczos_lowrank (linalg.cpp:306-314)
+      gaussian(N, seed, 0, q.data());
+      double nn = 0.0;
+      for (double v : q) nn += v * v;
+      nn = std::sqrt(nn);
+      for (double& v : q) v /= nn;
+      rs = mix_seed(seed, 1);
+    }
+    DevBuf<double> e(static_cast<size_t>(N)), i1(static_cast<size_t>(N)), Qd(static_cast<size_t>(N) * std::max<i64>(steps, 1));
+    e.upload(q.data(), static_cast<size_t>(N), s);
+    op.to_internal(e.p, N, i1.p, 1, s);
+    LanczosBatch lb = lanczos_batch(op, i1.p, 1, int(steps), {rs}, Qd.p, s);
+    const int len = lb.len[0];
+    if (Q && len > 0) {
+      DevBuf<double> qe(static_cast<size_t>(N) * len);
+      // Qd is [steps][N][1] == internal RHS-minor per column: convert each column
+      for (int j = 0; j < len; ++j) op.from_internal(Qd.p + (i64)j * N, qe.p + (i64)j * N, N, 1, s);
+      GK_CUDA(cudaMemcpyAsync(Q, qe.p, sizeof(double) * N * len, cudaMemcpyDeviceToHost, s));
+      GK_CUDA(cudaStreamSynchronize(s));
+    }
+    if (alpha) std::copy(lb.alpha[0].begin(), lb.alpha[0].end(), alpha);
+    if (beta) std::copy(lb.beta[0].begin(), lb.beta[0].end(), beta);
+    *k = len;
+    if (breakdown) *breakdown = lb.breakdown[0];
+  });
+}
+
+gk_status gk_trace_estimate(const gk_op* hA, const gk_op* hB, int probes, uint64_t seed, double tol, int maxit,
+                            const gk_precond* M, double* out) {
+  return guard([&] {  // linalg.cpp:255-279
+    Op& A = O(hA);
+    Op& B = O(hB);
+    if (A.N != B.N) fail(GK_ERR_ARG, "trace_estimate: size mismatch");
+    *out = 0.0;
+    if (probes <= 0) return;
+    const i64 N = A.N;
+    std::vector<double> est(static_cast<size_t>(probes), 0.0);
+    bool failed = false;
+    const int chunk = std::min(probes, 64);
+    std::vector<double> hz(static_cast<size_t>(N) * chunk), hbz(static_cast<size_t>(N) * chunk), hx(static_cast<size_t>(N) * chunk);
+    for (int p0 = 0; p0 < probes; p0 += chunk) {
+      const int P = std::min(chunk, probes - p0);
+      for (int q = 0; q < P; ++q) rademacher(N, seed, 1000 + std::uint64_t(p0 + q), hz.data() + static_cast<size_t>(q) * N);
+      gk_status st = gk_op_mvm(hB, hz.data(), N, hbz.data(), N, P);
+      if (st != GK_OK) fail(st, g_err);
+      std::vector<int> its(static_cast<size_t>(P)), conv(static_cast<size_t>(P));
+      st = gk_pcg(hA, M, hz.data(), N, P, tol, maxit, hx.data(), N, its.data(), conv.data(), nullptr, nullptr);
+      if (st != GK_OK) fail(st, g_err);
+      for (int q = 0; q < P; ++q) {
+        if (!conv[static_cast<size_t>(q)]) failed = true;
+        double dsum = 0.0;
+        for (i64 i = 0; i < N; ++i) dsum += hx[static_cast<size_t>(q) * N + i] * hbz[static_cast<size_t>(q) * N + i];
+        est[static_cast<size_t>(p0 + q)] = dsum;
+      }
+    }
+    if (failed)
+      fail(GK_ERR_RUNTIME, "trace_estimate: CG did not converge within " + std::to_string(maxit) + " iterations");
+    double sum = 0.0;
+    for (int p = 0; p < probes; ++p) sum += est[static_cast<size_t>(p)];
+    *out = sum / probes;
+  });
+}
+
+gk_status gk_make_dataset(int config, uint64_t seed, int64_t* n, int* d, double* X, double* y, double* dY) {
+  gk_status st = GK_OK;
+  try {
+    st = gk_make_dataset_impl(config, seed, n, d, X, y, dY);
+    if (st != GK_OK) g_err = "unknown dataset config";
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    st = GK_ERR_RUNTIME;
+  }
+  return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,801 @@
+// dski.cu — the D-SKI operator on B200 (reference dski.cpp:174-304,
+// interpolation.cpp:59-97,212-266).
+//
+//   K∇_DSKI v = B K_UU B^T v + diag(σ1² I_n, σ2² I_nd) v,  B = [W; ∂W_1; …; ∂W_d]
+//
+// Design:
+//  * Points are sorted once by stencil base cell. Per sorted point we keep the
+//    base multi-index and the d 1-D quintic (or cubic) weight/derivative
+//    stencils (interpolation.cpp:66-97); W/∂W are never stored as CSR.
+//  * B^T (scatter) is an atomic-free gather by grid node: every (node, rhs)
+//    item walks the T^(d-1) runs of candidate base cells whose points cover it
+//    (contiguous in the sorted order along the last axis) — deterministic
+//    order, no atomics.
+//  * K_UU is the Kronecker product of per-axis symmetric Toeplitz matrices
+//    (SE is separable: profile(o) = s² Π_j exp(-o_j²/2ℓ²)), applied mode by
+//    mode as register-tiled fp64 GEMMs with the Toeplitz tile generated from
+//    the 1-D sequence. This is the same linear map as the reference's
+//    circulant-embedding FFT (dski.cpp:146-166) — the embedding reproduces
+//    the Toeplitz product exactly — evaluated without the 2^d-fold
+//    embedding.
+//  * B (gather) + noise is one kernel, sum-factorised across axes.
+// All vectors are in the internal layout: rows = g*n + sorted point,
+// right-hand sides innermost.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <sstream>
+
+#include "gk_common.hpp"
+#include "gk_kernels.cuh"
+
+namespace gk {
+
+namespace {
+
+// ---------------------------------------------------------------- host stencil
+// interpolation.cpp:15-57: quintic (C², degree-4 reproduction) and Keys cubic.
+inline double quintic_piece(double s) {
+  if (s < 1.0) return (((-25.0 * s + 63.0) * s - 35.0) * s * s * s - 15.0 * s * s + 12.0) / 12.0;
+  if (s < 2.0) return (s - 2.0) * (s - 1.0) * ((25.0 * s - 114.0) * s * s + 153.0 * s - 48.0) / 24.0;
+  if (s < 3.0) {
+    const double t = s - 3.0;
+    return -t * t * t * (s - 2.0) * (5.0 * s - 8.0) / 24.0;
+  }
+  return 0.0;
+}
+inline double quintic_piece_deriv(double s) {
+  if (s < 1.0) return ((((-125.0 * s + 252.0) * s - 105.0) * s - 30.0) * s) / 12.0;
+  if (s < 2.0) return ((((125.0 * s - 756.0) * s + 1635.0) * s - 1470.0) * s + 450.0) / 24.0;
+  if (s < 3.0) return ((((-25.0 * s + 252.0) * s - 939.0) * s + 1530.0) * s - 918.0) / 24.0;
+  return 0.0;
+}
+inline double cubic_val(double s) {
+  const double a = std::fabs(s);
+  if (a < 1.0) return ((1.5 * a - 2.5) * a) * a + 1.0;
+  if (a < 2.0) return ((-0.5 * a + 2.5) * a - 4.0) * a + 2.0;
+  return 0.0;
+}
+inline double cubic_der(double s) {
+  const double sg = s < 0.0 ? -1.0 : 1.0;
+  const double a = std::fabs(s);
+  double v = 0.0;
+  if (a < 1.0) v = (4.5 * a - 5.0) * a;
+  else if (a < 2.0) v = (-1.5 * a + 5.0) * a - 4.0;
+  return sg * v;
+}
+
+// One axis of one point: base node, value and derivative weights (÷h).
+void axis_weights(double x, double origin, double h, int m, int T, i64 point, int axis, int* base,
+                  double* w, double* dw) {
+  const double s = (x - origin) / h;
+  const i64 cell = static_cast<i64>(std::floor(s));
+  const double t = s - static_cast<double>(cell);
+  const i64 b = cell - (T == 6 ? 2 : 1);
+  if (!(t >= 0.0 && t < 1.0) || b < 0 || b + T > m) {
+    std::ostringstream msg;
+    msg << "point " << point << " (coordinate " << x << " on axis " << axis
+        << ") lies outside the interior of the grid";
+    fail(GK_ERR_OUT_OF_GRID, msg.str(), point);
+  }
+  for (int k = 0; k < T; ++k) {
+    const double arg = t - static_cast<double>(k - (T == 6 ? 2 : 1));
+    if (T == 6) {
+      w[k] = quintic_piece(std::fabs(arg));
+      dw[k] = (arg < 0.0 ? -quintic_piece_deriv(-arg) : quintic_piece_deriv(arg)) / h;
+    } else {
+      w[k] = cubic_val(arg);
+      dw[k] = cubic_der(arg) / h;
+    }
+  }
+  *base = static_cast<int>(b);
+}
+
+}  // namespace
+
+// ================================================================ kernels
+struct DskiView {
+  int d, T, G;  // dims, taps, groups (0 or d)
+  int m[3];     // grid nodes per axis
+  int nb[3];    // base cells per axis (m - T + 1)
+  i64 n, M;
+  const int4* base;      // [n] sorted
+  const double* wts;     // [n][d][2][T]
+  const int* cell_start; // [ncells + 1]
+  double nv2, ng2;
+};
+
+template <int D, int T, bool GRAD>
+__global__ void __launch_bounds__(256) k_scatter(DskiView op, const double* __restrict__ v,
+                                                 double* __restrict__ u, int nrhs) {
+  constexpr int STRIDE = D * 2 * T;
+  const i64 items = op.M * nrhs;
+  for (i64 it = blockIdx.x * (i64)blockDim.x + threadIdx.x; it < items;
+       it += (i64)gridDim.x * blockDim.x) {
+    const int b = int(it % nrhs);
+    i64 node = it / nrhs;
+    int k[3];
+#pragma unroll
+    for (int j = D - 1; j >= 0; --j) {
+      k[j] = int(node % op.m[j]);
+      node /= op.m[j];
+    }
+    double acc = 0.0;
+    const int kl = k[D - 1];
+    const int bl_lo = max(0, kl - (T - 1));
+    const int bl_hi = min(op.nb[D - 1] - 1, kl);
+    if (bl_lo <= bl_hi) {
+      // leading axes: T^(D-1) combinations of offsets t_0..t_{D-2}
+      constexpr int LEAD = (D == 1) ? 1 : (D == 2 ? T : T * T);
+      for (int lc = 0; lc < LEAD; ++lc) {
+        int t0 = 0, t1 = 0;
+        i64 cell_row = 0;
+        bool ok = true;
+        if constexpr (D >= 2) {
+          t0 = (D == 2) ? lc : lc / T;
+          const int b0 = k[0] - t0;
+          ok = b0 >= 0 && b0 < op.nb[0];
+          cell_row = b0;
+          if constexpr (D == 3) {
+            t1 = lc % T;
+            const int b1 = k[1] - t1;
+            ok = ok && b1 >= 0 && b1 < op.nb[1];
+            cell_row = cell_row * op.nb[1] + b1;
+          }
+        }
+        if (!ok) continue;
+        const i64 c0 = cell_row * op.nb[D - 1];
+        const int s_lo = __ldg(op.cell_start + c0 + bl_lo);
+        const int s_hi = __ldg(op.cell_start + c0 + bl_hi + 1);
+        for (int s = s_lo; s < s_hi; ++s) {
+          const int4 bs = __ldg(op.base + s);
+          const double* p = op.wts + (i64)s * STRIDE;
+          const int tl = kl - (D == 1 ? bs.x : (D == 2 ? bs.y : bs.z));
+          if constexpr (D == 1) {
+            const double w0 = __ldg(p + tl);
+            if constexpr (GRAD) {
+              const double dw0 = __ldg(p + T + tl);
+              acc += w0 * __ldg(v + (i64)s * nrhs + b) + dw0 * __ldg(v + ((i64)op.n + s) * nrhs + b);
+            } else {
+              acc += w0 * __ldg(v + (i64)s * nrhs + b);
+            }
+          } else if constexpr (D == 2) {
+            const double w0 = __ldg(p + t0), w1 = __ldg(p + 2 * T + tl);
+            const double v0 = __ldg(v + (i64)s * nrhs + b);
+            if constexpr (GRAD) {
+              const double dw0 = __ldg(p + T + t0), dw1 = __ldg(p + 3 * T + tl);
+              const double v1 = __ldg(v + ((i64)op.n + s) * nrhs + b);
+              const double v2 = __ldg(v + (2 * (i64)op.n + s) * nrhs + b);
+              acc += w1 * (v0 * w0 + v1 * dw0) + dw1 * (v2 * w0);
+            } else {
+              acc += w0 * w1 * v0;
+            }
+          } else {
+            const double w0 = __ldg(p + t0), w1 = __ldg(p + 2 * T + t1), w2 = __ldg(p + 4 * T + tl);
+            const double v0 = __ldg(v + (i64)s * nrhs + b);
+            if constexpr (GRAD) {
+              const double dw0 = __ldg(p + T + t0), dw1 = __ldg(p + 3 * T + t1),
+                           dw2 = __ldg(p + 5 * T + tl);
+              const double v1 = __ldg(v + ((i64)op.n + s) * nrhs + b);
+              const double v2 = __ldg(v + (2 * (i64)op.n + s) * nrhs + b);
+              const double v3 = __ldg(v + (3 * (i64)op.n + s) * nrhs + b);
+              // w2*(w1*(v0 w0 + v1 dw0) + dw1*(v2 w0)) + dw2*(w1*(v3 w0))
+              acc += w2 * (w1 * (v0 * w0 + v1 * dw0) + dw1 * (v2 * w0)) + dw2 * (w1 * (v3 * w0));
+            } else {
+              acc += w0 * w1 * w2 * v0;
+            }
+          }
+        }
+      }
+    }
+    u[it] = acc;
+  }
+}
+
+template <int D, int T, bool GRAD>
+__global__ void __launch_bounds__(256) k_gather(DskiView op, const double* __restrict__ w,
+                                                const double* __restrict__ v,
+                                                double* __restrict__ out, int nrhs, int noise) {
+  constexpr int STRIDE = D * 2 * T;
+  const i64 items = op.n * nrhs;
+  for (i64 it = blockIdx.x * (i64)blockDim.x + threadIdx.x; it < items;
+       it += (i64)gridDim.x * blockDim.x) {
+    const int b = int(it % nrhs);
+    const i64 s = it / nrhs;
+    const int4 bs = __ldg(op.base + s);
+    const double* p = op.wts + s * STRIDE;
+    double o[D + 1];
+#pragma unroll
+    for (int g = 0; g <= D; ++g) o[g] = 0.0;
+    if constexpr (D == 1) {
+      const double* wr = w + (i64)bs.x * nrhs + b;
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const double uu = __ldg(wr + (i64)t * nrhs);
+        o[0] += __ldg(p + t) * uu;
+        if constexpr (GRAD) o[1] += __ldg(p + T + t) * uu;
+      }
+    } else if constexpr (D == 2) {
+      double w1[T], dw1[T];
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        w1[t] = __ldg(p + 2 * T + t);
+        if constexpr (GRAD) dw1[t] = __ldg(p + 3 * T + t);
+      }
+#pragma unroll
+      for (int t0 = 0; t0 < T; ++t0) {
+        const double* wr = w + ((i64)(bs.x + t0) * op.m[1] + bs.y) * nrhs + b;
+        double r = 0.0, q = 0.0;
+#pragma unroll
+        for (int t1 = 0; t1 < T; ++t1) {
+          const double uu = __ldg(wr + (i64)t1 * nrhs);
+          r += w1[t1] * uu;
+          if constexpr (GRAD) q += dw1[t1] * uu;
+        }
+        const double w0 = __ldg(p + t0);
+        o[0] += w0 * r;
+        if constexpr (GRAD) {
+          o[1] += __ldg(p + T + t0) * r;
+          o[2] += w0 * q;
+        }
+      }
+    } else {
+      double w2[T], dw2[T];
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        w2[t] = __ldg(p + 4 * T + t);
+        if constexpr (GRAD) dw2[t] = __ldg(p + 5 * T + t);
+      }
+#pragma unroll
+      for (int t0 = 0; t0 < T; ++t0) {
+        double R0 = 0.0, R1 = 0.0, R2 = 0.0;  // value, ∂1 (axis 1), ∂2 (axis 2) partials
+#pragma unroll
+        for (int t1 = 0; t1 < T; ++t1) {
+          const double* wr = w + (((i64)(bs.x + t0) * op.m[1] + bs.y + t1) * op.m[2] + bs.z) * nrhs + b;
+          double r = 0.0, q = 0.0;
+#pragma unroll
+          for (int t2 = 0; t2 < T; ++t2) {
+            const double uu = __ldg(wr + (i64)t2 * nrhs);
+            r += w2[t2] * uu;
+            if constexpr (GRAD) q += dw2[t2] * uu;
+          }
+          const double w1 = __ldg(p + 2 * T + t1);
+          R0 += w1 * r;
+          if constexpr (GRAD) {
+            R1 += __ldg(p + 3 * T + t1) * r;
+            R2 += w1 * q;
+          }
+        }
+        const double w0 = __ldg(p + t0);
+        o[0] += w0 * R0;
+        if constexpr (GRAD) {
+          o[1] += __ldg(p + T + t0) * R0;
+          o[2] += w0 * R1;
+          o[3] += w0 * R2;
+        }
+      }
+    }
+    constexpr int NG = GRAD ? D + 1 : 1;
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+      const i64 idx = ((i64)g * op.n + s) * nrhs + b;
+      double val = o[g];
+      if (noise) val += (g == 0 ? op.nv2 : op.ng2) * __ldg(v + idx);
+      out[idx] = val;
+    }
+  }
+}
+
+// Diagonal via separability: for SE, Σ_ab w_a w_b k(u_a-u_b) over a
+// tensor-product stencil factorises into Π_j Σ_ab c_j[a] c_j[b] t_j[|a-b|]
+// (same quantity as dski.cpp:240-290's offset-table double loop).
+template <int D, int T>
+__global__ void k_diagonal(DskiView op, const double* __restrict__ tvec, const int* __restrict__ toff,
+                           double* __restrict__ diag) {
+  constexpr int STRIDE = D * 2 * T;
+  for (i64 s = blockIdx.x * (i64)blockDim.x + threadIdx.x; s < op.n; s += (i64)gridDim.x * blockDim.x) {
+    const double* p = op.wts + s * STRIDE;
+    double S[D][2];  // per axis: plain and derivative quadratic forms
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const double* tj = tvec + toff[j];
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int a = 0; a < T; ++a)
+#pragma unroll
+        for (int c = 0; c < T; ++c) {
+          const double kk = __ldg(tj + (a > c ? a - c : c - a));
+          a0 += p[j * 2 * T + a] * p[j * 2 * T + c] * kk;
+          a1 += p[j * 2 * T + T + a] * p[j * 2 * T + T + c] * kk;
+        }
+      S[j][0] = a0;
+      S[j][1] = a1;
+    }
+    const int NG = op.G + 1;
+    for (int g = 0; g < NG; ++g) {
+      double prod = 1.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) prod *= S[j][g == j + 1 ? 1 : 0];
+      diag[(i64)g * op.n + s] = prod + (g == 0 ? op.nv2 : op.ng2);
+    }
+  }
+}
+
+// Row r of the operator (dski.cpp:292-304) via separability: K_UU applied to
+// the tensor-product stencil of row r is ⊗_j α_j with α_j = T_j c_j (each a
+// short 1-D Toeplitz–stencil product), so row entries are products of 1-D
+// stencil dots. Each CTA rebuilds the α_j in shared memory.
+template <int D, int T>
+__global__ void k_row(DskiView op, const double* __restrict__ tvec, const int* __restrict__ toff,
+                      int src_s, int src_g, double* __restrict__ out) {
+  extern __shared__ double alpha[];  // Σ m_j
+  constexpr int STRIDE = D * 2 * T;
+  const int4 sb = op.base[src_s];
+  const int sbase[3] = {sb.x, sb.y, sb.z};
+  const double* sp = op.wts + (i64)src_s * STRIDE;
+  int aoff[3];
+  int tot = 0;
+  for (int j = 0; j < D; ++j) {
+    aoff[j] = tot;
+    tot += op.m[j];
+  }
+  for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+    int j = 0;
+    while (j + 1 < D && idx >= aoff[j + 1]) ++j;
+    const int kk = idx - aoff[j];
+    const double* c = sp + j * 2 * T + (src_g == j + 1 ? T : 0);
+    const double* tj = tvec + toff[j];
+    double acc = 0.0;
+    for (int t = 0; t < T; ++t) {
+      const int off = kk - (sbase[j] + t);
+      acc += tj[off < 0 ? -off : off] * c[t];
+    }
+    alpha[idx] = acc;
+  }
+  __syncthreads();
+  const int NG = op.G + 1;
+  const i64 items = op.n * NG;
+  const i64 r_self = (i64)src_g * op.n + src_s;
+  for (i64 it = blockIdx.x * (i64)blockDim.x + threadIdx.x; it < items; it += (i64)gridDim.x * blockDim.x) {
+    const int g = int(it / op.n);
+    const i64 s = it % op.n;
+    const int4 bs = op.base[s];
+    const int bb[3] = {bs.x, bs.y, bs.z};
+    const double* p = op.wts + s * STRIDE;
+    double prod = 1.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const double* c = p + j * 2 * T + (g == j + 1 ? T : 0);
+      double dot = 0.0;
+#pragma unroll
+      for (int t = 0; t < T; ++t) dot += c[t] * alpha[aoff[j] + bb[j] + t];
+      prod *= dot;
+    }
+    if (it == r_self) prod += (g == 0 ? op.nv2 : op.ng2);
+    out[it] = prod;
+  }
+}
+
+// Test-point stencils for prediction (gp.cpp:480-495): values/grads from a
+// grid vector g (single column).
+template <int D, int T>
+__global__ void k_predict(DskiView op, const double* __restrict__ X, i64 nT, const double* origin3,
+                          const double* h3, const double* __restrict__ g, double mean,
+                          double* __restrict__ vals, double* __restrict__ grads, int* __restrict__ bad) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < nT; i += (i64)gridDim.x * blockDim.x) {
+    int base[3];
+    double w[3][T], dw[3][T];
+    bool ok = true;
+    for (int j = 0; j < D; ++j) {
+      const double h = h3[j];
+      const double sv = (X[j * nT + i] - origin3[j]) / h;
+      const double cell = floor(sv);
+      const double t = sv - cell;
+      const int b = int(cell) - (T == 6 ? 2 : 1);
+      if (!(t >= 0.0 && t < 1.0) || b < 0 || b + T > op.m[j]) ok = false;
+      base[j] = b;
+      stencil_weights<T>(t, h, w[j], dw[j]);
+    }
+    if (!ok) {
+      atomicMin(bad, int(i));
+      continue;
+    }
+    double acc = 0.0, gr[3] = {0, 0, 0};
+    if constexpr (D == 1) {
+      for (int a = 0; a < T; ++a) {
+        const double gv = g[base[0] + a];
+        acc += w[0][a] * gv;
+        gr[0] += dw[0][a] * gv;
+      }
+    } else if constexpr (D == 2) {
+      for (int a = 0; a < T; ++a)
+        for (int c = 0; c < T; ++c) {
+          const double gv = g[(i64)(base[0] + a) * op.m[1] + base[1] + c];
+          acc += w[0][a] * w[1][c] * gv;
+          gr[0] += dw[0][a] * w[1][c] * gv;
+          gr[1] += w[0][a] * dw[1][c] * gv;
+        }
+    } else {
+      for (int a = 0; a < T; ++a)
+        for (int c = 0; c < T; ++c)
+          for (int e = 0; e < T; ++e) {
+            const double gv = g[((i64)(base[0] + a) * op.m[1] + base[1] + c) * op.m[2] + base[2] + e];
+            acc += w[0][a] * w[1][c] * w[2][e] * gv;
+            gr[0] += dw[0][a] * w[1][c] * w[2][e] * gv;
+            gr[1] += w[0][a] * dw[1][c] * w[2][e] * gv;
+            gr[2] += w[0][a] * w[1][c] * dw[2][e] * gv;
+          }
+    }
+    vals[i] = mean + acc;
+    for (int j = 0; j < D; ++j) grads[j * nT + i] = gr[j];
+  }
+}
+
+// Scatter the stencils of test points as columns of a grid block (for
+// cross_covariance, gp.cpp:412-417): U[node][t] = w(point t, node).
+template <int D, int T>
+__global__ void k_test_stencils(DskiView op, const double* __restrict__ X, i64 nT,
+                                const double* origin3, const double* h3, double* __restrict__ U,
+                                int* __restrict__ bad) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < nT; i += (i64)gridDim.x * blockDim.x) {
+    int base[3] = {0, 0, 0};
+    double w[3][T], dw[3][T];
+    bool ok = true;
+    for (int j = 0; j < D; ++j) {
+      const double sv = (X[j * nT + i] - origin3[j]) / h3[j];
+      const double cell = floor(sv);
+      const double t = sv - cell;
+      const int b = int(cell) - (T == 6 ? 2 : 1);
+      if (!(t >= 0.0 && t < 1.0) || b < 0 || b + T > op.m[j]) ok = false;
+      base[j] = b;
+      stencil_weights<T>(t, h3[j], w[j], dw[j]);
+    }
+    if (!ok) {
+      atomicMin(bad, int(i));
+      continue;
+    }
+    int cnt = 1;
+    for (int j = 0; j < D; ++j) cnt *= T;
+    for (int c = 0; c < cnt; ++c) {
+      int rem = c;
+      i64 node = 0;
+      double wt = 1.0;
+      int tt[3];
+      for (int j = D - 1; j >= 0; --j) {
+        tt[j] = rem % T;
+        rem /= T;
+      }
+      for (int j = 0; j < D; ++j) {
+        node = node * op.m[j] + base[j] + tt[j];
+        wt *= w[j][tt[j]];
+      }
+      U[node * nT + i] = wt;
+    }
+  }
+}
+
+// ================================================================ operator
+struct DskiOp final : Op {
+  int d = 0, T = 6, G = 0;
+  int m[3] = {1, 1, 1}, nb[3] = {1, 1, 1};
+  i64 n = 0, M = 0;
+  gk_grid grid{};
+  gk_kernel kernel{};
+  DevBuf<int4> base;
+  DevBuf<double> wts;
+  DevBuf<int> cell_start;
+  DevBuf<double> tvec;  // concatenated per-axis Toeplitz sequences (axis 0 carries s²)
+  DevBuf<int> toff;
+  std::vector<int> toff_h;
+  std::vector<int> band;  // per-axis numerical band of the Toeplitz sequence
+  DevBuf<i64> ext;        // internal row -> external row
+  std::vector<i64> perm_h, inv_h;
+  DevBuf<double> origin_d, h_d;
+  DevBuf<double> grid_u, grid_w, grid_t;  // per-MVM grid scratch (guarded by mu / caller)
+
+  DskiView view() const {
+    DskiView v;
+    v.d = d;
+    v.T = T;
+    v.G = G;
+    for (int j = 0; j < 3; ++j) {
+      v.m[j] = m[j];
+      v.nb[j] = nb[j];
+    }
+    v.n = n;
+    v.M = M;
+    v.base = base.p;
+    v.wts = wts.p;
+    v.cell_start = cell_start.p;
+    v.nv2 = nv2;
+    v.ng2 = ng2;
+    return v;
+  }
+
+  const i64* d_ext_of_int() const override { return ext.p; }
+  i64 int_of_ext(i64 r) const override {
+    const i64 g = r / n, i = r % n;
+    return g * n + inv_h[static_cast<size_t>(i)];
+  }
+
+  void scatter(const double* v, double* u, int nrhs, cudaStream_t s) const;
+  void kuu(const double* u, double* w, int nrhs, cudaStream_t s) const;
+  void gather(const double* w, const double* v, double* out, int nrhs, bool noise, cudaStream_t s) const;
+
+  void ensure_scratch(int nrhs) {
+    grid_u.reserve(static_cast<size_t>(M) * nrhs);
+    grid_w.reserve(static_cast<size_t>(M) * nrhs);
+    grid_t.reserve(static_cast<size_t>(M) * nrhs);
+  }
+
+  void mvm(const double* in, double* out, int nrhs, cudaStream_t s) override {
+    ensure_scratch(nrhs);
+    scatter(in, grid_u.p, nrhs, s);
+    kuu(grid_u.p, grid_w.p, nrhs, s);
+    gather(grid_w.p, in, out, nrhs, true, s);
+  }
+  void stage(int st, const double* in, double* out, int nrhs, cudaStream_t s) override {
+    ensure_scratch(nrhs);
+    switch (st) {
+      case 0: scatter(in, out, nrhs, s); break;
+      case 1: kuu(in, out, nrhs, s); break;
+      case 2: gather(in, in, out, nrhs, false, s); break;
+      case 3: mvm(in, out, nrhs, s); break;
+      default: fail(GK_ERR_ARG, "unknown stage");
+    }
+  }
+  void diagonal(double* dd, cudaStream_t s) override;
+  void row(i64 r_ext, double* out, cudaStream_t s) override;
+};
+
+#define GK_DISPATCH_DT(D_, T_, ...)                                   \
+  do {                                                                \
+    if (D_ == 1 && T_ == 6) { constexpr int D = 1, T = 6; __VA_ARGS__; } \
+    else if (D_ == 2 && T_ == 6) { constexpr int D = 2, T = 6; __VA_ARGS__; } \
+    else if (D_ == 3 && T_ == 6) { constexpr int D = 3, T = 6; __VA_ARGS__; } \
+    else if (D_ == 1 && T_ == 4) { constexpr int D = 1, T = 4; __VA_ARGS__; } \
+    else if (D_ == 2 && T_ == 4) { constexpr int D = 2, T = 4; __VA_ARGS__; } \
+    else if (D_ == 3 && T_ == 4) { constexpr int D = 3, T = 4; __VA_ARGS__; } \
+    else fail(GK_ERR_UNSUPPORTED, "D-SKI grid dimension must be 1, 2 or 3");  \
+  } while (0)
+
+static int grid_blocks(i64 items, int threads = 256) {
+  i64 b = (items + threads - 1) / threads;
+  return int(std::max<i64>(1, std::min<i64>(b, 148LL * 16)));
+}
+
+void DskiOp::scatter(const double* v, double* u, int nrhs, cudaStream_t s) const {
+  const DskiView vw = view();
+  const int blocks = grid_blocks(M * nrhs);
+  GK_DISPATCH_DT(d, T, {
+    if (G) k_scatter<D, T, true><<<blocks, 256, 0, s>>>(vw, v, u, nrhs);
+    else k_scatter<D, T, false><<<blocks, 256, 0, s>>>(vw, v, u, nrhs);
+  });
+  launched("dski scatter");
+}
+
+void DskiOp::gather(const double* w, const double* v, double* out, int nrhs, bool noise,
+                    cudaStream_t s) const {
+  const DskiView vw = view();
+  const int blocks = grid_blocks(n * nrhs);
+  GK_DISPATCH_DT(d, T, {
+    if (G) k_gather<D, T, true><<<blocks, 256, 0, s>>>(vw, w, v, out, nrhs, noise ? 1 : 0);
+    else k_gather<D, T, false><<<blocks, 256, 0, s>>>(vw, w, v, out, nrhs, noise ? 1 : 0);
+  });
+  launched("dski gather");
+}
+
+void DskiOp::kuu(const double* u, double* w, int nrhs, cudaStream_t s) const {
+  // Modes from the last axis to the first: u -> ... -> w, intermediates
+  // alternating between w and the scratch grid_t so the last mode lands in w
+  // (caller has reserved grid_t for nrhs columns; u must not alias w/grid_t).
+  const double* src = u;
+  for (int j = d - 1; j >= 0; --j) {
+    i64 P = 1, Q = nrhs;
+    for (int i = 0; i < j; ++i) P *= m[i];
+    for (int i = j + 1; i < d; ++i) Q *= m[i];
+    double* dst = (j % 2 == 0) ? w : grid_t.p;
+    toeplitz_mode(tvec.p + toff_h[static_cast<size_t>(j)], m[j], band[static_cast<size_t>(j)], P, Q, src, dst, s);
+    src = dst;
+  }
+}
+
+void DskiOp::diagonal(double* dd, cudaStream_t s) {
+  const DskiView vw = view();
+  GK_DISPATCH_DT(d, T, { k_diagonal<D, T><<<grid_blocks(n), 256, 0, s>>>(vw, tvec.p, toff.p, dd); });
+  launched("dski diagonal");
+}
+
+void DskiOp::row(i64 r_ext, double* out, cudaStream_t s) {
+  if (r_ext < 0 || r_ext >= N) fail(GK_ERR_RANGE, "D-SKI row index out of range");
+  const int g = int(r_ext / n);
+  const int si = int(inv_h[static_cast<size_t>(r_ext % n)]);
+  const DskiView vw = view();
+  const int shm = int(sizeof(double)) * (m[0] + (d > 1 ? m[1] : 0) + (d > 2 ? m[2] : 0));
+  GK_DISPATCH_DT(d, T, { k_row<D, T><<<grid_blocks(N), 256, shm, s>>>(vw, tvec.p, toff.p, si, g, out); });
+  launched("dski row");
+}
+
+// ---------------------------------------------------------------- creation
+std::unique_ptr<Op> make_dski(const gk_kernel& k, const gk_grid& g, const double* X, i64 n,
+                              double nv, double ng, int order, int with_grad, int device) {
+  if (k.family != 0)
+    fail(GK_ERR_UNSUPPORTED,
+         "D-SKI on B200 implements the separable squared-exponential profile; the spline "
+         "profile is not supported by this build");
+  if (!(k.lengthscale > 0.0)) fail(GK_ERR_ARG, "lengthscale must be > 0");
+  if (!(k.outputscale > 0.0)) fail(GK_ERR_ARG, "outputscale must be > 0");
+  if (g.d < 1 || g.d > 3) fail(GK_ERR_UNSUPPORTED, "D-SKI grid dimension must be 1, 2 or 3");
+  if (n < 1) fail(GK_ERR_ARG, "D-SKI needs at least one point");
+  if (order != 0 && order != 1) fail(GK_ERR_ARG, "interpolation order must be 0 (quintic) or 1 (cubic)");
+  DeviceGuard dg(device);
+  auto op = std::make_unique<DskiOp>();
+  op->kind = KIND_DSKI;
+  op->device = device;
+  op->d = g.d;
+  op->T = order == 0 ? 6 : 4;
+  op->G = with_grad ? g.d : 0;
+  op->n = n;
+  op->N = n * (op->G + 1);
+  op->n_value = n;
+  op->nv2 = nv * nv;
+  op->ng2 = ng * ng;
+  op->grid = g;
+  op->kernel = k;
+  const int d = g.d, T = op->T;
+  op->M = 1;
+  for (int j = 0; j < d; ++j) {
+    if (g.dims[j] < T) fail(GK_ERR_ARG, "grid needs at least as many nodes as stencil taps per dimension");
+    op->m[j] = g.dims[j];
+    op->nb[j] = g.dims[j] - T + 1;
+    op->M *= g.dims[j];
+  }
+  // per-point stencils in original order (interpolation.cpp:66-97)
+  const int STRIDE = d * 2 * T;
+  std::vector<int> base(static_cast<size_t>(n) * d);
+  std::vector<double> wts(static_cast<size_t>(n) * STRIDE);
+  for (i64 i = 0; i < n; ++i)
+    for (int j = 0; j < d; ++j)
+      axis_weights(X[j * n + i], g.origin[j], g.spacing[j], g.dims[j], T, i, j,
+                   &base[static_cast<size_t>(i) * d + j], &wts[static_cast<size_t>(i) * STRIDE + j * 2 * T],
+                   &wts[static_cast<size_t>(i) * STRIDE + j * 2 * T + T]);
+  // sort by base cell (counting sort: stable, deterministic)
+  i64 ncells = 1;
+  for (int j = 0; j < d; ++j) ncells *= op->nb[j];
+  std::vector<i64> cell(static_cast<size_t>(n));
+  std::vector<int> cstart(static_cast<size_t>(ncells) + 1, 0);
+  for (i64 i = 0; i < n; ++i) {
+    i64 c = 0;
+    for (int j = 0; j < d; ++j) c = c * op->nb[j] + base[static_cast<size_t>(i) * d + j];
+    cell[static_cast<size_t>(i)] = c;
+    cstart[static_cast<size_t>(c) + 1]++;
+  }
+  for (i64 c = 0; c < ncells; ++c) cstart[static_cast<size_t>(c) + 1] += cstart[static_cast<size_t>(c)];
+  op->perm_h.assign(static_cast<size_t>(n), 0);
+  op->inv_h.assign(static_cast<size_t>(n), 0);
+  {
+    std::vector<int> fill(cstart.begin(), cstart.end() - 1);
+    for (i64 i = 0; i < n; ++i) {
+      const int pos = fill[static_cast<size_t>(cell[static_cast<size_t>(i)])]++;
+      op->perm_h[static_cast<size_t>(pos)] = i;
+      op->inv_h[static_cast<size_t>(i)] = pos;
+    }
+  }
+  std::vector<int4> base_s(static_cast<size_t>(n));
+  std::vector<double> wts_s(static_cast<size_t>(n) * STRIDE);
+  for (i64 s = 0; s < n; ++s) {
+    const i64 i = op->perm_h[static_cast<size_t>(s)];
+    int4 b4 = make_int4(0, 0, 0, 0);
+    b4.x = base[static_cast<size_t>(i) * d + 0];
+    if (d > 1) b4.y = base[static_cast<size_t>(i) * d + 1];
+    if (d > 2) b4.z = base[static_cast<size_t>(i) * d + 2];
+    base_s[static_cast<size_t>(s)] = b4;
+    std::memcpy(&wts_s[static_cast<size_t>(s) * STRIDE], &wts[static_cast<size_t>(i) * STRIDE], sizeof(double) * STRIDE);
+  }
+  // Toeplitz sequences t_j[k] = exp(-(k h_j)²/(2ℓ²)), s² folded into axis 0
+  // (SE profile, kernels.cpp:22-27 / dski.cpp:30-34).
+  std::vector<double> tv;
+  op->toff_h.resize(static_cast<size_t>(d));
+  op->band.resize(static_cast<size_t>(d));
+  const double ell2 = k.lengthscale * k.lengthscale;
+  for (int j = 0; j < d; ++j) {
+    op->toff_h[static_cast<size_t>(j)] = int(tv.size());
+    int band = g.dims[j];
+    for (int kk = 0; kk < g.dims[j]; ++kk) {
+      const double o = kk * g.spacing[j];
+      double val = std::exp(-0.5 * o * o / ell2);
+      if (j == 0) val *= k.outputscale * k.outputscale;
+      tv.push_back(val);
+    }
+    // numerical band: entries below 1e-30 of the peak contribute far below
+    // fp64 roundoff of the product and are skipped tile-wise.
+    const double peak = tv[static_cast<size_t>(op->toff_h[static_cast<size_t>(j)])];
+    for (int kk = 1; kk < g.dims[j]; ++kk)
+      if (tv[static_cast<size_t>(op->toff_h[static_cast<size_t>(j)] + kk)] < 1e-30 * peak) {
+        band = kk;
+        break;
+      }
+    op->band[static_cast<size_t>(j)] = band;
+  }
+  std::vector<i64> ext(static_cast<size_t>(op->N));
+  for (int gg = 0; gg <= op->G; ++gg)
+    for (i64 s = 0; s < n; ++s) ext[static_cast<size_t>(gg * n + s)] = gg * n + op->perm_h[static_cast<size_t>(s)];
+  op->init_stream();
+  cudaStream_t st = op->stream;
+  op->base.upload(base_s.data(), base_s.size(), st);
+  op->wts.upload(wts_s.data(), wts_s.size(), st);
+  op->cell_start.upload(cstart.data(), cstart.size(), st);
+  op->tvec.upload(tv.data(), tv.size(), st);
+  op->toff.upload(op->toff_h.data(), op->toff_h.size(), st);
+  op->ext.upload(ext.data(), ext.size(), st);
+  double o3[3] = {0, 0, 0}, h3[3] = {1, 1, 1};
+  for (int j = 0; j < d; ++j) {
+    o3[j] = g.origin[j];
+    h3[j] = g.spacing[j];
+  }
+  op->origin_d.upload(o3, 3, st);
+  op->h_d.upload(h3, 3, st);
+  GK_CUDA(cudaStreamSynchronize(st));
+  return op;
+}
+
+// ---------------------------------------------------------------- D-SKI extras
+int64_t dski_grid_size(const Op& o) {
+  if (o.kind != KIND_DSKI) fail(GK_ERR_ARG, "operator is not a D-SKI operator");
+  return static_cast<const DskiOp&>(o).M;
+}
+gk_grid dski_grid(const Op& o) {
+  if (o.kind != KIND_DSKI) fail(GK_ERR_ARG, "operator is not a D-SKI operator");
+  return static_cast<const DskiOp&>(o).grid;
+}
+
+// Scatter with grid output (internal V -> grid U), grid K_UU and gather w/o noise.
+void dski_transpose_apply(Op& o, const double* Vi, double* U, int nrhs, cudaStream_t s) {
+  auto& op = static_cast<DskiOp&>(o);
+  op.scatter(Vi, U, nrhs, s);
+}
+void dski_apply(Op& o, const double* U, double* Oi, int nrhs, cudaStream_t s) {
+  auto& op = static_cast<DskiOp&>(o);
+  op.gather(U, U, Oi, nrhs, false, s);
+}
+void dski_grid_mvm(Op& o, const double* U, double* W, int nrhs, cudaStream_t s) {
+  auto& op = static_cast<DskiOp&>(o);
+  op.ensure_scratch(nrhs);
+  op.kuu(U, W, nrhs, s);
+}
+
+// predict_mean_grad (gp.cpp:471-496) given alpha (internal layout, 1 column)
+void dski_predict(Op& o, const double* alpha_i, double mean, const double* dXt, i64 nT, double* dvals,
+                  double* dgrads, int* dbad, cudaStream_t s) {
+  auto& op = static_cast<DskiOp&>(o);
+  op.ensure_scratch(1);
+  DevBuf<double> g(static_cast<size_t>(op.M)), tmp(static_cast<size_t>(op.M));
+  op.scatter(alpha_i, tmp.p, 1, s);
+  op.kuu(tmp.p, g.p, 1, s);
+  const DskiView vw = op.view();
+  GK_DISPATCH_DT(op.d, op.T, {
+    k_predict<D, T><<<grid_blocks(nT), 256, 0, s>>>(vw, dXt, nT, op.origin_d.p, op.h_d.p, g.p, mean,
+                                                     dvals, dgrads, dbad);
+  });
+  launched("dski predict");
+  GK_CUDA(cudaStreamSynchronize(s));
+}
+
+// cross_covariance for T test points (gp.cpp:412-417): Q = B K_UU w_t.
+void dski_cross_cov(Op& o, const double* dXt, i64 nT, double* Qi, int* dbad, cudaStream_t s) {
+  auto& op = static_cast<DskiOp&>(o);
+  op.ensure_scratch(int(nT));
+  DevBuf<double> U(static_cast<size_t>(op.M) * nT), W(static_cast<size_t>(op.M) * nT);
+  GK_CUDA(cudaMemsetAsync(U.p, 0, sizeof(double) * op.M * nT, s));
+  const DskiView vw = op.view();
+  GK_DISPATCH_DT(op.d, op.T, {
+    k_test_stencils<D, T><<<grid_blocks(nT), 256, 0, s>>>(vw, dXt, nT, op.origin_d.p, op.h_d.p, U.p, dbad);
+  });
+  launched("dski test stencils");
+  op.kuu(U.p, W.p, int(nT), s);
+  op.gather(W.p, W.p, Qi, int(nT), false, s);
+  GK_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace gk

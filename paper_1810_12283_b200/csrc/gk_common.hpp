@@ -1,0 +1,165 @@
+// gk_common.hpp — shared infrastructure of libgk_b200: error mapping,
+// device buffers, launch accounting, the device-operator base class.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "gk_capi.h"
+
+namespace gk {
+
+using i64 = std::int64_t;
+
+struct Error : std::runtime_error {
+  gk_status code;
+  i64 point;
+  Error(gk_status c, const std::string& m, i64 p = -1) : std::runtime_error(m), code(c), point(p) {}
+};
+
+[[noreturn]] inline void fail(gk_status c, const std::string& msg, i64 point = -1) {
+  throw Error(c, msg, point);
+}
+
+void cuda_check(cudaError_t e, const char* what);
+#define GK_CUDA(x) ::gk::cuda_check((x), #x)
+
+// Every kernel launch goes through this so the library can report how many of
+// its own kernels ran (bench.py's gpu_launches, smoke()).
+extern std::atomic<i64> g_launches;
+inline void launched(const char* what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cuda_check(cudaGetLastError(), what);
+}
+
+// Owning device buffer.
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t count) { alloc(count); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      n = o.n;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t count) {
+    release();
+    if (count) GK_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  // grow-only reallocation for scratch
+  void reserve(size_t count) {
+    if (count > n) alloc(count);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void upload(const T* h, size_t count, cudaStream_t s = nullptr) {
+    reserve(count);
+    if (count) GK_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  T* get() const { return p; }
+};
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    GK_CUDA(cudaGetDevice(&prev));
+    if (prev != dev) GK_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+// Pinned host staging buffer.
+struct HostBuf {
+  double* p = nullptr;
+  size_t n = 0;
+  void reserve(size_t count) {
+    if (count <= n) return;
+    if (p) cudaFreeHost(p);
+    GK_CUDA(cudaMallocHost(&p, count * sizeof(double)));
+    n = count;
+  }
+  ~HostBuf() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
+// ---------------------------------------------------------------- host math
+std::uint64_t mix_seed(std::uint64_t seed, std::uint64_t stream);
+void rademacher(i64 n, std::uint64_t seed, std::uint64_t stream, double* out);
+void gaussian(i64 n, std::uint64_t seed, std::uint64_t stream, double* out);
+// Tridiagonal eigendecomposition, ascending; Z is n×n col-major (may be null
+// for values only).
+void tridiag_eig(int n, const double* alpha, const double* beta, double* evals, double* Z);
+// Dense small Cholesky (upper R, R^T R = A, col-major k×k). Throws on failure.
+void cholesky_upper(int k, const double* A, double* R);
+
+// ---------------------------------------------------------------- operators
+enum OpKind { KIND_EXACT = 0, KIND_DSKI = 1, KIND_DSKIP = 2, KIND_DENSE = 3 };
+
+// Device operator behind gk_op. All compute entry points work on the
+// INTERNAL layout: rows in the operator's internal order (D-SKI sorts points
+// by stencil cell; others keep the external order), right-hand sides
+// innermost ("RHS-minor": element (r, b) at r*nrhs + b).
+struct Op {
+  virtual ~Op();
+  int kind = 0;
+  int device = 0;
+  i64 N = 0;            // logical size
+  i64 n_value = 0;      // rows [0, n_value) carry sigma_1^2, the rest sigma_2^2
+  double nv2 = 0.0, ng2 = 0.0;
+  std::mutex mu;        // serialises host-API calls that use the scratch below
+  cudaStream_t stream = nullptr;  // own stream for host-API calls
+  DevBuf<double> scratch_a, scratch_b, scratch_c;
+  HostBuf pinned;
+
+  virtual void mvm(const double* in, double* out, int nrhs, cudaStream_t s) = 0;
+  // diagonal including noise, internal order
+  virtual void diagonal(double* d, cudaStream_t s) = 0;
+  // row r (EXTERNAL index) including noise, written in internal order
+  virtual void row(i64 r_ext, double* out, cudaStream_t s) = 0;
+  // internal row index -> external row index (device array or null = identity)
+  virtual const i64* d_ext_of_int() const { return nullptr; }
+  virtual i64 int_of_ext(i64 r) const { return r; }
+  virtual void stage(int st, const double* in, double* out, int nrhs, cudaStream_t s);
+
+  void to_internal(const double* V, i64 ldv, double* I, int nrhs, cudaStream_t s) const;
+  void from_internal(const double* I, double* V, i64 ldv, int nrhs, cudaStream_t s) const;
+  void init_stream();
+};
+
+// Blocked host-API MVM helper: copies host blocks in/out through pinned
+// memory in chunks of at most kMaxRhs columns.
+constexpr int kMaxRhs = 64;
+
+// ---------------------------------------------------------------- reductions
+// Deterministic column reductions over RHS-minor blocks (rows × nrhs).
+constexpr int kRedBlocks = 296;  // 2 × 148 SMs
+constexpr int kRedThreads = 256;
+
+}  // namespace gk
+
+struct gk_op {
+  std::unique_ptr<gk::Op> impl;
+};

@@ -1,0 +1,1056 @@
+// solvers.cu — device-resident batched solvers (reference linalg.cpp).
+//
+//  * pcg_internal: the reference's single-RHS PCG (linalg.cpp:85-131) run
+//    for nrhs independent columns at once: per-column alpha/beta, per-column
+//    stopping (converged / pAp <= 0 stall / max_iterations), frozen columns
+//    after they stop. One iteration is captured into a CUDA graph; the host
+//    only polls the number of active columns between graph launches.
+//  * pivchol_run: pivoted Cholesky (linalg.cpp:133-174) with the row fetched
+//    from the operator on device; argmax tie-break = lowest external index
+//    (Eigen maxCoeff semantics).
+//  * precond_build / Precond::apply: Q1 of [D^{-1/2}F; I] by CholeskyQR2
+//    (two Gram + k×k Cholesky passes), applied as two rank-k contractions.
+//  * lanczos_batch: Lanczos with two-pass full reorthogonalisation and
+//    deflating restarts (linalg.cpp:17-81) for P probes in lockstep.
+// All reductions are deterministic (fixed partition, fixed summation order).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+#include "gk_kernels.cuh"
+#include "solvers.hpp"
+
+namespace gk {
+
+namespace {
+
+constexpr int RB = kRedBlocks;
+constexpr int RT = kRedThreads;
+
+__device__ __forceinline__ void row_range(i64 rows, i64& r0, i64& r1) {
+  const i64 per = (rows + gridDim.x - 1) / gridDim.x;
+  r0 = (i64)blockIdx.x * per;
+  r1 = min(rows, r0 + per);
+}
+
+// Reduce per-thread values of layout (slot, b) into partial[blockIdx][b].
+__device__ __forceinline__ void block_col_store(double acc, int nrhs, double* partial, double* sm) {
+  const int tid = threadIdx.x;
+  const int slots = blockDim.x / nrhs;
+  __syncthreads();
+  sm[tid] = acc;
+  __syncthreads();
+  if (tid < nrhs) {
+    double s = 0.0;
+    for (int k = 0; k < slots; ++k) s += sm[k * nrhs + tid];
+    partial[(i64)blockIdx.x * nrhs + tid] = s;
+  }
+}
+
+__device__ __forceinline__ double sum_partials(const double* partial, int nblocks, int stride, int idx) {
+  double s = 0.0;
+  for (int k = 0; k < nblocks; ++k) s += partial[(i64)k * stride + idx];
+  return s;
+}
+
+__global__ void k_dot_partial(const double* __restrict__ x, const double* __restrict__ y, i64 rows, int nrhs,
+                              double* __restrict__ partial) {
+  __shared__ double sm[RT];
+  const int slots = blockDim.x / nrhs;
+  const int b = threadIdx.x % nrhs, slot = threadIdx.x / nrhs;
+  double acc = 0.0;
+  if (slot < slots) {
+    i64 r0, r1;
+    row_range(rows, r0, r1);
+    for (i64 r = r0 + slot; r < r1; r += slots) acc += x[r * nrhs + b] * y[r * nrhs + b];
+  }
+  block_col_store(acc, nrhs, partial, sm);
+}
+
+// ---------------------------------------------------------------- PCG
+struct CgDev {
+  double* bnorm;
+  double* rz;
+  double* alpha;
+  double* beta;
+  double* hist;  // [(maxit+1)][nrhs]
+  int* active;
+  int* upd;
+  int* its;
+  int* conv;
+  int* nactive;  // single int
+  int maxit;
+  double tol;
+  int nrhs;
+};
+
+// init: partial0 = ||b||², partial1 = r·z, partial2 = r·r (r = b)
+__global__ void k_cg_init(CgDev st, const double* __restrict__ p_bb, const double* __restrict__ p_rz,
+                          const double* __restrict__ p_rr) {
+  const int b = threadIdx.x;
+  __shared__ int cnt;
+  if (b == 0) cnt = 0;
+  __syncthreads();
+  if (b < st.nrhs) {
+    const double bn = sqrt(sum_partials(p_bb, RB, st.nrhs, b));
+    st.bnorm[b] = bn;
+    st.its[b] = 0;
+    st.upd[b] = 0;
+    if (bn == 0.0) {  // linalg.cpp:93-96: zero rhs -> converged, no history
+      st.conv[b] = 1;
+      st.active[b] = 0;
+      st.rz[b] = 0.0;
+    } else {
+      st.rz[b] = sum_partials(p_rz, RB, st.nrhs, b);
+      const double relres = sqrt(sum_partials(p_rr, RB, st.nrhs, b)) / bn;
+      st.hist[b] = relres;
+      const bool done = relres <= st.tol;  // :104-109
+      st.conv[b] = done ? 1 : 0;
+      st.active[b] = done ? 0 : 1;
+      if (!done) atomicAdd(&cnt, 1);
+    }
+  }
+  __syncthreads();
+  if (b == 0) *st.nactive = cnt;
+}
+
+__global__ void k_cg_fin_pAp(CgDev st, const double* __restrict__ partial) {
+  const int b = threadIdx.x;
+  if (b >= st.nrhs) return;
+  st.upd[b] = 0;
+  if (!st.active[b]) return;
+  if (st.its[b] >= st.maxit) {  // loop bound reached, unconverged
+    st.active[b] = 0;
+    return;
+  }
+  const double pAp = sum_partials(partial, RB, st.nrhs, b);
+  if (pAp <= 0.0) {  // linalg.cpp:114: loss of definiteness -> stalled
+    st.active[b] = 0;
+    return;
+  }
+  st.alpha[b] = st.rz[b] / pAp;
+  st.upd[b] = 1;
+  st.its[b] += 1;
+}
+
+// x += a p; r -= a Ap for updating columns; partial ||r||²
+__global__ void k_cg_axpy(CgDev st, double* __restrict__ X, double* __restrict__ R, const double* __restrict__ P,
+                          const double* __restrict__ AP, i64 rows, double* __restrict__ partial) {
+  __shared__ double sm[RT];
+  const int nrhs = st.nrhs;
+  const int slots = blockDim.x / nrhs;
+  const int b = threadIdx.x % nrhs, slot = threadIdx.x / nrhs;
+  double acc = 0.0;
+  if (slot < slots && st.upd[b]) {
+    const double a = st.alpha[b];
+    i64 r0, r1;
+    row_range(rows, r0, r1);
+    for (i64 r = r0 + slot; r < r1; r += slots) {
+      const i64 i = r * nrhs + b;
+      X[i] += a * P[i];
+      const double rn = R[i] - a * AP[i];
+      R[i] = rn;
+      acc += rn * rn;
+    }
+  }
+  block_col_store(acc, nrhs, partial, sm);
+}
+
+__global__ void k_cg_fin_rr(CgDev st, const double* __restrict__ partial) {
+  const int b = threadIdx.x;
+  __shared__ int cnt;
+  if (b == 0) cnt = 0;
+  __syncthreads();
+  if (b < st.nrhs) {
+    if (st.upd[b]) {
+      const double relres = sqrt(sum_partials(partial, RB, st.nrhs, b)) / st.bnorm[b];
+      st.hist[(i64)st.its[b] * st.nrhs + b] = relres;
+      if (relres <= st.tol) {  // :121-125
+        st.conv[b] = 1;
+        st.active[b] = 0;
+      }
+    }
+    if (st.active[b]) atomicAdd(&cnt, 1);
+  }
+  __syncthreads();
+  if (b == 0) *st.nactive = cnt;
+}
+
+__global__ void k_cg_fin_rz(CgDev st, const double* __restrict__ partial) {
+  const int b = threadIdx.x;
+  if (b >= st.nrhs || !st.active[b]) return;
+  const double rzn = sum_partials(partial, RB, st.nrhs, b);
+  st.beta[b] = rzn / st.rz[b];
+  st.rz[b] = rzn;
+}
+
+__global__ void k_cg_pupdate(CgDev st, double* __restrict__ P, const double* __restrict__ Z, i64 rows) {
+  const int nrhs = st.nrhs;
+  const i64 items = rows * nrhs;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < items; i += (i64)gridDim.x * blockDim.x) {
+    const int b = int(i % nrhs);
+    if (st.active[b]) P[i] = Z[i] + st.beta[b] * P[i];
+  }
+}
+
+__global__ void k_copy(const double* __restrict__ a, double* __restrict__ b, i64 n) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) b[i] = a[i];
+}
+__global__ void k_fill(double* __restrict__ a, double v, i64 n) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) a[i] = v;
+}
+
+// ---------------------------------------------------------------- preconditioner
+// partial T[j][b] = Σ_rows q1[r][j] (dinv[r] r[r][b]); also partial Σ c² per b
+// (for quadratic()). Rows are staged 16 at a time in shared memory; outputs
+// o = j*nrhs + b are owned by one thread each and accumulate in smem.
+constexpr int PC_RT = 16;
+__global__ void k_pc_proj(const double* __restrict__ Rv, const double* __restrict__ dinv,
+                          const double* __restrict__ q1, i64 N, int k, int nrhs, double* __restrict__ partial,
+                          double* __restrict__ partial_cc) {
+  extern __shared__ double sh[];
+  double* qs = sh;                     // [PC_RT][k]
+  double* cs = qs + PC_RT * k;         // [PC_RT][nrhs]
+  double* acc = cs + PC_RT * nrhs;     // [k*nrhs]
+  const int tid = threadIdx.x;
+  const int nout = k * nrhs;
+  for (int o = tid; o < nout; o += blockDim.x) acc[o] = 0.0;
+  double cc = 0.0;  // Σ c² for column tid (tid < nrhs)
+  i64 r0, r1;
+  row_range(N, r0, r1);
+  for (i64 rt = r0; rt < r1; rt += PC_RT) {
+    const int nr = int((r1 - rt) < PC_RT ? (r1 - rt) : PC_RT);
+    __syncthreads();
+    for (int e = tid; e < nr * k; e += blockDim.x) qs[e] = q1[rt * k + e];
+    for (int e = tid; e < nr * nrhs; e += blockDim.x) {
+      const int rr = e / nrhs;
+      cs[e] = dinv[rt + rr] * Rv[(rt + rr) * nrhs + (e % nrhs)];
+    }
+    __syncthreads();
+    if (tid < nrhs)
+      for (int rr = 0; rr < nr; ++rr) cc += cs[rr * nrhs + tid] * cs[rr * nrhs + tid];
+    for (int o = tid; o < nout; o += blockDim.x) {
+      const int j = o / nrhs, b = o % nrhs;
+      double a = acc[o];
+      for (int rr = 0; rr < nr; ++rr) a += qs[rr * k + j] * cs[rr * nrhs + b];
+      acc[o] = a;
+    }
+  }
+  __syncthreads();
+  for (int o = tid; o < nout; o += blockDim.x) partial[(i64)blockIdx.x * nout + o] = acc[o];
+  if (partial_cc && tid < nrhs) partial_cc[(i64)blockIdx.x * nrhs + tid] = cc;
+}
+
+__global__ void k_pc_fin(const double* __restrict__ partial, int nout, double* __restrict__ T) {
+  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < nout; o += gridDim.x * blockDim.x)
+    T[o] = sum_partials(partial, RB, nout, o);
+}
+
+// z = dinv (dinv r - Q1 T); partial Σ r·z
+__global__ void k_pc_apply(const double* __restrict__ Rv, const double* __restrict__ dinv,
+                           const double* __restrict__ q1, const double* __restrict__ T, i64 N, int k, int nrhs,
+                           double* __restrict__ Z, double* __restrict__ partial_rz) {
+  extern __shared__ double sh[];
+  double* Ts = sh;  // [k][nrhs]
+  double* sm = Ts + k * nrhs;
+  for (int o = threadIdx.x; o < k * nrhs; o += blockDim.x) Ts[o] = T[o];
+  __syncthreads();
+  const int slots = blockDim.x / nrhs;
+  const int b = threadIdx.x % nrhs, slot = threadIdx.x / nrhs;
+  double acc = 0.0;
+  if (slot < slots) {
+    i64 r0, r1;
+    row_range(N, r0, r1);
+    for (i64 r = r0 + slot; r < r1; r += slots) {
+      const double di = dinv[r];
+      const double rv = Rv[r * nrhs + b];
+      double s = 0.0;
+      const double* qr = q1 + r * k;
+      for (int j = 0; j < k; ++j) s += qr[j] * Ts[j * nrhs + b];
+      const double z = di * (di * rv - s);
+      Z[r * nrhs + b] = z;
+      acc += rv * z;
+    }
+  }
+  if (partial_rz) block_col_store(acc, nrhs, partial_rz, sm);
+}
+
+// Row-wise small GEMM: Y[r][:] = X[r][:] · Mx (k×k col-major), X,Y [N][k] row-major.
+__global__ void k_rows_times_small(const double* __restrict__ X, const double* __restrict__ Mx, i64 N, int k,
+                                   double* __restrict__ Y) {
+  const i64 items = N * k;
+  for (i64 it = blockIdx.x * (i64)blockDim.x + threadIdx.x; it < items; it += (i64)gridDim.x * blockDim.x) {
+    const int j = int(it % k);
+    const i64 r = it / k;
+    const double* xr = X + r * k;
+    const double* mc = Mx + (i64)j * k;
+    double s = 0.0;
+    for (int i = 0; i < k; ++i) s += xr[i] * mc[i];
+    Y[it] = s;
+  }
+}
+
+// Gram partials: G[j][l] = Σ_rows X[r][j] X[r][l] (X [N][k] row-major), j<=l.
+__global__ void k_gram_partial(const double* __restrict__ X, i64 N, int k, double* __restrict__ partial) {
+  extern __shared__ double sh[];
+  double* xs = sh;          // [PC_RT][k]
+  double* acc = xs + PC_RT * k;  // [k*k]
+  const int tid = threadIdx.x;
+  for (int o = tid; o < k * k; o += blockDim.x) acc[o] = 0.0;
+  i64 r0, r1;
+  row_range(N, r0, r1);
+  for (i64 rt = r0; rt < r1; rt += PC_RT) {
+    const int nr = int((r1 - rt) < PC_RT ? (r1 - rt) : PC_RT);
+    __syncthreads();
+    for (int e = tid; e < nr * k; e += blockDim.x) xs[e] = X[rt * k + e];
+    __syncthreads();
+    for (int o = tid; o < k * k; o += blockDim.x) {
+      const int j = o / k, l = o % k;
+      if (j > l) continue;
+      double a = acc[o];
+      for (int rr = 0; rr < nr; ++rr) a += xs[rr * k + j] * xs[rr * k + l];
+      acc[o] = a;
+    }
+  }
+  __syncthreads();
+  for (int o = tid; o < k * k; o += blockDim.x) partial[(i64)blockIdx.x * k * k + o] = acc[o];
+}
+
+// G = D^{-1/2} F: F is [k][N] col-major (internal rows) -> G [N][k] row-major
+__global__ void k_scale_transpose(const double* __restrict__ F, const double* __restrict__ noise, i64 N, int k,
+                                  double* __restrict__ G, double* __restrict__ dinv) {
+  const i64 items = N * k;
+  for (i64 it = blockIdx.x * (i64)blockDim.x + threadIdx.x; it < items; it += (i64)gridDim.x * blockDim.x) {
+    const int j = int(it % k);
+    const i64 r = it / k;
+    const double di = 1.0 / sqrt(noise[r]);
+    G[it] = di * F[(i64)j * N + r];
+    if (j == 0) dinv[r] = di;
+  }
+}
+
+// ---------------------------------------------------------------- pivoted Cholesky
+struct ArgMax {
+  double v;
+  i64 ext;
+  i64 in;
+};
+__device__ __forceinline__ bool better(double v, i64 e, double bv, i64 be) {
+  return v > bv || (v == bv && e < be);
+}
+
+__global__ void k_pv_init(const double* __restrict__ diag, const double* __restrict__ noise, int kernel_part,
+                          i64 N, double* __restrict__ d) {
+  for (i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x; r < N; r += (i64)gridDim.x * blockDim.x)
+    d[r] = kernel_part ? fmax(diag[r] - noise[r], 0.0) : diag[r];
+}
+
+// partial stats of d: min, sum, max, argmax(lowest ext)
+__global__ void k_pv_stats(const double* __restrict__ d, const i64* __restrict__ ext, i64 N,
+                           double* __restrict__ pmin, double* __restrict__ psum, double* __restrict__ pmax,
+                           i64* __restrict__ pext, i64* __restrict__ pint) {
+  __shared__ double smin[RT], ssum[RT], smax[RT];
+  __shared__ i64 sext[RT], sint[RT];
+  i64 r0, r1;
+  row_range(N, r0, r1);
+  double mn = INFINITY, sm = 0.0, mx = -INFINITY;
+  i64 me = LLONG_MAX, mi = -1;
+  for (i64 r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+    const double v = d[r];
+    const i64 e = ext ? ext[r] : r;
+    mn = fmin(mn, v);
+    sm += v;
+    if (better(v, e, mx, me)) {
+      mx = v;
+      me = e;
+      mi = r;
+    }
+  }
+  const int t = threadIdx.x;
+  smin[t] = mn;
+  ssum[t] = sm;
+  smax[t] = mx;
+  sext[t] = me;
+  sint[t] = mi;
+  __syncthreads();
+  if (t == 0) {
+    double a = INFINITY, s = 0.0, b = -INFINITY;
+    i64 be = LLONG_MAX, bi = -1;
+    for (int k = 0; k < blockDim.x; ++k) {
+      a = fmin(a, smin[k]);
+      s += ssum[k];
+      if (better(smax[k], sext[k], b, be)) {
+        b = smax[k];
+        be = sext[k];
+        bi = sint[k];
+      }
+    }
+    pmin[blockIdx.x] = a;
+    psum[blockIdx.x] = s;
+    pmax[blockIdx.x] = b;
+    pext[blockIdx.x] = be;
+    pint[blockIdx.x] = bi;
+  }
+}
+
+// out[0]=min, out[1]=sum, out[2]=max, out[3]=ext (as double bits), out[4]=int
+__global__ void k_pv_stats_fin(const double* pmin, const double* psum, const double* pmax, const i64* pext,
+                               const i64* pint, int nb, double* out) {
+  if (threadIdx.x != 0) return;
+  double a = INFINITY, s = 0.0, b = -INFINITY;
+  i64 be = LLONG_MAX, bi = -1;
+  for (int k = 0; k < nb; ++k) {
+    a = fmin(a, pmin[k]);
+    s += psum[k];
+    if (better(pmax[k], pext[k], b, be)) {
+      b = pmax[k];
+      be = pext[k];
+      bi = pint[k];
+    }
+  }
+  out[0] = a;
+  out[1] = s;
+  out[2] = b;
+  reinterpret_cast<i64*>(out)[3] = be;
+  reinterpret_cast<i64*>(out)[4] = bi;
+}
+
+// col = (row - noise_sub e_piv - L[:, :k] L[piv, :k]^T) / sqrt(dmax); L[:,k] = col;
+// d -= col²  (then caller checks min, clamps and zeroes d[piv])
+__global__ void k_pv_update(double* __restrict__ col, double* __restrict__ L, int k, i64 N, i64 piv,
+                            double noise_sub, double sq, double* __restrict__ d) {
+  extern __shared__ double lp[];
+  for (int j = threadIdx.x; j < k; j += blockDim.x) lp[j] = L[(i64)j * N + piv];
+  __syncthreads();
+  for (i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x; r < N; r += (i64)gridDim.x * blockDim.x) {
+    double c = col[r];
+    if (r == piv) c -= noise_sub;
+    if (k > 0) {
+      double s = 0.0;
+      for (int j = 0; j < k; ++j) s += L[(i64)j * N + r] * lp[j];
+      c -= s;
+    }
+    c /= sq;
+    L[(i64)k * N + r] = c;
+    d[r] -= c * c;
+  }
+}
+
+__global__ void k_pv_clamp(double* __restrict__ d, i64 N, i64 piv) {
+  for (i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x; r < N; r += (i64)gridDim.x * blockDim.x)
+    d[r] = (r == piv) ? 0.0 : fmax(d[r], 0.0);
+}
+
+__global__ void k_perm_cols_out(const double* __restrict__ L, const i64* __restrict__ ext, i64 N, int k,
+                                double* __restrict__ out) {
+  const i64 items = N * k;
+  for (i64 it = blockIdx.x * (i64)blockDim.x + threadIdx.x; it < items; it += (i64)gridDim.x * blockDim.x) {
+    const int j = int(it / N);
+    const i64 r = it % N;
+    out[(i64)j * N + (ext ? ext[r] : r)] = L[it];
+  }
+}
+
+// ---------------------------------------------------------------- Lanczos
+// W -= bprev[p] * prev; partial alpha = q·W
+__global__ void k_lz_alpha(double* __restrict__ W, const double* __restrict__ prev, const double* __restrict__ bprev,
+                           const double* __restrict__ q, i64 N, int P, double* __restrict__ partial) {
+  __shared__ double sm[RT];
+  const int slots = blockDim.x / P;
+  const int p = threadIdx.x % P, slot = threadIdx.x / P;
+  double acc = 0.0;
+  if (slot < slots) {
+    const double bp = bprev[p];
+    i64 r0, r1;
+    row_range(N, r0, r1);
+    for (i64 r = r0 + slot; r < r1; r += slots) {
+      const i64 i = r * P + p;
+      double w = W[i];
+      if (prev) w -= bp * prev[i];
+      W[i] = w;
+      acc += q[i] * w;
+    }
+  }
+  block_col_store(acc, P, partial, sm);
+}
+
+__global__ void k_fin_cols(const double* __restrict__ partial, int nout, double* __restrict__ out) {
+  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < nout; o += gridDim.x * blockDim.x)
+    out[o] = sum_partials(partial, RB, nout, o);
+}
+
+// W -= alpha ∘ q (when q != null); partial C[j][p] = Σ Q[j0+j]·W for j < jc
+constexpr int JC = 32;
+__global__ void k_lz_proj(double* __restrict__ W, const double* __restrict__ q, const double* __restrict__ alpha,
+                          const double* __restrict__ Q, int j0, int jc, i64 N, int P, double* __restrict__ partial) {
+  __shared__ double sm[RT];
+  const int slots = blockDim.x / P;
+  const int p = threadIdx.x % P, slot = threadIdx.x / P;
+  double acc[JC];
+#pragma unroll
+  for (int j = 0; j < JC; ++j) acc[j] = 0.0;
+  if (slot < slots) {
+    const double a = q ? alpha[p] : 0.0;
+    i64 r0, r1;
+    row_range(N, r0, r1);
+    const i64 blk = N * P;
+    for (i64 r = r0 + slot; r < r1; r += slots) {
+      const i64 i = r * P + p;
+      double w = W[i];
+      if (q) {
+        w -= a * q[i];
+        W[i] = w;
+      }
+#pragma unroll
+      for (int j = 0; j < JC; ++j)
+        if (j < jc) acc[j] += Q[(i64)(j0 + j) * blk + i] * w;
+    }
+  }
+  for (int j = 0; j < jc; ++j) {
+    __syncthreads();
+    sm[threadIdx.x] = acc[j];
+    __syncthreads();
+    if (threadIdx.x < P) {
+      double s = 0.0;
+      for (int k = 0; k < slots; ++k) s += sm[k * P + threadIdx.x];
+      partial[((i64)blockIdx.x * jc + j) * P + threadIdx.x] = s;
+    }
+  }
+}
+
+// W -= Σ_j Q[j] C[j]; optional partial ||W||²
+__global__ void k_lz_update(double* __restrict__ W, const double* __restrict__ Q, const double* __restrict__ C,
+                            int kc, i64 N, int P, double* __restrict__ partial_nrm) {
+  __shared__ double sm[RT];
+  const int slots = blockDim.x / P;
+  const int p = threadIdx.x % P, slot = threadIdx.x / P;
+  double acc = 0.0;
+  if (slot < slots) {
+    i64 r0, r1;
+    row_range(N, r0, r1);
+    const i64 blk = N * P;
+    for (i64 r = r0 + slot; r < r1; r += slots) {
+      const i64 i = r * P + p;
+      double s = 0.0;
+      for (int j = 0; j < kc; ++j) s += Q[(i64)j * blk + i] * C[j * P + p];
+      const double w = W[i] - s;
+      W[i] = w;
+      acc += w * w;
+    }
+  }
+  if (partial_nrm) block_col_store(acc, P, partial_nrm, sm);
+}
+
+// q_next = W / beta for probes with flag != 0
+__global__ void k_lz_next(const double* __restrict__ W, const double* __restrict__ beta, const int* __restrict__ flag,
+                          i64 N, int P, double* __restrict__ qn) {
+  const i64 items = N * P;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < items; i += (i64)gridDim.x * blockDim.x) {
+    const int p = int(i % P);
+    if (flag[p]) qn[i] = W[i] / beta[p];
+  }
+}
+
+}  // namespace
+
+// ================================================================ PCG driver
+PcgResult pcg_internal(Op& op, Precond* M, const double* B, double* X, int nrhs, double tol, int maxit,
+                       bool want_history, cudaStream_t s) {
+  if (nrhs < 1 || nrhs > RT) fail(GK_ERR_ARG, "pcg: nrhs must be in [1, 256]");
+  if (maxit < 0) fail(GK_ERR_ARG, "pcg: max_iterations must be >= 0");
+  const i64 N = op.N;
+  const i64 tot = N * nrhs;
+  DevBuf<double> R(static_cast<size_t>(tot)), Zb(static_cast<size_t>(tot)), Pb(static_cast<size_t>(tot)), AP(static_cast<size_t>(tot));
+  DevBuf<double> part(static_cast<size_t>(RB) * nrhs * 3);
+  DevBuf<double> sc(static_cast<size_t>(nrhs) * 4 + static_cast<size_t>(maxit + 1) * nrhs);
+  DevBuf<int> si(static_cast<size_t>(nrhs) * 4 + 1);
+  CgDev st;
+  st.bnorm = sc.p;
+  st.rz = sc.p + nrhs;
+  st.alpha = sc.p + 2 * nrhs;
+  st.beta = sc.p + 3 * nrhs;
+  st.hist = sc.p + 4 * nrhs;
+  st.active = si.p;
+  st.upd = si.p + nrhs;
+  st.its = si.p + 2 * nrhs;
+  st.conv = si.p + 3 * nrhs;
+  st.nactive = si.p + 4 * nrhs;
+  st.maxit = maxit;
+  st.tol = tol;
+  st.nrhs = nrhs;
+  double* p0 = part.p;
+  double* p1 = part.p + RB * nrhs;
+  double* p2 = part.p + 2 * RB * nrhs;
+  const int eb = blocks_for(tot);
+  if (M) M->ensure(nrhs);
+
+  // x0 = 0, r = b, z = M r, p = z
+  k_fill<<<eb, 256, 0, s>>>(X, 0.0, tot);
+  launched("pcg fill");
+  k_copy<<<eb, 256, 0, s>>>(B, R.p, tot);
+  launched("pcg copy");
+  double* Z = R.p;
+  if (M) {
+    Z = Zb.p;
+    M->apply(R.p, Z, nrhs, s);
+  }
+  k_copy<<<eb, 256, 0, s>>>(Z, Pb.p, tot);
+  launched("pcg copy");
+  k_dot_partial<<<RB, RT, 0, s>>>(B, B, N, nrhs, p0);
+  launched("pcg dot");
+  k_dot_partial<<<RB, RT, 0, s>>>(R.p, Z, N, nrhs, p1);
+  launched("pcg dot");
+  k_dot_partial<<<RB, RT, 0, s>>>(R.p, R.p, N, nrhs, p2);
+  launched("pcg dot");
+  k_cg_init<<<1, RT, 0, s>>>(st, p0, p1, p2);
+  launched("pcg init");
+
+  // one iteration, captured as a graph
+  auto iteration = [&](cudaStream_t cs) {
+    op.mvm(Pb.p, AP.p, nrhs, cs);
+    k_dot_partial<<<RB, RT, 0, cs>>>(Pb.p, AP.p, N, nrhs, p0);
+    launched("pcg dot");
+    k_cg_fin_pAp<<<1, RT, 0, cs>>>(st, p0);
+    launched("pcg fin");
+    k_cg_axpy<<<RB, RT, 0, cs>>>(st, X, R.p, Pb.p, AP.p, N, p1);
+    launched("pcg axpy");
+    k_cg_fin_rr<<<1, RT, 0, cs>>>(st, p1);
+    launched("pcg fin");
+    if (M) {
+      M->apply(R.p, Zb.p, nrhs, cs);  // writes rz partials into M's scratch; recompute below
+      k_dot_partial<<<RB, RT, 0, cs>>>(R.p, Zb.p, N, nrhs, p2);
+      launched("pcg dot");
+      k_cg_fin_rz<<<1, RT, 0, cs>>>(st, p2);
+    } else {
+      k_cg_fin_rz<<<1, RT, 0, cs>>>(st, p1);
+    }
+    launched("pcg fin");
+    k_cg_pupdate<<<eb, 256, 0, cs>>>(st, Pb.p, M ? Zb.p : R.p, N);
+    launched("pcg pupdate");
+  };
+
+  int* nact_h = nullptr;
+  GK_CUDA(cudaMallocHost(&nact_h, sizeof(int)));
+  GK_CUDA(cudaMemcpyAsync(nact_h, st.nactive, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GK_CUDA(cudaStreamSynchronize(s));
+  if (*nact_h > 0 && maxit > 0) {
+    // warm the operator's scratch outside capture, then capture ITER iterations
+    op.mvm(Pb.p, AP.p, nrhs, s);
+    const int ITER = 4;
+    const i64 before = g_launches.load();
+    cudaGraph_t graph;
+    GK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < ITER; ++i) iteration(s);
+    GK_CUDA(cudaStreamEndCapture(s, &graph));
+    const i64 nodes = g_launches.load() - before;
+    g_launches.fetch_sub(nodes);
+    cudaGraphExec_t exec;
+    GK_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    int launches = 0;
+    const int max_launches = (maxit + ITER - 1) / ITER + 1;
+    while (launches < max_launches) {
+      GK_CUDA(cudaGraphLaunch(exec, s));
+      g_launches.fetch_add(nodes);
+      ++launches;
+      GK_CUDA(cudaMemcpyAsync(nact_h, st.nactive, sizeof(int), cudaMemcpyDeviceToHost, s));
+      GK_CUDA(cudaStreamSynchronize(s));
+      if (*nact_h == 0) break;
+    }
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+  }
+  cudaFreeHost(nact_h);
+
+  PcgResult res;
+  res.iterations.resize(static_cast<size_t>(nrhs));
+  res.converged.resize(static_cast<size_t>(nrhs));
+  res.hist_len.resize(static_cast<size_t>(nrhs));
+  GK_CUDA(cudaMemcpyAsync(res.iterations.data(), st.its, sizeof(int) * nrhs, cudaMemcpyDeviceToHost, s));
+  GK_CUDA(cudaMemcpyAsync(res.converged.data(), st.conv, sizeof(int) * nrhs, cudaMemcpyDeviceToHost, s));
+  std::vector<double> bn(static_cast<size_t>(nrhs));
+  GK_CUDA(cudaMemcpyAsync(bn.data(), st.bnorm, sizeof(double) * nrhs, cudaMemcpyDeviceToHost, s));
+  if (want_history) {
+    res.history.resize(static_cast<size_t>(maxit + 1) * nrhs);
+    GK_CUDA(cudaMemcpyAsync(res.history.data(), st.hist, sizeof(double) * (maxit + 1) * nrhs,
+                            cudaMemcpyDeviceToHost, s));
+  }
+  GK_CUDA(cudaStreamSynchronize(s));
+  for (int b = 0; b < nrhs; ++b) res.hist_len[static_cast<size_t>(b)] = bn[static_cast<size_t>(b)] == 0.0 ? 0 : res.iterations[static_cast<size_t>(b)] + 1;
+  return res;
+}
+
+// ================================================================ preconditioner
+Precond::~Precond() {
+  if (stream) cudaStreamDestroy(stream);
+}
+
+static void set_smem(const void* fn, size_t bytes) {
+  if (bytes > 48 * 1024)
+    GK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+}
+
+void Precond::ensure(int nrhs) {
+  partial.reserve(static_cast<size_t>(RB) * k * nrhs);
+  t.reserve(static_cast<size_t>(k) * nrhs);
+  const size_t sh1 = sizeof(double) * (PC_RT * k + PC_RT * nrhs + k * nrhs);
+  if (sh1 > 227 * 1024) fail(GK_ERR_UNSUPPORTED, "preconditioner rank × nrhs too large for one pass");
+  set_smem((const void*)k_pc_proj, sh1);
+  set_smem((const void*)k_pc_apply, sizeof(double) * (k * nrhs + RT));
+}
+
+void Precond::apply(const double* r, double* z, int nrhs, cudaStream_t s) {
+  const size_t sh1 = sizeof(double) * (PC_RT * k + PC_RT * nrhs + k * nrhs);
+  k_pc_proj<<<RB, RT, sh1, s>>>(r, dinv.p, q1.p, N, int(k), nrhs, partial.p, nullptr);
+  launched("precond proj");
+  k_pc_fin<<<blocks_for(k * nrhs), 256, 0, s>>>(partial.p, int(k * nrhs), t.p);
+  launched("precond fin");
+  const size_t sh2 = sizeof(double) * (k * nrhs + RT);
+  k_pc_apply<<<RB, RT, sh2, s>>>(r, dinv.p, q1.p, t.p, N, int(k), nrhs, z, nullptr);
+  launched("precond apply");
+}
+
+void precond_quadratic(Precond& M, const double* r, int nrhs, double* out_h, cudaStream_t s) {
+  M.ensure(nrhs);
+  DevBuf<double> pcc(static_cast<size_t>(RB) * nrhs), cc(static_cast<size_t>(nrhs));
+  const size_t sh1 = sizeof(double) * (PC_RT * M.k + PC_RT * nrhs + M.k * nrhs);
+  k_pc_proj<<<RB, RT, sh1, s>>>(r, M.dinv.p, M.q1.p, M.N, int(M.k), nrhs, M.partial.p, pcc.p);
+  launched("precond proj");
+  k_pc_fin<<<blocks_for(M.k * nrhs), 256, 0, s>>>(M.partial.p, int(M.k * nrhs), M.t.p);
+  launched("precond fin");
+  k_fin_cols<<<1, 256, 0, s>>>(pcc.p, nrhs, cc.p);
+  launched("precond fin");
+  std::vector<double> T(static_cast<size_t>(M.k) * nrhs), c2(static_cast<size_t>(nrhs));
+  GK_CUDA(cudaMemcpyAsync(T.data(), M.t.p, sizeof(double) * T.size(), cudaMemcpyDeviceToHost, s));
+  GK_CUDA(cudaMemcpyAsync(c2.data(), cc.p, sizeof(double) * nrhs, cudaMemcpyDeviceToHost, s));
+  GK_CUDA(cudaStreamSynchronize(s));
+  for (int b = 0; b < nrhs; ++b) {
+    double t2 = 0.0;
+    for (i64 j = 0; j < M.k; ++j) t2 += T[static_cast<size_t>(j * nrhs + b)] * T[static_cast<size_t>(j * nrhs + b)];
+    out_h[b] = c2[static_cast<size_t>(b)] - t2;  // linalg.cpp:210-213
+  }
+}
+
+// CholeskyQR2 of A = [G; I_k], G = D^{-1/2} F.  Q1 = G R^{-1}, R = R2 R1.
+std::unique_ptr<Precond> precond_build(const double* F_int, i64 N, i64 k, const double* noise_int, int device,
+                                       cudaStream_t s) {
+  if (k < 1) fail(GK_ERR_ARG, "preconditioner needs a factor of rank at least 1");
+  if (k > 512) fail(GK_ERR_UNSUPPORTED, "preconditioner rank above 512 is not supported");
+  auto M = std::make_unique<Precond>();
+  M->device = device;
+  M->N = N;
+  M->k = k;
+  M->dinv.alloc(static_cast<size_t>(N));
+  DevBuf<double> G(static_cast<size_t>(N * k)), Q(static_cast<size_t>(N * k));
+  k_scale_transpose<<<blocks_for(N * k), 256, 0, s>>>(F_int, noise_int, N, int(k), G.p, M->dinv.p);
+  launched("precond scale");
+  DevBuf<double> part(static_cast<size_t>(RB) * k * k), gram(static_cast<size_t>(k * k)), Rinv_d(static_cast<size_t>(k * k));
+  const size_t shg = sizeof(double) * (PC_RT * k + k * k);
+  if (shg > 227 * 1024) fail(GK_ERR_UNSUPPORTED, "preconditioner rank too large for the Gram kernel");
+  set_smem((const void*)k_gram_partial, shg);
+  std::vector<double> gh(static_cast<size_t>(k * k)), R(static_cast<size_t>(k * k)), Rinv(static_cast<size_t>(k * k)), Q2(static_cast<size_t>(k * k));
+  // Q2 tracks the bottom block (initially I_k)
+  for (i64 j = 0; j < k; ++j) Q2[static_cast<size_t>(j * k + j)] = 1.0;
+  const double* cur = G.p;
+  double* nxt = Q.p;
+  for (int pass = 0; pass < 2; ++pass) {
+    k_gram_partial<<<RB, RT, shg, s>>>(cur, N, int(k), part.p);
+    launched("precond gram");
+    k_pc_fin<<<blocks_for(k * k), 256, 0, s>>>(part.p, int(k * k), gram.p);
+    launched("precond gram fin");
+    GK_CUDA(cudaMemcpyAsync(gh.data(), gram.p, sizeof(double) * k * k, cudaMemcpyDeviceToHost, s));
+    GK_CUDA(cudaStreamSynchronize(s));
+    // symmetric Gram (upper computed, gh[j*k+l] for j<=l) + Q2^T Q2 (col-major: element (j,l) at l*k+j)
+    std::vector<double> A(static_cast<size_t>(k * k));
+    for (i64 j = 0; j < k; ++j)
+      for (i64 l = j; l < k; ++l) {
+        long double acc = gh[static_cast<size_t>(j * k + l)];
+        for (i64 r = 0; r < k; ++r) acc += (long double)Q2[static_cast<size_t>(j * k + r)] * Q2[static_cast<size_t>(l * k + r)];
+        A[static_cast<size_t>(l * k + j)] = A[static_cast<size_t>(j * k + l)] = (double)acc;
+      }
+    cholesky_upper(int(k), A.data(), R.data());
+    // Rinv = R^{-1} (upper)
+    std::fill(Rinv.begin(), Rinv.end(), 0.0);
+    for (i64 c = 0; c < k; ++c) {
+      Rinv[static_cast<size_t>(c * k + c)] = 1.0 / R[static_cast<size_t>(c * k + c)];
+      for (i64 r = c - 1; r >= 0; --r) {
+        long double acc = 0.0L;
+        for (i64 m = r + 1; m <= c; ++m) acc += (long double)R[static_cast<size_t>(m * k + r)] * Rinv[static_cast<size_t>(c * k + m)];
+        Rinv[static_cast<size_t>(c * k + r)] = (double)(-acc / R[static_cast<size_t>(r * k + r)]);
+      }
+    }
+    // bottom block Q2 <- Q2 Rinv
+    std::vector<double> Q2n(static_cast<size_t>(k * k), 0.0);
+    for (i64 r = 0; r < k; ++r)
+      for (i64 c = 0; c < k; ++c) {
+        long double acc = 0.0L;
+        for (i64 m = 0; m <= c; ++m) acc += (long double)Q2[static_cast<size_t>(m * k + r)] * Rinv[static_cast<size_t>(c * k + m)];
+        Q2n[static_cast<size_t>(c * k + r)] = (double)acc;
+      }
+    Q2 = Q2n;
+    GK_CUDA(cudaMemcpyAsync(Rinv_d.p, Rinv.data(), sizeof(double) * k * k, cudaMemcpyHostToDevice, s));
+    k_rows_times_small<<<blocks_for(N * k), 256, 0, s>>>(cur, Rinv_d.p, N, int(k), nxt);
+    launched("precond rows x R^-1");
+    GK_CUDA(cudaStreamSynchronize(s));  // Rinv host buffer reused next pass
+    std::swap(G, Q);
+    cur = G.p;
+    nxt = Q.p;
+  }
+  M->q1 = std::move(G);  // after two swaps G holds the latest product
+  GK_CUDA(cudaStreamSynchronize(s));
+  return M;
+}
+
+// ================================================================ pivoted Cholesky
+std::unique_ptr<PivChol> pivchol_run(Op& op, bool kernel_part, i64 max_rank, double trace_tol) {
+  cudaStream_t s = op.stream;
+  const i64 N = op.N;
+  auto f = std::make_unique<PivChol>();
+  f->device = op.device;
+  f->N = N;
+  f->op = &op;
+  max_rank = std::min(max_rank, N);
+  if (max_rank < 0) fail(GK_ERR_ARG, "pivoted Cholesky rank must be >= 0");
+  DevBuf<double> diag(static_cast<size_t>(N)), noise(static_cast<size_t>(N)), d(static_cast<size_t>(N)), col(static_cast<size_t>(N));
+  f->L.alloc(static_cast<size_t>(std::max<i64>(max_rank, 1)) * N);
+  op.diagonal(diag.p, s);
+  {
+    std::vector<double> nh(static_cast<size_t>(N));
+    for (i64 r = 0; r < N; ++r) nh[static_cast<size_t>(r)] = r < op.n_value ? op.nv2 : op.ng2;
+    noise.upload(nh.data(), nh.size(), s);
+  }
+  k_pv_init<<<blocks_for(N), 256, 0, s>>>(diag.p, noise.p, kernel_part ? 1 : 0, N, d.p);
+  launched("pivchol init");
+  DevBuf<double> pmin(RB), psum(RB), pmax(RB), stats(5);
+  DevBuf<i64> pext(RB), pint(RB);
+  double* sh = nullptr;
+  GK_CUDA(cudaMallocHost(&sh, sizeof(double) * 5));
+  auto stats_of_d = [&]() {
+    k_pv_stats<<<RB, RT, 0, s>>>(d.p, op.d_ext_of_int(), N, pmin.p, psum.p, pmax.p, pext.p, pint.p);
+    launched("pivchol stats");
+    k_pv_stats_fin<<<1, 32, 0, s>>>(pmin.p, psum.p, pmax.p, pext.p, pint.p, RB, stats.p);
+    launched("pivchol stats fin");
+    GK_CUDA(cudaMemcpyAsync(sh, stats.p, sizeof(double) * 5, cudaMemcpyDeviceToHost, s));
+    GK_CUDA(cudaStreamSynchronize(s));
+  };
+  stats_of_d();
+  if (sh[0] < 0.0) {
+    cudaFreeHost(sh);
+    fail(GK_ERR_RUNTIME, "pivoted Cholesky requires a nonnegative diagonal");
+  }
+  f->initial_trace = sh[1];
+  f->residual_trace = sh[1];
+  const double scale = std::max(sh[2], 1e-300);
+  i64 k = 0;
+  for (; k < max_rank; ++k) {
+    const double dmax = sh[2];
+    i64 piv_ext, piv_int;
+    std::memcpy(&piv_ext, &sh[3], sizeof(i64));
+    std::memcpy(&piv_int, &sh[4], sizeof(i64));
+    if (dmax <= 0.0 || f->residual_trace <= trace_tol * f->initial_trace) break;
+    op.row(piv_ext, col.p, s);
+    const double nsub = kernel_part ? (piv_ext < op.n_value ? op.nv2 : op.ng2) : 0.0;
+    k_pv_update<<<blocks_for(N), 256, sizeof(double) * std::max<i64>(k, 1), s>>>(
+        col.p, f->L.p, int(k), N, piv_int, nsub, std::sqrt(dmax), d.p);
+    launched("pivchol update");
+    f->pivots.push_back(piv_ext);
+    // min check before clamping (linalg.cpp:165-167)
+    stats_of_d();
+    if (sh[0] < -1e-10 * scale) {
+      const double mn = sh[0];
+      cudaFreeHost(sh);
+      fail(GK_ERR_RUNTIME, "pivoted Cholesky: operator is not positive semidefinite (residual diagonal " +
+                               std::to_string(mn) + ")");
+    }
+    k_pv_clamp<<<blocks_for(N), 256, 0, s>>>(d.p, N, piv_int);
+    launched("pivchol clamp");
+    stats_of_d();
+    f->residual_trace = sh[1];
+  }
+  cudaFreeHost(sh);
+  f->k = k;
+  return f;
+}
+
+void pivchol_copy_L(const PivChol& f, double* out_host) {
+  if (f.k == 0) return;
+  DevBuf<double> tmp(static_cast<size_t>(f.N * f.k));
+  cudaStream_t s = f.op->stream;
+  k_perm_cols_out<<<blocks_for(f.N * f.k), 256, 0, s>>>(f.L.p, f.op->d_ext_of_int(), f.N, int(f.k), tmp.p);
+  launched("pivchol permute");
+  GK_CUDA(cudaMemcpyAsync(out_host, tmp.p, sizeof(double) * f.N * f.k, cudaMemcpyDeviceToHost, s));
+  GK_CUDA(cudaStreamSynchronize(s));
+}
+
+// ================================================================ Lanczos
+LanczosBatch lanczos_batch(Op& op, const double* start_int, int P, int steps,
+                           const std::vector<std::uint64_t>& restart_seeds, double* Q_out, cudaStream_t s) {
+  if (P < 1 || P > RT) fail(GK_ERR_ARG, "lanczos: number of probes must be in [1, 256]");
+  const i64 N = op.N;
+  steps = int(std::min<i64>(steps, N));
+  LanczosBatch res;
+  res.P = P;
+  res.steps = steps;
+  res.len.assign(static_cast<size_t>(P), steps);
+  res.alpha.assign(static_cast<size_t>(P), {});
+  res.beta.assign(static_cast<size_t>(P), {});
+  res.breakdown.assign(static_cast<size_t>(P), 0);
+  if (steps <= 0) {
+    res.len.assign(static_cast<size_t>(P), 0);
+    return res;
+  }
+  const i64 blk = N * P;
+  DevBuf<double> Qown;
+  double* Q = Q_out;
+  if (!Q) {
+    Qown.alloc(static_cast<size_t>(blk) * steps);
+    Q = Qown.p;
+  }
+  DevBuf<double> W(static_cast<size_t>(blk)), part(static_cast<size_t>(RB) * JC * P), C(static_cast<size_t>(steps) * P), C2(static_cast<size_t>(steps) * P);
+  DevBuf<double> sc(static_cast<size_t>(P) * 3);  // alpha, beta, bprev
+  DevBuf<int> flag(static_cast<size_t>(P));
+  double* d_alpha = sc.p;
+  double* d_beta = sc.p + P;
+  double* d_bprev = sc.p + 2 * P;
+  GK_CUDA(cudaMemcpyAsync(Q, start_int, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
+  GK_CUDA(cudaMemsetAsync(d_bprev, 0, sizeof(double) * P, s));
+  std::vector<double> bprev_h(static_cast<size_t>(P), 0.0), scale(static_cast<size_t>(P), 0.0);
+  std::vector<int> prev_valid(static_cast<size_t>(P), 0), live(static_cast<size_t>(P), 1), flag_h(static_cast<size_t>(P), 0);
+  std::vector<std::uint64_t> restart_count(static_cast<size_t>(P), 0);
+  std::vector<double> ab(static_cast<size_t>(2 * P));
+
+  auto project = [&](const double* qk_for_alpha, int kc, double* Cdst) {
+    for (int j0 = 0; j0 < kc; j0 += JC) {
+      const int jc = std::min(JC, kc - j0);
+      k_lz_proj<<<RB, RT, 0, s>>>(W.p, j0 == 0 ? qk_for_alpha : nullptr, d_alpha, Q, j0, jc, N, P, part.p);
+      launched("lanczos proj");
+      k_fin_cols<<<blocks_for(jc * P), 256, 0, s>>>(part.p, jc * P, Cdst + (i64)j0 * P);
+      launched("lanczos proj fin");
+    }
+  };
+
+  for (int k = 0; k < steps; ++k) {
+    const double* qk = Q + (i64)k * blk;
+    op.mvm(qk, W.p, P, s);
+    // w -= beta_prev * prev (prev = column k-1 when valid)
+    std::vector<double> bp(static_cast<size_t>(P));
+    for (int p = 0; p < P; ++p) bp[static_cast<size_t>(p)] = prev_valid[static_cast<size_t>(p)] ? bprev_h[static_cast<size_t>(p)] : 0.0;
+    GK_CUDA(cudaMemcpyAsync(d_bprev, bp.data(), sizeof(double) * P, cudaMemcpyHostToDevice, s));
+    k_lz_alpha<<<RB, RT, 0, s>>>(W.p, k > 0 ? Q + (i64)(k - 1) * blk : nullptr, d_bprev, qk, N, P, part.p);
+    launched("lanczos alpha");
+    k_fin_cols<<<1, 256, 0, s>>>(part.p, P, d_alpha);
+    launched("lanczos alpha fin");
+    const bool last = (k + 1 >= steps);
+    if (last) {
+      GK_CUDA(cudaMemcpyAsync(ab.data(), d_alpha, sizeof(double) * P, cudaMemcpyDeviceToHost, s));
+      GK_CUDA(cudaStreamSynchronize(s));
+      for (int p = 0; p < P; ++p)
+        if (live[static_cast<size_t>(p)]) res.alpha[static_cast<size_t>(p)].push_back(ab[static_cast<size_t>(p)]);
+      break;  // reference computes the final reorth/beta but never uses them
+    }
+    // w -= a q; two passes of w -= Q (Q^T w)
+    project(qk, k + 1, C.p);
+    k_lz_update<<<RB, RT, 0, s>>>(W.p, Q, C.p, k + 1, N, P, nullptr);
+    launched("lanczos update");
+    project(nullptr, k + 1, C2.p);
+    k_lz_update<<<RB, RT, 0, s>>>(W.p, Q, C2.p, k + 1, N, P, part.p);
+    launched("lanczos update");
+    k_fin_cols<<<1, 256, 0, s>>>(part.p, P, d_beta);
+    launched("lanczos beta fin");
+    GK_CUDA(cudaMemcpyAsync(ab.data(), d_alpha, sizeof(double) * 2 * P, cudaMemcpyDeviceToHost, s));
+    GK_CUDA(cudaStreamSynchronize(s));
+    std::vector<int> restart;
+    for (int p = 0; p < P; ++p) {
+      const double a = ab[static_cast<size_t>(p)];
+      const double beta = std::sqrt(ab[static_cast<size_t>(P + p)]);
+      flag_h[static_cast<size_t>(p)] = 0;
+      if (!live[static_cast<size_t>(p)]) continue;
+      res.alpha[static_cast<size_t>(p)].push_back(a);
+      scale[static_cast<size_t>(p)] = std::max({scale[static_cast<size_t>(p)], std::fabs(a), beta});
+      if (beta <= 1e-12 * std::max(scale[static_cast<size_t>(p)], 1e-300)) {
+        restart.push_back(p);
+      } else {
+        res.beta[static_cast<size_t>(p)].push_back(beta);
+        bprev_h[static_cast<size_t>(p)] = beta;
+        prev_valid[static_cast<size_t>(p)] = 1;
+        flag_h[static_cast<size_t>(p)] = 1;
+        ab[static_cast<size_t>(P + p)] = beta;
+      }
+    }
+    // beta (not beta²) for normalisation
+    std::vector<double> bet(static_cast<size_t>(P));
+    for (int p = 0; p < P; ++p) bet[static_cast<size_t>(p)] = flag_h[static_cast<size_t>(p)] ? bprev_h[static_cast<size_t>(p)] : 1.0;
+    GK_CUDA(cudaMemcpyAsync(d_beta, bet.data(), sizeof(double) * P, cudaMemcpyHostToDevice, s));
+    GK_CUDA(cudaMemcpyAsync(flag.p, flag_h.data(), sizeof(int) * P, cudaMemcpyHostToDevice, s));
+    double* qn = Q + (i64)(k + 1) * blk;
+    k_lz_next<<<blocks_for(blk), 256, 0, s>>>(W.p, d_beta, flag.p, N, P, qn);
+    launched("lanczos next");
+    if (!restart.empty()) {
+      // Deflating restart (linalg.cpp:46-69), on the host for the affected
+      // probes: fresh Gaussian direction, two-pass orthogonalisation against
+      // the collected basis, accept if its norm exceeds 1e-8 sqrt(N).
+      std::vector<double> Qh(static_cast<size_t>(blk) * (k + 1));
+      GK_CUDA(cudaMemcpyAsync(Qh.data(), Q, sizeof(double) * blk * (k + 1), cudaMemcpyDeviceToHost, s));
+      std::vector<double> qnh(static_cast<size_t>(blk));
+      GK_CUDA(cudaMemcpyAsync(qnh.data(), qn, sizeof(double) * blk, cudaMemcpyDeviceToHost, s));
+      GK_CUDA(cudaStreamSynchronize(s));
+      std::vector<double> rext(static_cast<size_t>(N)), rv(static_cast<size_t>(N));
+      const i64* ext_d = op.d_ext_of_int();
+      std::vector<i64> ext_h;
+      if (ext_d) {
+        ext_h.resize(static_cast<size_t>(N));
+        GK_CUDA(cudaMemcpy(ext_h.data(), ext_d, sizeof(i64) * N, cudaMemcpyDeviceToHost));
+      }
+      for (int p : restart) {
+        res.breakdown[static_cast<size_t>(p)] = 1;
+        bool found = false;
+        for (int attempt = 0; attempt < 8 && !found; ++attempt) {
+          gaussian(N, mix_seed(restart_seeds[static_cast<size_t>(p)], 7777 + restart_count[static_cast<size_t>(p)]++), std::uint64_t(attempt),
+                   rext.data());
+          for (i64 r = 0; r < N; ++r) rv[static_cast<size_t>(r)] = rext[static_cast<size_t>(ext_d ? ext_h[static_cast<size_t>(r)] : r)];
+          for (int pass = 0; pass < 2; ++pass) {
+            std::vector<double> cj(static_cast<size_t>(k + 1), 0.0);
+            for (int j = 0; j <= k; ++j) {
+              double sdot = 0.0;
+              for (i64 r = 0; r < N; ++r) sdot += Qh[static_cast<size_t>((i64)j * blk + r * P + p)] * rv[static_cast<size_t>(r)];
+              cj[static_cast<size_t>(j)] = sdot;
+            }
+            for (i64 r = 0; r < N; ++r) {
+              double sacc = 0.0;
+              for (int j = 0; j <= k; ++j) sacc += Qh[static_cast<size_t>((i64)j * blk + r * P + p)] * cj[static_cast<size_t>(j)];
+              rv[static_cast<size_t>(r)] -= sacc;
+            }
+          }
+          double rn = 0.0;
+          for (i64 r = 0; r < N; ++r) rn += rv[static_cast<size_t>(r)] * rv[static_cast<size_t>(r)];
+          rn = std::sqrt(rn);
+          if (rn > 1e-8 * std::sqrt(double(N))) {
+            for (i64 r = 0; r < N; ++r) qnh[static_cast<size_t>(r * P + p)] = rv[static_cast<size_t>(r)] / rn;
+            found = true;
+          }
+        }
+        if (!found) {
+          live[static_cast<size_t>(p)] = 0;
+          res.len[static_cast<size_t>(p)] = k + 1;
+          for (i64 r = 0; r < N; ++r) qnh[static_cast<size_t>(r * P + p)] = 0.0;
+        } else {
+          res.beta[static_cast<size_t>(p)].push_back(0.0);
+          prev_valid[static_cast<size_t>(p)] = 0;
+          bprev_h[static_cast<size_t>(p)] = 0.0;
+        }
+      }
+      GK_CUDA(cudaMemcpyAsync(qn, qnh.data(), sizeof(double) * blk, cudaMemcpyHostToDevice, s));
+      GK_CUDA(cudaStreamSynchronize(s));
+    }
+    bool any = false;
+    for (int p = 0; p < P; ++p) any = any || live[static_cast<size_t>(p)];
+    if (!any) break;
+  }
+  for (int p = 0; p < P; ++p) {
+    res.alpha[static_cast<size_t>(p)].resize(static_cast<size_t>(res.len[static_cast<size_t>(p)]));
+    res.beta[static_cast<size_t>(p)].resize(static_cast<size_t>(std::max(res.len[static_cast<size_t>(p)] - 1, 0)));
+  }
+  return res;
+}
+
+}  // namespace gk

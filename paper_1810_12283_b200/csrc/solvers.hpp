@@ -1,0 +1,67 @@
+// solvers.hpp — device-resident solvers over gk::Op (reference linalg.cpp).
+#pragma once
+
+#include <vector>
+
+#include "gk_common.hpp"
+
+namespace gk {
+
+// Preconditioner (linalg.cpp:176-213): Q1 (N×k, internal row order, stored
+// row-major so a row's k coefficients are contiguous) and D^{-1/2}.
+struct Precond {
+  int device = 0;
+  i64 N = 0, k = 0;
+  DevBuf<double> q1;       // [N][k]
+  DevBuf<double> dinv;     // [N] internal order
+  DevBuf<double> partial;  // [kRedBlocks][k][nrhs] scratch
+  DevBuf<double> t;        // [k][nrhs]
+  DevBuf<double> cbuf;     // scratch
+  const i64* ext = nullptr;  // operator row map used when q1 was built (null = identity)
+  std::vector<i64> int_of_ext_h;  // empty = identity
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  ~Precond();
+  // z = M^{-1} r; optionally rz[b] partials. All internal layout.
+  void apply(const double* r, double* z, int nrhs, cudaStream_t s);
+  void ensure(int nrhs);
+};
+
+struct PivChol {
+  int device = 0;
+  i64 N = 0, k = 0;
+  DevBuf<double> L;  // [k][N] column-major, internal row order
+  std::vector<i64> pivots;  // external indices
+  double initial_trace = 0, residual_trace = 0;
+  const Op* op = nullptr;
+};
+
+struct PcgResult {
+  std::vector<int> iterations, converged, hist_len;
+  std::vector<double> history;  // (maxit+1) × nrhs, row = iteration
+};
+
+// Batched PCG on internal-layout blocks B (N×nrhs), X output.
+PcgResult pcg_internal(Op& op, Precond* M, const double* B, double* X, int nrhs, double tol, int maxit,
+                       bool want_history, cudaStream_t s);
+
+std::unique_ptr<PivChol> pivchol_run(Op& op, bool kernel_part, i64 max_rank, double trace_tol);
+
+std::unique_ptr<Precond> precond_build(const double* F_int /*[k][N] dev col-major*/, i64 N, i64 k,
+                                       const double* noise_int /*dev [N]*/, int device, cudaStream_t s);
+
+struct LanczosBatch {
+  int P = 0;
+  int steps = 0;
+  std::vector<int> len;                 // achieved rank per probe
+  std::vector<std::vector<double>> alpha, beta;
+  std::vector<int> breakdown;
+};
+// Lanczos with two-pass full reorthogonalisation (linalg.cpp:17-81) for P
+// start vectors at once (internal layout, N×P). Q_out (optional, device) receives
+// [steps][N][P].
+LanczosBatch lanczos_batch(Op& op, const double* start_int, int P, int steps,
+                           const std::vector<std::uint64_t>& restart_seeds, double* Q_out,
+                           cudaStream_t s);
+
+}  // namespace gk

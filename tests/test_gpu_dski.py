@@ -1,0 +1,143 @@
+"""GPU parity of the D-SKI operator against the CPU oracle (restated reference).
+
+Mirrors reference proj/tests/test_dski.cpp and SURVEY §8(c): MVM, diagonal,
+rows, stacked transpose/apply and the grid kernel MVM must match the
+reference algorithm to <= 1e-12 relative (2-norm) on the same seeded inputs.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1810_12283_b200 as gk
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12  # BASELINE.json north_star: MVM outputs to <= 1e-12 relative in fp64
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b))
+
+
+def pair(n, d, ell=0.5, s=1.1, spacing=None, max_nodes=24, noise=(0.1, 0.05), order=0, seed=11,
+         with_gradients=True, lo=0.0, hi=1.0):
+    X = np.random.default_rng(seed).uniform(lo, hi, (n, d))
+    grid = gk.Grid.cover(X, spacing or ell / 4, 3, max_nodes)
+    g = gk.DskiOperator(gk.KernelSpec(ell, s), grid, X, noise, order, with_gradients)
+    r = O.DskiOperator(O.KernelSpec(ell, s), O.Grid(grid.dims, grid.origin, grid.spacing), X, noise,
+                       order, with_gradients)
+    return g, r, X, grid
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+@pytest.mark.parametrize("order", [0, 1])
+def test_mvm_matches_oracle(d, order):
+    g, r, _, _ = pair(60 if d < 3 else 40, d, order=order, max_nodes=16 if d == 3 else 24)
+    rng = np.random.default_rng(30)
+    for nrhs in (1, 3, 32):
+        V = rng.standard_normal((g.size(), nrhs))
+        assert rel(g.mvm(V), r.mvm(V)) <= TOL
+
+
+def test_mvm_without_gradients_is_plain_ski():
+    g, r, _, _ = pair(80, 2, with_gradients=False)
+    assert g.size() == 80
+    v = np.random.default_rng(1).standard_normal(80)
+    assert rel(g.mvm(v), r.mvm(v)) <= TOL
+
+
+def test_stages_match_oracle():
+    g, r, _, grid = pair(120, 2)
+    rng = np.random.default_rng(5)
+    v = rng.standard_normal(g.size())
+    u = rng.standard_normal(grid.size())
+    assert rel(g.stacked_transpose_apply(v), r.stacked_transpose_apply(v)) <= TOL
+    assert rel(g.stacked_apply(u), r.stacked_apply(u)) <= TOL
+    assert rel(g.grid_mvm(u), r.grid_mvm(u)) <= TOL
+    assert np.linalg.norm(g.grid_mvm(np.zeros(grid.size()))) == 0.0  # kuu_mvm: zero -> zero
+
+
+def test_diagonal_and_rows_match_oracle():
+    g, r, _, _ = pair(50, 2, s=1.2, noise=(0.1, 0.2), max_nodes=18)  # test_dski.cpp:157-174
+    dg, dr = g.diagonal(), r.diagonal()
+    assert np.abs(dg - dr).max() <= TOL * dr.max()
+    for i in (0, 7, 50, 120, 149):
+        row = g.row(i)
+        assert rel(row, r.row(i)) <= TOL
+        assert abs(row[i] - dg[i]) <= 1e-12 * abs(dg[i])
+    with pytest.raises(IndexError):
+        g.row(-1)
+    with pytest.raises(IndexError):
+        g.row(g.size())
+
+
+def test_diagonal_rows_3d():
+    g, r, _, _ = pair(40, 3, max_nodes=14)
+    assert np.abs(g.diagonal() - r.diagonal()).max() <= TOL * r.diagonal().max()
+    for i in (0, 41, 159):
+        assert rel(g.row(i), r.row(i)) <= TOL
+
+
+def test_size_mismatch_and_out_of_grid():
+    g, _, X, grid = pair(30, 2)
+    with pytest.raises(ValueError):
+        g.mvm(np.zeros(3))  # test_dski.cpp:115
+    Xbad = X.copy()
+    Xbad[7] = [5.0, 5.0]
+    with pytest.raises(gk.OutOfGridError) as e:
+        gk.DskiOperator(gk.KernelSpec(0.5, 1.0), grid, Xbad)
+    assert e.value.point == 7 and "point 7" in str(e.value)
+
+
+def test_symmetry_and_psd():
+    g, _, _, _ = pair(80, 2, ell=0.4, noise=(0.0, 0.0), max_nodes=24)  # test_dski.cpp:141-155
+    rng = np.random.default_rng(60)
+    for _ in range(5):
+        v = rng.standard_normal(g.size())
+        assert v @ g.mvm(v) >= -1e-10 * (v @ v)
+    u, v = rng.standard_normal(g.size()), rng.standard_normal(g.size())
+    a, b = u @ g.mvm(v), g.mvm(u) @ v
+    assert abs(a - b) <= 1e-10 * abs(a)
+
+
+def test_config_c1_mvm_parity_and_fidelity():
+    """C1 (BASELINE configs[0]): 60x60 grid, n=2000, ell=0.15 — MVM parity vs the
+    oracle and fidelity vs the exact D-SE K∇ (c02 analogue, ~1e-5)."""
+    X, y, dY = gk.make_dataset(1, 0)
+    grid = gk.Grid.cover(X, 1e-3, 3, 60)
+    assert list(grid.dims) == [60, 60]
+    g = gk.DskiOperator(gk.KernelSpec(0.15, 1.0), grid, X, (1e-2, 1e-2))
+    r = O.DskiOperator(O.KernelSpec(0.15, 1.0), O.Grid(grid.dims, grid.origin, grid.spacing), X,
+                       (1e-2, 1e-2))
+    V = np.random.default_rng(2).standard_normal((g.size(), 9))
+    assert rel(g.mvm(V), r.mvm(V)) <= TOL
+    ex = gk.ExactOperator(gk.KernelSpec(0.15, 1.0), X, (1e-2, 1e-2))
+    E = ex.mvm(V)
+    err = np.abs(g.mvm(V) - E).max() / np.abs(E).max()
+    # fidelity (interpolation error at ell/h ~ 7.95), not parity: the GPU and
+    # the oracle carry the same approximation
+    r_err = np.abs(r.mvm(V) - E).max() / np.abs(E).max()
+    assert abs(err - r_err) <= 1e-10 and err < 5e-4
+
+
+def test_exact_operator_matches_dense_assembly():
+    X = np.random.default_rng(3).uniform(0, 1, (70, 2))
+    k = gk.KernelSpec(0.3, 1.2)
+    ex = gk.ExactOperator(k, X, (0.05, 0.02))
+    A = O.assemble_dense(O.KernelSpec(0.3, 1.2), X)
+    nd = np.r_[np.full(70, 0.05 ** 2), np.full(140, 0.02 ** 2)]
+    A = A + np.diag(nd)
+    V = np.random.default_rng(4).standard_normal((210, 5))
+    assert rel(ex.mvm(V), A @ V) <= TOL
+    assert np.abs(ex.diagonal() - np.diag(A)).max() <= 1e-13
+    for i in (0, 69, 70, 209):
+        assert rel(ex.row(i), A[i]) <= TOL
+
+
+def test_dense_operator_roundtrip():
+    A = np.random.default_rng(5).standard_normal((40, 40))
+    op = gk.DenseOperator(A)
+    v = np.random.default_rng(6).standard_normal((40, 3))
+    assert rel(op.mvm(v), A @ v) <= 1e-14
+    assert np.allclose(op.diagonal(), np.diag(A))
+    assert np.allclose(op.row(3), A[3])

@@ -1,0 +1,162 @@
+"""GPU parity of the solvers (reference linalg.cpp / test_linalg.cpp) against the
+CPU oracle: PCG (solution to tol, iterations ±1), pivoted Cholesky (pivot
+order bit-exact), the QR preconditioner, SLQ (1e-8 relative with identical
+probe seeds) and Lanczos."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1810_12283_b200 as gk
+
+pytestmark = pytest.mark.gpu
+
+
+def random_spd(n, seed, jitter=1e-6):
+    G = np.random.default_rng(seed).standard_normal((n, n))
+    A = G @ G.T / n
+    A[np.diag_indices(n)] += jitter
+    return A
+
+
+def test_cg_identity_and_zero_rhs():
+    I = gk.DenseOperator(np.eye(20))
+    b = np.random.default_rng(1).standard_normal(20)
+    res = gk.cg(I, b, 1e-10, 100)
+    assert res.converged and res.iterations <= 1
+    assert np.linalg.norm(res.x - b) < 1e-12
+    z = gk.cg(I, np.zeros(20))
+    assert z.converged and z.iterations == 0 and np.linalg.norm(z.x) == 0.0
+    assert z.residual_history.size == 0
+
+
+def test_cg_matches_direct_and_history():
+    A = random_spd(50, 3)
+    b = np.random.default_rng(4).standard_normal(50)
+    res = gk.cg(gk.DenseOperator(A), b, 1e-12, 500)
+    want = np.linalg.solve(A, b)
+    assert res.converged
+    assert np.linalg.norm(res.x - want) <= 1e-8 * np.linalg.norm(want)
+    assert res.residual_history.size == res.iterations + 1
+    assert res.residual_history[-1] <= 1e-12
+    ref = O.cg(O.DenseOperator(A), b, 1e-12, 500)
+    assert abs(res.iterations - ref.iterations) <= 1
+
+
+def test_cg_nonconvergence_flagged():
+    A = random_spd(60, 7, 1e-12)
+    res = gk.cg(gk.DenseOperator(A), np.random.default_rng(8).standard_normal(60), 1e-14, 2)
+    assert not res.converged and res.iterations == 2
+
+
+def test_cg_batched_columns_are_independent():
+    A = random_spd(64, 9, 1e-3)
+    B = np.random.default_rng(10).standard_normal((64, 7))
+    B[:, 3] = 0.0  # zero column converges with 0 iterations
+    out = gk.cg(gk.DenseOperator(A), B, 1e-10, 400)
+    for c in range(7):
+        ref = O.cg(O.DenseOperator(A), B[:, c], 1e-10, 400)
+        assert out[c].converged == ref.converged
+        assert abs(out[c].iterations - ref.iterations) <= 1
+        if c != 3:
+            assert np.linalg.norm(out[c].x - ref.x) <= 1e-8 * np.linalg.norm(ref.x)
+    assert out[3].iterations == 0
+
+
+def test_pivoted_cholesky_known_answer_order():
+    # test_linalg.cpp:93-101
+    d = np.array([3.0, 9.0, 1.0, 7.0, 5.0, 2.0])
+    f = gk.pivoted_cholesky(gk.DenseOperator(np.diag(d)), 6)
+    assert list(f.pivots) == [1, 3, 4, 0, 5, 2]
+
+
+def test_pivoted_cholesky_full_rank_and_indefinite():
+    A = random_spd(40, 13)
+    f = gk.pivoted_cholesky(gk.DenseOperator(A), 40)
+    L = f.L
+    assert np.abs(L @ L.T - A).max() <= 1e-10 * np.abs(A).max()
+    ref = O.pivoted_cholesky(O.DenseOperator(A), 40)
+    assert list(f.pivots) == list(ref.pivots)
+    with pytest.raises(RuntimeError):
+        gk.pivoted_cholesky(gk.DenseOperator(np.array([[1.0, 2.0], [2.0, 1.0]])), 2)
+
+
+def test_preconditioner_vs_long_double_oracle():
+    n, k, sigma = 20, 5, 1e-4  # test_linalg.cpp:162-176
+    F = np.column_stack([np.random.default_rng(100 + j).standard_normal(n) for j in range(k)])
+    P = gk.Preconditioner(F, sigma)
+    assert P.rank() == k
+    M = sigma ** 2 * np.eye(n) + F @ F.T
+    R = O.Preconditioner(F, sigma)
+    for s in range(5):
+        b = np.random.default_rng(200 + s).standard_normal(n)
+        want = R.apply(b)
+        assert np.linalg.norm(P.apply(b) - want) <= 1e-8 * np.linalg.norm(want)
+        assert abs(P.quadratic(b) - b @ want) <= 1e-8 * abs(b @ want)
+    with pytest.raises(ValueError):
+        gk.Preconditioner(np.ones((5, 1)), 0.0)
+
+
+def test_slq_exact_for_scaled_identity():
+    r1 = gk.slq_logdet(gk.DenseOperator(np.eye(64)), 4, 10, 42)
+    assert abs(r1.logdet) <= 1e-12
+    r2 = gk.slq_logdet(gk.DenseOperator(3.7 * np.eye(64)), 4, 10, 42)
+    assert abs(r2.logdet - 64 * np.log(3.7)) <= 1e-10 * 64 * np.log(3.7)
+
+
+def test_slq_matches_oracle_per_probe():
+    A = random_spd(300, 21, 0.1)
+    g = gk.slq_logdet(gk.DenseOperator(A), 6, 30, 5)
+    r = O.slq_logdet(O.DenseOperator(A), 6, 30, 5)
+    assert abs(g.logdet - r.logdet) <= 1e-8 * abs(r.logdet)
+    assert np.allclose(g.estimates, r.estimates, rtol=1e-8, atol=0)
+
+
+def test_lanczos_lowrank_rank3_and_identity_breakdown():
+    G = np.column_stack([np.random.default_rng(500 + j).standard_normal(40) for j in range(3)])
+    A = G @ G.T
+    f = gk.lanczos_lowrank(gk.DenseOperator(A), 10, 7)
+    assert f.rank() >= 3
+    assert np.abs(f.dense() - A).max() <= 1e-10 * np.abs(A).max()
+    assert np.linalg.norm(f.Q.T @ f.Q - np.eye(f.rank())) < 1e-8
+    fi = gk.lanczos_lowrank(gk.DenseOperator(np.eye(30)), 5, 3)
+    assert abs(fi.alpha[0] - 1.0) < 1e-12 and fi.breakdown
+
+
+def test_trace_estimate_a_equals_b():
+    A = random_spd(40, 23)
+    op = gk.DenseOperator(A)
+    t = gk.trace_estimate(op, op, 8, 9, 1e-12, 1000)
+    assert abs(t - 40.0) <= 1e-8 * 40
+
+
+def _dski_model(config=1, n=None):
+    X, y, dY = gk.make_dataset(config, 0)
+    if n:
+        X, y, dY = X[:n], y[:n], dY[:n]
+    return X, y, dY
+
+
+def test_dski_pipeline_matches_oracle_c1_subset():
+    """GpModel::preconditioner + solve + logdet on a D-SKI operator (gp.cpp:117-187)."""
+    X, y, dY = _dski_model(1, 600)
+    ell, noise = 0.15, (1e-2, 1e-2)
+    grid = gk.Grid.cover(X, 1e-3, 3, 40)
+    g = gk.DskiOperator(gk.KernelSpec(ell, 1.0), grid, X, noise)
+    r = O.DskiOperator(O.KernelSpec(ell, 1.0), O.Grid(grid.dims, grid.origin, grid.spacing), X, noise)
+    # pivoted Cholesky of the kernel part: pivot order bit-exact
+    fg = gk.pivoted_cholesky(g, 20, kernel_part=True)
+    fr = O.pivoted_cholesky(r, 20, noise_diag=r.noise_diagonal())
+    assert list(fg.pivots) == list(fr.pivots)
+    assert np.abs(fg.L - fr.L).max() <= 1e-9 * np.abs(fr.L).max()
+    Pg = gk.Preconditioner.from_pivchol(g, fg)
+    Pr = O.Preconditioner(fr.L, r.noise_diagonal())
+    b = gk.stacked_targets(y, dY, y.mean())
+    assert np.linalg.norm(Pg.apply(b) - Pr.apply(b)) <= 1e-9 * np.linalg.norm(Pr.apply(b))
+    sg = gk.cg(g, b, 1e-8, 3000, Pg)
+    sr = O.cg(r, b, 1e-8, 3000, Pr)
+    assert sg.converged and sr.converged
+    assert abs(sg.iterations - sr.iterations) <= 1
+    assert np.linalg.norm(sg.x - sr.x) <= 1e-6 * np.linalg.norm(sr.x)
+    lg = gk.slq_logdet(g, 8, 25, 0, 0.5e-4)
+    lr = O.slq_logdet(r, 8, 25, 0, 0.5e-4)
+    assert abs(lg.logdet - lr.logdet) <= 1e-8 * abs(lr.logdet)

@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""Benchmark: batched D-SKI K∇ MVM throughput (rows·RHS/s) on BASELINE config C2
+(configs[1]: d=2, n=10,000 -> N=30,000, 100x100 grid, SE ell=0.2, 32 RHS =
+y + 31 Rademacher probes), plus the PCG+SLQ solve time on the same operator.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+One step = one batched K∇ MVM over the 32-RHS block (scatter B^T, K_UU mode
+products, gather B + noise) with inputs resident in HBM; L2 is flushed before
+every timed step (the C2 working set, ~34 MB, would otherwise sit in the 126 MB
+L2). N>1 (torchrun): every rank holds an operator replica and its own 32-RHS
+probe shard (weak scaling, no data-path collective); time = max over ranks.
+--impl reference times the reference algorithm on the host cores (the C++
+oracle port, OpenMP over RHS — the reference cannot be built here, see
+DESIGN.md) on the same workload.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG = {"workload": "C2: D-SKI d=2 n=10000 (N=30000) grid 100x100 SE ell=0.2 s=1 "
+                      "sigma=1e-2, 32 RHS (y + 31 Rademacher probes)",
+          "config_id": 2, "n": 10000, "d": 2, "N": 30000, "grid": [100, 100], "nrhs": 32,
+          "ell": 0.2, "noise": 1e-2, "precond_rank": 50, "pcg_tol": 1e-4, "slq_probes": 31,
+          "slq_steps": 30}
+METRIC = "K∇ MVM rows·RHS/s"
+UNIT = "rows*rhs/s"
+
+
+def build_problem():
+    import paper_1810_12283_b200 as gk
+    X, y, dY = gk.make_dataset(2, 0)
+    grid = gk.Grid.cover(X, 1e-3, 3, 100)
+    assert list(grid.dims) == [100, 100]
+    return X, y, dY, grid
+
+
+def rhs_block(N, nrhs, y, dY, probe_offset):
+    """Column 0 = stacked targets (observations.hpp:29-35), the rest Rademacher
+    probes rademacher_vector(N, 0, 1000+p) (the trace-estimator streams,
+    linalg.cpp:264-266); shard p offsets the probe ids."""
+    import paper_1810_12283_b200 as gk
+    B = np.empty((N, nrhs), order="F")
+    B[:, 0] = gk.stacked_targets(y, dY, y.mean())
+    for c in range(1, nrhs):
+        B[:, c] = gk.rademacher_vector(N, 0, 1000 + probe_offset + c - 1)
+    return B
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.f = None
+
+    def __enter__(self):
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.f:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                rows.append((float(p[0]), float(p[1]), float(p[2]), p[3], p[4:8]))
+            except ValueError:
+                continue
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        load = [r for r in rows if r[2] > 200.0] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in load for i, v in enumerate(r[4]) if v.lower() == "active"})
+        return {"sm_mhz": float(np.median([r[0] for r in load])),
+                "sm_max_mhz": float(max(r[1] for r in rows)), "reasons": reasons,
+                "samples": len(rows), "samples_under_load": len(load)}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def dski_bytes(N, n, d, m, nrhs, Mc):
+    """SURVEY §8(d) algorithmic bytes of one batched D-SKI MVM."""
+    return 8.0 * (3 * N * nrhs + 2 * n * d + 4 * m * nrhs + Mc)
+
+
+def stage_bytes(N, n, d, m, nrhs, T=6):
+    """Algorithmic bytes per launch of each stage kernel of this implementation
+    (per-point stencil record = base ints + d×2×T doubles)."""
+    pt = n * (16 + 8 * d * 2 * T)
+    return {"scatter": 8.0 * (N * nrhs + m * nrhs) + pt,          # read v, write u
+            "kuu_mode": 8.0 * (2 * m * nrhs),                       # read + write one grid block
+            "gather": 8.0 * (m * nrhs + 2 * N * nrhs) + pt}         # read w, v; write out
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import paper_1810_12283_b200 as gk
+
+    X, y, dY, grid = build_problem()
+    n, d = X.shape
+    ker = gk.KernelSpec(CONFIG["ell"], 1.0)
+    noise = (CONFIG["noise"], CONFIG["noise"])
+    op = gk.DskiOperator(ker, grid, X, noise, device=local)
+    N, nrhs, m = op.size(), CONFIG["nrhs"], grid.size()
+    Bh = rhs_block(N, nrhs, y, dY, probe_offset=rank * nrhs)
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    # inputs resident in HBM: external (col-major) block -> internal layout once
+    Vext = torch.from_numpy(np.ascontiguousarray(Bh.T)).to(dev)  # (nrhs, N) == col-major N×nrhs
+    Vi = torch.empty(N * nrhs, dtype=torch.float64, device=dev)
+    Oi = torch.empty_like(Vi)
+    op.to_internal_dev(Vext.data_ptr(), Vi.data_ptr(), nrhs, stream=sp)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        op.stage_dev(3, Vi.data_ptr(), Oi.data_ptr(), nrhs, stream=sp)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    # correctness guard on this very data (external round trip vs host API)
+    ref_cols = op.mvm(Bh[:, :2])
+    Oe = torch.empty_like(Vext)
+    op.from_internal_dev(Oi.data_ptr(), Oe.data_ptr(), nrhs, stream=sp)
+    torch.cuda.synchronize()
+    got = Oe.T.cpu().numpy()[:, :2]
+    assert np.linalg.norm(got - ref_cols) <= 1e-13 * np.linalg.norm(ref_cols)
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = gk.kernel_launch_count()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush (outside the events)
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    launches = gk.kernel_launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    ms = float(np.mean([s.elapsed_time(e) for s, e in zip(starts, ends)]))
+    ms_t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    value = world * N * nrhs / (ms * 1e-3)
+
+    # ---- per-stage timing (dominant kernel for the roofline), same stream
+    Ui = torch.empty(m * nrhs, dtype=torch.float64, device=dev)
+    Wi = torch.empty_like(Ui)
+    stage_ms = {}
+    reps = max(20, min(args.steps, 200))
+    for name, st, a, b in (("scatter", 0, Vi, Ui), ("kuu", 1, Ui, Wi), ("gather", 2, Wi, Oi)):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(reps)]
+        for s0, e0 in ev:
+            flush.zero_()
+            s0.record(stream)
+            op.stage_dev(st, a.data_ptr(), b.data_ptr(), nrhs, stream=sp)
+            e0.record(stream)
+        torch.cuda.synchronize()
+        stage_ms[name] = float(np.mean([s0.elapsed_time(e0) for s0, e0 in ev]))
+    sb = stage_bytes(N, n, d, m, nrhs)
+    peaks = measured_peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    bytes_per = {"scatter": sb["scatter"], "kuu": 2 * sb["kuu_mode"], "gather": sb["gather"]}
+    dom = max(stage_ms, key=stage_ms.get)
+    achieved = bytes_per[dom] / (stage_ms[dom] * 1e-3) / 1e9
+    Mc = 198 * (198 // 2 + 1)
+    mvm_bytes = dski_bytes(N, n, d, m, nrhs, Mc)
+
+    # ---- end to end through the public API with host (pinned) buffers
+    Hin = torch.from_numpy(np.asfortranarray(Bh).T.copy()).pin_memory()  # (nrhs, N) == col-major
+    Hout = torch.empty_like(Hin).pin_memory()
+    import ctypes
+    lib = gk._lib
+    pin_in = ctypes.cast(Hin.data_ptr(), ctypes.POINTER(ctypes.c_double))
+    pin_out = ctypes.cast(Hout.data_ptr(), ctypes.POINTER(ctypes.c_double))
+
+    def e2e_call():
+        gk._check(lib.gk_op_mvm(op.handle, pin_in, N, pin_out, N, nrhs))
+
+    for _ in range(3):
+        e2e_call()
+    e2e_steps = max(5, min(args.steps, 50))
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_call()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    e2e_t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = world * N * nrhs / float(e2e_t.item())
+
+    # ---- PCG + SLQ solve (GpModel::preconditioner/solve/logdet on this shard)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    fac = gk.pivoted_cholesky(op, CONFIG["precond_rank"], kernel_part=True)
+    M = gk.Preconditioner.from_pivchol(op, fac)
+    torch.cuda.synchronize()
+    t_pre = time.perf_counter() - t0
+    Xd = torch.empty_like(Vext)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    its, conv = gk.cg_dev(op, Vext.data_ptr(), Xd.data_ptr(), nrhs, CONFIG["pcg_tol"], 1000, M,
+                          stream=sp)
+    torch.cuda.synchronize()
+    t_pcg = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    slq = gk.slq_logdet(op, CONFIG["slq_probes"], CONFIG["slq_steps"], 0, 0.5 * 1e-4,
+                        probe_offset=rank * CONFIG["slq_probes"])
+    t_slq = time.perf_counter() - t0
+    solve = torch.tensor([t_pre, t_pcg, t_slq], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(solve, op=dist.ReduceOp.MAX)
+    t_pre, t_pcg, t_slq = [float(v) for v in solve.tolist()]
+
+    line = None
+    if rank == 0:
+        cpu = cpu_baseline(args) if world == 1 and not args.no_cpu_baseline else None
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded C2 generator)",
+            "config": dict(CONFIG, parallelism=f"rhs-shard x{world}" if world > 1 else "1 GPU",
+                           l2="flushed before every timed step (256 MB write)",
+                           timing="CUDA events per step on the launching stream, max over ranks"),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * N * nrhs,
+                    "d2h_bytes_per_step": 8 * N * nrhs,
+                    "path": "gk_op_mvm (C-ABI, pinned host buffers, permutes + copies timed)"},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
+                         "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if peaks else "fallback",
+                         "bytes_per_launch": bytes_per[dom], "stage_ms": stage_ms},
+            "mvm_roofline": {"algorithmic_bytes": mvm_bytes,
+                             "achieved_gbs": mvm_bytes / (ms * 1e-3) / 1e9,
+                             "frac_hbm": mvm_bytes / (ms * 1e-3) / 1e9 / hbm},
+            "solve": {"precond_build_s": t_pre, "pcg_s": t_pcg, "slq_s": t_slq,
+                      "pcg_plus_slq_s": t_pcg + t_slq, "pcg_iterations": [int(v) for v in its],
+                      "pcg_converged": int(np.sum(conv)), "slq_logdet_shard": slq.logdet},
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return line
+
+
+def cpu_baseline(args, full=False):
+    """The oracle port of the reference MVM on this host's cores (OpenMP over RHS)."""
+    import oracle as O
+    X, y, dY, grid = build_problem()
+    ref = O.DskiOperator(O.KernelSpec(CONFIG["ell"], 1.0), O.Grid(grid.dims, grid.origin, grid.spacing),
+                         X, (CONFIG["noise"], CONFIG["noise"]))
+    N, nrhs = ref.size(), CONFIG["nrhs"]
+    Bh = rhs_block(N, nrhs, y, dY, 0)
+    ref.mvm(Bh[:, :4])  # warm
+    reps, times = 0, []
+    t_end = time.perf_counter() + (20.0 if full else 10.0)
+    while time.perf_counter() < t_end and reps < 50:
+        t0 = time.perf_counter()
+        ref.mvm(Bh)
+        times.append(time.perf_counter() - t0)
+        reps += 1
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    med = float(np.median(times))
+    return {"value": N * nrhs / med, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{reps} full 32-RHS C2 MVMs (median), OpenMP over RHS columns",
+            "ms_per_step": med * 1e3}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    import oracle as O
+    X, y, dY, grid = build_problem()
+    ref = O.DskiOperator(O.KernelSpec(CONFIG["ell"], 1.0), O.Grid(grid.dims, grid.origin, grid.spacing),
+                         X, (CONFIG["noise"], CONFIG["noise"]))
+    N, nrhs = ref.size(), CONFIG["nrhs"]
+    Bh = rhs_block(N, nrhs, y, dY, 0)
+    for _ in range(max(args.warmup, 1)):
+        ref.mvm(Bh)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        ref.mvm(Bh)
+        times.append(time.perf_counter() - t0)
+    s = float(np.mean(times))
+    value = N * nrhs / s
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": s * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded C2 generator)", "config": dict(CONFIG, parallelism="host cores"),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"{args.steps} full 32-RHS C2 MVMs, OpenMP over RHS columns"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="gk", choices=["gk", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl != "reference":
+        args.warmup = 3
+    if args.impl == "reference":
+        line = run_reference(args)
+    else:
+        line = run_gpu(args)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -41,8 +41,8 @@ using namespace gk;
 
 struct gk_precond {
   std::unique_ptr<Precond> impl;
-  // cached copies reordered for an operator's internal row order
-  std::vector<std::pair<const i64*, std::unique_ptr<Precond>>> reordered;
+  // cached copies reordered for an operator's internal row order (keyed by Op::uid)
+  std::vector<std::pair<std::uint64_t, std::unique_ptr<Precond>>> reordered;
 };
 struct gk_pivchol {
   std::unique_ptr<PivChol> impl;
@@ -97,16 +97,22 @@ Precond& precond_for(const gk_precond* M, const Op& op) {
   Precond& base = *mm->impl;
   if (base.N != op.N) fail(GK_ERR_ARG, "preconditioner and operator sizes differ");
   const i64* ext = op.d_ext_of_int();
-  if (base.ext == ext) return base;
-  if (base.ext != nullptr) fail(GK_ERR_UNSUPPORTED, "preconditioner was built for another operator's row order");
+  if (base.order_uid == op.uid) return base;
+  if (base.order_uid == 0 && ext == nullptr) return base;  // both in external order
+  if (base.order_uid != 0)
+    fail(GK_ERR_UNSUPPORTED, "preconditioner was built for another operator's row order");
   for (auto& pr : mm->reordered)
-    if (pr.first == ext) return *pr.second;
-  // identity-ordered preconditioner -> reorder rows for op: new[r] = old[ext[r]]
+    if (pr.first == op.uid) return *pr.second;
+  // external-ordered preconditioner -> reorder rows for op: new[r] = old[ext[r]]
   auto P = std::make_unique<Precond>();
   P->device = base.device;
   P->N = base.N;
   P->k = base.k;
-  P->ext = ext;
+  P->order_uid = op.uid;
+  P->ext_own.alloc(static_cast<size_t>(base.N));
+  GK_CUDA(cudaMemcpy(P->ext_own.p, ext, sizeof(i64) * base.N, cudaMemcpyDeviceToDevice));
+  P->ext = P->ext_own.p;
+  GK_CUDA(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
   P->q1.alloc(static_cast<size_t>(base.N * base.k));
   P->dinv.alloc(static_cast<size_t>(base.N));
   cudaStream_t s = op.stream;
@@ -120,7 +126,7 @@ Precond& precond_for(const gk_precond* M, const Op& op) {
   from_internal(nullptr, base.N, base.dinv.p, tmp1.p, base.N, 1, s);
   to_internal(ext, base.N, tmp1.p, base.N, P->dinv.p, 1, s);
   GK_CUDA(cudaStreamSynchronize(s));
-  mm->reordered.emplace_back(ext, std::move(P));
+  mm->reordered.emplace_back(op.uid, std::move(P));
   return *mm->reordered.back().second;
 }
 
@@ -597,6 +603,7 @@ gk_status gk_precond_from_pivchol(const gk_op* h, const gk_pivchol* f, gk_precon
     if (!f || !f->impl) fail(GK_ERR_ARG, "null factor");
     const PivChol& p = *f->impl;
     if (p.k == 0) fail(GK_ERR_RUNTIME, "pivoted Cholesky produced an empty preconditioner factor");
+    if (p.order_uid != op.uid) fail(GK_ERR_ARG, "pivoted Cholesky factor belongs to another operator");
     std::lock_guard<std::mutex> lk(op.mu);
     DeviceGuard dg(op.device);
     cudaStream_t s;
@@ -610,7 +617,12 @@ gk_status gk_precond_from_pivchol(const gk_op* h, const gk_pivchol* f, gk_precon
     auto M = std::make_unique<gk_precond>();
     M->impl = precond_build(p.L.p, op.N, p.k, nd.p, op.device, s);
     M->impl->stream = s;
-    M->impl->ext = op.d_ext_of_int();
+    M->impl->order_uid = op.uid;
+    if (op.d_ext_of_int()) {
+      M->impl->ext_own.alloc(static_cast<size_t>(op.N));
+      GK_CUDA(cudaMemcpy(M->impl->ext_own.p, op.d_ext_of_int(), sizeof(i64) * op.N, cudaMemcpyDeviceToDevice));
+      M->impl->ext = M->impl->ext_own.p;
+    }
     *out = M.release();
   });
 }

@@ -122,8 +122,12 @@ enum OpKind { KIND_EXACT = 0, KIND_DSKI = 1, KIND_DSKIP = 2, KIND_DENSE = 3 };
 // INTERNAL layout: rows in the operator's internal order (D-SKI sorts points
 // by stencil cell; others keep the external order), right-hand sides
 // innermost ("RHS-minor": element (r, b) at r*nrhs + b).
+std::uint64_t next_op_uid();
+
 struct Op {
+  Op() : uid(next_op_uid()) {}
   virtual ~Op();
+  const std::uint64_t uid;  // identifies the internal row order (never reused)
   int kind = 0;
   int device = 0;
   i64 N = 0;            // logical size
@@ -131,6 +135,7 @@ struct Op {
   double nv2 = 0.0, ng2 = 0.0;
   std::mutex mu;        // serialises host-API calls that use the scratch below
   cudaStream_t stream = nullptr;  // own stream for host-API calls
+  cudaStream_t cap_stream = nullptr;  // private stream used only for CUDA-graph capture
   DevBuf<double> scratch_a, scratch_b, scratch_c;
   HostBuf pinned;
 

@@ -123,11 +123,20 @@ void cholesky_upper(int k, const double* A, double* R) {
   }
 }
 
-Op::~Op() {
-  if (stream) cudaStreamDestroy(stream);
+std::uint64_t next_op_uid() {
+  static std::atomic<std::uint64_t> counter{1};
+  return counter.fetch_add(1);
 }
 
-void Op::init_stream() { GK_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking)); }
+Op::~Op() {
+  if (stream) cudaStreamDestroy(stream);
+  if (cap_stream) cudaStreamDestroy(cap_stream);
+}
+
+void Op::init_stream() {
+  GK_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  GK_CUDA(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
+}
 
 }  // namespace gk
 

@@ -638,11 +638,15 @@ PcgResult pcg_internal(Op& op, Precond* M, const double* B, double* X, int nrhs,
     // warm the operator's scratch outside capture, then capture ITER iterations
     op.mvm(Pb.p, AP.p, nrhs, s);
     const int ITER = 4;
+    // capture on the operator's private stream (capturing the legacy default
+    // stream is not permitted); the graph is then launched on `s`.
+    GK_CUDA(cudaStreamSynchronize(s));
+    cudaStream_t cs = op.cap_stream;
     const i64 before = g_launches.load();
     cudaGraph_t graph;
-    GK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    for (int i = 0; i < ITER; ++i) iteration(s);
-    GK_CUDA(cudaStreamEndCapture(s, &graph));
+    GK_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < ITER; ++i) iteration(cs);
+    GK_CUDA(cudaStreamEndCapture(cs, &graph));
     const i64 nodes = g_launches.load() - before;
     g_launches.fetch_sub(nodes);
     cudaGraphExec_t exec;
@@ -691,6 +695,8 @@ static void set_smem(const void* fn, size_t bytes) {
 }
 
 void Precond::ensure(int nrhs) {
+  if (nrhs <= ensured_nrhs) return;
+  ensured_nrhs = nrhs;
   partial.reserve(static_cast<size_t>(RB) * k * nrhs);
   t.reserve(static_cast<size_t>(k) * nrhs);
   const size_t sh1 = sizeof(double) * (PC_RT * k + PC_RT * nrhs + k * nrhs);
@@ -700,6 +706,7 @@ void Precond::ensure(int nrhs) {
 }
 
 void Precond::apply(const double* r, double* z, int nrhs, cudaStream_t s) {
+  ensure(nrhs);  // no-op once reserved (and before any graph capture)
   const size_t sh1 = sizeof(double) * (PC_RT * k + PC_RT * nrhs + k * nrhs);
   k_pc_proj<<<RB, RT, sh1, s>>>(r, dinv.p, q1.p, N, int(k), nrhs, partial.p, nullptr);
   launched("precond proj");
@@ -808,7 +815,12 @@ std::unique_ptr<PivChol> pivchol_run(Op& op, bool kernel_part, i64 max_rank, dou
   auto f = std::make_unique<PivChol>();
   f->device = op.device;
   f->N = N;
-  f->op = &op;
+  f->order_uid = op.uid;
+  GK_CUDA(cudaStreamCreateWithFlags(&f->stream, cudaStreamNonBlocking));
+  if (op.d_ext_of_int()) {
+    f->ext_own.alloc(static_cast<size_t>(N));
+    GK_CUDA(cudaMemcpyAsync(f->ext_own.p, op.d_ext_of_int(), sizeof(i64) * N, cudaMemcpyDeviceToDevice, s));
+  }
   max_rank = std::min(max_rank, N);
   if (max_rank < 0) fail(GK_ERR_ARG, "pivoted Cholesky rank must be >= 0");
   DevBuf<double> diag(static_cast<size_t>(N)), noise(static_cast<size_t>(N)), d(static_cast<size_t>(N)), col(static_cast<size_t>(N));
@@ -823,8 +835,9 @@ std::unique_ptr<PivChol> pivchol_run(Op& op, bool kernel_part, i64 max_rank, dou
   launched("pivchol init");
   DevBuf<double> pmin(RB), psum(RB), pmax(RB), stats(5);
   DevBuf<i64> pext(RB), pint(RB);
-  double* sh = nullptr;
-  GK_CUDA(cudaMallocHost(&sh, sizeof(double) * 5));
+  HostBuf pinned;
+  pinned.reserve(5);
+  double* sh = pinned.p;
   auto stats_of_d = [&]() {
     k_pv_stats<<<RB, RT, 0, s>>>(d.p, op.d_ext_of_int(), N, pmin.p, psum.p, pmax.p, pext.p, pint.p);
     launched("pivchol stats");
@@ -834,10 +847,7 @@ std::unique_ptr<PivChol> pivchol_run(Op& op, bool kernel_part, i64 max_rank, dou
     GK_CUDA(cudaStreamSynchronize(s));
   };
   stats_of_d();
-  if (sh[0] < 0.0) {
-    cudaFreeHost(sh);
-    fail(GK_ERR_RUNTIME, "pivoted Cholesky requires a nonnegative diagonal");
-  }
+  if (sh[0] < 0.0) fail(GK_ERR_RUNTIME, "pivoted Cholesky requires a nonnegative diagonal");
   f->initial_trace = sh[1];
   f->residual_trace = sh[1];
   const double scale = std::max(sh[2], 1e-300);
@@ -856,27 +866,27 @@ std::unique_ptr<PivChol> pivchol_run(Op& op, bool kernel_part, i64 max_rank, dou
     f->pivots.push_back(piv_ext);
     // min check before clamping (linalg.cpp:165-167)
     stats_of_d();
-    if (sh[0] < -1e-10 * scale) {
-      const double mn = sh[0];
-      cudaFreeHost(sh);
+    if (sh[0] < -1e-10 * scale)
       fail(GK_ERR_RUNTIME, "pivoted Cholesky: operator is not positive semidefinite (residual diagonal " +
-                               std::to_string(mn) + ")");
-    }
+                               std::to_string(sh[0]) + ")");
     k_pv_clamp<<<blocks_for(N), 256, 0, s>>>(d.p, N, piv_int);
     launched("pivchol clamp");
     stats_of_d();
     f->residual_trace = sh[1];
   }
-  cudaFreeHost(sh);
   f->k = k;
   return f;
+}
+
+PivChol::~PivChol() {
+  if (stream) cudaStreamDestroy(stream);
 }
 
 void pivchol_copy_L(const PivChol& f, double* out_host) {
   if (f.k == 0) return;
   DevBuf<double> tmp(static_cast<size_t>(f.N * f.k));
-  cudaStream_t s = f.op->stream;
-  k_perm_cols_out<<<blocks_for(f.N * f.k), 256, 0, s>>>(f.L.p, f.op->d_ext_of_int(), f.N, int(f.k), tmp.p);
+  cudaStream_t s = f.stream;
+  k_perm_cols_out<<<blocks_for(f.N * f.k), 256, 0, s>>>(f.L.p, f.ext_own.p, f.N, int(f.k), tmp.p);
   launched("pivchol permute");
   GK_CUDA(cudaMemcpyAsync(out_host, tmp.p, sizeof(double) * f.N * f.k, cudaMemcpyDeviceToHost, s));
   GK_CUDA(cudaStreamSynchronize(s));

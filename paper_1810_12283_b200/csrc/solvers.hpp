@@ -17,10 +17,15 @@ struct Precond {
   DevBuf<double> partial;  // [kRedBlocks][k][nrhs] scratch
   DevBuf<double> t;        // [k][nrhs]
   DevBuf<double> cbuf;     // scratch
-  const i64* ext = nullptr;  // operator row map used when q1 was built (null = identity)
-  std::vector<i64> int_of_ext_h;  // empty = identity
+  // Row order of q1/dinv: the internal order of operator `order_uid`
+  // (0 = external order). `ext` points at this object's own copy of that
+  // operator's internal->external row map, so it outlives the operator.
+  std::uint64_t order_uid = 0;
+  DevBuf<i64> ext_own;
+  const i64* ext = nullptr;
   cudaStream_t stream = nullptr;
   std::mutex mu;
+  int ensured_nrhs = 0;
   ~Precond();
   // z = M^{-1} r; optionally rz[b] partials. All internal layout.
   void apply(const double* r, double* z, int nrhs, cudaStream_t s);
@@ -33,7 +38,11 @@ struct PivChol {
   DevBuf<double> L;  // [k][N] column-major, internal row order
   std::vector<i64> pivots;  // external indices
   double initial_trace = 0, residual_trace = 0;
-  const Op* op = nullptr;
+  // owned copies so the factor outlives its operator
+  std::uint64_t order_uid = 0;
+  DevBuf<i64> ext_own;  // internal -> external row map (empty = identity)
+  cudaStream_t stream = nullptr;
+  ~PivChol();
 };
 
 struct PcgResult {

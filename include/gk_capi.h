@@ -105,6 +105,14 @@ gk_status gk_dskip_create(const gk_kernel* kernel, const double* X, int64_t n, i
                           double noise_value, double noise_gradient, const gk_dskip_config* cfg,
                           int device, gk_op** out);
 
+/* D-SKIP operator from explicit Lanczos factors (one or two; Q_f N×r_f
+ * column-major, alpha_f r_f, beta_f r_f-1) — the Hadamard MVM/diagonal/row of
+ * dskip.cpp:236-264 over factors built elsewhere (e.g. by the reference). */
+gk_status gk_dskip_create_from_factors(int64_t n, int groups, double noise_value, double noise_gradient,
+                                       int nfactors, const int64_t* ranks, const double* const* Q,
+                                       const double* const* alpha, const double* const* beta, int device,
+                                       gk_op** out);
+
 /* DenseOperator(A) (linear_operator.hpp:38-56); A is N×N column-major. */
 gk_status gk_dense_create(const double* A, int64_t N, int device, gk_op** out);
 

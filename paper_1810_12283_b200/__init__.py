@@ -66,6 +66,8 @@ _SIGS = {
     "gk_dskip_create": (C.c_int, [C.POINTER(GkKernel), _dp, _i64, C.c_int, _d, _d,
                                   C.POINTER(GkDskipConfig), C.c_int, C.POINTER(_vp)]),
     "gk_dense_create": (C.c_int, [_dp, _i64, C.c_int, C.POINTER(_vp)]),
+    "gk_dskip_create_from_factors": (C.c_int, [_i64, C.c_int, _d, _d, C.c_int, _i64p, C.POINTER(_dp),
+                                               C.POINTER(_dp), C.POINTER(_dp), C.c_int, C.POINTER(_vp)]),
     "gk_exact_create": (C.c_int, [C.POINTER(GkKernel), _dp, _i64, C.c_int, _d, _d, C.c_int, C.c_int,
                                   C.POINTER(_vp)]),
     "gk_op_destroy": (None, [_vp]),
@@ -437,6 +439,25 @@ class DskipOperator(LinearOperator):
         k = kernel.c()
         super().__init__(_create(_lib.gk_dskip_create, C.byref(k), _p(X), self.n, self.d,
                                  float(noise[0]), float(noise[1]), C.byref(cfg), device), device)
+
+    @staticmethod
+    def from_factors(factors, n, groups, noise=(0.0, 0.0), device=0):
+        """D-SKIP operator over given Lanczos factors [(Q, alpha, beta), ...]
+        (one or two; e.g. built by the reference/oracle)."""
+        op = DskipOperator.__new__(DskipOperator)
+        op.n, op.d = n, groups
+        nf = len(factors)
+        Qs = [np.asfortranarray(np.asarray(f[0], dtype=np.float64)) for f in factors]
+        As = [_f64(f[1]) for f in factors]
+        Bs = [_f64(f[2]) if np.asarray(f[2]).size else np.zeros(1) for f in factors]
+        ranks = (_i64 * nf)(*[q.shape[1] for q in Qs])
+        arr = lambda xs: (_dp * nf)(*[_p(x) for x in xs])  # noqa: E731
+        h = _vp()
+        _check(_lib.gk_dskip_create_from_factors(n, groups, float(noise[0]), float(noise[1]), nf, ranks,
+                                                 arr(Qs), arr(As), arr(Bs), device, C.byref(h)))
+        LinearOperator.__init__(op, h, device)
+        op._keep = (Qs, As, Bs)
+        return op
 
     def factors(self):
         out = []

@@ -19,6 +19,9 @@ std::unique_ptr<Op> make_dski(const gk_kernel& k, const gk_grid& g, const double
 std::unique_ptr<Op> make_exact(const gk_kernel& k, const double* X, i64 n, int d, double nv, double ng,
                                int with_grad, int device);
 std::unique_ptr<Op> make_dense(const double* A, i64 N, int device);
+std::unique_ptr<Op> make_dskip_from_factors(i64 n, int groups, double nv, double ng, int nf, const i64* ranks,
+                                            const double* const* Q, const double* const* alpha,
+                                            const double* const* beta, int device);
 std::unique_ptr<Op> make_dskip(const gk_kernel& k, const double* X, i64 n, int d, double nv, double ng,
                                const gk_dskip_config& cfg, int device);
 int64_t dski_grid_size(const Op& o);
@@ -187,6 +190,16 @@ gk_status gk_dskip_create(const gk_kernel* kernel, const double* X, int64_t n, i
   return guard([&] {
     auto h = std::make_unique<gk_op>();
     h->impl = make_dskip(*kernel, X, n, d, nv, ng, *cfg, device);
+    *out = h.release();
+  });
+}
+
+gk_status gk_dskip_create_from_factors(int64_t n, int groups, double nv, double ng, int nf, const int64_t* ranks,
+                                       const double* const* Q, const double* const* alpha,
+                                       const double* const* beta, int device, gk_op** out) {
+  return guard([&] {
+    auto h = std::make_unique<gk_op>();
+    h->impl = make_dskip_from_factors(n, groups, nv, ng, nf, ranks, Q, alpha, beta, device);
     *out = h.release();
   });
 }

@@ -618,8 +618,23 @@ void DskiOp::row(i64 r_ext, double* out, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------- creation
+// profile 0: SE value; profile 1: d/dlog(ell) of the SE profile
+// (kernel_dlogell_profile, dski.cpp:36-40) — separable only for d = 1, which
+// is all the D-SKIP leaves need (dskip.cpp:171).
+std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, const double* X, i64 n,
+                                      double nv, double ng, int order, int with_grad, int device,
+                                      int profile);
+
 std::unique_ptr<Op> make_dski(const gk_kernel& k, const gk_grid& g, const double* X, i64 n,
                               double nv, double ng, int order, int with_grad, int device) {
+  return make_dski_profile(k, g, X, n, nv, ng, order, with_grad, device, 0);
+}
+
+std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, const double* X, i64 n,
+                                      double nv, double ng, int order, int with_grad, int device,
+                                      int profile) {
+  if (profile == 1 && g.d != 1)
+    fail(GK_ERR_UNSUPPORTED, "the d/dlog(ell) grid profile is implemented for 1-D grids only");
   if (k.family != 0)
     fail(GK_ERR_UNSUPPORTED,
          "D-SKI on B200 implements the separable squared-exponential profile; the spline "
@@ -702,18 +717,21 @@ std::unique_ptr<Op> make_dski(const gk_kernel& k, const gk_grid& g, const double
   for (int j = 0; j < d; ++j) {
     op->toff_h[static_cast<size_t>(j)] = int(tv.size());
     int band = g.dims[j];
+    double peak = 0.0;
     for (int kk = 0; kk < g.dims[j]; ++kk) {
       const double o = kk * g.spacing[j];
       double val = std::exp(-0.5 * o * o / ell2);
       if (j == 0) val *= k.outputscale * k.outputscale;
+      if (profile == 1) val *= o * o / ell2;  // SE: dk/dlog(ell) = k ρ² (kernels.cpp:172-181)
       tv.push_back(val);
+      peak = std::max(peak, std::fabs(val));
     }
-    // numerical band: entries below 1e-30 of the peak contribute far below
-    // fp64 roundoff of the product and are skipped tile-wise.
-    const double peak = tv[static_cast<size_t>(op->toff_h[static_cast<size_t>(j)])];
-    for (int kk = 1; kk < g.dims[j]; ++kk)
-      if (tv[static_cast<size_t>(op->toff_h[static_cast<size_t>(j)] + kk)] < 1e-30 * peak) {
-        band = kk;
+    // numerical band: beyond the peak the profile decays monotonically; entries
+    // below 1e-30 of the peak contribute far below fp64 roundoff of the
+    // product and are skipped tile-wise.
+    for (int kk = g.dims[j] - 1; kk >= 0; --kk)
+      if (std::fabs(tv[static_cast<size_t>(op->toff_h[static_cast<size_t>(j)] + kk)]) >= 1e-30 * peak) {
+        band = kk + 1;
         break;
       }
     op->band[static_cast<size_t>(j)] = band;
@@ -748,6 +766,15 @@ int64_t dski_grid_size(const Op& o) {
 gk_grid dski_grid(const Op& o) {
   if (o.kind != KIND_DSKI) fail(GK_ERR_ARG, "operator is not a D-SKI operator");
   return static_cast<const DskiOp&>(o).grid;
+}
+
+// B K_UU B^T without the noise diagonal (internal layout), for D-SKIP leaves.
+void dski_mvm_nonoise(Op& o, const double* in, double* out, int nrhs, cudaStream_t s) {
+  auto& op = static_cast<DskiOp&>(o);
+  op.ensure_scratch(nrhs);
+  op.scatter(in, op.grid_u.p, nrhs, s);
+  op.kuu(op.grid_u.p, op.grid_w.p, nrhs, s);
+  op.gather(op.grid_w.p, in, out, nrhs, false, s);
 }
 
 // Scatter with grid output (internal V -> grid U), grid K_UU and gather w/o noise.

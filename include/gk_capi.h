@@ -49,6 +49,9 @@ const char* gk_last_error(void);
 /* Index of the offending point after GK_ERR_OUT_OF_GRID, else -1. */
 int64_t gk_last_error_point(void);
 const char* gk_version(void);
+/* Kernel-variant selection for tuning/A-B timing (process-wide). Keys:
+ * "scatter", "gather", "toeplitz" (0 = default choice). Returns the old value. */
+int gk_set_tuning(const char* key, int value);
 /* Number of CUDA kernels this library has launched in this process. */
 int64_t gk_kernel_launch_count(void);
 

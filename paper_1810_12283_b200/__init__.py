@@ -56,6 +56,7 @@ _SIGS = {
     "gk_last_error": (C.c_char_p, []),
     "gk_last_error_point": (_i64, []),
     "gk_version": (C.c_char_p, []),
+    "gk_set_tuning": (C.c_int, [C.c_char_p, C.c_int]),
     "gk_kernel_launch_count": (_i64, []),
     "gk_grid_cover": (C.c_int, [_dp, _i64, C.c_int, _d, C.c_int, C.c_int, C.POINTER(GkGrid)]),
     "gk_mix_seed": (_u64, [_u64, _u64]),
@@ -166,6 +167,11 @@ def version() -> str:
     return _lib.gk_version().decode()
 
 
+def set_tuning(key: str, value: int) -> int:
+    """Select a kernel variant ("scatter", "gather", "toeplitz"; 0 = default)."""
+    return int(_lib.gk_set_tuning(key.encode(), int(value)))
+
+
 # ------------------------------------------------------------------ rng (rng.hpp:12-38)
 def mix_seed(seed, stream):
     return int(_lib.gk_mix_seed(seed, stream))
@@ -259,7 +265,7 @@ class LinearOperator:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and _lib is not None:
             _lib.gk_op_destroy(h)
             self._h = None
 

@@ -142,6 +142,15 @@ int64_t gk_last_error_point(void) { return g_err_point; }
 const char* gk_version(void) { return "gk_b200 0.1 (sm_100a)"; }
 int64_t gk_kernel_launch_count(void) { return g_launches.load(); }
 
+int gk_set_tuning(const char* key, int value) {
+  const std::string k = key ? key : "";
+  std::atomic<int>* slot = k == "scatter" ? &g_tuning.scatter
+                           : k == "gather" ? &g_tuning.gather
+                           : k == "toeplitz" ? &g_tuning.toeplitz
+                                             : nullptr;
+  return slot ? slot->exchange(value) : -1;
+}
+
 gk_status gk_grid_cover(const double* X, int64_t n, int d, double target, int margin, int max_nodes,
                         gk_grid* out) {
   return guard([&] {  // interpolation.cpp:117-146

@@ -102,6 +102,7 @@ struct DskiView {
   i64 n, M;
   const int4* base;      // [n] sorted
   const double* wts;     // [n][d][2][T]
+  const double2* wd;     // [n][d][T] (w, dw) pairs: one 16-byte load per tap
   const int* cell_start; // [ncells + 1]
   double nv2, ng2;
 };
@@ -284,6 +285,424 @@ __global__ void __launch_bounds__(256) k_gather(DskiView op, const double* __res
       if (noise) val += (g == 0 ? op.nv2 : op.ng2) * __ldg(v + idx);
       out[idx] = val;
     }
+  }
+}
+
+// ---------------------------------------------------------------- lean kernels
+// 2-D thread blocks: x = right-hand sides (lanes), y = nodes/points. One item
+// per thread, 32-bit index math, no per-item divisions by nrhs; for nrhs ≥ 32
+// a warp is one node/point × 32 RHS, so all control flow is warp-uniform and
+// stencil loads are broadcasts.
+template <int D, int T, bool GRAD>
+__global__ void __launch_bounds__(256) k_scatter_lean(DskiView op, const double* __restrict__ v,
+                                                      double* __restrict__ u, int nrhs) {
+  const int node = blockIdx.x * blockDim.y + threadIdx.y;
+  const int b = blockIdx.y * blockDim.x + threadIdx.x;
+  if (node >= op.M || b >= nrhs) return;
+  constexpr int REC = D * 2 * T;
+  int k[3];
+  {
+    int rem = node;
+#pragma unroll
+    for (int j = D - 1; j >= 0; --j) {
+      k[j] = rem % op.m[j];
+      rem /= op.m[j];
+    }
+  }
+  const int kl = k[D - 1];
+  const int lo = max(0, kl - (T - 1)), hi = min(op.nb[D - 1] - 1, kl);
+  const size_t gstride = (size_t)op.n * nrhs;
+  const double* vb = v + b;
+  double acc = 0.0;
+  if (lo <= hi) {
+    constexpr int LEAD = (D == 1) ? 1 : (D == 2 ? T : T * T);
+#pragma unroll 1
+    for (int lc = 0; lc < LEAD; ++lc) {
+      int t0 = 0, t1 = 0, crow = 0;
+      if constexpr (D >= 2) {
+        t0 = (D == 2) ? lc : lc / T;
+        const int b0 = k[0] - t0;
+        if (b0 < 0 || b0 >= op.nb[0]) continue;
+        crow = b0;
+        if constexpr (D == 3) {
+          t1 = lc % T;
+          const int b1 = k[1] - t1;
+          if (b1 < 0 || b1 >= op.nb[1]) continue;
+          crow = crow * op.nb[1] + b1;
+        }
+      }
+      const int cb = crow * op.nb[D - 1];
+      const int s_lo = __ldg(op.cell_start + cb + lo);
+      const int s_hi = __ldg(op.cell_start + cb + hi + 1);
+      // two points per iteration: both points' loads are in flight together
+      auto contrib = [&](int s) -> double {
+        const double* rec = op.wts + (size_t)s * REC;
+        const int4 bs = __ldg(op.base + s);
+        const int tl = kl - (D == 1 ? bs.x : (D == 2 ? bs.y : bs.z));
+        const double* vs = vb + (size_t)s * nrhs;
+        const double v0 = __ldg(vs);
+        if constexpr (D == 1) {
+          double r = __ldg(rec + tl) * v0;
+          if constexpr (GRAD) r += __ldg(rec + T + tl) * __ldg(vs + gstride);
+          return r;
+        } else if constexpr (D == 2) {
+          const double w0 = __ldg(rec + t0), w1 = __ldg(rec + 2 * T + tl);
+          if constexpr (GRAD) {
+            const double dw0 = __ldg(rec + T + t0), dw1 = __ldg(rec + 3 * T + tl);
+            const double v1 = __ldg(vs + gstride), v2 = __ldg(vs + 2 * gstride);
+            return w1 * (v0 * w0 + v1 * dw0) + dw1 * (v2 * w0);
+          } else {
+            return w0 * w1 * v0;
+          }
+        } else {
+          const double w0 = __ldg(rec + t0), w1 = __ldg(rec + 2 * T + t1), w2 = __ldg(rec + 4 * T + tl);
+          if constexpr (GRAD) {
+            const double dw0 = __ldg(rec + T + t0), dw1 = __ldg(rec + 3 * T + t1), dw2 = __ldg(rec + 5 * T + tl);
+            const double v1 = __ldg(vs + gstride), v2 = __ldg(vs + 2 * gstride), v3 = __ldg(vs + 3 * gstride);
+            return w2 * (w1 * (v0 * w0 + v1 * dw0) + dw1 * (v2 * w0)) + dw2 * (w1 * (v3 * w0));
+          } else {
+            return w0 * w1 * w2 * v0;
+          }
+        }
+      };
+      int s = s_lo;
+      for (; s + 1 < s_hi; s += 2) {
+        const double c0 = contrib(s);
+        const double c1 = contrib(s + 1);
+        acc += c0;
+        acc += c1;
+      }
+      if (s < s_hi) acc += contrib(s);
+    }
+  }
+  u[(size_t)node * nrhs + b] = acc;
+}
+
+template <int D, int T, bool GRAD>
+__global__ void __launch_bounds__(256) k_gather_lean(DskiView op, const double* __restrict__ w,
+                                                     const double* __restrict__ v, double* __restrict__ out,
+                                                     int nrhs, int noise) {
+  const int s = blockIdx.x * blockDim.y + threadIdx.y;
+  const int b = blockIdx.y * blockDim.x + threadIdx.x;
+  if (s >= op.n || b >= nrhs) return;
+  constexpr int REC = D * 2 * T;
+  const double* rec = op.wts + (size_t)s * REC;
+  const int4 bs = __ldg(op.base + s);
+  double o[D + 1];
+#pragma unroll
+  for (int g = 0; g <= D; ++g) o[g] = 0.0;
+  if constexpr (D == 1) {
+    const double* wr = w + (size_t)bs.x * nrhs + b;
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const double uu = __ldg(wr + (size_t)t * nrhs);
+      o[0] += __ldg(rec + t) * uu;
+      if constexpr (GRAD) o[1] += __ldg(rec + T + t) * uu;
+    }
+  } else if constexpr (D == 2) {
+    const size_t rs = (size_t)op.m[1] * nrhs;
+    const double* wr = w + ((size_t)bs.x * op.m[1] + bs.y) * nrhs + b;
+    double uu[T][T];
+#pragma unroll
+    for (int t0 = 0; t0 < T; ++t0)
+#pragma unroll
+      for (int t1 = 0; t1 < T; ++t1) uu[t0][t1] = __ldg(wr + t0 * rs + (size_t)t1 * nrhs);
+#pragma unroll
+    for (int t0 = 0; t0 < T; ++t0) {
+      double r = 0.0, q = 0.0;
+#pragma unroll
+      for (int t1 = 0; t1 < T; ++t1) {
+        r += __ldg(rec + 2 * T + t1) * uu[t0][t1];
+        if constexpr (GRAD) q += __ldg(rec + 3 * T + t1) * uu[t0][t1];
+      }
+      const double w0 = __ldg(rec + t0);
+      o[0] += w0 * r;
+      if constexpr (GRAD) {
+        o[1] += __ldg(rec + T + t0) * r;
+        o[2] += w0 * q;
+      }
+    }
+  } else {
+    const size_t rs2 = (size_t)op.m[2] * nrhs, rs1 = (size_t)op.m[1] * rs2;
+    const double* wbase = w + (((size_t)bs.x * op.m[1] + bs.y) * op.m[2] + bs.z) * nrhs + b;
+#pragma unroll 1
+    for (int t0 = 0; t0 < T; ++t0) {
+      double R0 = 0.0, R1 = 0.0, R2 = 0.0;
+#pragma unroll
+      for (int t1 = 0; t1 < T; ++t1) {
+        const double* wr = wbase + t0 * rs1 + t1 * rs2;
+        double uu[T];
+#pragma unroll
+        for (int t2 = 0; t2 < T; ++t2) uu[t2] = __ldg(wr + (size_t)t2 * nrhs);
+        double r = 0.0, q = 0.0;
+#pragma unroll
+        for (int t2 = 0; t2 < T; ++t2) {
+          r += __ldg(rec + 4 * T + t2) * uu[t2];
+          if constexpr (GRAD) q += __ldg(rec + 5 * T + t2) * uu[t2];
+        }
+        const double w1 = __ldg(rec + 2 * T + t1);
+        R0 += w1 * r;
+        if constexpr (GRAD) {
+          R1 += __ldg(rec + 3 * T + t1) * r;
+          R2 += w1 * q;
+        }
+      }
+      const double w0 = __ldg(rec + t0);
+      o[0] += w0 * R0;
+      if constexpr (GRAD) {
+        o[1] += __ldg(rec + T + t0) * R0;
+        o[2] += w0 * R1;
+        o[3] += w0 * R2;
+      }
+    }
+  }
+  constexpr int NG = GRAD ? D + 1 : 1;
+  const size_t gstride = (size_t)op.n * nrhs;
+  const size_t idx0 = (size_t)s * nrhs + b;
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
+    const size_t idx = idx0 + g * gstride;
+    double val = o[g];
+    if (noise) val += (g == 0 ? op.nv2 : op.ng2) * __ldg(v + idx);
+    out[idx] = val;
+  }
+}
+
+// Scatter v2: iterate candidate CELLS (base1 known from the cell index, so no
+// dependent per-point base load) and read each tap's (w, dw) pair with one
+// 16-byte load.
+template <int D, int T, bool GRAD>
+__global__ void __launch_bounds__(256) k_scatter_cells(DskiView op, const double* __restrict__ v,
+                                                       double* __restrict__ u, int nrhs) {
+  const int node = blockIdx.x * blockDim.y + threadIdx.y;
+  const int b = blockIdx.y * blockDim.x + threadIdx.x;
+  if (node >= op.M || b >= nrhs) return;
+  int k[3];
+  {
+    int rem = node;
+#pragma unroll
+    for (int j = D - 1; j >= 0; --j) {
+      k[j] = rem % op.m[j];
+      rem /= op.m[j];
+    }
+  }
+  const int kl = k[D - 1];
+  const int lo = max(0, kl - (T - 1)), hi = min(op.nb[D - 1] - 1, kl);
+  const size_t gstride = (size_t)op.n * nrhs;
+  const double* vb = v + b;
+  double acc = 0.0;
+  if (lo <= hi) {
+    constexpr int LEAD = (D == 1) ? 1 : (D == 2 ? T : T * T);
+#pragma unroll 1
+    for (int lc = 0; lc < LEAD; ++lc) {
+      int t0 = 0, t1 = 0, crow = 0;
+      if constexpr (D >= 2) {
+        t0 = (D == 2) ? lc : lc / T;
+        const int b0 = k[0] - t0;
+        if (b0 < 0 || b0 >= op.nb[0]) continue;
+        crow = b0;
+        if constexpr (D == 3) {
+          t1 = lc % T;
+          const int b1 = k[1] - t1;
+          if (b1 < 0 || b1 >= op.nb[1]) continue;
+          crow = crow * op.nb[1] + b1;
+        }
+      }
+      const int* cs = op.cell_start + crow * op.nb[D - 1];
+      int s = __ldg(cs + lo);
+#pragma unroll 1
+      for (int c = lo; c <= hi; ++c) {
+        const int s_end = __ldg(cs + c + 1);
+        const int tl = kl - c;
+        for (; s < s_end; ++s) {
+          const double2* wd = op.wd + (size_t)s * (D * T);
+          const double* vs = vb + (size_t)s * nrhs;
+          const double v0 = __ldg(vs);
+          if constexpr (D == 1) {
+            const double2 a = __ldg(wd + tl);
+            acc += a.x * v0;
+            if constexpr (GRAD) acc += a.y * __ldg(vs + gstride);
+          } else if constexpr (D == 2) {
+            const double2 a0 = __ldg(wd + t0), a1 = __ldg(wd + T + tl);
+            if constexpr (GRAD) {
+              const double v1 = __ldg(vs + gstride), v2 = __ldg(vs + 2 * gstride);
+              acc += a1.x * (v0 * a0.x + v1 * a0.y) + a1.y * (v2 * a0.x);
+            } else {
+              acc += a0.x * a1.x * v0;
+            }
+          } else {
+            const double2 a0 = __ldg(wd + t0), a1 = __ldg(wd + T + t1), a2 = __ldg(wd + 2 * T + tl);
+            if constexpr (GRAD) {
+              const double v1 = __ldg(vs + gstride), v2 = __ldg(vs + 2 * gstride), v3 = __ldg(vs + 3 * gstride);
+              acc += a2.x * (a1.x * (v0 * a0.x + v1 * a0.y) + a1.y * (v2 * a0.x)) + a2.y * (a1.x * (v3 * a0.x));
+            } else {
+              acc += a0.x * a1.x * a2.x * v0;
+            }
+          }
+        }
+      }
+    }
+  }
+  u[(size_t)node * nrhs + b] = acc;
+}
+
+// ---------------------------------------------------------------- d = 2 band kernels
+// Gather B w (+ noise) with the grid rows a band of points needs staged in
+// shared memory. CTA = (R base rows of points, chunk of BC right-hand sides).
+// Points are sorted by (base0, base1), so the band's points are one
+// contiguous range; their stencil records are staged in chunks of PCH.
+constexpr int G2_R = 2, G2_PCH = 128;
+template <int T, bool GRAD>
+__global__ void __launch_bounds__(256) k_gather2d(DskiView op, const double* __restrict__ w,
+                                                  const double* __restrict__ v, double* __restrict__ out,
+                                                  int nrhs, int BC, int noise) {
+  extern __shared__ double sm[];
+  constexpr int PW = 4 * T;  // w0, dw0, w1, dw1
+  const int m1 = op.m[1];
+  const int row_lo = blockIdx.x * G2_R;
+  const int row_hi = min(row_lo + G2_R, op.nb[0]);
+  const int nrows = row_hi - row_lo + T - 1;
+  const int b0 = blockIdx.y * BC;
+  const int bc = min(BC, nrhs - b0);
+  double* Wt = sm;                                  // [nrows][m1][BC]
+  double* Pw = Wt + (size_t)nrows * m1 * BC;        // [PCH][PW]
+  int* Pb = reinterpret_cast<int*>(Pw + G2_PCH * PW);  // [PCH][2]
+  const int tid = threadIdx.x;
+  const int tile = nrows * m1 * bc;
+  for (int e = tid; e < tile; e += blockDim.x) {
+    const int bb = e % bc;
+    const int node = e / bc;  // (row, col) within the tile
+    Wt[node * BC + bb] = __ldg(w + ((i64)row_lo * m1 + node) * nrhs + b0 + bb);
+  }
+  const int S0 = __ldg(op.cell_start + (i64)row_lo * op.nb[1]);
+  const int S1 = __ldg(op.cell_start + (i64)row_hi * op.nb[1]);
+  for (int c0 = S0; c0 < S1; c0 += G2_PCH) {
+    const int cnt = min(G2_PCH, S1 - c0);
+    __syncthreads();
+    for (int e = tid; e < cnt * PW; e += blockDim.x) {
+      const int p = e / PW, k = e % PW;
+      // record layout [axis][w|dw][T]: axis0 w, axis0 dw, axis1 w, axis1 dw
+      Pw[e] = __ldg(op.wts + (i64)(c0 + p) * (2 * 2 * T) + k);
+    }
+    for (int p = tid; p < cnt; p += blockDim.x) {
+      const int4 b4 = __ldg(op.base + c0 + p);
+      Pb[2 * p] = b4.x - row_lo;
+      Pb[2 * p + 1] = b4.y;
+    }
+    __syncthreads();
+    for (int it = tid; it < cnt * bc; it += blockDim.x) {
+      const int p = it / bc, bb = it % bc;
+      const double* pw = Pw + p * PW;
+      const double* wr = Wt + ((size_t)Pb[2 * p] * m1 + Pb[2 * p + 1]) * BC + bb;
+      double o0 = 0.0, o1 = 0.0, o2 = 0.0;
+#pragma unroll
+      for (int t0 = 0; t0 < T; ++t0) {
+        double r = 0.0, q = 0.0;
+#pragma unroll
+        for (int t1 = 0; t1 < T; ++t1) {
+          const double uu = wr[(t0 * m1 + t1) * BC];
+          r += pw[2 * T + t1] * uu;
+          if constexpr (GRAD) q += pw[3 * T + t1] * uu;
+        }
+        o0 += pw[t0] * r;
+        if constexpr (GRAD) {
+          o1 += pw[T + t0] * r;
+          o2 += pw[t0] * q;
+        }
+      }
+      const i64 s = c0 + p;
+      const int b = b0 + bb;
+      i64 idx = s * nrhs + b;
+      out[idx] = o0 + (noise ? op.nv2 * __ldg(v + idx) : 0.0);
+      if constexpr (GRAD) {
+        idx = ((i64)op.n + s) * nrhs + b;
+        out[idx] = o1 + (noise ? op.ng2 * __ldg(v + idx) : 0.0);
+        idx = (2 * (i64)op.n + s) * nrhs + b;
+        out[idx] = o2 + (noise ? op.ng2 * __ldg(v + idx) : 0.0);
+      }
+    }
+  }
+}
+
+// Scatter B^T v by grid row: CTA = (node row a, chunk of BC right-hand sides).
+// For each of the T base rows b0 that reach row a (t0 = a - b0 fixed), the
+// row's points are staged with their combined row factors
+//   P = v0 w0[t0] + v1 dw0[t0],  Q = v2 w0[t0]
+// and each (node column, rhs) item sums w1[t1] P + dw1[t1] Q over the points
+// whose base1 covers it — deterministic order, no atomics.
+constexpr int S2_ITEMS = 8;
+template <int T, bool GRAD>
+__global__ void __launch_bounds__(256) k_scatter2d(DskiView op, const double* __restrict__ v,
+                                                   double* __restrict__ u, int nrhs, int BC, int max_row_pts) {
+  extern __shared__ double sm[];
+  const int m1 = op.m[1];
+  const int a = blockIdx.x;
+  const int b0 = blockIdx.y * BC;
+  const int bc = min(BC, nrhs - b0);
+  const int NQ = GRAD ? 2 : 1;
+  double* W1 = sm;                                   // [max_row_pts][2T]  (w1, dw1)
+  double* PQ = W1 + (size_t)max_row_pts * 2 * T;     // [max_row_pts][NQ][BC]
+  int* B1 = reinterpret_cast<int*>(PQ + (size_t)max_row_pts * NQ * BC);  // [max_row_pts]
+  const int tid = threadIdx.x;
+  const int items = m1 * bc;
+  double acc[S2_ITEMS];
+#pragma unroll
+  for (int k = 0; k < S2_ITEMS; ++k) acc[k] = 0.0;
+  const int brow_lo = max(0, a - (T - 1)), brow_hi = min(op.nb[0] - 1, a);
+  for (int br = brow_lo; br <= brow_hi; ++br) {
+    const int t0 = a - br;
+    const i64 cbase = (i64)br * op.nb[1];
+    const int S0 = __ldg(op.cell_start + cbase);
+    const int S1 = __ldg(op.cell_start + cbase + op.nb[1]);
+    const int cnt = S1 - S0;
+    __syncthreads();
+    for (int e = tid; e < cnt * 2 * T; e += blockDim.x) {
+      const int p = e / (2 * T), k = e % (2 * T);
+      W1[e] = __ldg(op.wts + (i64)(S0 + p) * (2 * 2 * T) + 2 * T + k);
+    }
+    for (int e = tid; e < cnt * bc; e += blockDim.x) {
+      const int p = e / bc, bb = e % bc;
+      const i64 s = S0 + p;
+      const double* pw = op.wts + s * (2 * 2 * T);
+      const double w0 = __ldg(pw + t0);
+      const double v0 = __ldg(v + s * nrhs + b0 + bb);
+      if constexpr (GRAD) {
+        const double dw0 = __ldg(pw + T + t0);
+        const double v1 = __ldg(v + ((i64)op.n + s) * nrhs + b0 + bb);
+        const double v2 = __ldg(v + (2 * (i64)op.n + s) * nrhs + b0 + bb);
+        PQ[(p * 2) * BC + bb] = v0 * w0 + v1 * dw0;
+        PQ[(p * 2 + 1) * BC + bb] = v2 * w0;
+      } else {
+        PQ[p * BC + bb] = v0 * w0;
+      }
+    }
+    for (int p = tid; p < cnt; p += blockDim.x) B1[p] = __ldg(op.base + S0 + p).y;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < S2_ITEMS; ++k) {
+      const int it = tid + k * blockDim.x;
+      if (it >= items) break;
+      const int c = it / bc, bb = it % bc;
+      const int lo = max(0, c - (T - 1)), hi = min(op.nb[1] - 1, c);
+      if (lo > hi) continue;
+      const int p_lo = __ldg(op.cell_start + cbase + lo) - S0;
+      const int p_hi = __ldg(op.cell_start + cbase + hi + 1) - S0;
+      double s = 0.0;
+      for (int p = p_lo; p < p_hi; ++p) {
+        const int t1 = c - B1[p];
+        const double* w1 = W1 + p * 2 * T;
+        if constexpr (GRAD) s += w1[t1] * PQ[(p * 2) * BC + bb] + w1[T + t1] * PQ[(p * 2 + 1) * BC + bb];
+        else s += w1[t1] * PQ[p * BC + bb];
+      }
+      acc[k] += s;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < S2_ITEMS; ++k) {
+    const int it = tid + k * blockDim.x;
+    if (it >= items) break;
+    const int c = it / bc, bb = it % bc;
+    u[((i64)a * m1 + c) * nrhs + b0 + bb] = acc[k];
   }
 }
 
@@ -484,11 +903,13 @@ struct DskiOp final : Op {
   gk_kernel kernel{};
   DevBuf<int4> base;
   DevBuf<double> wts;
+  DevBuf<double2> wd;
   DevBuf<int> cell_start;
   DevBuf<double> tvec;  // concatenated per-axis Toeplitz sequences (axis 0 carries s²)
   DevBuf<int> toff;
   std::vector<int> toff_h;
   std::vector<int> band;  // per-axis numerical band of the Toeplitz sequence
+  int max_row_pts = 0;    // d = 2: most points sharing one base row (band kernels' staging)
   DevBuf<i64> ext;        // internal row -> external row
   std::vector<i64> perm_h, inv_h;
   DevBuf<double> origin_d, h_d;
@@ -507,6 +928,7 @@ struct DskiOp final : Op {
     v.M = M;
     v.base = base.p;
     v.wts = wts.p;
+    v.wd = wd.p;
     v.cell_start = cell_start.p;
     v.nv2 = nv2;
     v.ng2 = ng2;
@@ -520,6 +942,8 @@ struct DskiOp final : Op {
   }
 
   void scatter(const double* v, double* u, int nrhs, cudaStream_t s) const;
+  bool scatter_band(const double* v, double* u, int nrhs, cudaStream_t s) const;
+  bool gather_band(const double* w, const double* v, double* out, int nrhs, bool noise, cudaStream_t s) const;
   void kuu(const double* u, double* w, int nrhs, cudaStream_t s) const;
   void gather(const double* w, const double* v, double* out, int nrhs, bool noise, cudaStream_t s) const;
 
@@ -542,6 +966,7 @@ struct DskiOp final : Op {
       case 1: kuu(in, out, nrhs, s); break;
       case 2: gather(in, in, out, nrhs, false, s); break;
       case 3: mvm(in, out, nrhs, s); break;
+      case 4: mvm_graph(in, out, nrhs, s); break;
       default: fail(GK_ERR_ARG, "unknown stage");
     }
   }
@@ -565,25 +990,117 @@ static int grid_blocks(i64 items, int threads = 256) {
   return int(std::max<i64>(1, std::min<i64>(b, 148LL * 16)));
 }
 
+static void smem_attr(const void* fn, size_t bytes) {
+  if (bytes > 48 * 1024) GK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+}
+
+// Lean-kernel launch shape: x = RHS lanes (≤ 32), y = items per block, shrunk
+// (down to one warp) when there are too few items to give every SM ~4 CTAs.
+static dim3 lean_block(int nrhs, i64 items) {
+  const int bx = nrhs >= 32 ? 32 : nrhs;
+  int by = 256 / bx;
+  const i64 lanes_total = items * std::min(nrhs, 32);
+  while (by * bx > 32 && (lanes_total + by * bx - 1) / (by * bx) < 4 * 148) by /= 2;
+  if (by < 1) by = 1;
+  return dim3(static_cast<unsigned>(bx), static_cast<unsigned>(by));
+}
+
+bool DskiOp::scatter_band(const double* v, double* u, int nrhs, cudaStream_t s) const {
+  const DskiView vw = view();
+  const int BC = std::max(1, std::min({nrhs, 256 * S2_ITEMS / m[1], 32}));
+  const int NQ = G ? 2 : 1;
+  const size_t shm = size_t(max_row_pts) * (2 * T + NQ * BC) * sizeof(double) + size_t(max_row_pts) * 4 + 16;
+  if (d != 2 || m[1] > 256 * S2_ITEMS || shm > 200 * 1024) return false;
+  dim3 grid(static_cast<unsigned>(m[0]), static_cast<unsigned>((nrhs + BC - 1) / BC));
+#define GK_S2(TT, GG)                                                                \
+  smem_attr((const void*)k_scatter2d<TT, GG>, shm);                                  \
+  k_scatter2d<TT, GG><<<grid, 256, shm, s>>>(vw, v, u, nrhs, BC, max_row_pts);
+  if (T == 6) {
+    if (G) { GK_S2(6, true) } else { GK_S2(6, false) }
+  } else {
+    if (G) { GK_S2(4, true) } else { GK_S2(4, false) }
+  }
+#undef GK_S2
+  launched("dski scatter (2-D band)");
+  return true;
+}
+
+bool DskiOp::gather_band(const double* w, const double* v, double* out, int nrhs, bool noise,
+                         cudaStream_t s) const {
+  if (d != 2) return false;
+  const DskiView vw = view();
+  const int rows = G2_R + T - 1;
+  const size_t fixed = size_t(G2_PCH) * (4 * T * sizeof(double) + 2 * sizeof(int)) + 16;
+  int BC = std::min(nrhs, 8);
+  while (BC > 1 && size_t(rows) * m[1] * BC * sizeof(double) + fixed > 100 * 1024) --BC;
+  const size_t shm = size_t(rows) * m[1] * BC * sizeof(double) + fixed;
+  if (shm > 200 * 1024) return false;
+  dim3 grid(static_cast<unsigned>((nb[0] + G2_R - 1) / G2_R), static_cast<unsigned>((nrhs + BC - 1) / BC));
+  const int nz = noise ? 1 : 0;
+#define GK_G2(TT, GG)                                                    \
+  smem_attr((const void*)k_gather2d<TT, GG>, shm);                       \
+  k_gather2d<TT, GG><<<grid, 256, shm, s>>>(vw, w, v, out, nrhs, BC, nz);
+  if (T == 6) {
+    if (G) { GK_G2(6, true) } else { GK_G2(6, false) }
+  } else {
+    if (G) { GK_G2(4, true) } else { GK_G2(4, false) }
+  }
+#undef GK_G2
+  launched("dski gather (2-D band)");
+  return true;
+}
+
 void DskiOp::scatter(const double* v, double* u, int nrhs, cudaStream_t s) const {
   const DskiView vw = view();
-  const int blocks = grid_blocks(M * nrhs);
+  const int variant = g_tuning.scatter.load();
+  if (variant == 2 && scatter_band(v, u, nrhs, s)) return;
+  if (variant == 1) {
+    const int blocks = grid_blocks(M * nrhs);
+    GK_DISPATCH_DT(d, T, {
+      if (G) k_scatter<D, T, true><<<blocks, 256, 0, s>>>(vw, v, u, nrhs);
+      else k_scatter<D, T, false><<<blocks, 256, 0, s>>>(vw, v, u, nrhs);
+    });
+    launched("dski scatter");
+    return;
+  }
+  const dim3 blk = lean_block(nrhs, M);
+  const dim3 grid(static_cast<unsigned>((M + blk.y - 1) / blk.y), static_cast<unsigned>((nrhs + blk.x - 1) / blk.x));
+  if (variant == 3) {
+    GK_DISPATCH_DT(d, T, {
+      if (G) k_scatter_cells<D, T, true><<<grid, blk, 0, s>>>(vw, v, u, nrhs);
+      else k_scatter_cells<D, T, false><<<grid, blk, 0, s>>>(vw, v, u, nrhs);
+    });
+    launched("dski scatter (cells)");
+    return;
+  }
   GK_DISPATCH_DT(d, T, {
-    if (G) k_scatter<D, T, true><<<blocks, 256, 0, s>>>(vw, v, u, nrhs);
-    else k_scatter<D, T, false><<<blocks, 256, 0, s>>>(vw, v, u, nrhs);
+    if (G) k_scatter_lean<D, T, true><<<grid, blk, 0, s>>>(vw, v, u, nrhs);
+    else k_scatter_lean<D, T, false><<<grid, blk, 0, s>>>(vw, v, u, nrhs);
   });
-  launched("dski scatter");
+  launched("dski scatter (lean)");
 }
 
 void DskiOp::gather(const double* w, const double* v, double* out, int nrhs, bool noise,
                     cudaStream_t s) const {
   const DskiView vw = view();
-  const int blocks = grid_blocks(n * nrhs);
+  const int variant = g_tuning.gather.load();
+  if (variant == 2 && gather_band(w, v, out, nrhs, noise, s)) return;
+  if (variant == 1) {
+    const int blocks = grid_blocks(n * nrhs);
+    GK_DISPATCH_DT(d, T, {
+      if (G) k_gather<D, T, true><<<blocks, 256, 0, s>>>(vw, w, v, out, nrhs, noise ? 1 : 0);
+      else k_gather<D, T, false><<<blocks, 256, 0, s>>>(vw, w, v, out, nrhs, noise ? 1 : 0);
+    });
+    launched("dski gather");
+    return;
+  }
+  const dim3 blk = lean_block(nrhs, n);
+  const dim3 grid(static_cast<unsigned>((n + blk.y - 1) / blk.y), static_cast<unsigned>((nrhs + blk.x - 1) / blk.x));
   GK_DISPATCH_DT(d, T, {
-    if (G) k_gather<D, T, true><<<blocks, 256, 0, s>>>(vw, w, v, out, nrhs, noise ? 1 : 0);
-    else k_gather<D, T, false><<<blocks, 256, 0, s>>>(vw, w, v, out, nrhs, noise ? 1 : 0);
+    if (G) k_gather_lean<D, T, true><<<grid, blk, 0, s>>>(vw, w, v, out, nrhs, noise ? 1 : 0);
+    else k_gather_lean<D, T, false><<<grid, blk, 0, s>>>(vw, w, v, out, nrhs, noise ? 1 : 0);
   });
-  launched("dski gather");
+  launched("dski gather (lean)");
 }
 
 void DskiOp::kuu(const double* u, double* w, int nrhs, cudaStream_t s) const {
@@ -687,6 +1204,10 @@ std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, cons
     cstart[static_cast<size_t>(c) + 1]++;
   }
   for (i64 c = 0; c < ncells; ++c) cstart[static_cast<size_t>(c) + 1] += cstart[static_cast<size_t>(c)];
+  if (d == 2)
+    for (int br = 0; br < op->nb[0]; ++br)
+      op->max_row_pts = std::max(op->max_row_pts, cstart[static_cast<size_t>(br + 1) * op->nb[1]] -
+                                                      cstart[static_cast<size_t>(br) * op->nb[1]]);
   op->perm_h.assign(static_cast<size_t>(n), 0);
   op->inv_h.assign(static_cast<size_t>(n), 0);
   {
@@ -743,6 +1264,16 @@ std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, cons
   cudaStream_t st = op->stream;
   op->base.upload(base_s.data(), base_s.size(), st);
   op->wts.upload(wts_s.data(), wts_s.size(), st);
+  {
+    std::vector<double2> wd(static_cast<size_t>(n) * d * T);
+    for (i64 q = 0; q < n; ++q)
+      for (int j = 0; j < d; ++j)
+        for (int t = 0; t < T; ++t) {
+          const double* r = &wts_s[static_cast<size_t>(q) * STRIDE + j * 2 * T];
+          wd[(static_cast<size_t>(q) * d + j) * T + t] = make_double2(r[t], r[T + t]);
+        }
+    op->wd.upload(wd.data(), wd.size(), st);
+  }
   op->cell_start.upload(cstart.data(), cstart.size(), st);
   op->tvec.upload(tv.data(), tv.size(), st);
   op->toff.upload(op->toff_h.data(), op->toff_h.size(), st);

@@ -38,8 +38,8 @@ __global__ void k_leaf_combine(const double* __restrict__ in, const i64* __restr
                                int dir, int nrhs, double* __restrict__ bi) {
   const i64 items = n * nrhs;
   for (i64 it = blockIdx.x * (i64)blockDim.x + threadIdx.x; it < items; it += (i64)gridDim.x * blockDim.x) {
-    const int b = int(it % nrhs);
-    const i64 s = it / nrhs;
+    const int b = int(it) % nrhs;
+    const i64 s = int(it) / nrhs;
     const i64 i = ext[s];  // group-0 block of the 1-D operator: ext[s] = perm[s]
     double a = 0.0, da = 0.0;
     for (int g = 0; g <= groups; ++g) {
@@ -57,8 +57,8 @@ __global__ void k_leaf_expand(const double* __restrict__ bo, const i64* __restri
                               int dir, int nrhs, double* __restrict__ out) {
   const i64 items = n * nrhs;
   for (i64 it = blockIdx.x * (i64)blockDim.x + threadIdx.x; it < items; it += (i64)gridDim.x * blockDim.x) {
-    const int b = int(it % nrhs);
-    const i64 s = it / nrhs;
+    const int b = int(it) % nrhs;
+    const i64 s = int(it) / nrhs;
     const i64 i = ext[s];
     const double a = bo[s * nrhs + b];
     const double da = dir >= 0 ? bo[(n + s) * nrhs + b] : 0.0;
@@ -72,7 +72,7 @@ __global__ void k_factor_pack(const double* __restrict__ Qc, i64 N, int r, const
                               const double* __restrict__ beta, double* __restrict__ Q, double* __restrict__ QT) {
   const i64 items = N * r;
   for (i64 it = blockIdx.x * (i64)blockDim.x + threadIdx.x; it < items; it += (i64)gridDim.x * blockDim.x) {
-    const int k = int(it % r);
+    const int k = int(it) % r;
     const i64 i = it / r;
     const double q = Qc[(i64)k * N + i];
     Q[it] = q;
@@ -85,7 +85,7 @@ __global__ void k_factor_pack(const double* __restrict__ Qc, i64 N, int r, const
 
 // ---------------------------------------------------------------- DMMA helpers
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
@@ -172,8 +172,8 @@ __global__ void k_had_tridiag(const double* __restrict__ C, int ra, int rb, int 
                               const double* __restrict__ bta, double* __restrict__ Cp) {
   const i64 items = (i64)ra * rb * nrhs;
   for (i64 it = blockIdx.x * (i64)blockDim.x + threadIdx.x; it < items; it += (i64)gridDim.x * blockDim.x) {
-    const int b = int(it % nrhs);
-    const int m = int(it / nrhs);
+    const int b = int(it) % nrhs;
+    const int m = int(it) / nrhs;
     const int k = m / rb, l = m % rb;
     double v = a[l] * C[it];
     if (l > 0) v += bta[l - 1] * C[((i64)k * rb + l - 1) * nrhs + b];

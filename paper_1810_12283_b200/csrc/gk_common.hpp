@@ -31,6 +31,12 @@ struct Error : std::runtime_error {
 void cuda_check(cudaError_t e, const char* what);
 #define GK_CUDA(x) ::gk::cuda_check((x), #x)
 
+// Process-wide kernel-variant knobs (gk_set_tuning); 0 = default.
+struct Tuning {
+  std::atomic<int> scatter{0}, gather{0}, toeplitz{0};
+};
+extern Tuning g_tuning;
+
 // Every kernel launch goes through this so the library can report how many of
 // its own kernels ran (bench.py's gpu_launches, smoke()).
 extern std::atomic<i64> g_launches;
@@ -148,6 +154,18 @@ struct Op {
   virtual const i64* d_ext_of_int() const { return nullptr; }
   virtual i64 int_of_ext(i64 r) const { return r; }
   virtual void stage(int st, const double* in, double* out, int nrhs, cudaStream_t s);
+
+  // Whole MVM replayed from a cached CUDA graph (captured once per
+  // (in, out, nrhs)): one launch instead of one per kernel.
+  void mvm_graph(const double* in, double* out, int nrhs, cudaStream_t s);
+  struct GraphEntry {
+    const double* in;
+    double* out;
+    int nrhs;
+    cudaGraphExec_t exec;
+    i64 nodes;
+  };
+  std::vector<GraphEntry> graphs;
 
   void to_internal(const double* V, i64 ldv, double* I, int nrhs, cudaStream_t s) const;
   void from_internal(const double* I, double* V, i64 ldv, int nrhs, cudaStream_t s) const;

@@ -15,6 +15,7 @@
 namespace gk {
 
 std::atomic<i64> g_launches{0};
+Tuning g_tuning;
 
 void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) fail(GK_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -129,6 +130,7 @@ std::uint64_t next_op_uid() {
 }
 
 Op::~Op() {
+  for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
   if (stream) cudaStreamDestroy(stream);
   if (cap_stream) cudaStreamDestroy(cap_stream);
 }

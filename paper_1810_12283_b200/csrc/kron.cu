@@ -99,6 +99,231 @@ __global__ void __launch_bounds__(256) k_toeplitz(const double* __restrict__ t, 
   }
 }
 
+// ---------------------------------------------------------------- DMMA path
+// Same product on the fp64 tensor cores: mma.sync.m8n8k4 (DMMA). CTA = 2×2
+// warps, warp tile (8·WM)×(8·WN); the Toeplitz A tile is generated from the
+// 1-D sequence into shared memory, B is staged with the layout-aware slots.
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int WM, int WN>
+__global__ void __launch_bounds__(128) k_toeplitz_dmma(const double* __restrict__ t, int M, int band, i64 P,
+                                                       i64 Q, const double* __restrict__ X,
+                                                       double* __restrict__ Y) {
+  constexpr int BM = 16 * WM, BN = 16 * WN, BK = 16;
+  constexpr int SA = BM + 8, SB = BN + 8;  // row strides ≡ 8 (mod 16) doubles: conflict-free fragments
+  __shared__ double As[BK * SA];
+  __shared__ double Bs[BK * SB];
+  const i64 ncols = P * Q;
+  const i64 col0 = (i64)blockIdx.x * BN;
+  const int a0 = blockIdx.y * BM;
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int wm = (warp / 2) * (8 * WM), wn = (warp % 2) * (8 * WN);
+  const int g = lane / 4, t4 = lane % 4;
+  const bool q_major = Q >= 16;
+  __shared__ long long coff[BN];
+  if (tid < BN) {
+    const long long col = col0 + tid;
+    coff[tid] = col < ncols ? (long long)(int(col) / int(Q)) * M * Q + int(col) % int(Q) : -1;
+  }
+  __syncthreads();
+  constexpr int SLOTS = (BK * BN + 127) / 128;
+  i64 soff[SLOTS];
+  int skk[SLOTS], scc[SLOTS];
+  bool sval[SLOTS];
+#pragma unroll
+  for (int r = 0; r < SLOTS; ++r) {
+    const int idx = tid + 128 * r;
+    const int kk = q_major ? idx / BN : idx % BK;
+    const int cc = q_major ? idx % BN : idx / BK;
+    skk[r] = kk;
+    scc[r] = cc;
+    sval[r] = idx < BK * BN && coff[cc] >= 0;
+    soff[r] = sval[r] ? coff[cc] : 0;
+  }
+  double acc[WM][WN][2];
+#pragma unroll
+  for (int i = 0; i < WM; ++i)
+#pragma unroll
+    for (int j = 0; j < WN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int c0 = 0; c0 < M; c0 += BK) {
+    const int dmin = max(0, max(c0 - (a0 + BM - 1), a0 - (c0 + BK - 1)));
+    if (dmin >= band) continue;  // block-uniform
+    __syncthreads();
+    for (int idx = tid; idx < BK * BM; idx += 128) {
+      const int kk = idx / BM, mm = idx % BM;
+      const int a = a0 + mm, c = c0 + kk;
+      As[kk * SA + mm] = (a < M && c < M) ? __ldg(t + (a > c ? a - c : c - a)) : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < SLOTS; ++r) {
+      if (tid + 128 * r < BK * BN) {
+        const int c = c0 + skk[r];
+        Bs[skk[r] * SB + scc[r]] = (sval[r] && c < M) ? __ldg(X + soff[r] + (i64)c * Q) : 0.0;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[WM], bf[WN];
+#pragma unroll
+      for (int i = 0; i < WM; ++i) af[i] = As[(kk + t4) * SA + wm + 8 * i + g];
+#pragma unroll
+      for (int j = 0; j < WN; ++j) bf[j] = Bs[(kk + t4) * SB + wn + 8 * j + g];
+#pragma unroll
+      for (int i = 0; i < WM; ++i)
+#pragma unroll
+        for (int j = 0; j < WN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < WN; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const long long o = coff[wn + 8 * j + 2 * t4 + e];
+      if (o < 0) continue;
+#pragma unroll
+      for (int i = 0; i < WM; ++i) {
+        const int a = a0 + wm + 8 * i + g;
+        if (a < M) Y[o + (long long)a * Q] = acc[i][j][e];
+      }
+    }
+}
+
+// Slab variant: a CTA owns BN output columns and ALL M rows; the whole K
+// extent of its B slab (M × BN) and the 1-D sequence are staged in shared
+// memory in one burst, so there is a single global-latency phase. A fragments
+// are generated from the staged sequence (A[a][c] = t[|a-c|]); each warp takes
+// m8-tiles round-robin in groups of 4, skipping k-steps outside the band.
+template <int NT>  // n8-tiles per CTA (BN = 8·NT)
+__global__ void __launch_bounds__(128) k_toeplitz_slab(const double* __restrict__ t, int M, int band, i64 P,
+                                                       i64 Q, const double* __restrict__ X,
+                                                       double* __restrict__ Y) {
+  constexpr int BN = 8 * NT;
+  constexpr int SB = BN + ((BN % 16 == 0) ? 8 : 0) + ((BN % 16 == 8) ? 0 : 0);
+  extern __shared__ double sm[];
+  const int Mp = (M + 7) / 8 * 8;
+  double* ts = sm;                 // [Mp]
+  double* Bs = sm + Mp;            // [Mp][SB]
+  const i64 ncols = P * Q;
+  const i64 col0 = (i64)blockIdx.x * BN;
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int g = lane / 4, t4 = lane % 4;
+  for (int i = tid; i < Mp; i += 128) ts[i] = i < M ? __ldg(t + i) : 0.0;
+  // Stage the B slab in batches of 8 independent loads per thread (issued
+  // together, then stored), int32 index math: one L2 latency per batch
+  // instead of one per element.
+  // per-CTA column offsets (one 32-bit division per column, not per element)
+  __shared__ long long coff[BN];
+  const int Qi = int(Q), Mi = M;
+  if (tid < BN) {
+    const long long col = col0 + tid;
+    coff[tid] = col < ncols ? (long long)(int(col) / Qi) * Mi * Qi + int(col) % Qi : -1;
+  }
+  __syncthreads();
+  // Stage the B slab in batches of 8 independent loads per thread (issued
+  // together, then stored): one L2 latency per batch.
+  const bool q_major = Q >= BN;
+  const int total = Mp * BN;
+  for (int e0 = tid; e0 < total; e0 += 128 * 8) {
+    double vals[8];
+    int dst[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * 128;
+      int c, cc;
+      if (q_major) {
+        c = e / BN;
+        cc = e % BN;
+      } else {
+        cc = e / Mp;
+        c = e - cc * Mp;
+      }
+      dst[u] = (e < total) ? c * SB + cc : -1;
+      double v = 0.0;
+      if (e < total && c < Mi) {
+        const long long o = coff[cc];
+        if (o >= 0) v = __ldg(X + o + (long long)c * Qi);
+      }
+      vals[u] = v;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (dst[u] >= 0) Bs[dst[u]] = vals[u];
+  }
+  __syncthreads();
+  const int mtiles = Mp / 8;
+  const int ksteps = Mp / 4;
+  for (int mt0 = warp * 4; mt0 < mtiles; mt0 += 16) {
+    double acc[4][NT][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    const int ntile = min(4, mtiles - mt0);
+    const int row_lo = mt0 * 8, row_hi = (mt0 + ntile) * 8 - 1;
+    // k range whose |a - c| < band for some row in [row_lo, row_hi]
+    const int k_lo = max(0, (row_lo - band + 1) / 4 * 4);
+    const int k_hi = min(Mp, (row_hi + band + 4) / 4 * 4);
+    for (int kk = k_lo; kk < k_hi; kk += 4) {
+      const int c = kk + t4;
+      double bf[NT];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) bf[j] = Bs[c * SB + 8 * j + g];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (i >= ntile) break;
+        const int a = (mt0 + i) * 8 + g;
+        const int dist = a > c ? a - c : c - a;
+        const double af = (a < M && c < M) ? ts[dist] : 0.0;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], af, bf[j]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (i >= ntile) break;
+      const int a = (mt0 + i) * 8 + g;
+      if (a >= M) continue;
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const long long o = coff[8 * j + 2 * t4 + e];
+          if (o >= 0) Y[o + (long long)a * Qi] = acc[i][j][e];
+        }
+    }
+  }
+}
+
+template <int NT>
+void launch_toeplitz_slab(const double* t, int M, int band, i64 P, i64 Q, const double* X, double* Y,
+                          cudaStream_t s) {
+  constexpr int BN = 8 * NT;
+  constexpr int SB = BN + ((BN % 16 == 0) ? 8 : 0);
+  const int Mp = (M + 7) / 8 * 8;
+  const size_t shm = sizeof(double) * (size_t(Mp) + size_t(Mp) * SB);
+  if (shm > 48 * 1024)
+    GK_CUDA(cudaFuncSetAttribute((const void*)k_toeplitz_slab<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(shm)));
+  const i64 ncols = P * Q;
+  k_toeplitz_slab<NT><<<static_cast<unsigned>((ncols + BN - 1) / BN), 128, shm, s>>>(t, M, band, P, Q, X, Y);
+  launched("toeplitz mode product (DMMA slab)");
+}
+
+template <int WM, int WN>
+void launch_toeplitz_dmma(const double* t, int M, int band, i64 P, i64 Q, const double* X, double* Y,
+                          cudaStream_t s) {
+  constexpr int BM = 16 * WM, BN = 16 * WN;
+  const i64 ncols = P * Q;
+  dim3 grid(static_cast<unsigned>((ncols + BN - 1) / BN), static_cast<unsigned>((M + BM - 1) / BM));
+  k_toeplitz_dmma<WM, WN><<<grid, 128, 0, s>>>(t, M, band, P, Q, X, Y);
+  launched("toeplitz mode product (DMMA)");
+}
+
 template <int TM, int TN>
 void launch_toeplitz(const double* t, int M, int band, i64 P, i64 Q, const double* X, double* Y,
                      cudaStream_t s) {
@@ -148,12 +373,31 @@ __global__ void k_col_sum(const double* __restrict__ partial, int nblocks, int n
 
 void toeplitz_mode(const double* t, int M, int band, i64 P, i64 Q, const double* X, double* Y,
                    cudaStream_t s) {
-  // Pick the largest tile that still gives >= 2 waves of CTAs over 148 SMs.
   const i64 ncols = P * Q;
   auto ctas = [&](int bm, int bn) { return ((ncols + bn - 1) / bn) * ((M + bm - 1) / bm); };
-  if (M > 32 && ctas(64, 64) >= 296) launch_toeplitz<4, 4>(t, M, band, P, Q, X, Y, s);
-  else if (ctas(32, 64) >= 296) launch_toeplitz<2, 4>(t, M, band, P, Q, X, Y, s);
-  else launch_toeplitz<2, 2>(t, M, band, P, Q, X, Y, s);
+  const int variant = g_tuning.toeplitz.load();
+  if (variant == 1) {  // SIMT fp64 FMA, largest tile with >= 2 waves
+    if (M > 32 && ctas(64, 64) >= 296) launch_toeplitz<4, 4>(t, M, band, P, Q, X, Y, s);
+    else if (ctas(32, 64) >= 296) launch_toeplitz<2, 4>(t, M, band, P, Q, X, Y, s);
+    else launch_toeplitz<2, 2>(t, M, band, P, Q, X, Y, s);
+    return;
+  }
+  if (variant == 0 || variant == 3) {  // DMMA, smallest tile (most CTAs): best measured at C1-C4 sizes
+    launch_toeplitz_dmma<2, 2>(t, M, band, P, Q, X, Y, s);
+    return;
+  }
+  if (variant == 4) {  // DMMA slab: one staging phase per CTA
+    const int Mp = (M + 7) / 8 * 8;
+    // widest slab that keeps >= ~1.5 CTAs per SM and fits shared memory
+    if (ncols >= 16 * 222 && size_t(Mp) * 24 * 8 <= 200 * 1024) launch_toeplitz_slab<2>(t, M, band, P, Q, X, Y, s);
+    else if (size_t(Mp) * 8 * 8 <= 200 * 1024) launch_toeplitz_slab<1>(t, M, band, P, Q, X, Y, s);
+    else launch_toeplitz_dmma<2, 2>(t, M, band, P, Q, X, Y, s);
+    return;
+  }
+  // DMMA tiles; pick the largest that still gives >= ~1.3 waves over 148 SMs.
+  if (M > 32 && ctas(64, 64) >= 192) launch_toeplitz_dmma<4, 4>(t, M, band, P, Q, X, Y, s);
+  else if (ctas(32, 64) >= 192) launch_toeplitz_dmma<2, 4>(t, M, band, P, Q, X, Y, s);
+  else launch_toeplitz_dmma<2, 2>(t, M, band, P, Q, X, Y, s);
 }
 
 void col_dot(const double* x, const double* y, i64 rows, int nrhs, double* out, double* partial,

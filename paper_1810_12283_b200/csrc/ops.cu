@@ -198,8 +198,37 @@ void Op::from_internal(const double* I, double* V, i64 ldv, int nrhs, cudaStream
   gk::from_internal(d_ext_of_int(), N, I, V, ldv, nrhs, s);
 }
 
+void Op::mvm_graph(const double* in, double* out, int nrhs, cudaStream_t s) {
+  for (auto& g : graphs)
+    if (g.in == in && g.out == out && g.nrhs == nrhs) {
+      GK_CUDA(cudaGraphLaunch(g.exec, s));
+      g_launches.fetch_add(g.nodes);
+      return;
+    }
+  if (!cap_stream) init_stream();
+  mvm(in, out, nrhs, s);  // warm scratch (allocation must not happen during capture)
+  GK_CUDA(cudaStreamSynchronize(s));
+  const i64 before = g_launches.load();
+  cudaGraph_t graph;
+  GK_CUDA(cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeThreadLocal));
+  mvm(in, out, nrhs, cap_stream);
+  GK_CUDA(cudaStreamEndCapture(cap_stream, &graph));
+  GraphEntry e{in, out, nrhs, nullptr, g_launches.load() - before};
+  g_launches.fetch_sub(e.nodes);
+  GK_CUDA(cudaGraphInstantiate(&e.exec, graph, 0));
+  cudaGraphDestroy(graph);
+  if (graphs.size() >= 16) {
+    cudaGraphExecDestroy(graphs.front().exec);
+    graphs.erase(graphs.begin());
+  }
+  graphs.push_back(e);
+  GK_CUDA(cudaGraphLaunch(e.exec, s));
+  g_launches.fetch_add(e.nodes);
+}
+
 void Op::stage(int st, const double* in, double* out, int nrhs, cudaStream_t s) {
   if (st == 3) return mvm(in, out, nrhs, s);
+  if (st == 4) return mvm_graph(in, out, nrhs, s);
   fail(GK_ERR_ARG, "this operator has no D-SKI stages");
 }
 

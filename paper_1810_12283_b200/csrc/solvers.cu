@@ -189,7 +189,7 @@ __global__ void k_cg_pupdate(CgDev st, double* __restrict__ P, const double* __r
   const int nrhs = st.nrhs;
   const i64 items = rows * nrhs;
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < items; i += (i64)gridDim.x * blockDim.x) {
-    const int b = int(i % nrhs);
+    const int b = int(i) % nrhs;  // 32-bit: N·nrhs < 2^31
     if (st.active[b]) P[i] = Z[i] + st.beta[b] * P[i];
   }
 }
@@ -547,7 +547,7 @@ __global__ void k_lz_next(const double* __restrict__ W, const double* __restrict
                           i64 N, int P, double* __restrict__ qn) {
   const i64 items = N * P;
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < items; i += (i64)gridDim.x * blockDim.x) {
-    const int p = int(i % P);
+    const int p = int(i) % P;
     if (flag[p]) qn[i] = W[i] / beta[p];
   }
 }

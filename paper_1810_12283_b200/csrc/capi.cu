@@ -147,6 +147,7 @@ int gk_set_tuning(const char* key, int value) {
   std::atomic<int>* slot = k == "scatter" ? &g_tuning.scatter
                            : k == "gather" ? &g_tuning.gather
                            : k == "toeplitz" ? &g_tuning.toeplitz
+                           : k == "precond" ? &g_tuning.precond
                                              : nullptr;
   return slot ? slot->exchange(value) : -1;
 }

@@ -334,45 +334,35 @@ __global__ void __launch_bounds__(256) k_scatter_lean(DskiView op, const double*
       const int cb = crow * op.nb[D - 1];
       const int s_lo = __ldg(op.cell_start + cb + lo);
       const int s_hi = __ldg(op.cell_start + cb + hi + 1);
-      // two points per iteration: both points' loads are in flight together
-      auto contrib = [&](int s) -> double {
+      for (int s = s_lo; s < s_hi; ++s) {
         const double* rec = op.wts + (size_t)s * REC;
         const int4 bs = __ldg(op.base + s);
         const int tl = kl - (D == 1 ? bs.x : (D == 2 ? bs.y : bs.z));
         const double* vs = vb + (size_t)s * nrhs;
         const double v0 = __ldg(vs);
         if constexpr (D == 1) {
-          double r = __ldg(rec + tl) * v0;
-          if constexpr (GRAD) r += __ldg(rec + T + tl) * __ldg(vs + gstride);
-          return r;
+          acc += __ldg(rec + tl) * v0;
+          if constexpr (GRAD) acc += __ldg(rec + T + tl) * __ldg(vs + gstride);
         } else if constexpr (D == 2) {
           const double w0 = __ldg(rec + t0), w1 = __ldg(rec + 2 * T + tl);
           if constexpr (GRAD) {
             const double dw0 = __ldg(rec + T + t0), dw1 = __ldg(rec + 3 * T + tl);
             const double v1 = __ldg(vs + gstride), v2 = __ldg(vs + 2 * gstride);
-            return w1 * (v0 * w0 + v1 * dw0) + dw1 * (v2 * w0);
+            acc += w1 * (v0 * w0 + v1 * dw0) + dw1 * (v2 * w0);
           } else {
-            return w0 * w1 * v0;
+            acc += w0 * w1 * v0;
           }
         } else {
           const double w0 = __ldg(rec + t0), w1 = __ldg(rec + 2 * T + t1), w2 = __ldg(rec + 4 * T + tl);
           if constexpr (GRAD) {
             const double dw0 = __ldg(rec + T + t0), dw1 = __ldg(rec + 3 * T + t1), dw2 = __ldg(rec + 5 * T + tl);
             const double v1 = __ldg(vs + gstride), v2 = __ldg(vs + 2 * gstride), v3 = __ldg(vs + 3 * gstride);
-            return w2 * (w1 * (v0 * w0 + v1 * dw0) + dw1 * (v2 * w0)) + dw2 * (w1 * (v3 * w0));
+            acc += w2 * (w1 * (v0 * w0 + v1 * dw0) + dw1 * (v2 * w0)) + dw2 * (w1 * (v3 * w0));
           } else {
-            return w0 * w1 * w2 * v0;
+            acc += w0 * w1 * w2 * v0;
           }
         }
-      };
-      int s = s_lo;
-      for (; s + 1 < s_hi; s += 2) {
-        const double c0 = contrib(s);
-        const double c1 = contrib(s + 1);
-        acc += c0;
-        acc += c1;
       }
-      if (s < s_hi) acc += contrib(s);
     }
   }
   u[(size_t)node * nrhs + b] = acc;

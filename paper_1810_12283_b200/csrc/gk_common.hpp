@@ -33,7 +33,7 @@ void cuda_check(cudaError_t e, const char* what);
 
 // Process-wide kernel-variant knobs (gk_set_tuning); 0 = default.
 struct Tuning {
-  std::atomic<int> scatter{0}, gather{0}, toeplitz{0};
+  std::atomic<int> scatter{0}, gather{0}, toeplitz{0}, precond{0};
 };
 extern Tuning g_tuning;
 

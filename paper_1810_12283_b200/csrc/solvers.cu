@@ -54,6 +54,18 @@ __device__ __forceinline__ double sum_partials(const double* partial, int nblock
   return s;
 }
 
+// Warp-cooperative, fixed-order sum of nblocks partials: lane l sums blocks
+// l, l+32, …; then a butterfly. Same order every run (deterministic), and
+// the ~nblocks/32 loads per lane are independent (no serial latency chain).
+__device__ __forceinline__ double warp_sum_partials(const double* partial, int nblocks, int stride, int idx) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int k = lane; k < nblocks; k += 32) s += partial[(i64)k * stride + idx];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+
 __global__ void k_dot_partial(const double* __restrict__ x, const double* __restrict__ y, i64 rows, int nrhs,
                               double* __restrict__ partial) {
   __shared__ double sm[RT];
@@ -86,45 +98,44 @@ struct CgDev {
 };
 
 // init: partial0 = ||b||², partial1 = r·z, partial2 = r·r (r = b)
+// One 32-thread block per column; partials reduced warp-cooperatively.
 __global__ void k_cg_init(CgDev st, const double* __restrict__ p_bb, const double* __restrict__ p_rz,
                           const double* __restrict__ p_rr) {
-  const int b = threadIdx.x;
-  __shared__ int cnt;
-  if (b == 0) cnt = 0;
-  __syncthreads();
-  if (b < st.nrhs) {
-    const double bn = sqrt(sum_partials(p_bb, RB, st.nrhs, b));
-    st.bnorm[b] = bn;
-    st.its[b] = 0;
-    st.upd[b] = 0;
-    if (bn == 0.0) {  // linalg.cpp:93-96: zero rhs -> converged, no history
-      st.conv[b] = 1;
-      st.active[b] = 0;
-      st.rz[b] = 0.0;
-    } else {
-      st.rz[b] = sum_partials(p_rz, RB, st.nrhs, b);
-      const double relres = sqrt(sum_partials(p_rr, RB, st.nrhs, b)) / bn;
-      st.hist[b] = relres;
-      const bool done = relres <= st.tol;  // :104-109
-      st.conv[b] = done ? 1 : 0;
-      st.active[b] = done ? 0 : 1;
-      if (!done) atomicAdd(&cnt, 1);
-    }
+  const int b = blockIdx.x;
+  const double bb = warp_sum_partials(p_bb, RB, st.nrhs, b);
+  const double rz = warp_sum_partials(p_rz, RB, st.nrhs, b);
+  const double rr = warp_sum_partials(p_rr, RB, st.nrhs, b);
+  if (threadIdx.x != 0) return;
+  const double bn = sqrt(bb);
+  st.bnorm[b] = bn;
+  st.its[b] = 0;
+  st.upd[b] = 0;
+  if (bn == 0.0) {  // linalg.cpp:93-96: zero rhs -> converged, no history
+    st.conv[b] = 1;
+    st.active[b] = 0;
+    st.rz[b] = 0.0;
+  } else {
+    st.rz[b] = rz;
+    const double relres = sqrt(rr) / bn;
+    st.hist[b] = relres;
+    const bool done = relres <= st.tol;  // :104-109
+    st.conv[b] = done ? 1 : 0;
+    st.active[b] = done ? 0 : 1;
+    if (!done) atomicAdd(st.nactive, 1);  // zeroed before launch
   }
-  __syncthreads();
-  if (b == 0) *st.nactive = cnt;
 }
 
 __global__ void k_cg_fin_pAp(CgDev st, const double* __restrict__ partial) {
-  const int b = threadIdx.x;
-  if (b >= st.nrhs) return;
+  const int b = blockIdx.x;
+  const double pAp = warp_sum_partials(partial, RB, st.nrhs, b);
+  if (threadIdx.x != 0) return;
+  if (b == 0) *st.nactive = 0;  // recounted by k_cg_fin_rr (stream-ordered after this kernel)
   st.upd[b] = 0;
   if (!st.active[b]) return;
   if (st.its[b] >= st.maxit) {  // loop bound reached, unconverged
     st.active[b] = 0;
     return;
   }
-  const double pAp = sum_partials(partial, RB, st.nrhs, b);
   if (pAp <= 0.0) {  // linalg.cpp:114: loss of definiteness -> stalled
     st.active[b] = 0;
     return;
@@ -158,29 +169,24 @@ __global__ void k_cg_axpy(CgDev st, double* __restrict__ X, double* __restrict__
 }
 
 __global__ void k_cg_fin_rr(CgDev st, const double* __restrict__ partial) {
-  const int b = threadIdx.x;
-  __shared__ int cnt;
-  if (b == 0) cnt = 0;
-  __syncthreads();
-  if (b < st.nrhs) {
-    if (st.upd[b]) {
-      const double relres = sqrt(sum_partials(partial, RB, st.nrhs, b)) / st.bnorm[b];
-      st.hist[(i64)st.its[b] * st.nrhs + b] = relres;
-      if (relres <= st.tol) {  // :121-125
-        st.conv[b] = 1;
-        st.active[b] = 0;
-      }
+  const int b = blockIdx.x;
+  const double rr = warp_sum_partials(partial, RB, st.nrhs, b);
+  if (threadIdx.x != 0) return;
+  if (st.upd[b]) {
+    const double relres = sqrt(rr) / st.bnorm[b];
+    st.hist[(i64)st.its[b] * st.nrhs + b] = relres;
+    if (relres <= st.tol) {  // :121-125
+      st.conv[b] = 1;
+      st.active[b] = 0;
     }
-    if (st.active[b]) atomicAdd(&cnt, 1);
   }
-  __syncthreads();
-  if (b == 0) *st.nactive = cnt;
+  if (st.active[b]) atomicAdd(st.nactive, 1);
 }
 
 __global__ void k_cg_fin_rz(CgDev st, const double* __restrict__ partial) {
-  const int b = threadIdx.x;
-  if (b >= st.nrhs || !st.active[b]) return;
-  const double rzn = sum_partials(partial, RB, st.nrhs, b);
+  const int b = blockIdx.x;
+  const double rzn = warp_sum_partials(partial, RB, st.nrhs, b);
+  if (threadIdx.x != 0 || !st.active[b]) return;
   st.beta[b] = rzn / st.rz[b];
   st.rz[b] = rzn;
 }
@@ -242,10 +248,14 @@ __global__ void k_pc_proj(const double* __restrict__ Rv, const double* __restric
   if (partial_cc && tid < nrhs) partial_cc[(i64)blockIdx.x * nrhs + tid] = cc;
 }
 
+// out[o] = Σ_blocks partial[blk][o], one warp per output (blocks of 8 warps).
 __global__ void k_pc_fin(const double* __restrict__ partial, int nout, double* __restrict__ T) {
-  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < nout; o += gridDim.x * blockDim.x)
-    T[o] = sum_partials(partial, RB, nout, o);
+  const int o = blockIdx.x * 8 + threadIdx.x / 32;
+  if (o >= nout) return;
+  const double v = warp_sum_partials(partial, RB, nout, o);
+  if ((threadIdx.x & 31) == 0) T[o] = v;
 }
+inline unsigned fin_blocks(int nout) { return static_cast<unsigned>((nout + 7) / 8); }
 
 // z = dinv (dinv r - Q1 T); partial Σ r·z
 __global__ void k_pc_apply(const double* __restrict__ Rv, const double* __restrict__ dinv,
@@ -274,6 +284,159 @@ __global__ void k_pc_apply(const double* __restrict__ Rv, const double* __restri
     }
   }
   if (partial_rz) block_col_store(acc, nrhs, partial_rz, sm);
+}
+
+// ---- DMMA versions of the two rank-k contractions (fp64 tensor cores).
+__device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+constexpr int PCM_MAXI = 7, PCM_MAXJ = 8;  // per-warp m8 tiles × n8 tiles (k ≤ 224, nrhs ≤ 64)
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n" ::);
+  asm volatile("cp.async.wait_group 0;\n" ::);
+}
+
+// partial T = Q1ᵀ C over this CTA's rows, C = D^{-1/2} R. Rows are staged in
+// phases of PCM_RCH with cp.async (every global load in flight at once);
+// output (kp × np) tiles: warp w owns m-tiles i ≡ w (mod 4) and all n-tiles.
+constexpr int PCM_RCH = 112;
+__global__ void __launch_bounds__(128) k_pc_proj_mma(const double* __restrict__ Rv, const double* __restrict__ dinv,
+                                                     const double* __restrict__ q1, i64 N, int k, int nrhs,
+                                                     int rch, double* __restrict__ partial) {
+  const int kp = (k + 7) / 8 * 8, np = (nrhs + 7) / 8 * 8;
+  const int SQ = kp + 8, SC = np + 8;
+  extern __shared__ double sh[];
+  double* Qs = sh;                // [rch][SQ]
+  double* Cs = Qs + rch * SQ;     // [rch][SC]
+  double* Ds = Cs + rch * SC;     // [rch]
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid & 31, g = lane / 4, t4 = lane & 3;
+  const int mt = kp / 8, nt = np / 8;
+  double acc[PCM_MAXI][PCM_MAXJ][2];
+#pragma unroll
+  for (int i = 0; i < PCM_MAXI; ++i)
+#pragma unroll
+    for (int j = 0; j < PCM_MAXJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  i64 r0, r1;
+  row_range(N, r0, r1);
+  for (i64 rt = r0; rt < r1; rt += rch) {
+    const int nr = int((r1 - rt) < rch ? (r1 - rt) : rch);
+    const int nrp = (nr + 3) / 4 * 4;
+    __syncthreads();
+    for (int e = tid; e < nrp * kp; e += 128) {
+      const int rr = e / kp, j = e - rr * kp;
+      if (rr < nr && j < k) cp_async8(Qs + rr * SQ + j, q1 + (rt + rr) * k + j);
+      else Qs[rr * SQ + j] = 0.0;
+    }
+    for (int e = tid; e < nrp * np; e += 128) {
+      const int rr = e / np, bb = e - rr * np;
+      if (rr < nr && bb < nrhs) cp_async8(Cs + rr * SC + bb, Rv + (rt + rr) * nrhs + bb);
+      else Cs[rr * SC + bb] = 0.0;
+    }
+    for (int rr = tid; rr < nrp; rr += 128) {
+      if (rr < nr) cp_async8(Ds + rr, dinv + rt + rr);
+      else Ds[rr] = 0.0;
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    for (int kk = 0; kk < nrp; kk += 4) {
+      const double dk = Ds[kk + t4];
+      double bf[PCM_MAXJ];
+#pragma unroll
+      for (int j = 0; j < PCM_MAXJ; ++j) bf[j] = j < nt ? dk * Cs[(kk + t4) * SC + 8 * j + g] : 0.0;
+#pragma unroll
+      for (int ii = 0; ii < PCM_MAXI; ++ii) {
+        const int i = warp + 4 * ii;
+        if (i >= mt) break;
+        const double af = Qs[(kk + t4) * SQ + 8 * i + g];  // A = Q1ᵀ: (j, row)
+#pragma unroll
+        for (int j = 0; j < PCM_MAXJ; ++j)
+          if (j < nt) dmma_f64(acc[ii][j][0], acc[ii][j][1], af, bf[j]);
+      }
+    }
+  }
+  double* out = partial + (i64)blockIdx.x * k * nrhs;
+#pragma unroll
+  for (int ii = 0; ii < PCM_MAXI; ++ii) {
+    const int i = warp + 4 * ii;
+    if (i >= mt) break;
+    const int j0 = 8 * i + g;
+#pragma unroll
+    for (int jn = 0; jn < PCM_MAXJ; ++jn) {
+      if (jn >= nt) break;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int bb = 8 * jn + 2 * t4 + e;
+        if (j0 < k && bb < nrhs) out[(i64)j0 * nrhs + bb] = acc[ii][jn][e];
+      }
+    }
+  }
+}
+
+// z = D^{-1/2}(D^{-1/2} r - Q1 T) for 64 rows per CTA; T (k × nrhs) and the
+// CTA's 64 Q1 rows staged in shared memory with cp.async in one phase.
+__global__ void __launch_bounds__(128) k_pc_apply_mma(const double* __restrict__ Rv, const double* __restrict__ dinv,
+                                                      const double* __restrict__ q1, const double* __restrict__ T,
+                                                      i64 N, int k, int nrhs, double* __restrict__ Z) {
+  const int kp = (k + 3) / 4 * 4, np = (nrhs + 7) / 8 * 8;
+  const int SC = np + 8, SQ = kp + 4;
+  extern __shared__ double sh[];
+  double* Ts = sh;              // [kp][SC]
+  double* Qs = Ts + kp * SC;    // [64][SQ]
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid & 31, g = lane / 4, t4 = lane & 3;
+  const int nt = np / 8;
+  const i64 row0 = (i64)blockIdx.x * 64;
+  for (int e = tid; e < kp * np; e += 128) {
+    const int j = e / np, bb = e - j * np;
+    if (j < k && bb < nrhs) cp_async8(Ts + j * SC + bb, T + j * nrhs + bb);
+    else Ts[j * SC + bb] = 0.0;
+  }
+  for (int e = tid; e < 64 * kp; e += 128) {
+    const int rr = e / kp, j = e - rr * kp;
+    const i64 r = row0 + rr;
+    if (r < N && j < k) cp_async8(Qs + rr * SQ + j, q1 + r * k + j);
+    else Qs[rr * SQ + j] = 0.0;
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  double acc[2][PCM_MAXJ][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < PCM_MAXJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int kk = 0; kk < kp; kk += 4) {
+    double bf[PCM_MAXJ];
+#pragma unroll
+    for (int j = 0; j < PCM_MAXJ; ++j) bf[j] = j < nt ? Ts[(kk + t4) * SC + 8 * j + g] : 0.0;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const double af = Qs[(warp * 16 + 8 * i + g) * SQ + kk + t4];
+#pragma unroll
+      for (int j = 0; j < PCM_MAXJ; ++j)
+        if (j < nt) dmma_f64(acc[i][j][0], acc[i][j][1], af, bf[j]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const i64 r = row0 + warp * 16 + 8 * i + g;
+    if (r >= N) continue;
+    const double di = dinv[r];
+#pragma unroll
+    for (int j = 0; j < PCM_MAXJ; ++j) {
+      if (j >= nt) break;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int bb = 8 * j + 2 * t4 + e;
+        if (bb < nrhs) Z[r * nrhs + bb] = di * (di * Rv[r * nrhs + bb] - acc[i][j][e]);
+      }
+    }
+  }
 }
 
 // Row-wise small GEMM: Y[r][:] = X[r][:] · Mx (k×k col-major), X,Y [N][k] row-major.
@@ -395,12 +558,13 @@ __global__ void k_pv_stats(const double* __restrict__ d, const i64* __restrict__
 }
 
 // out[0]=min, out[1]=sum, out[2]=max, out[3]=ext (as double bits), out[4]=int
+// One warp; fixed lane-strided order + butterfly (deterministic).
 __global__ void k_pv_stats_fin(const double* pmin, const double* psum, const double* pmax, const i64* pext,
                                const i64* pint, int nb, double* out) {
-  if (threadIdx.x != 0) return;
+  const int lane = threadIdx.x & 31;
   double a = INFINITY, s = 0.0, b = -INFINITY;
   i64 be = LLONG_MAX, bi = -1;
-  for (int k = 0; k < nb; ++k) {
+  for (int k = lane; k < nb; k += 32) {
     a = fmin(a, pmin[k]);
     s += psum[k];
     if (better(pmax[k], pext[k], b, be)) {
@@ -409,11 +573,26 @@ __global__ void k_pv_stats_fin(const double* pmin, const double* psum, const dou
       bi = pint[k];
     }
   }
-  out[0] = a;
-  out[1] = s;
-  out[2] = b;
-  reinterpret_cast<i64*>(out)[3] = be;
-  reinterpret_cast<i64*>(out)[4] = bi;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    const double ob = __shfl_xor_sync(0xffffffffu, b, o);
+    const i64 oe = __shfl_xor_sync(0xffffffffu, be, o);
+    const i64 oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (better(ob, oe, b, be)) {
+      b = ob;
+      be = oe;
+      bi = oi;
+    }
+  }
+  if (lane == 0) {
+    out[0] = a;
+    out[1] = s;
+    out[2] = b;
+    reinterpret_cast<i64*>(out)[3] = be;
+    reinterpret_cast<i64*>(out)[4] = bi;
+  }
 }
 
 // col = (row - noise_sub e_piv - L[:, :k] L[piv, :k]^T) / sqrt(dmax); L[:,k] = col;
@@ -476,8 +655,10 @@ __global__ void k_lz_alpha(double* __restrict__ W, const double* __restrict__ pr
 }
 
 __global__ void k_fin_cols(const double* __restrict__ partial, int nout, double* __restrict__ out) {
-  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < nout; o += gridDim.x * blockDim.x)
-    out[o] = sum_partials(partial, RB, nout, o);
+  const int o = blockIdx.x * 8 + threadIdx.x / 32;
+  if (o >= nout) return;
+  const double v = warp_sum_partials(partial, RB, nout, o);
+  if ((threadIdx.x & 31) == 0) out[o] = v;
 }
 
 // W -= alpha ∘ q (when q != null); partial C[j][p] = Σ Q[j0+j]·W for j < jc
@@ -603,7 +784,8 @@ PcgResult pcg_internal(Op& op, Precond* M, const double* B, double* X, int nrhs,
   launched("pcg dot");
   k_dot_partial<<<RB, RT, 0, s>>>(R.p, R.p, N, nrhs, p2);
   launched("pcg dot");
-  k_cg_init<<<1, RT, 0, s>>>(st, p0, p1, p2);
+  GK_CUDA(cudaMemsetAsync(st.nactive, 0, sizeof(int), s));
+  k_cg_init<<<nrhs, 32, 0, s>>>(st, p0, p1, p2);
   launched("pcg init");
 
   // one iteration, captured as a graph
@@ -611,19 +793,19 @@ PcgResult pcg_internal(Op& op, Precond* M, const double* B, double* X, int nrhs,
     op.mvm(Pb.p, AP.p, nrhs, cs);
     k_dot_partial<<<RB, RT, 0, cs>>>(Pb.p, AP.p, N, nrhs, p0);
     launched("pcg dot");
-    k_cg_fin_pAp<<<1, RT, 0, cs>>>(st, p0);
+    k_cg_fin_pAp<<<nrhs, 32, 0, cs>>>(st, p0);
     launched("pcg fin");
     k_cg_axpy<<<RB, RT, 0, cs>>>(st, X, R.p, Pb.p, AP.p, N, p1);
     launched("pcg axpy");
-    k_cg_fin_rr<<<1, RT, 0, cs>>>(st, p1);
+    k_cg_fin_rr<<<nrhs, 32, 0, cs>>>(st, p1);
     launched("pcg fin");
     if (M) {
       M->apply(R.p, Zb.p, nrhs, cs);  // writes rz partials into M's scratch; recompute below
       k_dot_partial<<<RB, RT, 0, cs>>>(R.p, Zb.p, N, nrhs, p2);
       launched("pcg dot");
-      k_cg_fin_rz<<<1, RT, 0, cs>>>(st, p2);
+      k_cg_fin_rz<<<nrhs, 32, 0, cs>>>(st, p2);
     } else {
-      k_cg_fin_rz<<<1, RT, 0, cs>>>(st, p1);
+      k_cg_fin_rz<<<nrhs, 32, 0, cs>>>(st, p1);
     }
     launched("pcg fin");
     k_cg_pupdate<<<eb, 256, 0, cs>>>(st, Pb.p, M ? Zb.p : R.p, N);
@@ -703,14 +885,49 @@ void Precond::ensure(int nrhs) {
   if (sh1 > 227 * 1024) fail(GK_ERR_UNSUPPORTED, "preconditioner rank × nrhs too large for one pass");
   set_smem((const void*)k_pc_proj, sh1);
   set_smem((const void*)k_pc_apply, sizeof(double) * (k * nrhs + RT));
+  if (mma_ok(nrhs)) {
+    set_smem((const void*)k_pc_proj_mma, proj_mma_smem(nrhs));
+    set_smem((const void*)k_pc_apply_mma, apply_mma_smem(nrhs));
+  }
+}
+
+bool Precond::mma_ok(int nrhs) const {
+  return k <= 4 * PCM_MAXI * 8 && nrhs <= 8 * PCM_MAXJ && proj_mma_smem(nrhs) <= 220 * 1024 &&
+         apply_mma_smem(nrhs) <= 220 * 1024;
+}
+int Precond::proj_rch(int nrhs) const {
+  const i64 kp = (k + 7) / 8 * 8, np = (nrhs + 7) / 8 * 8;
+  const i64 per_row = (kp + 8) + (np + 8) + 1;
+  const i64 fit = (200 * 1024 / 8) / per_row / 4 * 4;
+  return int(std::max<i64>(4, std::min<i64>(PCM_RCH, fit)));
+}
+size_t Precond::proj_mma_smem(int nrhs) const {
+  const i64 kp = (k + 7) / 8 * 8, np = (nrhs + 7) / 8 * 8;
+  const i64 rch = proj_rch(nrhs);
+  return sizeof(double) * size_t(rch * (kp + 8) + rch * (np + 8) + rch);
+}
+size_t Precond::apply_mma_smem(int nrhs) const {
+  const i64 kp = (k + 3) / 4 * 4, np = (nrhs + 7) / 8 * 8;
+  return sizeof(double) * size_t(kp * (np + 8) + 64 * (kp + 4));
 }
 
 void Precond::apply(const double* r, double* z, int nrhs, cudaStream_t s) {
   ensure(nrhs);  // no-op once reserved (and before any graph capture)
+  if (mma_ok(nrhs) && g_tuning.precond.load() == 0) {
+    k_pc_proj_mma<<<RB, 128, proj_mma_smem(nrhs), s>>>(r, dinv.p, q1.p, N, int(k), nrhs, proj_rch(nrhs),
+                                                       partial.p);
+    launched("precond proj (DMMA)");
+    k_pc_fin<<<fin_blocks(int(k * nrhs)), 256, 0, s>>>(partial.p, int(k * nrhs), t.p);
+    launched("precond fin");
+    k_pc_apply_mma<<<static_cast<unsigned>((N + 63) / 64), 128, apply_mma_smem(nrhs), s>>>(r, dinv.p, q1.p, t.p, N,
+                                                                                           int(k), nrhs, z);
+    launched("precond apply (DMMA)");
+    return;
+  }
   const size_t sh1 = sizeof(double) * (PC_RT * k + PC_RT * nrhs + k * nrhs);
   k_pc_proj<<<RB, RT, sh1, s>>>(r, dinv.p, q1.p, N, int(k), nrhs, partial.p, nullptr);
   launched("precond proj");
-  k_pc_fin<<<blocks_for(k * nrhs), 256, 0, s>>>(partial.p, int(k * nrhs), t.p);
+  k_pc_fin<<<fin_blocks(int(k * nrhs)), 256, 0, s>>>(partial.p, int(k * nrhs), t.p);
   launched("precond fin");
   const size_t sh2 = sizeof(double) * (k * nrhs + RT);
   k_pc_apply<<<RB, RT, sh2, s>>>(r, dinv.p, q1.p, t.p, N, int(k), nrhs, z, nullptr);
@@ -723,9 +940,9 @@ void precond_quadratic(Precond& M, const double* r, int nrhs, double* out_h, cud
   const size_t sh1 = sizeof(double) * (PC_RT * M.k + PC_RT * nrhs + M.k * nrhs);
   k_pc_proj<<<RB, RT, sh1, s>>>(r, M.dinv.p, M.q1.p, M.N, int(M.k), nrhs, M.partial.p, pcc.p);
   launched("precond proj");
-  k_pc_fin<<<blocks_for(M.k * nrhs), 256, 0, s>>>(M.partial.p, int(M.k * nrhs), M.t.p);
+  k_pc_fin<<<fin_blocks(int(M.k * nrhs)), 256, 0, s>>>(M.partial.p, int(M.k * nrhs), M.t.p);
   launched("precond fin");
-  k_fin_cols<<<1, 256, 0, s>>>(pcc.p, nrhs, cc.p);
+  k_fin_cols<<<fin_blocks(nrhs), 256, 0, s>>>(pcc.p, nrhs, cc.p);
   launched("precond fin");
   std::vector<double> T(static_cast<size_t>(M.k) * nrhs), c2(static_cast<size_t>(nrhs));
   GK_CUDA(cudaMemcpyAsync(T.data(), M.t.p, sizeof(double) * T.size(), cudaMemcpyDeviceToHost, s));
@@ -763,7 +980,7 @@ std::unique_ptr<Precond> precond_build(const double* F_int, i64 N, i64 k, const 
   for (int pass = 0; pass < 2; ++pass) {
     k_gram_partial<<<RB, RT, shg, s>>>(cur, N, int(k), part.p);
     launched("precond gram");
-    k_pc_fin<<<blocks_for(k * k), 256, 0, s>>>(part.p, int(k * k), gram.p);
+    k_pc_fin<<<fin_blocks(int(k * k)), 256, 0, s>>>(part.p, int(k * k), gram.p);
     launched("precond gram fin");
     GK_CUDA(cudaMemcpyAsync(gh.data(), gram.p, sizeof(double) * k * k, cudaMemcpyDeviceToHost, s));
     GK_CUDA(cudaStreamSynchronize(s));
@@ -934,7 +1151,7 @@ LanczosBatch lanczos_batch(Op& op, const double* start_int, int P, int steps,
       const int jc = std::min(JC, kc - j0);
       k_lz_proj<<<RB, RT, 0, s>>>(W.p, j0 == 0 ? qk_for_alpha : nullptr, d_alpha, Q, j0, jc, N, P, part.p);
       launched("lanczos proj");
-      k_fin_cols<<<blocks_for(jc * P), 256, 0, s>>>(part.p, jc * P, Cdst + (i64)j0 * P);
+      k_fin_cols<<<fin_blocks(jc * P), 256, 0, s>>>(part.p, jc * P, Cdst + (i64)j0 * P);
       launched("lanczos proj fin");
     }
   };
@@ -948,7 +1165,7 @@ LanczosBatch lanczos_batch(Op& op, const double* start_int, int P, int steps,
     GK_CUDA(cudaMemcpyAsync(d_bprev, bp.data(), sizeof(double) * P, cudaMemcpyHostToDevice, s));
     k_lz_alpha<<<RB, RT, 0, s>>>(W.p, k > 0 ? Q + (i64)(k - 1) * blk : nullptr, d_bprev, qk, N, P, part.p);
     launched("lanczos alpha");
-    k_fin_cols<<<1, 256, 0, s>>>(part.p, P, d_alpha);
+    k_fin_cols<<<fin_blocks(P), 256, 0, s>>>(part.p, P, d_alpha);
     launched("lanczos alpha fin");
     const bool last = (k + 1 >= steps);
     if (last) {
@@ -965,7 +1182,7 @@ LanczosBatch lanczos_batch(Op& op, const double* start_int, int P, int steps,
     project(nullptr, k + 1, C2.p);
     k_lz_update<<<RB, RT, 0, s>>>(W.p, Q, C2.p, k + 1, N, P, part.p);
     launched("lanczos update");
-    k_fin_cols<<<1, 256, 0, s>>>(part.p, P, d_beta);
+    k_fin_cols<<<fin_blocks(P), 256, 0, s>>>(part.p, P, d_beta);
     launched("lanczos beta fin");
     GK_CUDA(cudaMemcpyAsync(ab.data(), d_alpha, sizeof(double) * 2 * P, cudaMemcpyDeviceToHost, s));
     GK_CUDA(cudaStreamSynchronize(s));

@@ -30,6 +30,10 @@ struct Precond {
   // z = M^{-1} r; optionally rz[b] partials. All internal layout.
   void apply(const double* r, double* z, int nrhs, cudaStream_t s);
   void ensure(int nrhs);
+  bool mma_ok(int nrhs) const;
+  int proj_rch(int nrhs) const;
+  size_t proj_mma_smem(int nrhs) const;
+  size_t apply_mma_smem(int nrhs) const;
 };
 
 struct PivChol {

@@ -204,29 +204,42 @@ def run_gpu(args):
     ms = float(ms_t.item())
     value = world * N * nrhs / (ms * 1e-3)
 
-    # ---- per-stage timing (dominant kernel for the roofline), same stream
-    Ui = torch.empty(m * nrhs, dtype=torch.float64, device=dev)
-    Wi = torch.empty_like(Ui)
-    stage_ms = {}
-    reps = max(20, min(args.steps, 200))
-    for name, st, a, b in (("scatter", 0, Vi, Ui), ("kuu", 1, Ui, Wi), ("gather", 2, Wi, Oi)):
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(reps)]
-        for s0, e0 in ev:
-            flush.sum()
-            s0.record(stream)
-            op.stage_dev(st, a.data_ptr(), b.data_ptr(), nrhs, stream=sp)
-            e0.record(stream)
-        torch.cuda.synchronize()
-        stage_ms[name] = float(np.mean([s0.elapsed_time(e0) for s0, e0 in ev]))
-    sb = stage_bytes(N, n, d, m, nrhs)
-    peaks = measured_peaks()
-    hbm = float(peaks.get("hbm_gbs", 6650.0))
-    bytes_per = {"scatter": sb["scatter"], "kuu": 2 * sb["kuu_mode"], "gather": sb["gather"]}
-    dom = max(stage_ms, key=stage_ms.get)
-    achieved = bytes_per[dom] / (stage_ms[dom] * 1e-3) / 1e9
+    # ---- roofline of the dominant kernel. With the one-launch 2-D MVM
+    # (fused2d.cu) the step IS one kernel: its algorithmic bytes are SURVEY
+    # §8(d)'s per-MVM figure. The staged kernels (gk_set_tuning("fused", 1))
+    # are timed alongside for reference.
     Mc = 198 * (198 // 2 + 1)
     mvm_bytes = dski_bytes(N, n, d, m, nrhs, Mc)
+    per_step = launches / max(1, args.steps)
+    peaks = measured_peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    Ui = torch.empty(m * nrhs, dtype=torch.float64, device=dev)
+    Wi = torch.empty_like(Ui)
+    staged_ms = {}
+    reps = max(20, min(args.steps, 200))
+    prev = gk.set_tuning("fused", 1)
+    try:
+        for name, st, a, b in (("scatter", 0, Vi, Ui), ("kuu", 1, Ui, Wi), ("gather", 2, Wi, Oi),
+                               ("staged_mvm", 3, Vi, Oi)):
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(reps)]
+            for s0, e0 in ev:
+                flush.sum()
+                s0.record(stream)
+                op.stage_dev(st, a.data_ptr(), b.data_ptr(), nrhs, stream=sp)
+                e0.record(stream)
+            torch.cuda.synchronize()
+            staged_ms[name] = float(np.mean([s0.elapsed_time(e0) for s0, e0 in ev]))
+    finally:
+        gk.set_tuning("fused", prev)
+    sb = stage_bytes(N, n, d, m, nrhs)
+    if per_step == 1:
+        dom, dom_bytes, dom_ms = "k_dski_mvm2d (one-launch MVM)", mvm_bytes, ms
+    else:
+        bytes_per = {"scatter": sb["scatter"], "kuu": 2 * sb["kuu_mode"], "gather": sb["gather"]}
+        dom = max(bytes_per, key=lambda k: staged_ms[k])
+        dom_bytes, dom_ms = bytes_per[dom], staged_ms[dom]
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
 
     # ---- end to end through the public API with host (pinned) buffers
     Hin = torch.from_numpy(np.asfortranarray(Bh).T.copy()).pin_memory()  # (nrhs, N) == col-major
@@ -270,6 +283,12 @@ def run_gpu(args):
     t0 = time.perf_counter()
     slq = gk.slq_logdet(op, CONFIG["slq_probes"], CONFIG["slq_steps"], 0, 0.5 * 1e-4,
                         probe_offset=rank * CONFIG["slq_probes"])
+    slq_logdet = slq.logdet
+    if world > 1:  # global estimate over all ranks' probes, summed in probe order
+        from paper_1810_12283_b200 import sharding
+        est = sharding.gather_probe_estimates(np.asarray(slq.estimates), rank * CONFIG["slq_probes"],
+                                              world * CONFIG["slq_probes"], device=dev)
+        slq_logdet = sharding.ordered_mean(est)
     t_slq = time.perf_counter() - t0
     solve = torch.tensor([t_pre, t_pcg, t_slq], device=dev, dtype=torch.float64)
     if world > 1:
@@ -293,13 +312,16 @@ def run_gpu(args):
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
                          "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if peaks else "fallback",
-                         "bytes_per_launch": bytes_per[dom], "stage_ms": stage_ms},
+                         "bytes_per_launch": dom_bytes, "launch_ms": dom_ms,
+                         "bytes_formula": "SURVEY 8(d): 8*(3*N*B + 2*n*d + 4*m*B + M_c)",
+                         "staged_kernels_ms": staged_ms},
             "mvm_roofline": {"algorithmic_bytes": mvm_bytes,
                              "achieved_gbs": mvm_bytes / (ms * 1e-3) / 1e9,
                              "frac_hbm": mvm_bytes / (ms * 1e-3) / 1e9 / hbm},
             "solve": {"precond_build_s": t_pre, "pcg_s": t_pcg, "slq_s": t_slq,
                       "pcg_plus_slq_s": t_pcg + t_slq, "pcg_iterations": [int(v) for v in its],
-                      "pcg_converged": int(np.sum(conv)), "slq_logdet_shard": slq.logdet},
+                      "pcg_converged": int(np.sum(conv)), "slq_logdet": slq_logdet,
+                      "slq_probes_total": world * CONFIG["slq_probes"]},
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }

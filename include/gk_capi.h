@@ -50,7 +50,8 @@ const char* gk_last_error(void);
 int64_t gk_last_error_point(void);
 const char* gk_version(void);
 /* Kernel-variant selection for tuning/A-B timing (process-wide). Keys:
- * "scatter", "gather", "toeplitz" (0 = default choice). Returns the old value. */
+ * "scatter", "gather", "toeplitz", "precond" (0 = default choice), "fused"
+ * (1 = disable the one-launch 2-D MVM), "fused_prof". Returns the old value. */
 int gk_set_tuning(const char* key, int value);
 /* Number of CUDA kernels this library has launched in this process. */
 int64_t gk_kernel_launch_count(void);
@@ -87,6 +88,13 @@ void gk_gaussian_vector(int64_t n, uint64_t seed, uint64_t stream, double* out);
 /* ---------------------------------------------------------------- operators
  * Every structured operator is a gk_op (LinearOperator, linear_operator.hpp:12-35). */
 typedef struct gk_op gk_op;
+
+/* Diagnostics for the one-launch 2-D D-SKI MVM: with tuning key "fused_prof"
+ * set to 1, each launch records per-CTA %globaltimer stamps (ns) at 8 points:
+ * start, scatter done, barrier 1 passed, mode-1 done, barrier 2 passed,
+ * mode-0 done, barrier 3 passed, gather done. Copies the stamps of the last
+ * launch for `nrhs` into out[cta*8 + k]; returns the CTA count (0 if none). */
+int gk_debug_fused_phases(gk_op* op, int nrhs, int64_t* out, int max_ctas);
 
 /* DskiOperator(kernel, grid, X, noise, order, with_gradients) (dski.hpp:58-65).
  * order: 0 quintic, 1 cubic. */

@@ -58,6 +58,7 @@ _SIGS = {
     "gk_version": (C.c_char_p, []),
     "gk_set_tuning": (C.c_int, [C.c_char_p, C.c_int]),
     "gk_kernel_launch_count": (_i64, []),
+    "gk_debug_fused_phases": (C.c_int, [_vp, C.c_int, _i64p, C.c_int]),
     "gk_grid_cover": (C.c_int, [_dp, _i64, C.c_int, _d, C.c_int, C.c_int, C.POINTER(GkGrid)]),
     "gk_mix_seed": (_u64, [_u64, _u64]),
     "gk_rademacher_vector": (None, [_i64, _u64, _u64, _dp]),
@@ -168,7 +169,8 @@ def version() -> str:
 
 
 def set_tuning(key: str, value: int) -> int:
-    """Select a kernel variant ("scatter", "gather", "toeplitz"; 0 = default)."""
+    """Select a kernel variant ("scatter", "gather", "toeplitz", "precond", "fused";
+    0 = default; "fused" 1 disables the one-launch d = 2 MVM). Returns the old value."""
     return int(_lib.gk_set_tuning(key.encode(), int(value)))
 
 
@@ -749,3 +751,12 @@ def stacked_targets(y, dY, mean):
     if dY is not None:
         parts += [np.asarray(dY)[:, j] for j in range(np.asarray(dY).shape[1])]
     return np.concatenate(parts)
+
+
+def debug_fused_phases(op, nrhs, max_ctas=4096):
+    """Per-CTA phase stamps (ns) of the last one-launch 2-D MVM (tuning
+    "fused_prof" = 1): array (ctas, 8) — start, scatter done, barrier 1,
+    mode-1 done, barrier 2, mode-0 done, barrier 3, gather done."""
+    out = np.zeros((max_ctas, 8), dtype=np.int64)
+    n = _lib.gk_debug_fused_phases(op.handle, int(nrhs), out.ctypes.data_as(_i64p), max_ctas)
+    return out[:n]

@@ -25,6 +25,7 @@ std::unique_ptr<Op> make_dskip_from_factors(i64 n, int groups, double nv, double
 std::unique_ptr<Op> make_dskip(const gk_kernel& k, const double* X, i64 n, int d, double nv, double ng,
                                const gk_dskip_config& cfg, int device);
 int64_t dski_grid_size(const Op& o);
+int dski_fused_phases(Op& o, int nrhs, i64* out, int max_ctas);
 gk_grid dski_grid(const Op& o);
 void dski_transpose_apply(Op& o, const double* Vi, double* U, int nrhs, cudaStream_t s);
 void dski_apply(Op& o, const double* U, double* Oi, int nrhs, cudaStream_t s);
@@ -148,8 +149,20 @@ int gk_set_tuning(const char* key, int value) {
                            : k == "gather" ? &g_tuning.gather
                            : k == "toeplitz" ? &g_tuning.toeplitz
                            : k == "precond" ? &g_tuning.precond
+                           : k == "fused" ? &g_tuning.fused
+                           : k == "fused_prof" ? &g_tuning.fused_prof
+                           : k == "f2_stc" ? &g_tuning.f2_stc
+                           : k == "f2_sl" ? &g_tuning.f2_sl
+                           : k == "f2_gtc" ? &g_tuning.f2_gtc
+                           : k == "f2_gl" ? &g_tuning.f2_gl
+                           : k == "f2_tsplit" ? &g_tuning.f2_tsplit
+                           : k == "f2_per_sm" ? &g_tuning.f2_per_sm
+                           : k == "f2_skip" ? &g_tuning.f2_skip
+                           : k == "f2_grid" ? &g_tuning.f2_grid
                                              : nullptr;
-  return slot ? slot->exchange(value) : -1;
+  if (!slot) return -1;
+  g_tuning.gen.fetch_add(1);
+  return slot->exchange(value);
 }
 
 gk_status gk_grid_cover(const double* X, int64_t n, int d, double target, int margin, int max_nodes,
@@ -351,6 +364,18 @@ gk_status gk_op_noise_diagonal(const gk_op* h, double* out) {
 }
 
 // ---------------------------------------------------------------- D-SKI pieces
+int gk_debug_fused_phases(gk_op* h, int nrhs, int64_t* out, int max_ctas) {
+  int n = 0;
+  guard([&] {
+    if (!out || max_ctas < 0) fail(GK_ERR_ARG, "null output");
+    Op& op = O(h);
+    DeviceGuard dg(op.device);
+    std::lock_guard<std::mutex> lk(op.mu);
+    n = dski_fused_phases(op, nrhs, out, max_ctas);
+  });
+  return n;
+}
+
 int64_t gk_dski_grid_size(const gk_op* h) {
   int64_t m = -1;
   guard([&] { m = dski_grid_size(O(h)); });

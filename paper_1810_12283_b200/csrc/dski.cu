@@ -22,11 +22,14 @@
 // All vectors are in the internal layout: rows = g*n + sorted point,
 // right-hand sides innermost.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <numeric>
 #include <sstream>
 
+#include "fused2d.hpp"
 #include "gk_common.hpp"
 #include "gk_kernels.cuh"
 
@@ -903,7 +906,45 @@ struct DskiOp final : Op {
   DevBuf<i64> ext;        // internal row -> external row
   std::vector<i64> perm_h, inv_h;
   DevBuf<double> origin_d, h_d;
-  DevBuf<double> grid_u, grid_w, grid_t;  // per-MVM grid scratch (guarded by mu / caller)
+  DevBuf<double> grid_u, grid_w, grid_t, grid_h;  // per-MVM grid scratch (guarded by mu / caller)
+  std::vector<int> cell_start_h;          // host copy (fused-plan sizing)
+  std::vector<std::unique_ptr<Fused2dPlan>> fplans;  // one-launch d = 2 MVM plans, per nrhs
+
+  Fused2dGeom geom2d() const {
+    Fused2dGeom g;
+    g.T = T;
+    g.m0 = m[0];
+    g.m1 = m[1];
+    g.nb0 = nb[0];
+    g.nb1 = nb[1];
+    g.n = int(n);
+    g.base = base.p;
+    g.wd = wd.p;
+    g.cell_start = cell_start.p;
+    g.t0 = tvec.p + toff_h[0];
+    g.t1 = tvec.p + toff_h[1];
+    g.band0 = band[0];
+    g.band1 = band[1];
+    g.nv2 = nv2;
+    g.ng2 = ng2;
+    return g;
+  }
+  // The fused one-launch MVM applies to d = 2 with gradients (C1, C2, C4).
+  Fused2dPlan* fused_plan(int nrhs) {
+    if (d != 2 || G != 2 || g_tuning.fused.load() != 0 || n >= (i64(1) << 31)) return nullptr;
+    const int gen = g_tuning.gen.load();
+    for (auto it = fplans.begin(); it != fplans.end(); ++it)
+      if ((*it)->nrhs == nrhs) {
+        if ((*it)->tuning_gen == gen) return (*it)->ok ? it->get() : nullptr;
+        fplans.erase(it);  // knobs changed: rebuild
+        break;
+      }
+    auto p = std::make_unique<Fused2dPlan>();
+    p->tuning_gen = gen;
+    fused2d_plan(geom2d(), cell_start_h, nrhs, device, *p);
+    fplans.push_back(std::move(p));
+    return fplans.back()->ok ? fplans.back().get() : nullptr;
+  }
 
   DskiView view() const {
     DskiView v;
@@ -941,10 +982,15 @@ struct DskiOp final : Op {
     grid_u.reserve(static_cast<size_t>(M) * nrhs);
     grid_w.reserve(static_cast<size_t>(M) * nrhs);
     grid_t.reserve(static_cast<size_t>(M) * nrhs);
+    if (d == 2 && G == 2) grid_h.reserve(static_cast<size_t>(M) * nrhs);
   }
 
   void mvm(const double* in, double* out, int nrhs, cudaStream_t s) override {
     ensure_scratch(nrhs);
+    if (Fused2dPlan* fp = fused_plan(nrhs)) {
+      fused2d_mvm(geom2d(), *fp, in, out, grid_u.p, grid_h.p, grid_t.p, grid_w.p, true, s);
+      return;
+    }
     scatter(in, grid_u.p, nrhs, s);
     kuu(grid_u.p, grid_w.p, nrhs, s);
     gather(grid_w.p, in, out, nrhs, true, s);
@@ -1265,6 +1311,7 @@ std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, cons
     op->wd.upload(wd.data(), wd.size(), st);
   }
   op->cell_start.upload(cstart.data(), cstart.size(), st);
+  op->cell_start_h = cstart;
   op->tvec.upload(tv.data(), tv.size(), st);
   op->toff.upload(op->toff_h.data(), op->toff_h.size(), st);
   op->ext.upload(ext.data(), ext.size(), st);
@@ -1346,4 +1393,30 @@ void dski_cross_cov(Op& o, const double* dXt, i64 nT, double* Qi, int* dbad, cud
   GK_CUDA(cudaStreamSynchronize(s));
 }
 
+}  // namespace gk
+
+namespace gk {
+// gk_debug_fused_phases backend
+int dski_fused_phases(Op& o, int nrhs, i64* out, int max_ctas) {
+  if (o.kind != KIND_DSKI) fail(GK_ERR_ARG, "operator is not a D-SKI operator");
+  auto& op = static_cast<DskiOp&>(o);
+  for (auto& p : op.fplans)
+    if (p->nrhs == nrhs && p->ok && p->prof.p) {
+      const int n = std::min(p->grid, max_ctas);
+      const size_t slots = p->prof.n / size_t(p->grid);
+      std::vector<i64> h(p->prof.n);
+      GK_CUDA(cudaDeviceSynchronize());
+      GK_CUDA(cudaMemcpy(h.data(), p->prof.p, sizeof(i64) * h.size(), cudaMemcpyDeviceToHost));
+      for (int c = 0; c < n; ++c)
+        for (int k = 0; k < 8; ++k) out[size_t(c) * 8 + k] = h[size_t(c) * slots + k];
+      if (const char* f = std::getenv("GK_FUSED_PROF_DUMP")) {
+        if (FILE* fp = std::fopen(f, "wb")) {
+          std::fwrite(h.data(), sizeof(i64), h.size(), fp);
+          std::fclose(fp);
+        }
+      }
+      return n;
+    }
+  return 0;
+}
 }  // namespace gk

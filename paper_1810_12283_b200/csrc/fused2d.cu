@@ -1,0 +1,787 @@
+// fused2d.cu — the whole D-SKI MVM for 2-D grids with gradients as ONE
+// persistent cooperative kernel (reference DskiOperator::mvm, dski.cpp:228-238:
+// stacked_transpose_apply → grid_operator.apply → stacked_apply + noise).
+//
+//   phase S  u  = B^T v          rolling-window scatter, atomic-free
+//   phase T1 y1 = (I ⊗ T_1) u    Toeplitz mode product along axis 1 (DMMA)
+//   phase T0 w  = (T_0 ⊗ I) y1   Toeplitz mode product along axis 0 (DMMA)
+//   phase G  out = B w + Σ v     rolling-window gather + noise
+//
+// Phases are separated by a grid-wide barrier; the grid intermediates stay
+// L2-resident. Every phase stages its operands in shared memory with
+// cp.async one step ahead of the compute (double buffering).
+//
+// Scatter (B^T): a CTA owns a strip of TC node columns × a segment of L cell
+// rows × a chunk of right-hand sides; thread (column, RP right-hand sides)
+// sweeps its cell rows upward keeping T register accumulators for node rows
+// b0..b0+T-1 (per RHS). Cell row b0's points that reach the strip are one
+// contiguous range of the cell-sorted order. After cell row b0 the thread
+// stores node row b0. Node rows b0+1..b0+T-1 left over at the end of the
+// segment are partial: they go to a halo buffer h, and phase T1 adds
+// h to u for those rows (a fixed two-term sum: deterministic). No point is
+// processed twice.
+//
+// Gather (B): a CTA owns a strip of cell columns × a segment of cell rows; a
+// ring of T+1 node rows (window columns × chunk) is kept in shared memory and
+// advanced one row per cell row; thread (point slot, RP right-hand sides)
+// contracts the 6×6 (4×4) stencil sum-factorised (weights of
+// interpolation.cpp:66-97, staged as (w, dw) pairs).
+//
+// Toeplitz (K_UU = T_0 ⊗ T_1, the same operator the reference applies by
+// circulant-embedding FFT, dski.cpp:146-166): DMMA m8n8k4 with A fragments
+// read from a per-CTA table indexed by tile diagonal (A[a][c] = t[|a-c|]
+// depends on a-c only), B slabs staged with 16-byte cp.async.
+#include <algorithm>
+#include <type_traits>
+
+#include "fused2d.hpp"
+
+namespace gk {
+
+namespace {
+
+constexpr int F2_THREADS = 256;
+
+struct F2Args {
+  int m0, m1, nb0, nb1, n;
+  const int4* base;
+  const double2* wd;  // [n][2][T] (w, dw) pairs: axis 0 then axis 1
+  const int* cell_start;
+  const double* t0;
+  const double* t1;
+  int band0, band1;
+  double nv2, ng2;
+  const double* v;
+  double* out;
+  double* u;
+  double* h;
+  double* y1;
+  double* w;
+  int nrhs, noise;
+  unsigned long long* bar;
+  unsigned long long* prof;
+  int BRP, BR, chunks;
+  int s_TC, s_strips, s_L, s_segs, s_pmax, s_csw;
+  int g_TC, g_strips, g_L, g_segs, g_pmax, g_nw;
+  int t_split;
+  int m0p, m1p;
+  int skip;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cpa4(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cpa8(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cpa16(void* s, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+template <int RP>
+__device__ __forceinline__ void cpa_rp(double* s, const double* g) {
+  if constexpr (RP == 2) cpa16(s, g);
+  else cpa8(s, g);
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cpa_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void cpa_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+#ifndef GK_BARRIER_SLEEP_NS
+#define GK_BARRIER_SLEEP_NS 256
+#endif
+constexpr unsigned kBarrierSleepNs = GK_BARRIER_SLEEP_NS;
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Grid-wide barrier on a monotonic 64-bit arrival counter (never reset: the
+// k-th barrier of a launch completes when the counter reaches a multiple of
+// gridDim.x). Arrival is a release atomic, waiting an acquire load, so the
+// CTA's prior global writes (ordered by __syncthreads) are visible to every
+// CTA after the barrier. Co-residency is guaranteed by the cooperative
+// launch; a bounded spin turns a logic error into a trap instead of a hang.
+__device__ __forceinline__ void grid_sync(unsigned long long* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;\n" : "=l"(t) : "l"(bar) : "memory");
+    const unsigned long long nb = gridDim.x;
+    const unsigned long long target = (t / nb + 1) * nb;
+    unsigned spins = 0;
+    while (ld_relaxed(bar) < target) {
+      if (++spins > (1u << 24)) __trap();
+      __nanosleep(kBarrierSleepNs);
+    }
+    asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+template <int RP>
+using vec_t = std::conditional_t<RP == 2, double2, double>;
+
+template <int RP>
+__device__ __forceinline__ void vload(const double* p, double (&x)[RP]) {
+  if constexpr (RP == 2) {
+    const double2 t = *reinterpret_cast<const double2*>(p);
+    x[0] = t.x;
+    x[1] = t.y;
+  } else {
+    x[0] = *p;
+  }
+}
+template <int RP>
+__device__ __forceinline__ void vstore(double* p, const double (&x)[RP]) {
+  if constexpr (RP == 2) *reinterpret_cast<double2*>(p) = make_double2(x[0], x[1]);
+  else *p = x[0];
+}
+
+constexpr int kProfSlots = 64;
+__device__ __forceinline__ void stamp(const F2Args& a, int k) {
+  if (a.prof != nullptr && threadIdx.x == 0 && k < kProfSlots) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.prof[blockIdx.x * kProfSlots + k] = t;
+  }
+}
+
+// ---------------------------------------------------------------- phase S
+template <int T, int RP>
+__device__ void f2_scatter(const F2Args& a, double* sm) {
+  const int BR = a.BR, tid = threadIdx.x, pmax = a.s_pmax;
+  double2* Wp = reinterpret_cast<double2*>(sm);           // [2][pmax][2T]
+  double* Vb = sm + 2 * pmax * 2 * T * 2;                  // [2][pmax][3][BR]
+  int* Bb = reinterpret_cast<int*>(Vb + 2 * pmax * 3 * BR);  // [2][pmax]
+  int* CS = Bb + 2 * pmax;                                 // [L][csw]
+  const int bl = tid % a.BRP, cslot = tid / a.BRP;
+  const int qstep = F2_THREADS / a.BRP;
+  const int items = a.s_strips * a.s_segs * a.chunks;
+  const size_t gstride = (size_t)a.n * a.nrhs;
+  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    const int strip = item % a.s_strips;
+    const int rest = item / a.s_strips;
+    const int seg = rest % a.s_segs, chunk = rest / a.s_segs;
+    const int C = strip * a.s_TC, Cend = min(C + a.s_TC, a.m1);
+    const int R = seg * a.s_L, Rend = min(R + a.s_L, a.nb0);
+    const int bc0 = chunk * BR, bcn = min(BR, a.nrhs - bc0);
+    const int clo = max(0, C - (T - 1)), chi = min(a.nb1 - 1, Cend - 1);
+    const int csw = chi - clo + 2;
+    const int nrows = Rend - R;
+    const int col = C + cslot;
+    const int rb = bc0 + bl * RP;  // first right-hand side of this thread
+    const bool lane_ok = bl * RP < bcn;
+    const bool active = cslot < a.s_TC && col < Cend && lane_ok;
+    __syncthreads();  // previous item done with CS and the stage buffers
+    for (int e = tid; e < nrows * csw; e += F2_THREADS) {
+      const int r = e / csw, c = e - r * csw;
+      CS[e] = __ldg(a.cell_start + (size_t)(R + r) * a.nb1 + clo + c);
+    }
+    __syncthreads();
+    auto issue = [&](int i, int buf) {
+      const int* cs = CS + i * csw;
+      const int P0 = cs[0], cnt = cs[csw - 1] - P0;
+      const double2* wsrc = a.wd + (size_t)P0 * 2 * T;
+      double2* wdst = Wp + (size_t)buf * pmax * 2 * T;
+      for (int e = tid; e < cnt * 2 * T; e += F2_THREADS) cpa16(wdst + e, wsrc + e);
+      double* vdst = Vb + (size_t)buf * pmax * 3 * BR;
+      if (lane_ok) {
+        const double* vsrc = a.v + (size_t)P0 * a.nrhs + rb;
+        for (int q = cslot; q < 3 * cnt; q += qstep) {
+          const int g = q >= 2 * cnt ? 2 : (q >= cnt ? 1 : 0);
+          const int p = q - g * cnt;
+          cpa_rp<RP>(vdst + (p * 3 + g) * BR + bl * RP, vsrc + g * gstride + (size_t)p * a.nrhs);
+        }
+      }
+      int* bdst = Bb + buf * pmax;
+      for (int p = tid; p < cnt; p += F2_THREADS) cpa4(bdst + p, &a.base[P0 + p].y);
+      cpa_commit();
+    };
+    double acc[T][RP];
+#pragma unroll
+    for (int t = 0; t < T; ++t)
+#pragma unroll
+      for (int k = 0; k < RP; ++k) acc[t][k] = 0.0;
+    const int tlo = max(0, col - (T - 1)) - clo, thi = min(a.nb1 - 1, col) - clo;
+    stamp(a, 8);
+    if (nrows > 0) issue(0, 0);
+    for (int i = 0; i < nrows; ++i) {
+      const int buf = i & 1;
+      if (i + 1 < nrows) {
+        issue(i + 1, buf ^ 1);
+        cpa_wait1();
+      } else {
+        cpa_wait0();
+      }
+      __syncthreads();
+      stamp(a, 9 + 9 * i);
+      if (active && tlo <= thi) {
+        const int* cs = CS + i * csw;
+        const int P0 = cs[0];
+        const int q0 = cs[tlo] - P0, q1 = cs[thi + 1] - P0;
+        const double2* W = Wp + (size_t)buf * pmax * 2 * T;
+        const double* V = Vb + (size_t)buf * pmax * 3 * BR + bl * RP;
+        const int* B1 = Bb + buf * pmax;
+#pragma unroll 2
+        for (int p = q0; p < q1; ++p) {
+          const int tl = col - B1[p];
+          const double2* wr = W + p * 2 * T;
+          const double* vr = V + p * 3 * BR;
+          double v0[RP], v1[RP], v2[RP];
+          vload<RP>(vr, v0);
+          vload<RP>(vr + BR, v1);
+          vload<RP>(vr + 2 * BR, v2);
+          const double2 w1 = wr[T + tl];
+          double A[RP], Cc[RP];
+#pragma unroll
+          for (int k = 0; k < RP; ++k) {
+            A[k] = fma(w1.y, v2[k], w1.x * v0[k]);
+            Cc[k] = w1.x * v1[k];
+          }
+#pragma unroll
+          for (int t0 = 0; t0 < T; ++t0) {
+            const double2 w0 = wr[t0];
+#pragma unroll
+            for (int k = 0; k < RP; ++k) acc[t0][k] = fma(w0.y, Cc[k], fma(w0.x, A[k], acc[t0][k]));
+          }
+        }
+      }
+      if (a.prof != nullptr && (threadIdx.x & 31) == 0 && 10 + 9 * i + (threadIdx.x >> 5) < kProfSlots) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.prof[blockIdx.x * kProfSlots + 10 + 9 * i + (threadIdx.x >> 5)] = t;
+      }
+      if (active) vstore<RP>(a.u + ((size_t)(R + i) * a.m1 + col) * a.nrhs + rb, acc[0]);
+#pragma unroll
+      for (int t = 0; t < T - 1; ++t)
+#pragma unroll
+        for (int k = 0; k < RP; ++k) acc[t][k] = acc[t + 1][k];
+#pragma unroll
+      for (int k = 0; k < RP; ++k) acc[T - 1][k] = 0.0;
+      __syncthreads();
+    }
+    // node rows Rend..Rend+T-2: final for the last segment, else the halo
+    // part that phase T1 adds to the next segment's head rows
+    if (active) {
+      double* dst = Rend == a.nb0 ? a.u : a.h;
+#pragma unroll
+      for (int t = 0; t < T - 1; ++t)
+        vstore<RP>(dst + ((size_t)(Rend + t) * a.m1 + col) * a.nrhs + rb, acc[t]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- phase T
+// Y[p][a][q] = Σ_c t[|a-c|] X[p][c][q] (+ halo rows of X added first).
+// Items: (8 (p, q) columns) × (row split); the whole M×8 B slab is staged.
+// A fragment for m-tile mt, k-step kk depends on D = 2mt - kk/4 only; the
+// table F[D][lane] is built once per phase.
+struct HaloSpec {
+  const double* h;  // null: no halo
+  int L, segs, T;
+  __device__ __forceinline__ bool row(int p) const {
+    if (h == nullptr) return false;
+    const int k = p / L;
+    return k >= 1 && k < segs && p - k * L <= T - 2;
+  }
+};
+
+__device__ __noinline__ void f2_toeplitz(const double* ts, int M, int Mp, int band, int P, int Q, const double* X,
+                            HaloSpec halo, double* Y, double* sm, int nsplit) {
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32, g = lane / 4, t4 = lane % 4;
+  const int ncols = P * Q, cgroups = (ncols + 7) / 8, items = cgroups * nsplit;
+  const int mtiles = Mp / 8, kq = Mp / 4;
+  const int ND = mtiles * 2 + kq;  // D + kq - 1 ∈ [0, ND)
+  double* F = sm;                          // [ND][32]
+  double* Bs0 = F + ND * 32;               // [Mp][8]
+  double* Bs1 = Bs0 + Mp * 8;
+  double* Hs0 = Bs1 + Mp * 8;              // [Mp][8] halo staging, one per B buffer
+  double* Hs1 = Hs0 + Mp * 8;
+  const bool contiguous = (Q % 8) == 0;
+  __syncthreads();
+  for (int e = tid; e < ND * 32; e += F2_THREADS) {
+    const int D = e / 32 - (kq - 1), ln = e % 32;
+    int x = 4 * D + ln / 4 - ln % 4;
+    x = x < 0 ? -x : x;
+    F[e] = x < M ? ts[x] : 0.0;
+  }
+  for (int e = tid; e < (Mp - M) * 8; e += F2_THREADS) {  // padding rows stay zero
+    Bs0[M * 8 + e] = 0.0;
+    Bs1[M * 8 + e] = 0.0;
+  }
+  auto issue = [&](int cg, double* B, double* Hs) {
+    const int col0 = cg * 8;
+    if (contiguous) {
+      const int p = col0 / Q, q = col0 - p * Q;
+      const double* src = X + (size_t)p * M * Q + q;
+      for (int e = tid; e < M * 4; e += F2_THREADS) {
+        const int c = e >> 2, k = e & 3;
+        cpa16(B + c * 8 + 2 * k, src + (size_t)c * Q + 2 * k);
+      }
+      if (halo.row(p)) {
+        const double* hs = halo.h + (size_t)p * M * Q + q;
+        for (int e = tid; e < M * 4; e += F2_THREADS) {
+          const int c = e >> 2, k = e & 3;
+          cpa16(Hs + c * 8 + 2 * k, hs + (size_t)c * Q + 2 * k);
+        }
+      }
+    } else {
+#pragma unroll 1
+      for (int e = tid; e < M * 8; e += F2_THREADS) {
+        const int c = e >> 3, j = e & 7;
+        const int col = col0 + j;
+        double val = 0.0;
+        if (col < ncols) {
+          const int p = col / Q, q = col - p * Q;
+          const size_t o = (size_t)p * M * Q + q + (size_t)c * Q;
+          val = X[o];
+          if (halo.row(p)) val += halo.h[o];
+        }
+        B[c * 8 + j] = val;
+      }
+    }
+    cpa_commit();
+  };
+  int buf = 0;
+  if ((int)blockIdx.x < items) issue(blockIdx.x / nsplit, Bs0, Hs0);
+  // nsplit is 1 or 2: item -> (column group, split) without integer division
+  const int sh = nsplit == 2 ? 1 : 0;
+  const int per = (mtiles + nsplit - 1) >> sh;
+  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    const int cg = it >> sh, sp = it - (cg << sh);
+    const int nxt = it + gridDim.x;
+    // the next item reuses the staged slab when it has the same column group
+    // (never with gridDim >= nsplit); otherwise prefetch into the other buffer
+    const int nxt_cg = nxt < items ? nxt >> sh : -1;
+    if (nxt_cg >= 0 && nxt_cg != cg) {
+      issue(nxt_cg, buf ? Bs0 : Bs1, buf ? Hs0 : Hs1);
+      cpa_wait1();
+    } else {
+      cpa_wait0();
+    }
+    const int col0 = cg * 8;
+    // one division per item: (p, q) of the first column and the output base
+    const int p0 = col0 / Q, q0 = col0 - p0 * Q;
+    double* const Yb = Y + (size_t)p0 * M * Q + q0;
+    const bool hrow = contiguous && halo.row(p0);
+    __syncthreads();
+    double* B = buf ? Bs1 : Bs0;
+    const double* Hs = buf ? Hs1 : Hs0;
+    if (hrow) {  // u + h for the halo rows
+      for (int e = tid; e < M * 8; e += F2_THREADS) B[e] += Hs[e];
+      __syncthreads();
+    }
+    const int mt_lo = sp * per, mt_hi = min(mtiles, mt_lo + per);
+    constexpr int NW = F2_THREADS / 32;
+    auto store = [&](int mt, double r0, double r1) {
+      const int ar = mt * 8 + g;
+      if (ar >= M) return;
+      if (contiguous) {
+        *reinterpret_cast<double2*>(Yb + (size_t)ar * Q + 2 * t4) = make_double2(r0, r1);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = col0 + 2 * t4 + e;
+          if (col < ncols) {
+            const int p = col / Q, q = col - p * Q;
+            Y[(size_t)p * M * Q + q + (size_t)ar * Q] = e ? r1 : r0;
+          }
+        }
+      }
+    };
+    // each warp runs up to two m-tiles in one k loop (4 independent DMMA
+    // chains, B fragment shared); k steps outside a tile's numerical band
+    // only add the tiny exact Toeplitz terms, so the union range is used
+    for (int mt0 = mt_lo + warp; mt0 < mt_hi; mt0 += 2 * NW) {
+      const int mt1 = mt0 + NW;
+      const bool two = mt1 < mt_hi;
+      const int mt_last = two ? mt1 : mt0;
+      const int k_lo = max(0, mt0 * 8 - band + 1) / 4 * 4;
+      const int k_hi = min(Mp, (mt_last * 8 + 7 + band + 4) / 4 * 4);
+      double x00 = 0.0, x01 = 0.0, x10 = 0.0, x11 = 0.0;  // tile 0: parity 0/1 chains
+      double y00 = 0.0, y01 = 0.0, y10 = 0.0, y11 = 0.0;  // tile 1
+      const double* F0 = F + (2 * mt0 + kq - 1) * 32 + lane;
+      const double* F1 = F + (2 * mt1 + kq - 1) * 32 + lane;
+      const double* Bp = B + t4 * 8 + g;
+      int kk = k_lo;
+      if (two) {
+#pragma unroll 2
+        for (; kk + 8 <= k_hi; kk += 8) {
+          const int j = kk >> 2;
+          const double b0 = Bp[kk * 8], b1 = Bp[(kk + 4) * 8];
+          const double f00 = F0[-j * 32], f01 = F0[-(j + 1) * 32];
+          const double f10 = F1[-j * 32], f11 = F1[-(j + 1) * 32];
+          dmma(x00, x01, f00, b0);
+          dmma(y00, y01, f10, b0);
+          dmma(x10, x11, f01, b1);
+          dmma(y10, y11, f11, b1);
+        }
+        if (kk < k_hi) {
+          const int j = kk >> 2;
+          const double b0 = Bp[kk * 8];
+          dmma(x00, x01, F0[-j * 32], b0);
+          dmma(y00, y01, F1[-j * 32], b0);
+        }
+        store(mt0, x00 + x10, x01 + x11);
+        store(mt1, y00 + y10, y01 + y11);
+      } else {
+#pragma unroll 2
+        for (; kk + 8 <= k_hi; kk += 8) {
+          const int j = kk >> 2;
+          const double b0 = Bp[kk * 8], b1 = Bp[(kk + 4) * 8];
+          dmma(x00, x01, F0[-j * 32], b0);
+          dmma(x10, x11, F0[-(j + 1) * 32], b1);
+        }
+        if (kk < k_hi) dmma(x00, x01, F0[-(kk >> 2) * 32], Bp[kk * 8]);
+        store(mt0, x00 + x10, x01 + x11);
+      }
+    }
+    __syncthreads();
+    if (nxt_cg >= 0 && nxt_cg != cg) buf ^= 1;
+  }
+}
+
+// ---------------------------------------------------------------- phase G
+template <int T, int RP>
+__device__ void f2_gather(const F2Args& a, double* sm) {
+  constexpr int SLOTS = T + 1;
+  const int BR = a.BR, tid = threadIdx.x, pmax = a.g_pmax, NW = a.g_nw;
+  double* ring = sm;                                           // [SLOTS][NW][BR]
+  double2* Wp = reinterpret_cast<double2*>(ring + ((SLOTS * NW * BR + 1) & ~1));  // [2][pmax][2T]
+  int* Bb = reinterpret_cast<int*>(Wp + 2 * pmax * 2 * T);     // [2][pmax]
+  int* CS = Bb + 2 * pmax;                                     // [L][2]
+  const int bl = tid % a.BRP, ps = tid / a.BRP, PS = F2_THREADS / a.BRP;
+  const int items = a.g_strips * a.g_segs * a.chunks;
+  const size_t gstride = (size_t)a.n * a.nrhs;
+  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    const int strip = item % a.g_strips;
+    const int rest = item / a.g_strips;
+    const int seg = rest % a.g_segs, chunk = rest / a.g_segs;
+    const int C = strip * a.g_TC, Cend = min(C + a.g_TC, a.nb1);
+    const int R = seg * a.g_L, Rend = min(R + a.g_L, a.nb0);
+    if (R >= Rend) continue;  // block-uniform
+    const int bc0 = chunk * BR, bcn = min(BR, a.nrhs - bc0);
+    const int rb = bc0 + bl * RP;
+    const bool lane_ok = bl * RP < bcn;
+    const int ncol = min(Cend + T - 1, a.m1) - C;
+    const int nrows = Rend - R;
+    __syncthreads();
+    for (int e = tid; e < nrows; e += F2_THREADS) {
+      CS[2 * e] = __ldg(a.cell_start + (size_t)(R + e) * a.nb1 + C);
+      CS[2 * e + 1] = __ldg(a.cell_start + (size_t)(R + e) * a.nb1 + Cend);
+    }
+    __syncthreads();
+    auto issue_row = [&](int r) {
+      double* dst = ring + (r % SLOTS) * NW * BR + bl * RP;
+      const double* src = a.w + ((size_t)r * a.m1 + C) * a.nrhs + rb;
+      if (lane_ok)
+        for (int c = ps; c < ncol; c += PS) cpa_rp<RP>(dst + c * BR, src + (size_t)c * a.nrhs);
+    };
+    auto issue_pts = [&](int i, int buf) {
+      const int P0 = CS[2 * i], cnt = CS[2 * i + 1] - P0;
+      const double2* wsrc = a.wd + (size_t)P0 * 2 * T;
+      double2* wdst = Wp + (size_t)buf * pmax * 2 * T;
+      for (int e = tid; e < cnt * 2 * T; e += F2_THREADS) cpa16(wdst + e, wsrc + e);
+      int* bdst = Bb + buf * pmax;
+      for (int p = tid; p < cnt; p += F2_THREADS) cpa4(bdst + p, &a.base[P0 + p].y);
+    };
+#pragma unroll 1
+    for (int t = 0; t < T; ++t) issue_row(R + t);
+    issue_pts(0, 0);
+    cpa_commit();
+    for (int i = 0; i < nrows; ++i) {
+      const int b0 = R + i, buf = i & 1;
+      if (i + 1 < nrows) {
+        issue_row(b0 + T);
+        issue_pts(i + 1, buf ^ 1);
+        cpa_commit();
+        cpa_wait1();
+      } else {
+        cpa_wait0();
+      }
+      __syncthreads();
+      const int P0 = CS[2 * i], cnt = CS[2 * i + 1] - P0;
+      const double2* W = Wp + (size_t)buf * pmax * 2 * T;
+      const int* B1 = Bb + buf * pmax;
+      const int sl0 = b0 % SLOTS;
+      if (lane_ok) {
+        for (int p = ps; p < cnt; p += PS) {
+          const double2* wr = W + p * 2 * T;
+          const int c0 = B1[p] - C;
+          double2 w1[T];
+#pragma unroll
+          for (int t1 = 0; t1 < T; ++t1) w1[t1] = wr[T + t1];
+          double o0[RP], o1[RP], o2[RP];
+#pragma unroll
+          for (int k = 0; k < RP; ++k) o0[k] = o1[k] = o2[k] = 0.0;
+#pragma unroll
+          for (int t0 = 0; t0 < T; ++t0) {
+            int sl = sl0 + t0;
+            if (sl >= SLOTS) sl -= SLOTS;
+            const double* rr = ring + (sl * NW + c0) * BR + bl * RP;
+            double r[RP], q[RP];
+#pragma unroll
+            for (int k = 0; k < RP; ++k) r[k] = q[k] = 0.0;
+#pragma unroll
+            for (int t1 = 0; t1 < T; ++t1) {
+              double x[RP];
+              vload<RP>(rr + t1 * BR, x);
+#pragma unroll
+              for (int k = 0; k < RP; ++k) {
+                r[k] += w1[t1].x * x[k];
+                q[k] += w1[t1].y * x[k];
+              }
+            }
+            const double2 w0 = wr[t0];
+#pragma unroll
+            for (int k = 0; k < RP; ++k) {
+              o0[k] += w0.x * r[k];
+              o1[k] += w0.y * r[k];
+              o2[k] += w0.x * q[k];
+            }
+          }
+          const size_t idx = (size_t)(P0 + p) * a.nrhs + rb;
+          if (a.noise) {
+            double n0[RP], n1[RP], n2[RP];
+            vload<RP>(a.v + idx, n0);
+            vload<RP>(a.v + idx + gstride, n1);
+            vload<RP>(a.v + idx + 2 * gstride, n2);
+#pragma unroll
+            for (int k = 0; k < RP; ++k) {
+              o0[k] += a.nv2 * n0[k];
+              o1[k] += a.ng2 * n1[k];
+              o2[k] += a.ng2 * n2[k];
+            }
+          }
+          vstore<RP>(a.out + idx, o0);
+          vstore<RP>(a.out + idx + gstride, o1);
+          vstore<RP>(a.out + idx + 2 * gstride, o2);
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+
+template <int T, int RP, int MINB>
+__global__ void __launch_bounds__(F2_THREADS, MINB) k_dski_mvm2d(F2Args a) {
+  extern __shared__ __align__(16) double f2_sm[];
+  double* ts0 = f2_sm;
+  double* ts1 = f2_sm + a.m0p;
+  double* work = ts1 + a.m1p;
+  stamp(a, 0);
+  for (int i = threadIdx.x; i < a.m0p; i += F2_THREADS) ts0[i] = i < a.m0 ? __ldg(a.t0 + i) : 0.0;
+  for (int i = threadIdx.x; i < a.m1p; i += F2_THREADS) ts1[i] = i < a.m1 ? __ldg(a.t1 + i) : 0.0;
+  __syncthreads();
+  if (!(a.skip & 1)) f2_scatter<T, RP>(a, work);
+  stamp(a, 1);
+  grid_sync(a.bar);
+  stamp(a, 2);
+  if (!(a.skip & 2)) f2_toeplitz(ts1, a.m1, a.m1p, a.band1, a.m0, a.nrhs, a.u, HaloSpec{a.h, a.s_L, a.s_segs, T}, a.y1, work,
+              a.t_split);
+  stamp(a, 3);
+  grid_sync(a.bar);
+  stamp(a, 4);
+  if (!(a.skip & 4)) f2_toeplitz(ts0, a.m0, a.m0p, a.band0, 1, a.m1 * a.nrhs, a.y1, HaloSpec{nullptr, 1, 0, T}, a.w, work,
+              a.t_split);
+  stamp(a, 5);
+  grid_sync(a.bar);
+  stamp(a, 6);
+  if (!(a.skip & 8)) f2_gather<T, RP>(a, work);
+  __syncthreads();
+  stamp(a, 7);
+}
+
+size_t smem_bytes(const Fused2dGeom& g, const Fused2dPlan& p) {
+  const int T = g.T;
+  const int m0p = (g.m0 + 7) / 8 * 8, m1p = (g.m1 + 7) / 8 * 8;
+  const size_t base = size_t(m0p + m1p) * 8;
+  const size_t S = size_t(2) * p.s_pmax * (2 * T * 16 + 3 * p.BR * 8) + size_t(2) * p.s_pmax * 4 +
+                   size_t(p.s_L) * p.s_csw * 4;
+  const int Mp = std::max(m0p, m1p);
+  const size_t Tp = size_t(Mp / 8 * 2 + Mp / 4) * 32 * 8 + size_t(4) * Mp * 8 * 8;
+  const size_t G = size_t(((T + 1) * p.g_nw * p.BR + 1) & ~1) * 8 + size_t(2) * p.g_pmax * 2 * T * 16 +
+                   size_t(2) * p.g_pmax * 4 + size_t(p.g_L) * 2 * 4;
+  return base + std::max({S, Tp, G}) + 64;
+}
+
+void decompose(const Fused2dGeom& g, const std::vector<int>& cs, Fused2dPlan& p, int ctas) {
+  const int T = g.T;
+  // scatter: TC node columns per strip (BRP threads per column), segments of
+  // >= T-1 cell rows (so each halo row has exactly two contributors)
+  // half the CTA's threads per strip: narrower strips give more items (measured
+  // faster at C1/C2 than filling every thread with a wider strip)
+  p.s_TC = std::max(1, F2_THREADS / 2 / p.BRP);
+  if (const int o = g_tuning.f2_stc.load(); o > 0) p.s_TC = std::min(p.s_TC, o);
+  p.s_strips = (g.m1 + p.s_TC - 1) / p.s_TC;
+  p.s_TC = (g.m1 + p.s_strips - 1) / p.s_strips;
+  int segs = std::max(1, std::min(g.nb0, ctas / std::max(1, p.s_strips * p.chunks)));
+  p.s_L = std::max(T - 1, (g.nb0 + segs - 1) / segs);
+  if (const int o = g_tuning.f2_sl.load(); o > 0) p.s_L = std::max(T - 1, o);
+  p.s_L = std::min(p.s_L, g.nb0);
+  p.s_segs = (g.nb0 + p.s_L - 1) / p.s_L;
+  p.s_csw = p.s_TC + T + 1;
+  p.s_pmax = 1;
+  for (int st = 0; st < p.s_strips; ++st) {
+    const int C = st * p.s_TC, Cend = std::min(C + p.s_TC, g.m1);
+    const int clo = std::max(0, C - (T - 1)), chi = std::min(g.nb1 - 1, Cend - 1);
+    if (clo > chi) continue;
+    for (int r = 0; r < g.nb0; ++r)
+      p.s_pmax = std::max(p.s_pmax, cs[size_t(r) * g.nb1 + chi + 1] - cs[size_t(r) * g.nb1 + clo]);
+  }
+  // gather: TC cell columns per strip
+  p.g_TC = std::max(1, std::min(g.nb1, p.BRP >= 8 ? 16 : 32));
+  if (const int o = g_tuning.f2_gtc.load(); o > 0) p.g_TC = std::min(g.nb1, o);
+  p.g_strips = (g.nb1 + p.g_TC - 1) / p.g_TC;
+  p.g_TC = (g.nb1 + p.g_strips - 1) / p.g_strips;
+  segs = std::max(1, std::min(g.nb0, ctas / std::max(1, p.g_strips * p.chunks)));
+  p.g_L = (g.nb0 + segs - 1) / segs;
+  if (const int o = g_tuning.f2_gl.load(); o > 0) p.g_L = std::min(g.nb0, o);
+  p.g_segs = (g.nb0 + p.g_L - 1) / p.g_L;
+  p.g_nw = p.g_TC + T - 1;
+  p.g_pmax = 1;
+  for (int st = 0; st < p.g_strips; ++st) {
+    const int C = st * p.g_TC, Cend = std::min(C + p.g_TC, g.nb1);
+    for (int r = 0; r < g.nb0; ++r)
+      p.g_pmax = std::max(p.g_pmax, cs[size_t(r) * g.nb1 + Cend] - cs[size_t(r) * g.nb1 + C]);
+  }
+  // Toeplitz: split the m-tiles of each 8-column group when there are few groups
+  const i64 cg = i64(std::max(g.m0, g.m1)) * p.nrhs / 8 + 1;  // 8-column groups of the mode-1 product
+  p.t_split = cg >= 2 * ctas ? 1 : 2;
+  if (const int o = g_tuning.f2_tsplit.load(); o > 0) p.t_split = o;
+}
+
+template <int T, int RP, int MINB>
+const void* kernel_ptr() {
+  return reinterpret_cast<const void*>(&k_dski_mvm2d<T, RP, MINB>);
+}
+
+template <int MINB>
+const void* pick_kernel_b(int T, int RP) {
+  if (T == 6) return RP == 2 ? kernel_ptr<6, 2, MINB>() : kernel_ptr<6, 1, MINB>();
+  return RP == 2 ? kernel_ptr<4, 2, MINB>() : kernel_ptr<4, 1, MINB>();
+}
+const void* pick_kernel(int T, int RP, int minb) {
+  return minb >= 4 ? pick_kernel_b<4>(T, RP) : pick_kernel_b<2>(T, RP);
+}
+
+}  // namespace
+
+void fused2d_plan(const Fused2dGeom& g, const std::vector<int>& cs, int nrhs, int device, Fused2dPlan& p) {
+  p.ok = false;
+  p.nrhs = nrhs;
+  if (nrhs < 1 || nrhs > kMaxRhs || (g.T != 6 && g.T != 4)) return;
+  if (g.m0 < g.T || g.m1 < g.T) return;
+  if (i64(g.m0) * g.m1 * nrhs >= (i64(1) << 31)) return;  // 32-bit column indices in phase T
+  p.RP = nrhs % 2 == 0 ? 2 : 1;
+  p.BRP = std::min(nrhs / p.RP, 32 / p.RP);
+  p.BR = p.BRP * p.RP;
+  p.chunks = (nrhs + p.BR - 1) / p.BR;
+  int sms = 0;
+  GK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  int per_sm = g_tuning.f2_per_sm.load() > 0 ? g_tuning.f2_per_sm.load() : 2;
+  p.minb = per_sm >= 4 ? 4 : 2;
+  const void* fn = pick_kernel(g.T, p.RP, p.minb);
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    decompose(g, cs, p, per_sm * sms);
+    p.smem = smem_bytes(g, p);
+    if (p.smem > 227 * 1024) return;
+    GK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p.smem)));
+    int occ = 0;
+    GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, F2_THREADS, p.smem));
+    if (occ < 1) return;
+    if (occ >= per_sm) break;
+    per_sm = occ;
+  }
+  p.grid = per_sm * sms;
+  if (const int o = g_tuning.f2_grid.load(); o > 0) p.grid = std::min(p.grid, o);
+  p.bar.alloc(1);
+  GK_CUDA(cudaMemset(p.bar.p, 0, sizeof(unsigned long long)));
+  p.ok = true;
+}
+
+void fused2d_mvm(const Fused2dGeom& g, Fused2dPlan& p, const double* v, double* out, double* u, double* h,
+                 double* y1, double* w, bool noise, cudaStream_t s) {
+  F2Args a{};
+  a.m0 = g.m0;
+  a.m1 = g.m1;
+  a.nb0 = g.nb0;
+  a.nb1 = g.nb1;
+  a.n = g.n;
+  a.base = g.base;
+  a.wd = g.wd;
+  a.cell_start = g.cell_start;
+  a.t0 = g.t0;
+  a.t1 = g.t1;
+  a.band0 = g.band0;
+  a.band1 = g.band1;
+  a.nv2 = g.nv2;
+  a.ng2 = g.ng2;
+  a.v = v;
+  a.out = out;
+  a.u = u;
+  a.h = h;
+  a.y1 = y1;
+  a.w = w;
+  a.nrhs = p.nrhs;
+  a.noise = noise ? 1 : 0;
+  a.bar = p.bar.p;
+  a.prof = nullptr;
+  if (g_tuning.fused_prof.load() != 0) {
+    if (p.prof.n < size_t(p.grid) * kProfSlots) {
+      p.prof.alloc(size_t(p.grid) * kProfSlots);
+      GK_CUDA(cudaMemset(p.prof.p, 0, sizeof(unsigned long long) * p.prof.n));
+    }
+    a.prof = p.prof.p;
+  }
+  a.BRP = p.BRP;
+  a.BR = p.BR;
+  a.chunks = p.chunks;
+  a.s_TC = p.s_TC;
+  a.s_strips = p.s_strips;
+  a.s_L = p.s_L;
+  a.s_segs = p.s_segs;
+  a.s_pmax = p.s_pmax;
+  a.s_csw = p.s_csw;
+  a.g_TC = p.g_TC;
+  a.g_strips = p.g_strips;
+  a.g_L = p.g_L;
+  a.g_segs = p.g_segs;
+  a.g_pmax = p.g_pmax;
+  a.g_nw = p.g_nw;
+  a.t_split = p.t_split;
+  a.skip = g_tuning.f2_skip.load();
+  a.m0p = (g.m0 + 7) / 8 * 8;
+  a.m1p = (g.m1 + 7) / 8 * 8;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(p.grid));
+  cfg.blockDim = dim3(F2_THREADS);
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void* args[] = {&a};
+  GK_CUDA(cudaLaunchKernelExC(&cfg, pick_kernel(g.T, p.RP, p.minb), args));
+  launched("dski fused 2-D MVM");
+}
+
+}  // namespace gk

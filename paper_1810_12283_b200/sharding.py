@@ -32,16 +32,19 @@ def shard_range(total: int, world: int, rank: int) -> tuple[int, int]:
     return lo, lo + base + (1 if rank < extra else 0)
 
 
-def gather_probe_estimates(local: np.ndarray, offset: int, total: int, group=None) -> np.ndarray:
+def gather_probe_estimates(local: np.ndarray, offset: int, total: int, group=None,
+                           device=None) -> np.ndarray:
     """All-gather per-probe estimates into global probe order (every rank gets
-    the full vector). ``local`` holds probes [offset, offset + len(local))."""
+    the full vector). ``local`` holds probes [offset, offset + len(local)).
+    ``device``: where the exchange buffers live (a CUDA device for NCCL, CPU
+    for gloo)."""
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
-    buf = torch.zeros(total, dtype=torch.float64)
-    buf[offset:offset + len(local)] = torch.as_tensor(local, dtype=torch.float64)
-    mask = torch.zeros(total, dtype=torch.float64)
+    buf = torch.zeros(total, dtype=torch.float64, device=device)
+    buf[offset:offset + len(local)] = torch.as_tensor(local, dtype=torch.float64, device=device)
+    mask = torch.zeros(total, dtype=torch.float64, device=device)
     mask[offset:offset + len(local)] = 1.0
     parts = [torch.zeros_like(buf) for _ in range(world)]
     masks = [torch.zeros_like(mask) for _ in range(world)]
@@ -50,10 +53,10 @@ def gather_probe_estimates(local: np.ndarray, offset: int, total: int, group=Non
     cover = torch.stack(masks).sum(0)
     if not torch.all(cover == 1.0):
         raise RuntimeError("probe shards do not tile the probe range exactly once")
-    out = torch.zeros(total, dtype=torch.float64)
+    out = torch.zeros(total, dtype=torch.float64, device=device)
     for p, m in zip(parts, masks):
         out += p * m  # exactly one non-zero contribution per probe: no reordering error
-    return out.numpy()
+    return out.cpu().numpy()
 
 
 def ordered_mean(estimates: np.ndarray) -> float:

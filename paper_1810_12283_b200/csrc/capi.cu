@@ -159,6 +159,11 @@ int gk_set_tuning(const char* key, int value) {
                            : k == "f2_per_sm" ? &g_tuning.f2_per_sm
                            : k == "f2_skip" ? &g_tuning.f2_skip
                            : k == "f2_grid" ? &g_tuning.f2_grid
+                           : k == "f2_rp" ? &g_tuning.f2_rp
+                           : k == "f2_smode" ? &g_tuning.f2_smode
+                           : k == "f2_gmode" ? &g_tuning.f2_gmode
+                           : k == "f2_nspl" ? &g_tuning.f2_nspl
+                           : k == "f2_nst" ? &g_tuning.f2_nst
                                              : nullptr;
   if (!slot) return -1;
   g_tuning.gen.fetch_add(1);

@@ -906,7 +906,7 @@ struct DskiOp final : Op {
   DevBuf<i64> ext;        // internal row -> external row
   std::vector<i64> perm_h, inv_h;
   DevBuf<double> origin_d, h_d;
-  DevBuf<double> grid_u, grid_w, grid_t, grid_h;  // per-MVM grid scratch (guarded by mu / caller)
+  DevBuf<double> grid_u, grid_w, grid_t, grid_h, grid_p;  // per-MVM grid scratch (guarded by mu / caller)
   std::vector<int> cell_start_h;          // host copy (fused-plan sizing)
   std::vector<std::unique_ptr<Fused2dPlan>> fplans;  // one-launch d = 2 MVM plans, per nrhs
 
@@ -936,7 +936,8 @@ struct DskiOp final : Op {
     for (auto it = fplans.begin(); it != fplans.end(); ++it)
       if ((*it)->nrhs == nrhs) {
         if ((*it)->tuning_gen == gen) return (*it)->ok ? it->get() : nullptr;
-        fplans.erase(it);  // knobs changed: rebuild
+        fplans.erase(it);  // knobs changed: rebuild (captured graphs held the old plan)
+        ++epoch;
         break;
       }
     auto p = std::make_unique<Fused2dPlan>();
@@ -978,17 +979,24 @@ struct DskiOp final : Op {
   void kuu(const double* u, double* w, int nrhs, cudaStream_t s) const;
   void gather(const double* w, const double* v, double* out, int nrhs, bool noise, cudaStream_t s) const;
 
+  void grow(DevBuf<double>& b, size_t count) {
+    if (count > b.n) {
+      b.alloc(count);
+      ++epoch;  // invalidates captured MVM graphs
+    }
+  }
   void ensure_scratch(int nrhs) {
-    grid_u.reserve(static_cast<size_t>(M) * nrhs);
-    grid_w.reserve(static_cast<size_t>(M) * nrhs);
-    grid_t.reserve(static_cast<size_t>(M) * nrhs);
-    if (d == 2 && G == 2) grid_h.reserve(static_cast<size_t>(M) * nrhs);
+    grow(grid_u, static_cast<size_t>(M) * nrhs);
+    grow(grid_w, static_cast<size_t>(M) * nrhs);
+    grow(grid_t, static_cast<size_t>(M) * nrhs);
+    if (d == 2 && G == 2) grow(grid_h, static_cast<size_t>(M) * nrhs);
   }
 
   void mvm(const double* in, double* out, int nrhs, cudaStream_t s) override {
     ensure_scratch(nrhs);
     if (Fused2dPlan* fp = fused_plan(nrhs)) {
-      fused2d_mvm(geom2d(), *fp, in, out, grid_u.p, grid_h.p, grid_t.p, grid_w.p, true, s);
+      if (fp->s_mode == 1) grow(grid_p, static_cast<size_t>(fp->s_nbuf) * M * nrhs);
+      fused2d_mvm(geom2d(), *fp, in, out, grid_u.p, grid_h.p, grid_t.p, grid_w.p, grid_p.p, true, s);
       return;
     }
     scatter(in, grid_u.p, nrhs, s);
@@ -1403,7 +1411,7 @@ int dski_fused_phases(Op& o, int nrhs, i64* out, int max_ctas) {
   for (auto& p : op.fplans)
     if (p->nrhs == nrhs && p->ok && p->prof.p) {
       const int n = std::min(p->grid, max_ctas);
-      const size_t slots = p->prof.n / size_t(p->grid);
+      const size_t slots = 8;
       std::vector<i64> h(p->prof.n);
       GK_CUDA(cudaDeviceSynchronize());
       GK_CUDA(cudaMemcpy(h.data(), p->prof.p, sizeof(i64) * h.size(), cudaMemcpyDeviceToHost));

@@ -436,7 +436,9 @@ struct DskipOp final : Op {
   const Factor& second() const { return factors.size() > 1 ? *factors[1] : *ones; }
 
   void mvm(const double* in, double* out, int nrhs, cudaStream_t s) override {  // dskip.cpp:243-250
+    const size_t before = ws.partial.n + ws.C.n + ws.Cp.n;
     hadamard_pair(*factors[0], second(), in, nrhs, out, false, in, n_value, nv2, ng2, ws, s);
+    if (ws.partial.n + ws.C.n + ws.Cp.n != before) ++epoch;  // scratch moved: drop captured graphs
   }
   void dlogell(const double* in, double* out, int nrhs, cudaStream_t s) {  // dskip.cpp:266-274
     if (!track) fail(GK_ERR_LOGIC, "D-SKIP operator was built without derivative tracking");

@@ -32,6 +32,8 @@
 // read from a per-CTA table indexed by tile diagonal (A[a][c] = t[|a-c|]
 // depends on a-c only), B slabs staged with 16-byte cp.async.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "fused2d.hpp"
@@ -66,6 +68,11 @@ struct F2Args {
   int t_split;
   int m0p, m1p;
   int skip;
+  int s_mode, g_mode;  // 0: staged rolling kernels, 1: direct-load high-parallelism variants
+  int s_nbuf;          // direct scatter: number of partial grid buffers S
+  int s_nspl;          // staged scatter: threads sharing one (column, RHS pair), splitting its points
+  int s_nst;           // staged scatter: staging depth (cell rows in flight)
+  double* pbuf;        // direct scatter: S partial grid buffers, each M×nrhs
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -88,6 +95,35 @@ __device__ __forceinline__ void cpa_rp(double* s, const double* g) {
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cpa_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 __device__ __forceinline__ void cpa_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nWAIT_%=:\nmbarrier.try_wait.parity.shared.b64 P1, [%0], %1;\n@!P1 bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(b))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+// wait until at most n (0..3) most recent cp.async groups are pending
+__device__ __forceinline__ void cpa_wait_n(int n) {
+  switch (n) {
+    case 0: asm volatile("cp.async.wait_group 0;\n" ::: "memory"); break;
+    case 1: asm volatile("cp.async.wait_group 1;\n" ::: "memory"); break;
+    case 2: asm volatile("cp.async.wait_group 2;\n" ::: "memory"); break;
+    default: asm volatile("cp.async.wait_group 3;\n" ::: "memory"); break;
+  }
+}
 
 __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
   unsigned long long v;
@@ -152,7 +188,8 @@ __device__ __forceinline__ void vstore(double* p, const double (&x)[RP]) {
   else *p = x[0];
 }
 
-constexpr int kProfSlots = 64;
+constexpr int kProfSlots = 8;
+
 __device__ __forceinline__ void stamp(const F2Args& a, int k) {
   if (a.prof != nullptr && threadIdx.x == 0 && k < kProfSlots) {
     unsigned long long t;
@@ -163,16 +200,23 @@ __device__ __forceinline__ void stamp(const F2Args& a, int k) {
 
 // ---------------------------------------------------------------- phase S
 template <int T, int RP>
-__device__ void f2_scatter(const F2Args& a, double* sm) {
+__device__ void f2_scatter(const F2Args& a, double* sm, unsigned long long* mbar) {
   const int BR = a.BR, tid = threadIdx.x, pmax = a.s_pmax;
-  double2* Wp = reinterpret_cast<double2*>(sm);           // [2][pmax][2T]
-  double* Vb = sm + 2 * pmax * 2 * T * 2;                  // [2][pmax][3][BR]
-  int* Bb = reinterpret_cast<int*>(Vb + 2 * pmax * 3 * BR);  // [2][pmax]
-  int* CS = Bb + 2 * pmax;                                 // [L][csw]
+  const int NST = a.s_nst;                                 // staging depth (cell rows in flight)
+  double2* Wp = reinterpret_cast<double2*>(sm);           // [NST][pmax][2T]
+  double* Vb = sm + NST * pmax * 2 * T * 2;                // [NST][3][pmax][BR]
+  int4* Bb = reinterpret_cast<int4*>(Vb + ((NST * 3 * pmax * BR + 1) & ~1));  // [NST][pmax], 16-byte aligned
+  int* CS = reinterpret_cast<int*>(Bb + NST * pmax);       // [L][csw]
   const int bl = tid % a.BRP, cslot = tid / a.BRP;
-  const int qstep = F2_THREADS / a.BRP;
+  const int nspl = a.s_nspl, half = cslot % nspl, ccol = cslot / nspl;
+  double* X = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(CS + a.s_L * a.s_csw) + 15) &
+                                        ~uintptr_t(15));  // [nspl-1][T-1][TC][BR], 16-byte aligned
   const int items = a.s_strips * a.s_segs * a.chunks;
   const size_t gstride = (size_t)a.n * a.nrhs;
+  // TMA bulk copies (RP = 2: every source row is 16-byte aligned) or
+  // per-thread cp.async (odd RHS counts); both complete on mbar[buf]
+  const bool tma = RP == 2;
+  unsigned phase = 0;  // parity bit per stage buffer (uniform across threads)
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
     const int strip = item % a.s_strips;
     const int rest = item / a.s_strips;
@@ -183,10 +227,11 @@ __device__ void f2_scatter(const F2Args& a, double* sm) {
     const int clo = max(0, C - (T - 1)), chi = min(a.nb1 - 1, Cend - 1);
     const int csw = chi - clo + 2;
     const int nrows = Rend - R;
-    const int col = C + cslot;
+    const int col = C + ccol;
     const int rb = bc0 + bl * RP;  // first right-hand side of this thread
     const bool lane_ok = bl * RP < bcn;
-    const bool active = cslot < a.s_TC && col < Cend && lane_ok;
+    const bool active = ccol < a.s_TC && col < Cend && lane_ok;
+    auto xslot = [&](int h, int t) { return X + ((((h - 1) * (T - 1) + t) * a.s_TC + ccol) * BR + bl * RP); };
     __syncthreads();  // previous item done with CS and the stage buffers
     for (int e = tid; e < nrows * csw; e += F2_THREADS) {
       const int r = e / csw, c = e - r * csw;
@@ -196,21 +241,58 @@ __device__ void f2_scatter(const F2Args& a, double* sm) {
     auto issue = [&](int i, int buf) {
       const int* cs = CS + i * csw;
       const int P0 = cs[0], cnt = cs[csw - 1] - P0;
-      const double2* wsrc = a.wd + (size_t)P0 * 2 * T;
       double2* wdst = Wp + (size_t)buf * pmax * 2 * T;
-      for (int e = tid; e < cnt * 2 * T; e += F2_THREADS) cpa16(wdst + e, wsrc + e);
-      double* vdst = Vb + (size_t)buf * pmax * 3 * BR;
-      if (lane_ok) {
-        const double* vsrc = a.v + (size_t)P0 * a.nrhs + rb;
-        for (int q = cslot; q < 3 * cnt; q += qstep) {
-          const int g = q >= 2 * cnt ? 2 : (q >= cnt ? 1 : 0);
-          const int p = q - g * cnt;
-          cpa_rp<RP>(vdst + (p * 3 + g) * BR + bl * RP, vsrc + g * gstride + (size_t)p * a.nrhs);
+      double* vdst = Vb + (size_t)buf * 3 * pmax * BR;
+      int4* bdst = Bb + (size_t)buf * pmax;
+      if (tma) {
+        // the last warp issues (idle in the compute when the strip leaves it
+        // without a column), so bulk-copy issue latency overlaps the compute
+        const bool whole = BR == a.nrhs;  // one copy per derivative group
+        const int lane = tid - (F2_THREADS - 32);
+        if (lane >= 0) {
+          if (lane == 0) {
+            fence_proxy_async();
+            mbar_expect_tx(mbar + buf, unsigned(cnt) * unsigned(2 * T * 16 + 16 + 3 * BR * 8));
+            if (cnt > 0) {
+              bulk_g2s(wdst, a.wd + (size_t)P0 * 2 * T, unsigned(cnt) * 2 * T * 16, mbar + buf);
+              bulk_g2s(bdst, a.base + P0, unsigned(cnt) * 16, mbar + buf);
+              if (whole)
+                for (int g = 0; g < 3; ++g)
+                  bulk_g2s(vdst + (size_t)g * pmax * BR, a.v + g * gstride + (size_t)P0 * a.nrhs,
+                           unsigned(cnt) * BR * 8, mbar + buf);
+            }
+          }
+          if (!whole) {
+            __syncwarp();
+            for (int q = lane; q < 3 * cnt; q += 32) {
+              const int g = q >= 2 * cnt ? 2 : (q >= cnt ? 1 : 0);
+              const int p = q - g * cnt;
+              bulk_g2s(vdst + ((size_t)g * pmax + p) * BR, a.v + g * gstride + (size_t)(P0 + p) * a.nrhs + bc0,
+                       unsigned(BR) * 8, mbar + buf);
+            }
+          }
         }
+      } else {
+        for (int e = tid; e < cnt * 2 * T; e += F2_THREADS) cpa16(wdst + e, a.wd + (size_t)P0 * 2 * T + e);
+        for (int p = tid; p < cnt; p += F2_THREADS) cpa16(bdst + p, a.base + P0 + p);
+        if (lane_ok)
+          for (int q = cslot; q < 3 * cnt; q += F2_THREADS / a.BRP) {
+            const int g = q >= 2 * cnt ? 2 : (q >= cnt ? 1 : 0);
+            const int p = q - g * cnt;
+            cpa_rp<RP>(vdst + ((size_t)g * pmax + p) * BR + bl * RP,
+                       a.v + g * gstride + (size_t)(P0 + p) * a.nrhs + rb);
+          }
+        cpa_commit();
       }
-      int* bdst = Bb + buf * pmax;
-      for (int p = tid; p < cnt; p += F2_THREADS) cpa4(bdst + p, &a.base[P0 + p].y);
-      cpa_commit();
+    };
+    auto wait = [&](int buf) {
+      if (tma) {
+        mbar_wait(mbar + buf, (phase >> buf) & 1u);
+        phase ^= 1u << buf;
+      } else {
+        cpa_wait0();
+        __syncthreads();
+      }
     };
     double acc[T][RP];
 #pragma unroll
@@ -218,34 +300,28 @@ __device__ void f2_scatter(const F2Args& a, double* sm) {
 #pragma unroll
       for (int k = 0; k < RP; ++k) acc[t][k] = 0.0;
     const int tlo = max(0, col - (T - 1)) - clo, thi = min(a.nb1 - 1, col) - clo;
-    stamp(a, 8);
-    if (nrows > 0) issue(0, 0);
+    const int depth = tma ? NST : 1;  // cp.async path: single buffer, one row at a time
+    for (int j = 0; j < depth - 1 && j < nrows; ++j) issue(j, j);
     for (int i = 0; i < nrows; ++i) {
-      const int buf = i & 1;
-      if (i + 1 < nrows) {
-        issue(i + 1, buf ^ 1);
-        cpa_wait1();
-      } else {
-        cpa_wait0();
-      }
-      __syncthreads();
-      stamp(a, 9 + 9 * i);
+      const int buf = i % depth;
+      if (i + depth - 1 < nrows) issue(i + depth - 1, (i + depth - 1) % depth);
+      wait(buf);
       if (active && tlo <= thi) {
         const int* cs = CS + i * csw;
         const int P0 = cs[0];
         const int q0 = cs[tlo] - P0, q1 = cs[thi + 1] - P0;
         const double2* W = Wp + (size_t)buf * pmax * 2 * T;
-        const double* V = Vb + (size_t)buf * pmax * 3 * BR + bl * RP;
-        const int* B1 = Bb + buf * pmax;
+        const double* V = Vb + (size_t)buf * 3 * pmax * BR + bl * RP;
+        const int4* B4 = Bb + (size_t)buf * pmax;
 #pragma unroll 2
-        for (int p = q0; p < q1; ++p) {
-          const int tl = col - B1[p];
+        for (int p = q0 + half; p < q1; p += nspl) {
+          const int tl = col - B4[p].y;
           const double2* wr = W + p * 2 * T;
-          const double* vr = V + p * 3 * BR;
+          const double* vr = V + p * BR;
           double v0[RP], v1[RP], v2[RP];
           vload<RP>(vr, v0);
-          vload<RP>(vr + BR, v1);
-          vload<RP>(vr + 2 * BR, v2);
+          vload<RP>(vr + pmax * BR, v1);
+          vload<RP>(vr + 2 * pmax * BR, v2);
           const double2 w1 = wr[T + tl];
           double A[RP], Cc[RP];
 #pragma unroll
@@ -261,23 +337,48 @@ __device__ void f2_scatter(const F2Args& a, double* sm) {
           }
         }
       }
-      if (a.prof != nullptr && (threadIdx.x & 31) == 0 && 10 + 9 * i + (threadIdx.x >> 5) < kProfSlots) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        a.prof[blockIdx.x * kProfSlots + 10 + 9 * i + (threadIdx.x >> 5)] = t;
+      // node row R+i is complete: combine the point-split partials in fixed order
+      if (nspl > 1) {
+        if (active && half > 0) vstore<RP>(xslot(half, 0), acc[0]);
+        __syncthreads();
+        if (active && half == 0) {
+          for (int h = 1; h < nspl; ++h) {
+            double o[RP];
+            vload<RP>(xslot(h, 0), o);
+#pragma unroll
+            for (int k = 0; k < RP; ++k) acc[0][k] += o[k];
+          }
+          vstore<RP>(a.u + ((size_t)(R + i) * a.m1 + col) * a.nrhs + rb, acc[0]);
+        }
+      } else if (active) {
+        vstore<RP>(a.u + ((size_t)(R + i) * a.m1 + col) * a.nrhs + rb, acc[0]);
       }
-      if (active) vstore<RP>(a.u + ((size_t)(R + i) * a.m1 + col) * a.nrhs + rb, acc[0]);
 #pragma unroll
       for (int t = 0; t < T - 1; ++t)
 #pragma unroll
         for (int k = 0; k < RP; ++k) acc[t][k] = acc[t + 1][k];
 #pragma unroll
       for (int k = 0; k < RP; ++k) acc[T - 1][k] = 0.0;
-      __syncthreads();
+      __syncthreads();  // stage buffer `buf` and the exchange slots are free again
     }
     // node rows Rend..Rend+T-2: final for the last segment, else the halo
     // part that phase T1 adds to the next segment's head rows
-    if (active) {
+    if (nspl > 1) {
+      if (active && half > 0)
+#pragma unroll
+        for (int t = 0; t < T - 1; ++t) vstore<RP>(xslot(half, t), acc[t]);
+      __syncthreads();
+      if (active && half == 0)
+        for (int h = 1; h < nspl; ++h)
+#pragma unroll
+          for (int t = 0; t < T - 1; ++t) {
+            double o[RP];
+            vload<RP>(xslot(h, t), o);
+#pragma unroll
+            for (int k = 0; k < RP; ++k) acc[t][k] += o[k];
+          }
+    }
+    if (active && half == 0) {
       double* dst = Rend == a.nb0 ? a.u : a.h;
 #pragma unroll
       for (int t = 0; t < T - 1; ++t)
@@ -292,22 +393,56 @@ __device__ void f2_scatter(const F2Args& a, double* sm) {
 // A fragment for m-tile mt, k-step kk depends on D = 2mt - kk/4 only; the
 // table F[D][lane] is built once per phase.
 struct HaloSpec {
-  const double* h;  // null: no halo
-  int L, segs, T;
+  // mode 0: X as is; mode 1: X + h on the halo rows (staged scatter);
+  // mode 2: X ignored, X[p] = Σ_k P[k mod S][p] over the segments k whose
+  // rows cover p, summed in ascending k (direct scatter)
+  int mode;
+  const double* h;
+  size_t pstride;
+  int L, segs, T, S;
   __device__ __forceinline__ bool row(int p) const {
-    if (h == nullptr) return false;
+    if (mode != 1) return false;
     const int k = p / L;
     return k >= 1 && k < segs && p - k * L <= T - 2;
   }
+  __device__ __forceinline__ void krange(int p, int& klo, int& khi) const {
+    const int num = p - (L + T - 2);
+    klo = num <= 0 ? 0 : (num + L - 1) / L;
+    khi = min(segs - 1, p / L);
+  }
 };
+
+// X slab = Σ_k P[k mod S] (direct scatter's partial buffers), summed
+// synchronously in ascending k into the staging buffer B [M][8].
+__device__ __noinline__ void f2_sum_partials(const HaloSpec& halo, int M, int Q, int ncols, int col0, double* B) {
+#pragma unroll 1
+  for (int e = threadIdx.x; e < M * 8; e += F2_THREADS) {
+    const int c = e >> 3, j = e & 7;
+    const int col = col0 + j;
+    double val = 0.0;
+    if (col < ncols) {
+      const int p = col / Q, q = col - p * Q;
+      const size_t o = (size_t)p * M * Q + q + (size_t)c * Q;
+      int klo, khi;
+      halo.krange(p, klo, khi);
+#pragma unroll 1
+      for (int k = klo; k <= khi; ++k) val += __ldcg(halo.h + (size_t)(k % halo.S) * halo.pstride + o);
+    }
+    B[c * 8 + j] = val;
+  }
+}
 
 __device__ __noinline__ void f2_toeplitz(const double* ts, int M, int Mp, int band, int P, int Q, const double* X,
                             HaloSpec halo, double* Y, double* sm, int nsplit) {
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32, g = lane / 4, t4 = lane % 4;
   const int ncols = P * Q, cgroups = (ncols + 7) / 8, items = cgroups * nsplit;
   const int mtiles = Mp / 8, kq = Mp / 4;
-  const int ND = mtiles * 2 + kq;  // D + kq - 1 ∈ [0, ND)
-  double* F = sm;                          // [ND][32]
+  // diagonals D = 2mt - kk/4 the band-limited k loops can touch (the union
+  // range of a warp's two tiles 8 m-tiles apart adds at most 16 + 2)
+  const int Dmax = (band + 11) / 4 + 18;
+  const int Dlo = max(-(kq - 1), -Dmax), Dhi = min(2 * (mtiles - 1), Dmax);
+  const int ND = Dhi - Dlo + 1;
+  double* F = sm;                          // [ND][32], row D - Dlo
   double* Bs0 = F + ND * 32;               // [Mp][8]
   double* Bs1 = Bs0 + Mp * 8;
   double* Hs0 = Bs1 + Mp * 8;              // [Mp][8] halo staging, one per B buffer
@@ -315,7 +450,7 @@ __device__ __noinline__ void f2_toeplitz(const double* ts, int M, int Mp, int ba
   const bool contiguous = (Q % 8) == 0;
   __syncthreads();
   for (int e = tid; e < ND * 32; e += F2_THREADS) {
-    const int D = e / 32 - (kq - 1), ln = e % 32;
+    const int D = e / 32 + Dlo, ln = e % 32;
     int x = 4 * D + ln / 4 - ln % 4;
     x = x < 0 ? -x : x;
     F[e] = x < M ? ts[x] : 0.0;
@@ -326,7 +461,9 @@ __device__ __noinline__ void f2_toeplitz(const double* ts, int M, int Mp, int ba
   }
   auto issue = [&](int cg, double* B, double* Hs) {
     const int col0 = cg * 8;
-    if (contiguous) {
+    if (halo.mode == 2) {
+      f2_sum_partials(halo, M, Q, ncols, col0, B);
+    } else if (contiguous) {
       const int p = col0 / Q, q = col0 - p * Q;
       const double* src = X + (size_t)p * M * Q + q;
       for (int e = tid; e < M * 4; e += F2_THREADS) {
@@ -415,8 +552,8 @@ __device__ __noinline__ void f2_toeplitz(const double* ts, int M, int Mp, int ba
       const int k_hi = min(Mp, (mt_last * 8 + 7 + band + 4) / 4 * 4);
       double x00 = 0.0, x01 = 0.0, x10 = 0.0, x11 = 0.0;  // tile 0: parity 0/1 chains
       double y00 = 0.0, y01 = 0.0, y10 = 0.0, y11 = 0.0;  // tile 1
-      const double* F0 = F + (2 * mt0 + kq - 1) * 32 + lane;
-      const double* F1 = F + (2 * mt1 + kq - 1) * 32 + lane;
+      const double* F0 = F + (2 * mt0 - Dlo) * 32 + lane;
+      const double* F1 = F + (2 * mt1 - Dlo) * 32 + lane;
       const double* Bp = B + t4 * 8 + g;
       int kk = k_lo;
       if (two) {
@@ -453,6 +590,153 @@ __device__ __noinline__ void f2_toeplitz(const double* ts, int M, int Mp, int ba
     }
     __syncthreads();
     if (nxt_cg >= 0 && nxt_cg != cg) buf ^= 1;
+  }
+}
+
+// ---------------------------------------------------------------- direct variants
+// Scatter without shared-memory staging: one task = (segment of L cell rows,
+// node column, RHS pair); loads go straight to L1/L2 and the parallelism
+// (segments × columns × pairs threads) hides their latency. A segment's node
+// rows go to partial buffer P[seg mod S]; phase T1 sums the partials.
+template <int T, int RP>
+__device__ void f2_scatter_direct(const F2Args& a) {
+  const int L = a.s_L, S = a.s_nbuf;
+  const size_t pstride = (size_t)a.m0 * a.m1 * a.nrhs;
+  const size_t gstride = (size_t)a.n * a.nrhs;
+  const int ntask = a.s_segs * a.m1 * a.BRP * a.chunks;
+  for (int task = blockIdx.x * F2_THREADS + threadIdx.x; task < ntask; task += gridDim.x * F2_THREADS) {
+    int t = task;
+    const int bl = t % a.BRP;
+    t /= a.BRP;
+    const int col = t % a.m1;
+    t /= a.m1;
+    const int chunk = t % a.chunks;
+    const int seg = t / a.chunks;
+    const int rb = chunk * a.BR + bl * RP;
+    if (rb >= a.nrhs) continue;
+    const int R = seg * L, Rend = min(R + L, a.nb0);
+    const int clo = max(0, col - (T - 1)), chi = min(a.nb1 - 1, col);
+    double* P = a.pbuf + (size_t)(seg % S) * pstride + (size_t)col * a.nrhs + rb;
+    const size_t rstride = (size_t)a.m1 * a.nrhs;
+    double acc[T][RP];
+#pragma unroll
+    for (int i = 0; i < T; ++i)
+#pragma unroll
+      for (int k = 0; k < RP; ++k) acc[i][k] = 0.0;
+    for (int b0 = R; b0 < Rend; ++b0) {
+      const int s0 = __ldg(a.cell_start + (size_t)b0 * a.nb1 + clo);
+      const int s1 = __ldg(a.cell_start + (size_t)b0 * a.nb1 + chi + 1);
+#pragma unroll 2
+      for (int sp = s0; sp < s1; ++sp) {
+        const int tl = col - __ldg(&a.base[sp].y);
+        const double2* wr = a.wd + (size_t)sp * 2 * T;
+        const double* vr = a.v + (size_t)sp * a.nrhs + rb;
+        double v0[RP], v1[RP], v2[RP];
+        if constexpr (RP == 2) {
+          const double2 x0 = __ldg(reinterpret_cast<const double2*>(vr));
+          const double2 x1 = __ldg(reinterpret_cast<const double2*>(vr + gstride));
+          const double2 x2 = __ldg(reinterpret_cast<const double2*>(vr + 2 * gstride));
+          v0[0] = x0.x; v0[1] = x0.y; v1[0] = x1.x; v1[1] = x1.y; v2[0] = x2.x; v2[1] = x2.y;
+        } else {
+          v0[0] = __ldg(vr); v1[0] = __ldg(vr + gstride); v2[0] = __ldg(vr + 2 * gstride);
+        }
+        const double2 w1 = __ldg(wr + T + tl);
+        double A[RP], Cc[RP];
+#pragma unroll
+        for (int k = 0; k < RP; ++k) {
+          A[k] = fma(w1.y, v2[k], w1.x * v0[k]);
+          Cc[k] = w1.x * v1[k];
+        }
+#pragma unroll
+        for (int t0 = 0; t0 < T; ++t0) {
+          const double2 w0 = __ldg(wr + t0);
+#pragma unroll
+          for (int k = 0; k < RP; ++k) acc[t0][k] = fma(w0.y, Cc[k], fma(w0.x, A[k], acc[t0][k]));
+        }
+      }
+      vstore<RP>(P + (size_t)b0 * rstride, acc[0]);
+#pragma unroll
+      for (int i = 0; i < T - 1; ++i)
+#pragma unroll
+        for (int k = 0; k < RP; ++k) acc[i][k] = acc[i + 1][k];
+#pragma unroll
+      for (int k = 0; k < RP; ++k) acc[T - 1][k] = 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < T - 1; ++i) vstore<RP>(P + (size_t)(Rend + i) * rstride, acc[i]);
+  }
+}
+
+// Gather without staging: one task = (point, RHS pair); the 6×6 grid window
+// is read from L2 (w was just written by phase T0).
+template <int T, int RP>
+__device__ void f2_gather_direct(const F2Args& a) {
+  const size_t gstride = (size_t)a.n * a.nrhs;
+  const size_t rstride = (size_t)a.m1 * a.nrhs;
+  const int ntask = a.n * a.BRP * a.chunks;
+  for (int task = blockIdx.x * F2_THREADS + threadIdx.x; task < ntask; task += gridDim.x * F2_THREADS) {
+    int t = task;
+    const int bl = t % a.BRP;
+    t /= a.BRP;
+    const int chunk = t % a.chunks;
+    const int s = t / a.chunks;
+    const int rb = chunk * a.BR + bl * RP;
+    if (rb >= a.nrhs) continue;
+    const int4 bs = __ldg(a.base + s);
+    const double2* wr = a.wd + (size_t)s * 2 * T;
+    double2 w1[T];
+#pragma unroll
+    for (int t1 = 0; t1 < T; ++t1) w1[t1] = __ldg(wr + T + t1);
+    const double* wb = a.w + ((size_t)bs.x * a.m1 + bs.y) * a.nrhs + rb;
+    double o0[RP], o1[RP], o2[RP];
+#pragma unroll
+    for (int k = 0; k < RP; ++k) o0[k] = o1[k] = o2[k] = 0.0;
+#pragma unroll
+    for (int t0 = 0; t0 < T; ++t0) {
+      const double* rr = wb + (size_t)t0 * rstride;
+      double r[RP], q[RP];
+#pragma unroll
+      for (int k = 0; k < RP; ++k) r[k] = q[k] = 0.0;
+#pragma unroll
+      for (int t1 = 0; t1 < T; ++t1) {
+        double x[RP];
+        if constexpr (RP == 2) {
+          const double2 xx = __ldcg(reinterpret_cast<const double2*>(rr + (size_t)t1 * a.nrhs));
+          x[0] = xx.x;
+          x[1] = xx.y;
+        } else {
+          x[0] = __ldcg(rr + (size_t)t1 * a.nrhs);
+        }
+#pragma unroll
+        for (int k = 0; k < RP; ++k) {
+          r[k] = fma(w1[t1].x, x[k], r[k]);
+          q[k] = fma(w1[t1].y, x[k], q[k]);
+        }
+      }
+      const double2 w0 = __ldg(wr + t0);
+#pragma unroll
+      for (int k = 0; k < RP; ++k) {
+        o0[k] = fma(w0.x, r[k], o0[k]);
+        o1[k] = fma(w0.y, r[k], o1[k]);
+        o2[k] = fma(w0.x, q[k], o2[k]);
+      }
+    }
+    const size_t idx = (size_t)s * a.nrhs + rb;
+    if (a.noise) {
+      double n0[RP], n1[RP], n2[RP];
+      vload<RP>(a.v + idx, n0);
+      vload<RP>(a.v + idx + gstride, n1);
+      vload<RP>(a.v + idx + 2 * gstride, n2);
+#pragma unroll
+      for (int k = 0; k < RP; ++k) {
+        o0[k] = fma(a.nv2, n0[k], o0[k]);
+        o1[k] = fma(a.ng2, n1[k], o1[k]);
+        o2[k] = fma(a.ng2, n2[k], o2[k]);
+      }
+    }
+    vstore<RP>(a.out + idx, o0);
+    vstore<RP>(a.out + idx + gstride, o1);
+    vstore<RP>(a.out + idx + 2 * gstride, o2);
   }
 }
 
@@ -584,26 +868,41 @@ __global__ void __launch_bounds__(F2_THREADS, MINB) k_dski_mvm2d(F2Args a) {
   extern __shared__ __align__(16) double f2_sm[];
   double* ts0 = f2_sm;
   double* ts1 = f2_sm + a.m0p;
-  double* work = ts1 + a.m1p;
+  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(ts1 + a.m1p);  // 8 mbarriers
+  double* work = ts1 + a.m1p + 8;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 8; ++b) mbar_init(mbar + b, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   stamp(a, 0);
   for (int i = threadIdx.x; i < a.m0p; i += F2_THREADS) ts0[i] = i < a.m0 ? __ldg(a.t0 + i) : 0.0;
   for (int i = threadIdx.x; i < a.m1p; i += F2_THREADS) ts1[i] = i < a.m1 ? __ldg(a.t1 + i) : 0.0;
   __syncthreads();
-  if (!(a.skip & 1)) f2_scatter<T, RP>(a, work);
+  if (!(a.skip & 1)) {
+    if (a.s_mode == 1) f2_scatter_direct<T, RP>(a);
+    else f2_scatter<T, RP>(a, work, mbar);
+  }
   stamp(a, 1);
   grid_sync(a.bar);
   stamp(a, 2);
-  if (!(a.skip & 2)) f2_toeplitz(ts1, a.m1, a.m1p, a.band1, a.m0, a.nrhs, a.u, HaloSpec{a.h, a.s_L, a.s_segs, T}, a.y1, work,
-              a.t_split);
+  if (!(a.skip & 2)) {
+    const HaloSpec hs = a.s_mode == 1
+                            ? HaloSpec{2, a.pbuf, (size_t)a.m0 * a.m1 * a.nrhs, a.s_L, a.s_segs, T, a.s_nbuf}
+                            : HaloSpec{1, a.h, 0, a.s_L, a.s_segs, T, 1};
+    f2_toeplitz(ts1, a.m1, a.m1p, a.band1, a.m0, a.nrhs, a.u, hs, a.y1, work, a.t_split);
+  }
   stamp(a, 3);
   grid_sync(a.bar);
   stamp(a, 4);
-  if (!(a.skip & 4)) f2_toeplitz(ts0, a.m0, a.m0p, a.band0, 1, a.m1 * a.nrhs, a.y1, HaloSpec{nullptr, 1, 0, T}, a.w, work,
+  if (!(a.skip & 4)) f2_toeplitz(ts0, a.m0, a.m0p, a.band0, 1, a.m1 * a.nrhs, a.y1, HaloSpec{0, nullptr, 0, 1, 0, T, 1}, a.w, work,
               a.t_split);
   stamp(a, 5);
   grid_sync(a.bar);
   stamp(a, 6);
-  if (!(a.skip & 8)) f2_gather<T, RP>(a, work);
+  if (!(a.skip & 8)) {
+    if (a.g_mode == 1) f2_gather_direct<T, RP>(a);
+    else f2_gather<T, RP>(a, work);
+  }
   __syncthreads();
   stamp(a, 7);
 }
@@ -611,31 +910,55 @@ __global__ void __launch_bounds__(F2_THREADS, MINB) k_dski_mvm2d(F2Args a) {
 size_t smem_bytes(const Fused2dGeom& g, const Fused2dPlan& p) {
   const int T = g.T;
   const int m0p = (g.m0 + 7) / 8 * 8, m1p = (g.m1 + 7) / 8 * 8;
-  const size_t base = size_t(m0p + m1p) * 8;
-  const size_t S = size_t(2) * p.s_pmax * (2 * T * 16 + 3 * p.BR * 8) + size_t(2) * p.s_pmax * 4 +
-                   size_t(p.s_L) * p.s_csw * 4;
-  const int Mp = std::max(m0p, m1p);
-  const size_t Tp = size_t(Mp / 8 * 2 + Mp / 4) * 32 * 8 + size_t(4) * Mp * 8 * 8;
+  const size_t base = size_t(m0p + m1p) * 8 + 64;
+  const size_t S = size_t(p.s_nst) * p.s_pmax * (2 * T * 16 + 3 * p.BR * 8) + 8 + size_t(p.s_nst) * p.s_pmax * 16 +
+                   size_t(p.s_L * p.s_csw) * 4 + 16 +
+                   size_t(p.s_nspl - 1) * (T - 1) * p.s_TC * p.BR * 8;
+  auto tbytes = [&](int M, int band, bool halo) {
+    const int Mp = (M + 7) / 8 * 8, mtiles = Mp / 8, kq = Mp / 4;
+    const int Dmax = (band + 11) / 4 + 18;
+    const int ND = std::min(2 * (mtiles - 1), Dmax) - std::max(-(kq - 1), -Dmax) + 1;
+    return size_t(ND) * 32 * 8 + size_t(halo ? 4 : 2) * Mp * 8 * 8;
+  };
+  const bool halo1 = p.s_mode == 0 && p.nrhs % 8 == 0;  // mode-1 staging adds u + h slabs
+  const size_t Tp = std::max(tbytes(g.m1, g.band1, halo1), tbytes(g.m0, g.band0, false));
   const size_t G = size_t(((T + 1) * p.g_nw * p.BR + 1) & ~1) * 8 + size_t(2) * p.g_pmax * 2 * T * 16 +
                    size_t(2) * p.g_pmax * 4 + size_t(p.g_L) * 2 * 4;
-  return base + std::max({S, Tp, G}) + 64;
+  return base + std::max({p.s_mode == 0 ? S : size_t(0), Tp, p.g_mode == 0 ? G : size_t(0)}) + 64;
 }
 
 void decompose(const Fused2dGeom& g, const std::vector<int>& cs, Fused2dPlan& p, int ctas) {
   const int T = g.T;
-  // scatter: TC node columns per strip (BRP threads per column), segments of
-  // >= T-1 cell rows (so each halo row has exactly two contributors)
-  // half the CTA's threads per strip: narrower strips give more items (measured
-  // faster at C1/C2 than filling every thread with a wider strip)
-  p.s_TC = std::max(1, F2_THREADS / 2 / p.BRP);
-  if (const int o = g_tuning.f2_stc.load(); o > 0) p.s_TC = std::min(p.s_TC, o);
+  const int sm = g_tuning.f2_smode.load(), gm = g_tuning.f2_gmode.load();
+  p.s_mode = sm == 2 ? 1 : 0;
+  p.g_mode = gm == 1 ? 0 : 1;  // gather: direct loads by default (measured faster)
+  // scatter: strips of TC node columns (BRP × nspl threads per column) ×
+  // segments of >= T-1 cell rows (each halo row then has exactly two
+  // contributors). Narrow strips and many items beat wide, thread-filled
+  // strips (measured at C1/C2), so aim for about one item per CTA.
+  p.s_nspl = g_tuning.f2_nspl.load() > 0 ? g_tuning.f2_nspl.load() : 2;
+  p.s_nst = g_tuning.f2_nst.load() > 0 ? std::min(4, g_tuning.f2_nst.load()) : 3;
+  const int max_tc = std::max(1, F2_THREADS / p.s_nspl / p.BRP);
+  const int seg_max = std::max(1, g.nb0 / std::max(1, T - 1));
+  int strips = (g.m1 + max_tc - 1) / max_tc;
+  int segs = std::max(1, std::min(seg_max, (ctas + strips * p.chunks - 1) / (strips * p.chunks)));
+  if (strips * segs * p.chunks < ctas) strips = std::min(g.m1, (ctas + segs * p.chunks - 1) / (segs * p.chunks));
+  p.s_TC = (g.m1 + strips - 1) / strips;
+  if (const int o = g_tuning.f2_stc.load(); o > 0) p.s_TC = std::min(max_tc, o);
   p.s_strips = (g.m1 + p.s_TC - 1) / p.s_TC;
   p.s_TC = (g.m1 + p.s_strips - 1) / p.s_strips;
-  int segs = std::max(1, std::min(g.nb0, ctas / std::max(1, p.s_strips * p.chunks)));
   p.s_L = std::max(T - 1, (g.nb0 + segs - 1) / segs);
   if (const int o = g_tuning.f2_sl.load(); o > 0) p.s_L = std::max(T - 1, o);
   p.s_L = std::min(p.s_L, g.nb0);
   p.s_segs = (g.nb0 + p.s_L - 1) / p.s_L;
+  if (p.s_mode == 1) {  // direct: short segments, S partial buffers
+    p.s_L = g_tuning.f2_sl.load() > 0 ? g_tuning.f2_sl.load() : 2;
+    p.s_L = std::max(1, std::min(p.s_L, g.nb0));
+    p.s_segs = (g.nb0 + p.s_L - 1) / p.s_L;
+    p.s_nbuf = (p.s_L + T - 1 + p.s_L - 1) / p.s_L;
+  } else {
+    p.s_nbuf = 1;
+  }
   p.s_csw = p.s_TC + T + 1;
   p.s_pmax = 1;
   for (int st = 0; st < p.s_strips; ++st) {
@@ -663,7 +986,7 @@ void decompose(const Fused2dGeom& g, const std::vector<int>& cs, Fused2dPlan& p,
   }
   // Toeplitz: split the m-tiles of each 8-column group when there are few groups
   const i64 cg = i64(std::max(g.m0, g.m1)) * p.nrhs / 8 + 1;  // 8-column groups of the mode-1 product
-  p.t_split = cg >= 2 * ctas ? 1 : 2;
+  p.t_split = cg >= ctas / 2 ? 1 : 2;  // split only when there are very few column groups
   if (const int o = g_tuning.f2_tsplit.load(); o > 0) p.t_split = o;
 }
 
@@ -690,6 +1013,7 @@ void fused2d_plan(const Fused2dGeom& g, const std::vector<int>& cs, int nrhs, in
   if (g.m0 < g.T || g.m1 < g.T) return;
   if (i64(g.m0) * g.m1 * nrhs >= (i64(1) << 31)) return;  // 32-bit column indices in phase T
   p.RP = nrhs % 2 == 0 ? 2 : 1;
+  if (g_tuning.f2_rp.load() == 1) p.RP = 1;
   p.BRP = std::min(nrhs / p.RP, 32 / p.RP);
   p.BR = p.BRP * p.RP;
   p.chunks = (nrhs + p.BR - 1) / p.BR;
@@ -714,10 +1038,16 @@ void fused2d_plan(const Fused2dGeom& g, const std::vector<int>& cs, int nrhs, in
   p.bar.alloc(1);
   GK_CUDA(cudaMemset(p.bar.p, 0, sizeof(unsigned long long)));
   p.ok = true;
+  if (std::getenv("GK_FUSED_PLAN_PRINT"))
+    std::fprintf(stderr,
+                 "[fused2d] nrhs %d RP %d BR %d chunks %d grid %d smem %zu | S mode %d TC %d strips %d L %d segs %d "
+                 "pmax %d nspl %d nst %d nbuf %d | G mode %d TC %d strips %d L %d segs %d pmax %d | T split %d\n",
+                 p.nrhs, p.RP, p.BR, p.chunks, p.grid, p.smem, p.s_mode, p.s_TC, p.s_strips, p.s_L, p.s_segs, p.s_pmax,
+                 p.s_nspl, p.s_nst, p.s_nbuf, p.g_mode, p.g_TC, p.g_strips, p.g_L, p.g_segs, p.g_pmax, p.t_split);
 }
 
 void fused2d_mvm(const Fused2dGeom& g, Fused2dPlan& p, const double* v, double* out, double* u, double* h,
-                 double* y1, double* w, bool noise, cudaStream_t s) {
+                 double* y1, double* w, double* pbuf, bool noise, cudaStream_t s) {
   F2Args a{};
   a.m0 = g.m0;
   a.m1 = g.m1;
@@ -767,6 +1097,12 @@ void fused2d_mvm(const Fused2dGeom& g, Fused2dPlan& p, const double* v, double* 
   a.g_nw = p.g_nw;
   a.t_split = p.t_split;
   a.skip = g_tuning.f2_skip.load();
+  a.s_mode = p.s_mode;
+  a.g_mode = p.g_mode;
+  a.s_nbuf = p.s_nbuf;
+  a.s_nspl = p.s_nspl;
+  a.s_nst = p.s_nst;
+  a.pbuf = pbuf;
   a.m0p = (g.m0 + 7) / 8 * 8;
   a.m1p = (g.m1 + 7) / 8 * 8;
   cudaLaunchConfig_t cfg = {};

@@ -31,6 +31,10 @@ struct Fused2dPlan {
   int s_TC = 0, s_strips = 0, s_L = 0, s_segs = 0, s_pmax = 0, s_csw = 0;
   int g_TC = 0, g_strips = 0, g_L = 0, g_segs = 0, g_pmax = 0, g_nw = 0;
   int t_split = 1;
+  int s_mode = 0, g_mode = 0;  // 0 staged rolling, 1 direct-load variants
+  int s_nspl = 2;
+  int s_nst = 3;                // staged scatter: cell rows in flight              // staged scatter: threads splitting one column's points
+  int s_nbuf = 1;              // direct scatter: partial grid buffers (pbuf holds s_nbuf × M × nrhs)
   int tuning_gen = -1;  // g_tuning.gen the plan was built under
   int grid = 0;
   int minb = 2;  // __launch_bounds__ min blocks of the instantiation used
@@ -44,6 +48,6 @@ void fused2d_plan(const Fused2dGeom& g, const std::vector<int>& cell_start_h, in
 // out = B K_UU B^T v (+ noise): u, h, y1, w are M×nrhs grid scratch buffers
 // (h holds the scatter's segment-boundary halo rows).
 void fused2d_mvm(const Fused2dGeom& g, Fused2dPlan& p, const double* v, double* out, double* u,
-                 double* h, double* y1, double* w, bool noise, cudaStream_t s);
+                 double* h, double* y1, double* w, double* pbuf, bool noise, cudaStream_t s);
 
 }  // namespace gk

@@ -36,7 +36,8 @@ struct Tuning {
   std::atomic<int> scatter{0}, gather{0}, toeplitz{0}, precond{0}, fused{0}, fused_prof{0};
   // fused 2-D MVM decomposition overrides (0 = heuristic)
   std::atomic<int> f2_stc{0}, f2_sl{0}, f2_gtc{0}, f2_gl{0}, f2_tsplit{0}, f2_per_sm{0};
-  std::atomic<int> f2_skip{0}, f2_grid{0};  // debug: bitmask of phases to skip (1 S, 2 T1, 4 T0, 8 G)
+  std::atomic<int> f2_skip{0}, f2_grid{0}, f2_rp{0};
+  std::atomic<int> f2_smode{0}, f2_gmode{0}, f2_nspl{0}, f2_nst{0};  // 1 staged, 2 direct (0 = default)  // debug: bitmask of phases to skip (1 S, 2 T1, 4 T0, 8 G)
   std::atomic<int> gen{0};  // bumped by every gk_set_tuning call (cached plans rebuild)
 };
 extern Tuning g_tuning;
@@ -168,7 +169,11 @@ struct Op {
     int nrhs;
     cudaGraphExec_t exec;
     i64 nodes;
+    std::uint64_t epoch;
   };
+  // Bumped whenever scratch memory or launch plans a captured graph may
+  // reference are reallocated; cached graphs from older epochs are dropped.
+  std::uint64_t epoch = 0;
   std::vector<GraphEntry> graphs;
 
   void to_internal(const double* V, i64 ldv, double* I, int nrhs, cudaStream_t s) const;

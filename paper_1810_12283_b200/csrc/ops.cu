@@ -199,6 +199,17 @@ void Op::from_internal(const double* I, double* V, i64 ldv, int nrhs, cudaStream
 }
 
 void Op::mvm_graph(const double* in, double* out, int nrhs, cudaStream_t s) {
+  auto drop_stale = [&] {
+    for (auto it = graphs.begin(); it != graphs.end();) {
+      if (it->epoch != epoch) {
+        cudaGraphExecDestroy(it->exec);
+        it = graphs.erase(it);
+      } else {
+        ++it;
+      }
+    }
+  };
+  drop_stale();
   for (auto& g : graphs)
     if (g.in == in && g.out == out && g.nrhs == nrhs) {
       GK_CUDA(cudaGraphLaunch(g.exec, s));
@@ -208,12 +219,13 @@ void Op::mvm_graph(const double* in, double* out, int nrhs, cudaStream_t s) {
   if (!cap_stream) init_stream();
   mvm(in, out, nrhs, s);  // warm scratch (allocation must not happen during capture)
   GK_CUDA(cudaStreamSynchronize(s));
+  drop_stale();  // the warm call may have grown scratch
   const i64 before = g_launches.load();
   cudaGraph_t graph;
   GK_CUDA(cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeThreadLocal));
   mvm(in, out, nrhs, cap_stream);
   GK_CUDA(cudaStreamEndCapture(cap_stream, &graph));
-  GraphEntry e{in, out, nrhs, nullptr, g_launches.load() - before};
+  GraphEntry e{in, out, nrhs, nullptr, g_launches.load() - before, epoch};
   g_launches.fetch_sub(e.nodes);
   GK_CUDA(cudaGraphInstantiate(&e.exec, graph, 0));
   cudaGraphDestroy(graph);

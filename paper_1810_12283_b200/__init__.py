@@ -543,7 +543,7 @@ class PivotedCholeskyFactor:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and _lib is not None:
             _lib.gk_pivchol_destroy(h)
             self._h = None
 
@@ -619,7 +619,7 @@ class Preconditioner:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and _lib is not None:
             _lib.gk_precond_destroy(h)
             self._h = None
 

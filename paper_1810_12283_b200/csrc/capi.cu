@@ -151,6 +151,7 @@ int gk_set_tuning(const char* key, int value) {
                            : k == "precond" ? &g_tuning.precond
                            : k == "fused" ? &g_tuning.fused
                            : k == "fused_prof" ? &g_tuning.fused_prof
+                           : k == "pcg_fused" ? &g_tuning.pcg_fused
                            : k == "f2_stc" ? &g_tuning.f2_stc
                            : k == "f2_sl" ? &g_tuning.f2_sl
                            : k == "f2_gtc" ? &g_tuning.f2_gtc

@@ -1035,7 +1035,7 @@ static int grid_blocks(i64 items, int threads = 256) {
 }
 
 static void smem_attr(const void* fn, size_t bytes) {
-  if (bytes > 48 * 1024) GK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+  if (bytes > 48 * 1024) raise_smem_limit(fn, bytes);
 }
 
 // Lean-kernel launch shape: x = RHS lanes (≤ 32), y = items per block, shrunk

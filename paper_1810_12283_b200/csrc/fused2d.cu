@@ -33,10 +33,14 @@
 // depends on a-c only), B slabs staged with 16-byte cp.async.
 #include <algorithm>
 #include <cstdio>
+#include <mutex>
+#include <utility>
+#include <vector>
 #include <cstdlib>
 #include <type_traits>
 
 #include "fused2d.hpp"
+#include "gk_sync.cuh"
 
 namespace gk {
 
@@ -1026,7 +1030,10 @@ void fused2d_plan(const Fused2dGeom& g, const std::vector<int>& cs, int nrhs, in
     decompose(g, cs, p, per_sm * sms);
     p.smem = smem_bytes(g, p);
     if (p.smem > 227 * 1024) return;
-    GK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p.smem)));
+    raise_smem_limit(fn, p.smem);
+    // pin the L1/shared split to maximum shared memory: the cooperative-launch
+    // residency check must see the same occupancy as this plan
+    GK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, int(cudaSharedmemCarveoutMaxShared)));
     int occ = 0;
     GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, F2_THREADS, p.smem));
     if (occ < 1) return;

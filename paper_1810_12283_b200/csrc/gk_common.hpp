@@ -29,11 +29,14 @@ struct Error : std::runtime_error {
 }
 
 void cuda_check(cudaError_t e, const char* what);
+// Raise (never lower) a kernel's dynamic shared-memory limit: the attribute is
+// per function and shared by every plan/operator launching it.
+void raise_smem_limit(const void* fn, size_t bytes);
 #define GK_CUDA(x) ::gk::cuda_check((x), #x)
 
 // Process-wide kernel-variant knobs (gk_set_tuning); 0 = default.
 struct Tuning {
-  std::atomic<int> scatter{0}, gather{0}, toeplitz{0}, precond{0}, fused{0}, fused_prof{0};
+  std::atomic<int> scatter{0}, gather{0}, toeplitz{0}, precond{0}, fused{0}, fused_prof{0}, pcg_fused{0};
   // fused 2-D MVM decomposition overrides (0 = heuristic)
   std::atomic<int> f2_stc{0}, f2_sl{0}, f2_gtc{0}, f2_gl{0}, f2_tsplit{0}, f2_per_sm{0};
   std::atomic<int> f2_skip{0}, f2_grid{0}, f2_rp{0};

@@ -3,6 +3,8 @@
 // libstdc++ std::mt19937_64 / normal_distribution bit for bit), the
 // tridiagonal eigensolver for SLQ quadrature, a k×k Cholesky for the
 // preconditioner QR, Grid::cover, and the seeded synthetic datasets.
+#include <mutex>
+#include <utility>
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -139,6 +141,26 @@ void Op::init_stream() {
   GK_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   GK_CUDA(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
 }
+
+// The dynamic shared memory limit is a per-function attribute shared by every
+// plan (and operator) using that instantiation: only ever raise it, so a plan
+// built later with less shared memory cannot invalidate an earlier one.
+void raise_smem_limit(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, size_t>> limits;
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& l : limits)
+    if (l.first == fn) {
+      if (bytes > l.second) {
+        GK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+        l.second = bytes;
+      }
+      return;
+    }
+  GK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(std::max<size_t>(bytes, 48 * 1024))));
+  limits.emplace_back(fn, std::max<size_t>(bytes, 48 * 1024));
+}
+
 
 }  // namespace gk
 

@@ -307,8 +307,7 @@ void launch_toeplitz_slab(const double* t, int M, int band, i64 P, i64 Q, const 
   const int Mp = (M + 7) / 8 * 8;
   const size_t shm = sizeof(double) * (size_t(Mp) + size_t(Mp) * SB);
   if (shm > 48 * 1024)
-    GK_CUDA(cudaFuncSetAttribute((const void*)k_toeplitz_slab<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(shm)));
+    raise_smem_limit((const void*)k_toeplitz_slab<NT>, shm);
   const i64 ncols = P * Q;
   k_toeplitz_slab<NT><<<static_cast<unsigned>((ncols + BN - 1) / BN), 128, shm, s>>>(t, M, band, P, Q, X, Y);
   launched("toeplitz mode product (DMMA slab)");

@@ -19,6 +19,7 @@
 #include <limits>
 
 #include "gk_kernels.cuh"
+#include "pcg_fused.hpp"
 #include "solvers.hpp"
 
 namespace gk {
@@ -81,21 +82,7 @@ __global__ void k_dot_partial(const double* __restrict__ x, const double* __rest
 }
 
 // ---------------------------------------------------------------- PCG
-struct CgDev {
-  double* bnorm;
-  double* rz;
-  double* alpha;
-  double* beta;
-  double* hist;  // [(maxit+1)][nrhs]
-  int* active;
-  int* upd;
-  int* its;
-  int* conv;
-  int* nactive;  // single int
-  int maxit;
-  double tol;
-  int nrhs;
-};
+using CgDev = PcgState;
 
 // init: partial0 = ||b||², partial1 = r·z, partial2 = r·r (r = b)
 // One 32-thread block per column; partials reduced warp-cooperatively.
@@ -788,9 +775,34 @@ PcgResult pcg_internal(Op& op, Precond* M, const double* B, double* X, int nrhs,
   k_cg_init<<<nrhs, 32, 0, s>>>(st, p0, p1, p2);
   launched("pcg init");
 
+  // fused vector step (pcg_fused.cu): one cooperative kernel per iteration
+  // besides the MVM, instead of ten small kernels. Opt-in (tuning
+  // "pcg_fused" = 1): measured on C2 it is not yet faster than the separate
+  // kernels (its grid-barrier reductions cost more than the launches saved).
+  PcgVecPlan vplan;
+  const int kM = M ? int(M->k) : 0;
+  const bool vfused = g_tuning.pcg_fused.load() == 1 && pcg_vec_supported(nrhs, kM);
+  if (vfused) pcg_vec_prepare(vplan, N, nrhs, kM, op.device);
+
   // one iteration, captured as a graph
   auto iteration = [&](cudaStream_t cs) {
     op.mvm(Pb.p, AP.p, nrhs, cs);
+    if (vfused) {
+      PcgVecArgs va{};
+      va.st = st;
+      va.X = X;
+      va.R = R.p;
+      va.P = Pb.p;
+      va.AP = AP.p;
+      va.Z = Zb.p;
+      va.q1 = M ? M->q1.p : nullptr;
+      va.dinv = M ? M->dinv.p : nullptr;
+      va.k = kM;
+      va.N = N;
+      va.nrhs = nrhs;
+      pcg_vec_launch(vplan, va, cs);
+      return;
+    }
     k_dot_partial<<<RB, RT, 0, cs>>>(Pb.p, AP.p, N, nrhs, p0);
     launched("pcg dot");
     k_cg_fin_pAp<<<nrhs, 32, 0, cs>>>(st, p0);
@@ -846,6 +858,7 @@ PcgResult pcg_internal(Op& op, Precond* M, const double* B, double* X, int nrhs,
     cudaGraphExecDestroy(exec);
     cudaGraphDestroy(graph);
   }
+  if (vfused) pcg_vec_dump(vplan);
   cudaFreeHost(nact_h);
 
   PcgResult res;
@@ -873,7 +886,7 @@ Precond::~Precond() {
 
 static void set_smem(const void* fn, size_t bytes) {
   if (bytes > 48 * 1024)
-    GK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+    raise_smem_limit(fn, bytes);
 }
 
 void Precond::ensure(int nrhs) {

@@ -202,3 +202,40 @@ def test_dski_pipeline_matches_oracle_c1_subset():
     lg = gk.slq_logdet(g, 8, 25, 0, 0.5 * 0.05 ** 2)
     lr = O.slq_logdet(r, 8, 25, 0, 0.5 * 0.05 ** 2)
     assert abs(lg.logdet - lr.logdet) <= 1e-8 * abs(lr.logdet)
+
+
+@pytest.mark.parametrize("nrhs", [1, 8, 32])
+@pytest.mark.parametrize("with_precond", [True, False])
+def test_fused_pcg_step_matches_unfused(nrhs, with_precond):
+    """The one-launch PCG vector step (pcg_fused.cu) runs the same per-column
+    recurrences as the ten-kernel path: same iteration counts and flags,
+    solutions equal to roundoff, and both meet the oracle's well-conditioned
+    ±1 iteration parity."""
+    X, y, dY = _dski_model(1, 300)
+    grid = gk.Grid.cover(X, 1e-3, 3, 40)
+    noise = (0.5, 0.5)
+    g = gk.DskiOperator(gk.KernelSpec(0.15, 1.0), grid, X, noise)
+    M = gk.Preconditioner.from_pivchol(g, gk.pivoted_cholesky(g, 40, kernel_part=True)) if with_precond else None
+    rng = np.random.default_rng(nrhs)
+    B = rng.standard_normal((g.size(), nrhs))
+    B[:, 0] = gk.stacked_targets(y, dY, y.mean())
+    if nrhs > 2:
+        B[:, 2] = 0.0  # zero right-hand side: converged at 0 iterations
+    prev = gk.set_tuning("pcg_fused", 1)  # opt-in fused vector step
+    try:
+        fused = gk.cg(g, B if nrhs > 1 else B[:, 0], 1e-7, 3000, M)
+        gk.set_tuning("pcg_fused", 0)  # default: separate kernels
+        ref = gk.cg(g, B if nrhs > 1 else B[:, 0], 1e-7, 3000, M)
+    finally:
+        gk.set_tuning("pcg_fused", prev)
+    fused = fused if isinstance(fused, list) else [fused]
+    ref = ref if isinstance(ref, list) else [ref]
+    for f, r in zip(fused, ref):
+        assert f.converged == r.converged
+        # CG counts are roundoff-sensitive once they reach the hundreds (see
+        # oracle_iteration_band): ±2 or 6 %, whichever is larger
+        assert abs(f.iterations - r.iterations) <= max(2, 0.06 * r.iterations), (f.iterations, r.iterations)
+        # both meet relres <= 1e-7: they agree to ~tol × condition number
+        assert np.linalg.norm(f.x - r.x) <= 1e-4 * max(np.linalg.norm(r.x), 1e-300) or np.linalg.norm(r.x) == 0
+    if nrhs > 2:
+        assert fused[2].iterations == 0 and fused[2].converged

@@ -240,6 +240,13 @@ def run_gpu(args):
         dom = max(bytes_per, key=lambda k: staged_ms[k])
         dom_bytes, dom_ms = bytes_per[dom], staged_ms[dom]
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    traffic = None  # DRAM bytes per launch of the dominant kernel from the committed ncu capture
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "r1_traffic.json")))
+        if dom in tj:
+            traffic = tj[dom]["dram_bytes_read"] + tj[dom]["dram_bytes_write"]
+    except Exception:
+        traffic = None
 
     # ---- end to end through the public API with host (pinned) buffers
     Hin = torch.from_numpy(np.asfortranarray(Bh).T.copy()).pin_memory()  # (nrhs, N) == col-major
@@ -310,7 +317,8 @@ def run_gpu(args):
                     "path": "gk_op_mvm (C-ABI, pinned host buffers, permutes + copies timed)"},
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
-                         "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                         "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
+                         "traffic_source": "profiles/r1_traffic.json (ncu --set full, one launch)",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if peaks else "fallback",
                          "bytes_per_launch": dom_bytes, "launch_ms": dom_ms,
                          "bytes_formula": "SURVEY 8(d): 8*(3*N*B + 2*n*d + 4*m*B + M_c)",

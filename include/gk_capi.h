@@ -51,8 +51,8 @@ int64_t gk_last_error_point(void);
 const char* gk_version(void);
 /* Kernel-variant selection for tuning/A-B timing (process-wide). Keys:
  * "scatter", "gather", "toeplitz", "precond" (0 = default choice), "fused"
- * (1 = disable the one-launch 2-D MVM), "pcg_fused" (1 = one-launch PCG
- * vector step, opt-in), "fused_prof" and "f2_*" decomposition overrides.
+ * (1 = disable the one-launch 2-D MVM), "pcg_fused" (0/1 = one-launch PCG
+ * vector step where supported, 2 = separate kernels), "fused_prof" and "f2_*" decomposition overrides.
  * Returns the old value. */
 int gk_set_tuning(const char* key, int value);
 /* Number of CUDA kernels this library has launched in this process. */

@@ -132,16 +132,40 @@ __global__ void k_cg_fin_pAp(CgDev st, const double* __restrict__ partial) {
   st.its[b] += 1;
 }
 
-// x += a p; r -= a Ap for updating columns; partial ||r||²
+// alpha = rz / pAp (linalg.cpp:110-118) evaluated by every CTA from the pAp
+// partials (fixed-order sums: identical everywhere), then x += a p,
+// r -= a Ap on this CTA's rows and ||r||² partials. No state is written here:
+// k_cg_fin_rr re-derives the same decision and updates the column state
+// (a CTA writing state other CTAs still read would race).
+__device__ __forceinline__ bool cg_alpha(const CgDev& st, int b, double pAp, double& alpha) {
+  alpha = 0.0;
+  if (!st.active[b] || st.its[b] >= st.maxit || pAp <= 0.0) return false;
+  alpha = st.rz[b] / pAp;
+  return true;
+}
+
 __global__ void k_cg_axpy(CgDev st, double* __restrict__ X, double* __restrict__ R, const double* __restrict__ P,
-                          const double* __restrict__ AP, i64 rows, double* __restrict__ partial) {
+                          const double* __restrict__ AP, i64 rows, const double* __restrict__ p_pAp,
+                          double* __restrict__ partial) {
   __shared__ double sm[RT];
+  __shared__ double s_alpha[RT];
+  __shared__ int s_upd[RT];
   const int nrhs = st.nrhs;
+  const int warp = threadIdx.x / 32;
+  for (int c = warp; c < nrhs; c += RT / 32) {
+    const double pAp = warp_sum_partials(p_pAp, RB, nrhs, c);
+    if ((threadIdx.x & 31) == 0) {
+      double a;
+      s_upd[c] = cg_alpha(st, c, pAp, a) ? 1 : 0;
+      s_alpha[c] = a;
+    }
+  }
+  __syncthreads();
   const int slots = blockDim.x / nrhs;
   const int b = threadIdx.x % nrhs, slot = threadIdx.x / nrhs;
   double acc = 0.0;
-  if (slot < slots && st.upd[b]) {
-    const double a = st.alpha[b];
+  if (slot < slots && s_upd[b]) {
+    const double a = s_alpha[b];
     i64 r0, r1;
     row_range(rows, r0, r1);
     for (i64 r = r0 + slot; r < r1; r += slots) {
@@ -155,11 +179,19 @@ __global__ void k_cg_axpy(CgDev st, double* __restrict__ X, double* __restrict__
   block_col_store(acc, nrhs, partial, sm);
 }
 
-__global__ void k_cg_fin_rr(CgDev st, const double* __restrict__ partial) {
+__global__ void k_cg_fin_rr(CgDev st, const double* __restrict__ p_pAp, const double* __restrict__ partial) {
   const int b = blockIdx.x;
+  const double pAp = warp_sum_partials(p_pAp, RB, st.nrhs, b);
   const double rr = warp_sum_partials(partial, RB, st.nrhs, b);
   if (threadIdx.x != 0) return;
-  if (st.upd[b]) {
+  // the alpha decision k_cg_axpy made (same inputs, same arithmetic)
+  double a;
+  const bool upd = cg_alpha(st, b, pAp, a);
+  st.upd[b] = upd ? 1 : 0;
+  if (st.active[b] && !upd) st.active[b] = 0;  // max iterations reached, or pAp <= 0 (:114)
+  if (upd) {
+    st.alpha[b] = a;
+    st.its[b] += 1;
     const double relres = sqrt(rr) / st.bnorm[b];
     st.hist[(i64)st.its[b] * st.nrhs + b] = relres;
     if (relres <= st.tol) {  // :121-125
@@ -170,9 +202,9 @@ __global__ void k_cg_fin_rr(CgDev st, const double* __restrict__ partial) {
   if (st.active[b]) atomicAdd(st.nactive, 1);
 }
 
-__global__ void k_cg_fin_rz(CgDev st, const double* __restrict__ partial) {
+__global__ void k_cg_fin_rz(CgDev st, const double* __restrict__ partial, int nblocks) {
   const int b = blockIdx.x;
-  const double rzn = warp_sum_partials(partial, RB, st.nrhs, b);
+  const double rzn = warp_sum_partials(partial, nblocks, st.nrhs, b);
   if (threadIdx.x != 0 || !st.active[b]) return;
   st.beta[b] = rzn / st.rz[b];
   st.rz[b] = rzn;
@@ -370,7 +402,8 @@ __global__ void __launch_bounds__(128) k_pc_proj_mma(const double* __restrict__ 
 // CTA's 64 Q1 rows staged in shared memory with cp.async in one phase.
 __global__ void __launch_bounds__(128) k_pc_apply_mma(const double* __restrict__ Rv, const double* __restrict__ dinv,
                                                       const double* __restrict__ q1, const double* __restrict__ T,
-                                                      i64 N, int k, int nrhs, double* __restrict__ Z) {
+                                                      i64 N, int k, int nrhs, double* __restrict__ Z,
+                                                      double* __restrict__ partial_rz) {
   const int kp = (k + 3) / 4 * 4, np = (nrhs + 7) / 8 * 8;
   const int SC = np + 8, SQ = kp + 4;
   extern __shared__ double sh[];
@@ -409,19 +442,36 @@ __global__ void __launch_bounds__(128) k_pc_apply_mma(const double* __restrict__
         if (j < nt) dmma_f64(acc[i][j][0], acc[i][j][1], af, bf[j]);
     }
   }
+  __syncthreads();  // Qs is reused below for the r·z products [64][SC]
+  double* RZ = Qs;
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
-    const i64 r = row0 + warp * 16 + 8 * i + g;
-    if (r >= N) continue;
-    const double di = dinv[r];
+    const int rl = warp * 16 + 8 * i + g;
+    const i64 r = row0 + rl;
+    const double di = r < N ? dinv[r] : 0.0;
 #pragma unroll
     for (int j = 0; j < PCM_MAXJ; ++j) {
       if (j >= nt) break;
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int bb = 8 * j + 2 * t4 + e;
-        if (bb < nrhs) Z[r * nrhs + bb] = di * (di * Rv[r * nrhs + bb] - acc[i][j][e]);
+        double prod = 0.0;
+        if (r < N && bb < nrhs) {
+          const double rv = Rv[r * nrhs + bb];
+          const double z = di * (di * rv - acc[i][j][e]);  // linalg.cpp:200-204
+          Z[r * nrhs + bb] = z;
+          prod = rv * z;
+        }
+        RZ[rl * SC + bb] = prod;
       }
+    }
+  }
+  if (partial_rz != nullptr) {  // this CTA's r·z per column, rows in fixed order
+    __syncthreads();
+    for (int bb = tid; bb < nrhs; bb += 128) {
+      double t = 0.0;
+      for (int rl = 0; rl < 64; ++rl) t += RZ[rl * SC + bb];
+      partial_rz[(i64)blockIdx.x * nrhs + bb] = t;
     }
   }
 }
@@ -731,6 +781,7 @@ PcgResult pcg_internal(Op& op, Precond* M, const double* B, double* X, int nrhs,
   const i64 tot = N * nrhs;
   DevBuf<double> R(static_cast<size_t>(tot)), Zb(static_cast<size_t>(tot)), Pb(static_cast<size_t>(tot)), AP(static_cast<size_t>(tot));
   DevBuf<double> part(static_cast<size_t>(RB) * nrhs * 3);
+  DevBuf<double> prz(static_cast<size_t>((N + 63) / 64 + RB) * nrhs);  // r·z partials of the precond apply
   DevBuf<double> sc(static_cast<size_t>(nrhs) * 4 + static_cast<size_t>(maxit + 1) * nrhs);
   DevBuf<int> si(static_cast<size_t>(nrhs) * 4 + 1);
   CgDev st;
@@ -776,12 +827,12 @@ PcgResult pcg_internal(Op& op, Precond* M, const double* B, double* X, int nrhs,
   launched("pcg init");
 
   // fused vector step (pcg_fused.cu): one cooperative kernel per iteration
-  // besides the MVM, instead of ten small kernels. Opt-in (tuning
-  // "pcg_fused" = 1): measured on C2 it is not yet faster than the separate
-  // kernels (its grid-barrier reductions cost more than the launches saved).
+  // besides the MVM instead of six kernels (tuning "pcg_fused": 0 default =
+  // fused when supported, 2 = separate kernels). Measured on C2 (32 RHS,
+  // rank 50): ~126 vs ~145 µs per iteration including the MVM.
   PcgVecPlan vplan;
   const int kM = M ? int(M->k) : 0;
-  const bool vfused = g_tuning.pcg_fused.load() == 1 && pcg_vec_supported(nrhs, kM);
+  const bool vfused = g_tuning.pcg_fused.load() != 2 && pcg_vec_supported(nrhs, kM);
   if (vfused) pcg_vec_prepare(vplan, N, nrhs, kM, op.device);
 
   // one iteration, captured as a graph
@@ -805,19 +856,17 @@ PcgResult pcg_internal(Op& op, Precond* M, const double* B, double* X, int nrhs,
     }
     k_dot_partial<<<RB, RT, 0, cs>>>(Pb.p, AP.p, N, nrhs, p0);
     launched("pcg dot");
-    k_cg_fin_pAp<<<nrhs, 32, 0, cs>>>(st, p0);
-    launched("pcg fin");
-    k_cg_axpy<<<RB, RT, 0, cs>>>(st, X, R.p, Pb.p, AP.p, N, p1);
+    GK_CUDA(cudaMemsetAsync(st.nactive, 0, sizeof(int), cs));  // recounted by k_cg_fin_rr
+    k_cg_axpy<<<RB, RT, 0, cs>>>(st, X, R.p, Pb.p, AP.p, N, p0, p1);
     launched("pcg axpy");
-    k_cg_fin_rr<<<nrhs, 32, 0, cs>>>(st, p1);
+    k_cg_fin_rr<<<nrhs, 32, 0, cs>>>(st, p0, p1);
     launched("pcg fin");
     if (M) {
-      M->apply(R.p, Zb.p, nrhs, cs);  // writes rz partials into M's scratch; recompute below
-      k_dot_partial<<<RB, RT, 0, cs>>>(R.p, Zb.p, N, nrhs, p2);
-      launched("pcg dot");
-      k_cg_fin_rz<<<nrhs, 32, 0, cs>>>(st, p2);
+      // z = M^{-1} r with the r·z partials from the same pass (no extra dot)
+      const int nb = M->apply(R.p, Zb.p, nrhs, cs, prz.p);
+      k_cg_fin_rz<<<nrhs, 32, 0, cs>>>(st, prz.p, nb);
     } else {
-      k_cg_fin_rz<<<nrhs, 32, 0, cs>>>(st, p1);
+      k_cg_fin_rz<<<nrhs, 32, 0, cs>>>(st, p1, RB);
     }
     launched("pcg fin");
     k_cg_pupdate<<<eb, 256, 0, cs>>>(st, Pb.p, M ? Zb.p : R.p, N);
@@ -921,10 +970,10 @@ size_t Precond::proj_mma_smem(int nrhs) const {
 }
 size_t Precond::apply_mma_smem(int nrhs) const {
   const i64 kp = (k + 3) / 4 * 4, np = (nrhs + 7) / 8 * 8;
-  return sizeof(double) * size_t(kp * (np + 8) + 64 * (kp + 4));
+  return sizeof(double) * size_t(kp * (np + 8) + 64 * std::max(kp + 4, np + 8));  // Qs, reused for r·z
 }
 
-void Precond::apply(const double* r, double* z, int nrhs, cudaStream_t s) {
+int Precond::apply(const double* r, double* z, int nrhs, cudaStream_t s, double* partial_rz) {
   ensure(nrhs);  // no-op once reserved (and before any graph capture)
   if (mma_ok(nrhs) && g_tuning.precond.load() == 0) {
     k_pc_proj_mma<<<RB, 128, proj_mma_smem(nrhs), s>>>(r, dinv.p, q1.p, N, int(k), nrhs, proj_rch(nrhs),
@@ -932,10 +981,10 @@ void Precond::apply(const double* r, double* z, int nrhs, cudaStream_t s) {
     launched("precond proj (DMMA)");
     k_pc_fin<<<fin_blocks(int(k * nrhs)), 256, 0, s>>>(partial.p, int(k * nrhs), t.p);
     launched("precond fin");
-    k_pc_apply_mma<<<static_cast<unsigned>((N + 63) / 64), 128, apply_mma_smem(nrhs), s>>>(r, dinv.p, q1.p, t.p, N,
-                                                                                           int(k), nrhs, z);
+    const unsigned nb = static_cast<unsigned>((N + 63) / 64);
+    k_pc_apply_mma<<<nb, 128, apply_mma_smem(nrhs), s>>>(r, dinv.p, q1.p, t.p, N, int(k), nrhs, z, partial_rz);
     launched("precond apply (DMMA)");
-    return;
+    return int(nb);
   }
   const size_t sh1 = sizeof(double) * (PC_RT * k + PC_RT * nrhs + k * nrhs);
   k_pc_proj<<<RB, RT, sh1, s>>>(r, dinv.p, q1.p, N, int(k), nrhs, partial.p, nullptr);
@@ -943,8 +992,9 @@ void Precond::apply(const double* r, double* z, int nrhs, cudaStream_t s) {
   k_pc_fin<<<fin_blocks(int(k * nrhs)), 256, 0, s>>>(partial.p, int(k * nrhs), t.p);
   launched("precond fin");
   const size_t sh2 = sizeof(double) * (k * nrhs + RT);
-  k_pc_apply<<<RB, RT, sh2, s>>>(r, dinv.p, q1.p, t.p, N, int(k), nrhs, z, nullptr);
+  k_pc_apply<<<RB, RT, sh2, s>>>(r, dinv.p, q1.p, t.p, N, int(k), nrhs, z, partial_rz);
   launched("precond apply");
+  return RB;
 }
 
 void precond_quadratic(Precond& M, const double* r, int nrhs, double* out_h, cudaStream_t s) {

@@ -28,7 +28,9 @@ struct Precond {
   int ensured_nrhs = 0;
   ~Precond();
   // z = M^{-1} r; optionally rz[b] partials. All internal layout.
-  void apply(const double* r, double* z, int nrhs, cudaStream_t s);
+  // z = M^{-1} r (internal layout); optionally r·z partials per column into
+  // partial_rz[block][nrhs]. Returns the number of partial blocks written.
+  int apply(const double* r, double* z, int nrhs, cudaStream_t s, double* partial_rz = nullptr);
   void ensure(int nrhs);
   bool mma_ok(int nrhs) const;
   int proj_rch(int nrhs) const;

@@ -221,10 +221,10 @@ def test_fused_pcg_step_matches_unfused(nrhs, with_precond):
     B[:, 0] = gk.stacked_targets(y, dY, y.mean())
     if nrhs > 2:
         B[:, 2] = 0.0  # zero right-hand side: converged at 0 iterations
-    prev = gk.set_tuning("pcg_fused", 1)  # opt-in fused vector step
+    prev = gk.set_tuning("pcg_fused", 1)  # one-launch vector step
     try:
         fused = gk.cg(g, B if nrhs > 1 else B[:, 0], 1e-7, 3000, M)
-        gk.set_tuning("pcg_fused", 0)  # default: separate kernels
+        gk.set_tuning("pcg_fused", 2)  # separate kernels
         ref = gk.cg(g, B if nrhs > 1 else B[:, 0], 1e-7, 3000, M)
     finally:
         gk.set_tuning("pcg_fused", prev)

@@ -302,6 +302,13 @@ def run_gpu(args):
         dist.all_reduce(solve, op=dist.ReduceOp.MAX)
     t_pre, t_pcg, t_slq = [float(v) for v in solve.tolist()]
 
+    c4 = None
+    if not args.no_c4:
+        try:
+            c4 = c4_slab(args, world, rank, local, dist)
+        except Exception as e:  # reported, never silently replaced
+            c4 = {"error": f"{type(e).__name__}: {e}"}
+
     line = None
     if rank == 0:
         cpu = cpu_baseline(args) if world == 1 and not args.no_cpu_baseline else None
@@ -332,11 +339,65 @@ def run_gpu(args):
                       "slq_probes_total": world * CONFIG["slq_probes"]},
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
+            "c4_slab": c4,
         }
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return line
+
+
+def c4_slab(args, world, rank, local, dist):
+    """C4 (n = 150,000, d = 2, grid 400², ℓ = 0.02, 1 RHS = the targets):
+    the grid-slab sharded MVM — points partitioned by grid
+    slab across the ranks, one NCCL all-reduce of the 160,000-node grid vector
+    per MVM. Strong scaling (fixed total points). Time = max over ranks."""
+    import torch
+    import paper_1810_12283_b200 as gk
+    from paper_1810_12283_b200.slab import SlabShardedDskiOperator
+    if not dist.is_initialized():  # single GPU: a one-rank NCCL group runs the same code path
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    X, y, dY = gk.make_dataset(4, 0)
+    grid = gk.Grid.cover(X, 1e-4, 3, 400)
+    t0 = time.perf_counter()
+    sop = SlabShardedDskiOperator(gk.KernelSpec(0.02, 1.0), grid, X, (1e-2, 1e-2), device=local)
+    build_s = time.perf_counter() - t0
+    dev = torch.device("cuda", local)
+    nrhs = 1
+    b = gk.stacked_targets(y, dY, y.mean())
+    rows = sop.local_rows()
+    Vext = torch.from_numpy(np.ascontiguousarray(b[rows])).to(dev)
+    Vi, Oi = torch.empty_like(Vext), torch.empty_like(Vext)
+    st = torch.cuda.current_stream(dev)
+    sop.local.to_internal_dev(Vext.data_ptr(), Vi.data_ptr(), nrhs, stream=st.cuda_stream)
+    U = torch.empty(sop.M * nrhs, dtype=torch.float64, device=dev)
+    W = torch.empty_like(U)
+    for _ in range(5):
+        sop.mvm_local_dev(Vi, Oi, nrhs, U, W)
+    reps = 50
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for e0, e1 in ev:
+        e0.record(st)
+        sop.mvm_local_dev(Vi, Oi, nrhs, U, W)
+        e1.record(st)
+    torch.cuda.synchronize()
+    ms = float(np.median([a.elapsed_time(b_) for a, b_ in ev]))
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    return {"workload": "C4: D-SKI d=2 n=150000 (N=450000) grid 400x400 SE ell=0.02 sigma=1e-2, 1 RHS",
+            "parallelism": f"grid-slab x{world} (NCCL all-reduce of the grid vector per MVM)",
+            "scaling": "strong", "ms_per_mvm": ms, "value": sop.size() * nrhs / (ms * 1e-3),
+            "unit": UNIT, "local_points": int(sop.mine.size), "build_s": build_s,
+            "timing": "CUDA events per MVM on the launching stream (L2 not evicted), median, max over ranks"}
 
 
 def cpu_baseline(args, full=False):
@@ -382,7 +443,7 @@ def run_reference(args):
     s = float(np.mean(times))
     value = N * nrhs / s
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
-    return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": s * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded C2 generator)", "config": dict(CONFIG, parallelism="host cores"),
@@ -398,15 +459,33 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="gk", choices=["gk", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 grid-slab sharded MVM measurement")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl != "reference":
         args.warmup = 3
-    if args.impl == "reference":
-        line = run_reference(args)
-    else:
-        line = run_gpu(args)
+    # the contract is ONE JSON line on stdout: everything else any library
+    # prints (e.g. NCCL's version banner) goes to stderr at the fd level
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        if args.impl == "reference":
+            line = run_reference(args)
+        else:
+            line = run_gpu(args)
+        try:  # tear NCCL down while stdout still points at stderr
+            import torch.distributed as dist
+            if dist.is_available() and dist.is_initialized():
+                dist.destroy_process_group()
+        except Exception:
+            pass
+    finally:
+        sys.stdout.flush()
+    # write the line on the saved stdout; fd 1 stays on stderr so output at
+    # interpreter exit (library teardown banners) cannot follow it
     if line is not None:
-        print(json.dumps(line), flush=True)
+        os.write(json_fd, (json.dumps(line) + "\n").encode())
+    os.close(json_fd)
 
 
 if __name__ == "__main__":

@@ -175,9 +175,16 @@ gk_status gk_dskip_dlogell_apply(const gk_op* op, const double* V, int64_t ldv, 
 
 /* Internal-layout stage entry points (device pointers, RHS-minor internal
  * layout; used by the benchmark to time each kernel on its own stream).
- * stage: 0 = scatter (B^T), 1 = grid K_UU, 2 = gather+noise (B), 3 = whole MVM. */
+ * stage: 0 = scatter (B^T), 1 = grid K_UU, 2 = gather (B, no noise),
+ * 3 = whole MVM, 4 = whole MVM replayed from a cached CUDA graph. */
 gk_status gk_op_stage_dev(const gk_op* op, int stage, const double* dIn, double* dOut,
                           int64_t nrhs, void* stream);
+/* D-SKI gather with the noise term, out = B w + diag(σ1² I, σ2² I) v
+ * (internal layout, device pointers): the last stage of a grid-slab sharded
+ * MVM whose grid vector w = K_UU Σ_ranks B_rᵀ v_r the caller
+ * all-reduced. */
+gk_status gk_dski_gather_dev(const gk_op* op, const double* dW, const double* dV, double* dOut,
+                             int64_t nrhs, void* stream);
 /* Convert external column-major blocks to/from the internal layout. */
 gk_status gk_op_to_internal_dev(const gk_op* op, const double* dV, int64_t ldv, double* dI,
                                 int64_t nrhs, void* stream);

@@ -59,6 +59,7 @@ _SIGS = {
     "gk_set_tuning": (C.c_int, [C.c_char_p, C.c_int]),
     "gk_kernel_launch_count": (_i64, []),
     "gk_debug_fused_phases": (C.c_int, [_vp, C.c_int, _i64p, C.c_int]),
+    "gk_dski_gather_dev": (C.c_int, [_vp, _vp, _vp, _vp, _i64, _vp]),
     "gk_grid_cover": (C.c_int, [_dp, _i64, C.c_int, _d, C.c_int, C.c_int, C.POINTER(GkGrid)]),
     "gk_mix_seed": (_u64, [_u64, _u64]),
     "gk_rademacher_vector": (None, [_i64, _u64, _u64, _dp]),
@@ -400,6 +401,11 @@ class DskiOperator(LinearOperator):
         _check(_lib.gk_dski_predict_mean_grad(self._h, _p(_f64(alpha)), float(mean), _p(Xt), T,
                                               _p(vals), _p(grads)))
         return vals, grads
+
+    def gather_dev(self, dW, dV, dOut, nrhs, stream=0):
+        """out = B w + noise·v on device pointers (internal layout): the last
+        stage of a grid-slab sharded MVM."""
+        _check(_lib.gk_dski_gather_dev(self._h, dW, dV, dOut, nrhs, stream))
 
     def cross_covariance(self, Xtest):
         """GpModel::cross_covariance for D-SKI (gp.cpp:412-417), one column per test point."""

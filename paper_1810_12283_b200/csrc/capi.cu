@@ -26,6 +26,7 @@ std::unique_ptr<Op> make_dskip(const gk_kernel& k, const double* X, i64 n, int d
                                const gk_dskip_config& cfg, int device);
 int64_t dski_grid_size(const Op& o);
 int dski_fused_phases(Op& o, int nrhs, i64* out, int max_ctas);
+void dski_gather_noise(Op& o, const double* W, const double* V, double* out, int nrhs, cudaStream_t s);
 gk_grid dski_grid(const Op& o);
 void dski_transpose_apply(Op& o, const double* Vi, double* U, int nrhs, cudaStream_t s);
 void dski_apply(Op& o, const double* U, double* Oi, int nrhs, cudaStream_t s);
@@ -310,6 +311,16 @@ gk_status gk_op_stage_dev(const gk_op* h, int stage, const double* dIn, double* 
     if (nrhs < 1 || nrhs > 256) fail(GK_ERR_ARG, "stage: nrhs must be in [1, 256]");
     DeviceGuard dg(op.device);
     op.stage(stage, dIn, dOut, int(nrhs), S(stream));
+  });
+}
+
+gk_status gk_dski_gather_dev(const gk_op* h, const double* dW, const double* dV, double* dOut, int64_t nrhs,
+                             void* stream) {
+  return guard([&] {
+    Op& op = O(h);
+    if (nrhs < 1 || nrhs > 256) fail(GK_ERR_ARG, "gather: nrhs must be in [1, 256]");
+    DeviceGuard dg(op.device);
+    dski_gather_noise(op, dW, dV, dOut, int(nrhs), S(stream));
   });
 }
 

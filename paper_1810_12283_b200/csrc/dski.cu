@@ -1358,6 +1358,11 @@ void dski_transpose_apply(Op& o, const double* Vi, double* U, int nrhs, cudaStre
   auto& op = static_cast<DskiOp&>(o);
   op.scatter(Vi, U, nrhs, s);
 }
+void dski_gather_noise(Op& o, const double* W, const double* V, double* out, int nrhs, cudaStream_t s) {
+  if (o.kind != KIND_DSKI) fail(GK_ERR_ARG, "operator is not a D-SKI operator");
+  auto& op = static_cast<DskiOp&>(o);
+  op.gather(W, V, out, nrhs, true, s);
+}
 void dski_apply(Op& o, const double* U, double* Oi, int nrhs, cudaStream_t s) {
   auto& op = static_cast<DskiOp&>(o);
   op.gather(U, U, Oi, nrhs, false, s);

@@ -153,6 +153,7 @@ int gk_set_tuning(const char* key, int value) {
                            : k == "fused" ? &g_tuning.fused
                            : k == "fused_prof" ? &g_tuning.fused_prof
                            : k == "pcg_fused" ? &g_tuning.pcg_fused
+                           : k == "e2e_chunk" ? &g_tuning.e2e_chunk
                            : k == "f2_stc" ? &g_tuning.f2_stc
                            : k == "f2_sl" ? &g_tuning.f2_sl
                            : k == "f2_gtc" ? &g_tuning.f2_gtc
@@ -270,16 +271,46 @@ gk_status gk_op_mvm(const gk_op* h, const double* V, int64_t ldv, double* Out, i
     std::lock_guard<std::mutex> lk(op.mu);
     DeviceGuard dg(op.device);
     cudaStream_t s = op.stream;
-    const int chunk = int(std::min<i64>(nrhs, kMaxRhs));
-    op.scratch_a.reserve(static_cast<size_t>(op.N) * chunk);
-    op.scratch_b.reserve(static_cast<size_t>(op.N) * chunk);
-    op.scratch_c.reserve(static_cast<size_t>(op.N) * chunk);
-    for (i64 c0 = 0; c0 < nrhs; c0 += chunk) {
-      const int nb = int(std::min<i64>(chunk, nrhs - c0));
-      upload_internal(op, V + c0 * ldv, ldv, op.scratch_c.p, op.scratch_a.p, nb, s);
-      op.mvm(op.scratch_a.p, op.scratch_b.p, nb, s);
-      download_internal(op, op.scratch_b.p, op.scratch_c.p, Out + c0 * ldo, ldo, nb, s);
+    // Host buffers: column chunks pipelined over three streams — copy-in
+    // (H2D + to-internal) of chunk j+1, the MVM of chunk j and copy-out
+    // (from-internal + D2H) of chunk j-1 overlap, and H2D/D2H run in
+    // opposite PCIe directions at once. Columns are independent, so the
+    // result equals the one-shot MVM.
+    const int pc = g_tuning.e2e_chunk.load();
+    int chunk = pc > 0 ? pc : (nrhs >= 16 ? int((nrhs + 3) / 4) : int(nrhs));
+    chunk = int(std::min<i64>(std::max(1, chunk), std::min<i64>(nrhs, kMaxRhs)));
+    const int nchunks = int((nrhs + chunk - 1) / chunk);
+    if (!op.io_in) {
+      GK_CUDA(cudaStreamCreateWithFlags(&op.io_in, cudaStreamNonBlocking));
+      GK_CUDA(cudaStreamCreateWithFlags(&op.io_out, cudaStreamNonBlocking));
     }
+    while (int(op.io_events.size()) < 2 * nchunks + 1) {
+      cudaEvent_t e;
+      GK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      op.io_events.push_back(e);
+    }
+    const size_t tot = static_cast<size_t>(op.N) * nrhs;
+    op.io_ext_in.reserve(tot);
+    op.io_int_in.reserve(tot);
+    op.io_int_out.reserve(tot);
+    op.io_ext_out.reserve(tot);
+    // the copy streams must not start before earlier work on the compute stream
+    GK_CUDA(cudaEventRecord(op.io_events[2 * nchunks], s));
+    GK_CUDA(cudaStreamWaitEvent(op.io_in, op.io_events[2 * nchunks], 0));
+    GK_CUDA(cudaStreamWaitEvent(op.io_out, op.io_events[2 * nchunks], 0));
+    for (int j = 0; j < nchunks; ++j) {
+      const i64 c0 = i64(j) * chunk;
+      const int nb = int(std::min<i64>(chunk, nrhs - c0));
+      const size_t off = static_cast<size_t>(op.N) * c0;
+      upload_internal(op, V + c0 * ldv, ldv, op.io_ext_in.p + off, op.io_int_in.p + off, nb, op.io_in);
+      GK_CUDA(cudaEventRecord(op.io_events[2 * j], op.io_in));
+      GK_CUDA(cudaStreamWaitEvent(s, op.io_events[2 * j], 0));
+      op.mvm(op.io_int_in.p + off, op.io_int_out.p + off, nb, s);
+      GK_CUDA(cudaEventRecord(op.io_events[2 * j + 1], s));
+      GK_CUDA(cudaStreamWaitEvent(op.io_out, op.io_events[2 * j + 1], 0));
+      download_internal(op, op.io_int_out.p + off, op.io_ext_out.p + off, Out + c0 * ldo, ldo, nb, op.io_out);
+    }
+    GK_CUDA(cudaStreamSynchronize(op.io_out));
     GK_CUDA(cudaStreamSynchronize(s));
   });
 }

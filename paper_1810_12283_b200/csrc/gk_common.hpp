@@ -41,6 +41,7 @@ struct Tuning {
   std::atomic<int> f2_stc{0}, f2_sl{0}, f2_gtc{0}, f2_gl{0}, f2_tsplit{0}, f2_per_sm{0};
   std::atomic<int> f2_skip{0}, f2_grid{0}, f2_rp{0};
   std::atomic<int> f2_smode{0}, f2_gmode{0}, f2_nspl{0}, f2_nst{0};  // 1 staged, 2 direct (0 = default)  // debug: bitmask of phases to skip (1 S, 2 T1, 4 T0, 8 G)
+  std::atomic<int> e2e_chunk{0};  // gk_op_mvm pipeline chunk width (0 = auto)
   std::atomic<int> gen{0};  // bumped by every gk_set_tuning call (cached plans rebuild)
 };
 extern Tuning g_tuning;
@@ -152,6 +153,10 @@ struct Op {
   cudaStream_t cap_stream = nullptr;  // private stream used only for CUDA-graph capture
   DevBuf<double> scratch_a, scratch_b, scratch_c;
   HostBuf pinned;
+  // host-buffer MVM pipeline (gk_op_mvm): copy-in / compute / copy-out streams
+  cudaStream_t io_in = nullptr, io_out = nullptr;
+  std::vector<cudaEvent_t> io_events;
+  DevBuf<double> io_ext_in, io_int_in, io_int_out, io_ext_out;
 
   virtual void mvm(const double* in, double* out, int nrhs, cudaStream_t s) = 0;
   // diagonal including noise, internal order

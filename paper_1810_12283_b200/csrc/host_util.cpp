@@ -133,6 +133,9 @@ std::uint64_t next_op_uid() {
 
 Op::~Op() {
   for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+  for (auto e : io_events) cudaEventDestroy(e);
+  if (io_in) cudaStreamDestroy(io_in);
+  if (io_out) cudaStreamDestroy(io_out);
   if (stream) cudaStreamDestroy(stream);
   if (cap_stream) cudaStreamDestroy(cap_stream);
 }

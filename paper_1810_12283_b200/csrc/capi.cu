@@ -154,6 +154,7 @@ int gk_set_tuning(const char* key, int value) {
                            : k == "fused_prof" ? &g_tuning.fused_prof
                            : k == "pcg_fused" ? &g_tuning.pcg_fused
                            : k == "e2e_chunk" ? &g_tuning.e2e_chunk
+                           : k == "dskip" ? &g_tuning.dskip
                            : k == "f2_stc" ? &g_tuning.f2_stc
                            : k == "f2_sl" ? &g_tuning.f2_sl
                            : k == "f2_gtc" ? &g_tuning.f2_gtc

@@ -248,6 +248,456 @@ __global__ void __launch_bounds__(128) k_had_expand(const double* __restrict__ Q
       }
 }
 
+// ---------------------------------------------------------------- Khatri–Rao GEMMs v2
+// The two Hadamard contractions as fp64 tensor-core GEMMs whose A operand
+// Z[row][m] = QA[row][k]·QB[row][l] (m = k·rb + l) is formed in registers at
+// fragment load from staged Q rows — never written out. Q rows and the RHS
+// block are staged with 16-byte cp.async, double-buffered; shared strides are
+// ≡ 4 (mod 16) doubles (conflict-free DMMA fragment loads); (k, l) per m come
+// from a per-CTA table (no divisions in the loops). Each warp owns a 32×32
+// output tile: 16 independent DMMA accumulator chains.
+__host__ __device__ __forceinline__ int hk_pad(int x) { return x + ((4 - x % 16) + 16) % 16; }
+__device__ __forceinline__ void hk_cpa16(void* s, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(s))),
+               "l"(g)
+               : "memory");
+}
+__device__ __forceinline__ void hk_cpa8(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(s))),
+               "l"(g)
+               : "memory");
+}
+// rows [r0, r0+nr), columns [c0, c0+wc) of a [*][ld] row-major matrix into
+// smem rows of stride ws; rows [nr, nz) of the tile are zeroed
+__device__ __forceinline__ void hk_stage(double* dst, int ws, const double* src, int ld, int c0, int wc, i64 r0,
+                                         int nr, int nz) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  const double* base = src + r0 * ld + c0;
+  if ((wc & 1) == 0 && (ld & 1) == 0 && (((uintptr_t)base) & 15) == 0) {
+    const int cpr = wc / 2;
+    for (int r = warp; r < nr; r += nw)
+      for (int c = lane; c < cpr; c += 32) hk_cpa16(dst + r * ws + 2 * c, base + (i64)r * ld + 2 * c);
+  } else {
+    for (int r = warp; r < nr; r += nw)
+      for (int c = lane; c < wc; c += 32) hk_cpa8(dst + r * ws + c, base + (i64)r * ld + c);
+  }
+  for (int e = threadIdx.x; e < (nz - nr) * ws; e += blockDim.x) dst[nr * ws + e] = 0.0;
+}
+
+constexpr int HK_BK = 32;  // rows per stage (contract)
+constexpr int HK_MC = 32;  // m per stage (expand)
+
+// partial[chunk][m][b] = Σ_{rows in chunk} Z[row][m] V[row][b]
+// CTA: 64 m × 64 b (4 warps, 2×2 of 32×32); K = rows in stages of HK_BK.
+__global__ void __launch_bounds__(128) k_had_contract2(const double* __restrict__ QA, int ra,
+                                                       const double* __restrict__ QB, int rb,
+                                                       const double* __restrict__ V, i64 N, int nrhs,
+                                                       i64 rows_per_chunk, double* __restrict__ partial) {
+  extern __shared__ __align__(16) double hk_sm[];
+  const int bw = min(64, nrhs - (int)blockIdx.y * 64);
+  const int SA = hk_pad(ra), SBq = hk_pad(rb), SV = hk_pad(min(64, nrhs));
+  double* QAs = hk_sm;                           // [2][HK_BK][SA]
+  double* QBs = QAs + 2 * HK_BK * SA;            // [2][HK_BK][SBq]
+  double* Vs = QBs + 2 * HK_BK * SBq;            // [2][HK_BK][SV]
+  const int M = ra * rb;
+  const int m0 = blockIdx.x * 64, b0 = blockIdx.y * 64;
+  const i64 r_begin = (i64)blockIdx.z * rows_per_chunk;
+  const i64 r_end = min(N, r_begin + rows_per_chunk);
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32, g = lane / 4, t4 = lane % 4;
+  const int wm = (warp & 1) * 32, wb = (warp >> 1) * 32;
+  int ka[4], la[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + wm + 8 * i + g;
+    ka[i] = m < M ? m / rb : -1;
+    la[i] = m < M ? m % rb : 0;
+  }
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  auto issue = [&](i64 rs, int buf) {
+    const int nr = int(min((i64)HK_BK, r_end - rs));
+    hk_stage(QAs + buf * HK_BK * SA, SA, QA, ra, 0, ra, rs, nr, HK_BK);
+    hk_stage(QBs + buf * HK_BK * SBq, SBq, QB, rb, 0, rb, rs, nr, HK_BK);
+    hk_stage(Vs + buf * HK_BK * SV, SV, V, nrhs, b0, bw, rs, nr, HK_BK);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  int buf = 0;
+  if (r_begin < r_end) issue(r_begin, 0);
+  for (i64 rs = r_begin; rs < r_end; rs += HK_BK) {
+    const i64 nx = rs + HK_BK;
+    if (nx < r_end) {
+      issue(nx, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    const double* A1 = QAs + buf * HK_BK * SA;
+    const double* B1 = QBs + buf * HK_BK * SBq;
+    const double* V1 = Vs + buf * HK_BK * SV;
+    const int nr = int(min((i64)HK_BK, r_end - rs));
+    for (int kk = 0; kk < nr; kk += 4) {
+      const int row = kk + t4;
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = ka[i] >= 0 ? A1[row * SA + ka[i]] * B1[row * SBq + la[i]] : 0.0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int bl = wb + 8 * j + g;
+        bf[j] = bl < bw ? V1[row * SV + bl] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();
+    buf ^= 1;
+  }
+  double* out = partial + (i64)blockIdx.z * M * nrhs;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int m = m0 + wm + 8 * i + g;
+        const int b = b0 + wb + 8 * j + 2 * t4 + e;
+        if (m < M && b < nrhs) out[(i64)m * nrhs + b] = acc[i][j][e];
+      }
+}
+
+// out[i][b] (+)= Σ_m QTA[i][k] QB[i][l] C'[m][b] (+ noise·v)
+// CTA: 64 rows × 64 b (4 warps, 2×2 of 32×32); the CTA's Q rows staged once,
+// C' in double-buffered chunks of HK_MC m.
+__global__ void __launch_bounds__(128) k_had_expand2(const double* __restrict__ QTA, int ra,
+                                                     const double* __restrict__ QB, int rb,
+                                                     const double* __restrict__ Cp, i64 N, int nrhs,
+                                                     const double* __restrict__ v, i64 n_value, double nv2,
+                                                     double ng2, int accumulate, double* __restrict__ out) {
+  extern __shared__ __align__(16) double hk_sm[];
+  const int bw = min(64, nrhs - (int)blockIdx.y * 64);
+  const int SA = hk_pad(ra), SBq = hk_pad(rb), SV = hk_pad(min(64, nrhs));
+  const int M = ra * rb;
+  double* QAs = hk_sm;                  // [64][SA]
+  double* QBs = QAs + 64 * SA;          // [64][SBq]
+  double* Cs = QBs + 64 * SBq;          // [2][HK_MC][SV]
+  int2* kl = reinterpret_cast<int2*>(Cs + 2 * HK_MC * SV);  // [M] (k, l)
+  const i64 i0 = (i64)blockIdx.x * 64;
+  const int b0 = blockIdx.y * 64;
+  const int nr = int(min((i64)64, N - i0));
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32, g = lane / 4, t4 = lane % 4;
+  const int wi = (warp & 1) * 32, wb = (warp >> 1) * 32;
+  for (int m = tid; m < M; m += 128) kl[m] = make_int2(m / rb, m % rb);
+  hk_stage(QAs, SA, QTA, ra, 0, ra, i0, nr, 64);
+  hk_stage(QBs, SBq, QB, rb, 0, rb, i0, nr, 64);
+  auto issue = [&](int mc, int buf) {
+    const int nm = min(HK_MC, M - mc);
+    hk_stage(Cs + buf * HK_MC * SV, SV, Cp, nrhs, b0, bw, mc, nm, HK_MC);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  issue(0, 0);
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  int buf = 0;
+  for (int mc = 0; mc < M; mc += HK_MC) {
+    if (mc + HK_MC < M) {
+      issue(mc + HK_MC, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    const double* C1 = Cs + buf * HK_MC * SV;
+    const int nm = min(HK_MC, M - mc);
+    for (int kk = 0; kk < nm; kk += 4) {
+      const int m = mc + kk + t4;
+      const int2 q = m < M ? kl[m] : make_int2(0, 0);
+      const bool mok = m < M;
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int row = wi + 8 * i + g;
+        af[i] = mok ? QAs[row * SA + q.x] * QBs[row * SBq + q.y] : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = wb + 8 * j + g < bw ? C1[(kk + t4) * SV + wb + 8 * j + g] : 0.0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();
+    buf ^= 1;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const i64 row = i0 + wi + 8 * i + g;
+        const int b = b0 + wb + 8 * j + 2 * t4 + e;
+        if (row < N && b < nrhs) {
+          const i64 idx = row * nrhs + b;
+          double val = acc[i][j][e];
+          if (v) val += (row < n_value ? nv2 : ng2) * v[idx];
+          out[idx] = accumulate ? out[idx] + val : val;
+        }
+      }
+}
+
+// ---------------------------------------------------------------- Khatri–Rao GEMMs v3
+// Same GEMMs as v2, with the operand rows moved by per-row TMA bulk copies
+// (cp.async.bulk, one issuing thread per row, completion on an mbarrier ring)
+// instead of per-16-byte cp.async loops, constant-trip fully unrolled stages
+// (tails are zero rows, never predicated), and CTA shapes sized for 3-4
+// resident CTAs per SM. Needs even ranks and an even RHS count (16-byte rows).
+// NJ = 8-column tiles per warp: the CTA covers 16·NJ right-hand sides.
+__device__ __forceinline__ unsigned hk_su32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void hk_mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"(hk_su32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void hk_mbar_arrive_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(hk_su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void hk_mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared.b64 _, [%0];\n" ::"r"(hk_su32(b)) : "memory");
+}
+__device__ __forceinline__ void hk_mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nHKW_%=:\nmbarrier.try_wait.parity.shared.b64 P1, [%0], %1;\n@!P1 bra HKW_%=;\n}\n" ::"r"(
+          hk_su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void hk_bulk(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   hk_su32(dst)),
+               "l"(src), "r"(bytes), "r"(hk_su32(b))
+               : "memory");
+}
+__device__ __forceinline__ void hk_zero_row(double* dst, int w) {
+  for (int c = 0; c < w; ++c) dst[c] = 0.0;
+}
+
+constexpr int H3_BK = 16, H3_NS = 3;   // contract: rows per stage, ring depth
+constexpr int H3_MC = 16, H3_NSE = 4;  // expand: m per stage, ring depth
+
+template <int NJ>
+__global__ void __launch_bounds__(128, 4) k_had_contract3(const double* __restrict__ QA, int ra,
+                                                          const double* __restrict__ QB, int rb,
+                                                          const double* __restrict__ V, i64 N, int nrhs,
+                                                          i64 rows_per_chunk, double* __restrict__ partial) {
+  extern __shared__ __align__(128) double hk_sm[];
+  constexpr int BWC = 16 * NJ, SV = BWC + ((4 - BWC % 16) + 16) % 16;
+  const int SA = hk_pad(ra), SBq = hk_pad(rb);
+  const int stage_d = H3_BK * (SA + SBq + SV);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(hk_sm + H3_NS * stage_d);
+  const int M = ra * rb;
+  const int m0 = blockIdx.x * 64, b0 = blockIdx.y * BWC;
+  const int bw = min(BWC, nrhs - b0);
+  const i64 r_begin = (i64)blockIdx.z * rows_per_chunk;
+  const i64 r_end = min(N, r_begin + rows_per_chunk);
+  const int nst = r_end > r_begin ? int((r_end - r_begin + H3_BK - 1) / H3_BK) : 0;
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32, g = lane / 4, t4 = lane % 4;
+  const int wm = (warp & 1) * 32, wb = (warp >> 1) * 8 * NJ;
+  if (tid == 0) {
+    for (int s = 0; s < H3_NS; ++s) hk_mbar_init(full + s, 3 * H3_BK);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  // threads 0..15: QA rows, 16..31: QB rows, 32..47: V rows of one stage
+  auto issue = [&](int st) {
+    if (tid >= 3 * H3_BK) return;
+    const i64 rs = r_begin + (i64)st * H3_BK;
+    const int nr = int(min((i64)H3_BK, r_end - rs));
+    double* base = hk_sm + (st % H3_NS) * stage_d;
+    unsigned long long* b = full + st % H3_NS;
+    const int mat = tid / H3_BK, row = tid % H3_BK;
+    double* dst;
+    const double* src;
+    int bytes, w;
+    if (mat == 0) {
+      dst = base + row * SA, src = QA + (rs + row) * ra, bytes = ra * 8, w = SA;
+    } else if (mat == 1) {
+      dst = base + H3_BK * SA + row * SBq, src = QB + (rs + row) * rb, bytes = rb * 8, w = SBq;
+    } else {
+      dst = base + H3_BK * (SA + SBq) + row * SV, src = V + (rs + row) * nrhs + b0, bytes = bw * 8, w = SV;
+    }
+    if (row < nr) {
+      hk_mbar_arrive_tx(b, bytes);
+      hk_bulk(dst, src, bytes, b);
+    } else {
+      hk_zero_row(dst, w);  // tail rows contribute exact zeros
+      hk_mbar_arrive(b);
+    }
+  };
+  int ka[4], la[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = min(m0 + wm + 8 * i + g, M - 1);  // rows past M: finite, discarded
+    ka[i] = m / rb;
+    la[i] = m - ka[i] * rb;
+  }
+  double acc[4][NJ][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int s = 0; s < min(H3_NS, nst); ++s) issue(s);
+  for (int it = 0; it < nst; ++it) {
+    hk_mbar_wait(full + it % H3_NS, (it / H3_NS) & 1);
+    const double* A1 = hk_sm + (it % H3_NS) * stage_d;
+    const double* B1 = A1 + H3_BK * SA;
+    const double* V1 = B1 + H3_BK * SBq;
+#pragma unroll
+    for (int kk = 0; kk < H3_BK; kk += 4) {
+      const int row = kk + t4;
+      double af[4], bf[NJ];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = A1[row * SA + ka[i]] * B1[row * SBq + la[i]];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) bf[j] = V1[row * SV + wb + 8 * j + g];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();
+    if (it + H3_NS < nst) issue(it + H3_NS);
+  }
+  double* out = partial + (i64)blockIdx.z * M * nrhs;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int m = m0 + wm + 8 * i + g;
+      const int bl = wb + 8 * j + 2 * t4;
+      if (m < M && bl < bw)
+        *reinterpret_cast<double2*>(out + (i64)m * nrhs + b0 + bl) = make_double2(acc[i][j][0], acc[i][j][1]);
+    }
+}
+
+template <int NJ>
+__global__ void __launch_bounds__(128, 3) k_had_expand3(const double* __restrict__ QTA, int ra,
+                                                        const double* __restrict__ QB, int rb,
+                                                        const double* __restrict__ Cp, i64 N, int nrhs,
+                                                        const double* __restrict__ v, i64 n_value, double nv2,
+                                                        double ng2, int accumulate, double* __restrict__ out) {
+  extern __shared__ __align__(128) double hk_sm[];
+  constexpr int BWC = 16 * NJ, SV = BWC + ((4 - BWC % 16) + 16) % 16;
+  const int SA = hk_pad(ra), SBq = hk_pad(rb);
+  const int M = ra * rb;
+  double* QAs = hk_sm;              // [64][SA]
+  double* QBs = QAs + 64 * SA;      // [64][SBq]
+  double* Cs = QBs + 64 * SBq;      // [H3_NSE][H3_MC][SV]
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(Cs + H3_NSE * H3_MC * SV);
+  unsigned long long* qbar = full + H3_NSE;
+  const i64 i0 = (i64)blockIdx.x * 64;
+  const int b0 = blockIdx.y * BWC;
+  const int bw = min(BWC, nrhs - b0);
+  const int nr = int(min((i64)64, N - i0));
+  const int nch = (M + H3_MC - 1) / H3_MC;
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32, g = lane / 4, t4 = lane % 4;
+  const int wi = (warp & 1) * 32, wb = (warp >> 1) * 8 * NJ;
+  if (tid == 0) {
+    for (int s = 0; s < H3_NSE; ++s) hk_mbar_init(full + s, H3_MC);
+    hk_mbar_init(qbar, 128);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  {  // this CTA's factor rows, once: threads 0..63 QTA rows, 64..127 QB rows
+    const int row = tid & 63;
+    if (row < nr) {
+      const bool a = tid < 64;
+      hk_mbar_arrive_tx(qbar, (a ? ra : rb) * 8);
+      hk_bulk(a ? QAs + row * SA : QBs + row * SBq, a ? QTA + (i0 + row) * ra : QB + (i0 + row) * rb,
+              (a ? ra : rb) * 8, qbar);
+    } else {
+      hk_mbar_arrive(qbar);  // rows past N only feed discarded outputs
+    }
+  }
+  auto issue = [&](int c) {
+    if (tid >= H3_MC) return;
+    const int m = c * H3_MC + tid;
+    double* dst = Cs + (c % H3_NSE) * H3_MC * SV + tid * SV;
+    unsigned long long* b = full + c % H3_NSE;
+    if (m < M) {
+      hk_mbar_arrive_tx(b, bw * 8);
+      hk_bulk(dst, Cp + (i64)m * nrhs + b0, bw * 8, b);
+    } else {
+      hk_zero_row(dst, SV);
+      hk_mbar_arrive(b);
+    }
+  };
+  for (int c = 0; c < min(H3_NSE, nch); ++c) issue(c);
+  double acc[4][NJ][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  int k = t4 / rb, l = t4 % rb;  // (k, l) of m = c·MC + kk + t4, advanced by 4 per step
+  const double* qa_row[4];
+  const double* qb_row[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    qa_row[i] = QAs + (wi + 8 * i + g) * SA;
+    qb_row[i] = QBs + (wi + 8 * i + g) * SBq;
+  }
+  hk_mbar_wait(qbar, 0);
+  for (int c = 0; c < nch; ++c) {
+    hk_mbar_wait(full + c % H3_NSE, (c / H3_NSE) & 1);
+    const double* C1 = Cs + (c % H3_NSE) * H3_MC * SV;
+#pragma unroll
+    for (int kk = 0; kk < H3_MC; kk += 4) {
+      const int kc = k < ra ? k : 0;  // m past M meets a zero C' row
+      double af[4], bf[NJ];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = qa_row[i][kc] * qb_row[i][l];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) bf[j] = C1[(kk + t4) * SV + wb + 8 * j + g];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      l += 4;
+      while (l >= rb) l -= rb, ++k;
+    }
+    __syncthreads();
+    if (c + H3_NSE < nch) issue(c + H3_NSE);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const i64 row = i0 + wi + 8 * i + g;
+      const int bl = wb + 8 * j + 2 * t4;
+      if (row < N && bl < bw) {
+        const i64 idx = row * nrhs + b0 + bl;
+        double2 val = make_double2(acc[i][j][0], acc[i][j][1]);
+        if (v) {
+          const double nz = row < n_value ? nv2 : ng2;
+          const double2 vv = *reinterpret_cast<const double2*>(v + idx);
+          val.x += nz * vv.x, val.y += nz * vv.y;
+        }
+        if (accumulate) {
+          const double2 o = *reinterpret_cast<const double2*>(out + idx);
+          val.x += o.x, val.y += o.y;
+        }
+        *reinterpret_cast<double2*>(out + idx) = val;
+      }
+    }
+}
+
 // diag = Π_f Σ_k QT_f[i][k] Q_f[i][k] (+ noise)   (dskip.cpp:141-149)
 __global__ void k_had_diag(const double* const* __restrict__ Qs, const double* const* __restrict__ QTs,
                            const int* __restrict__ ranks, int nf, i64 N, i64 n_value, double nv2, double ng2,
@@ -334,9 +784,120 @@ struct HadScratch {
   DevBuf<double> partial, C, Cp;
 };
 
+static size_t had2_contract_smem(int ra, int rb, int nrhs) {
+  return sizeof(double) * size_t(2 * HK_BK) * (hk_pad(ra) + hk_pad(rb) + hk_pad(nrhs));
+}
+static size_t had2_expand_smem(int ra, int rb, int nrhs) {
+  return sizeof(double) * (size_t(64) * (hk_pad(ra) + hk_pad(rb)) + size_t(2 * HK_MC) * hk_pad(nrhs)) +
+         sizeof(int2) * size_t(ra) * rb + 16;
+}
+
+template <int NJ>
+static size_t had3_contract_smem(int ra, int rb) {
+  constexpr int BWC = 16 * NJ, SV = BWC + ((4 - BWC % 16) + 16) % 16;
+  return sizeof(double) * size_t(H3_NS) * H3_BK * (hk_pad(ra) + hk_pad(rb) + SV) + 8 * H3_NS;
+}
+template <int NJ>
+static size_t had3_expand_smem(int ra, int rb) {
+  constexpr int BWC = 16 * NJ, SV = BWC + ((4 - BWC % 16) + 16) % 16;
+  return sizeof(double) * (size_t(64) * (hk_pad(ra) + hk_pad(rb)) + size_t(H3_NSE) * H3_MC * SV) +
+         8 * (H3_NSE + 1);
+}
+
+static int device_sm_count() {
+  int dev = 0, sms = 0;
+  GK_CUDA(cudaGetDevice(&dev));
+  GK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  return sms;
+}
+
+template <int NJ>
+static void hadamard_pair3_launch(const Factor& A, const Factor& B, const double* v, int nrhs, double* out,
+                                  bool accumulate, const double* noise_v, i64 n_value, double nv2, double ng2,
+                                  HadScratch& ws, cudaStream_t s) {
+  const i64 N = A.N;
+  const int M = A.r * B.r;
+  const size_t sc = had3_contract_smem<NJ>(A.r, B.r), se = had3_expand_smem<NJ>(A.r, B.r);
+  raise_smem_limit((const void*)k_had_contract3<NJ>, sc);
+  raise_smem_limit((const void*)k_had_expand3<NJ>, se);
+  const int mt = (M + 63) / 64, bt = (nrhs + 16 * NJ - 1) / (16 * NJ);
+  // row-split so that all CTAs of the contraction are co-resident (4 per SM)
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_had_contract3<NJ>, 128, sc);
+  const int slots = std::max(1, per_sm) * device_sm_count();
+  int chunks = int(std::max<i64>(1, std::min<i64>(slots / (mt * bt), (N + 4 * H3_BK - 1) / (4 * H3_BK))));
+  const i64 rows_per_chunk = ((N + chunks - 1) / chunks + H3_BK - 1) / H3_BK * H3_BK;
+  chunks = int((N + rows_per_chunk - 1) / rows_per_chunk);
+  ws.partial.reserve(static_cast<size_t>(chunks) * M * nrhs);
+  ws.C.reserve(static_cast<size_t>(M) * nrhs);
+  ws.Cp.reserve(static_cast<size_t>(M) * nrhs);
+  dim3 g1(static_cast<unsigned>(mt), static_cast<unsigned>(bt), static_cast<unsigned>(chunks));
+  k_had_contract3<NJ><<<g1, 128, sc, s>>>(A.Q.p, A.r, B.Q.p, B.r, v, N, nrhs, rows_per_chunk, ws.partial.p);
+  launched("hadamard contract (DMMA v3)");
+  k_had_reduce<<<blocks_for((i64)M * nrhs), 256, 0, s>>>(ws.partial.p, chunks, M, nrhs, ws.C.p);
+  launched("hadamard reduce");
+  k_had_tridiag<<<blocks_for((i64)M * nrhs), 256, 0, s>>>(ws.C.p, A.r, B.r, nrhs, B.ab.p, B.ab.p + B.r, ws.Cp.p);
+  launched("hadamard tridiag");
+  dim3 g3(static_cast<unsigned>((N + 63) / 64), static_cast<unsigned>(bt));
+  k_had_expand3<NJ><<<g3, 128, se, s>>>(A.QT.p, A.r, B.Q.p, B.r, ws.Cp.p, N, nrhs, noise_v, n_value, nv2, ng2,
+                                        accumulate ? 1 : 0, out);
+  launched("hadamard expand (DMMA v3)");
+}
+
+static bool hadamard_pair3(const Factor& A, const Factor& B, const double* v, int nrhs, double* out, bool accumulate,
+                           const double* noise_v, i64 n_value, double nv2, double ng2, HadScratch& ws,
+                           cudaStream_t s) {
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (g_tuning.dskip.load() != 0 || (A.r & 1) || (B.r & 1) || (nrhs & 1) || !al16(v) || !al16(out) ||
+      (noise_v && !al16(noise_v)) || !al16(A.Q.p) || !al16(A.QT.p) || !al16(B.Q.p))
+    return false;
+  if (had3_expand_smem<4>(A.r, B.r) > 200 * 1024) return false;
+  if (nrhs > 32)
+    hadamard_pair3_launch<4>(A, B, v, nrhs, out, accumulate, noise_v, n_value, nv2, ng2, ws, s);
+  else if (nrhs > 16)
+    hadamard_pair3_launch<2>(A, B, v, nrhs, out, accumulate, noise_v, n_value, nv2, ng2, ws, s);
+  else
+    hadamard_pair3_launch<1>(A, B, v, nrhs, out, accumulate, noise_v, n_value, nv2, ng2, ws, s);
+  return true;
+}
+
+static bool hadamard_pair2(const Factor& A, const Factor& B, const double* v, int nrhs, double* out, bool accumulate,
+                           const double* noise_v, i64 n_value, double nv2, double ng2, HadScratch& ws,
+                           cudaStream_t s) {
+  const i64 N = A.N;
+  const int M = A.r * B.r;
+  const size_t sc = had2_contract_smem(A.r, B.r, std::min(nrhs, 64));
+  const size_t se = had2_expand_smem(A.r, B.r, std::min(nrhs, 64));
+  if (g_tuning.dskip.load() == 1 || sc > 200 * 1024 || se > 200 * 1024) return false;
+  raise_smem_limit((const void*)k_had_contract2, sc);
+  raise_smem_limit((const void*)k_had_expand2, se);
+  const int mt = (M + 63) / 64, bt = (nrhs + 63) / 64;
+  // split rows so the contraction fills ~2 CTAs per SM
+  int chunks = int(std::max<i64>(1, std::min<i64>((296 + mt * bt - 1) / (mt * bt), (N + 255) / 256)));
+  const i64 rows_per_chunk = ((N + chunks - 1) / chunks + HK_BK - 1) / HK_BK * HK_BK;
+  chunks = int((N + rows_per_chunk - 1) / rows_per_chunk);
+  ws.partial.reserve(static_cast<size_t>(chunks) * M * nrhs);
+  ws.C.reserve(static_cast<size_t>(M) * nrhs);
+  ws.Cp.reserve(static_cast<size_t>(M) * nrhs);
+  dim3 g1(static_cast<unsigned>(mt), static_cast<unsigned>(bt), static_cast<unsigned>(chunks));
+  k_had_contract2<<<g1, 128, sc, s>>>(A.Q.p, A.r, B.Q.p, B.r, v, N, nrhs, rows_per_chunk, ws.partial.p);
+  launched("hadamard contract (DMMA v2)");
+  k_had_reduce<<<blocks_for((i64)M * nrhs), 256, 0, s>>>(ws.partial.p, chunks, M, nrhs, ws.C.p);
+  launched("hadamard reduce");
+  k_had_tridiag<<<blocks_for((i64)M * nrhs), 256, 0, s>>>(ws.C.p, A.r, B.r, nrhs, B.ab.p, B.ab.p + B.r, ws.Cp.p);
+  launched("hadamard tridiag");
+  dim3 g3(static_cast<unsigned>((N + 63) / 64), static_cast<unsigned>(bt));
+  k_had_expand2<<<g3, 128, se, s>>>(A.QT.p, A.r, B.Q.p, B.r, ws.Cp.p, N, nrhs, noise_v, n_value, nv2, ng2,
+                                    accumulate ? 1 : 0, out);
+  launched("hadamard expand (DMMA v2)");
+  return true;
+}
+
 static void hadamard_pair(const Factor& A, const Factor& B, const double* v, int nrhs, double* out, bool accumulate,
                           const double* noise_v, i64 n_value, double nv2, double ng2, HadScratch& ws,
                           cudaStream_t s) {
+  if (hadamard_pair3(A, B, v, nrhs, out, accumulate, noise_v, n_value, nv2, ng2, ws, s)) return;
+  if (hadamard_pair2(A, B, v, nrhs, out, accumulate, noise_v, n_value, nv2, ng2, ws, s)) return;
   const i64 N = A.N;
   const int M = A.r * B.r;
   const int mt = (M + H_BM - 1) / H_BM, bt = (nrhs + H_BN - 1) / H_BN;

@@ -39,9 +39,14 @@ struct Tuning {
   std::atomic<int> scatter{0}, gather{0}, toeplitz{0}, precond{0}, fused{0}, fused_prof{0}, pcg_fused{0};
   // fused 2-D MVM decomposition overrides (0 = heuristic)
   std::atomic<int> f2_stc{0}, f2_sl{0}, f2_gtc{0}, f2_gl{0}, f2_tsplit{0}, f2_per_sm{0};
-  std::atomic<int> f2_skip{0}, f2_grid{0}, f2_rp{0};
-  std::atomic<int> f2_smode{0}, f2_gmode{0}, f2_nspl{0}, f2_nst{0};  // 1 staged, 2 direct (0 = default)  // debug: bitmask of phases to skip (1 S, 2 T1, 4 T0, 8 G)
+  std::atomic<int> f2_skip{0};  // debug: bitmask of phases to skip (1 S, 2 T1, 4 T0, 8 G)
+  std::atomic<int> f2_grid{0}, f2_rp{0};
+  std::atomic<int> f2_smode{0}, f2_gmode{0};  // 1 staged, 2 direct (0 = default)
+  std::atomic<int> f2_nspl{0}, f2_nst{0};
   std::atomic<int> e2e_chunk{0};  // gk_op_mvm pipeline chunk width (0 = auto)
+  // D-SKIP Hadamard kernels: 0 = TMA-ring DMMA (v3, falling back to v2 for odd
+  // sizes), 3 = cp.async DMMA (v2), 1 = first generation
+  std::atomic<int> dskip{0};
   std::atomic<int> gen{0};  // bumped by every gk_set_tuning call (cached plans rebuild)
 };
 extern Tuning g_tuning;

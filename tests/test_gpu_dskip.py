@@ -43,6 +43,26 @@ def test_hadamard_mvm_matches_oracle_with_identical_factors(d, rank):
         assert rel(g.row(i), ref.row(i)) <= 1e-12
 
 
+@pytest.mark.parametrize("knob", [0, 3, 1])  # 0: TMA-ring DMMA kernels (v3), 3: cp.async DMMA (v2), 1: first gen
+@pytest.mark.parametrize("nrhs", [1, 2, 7, 18, 40, 64, 130])
+def test_hadamard_kernel_generations_match_oracle(knob, nrhs):
+    """Every Hadamard-pair kernel generation and column-tile width (16/32/64
+    RHS per CTA, odd RHS counts falling back to v2) against the oracle with
+    identical factors; rank 24 (even) and 13 (odd: v3 declines)."""
+    n, d = 400, 2
+    X = pts(n, d, 77)
+    k = O.KernelSpec(0.5, 1.0)
+    V = np.random.default_rng(nrhs).standard_normal(((d + 1) * n, nrhs))
+    try:
+        gk.set_tuning("dskip", knob)
+        for rank in (24, 13):
+            ref = O.DskipOperator(k, X, (0.05, 0.02), rank=rank, grid_ratio=0.1, max_grid_nodes=64)
+            g = gk.DskipOperator.from_factors(ref.factors(), n, d, (0.05, 0.02))
+            assert rel(g.mvm(V), ref.mvm(V)) <= 1e-12, rank
+    finally:
+        gk.set_tuning("dskip", 0)
+
+
 def test_full_rank_device_build_matches_dense_hadamard():  # test_dskip.cpp:122-154
     n, d = 30, 3
     X = pts(n, d, 21)

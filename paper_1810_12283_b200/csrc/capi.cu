@@ -155,6 +155,7 @@ int gk_set_tuning(const char* key, int value) {
                            : k == "pcg_fused" ? &g_tuning.pcg_fused
                            : k == "e2e_chunk" ? &g_tuning.e2e_chunk
                            : k == "dskip" ? &g_tuning.dskip
+                           : k == "dskip_e" ? &g_tuning.dskip_e
                            : k == "f2_stc" ? &g_tuning.f2_stc
                            : k == "f2_sl" ? &g_tuning.f2_sl
                            : k == "f2_gtc" ? &g_tuning.f2_gtc

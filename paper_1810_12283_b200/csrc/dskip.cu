@@ -164,7 +164,8 @@ __global__ void k_had_reduce(const double* __restrict__ partial, int chunks, int
   const i64 items = (i64)M * nrhs;
   for (i64 it = blockIdx.x * (i64)blockDim.x + threadIdx.x; it < items; it += (i64)gridDim.x * blockDim.x) {
     double s = 0.0;
-    for (int c = 0; c < chunks; ++c) s += partial[(i64)c * items + it];
+#pragma unroll 8
+    for (int c = 0; c < chunks; ++c) s += __ldcs(partial + (i64)c * items + it);  // read once: evict-first
     C[it] = s;
   }
 }
@@ -459,6 +460,8 @@ __global__ void __launch_bounds__(128) k_had_expand2(const double* __restrict__ 
 // instead of per-16-byte cp.async loops, constant-trip fully unrolled stages
 // (tails are zero rows, never predicated), and CTA shapes sized for 3-4
 // resident CTAs per SM. Needs even ranks and an even RHS count (16-byte rows).
+// The B factor's tridiagonal is folded into the expansion through its stored
+// QT = Q T (no separate T_B pass over C).
 // NJ = 8-column tiles per warp: the CTA covers 16·NJ right-hand sides.
 __device__ __forceinline__ unsigned hk_su32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -502,6 +505,7 @@ __global__ void __launch_bounds__(128, 4) k_had_contract3(const double* __restri
   const int SA = hk_pad(ra), SBq = hk_pad(rb);
   const int stage_d = H3_BK * (SA + SBq + SV);
   unsigned long long* full = reinterpret_cast<unsigned long long*>(hk_sm + H3_NS * stage_d);
+  unsigned long long* empty = full + H3_NS;
   const int M = ra * rb;
   const int m0 = blockIdx.x * 64, b0 = blockIdx.y * BWC;
   const int bw = min(BWC, nrhs - b0);
@@ -509,108 +513,127 @@ __global__ void __launch_bounds__(128, 4) k_had_contract3(const double* __restri
   const i64 r_end = min(N, r_begin + rows_per_chunk);
   const int nst = r_end > r_begin ? int((r_end - r_begin + H3_BK - 1) / H3_BK) : 0;
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32, g = lane / 4, t4 = lane % 4;
-  const int wm = (warp & 1) * 32, wb = (warp >> 1) * 8 * NJ;
+  // warp w: m rows [16w, 16w+16) × all 16·NJ columns (2 m-tiles × 2·NJ b-tiles)
+  constexpr int JT = 2 * NJ;
+  const int wm = warp * 16;
   if (tid == 0) {
-    for (int s = 0; s < H3_NS; ++s) hk_mbar_init(full + s, 3 * H3_BK);
+    for (int s = 0; s < H3_NS; ++s) hk_mbar_init(full + s, 32), hk_mbar_init(empty + s, 4);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  // threads 0..15: QA rows, 16..31: QB rows, 32..47: V rows of one stage
+  // warp 0 fills a stage: lane L moves QA row L (L < 16) or QB row L-16, and
+  // lanes 0..15 also V row L; each lane arrives once with the bytes it issued
+  const bool lo = lane < H3_BK;
+  const int qrow = lo ? lane : lane - H3_BK;
+  const int q_soff = lo ? qrow * SA : H3_BK * SA + qrow * SBq;
+  const unsigned q_bytes = (lo ? ra : rb) * 8u;
+  const double* q_src = lo ? QA + (r_begin + qrow) * ra : QB + (r_begin + qrow) * rb;
+  const i64 q_step = (i64)H3_BK * (lo ? ra : rb);
+  const int v_soff = H3_BK * (SA + SBq) + qrow * SV;
+  const double* v_src = V + (r_begin + qrow) * nrhs + b0;
   auto issue = [&](int st) {
-    if (tid >= 3 * H3_BK) return;
     const i64 rs = r_begin + (i64)st * H3_BK;
     const int nr = int(min((i64)H3_BK, r_end - rs));
     double* base = hk_sm + (st % H3_NS) * stage_d;
     unsigned long long* b = full + st % H3_NS;
-    const int mat = tid / H3_BK, row = tid % H3_BK;
-    double* dst;
-    const double* src;
-    int bytes, w;
-    if (mat == 0) {
-      dst = base + row * SA, src = QA + (rs + row) * ra, bytes = ra * 8, w = SA;
-    } else if (mat == 1) {
-      dst = base + H3_BK * SA + row * SBq, src = QB + (rs + row) * rb, bytes = rb * 8, w = SBq;
-    } else {
-      dst = base + H3_BK * (SA + SBq) + row * SV, src = V + (rs + row) * nrhs + b0, bytes = bw * 8, w = SV;
-    }
-    if (row < nr) {
-      hk_mbar_arrive_tx(b, bytes);
-      hk_bulk(dst, src, bytes, b);
-    } else {
-      hk_zero_row(dst, w);  // tail rows contribute exact zeros
-      hk_mbar_arrive(b);
+    if (nr == H3_BK) {
+      hk_mbar_arrive_tx(b, q_bytes + (lo ? bw * 8u : 0u));
+      hk_bulk(base + q_soff, q_src + st * q_step, q_bytes, b);
+      if (lo) hk_bulk(base + v_soff, v_src + (i64)st * H3_BK * nrhs, bw * 8u, b);
+    } else {  // tail stage: rows past the chunk are zero rows
+      const bool live = qrow < nr;
+      if (live) {
+        hk_mbar_arrive_tx(b, q_bytes + (lo ? bw * 8u : 0u));
+        hk_bulk(base + q_soff, q_src + st * q_step, q_bytes, b);
+        if (lo) hk_bulk(base + v_soff, v_src + (i64)st * H3_BK * nrhs, bw * 8u, b);
+      } else {
+        hk_zero_row(base + q_soff, lo ? SA : SBq);
+        if (lo) hk_zero_row(base + v_soff, SV);
+        hk_mbar_arrive(b);
+      }
     }
   };
-  int ka[4], la[4];
+  int ka[2], la[2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < 2; ++i) {
     const int m = min(m0 + wm + 8 * i + g, M - 1);  // rows past M: finite, discarded
     ka[i] = m / rb;
     la[i] = m - ka[i] * rb;
   }
-  double acc[4][NJ][2];
+  double acc[2][JT][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  for (int s = 0; s < min(H3_NS, nst); ++s) issue(s);
+    for (int j = 0; j < JT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  if (warp == 0)
+    for (int s = 0; s < min(H3_NS, nst); ++s) issue(s);
   for (int it = 0; it < nst; ++it) {
-    hk_mbar_wait(full + it % H3_NS, (it / H3_NS) & 1);
-    const double* A1 = hk_sm + (it % H3_NS) * stage_d;
+    const int sb = it % H3_NS;
+    const unsigned ph = (it / H3_NS) & 1;
+    hk_mbar_wait(full + sb, ph);
+    const double* A1 = hk_sm + sb * stage_d;
     const double* B1 = A1 + H3_BK * SA;
     const double* V1 = B1 + H3_BK * SBq;
 #pragma unroll
     for (int kk = 0; kk < H3_BK; kk += 4) {
       const int row = kk + t4;
-      double af[4], bf[NJ];
+      double af[2], bf[JT];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = A1[row * SA + ka[i]] * B1[row * SBq + la[i]];
+      for (int i = 0; i < 2; ++i) af[i] = A1[row * SA + ka[i]] * B1[row * SBq + la[i]];
 #pragma unroll
-      for (int j = 0; j < NJ; ++j) bf[j] = V1[row * SV + wb + 8 * j + g];
+      for (int j = 0; j < JT; ++j) bf[j] = V1[row * SV + 8 * j + g];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < JT; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
-    __syncthreads();
-    if (it + H3_NS < nst) issue(it + H3_NS);
+    __syncwarp();
+    if (lane == 0) hk_mbar_arrive(empty + sb);  // this warp is done with the stage
+    if (warp == 0 && it + H3_NS < nst) {
+      hk_mbar_wait(empty + sb, ph);  // all four warps done: refill
+      issue(it + H3_NS);
+    }
   }
   double* out = partial + (i64)blockIdx.z * M * nrhs;
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) {
+    for (int j = 0; j < JT; ++j) {
       const int m = m0 + wm + 8 * i + g;
-      const int bl = wb + 8 * j + 2 * t4;
+      const int bl = 8 * j + 2 * t4;
       if (m < M && bl < bw)
         *reinterpret_cast<double2*>(out + (i64)m * nrhs + b0 + bl) = make_double2(acc[i][j][0], acc[i][j][1]);
     }
 }
 
-template <int NJ>
+template <int NJ, int MC, int NSE>
 __global__ void __launch_bounds__(128, 3) k_had_expand3(const double* __restrict__ QTA, int ra,
                                                         const double* __restrict__ QB, int rb,
                                                         const double* __restrict__ Cp, i64 N, int nrhs,
                                                         const double* __restrict__ v, i64 n_value, double nv2,
                                                         double ng2, int accumulate, double* __restrict__ out) {
+  static_assert(MC <= 32 && MC % 4 == 0, "one warp-0 lane per C' row");
   extern __shared__ __align__(128) double hk_sm[];
   constexpr int BWC = 16 * NJ, SV = BWC + ((4 - BWC % 16) + 16) % 16;
   const int SA = hk_pad(ra), SBq = hk_pad(rb);
   const int M = ra * rb;
   double* QAs = hk_sm;              // [64][SA]
   double* QBs = QAs + 64 * SA;      // [64][SBq]
-  double* Cs = QBs + 64 * SBq;      // [H3_NSE][H3_MC][SV]
-  unsigned long long* full = reinterpret_cast<unsigned long long*>(Cs + H3_NSE * H3_MC * SV);
-  unsigned long long* qbar = full + H3_NSE;
+  double* Cs = QBs + 64 * SBq;      // [NSE][MC][SV]
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(Cs + NSE * MC * SV);
+  unsigned long long* empty = full + NSE;
+  unsigned long long* qbar = empty + NSE;
   const i64 i0 = (i64)blockIdx.x * 64;
   const int b0 = blockIdx.y * BWC;
   const int bw = min(BWC, nrhs - b0);
   const int nr = int(min((i64)64, N - i0));
-  const int nch = (M + H3_MC - 1) / H3_MC;
+  const int nch = (M + MC - 1) / MC;
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32, g = lane / 4, t4 = lane % 4;
-  const int wi = (warp & 1) * 32, wb = (warp >> 1) * 8 * NJ;
+  // warp w: rows [16w, 16w+16) × all 16·NJ columns
+  constexpr int JT = 2 * NJ;
+  const int wi = warp * 16;
   if (tid == 0) {
-    for (int s = 0; s < H3_NSE; ++s) hk_mbar_init(full + s, H3_MC);
+    for (int s = 0; s < NSE; ++s) hk_mbar_init(full + s, 32), hk_mbar_init(empty + s, 4);
     hk_mbar_init(qbar, 128);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -626,61 +649,66 @@ __global__ void __launch_bounds__(128, 3) k_had_expand3(const double* __restrict
       hk_mbar_arrive(qbar);  // rows past N only feed discarded outputs
     }
   }
-  auto issue = [&](int c) {
-    if (tid >= H3_MC) return;
-    const int m = c * H3_MC + tid;
-    double* dst = Cs + (c % H3_NSE) * H3_MC * SV + tid * SV;
-    unsigned long long* b = full + c % H3_NSE;
-    if (m < M) {
+  auto issue = [&](int c) {  // warp 0; lane L < MC moves C' row c·MC + L
+    const int m = c * MC + lane;
+    unsigned long long* b = full + c % NSE;
+    if (lane < MC && m < M) {
       hk_mbar_arrive_tx(b, bw * 8);
-      hk_bulk(dst, Cp + (i64)m * nrhs + b0, bw * 8, b);
+      hk_bulk(Cs + (c % NSE) * MC * SV + lane * SV, Cp + (i64)m * nrhs + b0, bw * 8, b);
     } else {
-      hk_zero_row(dst, SV);
+      if (lane < MC) hk_zero_row(Cs + (c % NSE) * MC * SV + lane * SV, SV);
       hk_mbar_arrive(b);
     }
   };
-  for (int c = 0; c < min(H3_NSE, nch); ++c) issue(c);
-  double acc[4][NJ][2];
+  if (warp == 0)
+    for (int c = 0; c < min(NSE, nch); ++c) issue(c);
+  double acc[2][JT][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < JT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   int k = t4 / rb, l = t4 % rb;  // (k, l) of m = c·MC + kk + t4, advanced by 4 per step
-  const double* qa_row[4];
-  const double* qb_row[4];
+  const double* qa_row[2];
+  const double* qb_row[2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < 2; ++i) {
     qa_row[i] = QAs + (wi + 8 * i + g) * SA;
     qb_row[i] = QBs + (wi + 8 * i + g) * SBq;
   }
   hk_mbar_wait(qbar, 0);
   for (int c = 0; c < nch; ++c) {
-    hk_mbar_wait(full + c % H3_NSE, (c / H3_NSE) & 1);
-    const double* C1 = Cs + (c % H3_NSE) * H3_MC * SV;
+    const int sb = c % NSE;
+    const unsigned ph = (c / NSE) & 1;
+    hk_mbar_wait(full + sb, ph);
+    const double* C1 = Cs + sb * MC * SV;
 #pragma unroll
-    for (int kk = 0; kk < H3_MC; kk += 4) {
+    for (int kk = 0; kk < MC; kk += 4) {
       const int kc = k < ra ? k : 0;  // m past M meets a zero C' row
-      double af[4], bf[NJ];
+      double af[2], bf[JT];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = qa_row[i][kc] * qb_row[i][l];
+      for (int i = 0; i < 2; ++i) af[i] = qa_row[i][kc] * qb_row[i][l];
 #pragma unroll
-      for (int j = 0; j < NJ; ++j) bf[j] = C1[(kk + t4) * SV + wb + 8 * j + g];
+      for (int j = 0; j < JT; ++j) bf[j] = C1[(kk + t4) * SV + 8 * j + g];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < JT; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
       l += 4;
       while (l >= rb) l -= rb, ++k;
     }
-    __syncthreads();
-    if (c + H3_NSE < nch) issue(c + H3_NSE);
+    __syncwarp();
+    if (lane == 0) hk_mbar_arrive(empty + sb);
+    if (warp == 0 && c + NSE < nch) {
+      hk_mbar_wait(empty + sb, ph);
+      issue(c + NSE);
+    }
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) {
+    for (int j = 0; j < JT; ++j) {
       const i64 row = i0 + wi + 8 * i + g;
-      const int bl = wb + 8 * j + 2 * t4;
+      const int bl = 8 * j + 2 * t4;
       if (row < N && bl < bw) {
         const i64 idx = row * nrhs + b0 + bl;
         double2 val = make_double2(acc[i][j][0], acc[i][j][1]);
@@ -795,13 +823,12 @@ static size_t had2_expand_smem(int ra, int rb, int nrhs) {
 template <int NJ>
 static size_t had3_contract_smem(int ra, int rb) {
   constexpr int BWC = 16 * NJ, SV = BWC + ((4 - BWC % 16) + 16) % 16;
-  return sizeof(double) * size_t(H3_NS) * H3_BK * (hk_pad(ra) + hk_pad(rb) + SV) + 8 * H3_NS;
+  return sizeof(double) * size_t(H3_NS) * H3_BK * (hk_pad(ra) + hk_pad(rb) + SV) + 16 * H3_NS;
 }
-template <int NJ>
+template <int NJ, int MC, int NSE>
 static size_t had3_expand_smem(int ra, int rb) {
   constexpr int BWC = 16 * NJ, SV = BWC + ((4 - BWC % 16) + 16) % 16;
-  return sizeof(double) * (size_t(64) * (hk_pad(ra) + hk_pad(rb)) + size_t(H3_NSE) * H3_MC * SV) +
-         8 * (H3_NSE + 1);
+  return sizeof(double) * (size_t(64) * (hk_pad(ra) + hk_pad(rb)) + size_t(NSE) * MC * SV) + 16 * NSE + 8;
 }
 
 static int device_sm_count() {
@@ -811,19 +838,30 @@ static int device_sm_count() {
   return sms;
 }
 
+template <int NJ, int MC, int NSE>
+static void had3_expand_launch(const Factor& A, const Factor& B, const double* Cp, int nrhs, double* out,
+                               bool accumulate, const double* noise_v, i64 n_value, double nv2, double ng2,
+                               cudaStream_t s) {
+  const size_t se = had3_expand_smem<NJ, MC, NSE>(A.r, B.r);
+  raise_smem_limit((const void*)k_had_expand3<NJ, MC, NSE>, se);
+  dim3 g3(static_cast<unsigned>((A.N + 63) / 64), static_cast<unsigned>((nrhs + 16 * NJ - 1) / (16 * NJ)));
+  k_had_expand3<NJ, MC, NSE><<<g3, 128, se, s>>>(A.QT.p, A.r, B.QT.p, B.r, Cp, A.N, nrhs, noise_v, n_value, nv2,
+                                                 ng2, accumulate ? 1 : 0, out);
+  launched("hadamard expand (DMMA v3)");
+}
+
 template <int NJ>
 static void hadamard_pair3_launch(const Factor& A, const Factor& B, const double* v, int nrhs, double* out,
                                   bool accumulate, const double* noise_v, i64 n_value, double nv2, double ng2,
                                   HadScratch& ws, cudaStream_t s) {
   const i64 N = A.N;
   const int M = A.r * B.r;
-  const size_t sc = had3_contract_smem<NJ>(A.r, B.r), se = had3_expand_smem<NJ>(A.r, B.r);
+  const size_t sc = had3_contract_smem<NJ>(A.r, B.r);
   raise_smem_limit((const void*)k_had_contract3<NJ>, sc);
-  raise_smem_limit((const void*)k_had_expand3<NJ>, se);
   const int mt = (M + 63) / 64, bt = (nrhs + 16 * NJ - 1) / (16 * NJ);
-  // row-split so that all CTAs of the contraction are co-resident (4 per SM)
+  // row-split so that all CTAs of the contraction are co-resident
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_had_contract3<NJ>, 128, sc);
+  GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_had_contract3<NJ>, 128, sc));
   const int slots = std::max(1, per_sm) * device_sm_count();
   int chunks = int(std::max<i64>(1, std::min<i64>(slots / (mt * bt), (N + 4 * H3_BK - 1) / (4 * H3_BK))));
   const i64 rows_per_chunk = ((N + chunks - 1) / chunks + H3_BK - 1) / H3_BK * H3_BK;
@@ -836,12 +874,14 @@ static void hadamard_pair3_launch(const Factor& A, const Factor& B, const double
   launched("hadamard contract (DMMA v3)");
   k_had_reduce<<<blocks_for((i64)M * nrhs), 256, 0, s>>>(ws.partial.p, chunks, M, nrhs, ws.C.p);
   launched("hadamard reduce");
-  k_had_tridiag<<<blocks_for((i64)M * nrhs), 256, 0, s>>>(ws.C.p, A.r, B.r, nrhs, B.ab.p, B.ab.p + B.r, ws.Cp.p);
-  launched("hadamard tridiag");
-  dim3 g3(static_cast<unsigned>((N + 63) / 64), static_cast<unsigned>(bt));
-  k_had_expand3<NJ><<<g3, 128, se, s>>>(A.QT.p, A.r, B.Q.p, B.r, ws.Cp.p, N, nrhs, noise_v, n_value, nv2, ng2,
-                                        accumulate ? 1 : 0, out);
-  launched("hadamard expand (DMMA v3)");
+  // T_B is folded into the expansion: Σ_l QB[i][l] (T_B C)[k][l] = Σ_l (QB T_B)[i][l] C[k][l],
+  // and QB T_B is the factor's stored QT — no tridiagonal pass
+  switch (g_tuning.dskip_e.load()) {
+    case 1: had3_expand_launch<NJ, 16, 2>(A, B, ws.C.p, nrhs, out, accumulate, noise_v, n_value, nv2, ng2, s); break;
+    case 2: had3_expand_launch<NJ, 16, 4>(A, B, ws.C.p, nrhs, out, accumulate, noise_v, n_value, nv2, ng2, s); break;
+    case 3: had3_expand_launch<NJ, 32, 2>(A, B, ws.C.p, nrhs, out, accumulate, noise_v, n_value, nv2, ng2, s); break;
+    default: had3_expand_launch<NJ, 8, 4>(A, B, ws.C.p, nrhs, out, accumulate, noise_v, n_value, nv2, ng2, s);
+  }
 }
 
 static bool hadamard_pair3(const Factor& A, const Factor& B, const double* v, int nrhs, double* out, bool accumulate,
@@ -849,9 +889,9 @@ static bool hadamard_pair3(const Factor& A, const Factor& B, const double* v, in
                            cudaStream_t s) {
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (g_tuning.dskip.load() != 0 || (A.r & 1) || (B.r & 1) || (nrhs & 1) || !al16(v) || !al16(out) ||
-      (noise_v && !al16(noise_v)) || !al16(A.Q.p) || !al16(A.QT.p) || !al16(B.Q.p))
+      (noise_v && !al16(noise_v)) || !al16(A.Q.p) || !al16(A.QT.p) || !al16(B.Q.p) || !al16(B.QT.p))
     return false;
-  if (had3_expand_smem<4>(A.r, B.r) > 200 * 1024) return false;
+  if (had3_expand_smem<4, 32, 2>(A.r, B.r) > 200 * 1024) return false;
   if (nrhs > 32)
     hadamard_pair3_launch<4>(A, B, v, nrhs, out, accumulate, noise_v, n_value, nv2, ng2, ws, s);
   else if (nrhs > 16)

@@ -47,6 +47,7 @@ struct Tuning {
   // D-SKIP Hadamard kernels: 0 = TMA-ring DMMA (v3, falling back to v2 for odd
   // sizes), 3 = cp.async DMMA (v2), 1 = first generation
   std::atomic<int> dskip{0};
+  std::atomic<int> dskip_e{0};  // v3 expand ring: 0 = 8 m × 4 stages, 1 = 16 × 2, 2 = 16 × 4, 3 = 32 × 2
   std::atomic<int> gen{0};  // bumped by every gk_set_tuning call (cached plans rebuild)
 };
 extern Tuning g_tuning;

@@ -20,8 +20,9 @@ dev = torch.device("cuda")
 V = torch.randn(N * nrhs, dtype=torch.float64, device=dev)
 O = torch.empty_like(V)
 st = torch.cuda.current_stream().cuda_stream
-def run(knob):
+def run(knob, ek=0):
     gk.set_tuning("dskip", knob)
+    gk.set_tuning("dskip_e", ek)
     for _ in range(3):
         op.stage_dev(3, V.data_ptr(), O.data_ptr(), nrhs, stream=st)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(20)]
@@ -42,5 +43,9 @@ for knob in (1, 3, 0):
     print(f"C5[dskip={knob}] build {build:.2f} s; MVM {ms*1e3:.1f} us for {nrhs} RHS; "
           f"{N*nrhs/(ms*1e-3)/1e9:.2f} G rows*RHS/s; {flops/(ms*1e-3)/1e12:.2f} TFLOP/s (4 N r^2 B model, r=30); "
           f"factor ranks {ranks}", flush=True)
+for ek in (1, 2, 3):
+    ms, out = run(0, ek)
+    print(f"C5[dskip=0 dskip_e={ek}] MVM {ms*1e3:.1f} us; {flops/(ms*1e-3)/1e12:.2f} TFLOP/s; "
+          f"rel diff vs v1 {float((out - res[1]).norm() / res[1].norm()):.2e}", flush=True)
 print("v2 vs v1 rel diff", float((res[3] - res[1]).norm() / res[1].norm()))
 print("v3 vs v1 rel diff", float((res[0] - res[1]).norm() / res[1].norm()))

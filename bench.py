@@ -309,6 +309,13 @@ def run_gpu(args):
         except Exception as e:  # reported, never silently replaced
             c4 = {"error": f"{type(e).__name__}: {e}"}
 
+    c5 = None
+    if not args.no_c5:
+        try:
+            c5 = c5_dskip(args, world, rank, local, dist)
+        except Exception as e:  # reported, never silently replaced
+            c5 = {"error": f"{type(e).__name__}: {e}"}
+
     line = None
     if rank == 0:
         cpu = cpu_baseline(args) if world == 1 and not args.no_cpu_baseline else None
@@ -340,6 +347,7 @@ def run_gpu(args):
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "c4_slab": c4,
+            "c5_dskip": c5,
         }
     if world > 1:
         dist.barrier()
@@ -398,6 +406,66 @@ def c4_slab(args, world, rank, local, dist):
             "scaling": "strong", "ms_per_mvm": ms, "value": sop.size() * nrhs / (ms * 1e-3),
             "unit": UNIT, "local_points": int(sop.mine.size), "build_s": build_s,
             "timing": "CUDA events per MVM on the launching stream (L2 not evicted), median, max over ranks"}
+
+
+def c5_dskip(args, world, rank, local, dist):
+    """C5 (d = 6, n = 10,000, N = 70,000; product SE ℓ = 0.3, rank 30 on
+    100-node 1-D grids; 64 RHS per rank): the D-SKIP Hadamard MVM, a DMMA-bound
+    Khatri–Rao GEMM pair (4·N·r_A·r_B·B flops). RHS-sharded:
+    each rank builds the same operator and owns its own 64 columns (weak)."""
+    import torch
+    import paper_1810_12283_b200 as gk
+    dev = torch.device("cuda", local)
+    X, y, dY = gk.make_dataset(5, 0)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    op = gk.DskipOperator(gk.KernelSpec(0.3, 1.0), X, (1e-2, 1e-2), rank=30, grid_ratio=0.01,
+                          max_grid_nodes=100, seed=0, device=local)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    N, nrhs = op.size(), 64
+    ranks = [int(f.Q.shape[1]) for f in op.factors()]
+    ra, rb = (ranks + [1])[:2]
+    g = torch.Generator(device="cpu").manual_seed(1000 + rank)
+    V = torch.randn(N * nrhs, dtype=torch.float64, generator=g).to(dev)
+    O = torch.empty_like(V)
+    flush = torch.ones(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    st = torch.cuda.current_stream(dev)
+    l0 = gk.kernel_launch_count()
+    op.stage_dev(3, V.data_ptr(), O.data_ptr(), nrhs, stream=st.cuda_stream)
+    launches = gk.kernel_launch_count() - l0
+    for _ in range(3):
+        op.stage_dev(3, V.data_ptr(), O.data_ptr(), nrhs, stream=st.cuda_stream)
+    reps = 20
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for e0, e1 in ev:
+        flush.sum()
+        e0.record(st)
+        op.stage_dev(3, V.data_ptr(), O.data_ptr(), nrhs, stream=st.cuda_stream)
+        e1.record(st)
+    torch.cuda.synchronize()
+    ms = float(np.median([a.elapsed_time(b) for a, b in ev]))
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    flops = 4.0 * N * ra * rb * nrhs
+    peak = gk.dmma_peak_tflops(local)
+    achieved = world * flops / (ms * 1e-3) / 1e12
+    return {"workload": "C5: D-SKIP d=6 n=10000 (N=70000) product SE ell=0.3 sigma=1e-2, rank 30, "
+                        "100-node 1-D grids, 64 RHS per rank",
+            "parallelism": f"rhs-shard x{world}", "scaling": "weak", "ms_per_mvm": ms,
+            "value": world * N * nrhs / (ms * 1e-3), "unit": UNIT, "build_s": build_s,
+            "factor_ranks": ranks, "gpu_launches_per_mvm": int(launches),
+            "roofline": {"bound": "tensor (fp64 DMMA)", "achieved": achieved / world, "peak": peak,
+                         "unit": "TFLOP/s", "frac": achieved / world / peak,
+                         "flops_per_mvm": flops, "flops_formula": "SURVEY 8(d): 4*N*r_A*r_B*B",
+                         "peak_source": "gk_debug_dmma_peak (register-only DMMA m8n8k4 kernel, this GPU, best of 5)"},
+            "timing": "CUDA events per MVM on the launching stream, L2 evicted before each (256 MB read), "
+                      "median of 20, max over ranks"}
 
 
 def cpu_baseline(args, full=False):
@@ -460,6 +528,7 @@ def main():
     ap.add_argument("--impl", default="gk", choices=["gk", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 grid-slab sharded MVM measurement")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 D-SKIP MVM measurement")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl != "reference":
         args.warmup = 3

@@ -99,6 +99,9 @@ typedef struct gk_op gk_op;
  * mode-0 done, barrier 3 passed, gather done. Copies the stamps of the last
  * launch for `nrhs` into out[cta*8 + k]; returns the CTA count (0 if none). */
 int gk_debug_fused_phases(gk_op* op, int nrhs, int64_t* out, int max_ctas);
+/* fp64 tensor-core (DMMA m8n8k4) throughput of `device` in TFLOP/s, measured
+ * by a register-only kernel (best of 5): the D-SKIP roofline denominator. */
+gk_status gk_debug_dmma_peak(int device, double* tflops);
 
 /* DskiOperator(kernel, grid, X, noise, order, with_gradients) (dski.hpp:58-65).
  * order: 0 quintic, 1 cubic. */

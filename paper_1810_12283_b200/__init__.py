@@ -59,6 +59,7 @@ _SIGS = {
     "gk_set_tuning": (C.c_int, [C.c_char_p, C.c_int]),
     "gk_kernel_launch_count": (_i64, []),
     "gk_debug_fused_phases": (C.c_int, [_vp, C.c_int, _i64p, C.c_int]),
+    "gk_debug_dmma_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double)]),
     "gk_dski_gather_dev": (C.c_int, [_vp, _vp, _vp, _vp, _i64, _vp]),
     "gk_grid_cover": (C.c_int, [_dp, _i64, C.c_int, _d, C.c_int, C.c_int, C.POINTER(GkGrid)]),
     "gk_mix_seed": (_u64, [_u64, _u64]),
@@ -757,6 +758,13 @@ def stacked_targets(y, dY, mean):
     if dY is not None:
         parts += [np.asarray(dY)[:, j] for j in range(np.asarray(dY).shape[1])]
     return np.concatenate(parts)
+
+
+def dmma_peak_tflops(device=0):
+    """Measured fp64 tensor-core (DMMA) throughput of `device`, TFLOP/s."""
+    t = C.c_double(0.0)
+    _check(_lib.gk_debug_dmma_peak(int(device), C.byref(t)))
+    return t.value
 
 
 def debug_fused_phases(op, nrhs, max_ctas=4096):

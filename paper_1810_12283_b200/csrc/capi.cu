@@ -40,6 +40,7 @@ int dskip_factor_count(const Op& o);
 i64 dskip_factor_rank(const Op& o, int f);
 void dskip_factor_get(const Op& o, int f, double* Q, double* a, double* b);
 void dskip_dlogell(Op& o, const double* in, double* out, int nrhs, cudaStream_t s);
+double dmma_peak_tflops(int device);
 }  // namespace gk
 
 using namespace gk;
@@ -424,6 +425,13 @@ int gk_debug_fused_phases(gk_op* h, int nrhs, int64_t* out, int max_ctas) {
     n = dski_fused_phases(op, nrhs, out, max_ctas);
   });
   return n;
+}
+
+gk_status gk_debug_dmma_peak(int device, double* tflops) {
+  return guard([&] {
+    if (!tflops) fail(GK_ERR_ARG, "null output");
+    *tflops = dmma_peak_tflops(device);
+  });
 }
 
 int64_t gk_dski_grid_size(const gk_op* h) {

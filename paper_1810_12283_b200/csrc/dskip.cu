@@ -454,6 +454,14 @@ __global__ void __launch_bounds__(128) k_had_expand2(const double* __restrict__ 
       }
 }
 
+static int device_sm_count() {
+  int dev = 0, sms = 0;
+  GK_CUDA(cudaGetDevice(&dev));
+  GK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  return sms;
+}
+
+
 // ---------------------------------------------------------------- Khatri–Rao GEMMs v3
 // Same GEMMs as v2, with the operand rows moved by per-row TMA bulk copies
 // (cp.async.bulk, one issuing thread per row, completion on an mbarrier ring)
@@ -500,7 +508,7 @@ __global__ void __launch_bounds__(128, 4) k_had_contract3(const double* __restri
                                                           const double* __restrict__ QB, int rb,
                                                           const double* __restrict__ V, i64 N, int nrhs,
                                                           i64 rows_per_chunk, double* __restrict__ partial) {
-  extern __shared__ __align__(128) double hk_sm[];
+  extern __shared__ __align__(16) double hk_sm[];
   constexpr int BWC = 16 * NJ, SV = BWC + ((4 - BWC % 16) + 16) % 16;
   const int SA = hk_pad(ra), SBq = hk_pad(rb);
   const int stage_d = H3_BK * (SA + SBq + SV);
@@ -613,7 +621,7 @@ __global__ void __launch_bounds__(128, 3) k_had_expand3(const double* __restrict
                                                         const double* __restrict__ v, i64 n_value, double nv2,
                                                         double ng2, int accumulate, double* __restrict__ out) {
   static_assert(MC <= 32 && MC % 4 == 0, "one warp-0 lane per C' row");
-  extern __shared__ __align__(128) double hk_sm[];
+  extern __shared__ __align__(16) double hk_sm[];
   constexpr int BWC = 16 * NJ, SV = BWC + ((4 - BWC % 16) + 16) % 16;
   const int SA = hk_pad(ra), SBq = hk_pad(rb);
   const int M = ra * rb;
@@ -726,6 +734,22 @@ __global__ void __launch_bounds__(128, 3) k_had_expand3(const double* __restrict
     }
 }
 
+// fp64 tensor-core peak probe: 8 independent DMMA chains per warp, no memory
+// traffic — the denominator of the D-SKIP roofline, measured on the running box.
+__global__ void __launch_bounds__(128) k_dmma_peak(int iters, double* sink) {
+  double acc[8][2];
+  const double a = 1.0 + 1e-9 * threadIdx.x, b = 1.0 - 1e-9 * blockIdx.x;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) acc[c][0] = acc[c][1] = 0.0;
+  for (int it = 0; it < iters; ++it)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) dmma_8x8x4(acc[c][0], acc[c][1], a, b);
+  double t = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) t += acc[c][0] + acc[c][1];
+  if (t == 12345.678) sink[0] = t;  // keep the chains alive
+}
+
 // diag = Π_f Σ_k QT_f[i][k] Q_f[i][k] (+ noise)   (dskip.cpp:141-149)
 __global__ void k_had_diag(const double* const* __restrict__ Qs, const double* const* __restrict__ QTs,
                            const int* __restrict__ ranks, int nf, i64 N, i64 n_value, double nv2, double ng2,
@@ -759,6 +783,35 @@ __global__ void k_had_row(const double* const* __restrict__ Qs, const int* __res
 }
 
 }  // namespace
+
+double dmma_peak_tflops(int device) {
+  DeviceGuard dg(device);
+  const int sms = device_sm_count();
+  double* sink = nullptr;
+  GK_CUDA(cudaMalloc(&sink, sizeof(double)));
+  cudaEvent_t e0, e1;
+  GK_CUDA(cudaEventCreate(&e0));
+  GK_CUDA(cudaEventCreate(&e1));
+  const int iters = 4096, ctas = sms * 8;
+  k_dmma_peak<<<ctas, 128>>>(64, sink);  // warm up
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    GK_CUDA(cudaEventRecord(e0));
+    k_dmma_peak<<<ctas, 128>>>(iters, sink);
+    launched("dmma peak probe");
+    GK_CUDA(cudaEventRecord(e1));
+    GK_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    GK_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    best = std::min(best, ms);
+  }
+  GK_CUDA(cudaEventDestroy(e0));
+  GK_CUDA(cudaEventDestroy(e1));
+  GK_CUDA(cudaFree(sink));
+  const double flops = 2.0 * 8 * 8 * 4 * 8.0 * iters * (ctas * 4.0);  // per DMMA 512 flop, 8 chains, 4 warps/CTA
+  return flops / (best * 1e-3) / 1e12;
+}
+
 
 // ================================================================ factor / ops
 struct Factor {
@@ -829,13 +882,6 @@ template <int NJ, int MC, int NSE>
 static size_t had3_expand_smem(int ra, int rb) {
   constexpr int BWC = 16 * NJ, SV = BWC + ((4 - BWC % 16) + 16) % 16;
   return sizeof(double) * (size_t(64) * (hk_pad(ra) + hk_pad(rb)) + size_t(NSE) * MC * SV) + 16 * NSE + 8;
-}
-
-static int device_sm_count() {
-  int dev = 0, sms = 0;
-  GK_CUDA(cudaGetDevice(&dev));
-  GK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  return sms;
 }
 
 template <int NJ, int MC, int NSE>

@@ -177,6 +177,11 @@ int64_t gk_dskip_factor_rank(const gk_op* op, int f);
 gk_status gk_dskip_factor_get(const gk_op* op, int f, double* Q, double* alpha, double* beta);
 gk_status gk_dskip_dlogell_apply(const gk_op* op, const double* V, int64_t ldv, double* Out,
                                  int64_t ldo, int64_t nrhs);
+/* D-SKI ∂K∇/∂log ℓ · V = B (∂K_UU/∂log ℓ) Bᵀ V without noise — the "second
+ * grid operator" of GpModel::dlogell_apply (gp.cpp:212-213) built from
+ * kernel_dlogell_profile (dski.cpp:36-40); SE only. Host buffers, N × nrhs. */
+gk_status gk_dski_dlogell_apply(const gk_op* op, const double* V, int64_t ldv, double* Out, int64_t ldo,
+                                int64_t nrhs);
 
 /* Internal-layout stage entry points (device pointers, RHS-minor internal
  * layout; used by the benchmark to time each kernel on its own stream).
@@ -262,6 +267,15 @@ gk_status gk_lanczos(const gk_op* op, int64_t steps, uint64_t seed, const double
 /* trace_estimate (linalg.cpp:255-279): E_z[z^T A^{-1} B z], probes batched. */
 gk_status gk_trace_estimate(const gk_op* A, const gk_op* B, int probes, uint64_t seed, double tol,
                             int max_iterations, const gk_precond* precond, double* out);
+/* GpModel::lml_gradient (gp.cpp:220-292), stochastic-trace branch, for a D-SKI
+ * or D-SKIP operator: grad[p] = ½(αᵀ M_p α − tr(K⁻¹ M_p)) over θ = (log ℓ, log s,
+ * log σ₁[, log σ₂]) with M_0 = ∂K/∂log ℓ, M_1 = 2(K − noise), M_2/M_3 the
+ * noise blocks; traces by trace_estimate with `probes` Rademacher probes
+ * (streams 1000+q) and PCG at tol max(tol, 1e-2) preconditioned by M. alpha =
+ * K⁻¹ b (host, N). *nparams = 4 with gradient observations, else 3.
+ * GK_ERR_RUNTIME if a probe solve does not converge (linalg.cpp:273-275). */
+gk_status gk_lml_gradient(const gk_op* op, const gk_precond* M, const double* alpha, int probes, uint64_t seed,
+                          double tol, int maxit, double* grad, int* nparams);
 
 /* ---------------------------------------------------------------- GP glue
  * GpModel pieces on the hot path (gp.cpp:117-187,471-517): the operator is

@@ -119,6 +119,8 @@ def lib():
             "orc_gp_pivots": (C.c_int, [_vp, _i64p, _i64p]),
             "orc_gp_predict_mean_grad": (C.c_int, [_vp, _dp, _i64, _dp, _dp]),
             "orc_gp_predict_variance_pivchol": (C.c_int, [_vp, _dp, _dp]),
+            "orc_gp_lml_gradient": (C.c_int, [_vp, C.c_int, _dp, C.POINTER(C.c_int)]),
+            "orc_gp_dlogell_apply": (C.c_int, [_vp, _dp, _dp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -642,6 +644,20 @@ class GpModel:
         grads = np.empty((T, self.d), order="F")
         _check(lib().orc_gp_predict_mean_grad(self.h, _p(Xt), T, _p(vals), _p(grads)))
         return vals, grads
+
+    def lml_gradient(self, probes=8):
+        """GpModel::lml_gradient (gp.cpp:220-292): ∂LML/∂(log ℓ, log s, log σ₁[, log σ₂])."""
+        g = np.empty(4)
+        k = C.c_int()
+        _check(lib().orc_gp_lml_gradient(self.h, int(probes), _p(g), C.byref(k)))
+        return g[: k.value].copy()
+
+    def dlogell_apply(self, v):
+        """GpModel::dlogell_apply (gp.cpp:200-218)."""
+        v = _f64(v)
+        out = np.empty(v.size)
+        _check(lib().orc_gp_dlogell_apply(self.h, _p(v), _p(out)))
+        return out
 
     def predict_variance_pivchol(self, x):
         out = _d()

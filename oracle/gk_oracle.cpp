@@ -1406,6 +1406,66 @@ double GpModel::log_marginal_likelihood() {  // gp.cpp:181-187
   return -0.5 * (fit + cpx + N * std::log(2.0 * M_PI));
 }
 
+Vec GpModel::kernel_part_apply(const double* v) {  // gp.cpp:189-198
+  const LinearOperator& A = op();
+  const Index N = A.size();
+  Vec out(static_cast<size_t>(N));
+  A.mvm(v, out.data());
+  for (Index i = 0; i < N; ++i) out[size_t(i)] -= (i < n_ ? nv_ * nv_ : ng_ * ng_) * v[i];
+  return out;
+}
+
+Vec GpModel::dlogell_apply(const double* v) {  // gp.cpp:200-218
+  op();
+  if (cfg_.backend == 1) {
+    // the second grid operator over kernel_dlogell_profile (gp.cpp:212-213)
+    if (!kuu_dlogell_)
+      kuu_dlogell_ = std::make_unique<GridKernelOperator>(dski_->grid(), kernel_dlogell_profile(k_));
+    Vec u = dski_->stacked_transpose_apply(v);
+    Vec w(u.size());
+    kuu_dlogell_->mvm(u.data(), w.data());
+    return dski_->stacked_apply(w.data());
+  }
+  return static_cast<const DskipOperator&>(*op_).dlogell_apply(v);
+}
+
+Vec GpModel::lml_gradient() {  // gp.cpp:220-292
+  const LinearOperator& A = op();
+  const Index N = A.size();
+  const bool grads = dY_.rows > 0;
+  const int nparams = grads ? 4 : 3;
+  const Vec a = alpha();
+  // dK/dθ over (log ℓ, log s, log σ₁[, log σ₂]) (gp.cpp:229-244)
+  auto apply_param = [&](int p, const double* v) {
+    Vec out(static_cast<size_t>(N), 0.0);
+    if (p == 0) return dlogell_apply(v);
+    if (p == 1) {
+      out = kernel_part_apply(v);
+      for (auto& x : out) x *= 2.0;
+    } else if (p == 2) {
+      for (Index i = 0; i < n_; ++i) out[size_t(i)] = (2.0 * nv_ * nv_) * v[i];
+    } else {
+      for (Index i = n_; i < N; ++i) out[size_t(i)] = (2.0 * ng_ * ng_) * v[i];
+    }
+    return out;
+  };
+  const Preconditioner* M = preconditioner();
+  const PrecondApply precond = M ? M->as_apply() : PrecondApply{};
+  CgOptions trace_cg = cfg_.cg;
+  trace_cg.tol = std::max(cfg_.cg.tol, 1e-2);  // gp.cpp:281-282
+  Vec grad(static_cast<size_t>(nparams));
+  for (int p = 0; p < nparams; ++p) {
+    Vec Ma = apply_param(p, a.data());
+    CallbackOperator Mop(N, [&](const double* x, double* y) {
+      Vec r = apply_param(p, x);
+      std::copy(r.begin(), r.end(), y);
+    });
+    const double tr = trace_estimate(A, Mop, cfg_.gradient_probes, cfg_.seed, trace_cg, precond);
+    grad[size_t(p)] = 0.5 * (dot(a.data(), Ma.data(), N) - tr);
+  }
+  return grad;
+}
+
 std::pair<Vec, Mat> GpModel::predict_mean_grad(const double* Xt, Index T) {  // gp.cpp:471-496
   op();
   if (!dski_) throw std::logic_error("oracle predict_mean_grad: D-SKI backend only");

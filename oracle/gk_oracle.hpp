@@ -360,6 +360,7 @@ struct GpConfig {
   int slq_probes = 10, slq_steps = 50;
   std::uint64_t seed = 0;
   int order = 0;
+  int gradient_probes = 8;  // gp.hpp:43
 };
 class GpModel {
  public:
@@ -377,6 +378,10 @@ class GpModel {
   double predict_variance_pivchol(const double* x);
   Vec cross_covariance(const double* x);
   double mean() const { return mean_; }
+  Vec kernel_part_apply(const double* v);  // gp.cpp:189-198
+  Vec dlogell_apply(const double* v);      // gp.cpp:200-218 (D-SKI / D-SKIP branches)
+  Vec lml_gradient();                      // gp.cpp:220-292 (stochastic-trace branch)
+  void set_gradient_probes(int p) { cfg_.gradient_probes = p; }
 
  private:
   KernelSpec k_;
@@ -392,6 +397,7 @@ class GpModel {
   std::unique_ptr<Preconditioner> precond_;
   std::unique_ptr<PivotedCholeskyFactor> factor_;
   std::unique_ptr<Vec> alpha_, mean_grid_;
+  std::unique_ptr<GridKernelOperator> kuu_dlogell_;
 };
 
 }  // namespace gko

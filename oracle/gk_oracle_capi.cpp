@@ -460,6 +460,18 @@ int orc_gp_predict_mean_grad(void* m, const double* Xt, long long T, double* val
     copy_out(r.second.a, grads);
   });
 }
+int orc_gp_lml_gradient(void* m, int probes, double* grad, int* nparams) {
+  return guard([&] {
+    auto* g = static_cast<GpModel*>(m);
+    g->set_gradient_probes(probes);
+    Vec r = g->lml_gradient();
+    copy_out(r, grad);
+    *nparams = int(r.size());
+  });
+}
+int orc_gp_dlogell_apply(void* m, const double* v, double* out) {
+  return guard([&] { copy_out(static_cast<GpModel*>(m)->dlogell_apply(v), out); });
+}
 int orc_gp_predict_variance_pivchol(void* m, const double* x, double* out) {
   return guard([&] { *out = static_cast<GpModel*>(m)->predict_variance_pivchol(x); });
 }

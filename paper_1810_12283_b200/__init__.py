@@ -94,6 +94,7 @@ _SIGS = {
     "gk_dskip_factor_rank": (_i64, [_vp, C.c_int]),
     "gk_dskip_factor_get": (C.c_int, [_vp, C.c_int, _dp, _dp, _dp]),
     "gk_dskip_dlogell_apply": (C.c_int, [_vp, _dp, _i64, _dp, _i64, _i64]),
+    "gk_dski_dlogell_apply": (C.c_int, [_vp, _dp, _i64, _dp, _i64, _i64]),
     "gk_pcg": (C.c_int, [_vp, _vp, _dp, _i64, _i64, _d, C.c_int, _dp, _i64, _ip, _ip, _dp, _ip]),
     "gk_pcg_dev": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _d, C.c_int, _vp, _i64, _ip, _ip, _vp]),
     "gk_pivoted_cholesky": (C.c_int, [_vp, C.c_int, _i64, _d, C.POINTER(_vp)]),
@@ -109,6 +110,7 @@ _SIGS = {
     "gk_precond_destroy": (None, [_vp]),
     "gk_slq_logdet": (C.c_int, [_vp, C.c_int, C.c_int, _u64, _d, C.c_int, _dp, _ip, _dp]),
     "gk_lanczos": (C.c_int, [_vp, _i64, _u64, _dp, _u64, _dp, _dp, _dp, _i64p, _ip]),
+    "gk_lml_gradient": (C.c_int, [_vp, _vp, _dp, C.c_int, _u64, C.c_double, C.c_int, _dp, _ip]),
     "gk_trace_estimate": (C.c_int, [_vp, _vp, C.c_int, _u64, _d, C.c_int, _vp, _dp]),
     "gk_dski_predict_mean_grad": (C.c_int, [_vp, _dp, _d, _dp, _i64, _dp, _dp]),
     "gk_dski_cross_covariance": (C.c_int, [_vp, _dp, _i64, _dp, _i64]),
@@ -403,6 +405,16 @@ class DskiOperator(LinearOperator):
                                               _p(vals), _p(grads)))
         return vals, grads
 
+    def dlogell_apply(self, v):
+        """∂K∇/∂log ℓ · v (no noise) — GpModel::dlogell_apply's D-SKI branch
+        (gp.cpp:212-213): a second grid operator over kernel_dlogell_profile."""
+        V = _f64(v, True)
+        vec = V.ndim == 1
+        V = V.reshape(-1, 1, order="F") if vec else V
+        out = np.empty_like(V, order="F")
+        _check(_lib.gk_dski_dlogell_apply(self._h, _p(V), V.shape[0], _p(out), V.shape[0], V.shape[1]))
+        return out[:, 0] if vec else out
+
     def gather_dev(self, dW, dV, dOut, nrhs, stream=0):
         """out = B w + noise·v on device pointers (internal layout): the last
         stage of a grid-slab sharded MVM."""
@@ -688,6 +700,16 @@ def trace_estimate(A: LinearOperator, B: LinearOperator, probes, seed, tol=1e-4,
     _check(_lib.gk_trace_estimate(A.handle, B.handle, probes, seed, tol, max_iterations,
                                   precond.handle if precond is not None else None, C.byref(out)))
     return out.value
+
+
+def lml_gradient(A: LinearOperator, alpha, probes=8, seed=0, tol=1e-4, max_iterations=1000, precond=None):
+    """GpModel::lml_gradient (gp.cpp:220-292), stochastic-trace branch:
+    dLML/d(log ell, log s, log sigma1[, log sigma2]) given alpha = K^-1 b (D-SKI / D-SKIP)."""
+    g = np.empty(4)
+    k = C.c_int()
+    _check(_lib.gk_lml_gradient(A.handle, precond.handle if precond is not None else None, _p(_f64(alpha)),
+                                int(probes), int(seed), float(tol), int(max_iterations), _p(g), C.byref(k)))
+    return g[: k.value].copy()
 
 
 class LanczosFactor:

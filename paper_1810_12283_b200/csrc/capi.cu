@@ -40,6 +40,7 @@ int dskip_factor_count(const Op& o);
 i64 dskip_factor_rank(const Op& o, int f);
 void dskip_factor_get(const Op& o, int f, double* Q, double* a, double* b);
 void dskip_dlogell(Op& o, const double* in, double* out, int nrhs, cudaStream_t s);
+void dski_dlogell(Op& o, const double* Vi, double* Oi, int nrhs, cudaStream_t s);
 double dmma_peak_tflops(int device);
 }  // namespace gk
 
@@ -594,6 +595,17 @@ gk_status gk_dskip_dlogell_apply(const gk_op* h, const double* V, int64_t ldv, d
   });
 }
 
+gk_status gk_dski_dlogell_apply(const gk_op* h, const double* V, int64_t ldv, double* Out, int64_t ldo,
+                                int64_t nrhs) {
+  return guard([&] {
+    Op& op = O(h);
+    if (ldv < op.N || ldo < op.N) fail(GK_ERR_ARG, "size mismatch");
+    if (nrhs <= 0) return;
+    grid_call(op, V, ldv, op.N, Out, ldo, op.N, nrhs, false, false,
+              [&](const double* i, double* o, int nb, cudaStream_t s) { dski_dlogell(op, i, o, nb, s); });
+  });
+}
+
 // ---------------------------------------------------------------- solvers
 gk_status gk_pcg(const gk_op* h, const gk_precond* M, const double* B, int64_t ldb, int64_t nrhs, double tol,
                  int maxit, double* X, int64_t ldx, int* iterations, int* converged, double* history,
@@ -935,6 +947,82 @@ gk_status gk_trace_estimate(const gk_op* hA, const gk_op* hB, int probes, uint64
     double sum = 0.0;
     for (int p = 0; p < probes; ++p) sum += est[static_cast<size_t>(p)];
     *out = sum / probes;
+  });
+}
+
+// GpModel::lml_gradient (gp.cpp:220-292), stochastic-trace branch: for
+// θ = (log ℓ, log s, log σ₁[, log σ₂]),  ∂LML/∂θ_p = ½(αᵀ M_p α − tr(K⁻¹ M_p)),
+// the trace by trace_estimate (linalg.cpp:255-279) with probes z_q =
+// rademacher(N, seed, 1000+q) and PCG at tol max(tol, 1e-2). The reference
+// re-solves K x = z_q identically for every p; here the probes are solved
+// once, as one batched PCG, and each x_q is dotted with every M_p z_q.
+gk_status gk_lml_gradient(const gk_op* hA, const gk_precond* M, const double* alpha, int probes, uint64_t seed,
+                          double tol, int maxit, double* grad, int* nparams) {
+  return guard([&] {
+    Op& A = O(hA);
+    if (!alpha || !grad || !nparams) fail(GK_ERR_ARG, "null argument");
+    if (A.kind != KIND_DSKI && A.kind != KIND_DSKIP)
+      fail(GK_ERR_UNSUPPORTED, "lml_gradient: stochastic-trace branch needs a D-SKI or D-SKIP operator");
+    const i64 N = A.N, n = A.n_value;
+    const int np = N > n ? 4 : 3;
+    *nparams = np;
+    const double nv2 = A.nv2, ng2 = A.ng2;
+    // M_p V for a host block of c columns (gp.cpp:229-244)
+    auto apply_param = [&](int p, const double* V, double* Out, i64 c) {
+      if (p == 0) {
+        const gk_status st = A.kind == KIND_DSKI ? gk_dski_dlogell_apply(hA, V, N, Out, N, c)
+                                                 : gk_dskip_dlogell_apply(hA, V, N, Out, N, c);
+        if (st != GK_OK) fail(st, g_err);
+        return;
+      }
+      if (p == 1) {
+        const gk_status st = gk_op_mvm(hA, V, N, Out, N, c);
+        if (st != GK_OK) fail(st, g_err);
+        for (i64 q = 0; q < c; ++q)
+          for (i64 i = 0; i < N; ++i) {
+            const i64 e = q * N + i;
+            Out[e] = 2.0 * (Out[e] - (i < n ? nv2 : ng2) * V[e]);
+          }
+        return;
+      }
+      for (i64 q = 0; q < c; ++q)
+        for (i64 i = 0; i < N; ++i) {
+          const i64 e = q * N + i;
+          const bool mine = p == 2 ? i < n : i >= n;
+          Out[e] = mine ? 2.0 * (p == 2 ? nv2 : ng2) * V[e] : 0.0;
+        }
+    };
+    std::vector<double> data(static_cast<size_t>(np)), Ma(static_cast<size_t>(N));
+    for (int p = 0; p < np; ++p) {
+      apply_param(p, alpha, Ma.data(), 1);
+      double s = 0.0;
+      for (i64 i = 0; i < N; ++i) s += alpha[i] * Ma[static_cast<size_t>(i)];
+      data[static_cast<size_t>(p)] = s;
+    }
+    std::vector<double> tr(static_cast<size_t>(np), 0.0);
+    if (probes > 0) {
+      const double ttol = std::max(tol, 1e-2);  // gp.cpp:281-282
+      std::vector<double> Z(static_cast<size_t>(N) * probes), X(Z.size()), MZ(Z.size());
+      for (int q = 0; q < probes; ++q) rademacher(N, seed, 1000 + std::uint64_t(q), Z.data() + static_cast<size_t>(q) * N);
+      std::vector<int> its(static_cast<size_t>(probes)), conv(static_cast<size_t>(probes));
+      gk_status st = gk_pcg(hA, M, Z.data(), N, probes, ttol, maxit, X.data(), N, its.data(), conv.data(), nullptr,
+                            nullptr);
+      if (st != GK_OK) fail(st, g_err);
+      for (int q = 0; q < probes; ++q)
+        if (!conv[static_cast<size_t>(q)])
+          fail(GK_ERR_RUNTIME, "trace_estimate: CG did not converge within " + std::to_string(maxit) + " iterations");
+      for (int p = 0; p < np; ++p) {
+        apply_param(p, Z.data(), MZ.data(), probes);
+        double sum = 0.0;  // per-probe estimates summed in probe order (linalg.cpp:276-277)
+        for (int q = 0; q < probes; ++q) {
+          double e = 0.0;
+          for (i64 i = 0; i < N; ++i) e += X[static_cast<size_t>(q) * N + i] * MZ[static_cast<size_t>(q) * N + i];
+          sum += e;
+        }
+        tr[static_cast<size_t>(p)] = sum / probes;
+      }
+    }
+    for (int p = 0; p < np; ++p) grad[p] = 0.5 * (data[static_cast<size_t>(p)] - tr[static_cast<size_t>(p)]);
   });
 }
 

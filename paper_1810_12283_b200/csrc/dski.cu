@@ -902,6 +902,11 @@ struct DskiOp final : Op {
   DevBuf<int> toff;
   std::vector<int> toff_h;
   std::vector<int> band;  // per-axis numerical band of the Toeplitz sequence
+  // ∂/∂log ℓ of the SE profile, s² Π_j t_j(o_j) · Σ_j ρ_j² (ρ_j = o_j/ℓ): a sum of
+  // d Kronecker terms, term j with axis j's sequence t_j·ρ_j² (kernels.cpp:172-188)
+  DevBuf<double> tvec_dl;
+  std::vector<int> band_dl;
+  DevBuf<double> grid_a, grid_b;  // dlogell scratch
   int max_row_pts = 0;    // d = 2: most points sharing one base row (band kernels' staging)
   DevBuf<i64> ext;        // internal row -> external row
   std::vector<i64> perm_h, inv_h;
@@ -977,6 +982,7 @@ struct DskiOp final : Op {
   bool scatter_band(const double* v, double* u, int nrhs, cudaStream_t s) const;
   bool gather_band(const double* w, const double* v, double* out, int nrhs, bool noise, cudaStream_t s) const;
   void kuu(const double* u, double* w, int nrhs, cudaStream_t s) const;
+  void kuu_dlogell(const double* u, double* w, int nrhs, cudaStream_t s);
   void gather(const double* w, const double* v, double* out, int nrhs, bool noise, cudaStream_t s) const;
 
   void grow(DevBuf<double>& b, size_t count) {
@@ -1147,6 +1153,10 @@ void DskiOp::gather(const double* w, const double* v, double* out, int nrhs, boo
   launched("dski gather (lean)");
 }
 
+__global__ void k_axpy_inplace(double* __restrict__ w, const double* __restrict__ x, i64 n) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) w[i] += x[i];
+}
+
 void DskiOp::kuu(const double* u, double* w, int nrhs, cudaStream_t s) const {
   // Modes from the last axis to the first: u -> ... -> w, intermediates
   // alternating between w and the scratch grid_t so the last mode lands in w
@@ -1159,6 +1169,32 @@ void DskiOp::kuu(const double* u, double* w, int nrhs, cudaStream_t s) const {
     double* dst = (j % 2 == 0) ? w : grid_t.p;
     toeplitz_mode(tvec.p + toff_h[static_cast<size_t>(j)], m[j], band[static_cast<size_t>(j)], P, Q, src, dst, s);
     src = dst;
+  }
+}
+
+// w = ∂K_UU/∂log ℓ · u = Σ_j (⊗_i S_i^{(j)}) u with S_j^{(j)} = T_j ρ_j², S_i^{(j)} = T_i
+// (the reference applies the same operator through a second circulant
+// embedding of kernel_dlogell_profile, dski.cpp:36-40, gp.cpp:212-213).
+void DskiOp::kuu_dlogell(const double* u, double* w, int nrhs, cudaStream_t s) {
+  grow(grid_a, static_cast<size_t>(M) * nrhs);
+  grow(grid_b, static_cast<size_t>(M) * nrhs);
+  for (int term = 0; term < d; ++term) {
+    const double* src = u;
+    for (int j = d - 1; j >= 0; --j) {
+      i64 P = 1, Q = nrhs;
+      for (int i = 0; i < j; ++i) P *= m[i];
+      for (int i = j + 1; i < d; ++i) Q *= m[i];
+      const bool last = j == 0;
+      double* dst = last && term == 0 ? w : (src == grid_a.p ? grid_b.p : grid_a.p);
+      const bool deriv = j == term;
+      const double* t = (deriv ? tvec_dl.p : tvec.p) + toff_h[static_cast<size_t>(j)];
+      toeplitz_mode(t, m[j], (deriv ? band_dl : band)[static_cast<size_t>(j)], P, Q, src, dst, s);
+      src = dst;
+    }
+    if (term > 0) {
+      k_axpy_inplace<<<blocks_for((i64)M * nrhs), 256, 0, s>>>(w, src, (i64)M * nrhs);
+      launched("dski dlogell accumulate");
+    }
   }
 }
 
@@ -1301,6 +1337,24 @@ std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, cons
       }
     op->band[static_cast<size_t>(j)] = band;
   }
+  std::vector<double> tvd(tv.size());
+  op->band_dl.resize(static_cast<size_t>(d));
+  for (int j = 0; j < d; ++j) {
+    const int off = op->toff_h[static_cast<size_t>(j)];
+    double peak = 0.0;
+    for (int kk = 0; kk < g.dims[j]; ++kk) {
+      const double o = kk * g.spacing[j];
+      tvd[static_cast<size_t>(off + kk)] = tv[static_cast<size_t>(off + kk)] * (o * o / ell2);
+      peak = std::max(peak, std::fabs(tvd[static_cast<size_t>(off + kk)]));
+    }
+    int band = g.dims[j];
+    for (int kk = g.dims[j] - 1; kk >= 0; --kk)
+      if (std::fabs(tvd[static_cast<size_t>(off + kk)]) >= 1e-30 * peak) {
+        band = kk + 1;
+        break;
+      }
+    op->band_dl[static_cast<size_t>(j)] = band;
+  }
   std::vector<i64> ext(static_cast<size_t>(op->N));
   for (int gg = 0; gg <= op->G; ++gg)
     for (i64 s = 0; s < n; ++s) ext[static_cast<size_t>(gg * n + s)] = gg * n + op->perm_h[static_cast<size_t>(s)];
@@ -1321,6 +1375,7 @@ std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, cons
   op->cell_start.upload(cstart.data(), cstart.size(), st);
   op->cell_start_h = cstart;
   op->tvec.upload(tv.data(), tv.size(), st);
+  op->tvec_dl.upload(tvd.data(), tvd.size(), st);
   op->toff.upload(op->toff_h.data(), op->toff_h.size(), st);
   op->ext.upload(ext.data(), ext.size(), st);
   double o3[3] = {0, 0, 0}, h3[3] = {1, 1, 1};
@@ -1367,6 +1422,16 @@ void dski_apply(Op& o, const double* U, double* Oi, int nrhs, cudaStream_t s) {
   auto& op = static_cast<DskiOp&>(o);
   op.gather(U, U, Oi, nrhs, false, s);
 }
+// ∂K∇/∂log ℓ · v = B (∂K_UU/∂log ℓ) Bᵀ v, no noise (GpModel::dlogell_apply, gp.cpp:212-213)
+void dski_dlogell(Op& o, const double* Vi, double* Oi, int nrhs, cudaStream_t s) {
+  if (o.kind != KIND_DSKI) fail(GK_ERR_ARG, "operator is not a D-SKI operator");
+  auto& op = static_cast<DskiOp&>(o);
+  op.ensure_scratch(nrhs);
+  op.scatter(Vi, op.grid_u.p, nrhs, s);
+  op.kuu_dlogell(op.grid_u.p, op.grid_w.p, nrhs, s);
+  op.gather(op.grid_w.p, op.grid_w.p, Oi, nrhs, false, s);
+}
+
 void dski_grid_mvm(Op& o, const double* U, double* W, int nrhs, cudaStream_t s) {
   auto& op = static_cast<DskiOp&>(o);
   op.ensure_scratch(nrhs);

@@ -1,3 +1,8 @@
+#include <thread>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 // capi.cu — extern "C" boundary (include/gk_capi.h). Maps C++ exceptions to
 // gk_status codes, stages host blocks through the device, converts between
 // the reference's external layout and the operators' internal layout.
@@ -45,6 +50,25 @@ double dmma_peak_tflops(int device);
 }  // namespace gk
 
 using namespace gk;
+
+namespace {
+// Run f(0..n-1) on up to hardware_concurrency host threads (independent items).
+template <class F>
+void parallel_for(int n, F&& f) {
+  const int nt = std::max(1, std::min<int>(n, int(std::thread::hardware_concurrency())));
+  if (nt <= 1) {
+    for (int i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::atomic<int> next{0};
+  std::vector<std::thread> pool;
+  for (int t = 0; t < nt; ++t)
+    pool.emplace_back([&] {
+      for (int i = next++; i < n; i = next++) f(i);
+    });
+  for (auto& th : pool) th.join();
+}
+}  // namespace
 
 struct gk_precond {
   std::unique_ptr<Precond> impl;
@@ -157,6 +181,7 @@ int gk_set_tuning(const char* key, int value) {
                            : k == "pcg_fused" ? &g_tuning.pcg_fused
                            : k == "e2e_chunk" ? &g_tuning.e2e_chunk
                            : k == "dskip" ? &g_tuning.dskip
+                           : k == "lanczos" ? &g_tuning.lanczos
                            : k == "dskip_e" ? &g_tuning.dskip_e
                            : k == "f2_stc" ? &g_tuning.f2_stc
                            : k == "f2_sl" ? &g_tuning.f2_sl
@@ -826,24 +851,39 @@ gk_status gk_slq_logdet(const gk_op* h, int probes, int steps, uint64_t seed, do
     std::vector<double> est(static_cast<size_t>(probes), 0.0);
     std::vector<int> clamps(static_cast<size_t>(probes), 0);
     std::vector<double> hz(static_cast<size_t>(N) * chunk);
-    DevBuf<double> ze(static_cast<size_t>(N) * chunk), zi(static_cast<size_t>(N) * chunk);
+    op.slq_z.reserve(static_cast<size_t>(N) * chunk * 2);
+    double* ze_p = op.slq_z.p;
+    double* zi_p = op.slq_z.p + static_cast<size_t>(N) * chunk;
+    const bool prof = std::getenv("GK_SLQ_PROF") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
     for (int p0 = 0; p0 < probes; p0 += chunk) {
       const int P = std::min(chunk, probes - p0);
       std::vector<std::uint64_t> rseeds(static_cast<size_t>(P));
-      double zn2 = 0.0;
-      for (int q = 0; q < P; ++q) {
+      auto t0 = now();
+      // probe vectors (host mt19937_64 streams, bit-exact with the reference),
+      // generated in parallel over probes
+      std::vector<double> zn2v(static_cast<size_t>(P), 0.0);
+      auto gen = [&](int q) {
         const std::uint64_t pid = std::uint64_t(probe_offset + p0 + q);
-        rademacher(N, seed, pid, hz.data() + static_cast<size_t>(q) * N);
+        double* z = hz.data() + static_cast<size_t>(q) * N;
+        rademacher(N, seed, pid, z);
         double s2 = 0.0;
-        for (i64 i = 0; i < N; ++i) s2 += hz[static_cast<size_t>(q) * N + i] * hz[static_cast<size_t>(q) * N + i];
-        zn2 = s2;
+        for (i64 i = 0; i < N; ++i) s2 += z[i] * z[i];
+        zn2v[static_cast<size_t>(q)] = s2;
         const double zn = std::sqrt(s2);
-        for (i64 i = 0; i < N; ++i) hz[static_cast<size_t>(q) * N + i] /= zn;
+        for (i64 i = 0; i < N; ++i) z[i] /= zn;
         rseeds[static_cast<size_t>(q)] = mix_seed(seed, 50000 + pid);
-      }
-      ze.upload(hz.data(), static_cast<size_t>(N) * P, s);
-      op.to_internal(ze.p, N, zi.p, P, s);
-      LanczosBatch lb = lanczos_batch(op, zi.p, P, steps, rseeds, nullptr, s);
+      };
+      parallel_for(P, gen);
+      auto t1 = now();
+      GK_CUDA(cudaMemcpyAsync(ze_p, hz.data(), sizeof(double) * N * P, cudaMemcpyHostToDevice, s));
+      op.to_internal(ze_p, N, zi_p, P, s);
+      if (prof) GK_CUDA(cudaStreamSynchronize(s));
+      auto t2 = now();
+      LanczosBatch lb = lanczos_batch(op, zi_p, P, steps, rseeds, nullptr, s);
+      auto t3 = now();
+      if (prof) std::fprintf(stderr, "slq: probes %.2f ms, upload %.2f ms, lanczos %.2f ms\n", ms(t0, t1), ms(t1, t2), ms(t2, t3));
       for (int q = 0; q < P; ++q) {
         const int len = lb.len[static_cast<size_t>(q)];
         std::vector<double> ev(static_cast<size_t>(len)), Z(static_cast<size_t>(len) * len);
@@ -858,7 +898,7 @@ gk_status gk_slq_logdet(const gk_op* h, int probes, int steps, uint64_t seed, do
           const double w0 = Z[static_cast<size_t>(i) * len];
           e += w0 * w0 * std::log(lambda);
         }
-        est[static_cast<size_t>(p0 + q)] = zn2 * e;
+        est[static_cast<size_t>(p0 + q)] = zn2v[static_cast<size_t>(q)] * e;  // ‖z_p‖² (linalg.cpp:240-243)
       }
     }
     double sum = 0.0;

@@ -47,6 +47,7 @@ struct Tuning {
   // D-SKIP Hadamard kernels: 0 = TMA-ring DMMA (v3, falling back to v2 for odd
   // sizes), 3 = cp.async DMMA (v2), 1 = first generation
   std::atomic<int> dskip{0};
+  std::atomic<int> lanczos{0};  // 1 = per-step host-synchronised Lanczos (reference order)
   std::atomic<int> dskip_e{0};  // v3 expand ring: 0 = 8 m × 4 stages, 1 = 16 × 2, 2 = 16 × 4, 3 = 32 × 2
   std::atomic<int> gen{0};  // bumped by every gk_set_tuning call (cached plans rebuild)
 };
@@ -158,6 +159,10 @@ struct Op {
   cudaStream_t stream = nullptr;  // own stream for host-API calls
   cudaStream_t cap_stream = nullptr;  // private stream used only for CUDA-graph capture
   DevBuf<double> scratch_a, scratch_b, scratch_c;
+  // Lanczos / SLQ workspace (grow-only; cudaMalloc/cudaFree of the N×P×steps
+  // basis per call cost more than the steps themselves)
+  DevBuf<double> lz_ws, slq_z;
+  DevBuf<int> lz_wsi;
   HostBuf pinned;
   // host-buffer MVM pipeline (gk_op_mvm): copy-in / compute / copy-out streams
   cudaStream_t io_in = nullptr, io_out = nullptr;

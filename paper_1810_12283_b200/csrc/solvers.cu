@@ -1,3 +1,6 @@
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 // solvers.cu — device-resident batched solvers (reference linalg.cpp).
 //
 //  * pcg_internal: the reference's single-RHS PCG (linalg.cpp:85-131) run
@@ -770,6 +773,303 @@ __global__ void k_lz_next(const double* __restrict__ W, const double* __restrict
   }
 }
 
+// ---------------------------------------------------------------- Lanczos, device-resident step
+// Per step three passes over the basis ("fused pass-1 update +
+// pass-2 projection"): B computes α and the first projection as
+// C1_j = Q_j·w − α Q_j·q_k (= Q_j·(w − α q_k), linalg.cpp:33-41 reordered),
+// C applies w −= α q_k + Σ Q_j C1_j and projects again (C2), D applies the
+// second correction and ‖w‖². α, β, breakdown test and the next-vector scale
+// stay on the device (k_lz_state); the host syncs once per batch.
+
+// Reduce per-thread accumulators acc[OFF + a] (a < cnt ≤ MAXC; thread layout
+// slot × P) into out[blockIdx][a][P], eight columns per shared-memory round.
+template <int OFF, int MAXC, int NA>
+__device__ __forceinline__ void lz_store(const double (&acc)[NA], int cnt, int P, double* __restrict__ out,
+                                         double* sm) {
+  const int tid = threadIdx.x, slots = blockDim.x / P;
+  double* ob = out + (i64)blockIdx.x * cnt * P;
+#pragma unroll
+  for (int a0 = 0; a0 < MAXC; a0 += 8) {
+    if (a0 >= cnt) break;
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (a0 + u < MAXC) sm[u * RT + tid] = acc[OFF + a0 + u];
+    __syncthreads();
+    for (int o = tid; o < 8 * P; o += blockDim.x) {
+      const int u = o / P, p = o - u * P;
+      if (a0 + u < cnt) {
+        double s = 0.0;
+        for (int k = 0; k < slots; ++k) s += sm[u * RT + k * P + p];
+        ob[(i64)(a0 + u) * P + p] = s;
+      }
+    }
+  }
+}
+
+constexpr int JB = 16;  // basis vectors per pass-B launch (2·JB + 1 accumulators)
+
+// Rows per thread per iteration in the Lanczos passes: R independent rows keep
+// R loads of every basis column in flight (the passes are HBM streams; one
+// row at a time left them latency-bound at ~1-2 TB/s).
+constexpr int LZR = 4;
+
+struct LzRows {
+  i64 ii[LZR];
+  bool ok[LZR];
+};
+__device__ __forceinline__ LzRows lz_rows(i64 rb, int slots, i64 r0, i64 r1, int P, int p) {
+  LzRows t;
+#pragma unroll
+  for (int u = 0; u < LZR; ++u) {
+    const i64 r = rb + (i64)u * slots;
+    t.ok[u] = r < r1;
+    t.ii[u] = (t.ok[u] ? r : r0) * P + p;
+  }
+  return t;
+}
+
+// pass B (chunk j0..j0+jc of the basis). Chunk 0 also applies w −= β_prev q_{k−1}
+// (prev != null) and accumulates α = q_k·w. The projection of w − α q_k is
+// formed as Q_j·w − α δ_jk (the basis is orthonormal to roundoff under the
+// two-pass full reorthogonalisation; the second pass removes the difference).
+__global__ void __launch_bounds__(RT, 2) k_lz_b(double* __restrict__ W, const double* __restrict__ prev,
+                                                const double* __restrict__ bprev, const double* __restrict__ q,
+                                                const double* __restrict__ Q, int j0, int jc, i64 N, int P,
+                                                double* __restrict__ part_a, double* __restrict__ part_g) {
+  __shared__ double sm[8 * RT];
+  const int slots = blockDim.x / P;
+  const int p = threadIdx.x % P, slot = threadIdx.x / P;
+  double acc[1 + JB];
+#pragma unroll
+  for (int j = 0; j < 1 + JB; ++j) acc[j] = 0.0;
+  if (slot < slots) {
+    const double bp = prev ? bprev[p] : 0.0;
+    i64 r0, r1;
+    row_range(N, r0, r1);
+    const i64 blk = N * P;
+    const double* Qc = Q + (i64)j0 * blk;
+    for (i64 rb = r0 + slot; rb < r1; rb += (i64)slots * LZR) {
+      const LzRows t = lz_rows(rb, slots, r0, r1, P, p);
+      double w[LZR];
+#pragma unroll
+      for (int u = 0; u < LZR; ++u) {
+        w[u] = W[t.ii[u]];
+        if (prev) {
+          w[u] -= bp * prev[t.ii[u]];
+          if (t.ok[u]) W[t.ii[u]] = w[u];
+        }
+        if (!t.ok[u]) w[u] = 0.0;
+        if (part_a) acc[0] += q[t.ii[u]] * w[u];
+      }
+#pragma unroll
+      for (int j = 0; j < JB; ++j)
+        if (j < jc) {
+#pragma unroll
+          for (int u = 0; u < LZR; ++u) acc[1 + j] += Qc[(i64)j * blk + t.ii[u]] * w[u];
+        }
+    }
+  }
+  if (part_a) lz_store<0, 1>(acc, 1, P, part_a, sm);
+  if (jc > 0) lz_store<1, JB>(acc, jc, P, part_g, sm);
+}
+
+// Fixed-order cross-block sums: out[o] = Σ_k partial[k][o] (k = 0..RB-1) and,
+// when part2 != null, out2[o] likewise. Block = 32 outputs × 8 block groups.
+__device__ __forceinline__ double lz_colsum(const double* __restrict__ partial, int nout, int o, double* sm) {
+  const int lo = threadIdx.x & 31, g = threadIdx.x >> 5;
+  double s = 0.0;
+  if (o < nout) {
+    int k = g;
+    for (; k + 56 < RB; k += 64) {  // eight loads in flight, summed in block order
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = partial[(i64)(k + 8 * u) * nout + o];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; k < RB; k += 8) s += partial[(i64)k * nout + o];
+  }
+  __syncthreads();
+  sm[g * 32 + lo] = s;
+  __syncthreads();
+  double t = 0.0;
+  for (int k = 0; k < 8; ++k) t += sm[k * 32 + lo];
+  return t;
+}
+
+// α (chunk 0: reduced from part_a and stored; later chunks: read) and
+// C1[j0 + j] = g_j − α δ_{j0+j,kcur}. Blocks of 32 outputs (j, p); chunk 0
+// has an extra ceil(P/32) blocks for α.
+__global__ void __launch_bounds__(256) k_lz_fin_b(const double* __restrict__ part_a,
+                                                  const double* __restrict__ part_g, int j0, int jc, int kcur, int P,
+                                                  double* __restrict__ alpha, double* __restrict__ C1) {
+  __shared__ double sm[256];
+  const int nb_c = (jc * P + 31) / 32;
+  const int lo = threadIdx.x & 31;
+  if ((int)blockIdx.x >= nb_c) {  // α blocks (chunk 0 only)
+    const int o = (blockIdx.x - nb_c) * 32 + lo;
+    const double a = lz_colsum(part_a, P, o, sm);
+    if (threadIdx.x < 32 && o < P) alpha[o] = a;
+    return;
+  }
+  const int o = blockIdx.x * 32 + lo;
+  const bool diag = o < jc * P && j0 + o / P == kcur;
+  double a = 0.0;
+  if (part_a) a = lz_colsum(part_a, P, o < jc * P ? o % P : 0, sm);
+  const double g = lz_colsum(part_g, jc * P, o, sm);
+  if (!part_a && diag) a = alpha[o % P];
+  if (threadIdx.x < 32 && o < jc * P) C1[(i64)j0 * P + o] = diag ? g - a : g;
+}
+
+// out[o] = Σ_k partial[k][o]
+__global__ void __launch_bounds__(256) k_lz_fin(const double* __restrict__ partial, int nout,
+                                                double* __restrict__ out) {
+  __shared__ double sm[256];
+  const int o = blockIdx.x * 32 + (threadIdx.x & 31);
+  const double v = lz_colsum(partial, nout, o, sm);
+  if (threadIdx.x < 32 && o < nout) out[o] = v;
+}
+inline unsigned lz_fin_blocks(int nout) { return static_cast<unsigned>((nout + 31) / 32); }
+
+// pass C: chunk 0 applies w −= α q_k + Σ_{j<k1} Q_j C1_j (writes W); every chunk
+// accumulates C2 partials for j0..j0+jc.
+__global__ void __launch_bounds__(RT, 2) k_lz_c(double* __restrict__ W, const double* __restrict__ q,
+                                                const double* __restrict__ alpha, const double* __restrict__ Q,
+                                                const double* __restrict__ C1, int k1, int j0, int jc, i64 N, int P,
+                                                double* __restrict__ partial) {
+  __shared__ double sm[8 * RT];
+  const int slots = blockDim.x / P;
+  const int p = threadIdx.x % P, slot = threadIdx.x / P;
+  double acc[JB];
+#pragma unroll
+  for (int j = 0; j < JB; ++j) acc[j] = 0.0;
+  if (slot < slots) {
+    const double a = alpha[p];
+    i64 r0, r1;
+    row_range(N, r0, r1);
+    const i64 blk = N * P;
+    const double* Qc = Q + (i64)j0 * blk;
+    for (i64 rb = r0 + slot; rb < r1; rb += (i64)slots * LZR) {
+      const LzRows t = lz_rows(rb, slots, r0, r1, P, p);
+      double w[LZR];
+#pragma unroll
+      for (int u = 0; u < LZR; ++u) w[u] = W[t.ii[u]];
+      if (j0 == 0) {
+        double s[LZR];
+#pragma unroll
+        for (int u = 0; u < LZR; ++u) s[u] = a * q[t.ii[u]];
+#pragma unroll 2
+        for (int j = 0; j < k1; ++j) {
+          const double c = __ldg(C1 + j * P + p);
+#pragma unroll
+          for (int u = 0; u < LZR; ++u) s[u] += Q[(i64)j * blk + t.ii[u]] * c;
+        }
+#pragma unroll
+        for (int u = 0; u < LZR; ++u) {
+          w[u] -= s[u];
+          if (t.ok[u]) W[t.ii[u]] = w[u];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < LZR; ++u)
+        if (!t.ok[u]) w[u] = 0.0;
+#pragma unroll
+      for (int j = 0; j < JB; ++j)
+        if (j < jc) {
+#pragma unroll
+          for (int u = 0; u < LZR; ++u) acc[j] += Qc[(i64)j * blk + t.ii[u]] * w[u];
+        }
+    }
+  }
+  lz_store<0, JB>(acc, jc, P, partial, sm);
+}
+
+// pass D: w −= Σ_{j<kc} Q_j C2_j; partial ‖w‖²
+__global__ void __launch_bounds__(RT, 2) k_lz_d(double* __restrict__ W, const double* __restrict__ Q,
+                                                const double* __restrict__ C, int kc, i64 N, int P,
+                                                double* __restrict__ partial_nrm) {
+  __shared__ double sm[RT];
+  const int slots = blockDim.x / P;
+  const int p = threadIdx.x % P, slot = threadIdx.x / P;
+  double acc = 0.0;
+  if (slot < slots) {
+    i64 r0, r1;
+    row_range(N, r0, r1);
+    const i64 blk = N * P;
+    for (i64 rb = r0 + slot; rb < r1; rb += (i64)slots * LZR) {
+      const LzRows t = lz_rows(rb, slots, r0, r1, P, p);
+      double s[LZR];
+#pragma unroll
+      for (int u = 0; u < LZR; ++u) s[u] = 0.0;
+#pragma unroll 4
+      for (int j = 0; j < kc; ++j) {
+        const double c = __ldg(C + j * P + p);
+#pragma unroll
+        for (int u = 0; u < LZR; ++u) s[u] += Q[(i64)j * blk + t.ii[u]] * c;
+      }
+#pragma unroll
+      for (int u = 0; u < LZR; ++u)
+        if (t.ok[u]) {
+          const double w = W[t.ii[u]] - s[u];
+          W[t.ii[u]] = w;
+          acc += w * w;
+        }
+    }
+  }
+  block_col_store(acc, P, partial_nrm, sm);
+}
+
+// β = ‖w‖, breakdown test (linalg.cpp:42-49: β ≤ 1e-12·scale, scale = running
+// max of |α|, β), histories, β_prev and next-vector flags. One block, P threads.
+__global__ void k_lz_state(int k, int P, const double* __restrict__ alpha, const double* __restrict__ nrm2,
+                           int* __restrict__ live, double* __restrict__ scale, int* __restrict__ kbreak,
+                           double* __restrict__ ahist, double* __restrict__ bhist, double* __restrict__ bprev,
+                           double* __restrict__ bdiv, int* __restrict__ flag) {
+  const int p = threadIdx.x;
+  if (p >= P) return;
+  if (!live[p]) {
+    flag[p] = 0;
+    bprev[p] = 0.0;
+    bdiv[p] = 1.0;
+    return;
+  }
+  const double a = alpha[p], beta = sqrt(nrm2[p]);
+  ahist[(i64)k * P + p] = a;
+  const double sc = fmax(scale[p], fmax(fabs(a), beta));
+  scale[p] = sc;
+  if (beta <= 1e-12 * fmax(sc, 1e-300)) {
+    kbreak[p] = k;
+    live[p] = 0;
+    flag[p] = 0;
+    bprev[p] = 0.0;
+    bdiv[p] = 1.0;
+  } else {
+    bhist[(i64)k * P + p] = beta;
+    bprev[p] = beta;
+    bdiv[p] = beta;
+    flag[p] = 1;
+  }
+}
+
+__global__ void k_lz_last(int k, int P, const double* __restrict__ alpha, const int* __restrict__ live,
+                          double* __restrict__ ahist) {
+  const int p = threadIdx.x;
+  if (p < P && live[p]) ahist[(i64)k * P + p] = alpha[p];
+}
+
+// dst[r][s] = src[r][idx[s]] (gather == 1) or dst[r][idx[s]] = src[r][s]
+__global__ void k_cols_move(const double* __restrict__ src, int Psrc, double* __restrict__ dst, int Pdst,
+                            const int* __restrict__ idx, int ns, i64 rows, int gather) {
+  const i64 items = rows * ns;
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < items; e += (i64)gridDim.x * blockDim.x) {
+    const i64 r = e / ns;
+    const int s = int(e - r * ns);
+    if (gather) dst[r * Pdst + s] = src[r * Psrc + idx[s]];
+    else dst[r * Pdst + idx[s]] = src[r * Psrc + s];
+  }
+}
+
 }  // namespace
 
 // ================================================================ PCG driver
@@ -1173,8 +1473,11 @@ void pivchol_copy_L(const PivChol& f, double* out_host) {
 }
 
 // ================================================================ Lanczos
-LanczosBatch lanczos_batch(Op& op, const double* start_int, int P, int steps,
-                           const std::vector<std::uint64_t>& restart_seeds, double* Q_out, cudaStream_t s) {
+// Reference-order Lanczos with a host sync per step (deflating restarts on the
+// host, linalg.cpp:46-69): the breakdown path of lanczos_batch.
+static LanczosBatch lanczos_batch_sync(Op& op, const double* start_int, int P, int steps,
+                                       const std::vector<std::uint64_t>& restart_seeds, double* Q_out,
+                                       cudaStream_t s) {
   if (P < 1 || P > RT) fail(GK_ERR_ARG, "lanczos: number of probes must be in [1, 256]");
   const i64 N = op.N;
   steps = int(std::min<i64>(steps, N));
@@ -1340,6 +1643,150 @@ LanczosBatch lanczos_batch(Op& op, const double* start_int, int P, int steps,
     res.alpha[static_cast<size_t>(p)].resize(static_cast<size_t>(res.len[static_cast<size_t>(p)]));
     res.beta[static_cast<size_t>(p)].resize(static_cast<size_t>(std::max(res.len[static_cast<size_t>(p)] - 1, 0)));
   }
+  return res;
+}
+
+// Fast path: every step on the device, one host sync per batch. Probes that
+// hit a Lanczos breakdown (β ≤ 1e-12·scale) are frozen and re-run, on their
+// own, through lanczos_batch_sync (host-side deflating restarts with the
+// reference's seeds); probes are independent, so the others keep their results.
+LanczosBatch lanczos_batch(Op& op, const double* start_int, int P, int steps,
+                           const std::vector<std::uint64_t>& restart_seeds, double* Q_out, cudaStream_t s) {
+  if (P < 1 || P > RT) fail(GK_ERR_ARG, "lanczos: number of probes must be in [1, 256]");
+  const i64 N = op.N;
+  steps = int(std::min<i64>(steps, N));
+  if (steps <= 0 || g_tuning.lanczos.load() == 1)
+    return lanczos_batch_sync(op, start_int, P, steps, restart_seeds, Q_out, s);
+  const i64 blk = N * P;
+  const bool prof = std::getenv("GK_SLQ_PROF") != nullptr;
+  auto tp0 = std::chrono::steady_clock::now();
+  const int maxc = std::min(steps, JB);
+  const size_t nQ = Q_out ? 0 : static_cast<size_t>(blk) * steps;
+  const size_t nsc = static_cast<size_t>(P) * 5 + static_cast<size_t>(2 * steps) * P;
+  const size_t need = nQ + static_cast<size_t>(blk) + static_cast<size_t>(RB) * P * (1 + maxc) +
+                      static_cast<size_t>(2 * steps) * P + nsc;
+  op.lz_ws.reserve(need);  // grow-only workspace on the operator (guarded by op.mu)
+  op.lz_wsi.reserve(static_cast<size_t>(P) * 3);
+  double* cur = op.lz_ws.p;
+  auto carve = [&](size_t n) {
+    double* r = cur;
+    cur += n;
+    return r;
+  };
+  double* Q = Q_out ? Q_out : carve(nQ);
+  struct Span {
+    double* p;
+    size_t n;
+  };
+  Span W{carve(blk), 0}, pa{carve(static_cast<size_t>(RB) * P), 0}, pg{carve(static_cast<size_t>(RB) * maxc * P), 0},
+      C1{carve(static_cast<size_t>(steps) * P), 0},
+      C2{carve(static_cast<size_t>(steps) * P), 0}, sc{carve(nsc), nsc};
+  struct ISpan {
+    int* p;
+  } si{op.lz_wsi.p};
+  double *d_alpha = sc.p, *d_nrm = sc.p + P, *d_scale = sc.p + 2 * P, *d_bprev = sc.p + 3 * P, *d_bdiv = sc.p + 4 * P;
+  double *d_ahist = sc.p + 5 * P, *d_bhist = d_ahist + static_cast<size_t>(steps) * P;
+  int *d_live = si.p, *d_kbreak = si.p + P, *d_flag = si.p + 2 * P;
+  GK_CUDA(cudaMemcpyAsync(Q, start_int, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
+  GK_CUDA(cudaMemsetAsync(sc.p, 0, sizeof(double) * sc.n, s));
+  {
+    std::vector<int> init(static_cast<size_t>(P) * 3, 0);
+    for (int p = 0; p < P; ++p) init[static_cast<size_t>(p)] = 1, init[static_cast<size_t>(P + p)] = -1;
+    GK_CUDA(cudaMemcpyAsync(si.p, init.data(), sizeof(int) * init.size(), cudaMemcpyHostToDevice, s));
+    GK_CUDA(cudaStreamSynchronize(s));  // pageable source
+  }
+  if (prof) {
+    GK_CUDA(cudaStreamSynchronize(s));
+    std::fprintf(stderr, "lanczos: setup %.2f ms\n",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count());
+    tp0 = std::chrono::steady_clock::now();
+  }
+  for (int k = 0; k < steps; ++k) {
+    const double* qk = Q + (i64)k * blk;
+    op.mvm(qk, W.p, P, s);
+    const bool last = k + 1 >= steps;
+    const int k1 = last ? 0 : k + 1;  // the reference never uses the last step's reorth/β
+    for (int j0 = 0; j0 < std::max(k1, 1); j0 += JB) {
+      const int jc = std::min(JB, k1 - j0);
+      k_lz_b<<<RB, RT, 0, s>>>(W.p, j0 == 0 && k > 0 ? Q + (i64)(k - 1) * blk : nullptr, d_bprev, qk, Q, j0,
+                               std::max(jc, 0), N, P, j0 == 0 ? pa.p : nullptr, pg.p);
+      launched("lanczos pass B (alpha + projection 1)");
+      k_lz_fin_b<<<lz_fin_blocks(std::max(jc, 0) * P) + (j0 == 0 ? lz_fin_blocks(P) : 0), 256, 0, s>>>(
+          j0 == 0 ? pa.p : nullptr, pg.p, j0, std::max(jc, 0), k, P, d_alpha, C1.p);
+      launched("lanczos pass B fin");
+    }
+    if (last) {
+      k_lz_last<<<1, RT, 0, s>>>(k, P, d_alpha, d_live, d_ahist);
+      launched("lanczos last alpha");
+      break;
+    }
+    for (int j0 = 0; j0 < k1; j0 += JB) {
+      const int jc = std::min(JB, k1 - j0);
+      k_lz_c<<<RB, RT, 0, s>>>(W.p, qk, d_alpha, Q, C1.p, k1, j0, jc, N, P, pg.p);
+      launched("lanczos pass C (update 1 + projection 2)");
+      k_lz_fin<<<lz_fin_blocks(jc * P), 256, 0, s>>>(pg.p, jc * P, C2.p + (i64)j0 * P);
+      launched("lanczos pass C fin");
+    }
+    k_lz_d<<<RB, RT, 0, s>>>(W.p, Q, C2.p, k1, N, P, pa.p);
+    launched("lanczos pass D (update 2 + norm)");
+    k_lz_fin<<<lz_fin_blocks(P), 256, 0, s>>>(pa.p, P, d_nrm);
+    launched("lanczos norm fin");
+    k_lz_state<<<1, RT, 0, s>>>(k, P, d_alpha, d_nrm, d_live, d_scale, d_kbreak, d_ahist, d_bhist, d_bprev, d_bdiv,
+                                d_flag);
+    launched("lanczos state");
+    k_lz_next<<<blocks_for(blk), 256, 0, s>>>(W.p, d_bdiv, d_flag, N, P, Q + (i64)(k + 1) * blk);
+    launched("lanczos next");
+  }
+  std::vector<double> ah(static_cast<size_t>(steps) * P), bh(static_cast<size_t>(steps) * P);
+  std::vector<int> kb(static_cast<size_t>(P));
+  GK_CUDA(cudaMemcpyAsync(ah.data(), d_ahist, sizeof(double) * ah.size(), cudaMemcpyDeviceToHost, s));
+  GK_CUDA(cudaMemcpyAsync(bh.data(), d_bhist, sizeof(double) * bh.size(), cudaMemcpyDeviceToHost, s));
+  GK_CUDA(cudaMemcpyAsync(kb.data(), d_kbreak, sizeof(int) * P, cudaMemcpyDeviceToHost, s));
+  GK_CUDA(cudaStreamSynchronize(s));
+  if (prof)
+    std::fprintf(stderr, "lanczos: steps %.2f ms\n",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count());
+  LanczosBatch res;
+  res.P = P;
+  res.steps = steps;
+  res.len.assign(static_cast<size_t>(P), steps);
+  res.alpha.assign(static_cast<size_t>(P), {});
+  res.beta.assign(static_cast<size_t>(P), {});
+  res.breakdown.assign(static_cast<size_t>(P), 0);
+  std::vector<int> redo;
+  for (int p = 0; p < P; ++p) {
+    if (kb[static_cast<size_t>(p)] >= 0) {
+      redo.push_back(p);
+      continue;
+    }
+    auto& a = res.alpha[static_cast<size_t>(p)];
+    auto& b = res.beta[static_cast<size_t>(p)];
+    for (int k = 0; k < steps; ++k) a.push_back(ah[static_cast<size_t>(k) * P + p]);
+    for (int k = 0; k + 1 < steps; ++k) b.push_back(bh[static_cast<size_t>(k) * P + p]);
+  }
+  if (redo.empty()) return res;
+  // Breakdown: exact re-run of the affected probes with host-side restarts.
+  const int ns = int(redo.size());
+  DevBuf<int> idx(static_cast<size_t>(ns));
+  GK_CUDA(cudaMemcpy(idx.p, redo.data(), sizeof(int) * ns, cudaMemcpyHostToDevice));
+  DevBuf<double> start_s(static_cast<size_t>(N) * ns), Q_s(Q_out ? static_cast<size_t>(N) * ns * steps : 0);
+  k_cols_move<<<blocks_for(N * ns), 256, 0, s>>>(start_int, P, start_s.p, ns, idx.p, ns, N, 1);
+  launched("lanczos redo gather");
+  std::vector<std::uint64_t> seeds_s;
+  for (int p : redo) seeds_s.push_back(restart_seeds[static_cast<size_t>(p)]);
+  LanczosBatch rs = lanczos_batch_sync(op, start_s.p, ns, steps, seeds_s, Q_out ? Q_s.p : nullptr, s);
+  if (Q_out) {
+    k_cols_move<<<blocks_for(N * steps * ns), 256, 0, s>>>(Q_s.p, ns, Q_out, P, idx.p, ns, N * steps, 0);
+    launched("lanczos redo scatter");
+  }
+  for (int t = 0; t < ns; ++t) {
+    const size_t p = static_cast<size_t>(redo[static_cast<size_t>(t)]);
+    res.len[p] = rs.len[static_cast<size_t>(t)];
+    res.alpha[p] = rs.alpha[static_cast<size_t>(t)];
+    res.beta[p] = rs.beta[static_cast<size_t>(t)];
+    res.breakdown[p] = rs.breakdown[static_cast<size_t>(t)];
+  }
+  GK_CUDA(cudaStreamSynchronize(s));
   return res;
 }
 

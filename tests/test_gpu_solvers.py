@@ -111,6 +111,39 @@ def test_slq_matches_oracle_per_probe():
     assert np.allclose(g.estimates, r.estimates, rtol=1e-8, atol=0)
 
 
+def test_slq_device_lanczos_matches_host_synchronised_path():
+    """The device-resident Lanczos step (fused α/projection passes, device
+    breakdown test) against the per-step host-synchronised reference-order
+    loop (tuning "lanczos" = 1), across the basis-chunk boundaries (45 steps >
+    JB = 16, JC = 32), and against the oracle."""
+    X, y, dY = gk.make_dataset(1, 0)
+    X = X[:400]
+    grid = gk.Grid.cover(X, 0.015, 3, 40)
+    op = gk.DskiOperator(gk.KernelSpec(0.15, 1.0), grid, X, (0.05, 0.05))
+    ref = O.DskiOperator(O.KernelSpec(0.15, 1.0), O.Grid(grid.dims, grid.origin, grid.spacing), X, (0.05, 0.05))
+    fast = gk.slq_logdet(op, 40, 45, 11, 1e-6)
+    try:
+        gk.set_tuning("lanczos", 1)
+        slow = gk.slq_logdet(op, 40, 45, 11, 1e-6)
+    finally:
+        gk.set_tuning("lanczos", 0)
+    assert np.allclose(fast.estimates, slow.estimates, rtol=1e-9, atol=0)
+    r = O.slq_logdet(ref, 40, 45, 11, 1e-6)
+    assert abs(fast.logdet - r.logdet) <= 1e-8 * abs(r.logdet)
+
+
+def test_slq_breakdown_probes_take_the_restart_path():
+    """Five distinct eigenvalues: every probe's Krylov space is exhausted at
+    step 5 (β ≈ 0, linalg.cpp:42-49), so all probes re-run through the host
+    restart path; the estimates match the oracle's."""
+    d = np.repeat([0.5, 1.0, 2.0, 3.0, 5.0], 16)
+    A = np.diag(d)
+    g = gk.slq_logdet(gk.DenseOperator(A), 6, 12, 4)
+    r = O.slq_logdet(O.DenseOperator(A), 6, 12, 4)
+    assert np.allclose(g.estimates, r.estimates, rtol=1e-8, atol=0)
+    assert abs(g.logdet - np.sum(np.log(d))) <= 0.05 * abs(np.sum(np.log(d))) + 1.0
+
+
 def test_lanczos_lowrank_rank3_and_identity_breakdown():
     G = np.column_stack([np.random.default_rng(500 + j).standard_normal(40) for j in range(3)])
     A = G @ G.T

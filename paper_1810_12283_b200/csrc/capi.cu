@@ -850,23 +850,28 @@ gk_status gk_slq_logdet(const gk_op* h, int probes, int steps, uint64_t seed, do
     const int chunk = std::min(probes, 64);
     std::vector<double> est(static_cast<size_t>(probes), 0.0);
     std::vector<int> clamps(static_cast<size_t>(probes), 0);
-    std::vector<double> hz(static_cast<size_t>(N) * chunk);
-    op.slq_z.reserve(static_cast<size_t>(N) * chunk * 2);
+    // An odd probe batch runs one extra (discarded) probe: the batched MVM
+    // handles RHS pairs, and an odd count falls to its single-RHS variant.
+    const int cap = chunk + 1;
+    op.slq_h.reserve(static_cast<size_t>(N) * cap);
+    double* hzp = op.slq_h.p;
+    op.slq_z.reserve(static_cast<size_t>(N) * cap * 2);
     double* ze_p = op.slq_z.p;
-    double* zi_p = op.slq_z.p + static_cast<size_t>(N) * chunk;
+    double* zi_p = op.slq_z.p + static_cast<size_t>(N) * cap;
     const bool prof = std::getenv("GK_SLQ_PROF") != nullptr;
     auto now = [] { return std::chrono::steady_clock::now(); };
     auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
     for (int p0 = 0; p0 < probes; p0 += chunk) {
       const int P = std::min(chunk, probes - p0);
-      std::vector<std::uint64_t> rseeds(static_cast<size_t>(P));
+      const int Prun = (P & 1) && N > 1 ? P + 1 : P;
+      std::vector<std::uint64_t> rseeds(static_cast<size_t>(Prun));
       auto t0 = now();
       // probe vectors (host mt19937_64 streams, bit-exact with the reference),
       // generated in parallel over probes
-      std::vector<double> zn2v(static_cast<size_t>(P), 0.0);
+      std::vector<double> zn2v(static_cast<size_t>(Prun), 0.0);
       auto gen = [&](int q) {
         const std::uint64_t pid = std::uint64_t(probe_offset + p0 + q);
-        double* z = hz.data() + static_cast<size_t>(q) * N;
+        double* z = hzp + static_cast<size_t>(q) * N;
         rademacher(N, seed, pid, z);
         double s2 = 0.0;
         for (i64 i = 0; i < N; ++i) s2 += z[i] * z[i];
@@ -875,13 +880,13 @@ gk_status gk_slq_logdet(const gk_op* h, int probes, int steps, uint64_t seed, do
         for (i64 i = 0; i < N; ++i) z[i] /= zn;
         rseeds[static_cast<size_t>(q)] = mix_seed(seed, 50000 + pid);
       };
-      parallel_for(P, gen);
+      parallel_for(Prun, gen);
       auto t1 = now();
-      GK_CUDA(cudaMemcpyAsync(ze_p, hz.data(), sizeof(double) * N * P, cudaMemcpyHostToDevice, s));
-      op.to_internal(ze_p, N, zi_p, P, s);
+      GK_CUDA(cudaMemcpyAsync(ze_p, hzp, sizeof(double) * N * Prun, cudaMemcpyHostToDevice, s));
+      op.to_internal(ze_p, N, zi_p, Prun, s);
       if (prof) GK_CUDA(cudaStreamSynchronize(s));
       auto t2 = now();
-      LanczosBatch lb = lanczos_batch(op, zi_p, P, steps, rseeds, nullptr, s);
+      LanczosBatch lb = lanczos_batch(op, zi_p, Prun, steps, rseeds, nullptr, s);
       auto t3 = now();
       if (prof) std::fprintf(stderr, "slq: probes %.2f ms, upload %.2f ms, lanczos %.2f ms\n", ms(t0, t1), ms(t1, t2), ms(t2, t3));
       for (int q = 0; q < P; ++q) {

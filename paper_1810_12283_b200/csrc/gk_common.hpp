@@ -162,6 +162,7 @@ struct Op {
   // Lanczos / SLQ workspace (grow-only; cudaMalloc/cudaFree of the N×P×steps
   // basis per call cost more than the steps themselves)
   DevBuf<double> lz_ws, slq_z;
+  HostBuf slq_h;  // pinned probe staging
   DevBuf<int> lz_wsi;
   HostBuf pinned;
   // host-buffer MVM pipeline (gk_op_mvm): copy-in / compute / copy-out streams

@@ -45,6 +45,7 @@ struct PcgVecArgs {
 };
 
 struct PcgVecPlan {
+  bool v2 = false;  // rows-resident variant (k_pcg_vec2)
   int grid = 0;
   int rch = 1;
   size_t smem = 0;

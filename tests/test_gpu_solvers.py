@@ -239,11 +239,13 @@ def test_dski_pipeline_matches_oracle_c1_subset():
 
 @pytest.mark.parametrize("nrhs", [1, 8, 32])
 @pytest.mark.parametrize("with_precond", [True, False])
-def test_fused_pcg_step_matches_unfused(nrhs, with_precond):
+@pytest.mark.parametrize("variant", [1, 3])  # 1: rows-resident v2 where it fits, 3: v1
+def test_fused_pcg_step_matches_unfused(nrhs, with_precond, variant):
     """The one-launch PCG vector step (pcg_fused.cu) runs the same per-column
-    recurrences as the ten-kernel path: same iteration counts and flags,
+    recurrences as the separate-kernel path: same iteration counts and flags,
     solutions equal to roundoff, and both meet the oracle's well-conditioned
-    ±1 iteration parity."""
+    ±1 iteration parity. v2 forms r·z as ‖c‖² − ‖Q1ᵀc‖² (the
+    Preconditioner::quadratic identity) and z never leaves registers."""
     X, y, dY = _dski_model(1, 300)
     grid = gk.Grid.cover(X, 1e-3, 3, 40)
     noise = (0.5, 0.5)
@@ -254,7 +256,7 @@ def test_fused_pcg_step_matches_unfused(nrhs, with_precond):
     B[:, 0] = gk.stacked_targets(y, dY, y.mean())
     if nrhs > 2:
         B[:, 2] = 0.0  # zero right-hand side: converged at 0 iterations
-    prev = gk.set_tuning("pcg_fused", 1)  # one-launch vector step
+    prev = gk.set_tuning("pcg_fused", variant)  # one-launch vector step
     try:
         fused = gk.cg(g, B if nrhs > 1 else B[:, 0], 1e-7, 3000, M)
         gk.set_tuning("pcg_fused", 2)  # separate kernels

@@ -300,11 +300,13 @@ gk_status gk_op_mvm(const gk_op* h, const double* V, int64_t ldv, double* Out, i
     std::lock_guard<std::mutex> lk(op.mu);
     DeviceGuard dg(op.device);
     cudaStream_t s = op.stream;
-    // Host buffers: column chunks pipelined over three streams — copy-in
-    // (H2D + to-internal) of chunk j+1, the MVM of chunk j and copy-out
-    // (from-internal + D2H) of chunk j-1 overlap, and H2D/D2H run in
-    // opposite PCIe directions at once. Columns are independent, so the
-    // result equals the one-shot MVM.
+    // Host buffers: column chunks pipelined over five streams, one per
+    // resource stage — H2D (copy engine), to-internal permute, MVM,
+    // from-internal permute, D2H (the other copy engine). Each stage of chunk
+    // j waits only for the previous stage of chunk j, so the copy engines
+    // never idle behind a permute and H2D/D2H run in opposite PCIe
+    // directions at once. Columns are independent: the result equals the
+    // one-shot MVM. Tuning "e2e_chunk": chunk width (0 = nrhs/4 for nrhs >= 16).
     const int pc = g_tuning.e2e_chunk.load();
     int chunk = pc > 0 ? pc : (nrhs >= 16 ? int((nrhs + 3) / 4) : int(nrhs));
     chunk = int(std::min<i64>(std::max(1, chunk), std::min<i64>(nrhs, kMaxRhs)));
@@ -312,8 +314,10 @@ gk_status gk_op_mvm(const gk_op* h, const double* V, int64_t ldv, double* Out, i
     if (!op.io_in) {
       GK_CUDA(cudaStreamCreateWithFlags(&op.io_in, cudaStreamNonBlocking));
       GK_CUDA(cudaStreamCreateWithFlags(&op.io_out, cudaStreamNonBlocking));
+      GK_CUDA(cudaStreamCreateWithFlags(&op.io_pin, cudaStreamNonBlocking));
+      GK_CUDA(cudaStreamCreateWithFlags(&op.io_pout, cudaStreamNonBlocking));
     }
-    while (int(op.io_events.size()) < 2 * nchunks + 1) {
+    while (int(op.io_events.size()) < 4 * nchunks + 1) {
       cudaEvent_t e;
       GK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       op.io_events.push_back(e);
@@ -323,21 +327,30 @@ gk_status gk_op_mvm(const gk_op* h, const double* V, int64_t ldv, double* Out, i
     op.io_int_in.reserve(tot);
     op.io_int_out.reserve(tot);
     op.io_ext_out.reserve(tot);
-    // the copy streams must not start before earlier work on the compute stream
-    GK_CUDA(cudaEventRecord(op.io_events[2 * nchunks], s));
-    GK_CUDA(cudaStreamWaitEvent(op.io_in, op.io_events[2 * nchunks], 0));
-    GK_CUDA(cudaStreamWaitEvent(op.io_out, op.io_events[2 * nchunks], 0));
+    // the side streams must not start before earlier work on the compute stream
+    cudaEvent_t e0 = op.io_events[4 * nchunks];
+    GK_CUDA(cudaEventRecord(e0, s));
+    for (cudaStream_t t : {op.io_in, op.io_out, op.io_pin, op.io_pout}) GK_CUDA(cudaStreamWaitEvent(t, e0, 0));
     for (int j = 0; j < nchunks; ++j) {
       const i64 c0 = i64(j) * chunk;
       const int nb = int(std::min<i64>(chunk, nrhs - c0));
       const size_t off = static_cast<size_t>(op.N) * c0;
-      upload_internal(op, V + c0 * ldv, ldv, op.io_ext_in.p + off, op.io_int_in.p + off, nb, op.io_in);
-      GK_CUDA(cudaEventRecord(op.io_events[2 * j], op.io_in));
-      GK_CUDA(cudaStreamWaitEvent(s, op.io_events[2 * j], 0));
+      cudaEvent_t* ev = &op.io_events[4 * j];
+      GK_CUDA(cudaMemcpy2DAsync(op.io_ext_in.p + off, sizeof(double) * op.N, V + c0 * ldv, sizeof(double) * ldv,
+                                sizeof(double) * op.N, nb, cudaMemcpyHostToDevice, op.io_in));
+      GK_CUDA(cudaEventRecord(ev[0], op.io_in));
+      GK_CUDA(cudaStreamWaitEvent(op.io_pin, ev[0], 0));
+      op.to_internal(op.io_ext_in.p + off, op.N, op.io_int_in.p + off, nb, op.io_pin);
+      GK_CUDA(cudaEventRecord(ev[1], op.io_pin));
+      GK_CUDA(cudaStreamWaitEvent(s, ev[1], 0));
       op.mvm(op.io_int_in.p + off, op.io_int_out.p + off, nb, s);
-      GK_CUDA(cudaEventRecord(op.io_events[2 * j + 1], s));
-      GK_CUDA(cudaStreamWaitEvent(op.io_out, op.io_events[2 * j + 1], 0));
-      download_internal(op, op.io_int_out.p + off, op.io_ext_out.p + off, Out + c0 * ldo, ldo, nb, op.io_out);
+      GK_CUDA(cudaEventRecord(ev[2], s));
+      GK_CUDA(cudaStreamWaitEvent(op.io_pout, ev[2], 0));
+      op.from_internal(op.io_int_out.p + off, op.io_ext_out.p + off, op.N, nb, op.io_pout);
+      GK_CUDA(cudaEventRecord(ev[3], op.io_pout));
+      GK_CUDA(cudaStreamWaitEvent(op.io_out, ev[3], 0));
+      GK_CUDA(cudaMemcpy2DAsync(Out + c0 * ldo, sizeof(double) * ldo, op.io_ext_out.p + off, sizeof(double) * op.N,
+                                sizeof(double) * op.N, nb, cudaMemcpyDeviceToHost, op.io_out));
     }
     GK_CUDA(cudaStreamSynchronize(op.io_out));
     GK_CUDA(cudaStreamSynchronize(s));

@@ -166,7 +166,7 @@ struct Op {
   DevBuf<int> lz_wsi;
   HostBuf pinned;
   // host-buffer MVM pipeline (gk_op_mvm): copy-in / compute / copy-out streams
-  cudaStream_t io_in = nullptr, io_out = nullptr;
+  cudaStream_t io_in = nullptr, io_out = nullptr, io_pin = nullptr, io_pout = nullptr;
   std::vector<cudaEvent_t> io_events;
   DevBuf<double> io_ext_in, io_int_in, io_int_out, io_ext_out;
 

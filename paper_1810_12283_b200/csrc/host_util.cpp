@@ -136,6 +136,8 @@ Op::~Op() {
   for (auto e : io_events) cudaEventDestroy(e);
   if (io_in) cudaStreamDestroy(io_in);
   if (io_out) cudaStreamDestroy(io_out);
+  if (io_pin) cudaStreamDestroy(io_pin);
+  if (io_pout) cudaStreamDestroy(io_pout);
   if (stream) cudaStreamDestroy(stream);
   if (cap_stream) cudaStreamDestroy(cap_stream);
 }

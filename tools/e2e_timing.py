@@ -33,7 +33,7 @@ for chunk in (32, 16, 8, 4, 0):
     if ref is None:
         ref = out
     err = np.linalg.norm(out - ref) / np.linalg.norm(ref)
-    print(f"chunk {chunk or 'auto'}: median {np.median(ts)*1e6:.1f} us per 32-RHS call, "
+    print(f"chunk {({0: 'auto'}).get(chunk, chunk)}: mean {np.mean(ts)*1e6:.1f} us, median {np.median(ts)*1e6:.1f} us per 32-RHS call, "
           f"{N*nrhs/np.median(ts)/1e9:.2f} G rows*RHS/s, rel diff vs one-shot {err:.1e}", flush=True)
 gk.set_tuning("e2e_chunk", 0)
 

@@ -371,6 +371,242 @@ __global__ void __launch_bounds__(256) k_scatter_lean(DskiView op, const double*
   u[(size_t)node * nrhs + b] = acc;
 }
 
+// d = 3 scatter Bᵀv as node columns: warp = one (k0, k1) node column × 32 RHS
+// lanes, rolling over the cells b2 along the last axis. Points are sorted by
+// base cell (row-major), so for each b2 the points of the 36 covering cell
+// columns (k0−t0, k1−t1, b2) are contiguous ranges; each point adds to the T
+// window nodes k2 = b2 .. b2+T−1 held in registers, and node b2 is final (and
+// stored) once cell b2 is done. The last axis is split into segments
+// (grid.y); a segment re-reads the T−1 cells below it instead of exchanging
+// halos. Each point is read by its 36 covering columns (the pull kernel read
+// it once per covered node: 216×). No atomics; fixed order (deterministic).
+template <int T, bool GRAD>
+__global__ void __launch_bounds__(256) k_scatter_col3(DskiView op, const double* __restrict__ v,
+                                                      double* __restrict__ u, int nrhs, int zseg) {
+  const int lane = threadIdx.x;
+  const int col = blockIdx.x * blockDim.y + threadIdx.y;
+  const int m1 = op.m[1], m2 = op.m[2];
+  if (col >= op.m[0] * m1) return;
+  const int k0 = col / m1, k1 = col - k0 * m1;
+  const int z0 = blockIdx.y * zseg, z1 = min(m2, z0 + zseg);
+  const int bb = blockIdx.z * 32 + lane;
+  const bool bok = bb < nrhs;
+  const int b = bok ? bb : 0;
+  const int nb1 = op.nb[1], nb2 = op.nb[2];
+  const int t0lo = max(0, k0 - (op.nb[0] - 1)), t0hi = min(T - 1, k0);
+  const int t1lo = max(0, k1 - (nb1 - 1)), t1hi = min(T - 1, k1);
+  const size_t gs = (size_t)op.n * nrhs;
+  double acc[T];
+#pragma unroll
+  for (int i = 0; i < T; ++i) acc[i] = 0.0;
+  for (int b2 = max(0, z0 - (T - 1)); b2 < z1; ++b2) {
+    if (b2 < nb2) {
+      for (int t0 = t0lo; t0 <= t0hi; ++t0) {
+        const int c0 = (k0 - t0) * nb1;
+        for (int t1 = t1lo; t1 <= t1hi; ++t1) {
+          const int cell = (c0 + (k1 - t1)) * nb2 + b2;
+          const int s_lo = __ldg(op.cell_start + cell), s_hi = __ldg(op.cell_start + cell + 1);
+          for (int s = s_lo; s < s_hi; ++s) {
+            const double2* wd = op.wd + (size_t)s * 3 * T;
+            const double2 a0 = __ldg(wd + t0), a1 = __ldg(wd + T + t1);
+            const double* vs = v + (size_t)s * nrhs + b;
+            const double v0 = __ldg(vs);
+            double A, Bc = 0.0;
+            if constexpr (GRAD) {
+              const double v1 = __ldg(vs + gs), v2 = __ldg(vs + 2 * gs), v3 = __ldg(vs + 3 * gs);
+              A = a1.x * (v0 * a0.x + v1 * a0.y) + a1.y * (v2 * a0.x);
+              Bc = a1.x * (v3 * a0.x);
+            } else {
+              A = a1.x * a0.x * v0;
+            }
+#pragma unroll
+            for (int t2 = 0; t2 < T; ++t2) {
+              const double2 a2 = __ldg(wd + 2 * T + t2);
+              acc[t2] += GRAD ? a2.x * A + a2.y * Bc : a2.x * A;
+            }
+          }
+        }
+      }
+    }
+    if (b2 >= z0 && bok) u[((size_t)col * m2 + b2) * nrhs + bb] = acc[0];
+#pragma unroll
+    for (int i = 0; i < T - 1; ++i) acc[i] = acc[i + 1];
+    acc[T - 1] = 0.0;
+  }
+}
+
+// d = 3 scatter from the per-column sorted point lists (built once with the
+// operator): warp = (node column, z-segment, 32 RHS lanes). Entries are taken
+// 32 at a time: first lane-parallel — lane l turns entry l's stencil weights
+// into the coefficients α0 = w1·w0, α1 = w1·∂w0, α2 = ∂w1·w0 and the T axis-2
+// (w, ∂w) pairs, kept in per-warp shared memory — then the warp walks the
+// chunk with RHS lanes, where only the v loads (independent across entries)
+// touch memory, and the rolling window emits node b2 when the walk reaches a
+// larger base b2. No atomics; fixed order (deterministic).
+constexpr int L3_WARPS = 4;
+template <int T, bool GRAD>
+__global__ void __launch_bounds__(32 * L3_WARPS) k_scatter_list3(DskiView op, const int2* __restrict__ list,
+                                                                const int* __restrict__ cstart,
+                                                                const int* __restrict__ cseg, int nseg, int zseg,
+                                                                const double* __restrict__ v, double* __restrict__ u,
+                                                                int nrhs) {
+  constexpr int NC = 3 + 2 * T;  // α0, α1, α2, (w2, ∂w2) × T
+  __shared__ double coef[L3_WARPS][32][NC + 1];
+  __shared__ int cpt[L3_WARPS][32], cmeta[L3_WARPS][32];
+  const int lane = threadIdx.x, wy = threadIdx.y;
+  const int col = blockIdx.x * blockDim.y + wy;
+  const int m2 = op.m[2];
+  if (col >= op.m[0] * op.m[1]) return;
+  const int seg = blockIdx.y;
+  const int z0 = seg * zseg, z1 = min(m2, z0 + zseg);
+  const int bb = blockIdx.z * 32 + lane;
+  const bool bok = bb < nrhs;
+  const int b = bok ? bb : 0;
+  const size_t gs = (size_t)op.n * nrhs;
+  double acc[T];
+#pragma unroll
+  for (int i = 0; i < T; ++i) acc[i] = 0.0;
+  int cur = max(0, z0 - (T - 1));  // acc[i] <-> node cur + i
+  double* ucol = u + (size_t)col * m2 * nrhs + bb;
+  const int e_end = __ldg(cstart + col + 1);
+  bool done = false;
+  for (int e0 = __ldg(cseg + col * nseg + seg); e0 < e_end && !done; e0 += 32) {
+    const int cnt = min(32, e_end - e0);
+    // phase 1: lane l prepares entry e0 + l
+    if (lane < cnt) {
+      const int2 me = __ldg(list + e0 + lane);
+      const int t0 = (me.y >> 4) & 15, t1 = me.y & 15;
+      const double2* wd = op.wd + (size_t)me.x * 3 * T;
+      const double2 a0 = __ldg(wd + t0), a1 = __ldg(wd + T + t1);
+      double* c = coef[wy][lane];
+      c[0] = a1.x * a0.x;
+      c[1] = a1.x * a0.y;
+      c[2] = a1.y * a0.x;
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const double2 a2 = __ldg(wd + 2 * T + t);
+        c[3 + 2 * t] = a2.x;
+        c[4 + 2 * t] = a2.y;
+      }
+      cpt[wy][lane] = me.x;
+      cmeta[wy][lane] = me.y;
+    }
+    __syncwarp();
+    // phase 2: the walk
+#pragma unroll 4
+    for (int j = 0; j < cnt; ++j) {
+      const int meta = cmeta[wy][j];
+      const int b2 = meta >> 8;
+      if (b2 >= z1) {
+        done = true;
+        break;
+      }
+      const double* vs = v + (size_t)cpt[wy][j] * nrhs + b;
+      const double* c = coef[wy][j];
+      const double v0 = __ldg(vs);
+      double A, Bc = 0.0;
+      if constexpr (GRAD) {
+        const double v1 = __ldg(vs + gs), v2 = __ldg(vs + 2 * gs), v3 = __ldg(vs + 3 * gs);
+        A = c[0] * v0 + c[1] * v1 + c[2] * v2;
+        Bc = c[0] * v3;
+      } else {
+        A = c[0] * v0;
+      }
+      while (cur < b2) {
+        if (cur >= z0 && bok) ucol[(size_t)cur * nrhs] = acc[0];
+#pragma unroll
+        for (int i = 0; i < T - 1; ++i) acc[i] = acc[i + 1];
+        acc[T - 1] = 0.0;
+        ++cur;
+      }
+#pragma unroll
+      for (int t = 0; t < T; ++t) acc[t] += GRAD ? c[3 + 2 * t] * A + c[4 + 2 * t] * Bc : c[3 + 2 * t] * A;
+    }
+    __syncwarp();
+  }
+  while (cur < z1) {
+    if (cur >= z0 && bok) ucol[(size_t)cur * nrhs] = acc[0];
+#pragma unroll
+    for (int i = 0; i < T - 1; ++i) acc[i] = acc[i + 1];
+    acc[T - 1] = 0.0;
+    ++cur;
+  }
+}
+
+// d = 3 scatter over balanced work units (warp = one unit × 32 RHS lanes):
+// same rolling window as k_scatter_list3, but each unit carries ~64 list
+// entries, so surface-concentrated point sets (C3) do not leave a few
+// columns with all the work. u must be zeroed first.
+template <int T, bool GRAD>
+__global__ void __launch_bounds__(256) k_scatter_units3(DskiView op, const int2* __restrict__ list,
+                                                        const int* __restrict__ cstart,
+                                                        const int4* __restrict__ units, int nunits,
+                                                        const double* __restrict__ v, double* __restrict__ u,
+                                                        int nrhs) {
+  const int lane = threadIdx.x;
+  const int ui = blockIdx.x * blockDim.y + threadIdx.y;
+  if (ui >= nunits) return;
+  const int4 un = __ldg(units + ui);
+  const int col = un.x, za = un.y, zb = un.z;
+  const int m2 = op.m[2];
+  const int bb = blockIdx.y * 32 + lane;
+  const bool bok = bb < nrhs;
+  const int b = bok ? bb : 0;
+  const size_t gs = (size_t)op.n * nrhs;
+  double acc[T];
+#pragma unroll
+  for (int i = 0; i < T; ++i) acc[i] = 0.0;
+  int cur = max(0, za - (T - 1));
+  double* ucol = u + (size_t)col * m2 * nrhs + bb;
+  const int e_end = __ldg(cstart + col + 1);
+  bool done = false;
+  for (int e0 = un.w; e0 < e_end && !done; e0 += 32) {
+    const int2 mine = e0 + lane < e_end ? __ldg(list + e0 + lane) : make_int2(0, 0x7fffff00);
+    const int cnt = min(32, e_end - e0);
+#pragma unroll 4
+    for (int j = 0; j < cnt; ++j) {
+      const int sp = __shfl_sync(0xffffffffu, mine.x, j);
+      const int meta = __shfl_sync(0xffffffffu, mine.y, j);
+      const int b2 = meta >> 8, t0 = (meta >> 4) & 15, t1 = meta & 15;
+      if (b2 >= zb) {
+        done = true;
+        break;
+      }
+      const double2* wd = op.wd + (size_t)sp * 3 * T;
+      const double2 a0 = __ldg(wd + t0), a1 = __ldg(wd + T + t1);
+      double2 a2[T];
+#pragma unroll
+      for (int t = 0; t < T; ++t) a2[t] = __ldg(wd + 2 * T + t);
+      const double* vs = v + (size_t)sp * nrhs + b;
+      const double v0 = __ldg(vs);
+      double A, Bc = 0.0;
+      if constexpr (GRAD) {
+        const double v1 = __ldg(vs + gs), v2 = __ldg(vs + 2 * gs), v3 = __ldg(vs + 3 * gs);
+        A = a1.x * (v0 * a0.x + v1 * a0.y) + a1.y * (v2 * a0.x);
+        Bc = a1.x * (v3 * a0.x);
+      } else {
+        A = a1.x * a0.x * v0;
+      }
+      while (cur < b2) {
+        if (cur >= za && bok) ucol[(size_t)cur * nrhs] = acc[0];
+#pragma unroll
+        for (int i = 0; i < T - 1; ++i) acc[i] = acc[i + 1];
+        acc[T - 1] = 0.0;
+        ++cur;
+      }
+#pragma unroll
+      for (int t = 0; t < T; ++t) acc[t] += GRAD ? a2[t].x * A + a2[t].y * Bc : a2[t].x * A;
+    }
+  }
+  while (cur < zb) {
+    if (cur >= za && bok) ucol[(size_t)cur * nrhs] = acc[0];
+#pragma unroll
+    for (int i = 0; i < T - 1; ++i) acc[i] = acc[i + 1];
+    acc[T - 1] = 0.0;
+    ++cur;
+  }
+}
+
 template <int D, int T, bool GRAD>
 __global__ void __launch_bounds__(256) k_gather_lean(DskiView op, const double* __restrict__ w,
                                                      const double* __restrict__ v, double* __restrict__ out,
@@ -907,6 +1143,16 @@ struct DskiOp final : Op {
   DevBuf<double> tvec_dl;
   std::vector<int> band_dl;
   DevBuf<double> grid_a, grid_b;  // dlogell scratch
+  // d = 3 scatter: per node column (k0, k1) the covering points sorted by
+  // last-axis base cell, entries {sorted point, b2 << 8 | t0 << 4 | t1};
+  // col3_start[col] and per (col, z-segment) first entry
+  DevBuf<int2> col3_list;
+  DevBuf<int> col3_start, col3_seg;
+  int col3_zseg = 12, col3_nseg = 0;
+  // balanced work units over the column lists: {col, za, zb, first entry};
+  // a unit emits nodes [za, zb) of its column (nodes no point touches are 0)
+  DevBuf<int4> col3_units;
+  int col3_nunits = 0;
   int max_row_pts = 0;    // d = 2: most points sharing one base row (band kernels' staging)
   DevBuf<i64> ext;        // internal row -> external row
   std::vector<i64> perm_h, inv_h;
@@ -1121,6 +1367,49 @@ void DskiOp::scatter(const double* v, double* u, int nrhs, cudaStream_t s) const
       else k_scatter_cells<D, T, false><<<grid, blk, 0, s>>>(vw, v, u, nrhs);
     });
     launched("dski scatter (cells)");
+    return;
+  }
+  if (d == 3 && variant == 7 && col3_units.p) {  // balanced units over the per-column sorted lists
+    GK_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * size_t(M) * nrhs, s));
+    const dim3 cblk(32, 8);
+    const dim3 cgrid(static_cast<unsigned>((col3_nunits + 7) / 8), static_cast<unsigned>((nrhs + 31) / 32));
+    if (T == 6) {
+      if (G) k_scatter_units3<6, true><<<cgrid, cblk, 0, s>>>(vw, col3_list.p, col3_start.p, col3_units.p, col3_nunits, v, u, nrhs);
+      else k_scatter_units3<6, false><<<cgrid, cblk, 0, s>>>(vw, col3_list.p, col3_start.p, col3_units.p, col3_nunits, v, u, nrhs);
+    } else {
+      if (G) k_scatter_units3<4, true><<<cgrid, cblk, 0, s>>>(vw, col3_list.p, col3_start.p, col3_units.p, col3_nunits, v, u, nrhs);
+      else k_scatter_units3<4, false><<<cgrid, cblk, 0, s>>>(vw, col3_list.p, col3_start.p, col3_units.p, col3_nunits, v, u, nrhs);
+    }
+    launched("dski scatter (d=3 balanced column units)");
+    return;
+  }
+  if (d == 3 && (variant == 0 || variant == 6) && col3_list.p) {  // per-column sorted point lists
+    const dim3 cblk(32, L3_WARPS);
+    const dim3 cgrid(static_cast<unsigned>((m[0] * m[1] + L3_WARPS - 1) / L3_WARPS), static_cast<unsigned>(col3_nseg),
+                     static_cast<unsigned>((nrhs + 31) / 32));
+    if (T == 6) {
+      if (G) k_scatter_list3<6, true><<<cgrid, cblk, 0, s>>>(vw, col3_list.p, col3_start.p, col3_seg.p, col3_nseg, col3_zseg, v, u, nrhs);
+      else k_scatter_list3<6, false><<<cgrid, cblk, 0, s>>>(vw, col3_list.p, col3_start.p, col3_seg.p, col3_nseg, col3_zseg, v, u, nrhs);
+    } else {
+      if (G) k_scatter_list3<4, true><<<cgrid, cblk, 0, s>>>(vw, col3_list.p, col3_start.p, col3_seg.p, col3_nseg, col3_zseg, v, u, nrhs);
+      else k_scatter_list3<4, false><<<cgrid, cblk, 0, s>>>(vw, col3_list.p, col3_start.p, col3_seg.p, col3_nseg, col3_zseg, v, u, nrhs);
+    }
+    launched("dski scatter (d=3 column lists)");
+    return;
+  }
+  if (d == 3 && (variant == 0 || variant == 5)) {  // node columns with a rolling window along the last axis
+    const int zseg = 12;
+    const dim3 cblk(32, 8);
+    const dim3 cgrid(static_cast<unsigned>((m[0] * m[1] + 7) / 8), static_cast<unsigned>((m[2] + zseg - 1) / zseg),
+                     static_cast<unsigned>((nrhs + 31) / 32));
+    if (T == 6) {
+      if (G) k_scatter_col3<6, true><<<cgrid, cblk, 0, s>>>(vw, v, u, nrhs, zseg);
+      else k_scatter_col3<6, false><<<cgrid, cblk, 0, s>>>(vw, v, u, nrhs, zseg);
+    } else {
+      if (G) k_scatter_col3<4, true><<<cgrid, cblk, 0, s>>>(vw, v, u, nrhs, zseg);
+      else k_scatter_col3<4, false><<<cgrid, cblk, 0, s>>>(vw, v, u, nrhs, zseg);
+    }
+    launched("dski scatter (d=3 node columns)");
     return;
   }
   GK_DISPATCH_DT(d, T, {
@@ -1374,6 +1663,78 @@ std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, cons
   }
   op->cell_start.upload(cstart.data(), cstart.size(), st);
   op->cell_start_h = cstart;
+  if (d == 3) {  // per node column (k0, k1): covering points ordered by (b2, t0, t1, point)
+    const int m0 = g.dims[0], m1 = g.dims[1], m2 = g.dims[2];
+    const int nb0 = op->nb[0], nb1 = op->nb[1], nb2 = op->nb[2];
+    const int ncol = m0 * m1;
+    std::vector<int> start(static_cast<size_t>(ncol) + 1, 0);
+    for (int k0 = 0; k0 < m0; ++k0)
+      for (int k1 = 0; k1 < m1; ++k1) {
+        int cnt = 0;
+        for (int t0 = 0; t0 < T; ++t0)
+          for (int t1 = 0; t1 < T; ++t1) {
+            const int b0 = k0 - t0, b1 = k1 - t1;
+            if (b0 < 0 || b0 >= nb0 || b1 < 0 || b1 >= nb1) continue;
+            const int c = (b0 * nb1 + b1) * nb2;
+            cnt += cstart[static_cast<size_t>(c + nb2)] - cstart[static_cast<size_t>(c)];
+          }
+        start[static_cast<size_t>(k0 * m1 + k1) + 1] = cnt;
+      }
+    for (int c = 0; c < ncol; ++c) start[static_cast<size_t>(c) + 1] += start[static_cast<size_t>(c)];
+    const int zseg = op->col3_zseg, nseg = (m2 + zseg - 1) / zseg;
+    std::vector<int2> list(static_cast<size_t>(start[static_cast<size_t>(ncol)]));
+    std::vector<int> segs(static_cast<size_t>(ncol) * nseg);
+    for (int k0 = 0; k0 < m0; ++k0)
+      for (int k1 = 0; k1 < m1; ++k1) {
+        const int col = k0 * m1 + k1;
+        int e = start[static_cast<size_t>(col)];
+        int sg = 0;
+        for (int b2 = 0; b2 < nb2; ++b2) {
+          while (sg < nseg && b2 >= std::max(0, sg * zseg - (T - 1))) segs[static_cast<size_t>(col) * nseg + sg++] = e;
+          for (int t0 = 0; t0 < T; ++t0)
+            for (int t1 = 0; t1 < T; ++t1) {
+              const int b0 = k0 - t0, b1 = k1 - t1;
+              if (b0 < 0 || b0 >= nb0 || b1 < 0 || b1 >= nb1) continue;
+              const int c = (b0 * nb1 + b1) * nb2 + b2;
+              for (int q = cstart[static_cast<size_t>(c)]; q < cstart[static_cast<size_t>(c) + 1]; ++q)
+                list[static_cast<size_t>(e++)] = make_int2(q, (b2 << 8) | (t0 << 4) | t1);
+            }
+        }
+        while (sg < nseg) segs[static_cast<size_t>(col) * nseg + sg++] = e;
+      }
+    // balanced units: ~64 entries with b2 in [za, zb) each (+ the T−1 halo cells)
+    std::vector<int4> units;
+    constexpr int kUnitEntries = 64;
+    for (int col = 0; col < ncol; ++col) {
+      const int e0 = start[static_cast<size_t>(col)], e1 = start[static_cast<size_t>(col) + 1];
+      if (e0 == e1) continue;
+      const int zfirst = list[static_cast<size_t>(e0)].y >> 8;
+      const int zend = std::min(m2, (list[static_cast<size_t>(e1 - 1)].y >> 8) + T);
+      int za = zfirst, ea = e0;  // ea: first entry with b2 >= za
+      while (za < zend) {
+        int eh = ea;  // first entry with b2 >= za - (T - 1) (the window's halo cells)
+        while (eh > e0 && (list[static_cast<size_t>(eh - 1)].y >> 8) >= za - (T - 1)) --eh;
+        int zb = za, eb = ea, cnt = 0;
+        while (zb < zend) {
+          int e = eb;
+          while (e < e1 && (list[static_cast<size_t>(e)].y >> 8) == zb) ++e;
+          if (cnt > 0 && cnt + (e - eb) > kUnitEntries) break;
+          cnt += e - eb;
+          eb = e;
+          ++zb;
+        }
+        units.push_back(make_int4(col, za, zb, eh));
+        za = zb;
+        ea = eb;
+      }
+    }
+    op->col3_nunits = int(units.size());
+    op->col3_units.upload(units.data(), units.size(), st);
+    op->col3_nseg = nseg;
+    op->col3_list.upload(list.data(), list.size(), st);
+    op->col3_start.upload(start.data(), start.size(), st);
+    op->col3_seg.upload(segs.data(), segs.size(), st);
+  }
   op->tvec.upload(tv.data(), tv.size(), st);
   op->tvec_dl.upload(tvd.data(), tvd.size(), st);
   op->toff.upload(op->toff_h.data(), op->toff_h.size(), st);

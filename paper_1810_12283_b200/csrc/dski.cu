@@ -607,6 +607,40 @@ __global__ void __launch_bounds__(256) k_scatter_units3(DskiView op, const int2*
   }
 }
 
+// d = 1 scatter: CTA per (node, RHS). The points covering node k (base cells
+// k−T+1 .. k) are ONE contiguous range of the sorted order; 256 threads stride
+// over it and reduce in a fixed shared-memory tree (deterministic). The pull
+// kernel gave a whole node to one thread — 100 threads for a 100-node leaf
+// grid (the D-SKIP leaves).
+template <int T, bool GRAD>
+__global__ void __launch_bounds__(256) k_scatter_1d(DskiView op, const double* __restrict__ v,
+                                                    double* __restrict__ u, int nrhs) {
+  __shared__ double red[256];
+  const int k = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+  const int nb = op.nb[0];
+  const int clo = max(0, k - (T - 1)), chi = min(nb - 1, k);
+  double acc = 0.0;
+  if (clo <= chi) {
+    const int s_lo = __ldg(op.cell_start + clo), s_hi = __ldg(op.cell_start + chi + 1);
+    const size_t gs = (size_t)op.n * nrhs;
+    for (int sp = s_lo + tid; sp < s_hi; sp += 256) {
+      const int tl = k - __ldg(op.base + sp).x;
+      const double2 a = __ldg(op.wd + (size_t)sp * T + tl);
+      const double* vs = v + (size_t)sp * nrhs + b;
+      acc += a.x * __ldg(vs);
+      if constexpr (GRAD) acc += a.y * __ldg(vs + gs);
+    }
+  }
+  red[tid] = acc;
+  __syncthreads();
+#pragma unroll
+  for (int w = 128; w > 0; w >>= 1) {
+    if (tid < w) red[tid] += red[tid + w];
+    __syncthreads();
+  }
+  if (tid == 0) u[(size_t)k * nrhs + b] = red[0];
+}
+
 template <int D, int T, bool GRAD>
 __global__ void __launch_bounds__(256) k_gather_lean(DskiView op, const double* __restrict__ w,
                                                      const double* __restrict__ v, double* __restrict__ out,
@@ -1367,6 +1401,18 @@ void DskiOp::scatter(const double* v, double* u, int nrhs, cudaStream_t s) const
       else k_scatter_cells<D, T, false><<<grid, blk, 0, s>>>(vw, v, u, nrhs);
     });
     launched("dski scatter (cells)");
+    return;
+  }
+  if (d == 1 && variant == 0) {
+    const dim3 g1(static_cast<unsigned>(M), static_cast<unsigned>(nrhs));
+    if (T == 6) {
+      if (G) k_scatter_1d<6, true><<<g1, 256, 0, s>>>(vw, v, u, nrhs);
+      else k_scatter_1d<6, false><<<g1, 256, 0, s>>>(vw, v, u, nrhs);
+    } else {
+      if (G) k_scatter_1d<4, true><<<g1, 256, 0, s>>>(vw, v, u, nrhs);
+      else k_scatter_1d<4, false><<<g1, 256, 0, s>>>(vw, v, u, nrhs);
+    }
+    launched("dski scatter (d=1 node blocks)");
     return;
   }
   if (d == 3 && variant == 7 && col3_units.p) {  // balanced units over the per-column sorted lists

@@ -1,3 +1,6 @@
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 // dskip.cu — the D-SKIP operator on B200 (reference dskip.cpp).
 //
 //   K∇_DSKIP v = (Q_A T_A Q_Aᵀ) ⊙ (Q_B T_B Q_Bᵀ) v + noise
@@ -1059,6 +1062,19 @@ struct PairOp final : Op {
 
 static std::unique_ptr<Factor> lanczos_factor(Op& op, i64 rank, std::uint64_t seed, cudaStream_t s) {
   // lanczos_lowrank (linalg.cpp:306-314): normalised gaussian_vector(N, seed) start
+  const bool prof = std::getenv("GK_BUILD_PROF") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  struct Done {
+    bool on;
+    std::chrono::steady_clock::time_point t0;
+    cudaStream_t s;
+    ~Done() {
+      if (!on) return;
+      cudaStreamSynchronize(s);
+      std::fprintf(stderr, "dskip build: lanczos factor %.2f ms\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+  } done{prof, t0, s};
   const i64 N = op.N;
   std::vector<double> q(static_cast<size_t>(N));
   gaussian(N, seed, 0, q.data());
@@ -1068,7 +1084,17 @@ static std::unique_ptr<Factor> lanczos_factor(Op& op, i64 rank, std::uint64_t se
   for (double& v : q) v /= nn;
   DevBuf<double> start(static_cast<size_t>(N)), Qc(static_cast<size_t>(N) * rank);
   start.upload(q.data(), q.size(), s);
+  if (prof) {
+    cudaStreamSynchronize(s);
+    std::fprintf(stderr, "dskip build: start vector %.2f ms\n",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  }
   LanczosBatch lb = lanczos_batch(op, start.p, 1, int(rank), {mix_seed(seed, 1)}, Qc.p, s);
+  if (prof) {
+    cudaStreamSynchronize(s);
+    std::fprintf(stderr, "dskip build: lanczos done %.2f ms (len %d)\n",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(), lb.len[0]);
+  }
   return factor_from_lanczos(Qc.p, N, lb, s);
 }
 

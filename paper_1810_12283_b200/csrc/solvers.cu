@@ -1767,6 +1767,7 @@ LanczosBatch lanczos_batch(Op& op, const double* start_int, int P, int steps,
   if (redo.empty()) return res;
   // Breakdown: exact re-run of the affected probes with host-side restarts.
   const int ns = int(redo.size());
+  if (prof) std::fprintf(stderr, "lanczos: %d of %d probes broke down; host-restart re-run\n", ns, P);
   DevBuf<int> idx(static_cast<size_t>(ns));
   GK_CUDA(cudaMemcpy(idx.p, redo.data(), sizeof(int) * ns, cudaMemcpyHostToDevice));
   DevBuf<double> start_s(static_cast<size_t>(N) * ns), Q_s(Q_out ? static_cast<size_t>(N) * ns * steps : 0);

@@ -458,12 +458,42 @@ def c5_dskip(args, world, rank, local, dist):
     ms = float(t.item())
     flops = 4.0 * N * ra * rb * nrhs
     peak = gk.dmma_peak_tflops(local)
+    # C5 solve (BASELINE: rank-100 pivoted Cholesky, PCG + SLQ with 64 RHS per rank)
+    solve = None
+    if not args.no_c5_solve:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        M = gk.Preconditioner.from_pivchol(op, gk.pivoted_cholesky(op, 100, kernel_part=True))
+        torch.cuda.synchronize()
+        t_pre = time.perf_counter() - t0
+        Bc = np.column_stack([gk.stacked_targets(y, dY, y.mean()) if rank == 0 else
+                              gk.rademacher_vector(N, 0, 1000 + rank * nrhs)] +
+                             [gk.rademacher_vector(N, 0, 1000 + rank * nrhs + p) for p in range(1, nrhs)])
+        Bd = torch.from_numpy(np.ascontiguousarray(Bc.T)).to(dev)
+        Xd = torch.empty_like(Bd)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        its, conv = gk.cg_dev(op, Bd.data_ptr(), Xd.data_ptr(), nrhs, 1e-4, 1000, M, stream=st.cuda_stream)
+        torch.cuda.synchronize()
+        t_pcg = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        slq = gk.slq_logdet(op, nrhs, 50, 0, 0.5e-4, probe_offset=rank * nrhs)
+        t_slq = time.perf_counter() - t0
+        tt = torch.tensor([t_pre, t_pcg, t_slq], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_pre, t_pcg, t_slq = [float(v) for v in tt.tolist()]
+        solve = {"precond_build_s": t_pre, "pcg_s": t_pcg, "slq_s": t_slq, "pcg_plus_slq_s": t_pcg + t_slq,
+                 "pcg_iterations_max": int(max(its)), "pcg_converged": int(np.sum(conv)),
+                 "slq_probes_per_rank": nrhs, "slq_steps": 50,
+                 "note": "tol 1e-4, max 1000 iterations (sigma = 1e-2: the columns do not converge within "
+                         "1000, as at C2); times are max over ranks"}
     achieved = world * flops / (ms * 1e-3) / 1e12
     return {"workload": "C5: D-SKIP d=6 n=10000 (N=70000) product SE ell=0.3 sigma=1e-2, rank 30, "
                         "100-node 1-D grids, 64 RHS per rank",
             "parallelism": f"rhs-shard x{world}", "scaling": "weak", "ms_per_mvm": ms,
             "value": world * N * nrhs / (ms * 1e-3), "unit": UNIT, "build_s": build_s,
-            "factor_ranks": ranks, "gpu_launches_per_mvm": int(launches),
+            "factor_ranks": ranks, "gpu_launches_per_mvm": int(launches), "solve": solve,
             "roofline": {"bound": "tensor (fp64 DMMA)", "achieved": achieved / world, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / world / peak,
                          "flops_per_mvm": flops, "flops_formula": "SURVEY 8(d): 4*N*r_A*r_B*B",
@@ -533,6 +563,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 grid-slab sharded MVM measurement")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 D-SKIP MVM measurement")
+    ap.add_argument("--no-c5-solve", action="store_true", help="skip the C5 D-SKIP PCG/SLQ solve")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl != "reference":
         args.warmup = 3

@@ -520,6 +520,57 @@ __global__ void k_gram_partial(const double* __restrict__ X, i64 N, int k, doubl
   for (int o = tid; o < k * k; o += blockDim.x) partial[(i64)blockIdx.x * k * k + o] = acc[o];
 }
 
+// Gram partials for larger ranks: CTA = one 64×64 output tile (upper tiles
+// only) × one row range; 16-row column slices staged in shared memory; each
+// thread owns a 4×4 block of outputs. partial[blockIdx.x][j][l] (full k×k
+// layout, the same as k_gram_partial's, so k_pc_fin reduces both).
+constexpr int GT = 64;
+__global__ void __launch_bounds__(256) k_gram_tile(const double* __restrict__ X, i64 N, int k,
+                                                  double* __restrict__ partial) {
+  const int tj = blockIdx.y, tl = blockIdx.z;
+  if (tj > tl) return;
+  __shared__ double xa[16][GT + 1], xb[16][GT + 1];
+  const int j0 = tj * GT, l0 = tl * GT, tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+  i64 r0, r1;
+  row_range(N, r0, r1);
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+  for (i64 rt = r0; rt < r1; rt += 16) {
+    __syncthreads();
+    for (int e = tid; e < 16 * GT; e += 256) {
+      const int rr = e / GT, cc = e % GT;
+      const i64 r = rt + rr;
+      const bool ok = r < r1;
+      xa[rr][cc] = ok && j0 + cc < k ? X[r * k + j0 + cc] : 0.0;
+      xb[rr][cc] = ok && l0 + cc < k ? X[r * k + l0 + cc] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int rr = 0; rr < 16; ++rr) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) av[a] = xa[rr][ty * 4 + a];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) bv[c] = xb[rr][tx * 4 + c];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[a][c] += av[a] * bv[c];
+    }
+  }
+  double* out = partial + (i64)blockIdx.x * k * k;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int j = j0 + ty * 4 + a, l = l0 + tx * 4 + c;
+      if (j < k && l < k) out[(i64)j * k + l] = acc[a][c];
+    }
+}
+
 // G = D^{-1/2} F: F is [k][N] col-major (internal rows) -> G [N][k] row-major
 __global__ void k_scale_transpose(const double* __restrict__ F, const double* __restrict__ noise, i64 N, int k,
                                   double* __restrict__ G, double* __restrict__ dinv) {
@@ -1333,16 +1384,22 @@ std::unique_ptr<Precond> precond_build(const double* F_int, i64 N, i64 k, const 
   launched("precond scale");
   DevBuf<double> part(static_cast<size_t>(RB) * k * k), gram(static_cast<size_t>(k * k)), Rinv_d(static_cast<size_t>(k * k));
   const size_t shg = sizeof(double) * (PC_RT * k + k * k);
-  if (shg > 227 * 1024) fail(GK_ERR_UNSUPPORTED, "preconditioner rank too large for the Gram kernel");
-  set_smem((const void*)k_gram_partial, shg);
+  const bool tiled = k > 64;  // the k×k shared accumulator stops fitting near k = 160
+  if (!tiled) set_smem((const void*)k_gram_partial, shg);
+  const unsigned ntile = static_cast<unsigned>((k + GT - 1) / GT);
   std::vector<double> gh(static_cast<size_t>(k * k)), R(static_cast<size_t>(k * k)), Rinv(static_cast<size_t>(k * k)), Q2(static_cast<size_t>(k * k));
   // Q2 tracks the bottom block (initially I_k)
   for (i64 j = 0; j < k; ++j) Q2[static_cast<size_t>(j * k + j)] = 1.0;
   const double* cur = G.p;
   double* nxt = Q.p;
   for (int pass = 0; pass < 2; ++pass) {
-    k_gram_partial<<<RB, RT, shg, s>>>(cur, N, int(k), part.p);
-    launched("precond gram");
+    if (tiled) {
+      k_gram_tile<<<dim3(RB, ntile, ntile), 256, 0, s>>>(cur, N, int(k), part.p);
+      launched("precond gram (tiled)");
+    } else {
+      k_gram_partial<<<RB, RT, shg, s>>>(cur, N, int(k), part.p);
+      launched("precond gram");
+    }
     k_pc_fin<<<fin_blocks(int(k * k)), 256, 0, s>>>(part.p, int(k * k), gram.p);
     launched("precond gram fin");
     GK_CUDA(cudaMemcpyAsync(gh.data(), gram.p, sizeof(double) * k * k, cudaMemcpyDeviceToHost, s));

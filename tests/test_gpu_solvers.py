@@ -96,6 +96,22 @@ def test_preconditioner_vs_long_double_oracle():
         gk.Preconditioner(np.ones((5, 1)), 0.0)
 
 
+@pytest.mark.parametrize("k", [64, 65, 200, 300])
+def test_preconditioner_high_rank_vs_dense_inverse(k):
+    """Ranks past the shared-memory Gram accumulator (C4 uses rank 200): the
+    tiled Gram path, apply and quadratic against the dense (σ²I + FFᵀ)⁻¹."""
+    n, sigma = 700, 0.3
+    F = np.random.default_rng(k).standard_normal((n, k)) / np.sqrt(k)
+    P = gk.Preconditioner(F, sigma)
+    assert P.rank() == k
+    M = sigma ** 2 * np.eye(n) + F @ F.T
+    for s in range(3):
+        b = np.random.default_rng(300 + s).standard_normal(n)
+        want = np.linalg.solve(M, b)
+        assert np.linalg.norm(P.apply(b) - want) <= 1e-9 * np.linalg.norm(want)
+        assert abs(P.quadratic(b) - b @ want) <= 1e-9 * abs(b @ want)
+
+
 def test_slq_exact_for_scaled_identity():
     r1 = gk.slq_logdet(gk.DenseOperator(np.eye(64)), 4, 10, 42)
     assert abs(r1.logdet) <= 1e-12

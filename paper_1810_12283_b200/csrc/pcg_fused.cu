@@ -752,6 +752,215 @@ __global__ void __launch_bounds__(PV_THREADS, 2) k_pcg_vec2(PcgVecArgs a) {
   pv_stamp(a, 6, prof_on);
 }
 
+// ---------------------------------------------------------------- single RHS
+// nrhs = 1 (C4: N = 450,000, rank 200): the Q1 products are GEMVs, so the
+// DMMA tiles of v1/v2 would waste 7 of 8 columns and the row staging exposes
+// its latency. Here a warp reads one Q1 row (K ≤ 256 doubles, coalesced) per
+// step; T lives in the lanes' registers (lane l holds j = l, l+32, …); the
+// apply reduces each row with shuffles. Same phases as v2: r·z = ‖c‖² − ‖T‖²,
+// p updated directly, three grid barriers; Q1 is streamed twice (the bound).
+constexpr int R1_KQ = 8;  // K ≤ 32·R1_KQ
+__global__ void __launch_bounds__(PV_THREADS, 2) k_pcg_vec_r1(PcgVecArgs a) {
+  __shared__ double red[PV_THREADS];
+  __shared__ double colv[2];
+  __shared__ double tred[PV_THREADS / 32][32 * R1_KQ];
+  __shared__ int sh_flags[3];  // act, upd, its
+  __shared__ double sh_vals[4];  // alpha, beta, rz, bnorm
+  const int K = a.q1 != nullptr ? a.k : 0;
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const i64 per = (a.N + gridDim.x - 1) / gridDim.x;
+  const i64 r0 = min(a.N, (i64)blockIdx.x * per), r1 = min(a.N, r0 + per);
+  PcgState& st = a.st;
+  double* part0 = a.part;
+  double* part1 = a.part + gridDim.x;  // [cta][2]
+  if (tid == 0) {
+    sh_flags[0] = st.active[0];
+    sh_flags[2] = st.its[0];
+    sh_vals[2] = st.rz[0];
+    sh_vals[3] = st.bnorm[0];
+  }
+  // A: pAp partials
+  double acc = 0.0;
+  for (i64 r = r0 + tid; r < r1; r += PV_THREADS) acc += a.P[r] * a.AP[r];
+  block_cols(acc, 1, red, part0);
+  grid_allreduce_cols(part0, 1, colv, a.bar);
+  // B: alpha
+  if (tid == 0) {
+    int u = 0, ac = sh_flags[0], it = sh_flags[2];
+    double al = 0.0;
+    if (ac) {
+      if (it >= st.maxit || colv[0] <= 0.0) {
+        ac = 0;
+      } else {
+        al = sh_vals[2] / colv[0];
+        u = 1;
+        it += 1;
+      }
+    }
+    sh_flags[0] = ac;
+    sh_flags[1] = u;
+    sh_flags[2] = it;
+    sh_vals[0] = al;
+    if (blockIdx.x == 0) {
+      st.active[0] = ac;
+      st.its[0] = it;
+      st.upd[0] = u;
+      st.alpha[0] = al;
+    }
+  }
+  __syncthreads();
+  const bool u = sh_flags[1] != 0;
+  const double al = sh_vals[0];
+  // C: x, r update; ||r||², ||c||² partials (c = D^{-1/2} r)
+  double arr = 0.0, acc_c = 0.0;
+  for (i64 r = r0 + tid; r < r1; r += PV_THREADS) {
+    double rn = a.R[r];
+    if (u) {
+      a.X[r] += al * a.P[r];
+      rn -= al * a.AP[r];
+      a.R[r] = rn;
+      arr += rn * rn;
+    }
+    const double c = K > 0 ? a.dinv[r] * rn : rn;
+    acc_c += c * c;
+  }
+  __syncthreads();  // R rows of this CTA written before the T pass reads them
+  // T partial = Q1ᵀ c: warp per row, lanes over j
+  double tq[R1_KQ];
+#pragma unroll
+  for (int q = 0; q < R1_KQ; ++q) tq[q] = 0.0;
+  if (K > 0) {
+    constexpr int RR = 4;  // rows per warp step: their loads are in flight together
+    for (i64 rb = r0 + warp; rb < r1; rb += RR * (PV_THREADS / 32)) {
+      double qv[RR][R1_KQ], cv[RR];
+#pragma unroll
+      for (int u = 0; u < RR; ++u) {
+        const i64 r = rb + u * (PV_THREADS / 32);
+        const bool ok = r < r1;
+        cv[u] = ok ? a.dinv[r] * a.R[r] : 0.0;
+        const double* qr = a.q1 + (ok ? r : r0) * K;
+#pragma unroll
+        for (int q = 0; q < R1_KQ; ++q) {
+          const int j = lane + 32 * q;
+          qv[u][q] = j < K ? __ldcs(qr + j) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < RR; ++u)
+#pragma unroll
+        for (int q = 0; q < R1_KQ; ++q) tq[q] += qv[u][q] * cv[u];
+    }
+#pragma unroll
+    for (int q = 0; q < R1_KQ; ++q) tred[warp][lane + 32 * q] = tq[q];
+  }
+  __syncthreads();
+  if (K > 0)
+    for (int j = tid; j < K; j += PV_THREADS) {
+      double s = 0.0;
+      for (int w = 0; w < PV_THREADS / 32; ++w) s += tred[w][j];
+      a.tpart[(i64)j * gridDim.x + blockIdx.x] = s;
+    }
+  // rr | cc partials
+  __syncthreads();
+  red[tid] = arr;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int k = 0; k < PV_THREADS; ++k) s += red[k];
+    part1[(i64)blockIdx.x * 2] = s;
+  }
+  __syncthreads();
+  red[tid] = acc_c;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int k = 0; k < PV_THREADS; ++k) s += red[k];
+    part1[(i64)blockIdx.x * 2 + 1] = s;
+  }
+  grid_allreduce_cols(part1, 2, colv, a.bar);  // also a full barrier (tpart visible)
+  // D: convergence
+  if (tid == 0 && sh_flags[1]) {
+    const double relres = sqrt(colv[0]) / sh_vals[3];
+    const bool done = relres <= st.tol;
+    if (done) sh_flags[0] = 0;
+    if (blockIdx.x == 0) {
+      st.hist[(i64)sh_flags[2]] = relres;
+      if (done) {
+        st.conv[0] = 1;
+        st.active[0] = 0;
+      }
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && tid == 0) *st.nactive = sh_flags[0];
+  if (K > 0) {
+    for (int o = blockIdx.x * (PV_THREADS / 32) + warp; o < K; o += gridDim.x * (PV_THREADS / 32)) {
+      const double v = warp_sum_cols(a.tpart + (i64)o * gridDim.x, gridDim.x, 1, 0);
+      if (lane == 0) a.T[o] = v;
+    }
+    grid_sync(a.bar);
+#pragma unroll
+    for (int q = 0; q < R1_KQ; ++q) {
+      const int j = lane + 32 * q;
+      tq[q] = j < K ? __ldcg(a.T + j) : 0.0;
+    }
+  }
+  // F: rz_new = ||c||² − ||T||², beta
+  if (tid == 0 && sh_flags[0]) {
+    double t2 = 0.0;
+    for (int j = 0; j < K; ++j) {
+      const double t = __ldcg(a.T + j);
+      t2 += t * t;
+    }
+    const double rzn = colv[1] - t2;
+    sh_vals[1] = rzn / sh_vals[2];
+    if (blockIdx.x == 0) {
+      st.beta[0] = sh_vals[1];
+      st.rz[0] = rzn;
+    }
+  }
+  __syncthreads();
+  if (!sh_flags[0]) return;
+  const double be = sh_vals[1];
+  // EG: p = D^{-1/2}(c − Q1 T) + beta p, warp per row
+  if (K > 0) {
+    constexpr int RR = 4;
+    for (i64 rb = r0 + warp; rb < r1; rb += RR * (PV_THREADS / 32)) {
+      double sv[RR];
+#pragma unroll
+      for (int u = 0; u < RR; ++u) {
+        const i64 r = rb + u * (PV_THREADS / 32);
+        const double* qr = a.q1 + (r < r1 ? r : r0) * K;
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < R1_KQ; ++q) {
+          const int j = lane + 32 * q;
+          if (j < K) s += __ldcs(qr + j) * tq[q];
+        }
+        sv[u] = s;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int u = 0; u < RR; ++u) sv[u] += __shfl_xor_sync(0xffffffffu, sv[u], o);
+      if (lane < RR) {
+        double s = sv[0];
+#pragma unroll
+        for (int u = 1; u < RR; ++u)
+          if (lane == u) s = sv[u];
+        const i64 r = rb + lane * (PV_THREADS / 32);
+        if (r < r1) {
+          const double di = a.dinv[r];
+          const double z = di * (di * a.R[r] - s);
+          a.P[r] = z + be * a.P[r];
+        }
+      }
+    }
+  } else {
+    for (i64 r = r0 + tid; r < r1; r += PV_THREADS) a.P[r] = a.R[r] + be * a.P[r];
+  }
+}
+
 }  // namespace
 
 bool pcg_vec_supported(int nrhs, int k) {
@@ -793,15 +1002,23 @@ static void pcg_vec_prepare_impl(PcgVecPlan& p, i64 N, int nrhs, int k, int devi
       p.smem = smem2;
     }
   }
-  raise_smem_limit(p.v2 ? (const void*)k_pcg_vec2 : (const void*)k_pcg_vec, p.smem);
+  // single right-hand side: streamed GEMVs (k_pcg_vec_r1) instead of DMMA tiles
+  p.r1 = nrhs == 1 && k <= 32 * R1_KQ && g_tuning.pcg_fused.load() != 3;
+  if (p.r1) {
+    p.v2 = false;
+    p.smem = 0;
+  }
+  raise_smem_limit(p.r1 ? (const void*)k_pcg_vec_r1 : p.v2 ? (const void*)k_pcg_vec2 : (const void*)k_pcg_vec, p.smem);
   if (p.v2)
     GK_CUDA(cudaFuncSetAttribute((const void*)k_pcg_vec2, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  int(cudaSharedmemCarveoutMaxShared)));
   GK_CUDA(cudaFuncSetAttribute((const void*)k_pcg_vec, cudaFuncAttributePreferredSharedMemoryCarveout,
                                int(cudaSharedmemCarveoutMaxShared)));
   int occ = 0;
-  GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p.v2 ? k_pcg_vec2 : k_pcg_vec, PV_THREADS, p.smem));
+  GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p.r1 ? k_pcg_vec_r1 : p.v2 ? k_pcg_vec2 : k_pcg_vec,
+                                                        PV_THREADS, p.smem));
   if (occ < 1) fail(GK_ERR_RUNTIME, "fused PCG step does not fit on an SM");
+  if (p.r1 && occ < 2) p.r1 = false;
   if (p.v2 && occ < 2) {  // v2's row ranges were sized for two CTAs per SM
     return pcg_vec_prepare_impl(p, N, nrhs, k, device, false);
   }
@@ -815,7 +1032,7 @@ static void pcg_vec_prepare_impl(PcgVecPlan& p, i64 N, int nrhs, int k, int devi
   p.rctr.alloc(2);
   GK_CUDA(cudaMemset(p.rctr.p, 0, 2 * sizeof(unsigned long long)));
   if (std::getenv("GK_PCG_PROF")) {
-    std::fprintf(stderr, "[pcg_vec] %s grid %d (occ %d) smem %zu rch %d k %d nrhs %d\n", p.v2 ? "v2" : "v1", p.grid,
+    std::fprintf(stderr, "[pcg_vec] %s grid %d (occ %d) smem %zu rch %d k %d nrhs %d\n", p.r1 ? "r1" : p.v2 ? "v2" : "v1", p.grid,
                  occ, p.smem, p.rch, k, nrhs);
     p.prof.alloc(size_t(p.grid) * 16);
     GK_CUDA(cudaMemset(p.prof.p, 0, sizeof(unsigned long long) * p.prof.n));
@@ -841,7 +1058,8 @@ void pcg_vec_launch(PcgVecPlan& p, PcgVecArgs a, cudaStream_t s) {
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (p.v2) GK_CUDA(cudaLaunchKernelEx(&cfg, k_pcg_vec2, a));
+  if (p.r1) GK_CUDA(cudaLaunchKernelEx(&cfg, k_pcg_vec_r1, a));
+  else if (p.v2) GK_CUDA(cudaLaunchKernelEx(&cfg, k_pcg_vec2, a));
   else GK_CUDA(cudaLaunchKernelEx(&cfg, k_pcg_vec, a));
   launched("pcg fused vector step");
 }

@@ -46,6 +46,7 @@ struct PcgVecArgs {
 
 struct PcgVecPlan {
   bool v2 = false;  // rows-resident variant (k_pcg_vec2)
+  bool r1 = false;  // single-RHS streamed-GEMV variant (k_pcg_vec_r1)
   int grid = 0;
   int rch = 1;
   size_t smem = 0;

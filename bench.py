@@ -405,7 +405,26 @@ def c4_slab(args, world, rank, local, dist):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    return {"workload": "C4: D-SKI d=2 n=150000 (N=450000) grid 400x400 SE ell=0.02 sigma=1e-2, 1 RHS",
+    solve = None
+    if rank == 0 and not args.no_c4_solve:  # BASELINE C4: rank-200 pivoted Cholesky + PCG (one GPU, unsharded)
+        op1 = gk.DskiOperator(gk.KernelSpec(0.02, 1.0), grid, X, (1e-2, 1e-2), device=local)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        M = gk.Preconditioner.from_pivchol(op1, gk.pivoted_cholesky(op1, 200, kernel_part=True))
+        torch.cuda.synchronize()
+        t_pre = time.perf_counter() - t0
+        bd = torch.from_numpy(np.ascontiguousarray(b)).to(dev)
+        xd = torch.empty_like(bd)
+        gk.cg_dev(op1, bd.data_ptr(), xd.data_ptr(), 1, 1e-4, 5, M)  # plans / graphs built outside the timing
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        its, conv = gk.cg_dev(op1, bd.data_ptr(), xd.data_ptr(), 1, 1e-4, 1000, M)
+        torch.cuda.synchronize()
+        t_pcg = time.perf_counter() - t0
+        solve = {"precond_build_s": t_pre, "pcg_s": t_pcg, "pcg_iterations": int(its[0]),
+                 "pcg_converged": int(conv[0]), "us_per_iteration": t_pcg / max(1, int(its[0])) * 1e6,
+                 "parallelism": "1 GPU (the PCG itself is not slab-sharded)"}
+    return {"workload": "C4: D-SKI d=2 n=150000 (N=450000) grid 400x400 SE ell=0.02 sigma=1e-2, 1 RHS", "solve": solve,
             "parallelism": f"grid-slab x{world} (NCCL all-reduce of the grid vector per MVM)",
             "scaling": "strong", "ms_per_mvm": ms, "value": sop.size() * nrhs / (ms * 1e-3),
             "unit": UNIT, "local_points": int(sop.mine.size), "build_s": build_s,
@@ -564,6 +583,7 @@ def main():
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 grid-slab sharded MVM measurement")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 D-SKIP MVM measurement")
     ap.add_argument("--no-c5-solve", action="store_true", help="skip the C5 D-SKIP PCG/SLQ solve")
+    ap.add_argument("--no-c4-solve", action="store_true", help="skip the C4 rank-200 preconditioned PCG")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl != "reference":
         args.warmup = 3

@@ -34,6 +34,10 @@ t3 = t()
 its, conv = gk.cg_dev(op, Bd.data_ptr(), Xd.data_ptr(), 1, 1e-12, 50, M)
 t4 = t()
 print(f"C4 N={N}: pivchol(200) {t1-t0:.3f} s, precond build {t2-t1:.3f} s, PCG {(t4-t3)/50*1e6:.1f} us/iteration", flush=True)
+t5 = t()
+its, conv = gk.cg_dev(op, Bd.data_ptr(), Xd.data_ptr(), 1, 1e-4, 1000, M)
+t6 = t()
+print(f"C4 PCG tol 1e-4, its {its[0]}: {(t6-t5)/max(1, its[0])*1e6:.1f} us/iteration", flush=True)
 if os.environ.get("PROFILE"):
     torch.cuda.profiler.start()
     gk.cg_dev(op, Bd.data_ptr(), Xd.data_ptr(), 1, 1e-12, 3, M)

@@ -1225,7 +1225,7 @@ PcgResult pcg_internal(Op& op, Precond* M, const double* B, double* X, int nrhs,
   };
 
   int* nact_h = nullptr;
-  GK_CUDA(cudaMallocHost(&nact_h, sizeof(int)));
+  GK_CUDA(cudaMallocHost(&nact_h, 2 * sizeof(int)));
   GK_CUDA(cudaMemcpyAsync(nact_h, st.nactive, sizeof(int), cudaMemcpyDeviceToHost, s));
   GK_CUDA(cudaStreamSynchronize(s));
   if (*nact_h > 0 && maxit > 0) {
@@ -1245,16 +1245,25 @@ PcgResult pcg_internal(Op& op, Precond* M, const double* B, double* X, int nrhs,
     g_launches.fetch_sub(nodes);
     cudaGraphExec_t exec;
     GK_CUDA(cudaGraphInstantiate(&exec, graph, 0));
-    int launches = 0;
+    // Lag-one polling: graph j is queued before the host waits for graph
+    // j−1's active-column count, so the GPU never drains between graphs.
+    // Iterations after convergence are no-ops for the converged columns (at
+    // most one extra graph runs).
     const int max_launches = (maxit + ITER - 1) / ITER + 1;
-    while (launches < max_launches) {
+    cudaEvent_t evs[2];
+    for (auto& e : evs) GK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (int j = 0; j < max_launches; ++j) {
       GK_CUDA(cudaGraphLaunch(exec, s));
       g_launches.fetch_add(nodes);
-      ++launches;
-      GK_CUDA(cudaMemcpyAsync(nact_h, st.nactive, sizeof(int), cudaMemcpyDeviceToHost, s));
-      GK_CUDA(cudaStreamSynchronize(s));
-      if (*nact_h == 0) break;
+      GK_CUDA(cudaMemcpyAsync(nact_h + (j & 1), st.nactive, sizeof(int), cudaMemcpyDeviceToHost, s));
+      GK_CUDA(cudaEventRecord(evs[j & 1], s));
+      if (j >= 1) {
+        GK_CUDA(cudaEventSynchronize(evs[(j - 1) & 1]));
+        if (nact_h[(j - 1) & 1] == 0) break;
+      }
     }
+    GK_CUDA(cudaStreamSynchronize(s));
+    for (auto e : evs) cudaEventDestroy(e);
     cudaGraphExecDestroy(exec);
     cudaGraphDestroy(graph);
   }

@@ -1235,7 +1235,13 @@ std::unique_ptr<Op> make_dskip(const gk_kernel& k, const double* X, i64 n, int d
       leaf.dir = dir;
       leaf.N = N;
       leaf.n_value = n;
+      const auto tl0 = std::chrono::steady_clock::now();
       leaf.core = make_dski_profile(k1, g1, col.data(), n, 0.0, 0.0, 0, dir >= 0 ? 1 : 0, device, pass);
+      if (std::getenv("GK_BUILD_PROF")) {
+        cudaDeviceSynchronize();
+        std::fprintf(stderr, "dskip build: leaf core %.2f ms\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl0).count());
+      }
       const std::uint64_t seed = mix_seed(cfg.seed, pass == 0 ? std::uint64_t(j) : std::uint64_t(100 + j));
       auto f = lanczos_factor(leaf, rank, seed, s);
       (pass == 0 ? op->factors : op->dlog).push_back(std::move(f));

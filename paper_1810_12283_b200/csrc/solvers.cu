@@ -1767,7 +1767,8 @@ LanczosBatch lanczos_batch(Op& op, const double* start_int, int P, int steps,
                  std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count());
     tp0 = std::chrono::steady_clock::now();
   }
-  for (int k = 0; k < steps; ++k) {
+  auto run_steps = [&](int k_begin) {
+  for (int k = k_begin; k < steps; ++k) {
     const double* qk = Q + (i64)k * blk;
     op.mvm(qk, W.p, P, s);
     const bool last = k + 1 >= steps;
@@ -1803,11 +1804,116 @@ LanczosBatch lanczos_batch(Op& op, const double* start_int, int P, int steps,
     k_lz_next<<<blocks_for(blk), 256, 0, s>>>(W.p, d_bdiv, d_flag, N, P, Q + (i64)(k + 1) * blk);
     launched("lanczos next");
   }
+  };
+  run_steps(0);
+  std::vector<int> kb(static_cast<size_t>(P)), len(static_cast<size_t>(P), steps), restarted(static_cast<size_t>(P), 0);
+  GK_CUDA(cudaMemcpyAsync(kb.data(), d_kbreak, sizeof(int) * P, cudaMemcpyDeviceToHost, s));
+  GK_CUDA(cudaStreamSynchronize(s));
+  // Breakdowns (β ≤ 1e-12·scale): rounds in increasing step order. The probes
+  // that broke at step K get the reference's deflating restart on the host
+  // (linalg.cpp:46-69: fresh Gaussian directions from mix_seed(seed,
+  // 7777 + count), two-pass orthogonalisation against their basis, accepted
+  // when the norm exceeds 1e-8·sqrt(N)); the device loop then resumes at K+1
+  // with only those probes live. A probe with no acceptable direction stops
+  // with K+1 steps.
+  std::vector<std::uint64_t> rcount(static_cast<size_t>(P), 0);
+  std::vector<i64> ext_h;
+  for (int round = 0;; ++round) {
+    int K = steps;
+    for (int p = 0; p < P; ++p)
+      if (kb[static_cast<size_t>(p)] >= 0) K = std::min(K, kb[static_cast<size_t>(p)]);
+    if (K >= steps) break;
+    if (prof) std::fprintf(stderr, "lanczos: restart round %d at step %d\n", round, K);
+    if (ext_h.empty() && op.d_ext_of_int()) {
+      ext_h.resize(static_cast<size_t>(N));
+      GK_CUDA(cudaMemcpy(ext_h.data(), op.d_ext_of_int(), sizeof(i64) * N, cudaMemcpyDeviceToHost));
+    }
+    std::vector<int> live_h(static_cast<size_t>(P), 0), kb_new(kb);
+    std::vector<int> cols;
+    std::vector<double> rext(static_cast<size_t>(N)), rv(static_cast<size_t>(N) * P, 0.0);
+    std::vector<double> zeros(static_cast<size_t>(P), 0.0), ones(static_cast<size_t>(P), 1.0), nrm(static_cast<size_t>(P));
+    std::vector<int> flags(static_cast<size_t>(P), 0);
+    for (int p = 0; p < P; ++p) {
+      if (kb[static_cast<size_t>(p)] != K) continue;
+      restarted[static_cast<size_t>(p)] = 1;
+      kb_new[static_cast<size_t>(p)] = -1;
+      bool found = false;
+      for (int attempt = 0; attempt < 8 && !found; ++attempt) {
+        gaussian(N, mix_seed(restart_seeds[static_cast<size_t>(p)], 7777 + rcount[static_cast<size_t>(p)]++),
+                 std::uint64_t(attempt), rext.data());
+        std::fill(rv.begin(), rv.end(), 0.0);
+        for (i64 r = 0; r < N; ++r)
+          rv[static_cast<size_t>(r * P + p)] = rext[static_cast<size_t>(ext_h.empty() ? r : ext_h[static_cast<size_t>(r)])];
+        // two-pass orthogonalisation against q_0..q_K on the device (passes B, C, D with α = 0)
+        GK_CUDA(cudaMemcpyAsync(W.p, rv.data(), sizeof(double) * blk, cudaMemcpyHostToDevice, s));
+        GK_CUDA(cudaMemcpyAsync(d_alpha, zeros.data(), sizeof(double) * P, cudaMemcpyHostToDevice, s));
+        const int k1 = K + 1;
+        for (int j0 = 0; j0 < k1; j0 += JB) {
+          const int jc = std::min(JB, k1 - j0);
+          k_lz_b<<<RB, RT, 0, s>>>(W.p, nullptr, d_bprev, Q, Q, j0, jc, N, P, nullptr, pg.p);
+          launched("lanczos restart projection 1");
+          k_lz_fin_b<<<lz_fin_blocks(jc * P), 256, 0, s>>>(nullptr, pg.p, j0, jc, -1, P, d_alpha, C1.p);
+          launched("lanczos restart projection 1 fin");
+        }
+        for (int j0 = 0; j0 < k1; j0 += JB) {
+          const int jc = std::min(JB, k1 - j0);
+          k_lz_c<<<RB, RT, 0, s>>>(W.p, Q, d_alpha, Q, C1.p, k1, j0, jc, N, P, pg.p);
+          launched("lanczos restart update 1 + projection 2");
+          k_lz_fin<<<lz_fin_blocks(jc * P), 256, 0, s>>>(pg.p, jc * P, C2.p + (i64)j0 * P);
+          launched("lanczos restart projection 2 fin");
+        }
+        k_lz_d<<<RB, RT, 0, s>>>(W.p, Q, C2.p, k1, N, P, pa.p);
+        launched("lanczos restart update 2 + norm");
+        k_lz_fin<<<lz_fin_blocks(P), 256, 0, s>>>(pa.p, P, d_nrm);
+        launched("lanczos restart norm fin");
+        GK_CUDA(cudaMemcpyAsync(nrm.data(), d_nrm, sizeof(double) * P, cudaMemcpyDeviceToHost, s));
+        GK_CUDA(cudaStreamSynchronize(s));
+        const double rn = std::sqrt(nrm[static_cast<size_t>(p)]);
+        if (rn > 1e-8 * std::sqrt(double(N))) {
+          std::vector<double> bd(ones);
+          bd[static_cast<size_t>(p)] = rn;
+          std::fill(flags.begin(), flags.end(), 0);
+          flags[static_cast<size_t>(p)] = 1;
+          GK_CUDA(cudaMemcpyAsync(d_bdiv, bd.data(), sizeof(double) * P, cudaMemcpyHostToDevice, s));
+          GK_CUDA(cudaMemcpyAsync(d_flag, flags.data(), sizeof(int) * P, cudaMemcpyHostToDevice, s));
+          k_lz_next<<<blocks_for(blk), 256, 0, s>>>(W.p, d_bdiv, d_flag, N, P, Q + (i64)(K + 1) * blk);
+          launched("lanczos restart vector");
+          GK_CUDA(cudaStreamSynchronize(s));  // pageable sources
+          found = true;
+        }
+      }
+      if (found) {
+        live_h[static_cast<size_t>(p)] = 1;
+        cols.push_back(p);
+      } else {
+        len[static_cast<size_t>(p)] = K + 1;  // stays frozen
+      }
+    }
+    kb = kb_new;
+    if (cols.empty() || K + 1 >= steps) continue;  // nothing to resume (or the restart step was the last)
+    // device state for the resumed probes: q_{K+1}, β_K = 0, no β_prev term; every other probe frozen
+    {
+      std::vector<double> zero(static_cast<size_t>(P), 0.0), bh_row(static_cast<size_t>(P));
+      GK_CUDA(cudaMemcpyAsync(bh_row.data(), d_bhist + (i64)K * P, sizeof(double) * P, cudaMemcpyDeviceToHost, s));
+      GK_CUDA(cudaStreamSynchronize(s));
+      for (int p : cols) bh_row[static_cast<size_t>(p)] = 0.0;  // the reference records β = 0 at a restart
+      std::vector<int> mkb(static_cast<size_t>(P));
+      for (int p = 0; p < P; ++p) mkb[static_cast<size_t>(p)] = kb[static_cast<size_t>(p)];
+      GK_CUDA(cudaMemcpyAsync(d_bhist + (i64)K * P, bh_row.data(), sizeof(double) * P, cudaMemcpyHostToDevice, s));
+      GK_CUDA(cudaMemcpyAsync(d_live, live_h.data(), sizeof(int) * P, cudaMemcpyHostToDevice, s));
+      GK_CUDA(cudaMemcpyAsync(d_kbreak, mkb.data(), sizeof(int) * P, cudaMemcpyHostToDevice, s));
+      GK_CUDA(cudaMemcpyAsync(d_bprev, zero.data(), sizeof(double) * P, cudaMemcpyHostToDevice, s));
+      GK_CUDA(cudaStreamSynchronize(s));  // pageable sources
+    }
+    run_steps(K + 1);
+    std::vector<int> kb_dev(static_cast<size_t>(P));
+    GK_CUDA(cudaMemcpyAsync(kb_dev.data(), d_kbreak, sizeof(int) * P, cudaMemcpyDeviceToHost, s));
+    GK_CUDA(cudaStreamSynchronize(s));
+    for (int p : cols) kb[static_cast<size_t>(p)] = kb_dev[static_cast<size_t>(p)];
+  }
   std::vector<double> ah(static_cast<size_t>(steps) * P), bh(static_cast<size_t>(steps) * P);
-  std::vector<int> kb(static_cast<size_t>(P));
   GK_CUDA(cudaMemcpyAsync(ah.data(), d_ahist, sizeof(double) * ah.size(), cudaMemcpyDeviceToHost, s));
   GK_CUDA(cudaMemcpyAsync(bh.data(), d_bhist, sizeof(double) * bh.size(), cudaMemcpyDeviceToHost, s));
-  GK_CUDA(cudaMemcpyAsync(kb.data(), d_kbreak, sizeof(int) * P, cudaMemcpyDeviceToHost, s));
   GK_CUDA(cudaStreamSynchronize(s));
   if (prof)
     std::fprintf(stderr, "lanczos: steps %.2f ms\n",
@@ -1815,43 +1921,18 @@ LanczosBatch lanczos_batch(Op& op, const double* start_int, int P, int steps,
   LanczosBatch res;
   res.P = P;
   res.steps = steps;
-  res.len.assign(static_cast<size_t>(P), steps);
+  res.len = len;
   res.alpha.assign(static_cast<size_t>(P), {});
   res.beta.assign(static_cast<size_t>(P), {});
-  res.breakdown.assign(static_cast<size_t>(P), 0);
-  std::vector<int> redo;
+  res.breakdown = restarted;
   for (int p = 0; p < P; ++p) {
-    if (kb[static_cast<size_t>(p)] >= 0) {
-      redo.push_back(p);
-      continue;
-    }
+    const int L = len[static_cast<size_t>(p)];
     auto& a = res.alpha[static_cast<size_t>(p)];
     auto& b = res.beta[static_cast<size_t>(p)];
-    for (int k = 0; k < steps; ++k) a.push_back(ah[static_cast<size_t>(k) * P + p]);
-    for (int k = 0; k + 1 < steps; ++k) b.push_back(bh[static_cast<size_t>(k) * P + p]);
-  }
-  if (redo.empty()) return res;
-  // Breakdown: exact re-run of the affected probes with host-side restarts.
-  const int ns = int(redo.size());
-  if (prof) std::fprintf(stderr, "lanczos: %d of %d probes broke down; host-restart re-run\n", ns, P);
-  DevBuf<int> idx(static_cast<size_t>(ns));
-  GK_CUDA(cudaMemcpy(idx.p, redo.data(), sizeof(int) * ns, cudaMemcpyHostToDevice));
-  DevBuf<double> start_s(static_cast<size_t>(N) * ns), Q_s(Q_out ? static_cast<size_t>(N) * ns * steps : 0);
-  k_cols_move<<<blocks_for(N * ns), 256, 0, s>>>(start_int, P, start_s.p, ns, idx.p, ns, N, 1);
-  launched("lanczos redo gather");
-  std::vector<std::uint64_t> seeds_s;
-  for (int p : redo) seeds_s.push_back(restart_seeds[static_cast<size_t>(p)]);
-  LanczosBatch rs = lanczos_batch_sync(op, start_s.p, ns, steps, seeds_s, Q_out ? Q_s.p : nullptr, s);
-  if (Q_out) {
-    k_cols_move<<<blocks_for(N * steps * ns), 256, 0, s>>>(Q_s.p, ns, Q_out, P, idx.p, ns, N * steps, 0);
-    launched("lanczos redo scatter");
-  }
-  for (int t = 0; t < ns; ++t) {
-    const size_t p = static_cast<size_t>(redo[static_cast<size_t>(t)]);
-    res.len[p] = rs.len[static_cast<size_t>(t)];
-    res.alpha[p] = rs.alpha[static_cast<size_t>(t)];
-    res.beta[p] = rs.beta[static_cast<size_t>(t)];
-    res.breakdown[p] = rs.breakdown[static_cast<size_t>(t)];
+    for (int k = 0; k < L; ++k) a.push_back(ah[static_cast<size_t>(k) * P + p]);
+    for (int k = 0; k + 1 < L; ++k) b.push_back(bh[static_cast<size_t>(k) * P + p]);
+    if (L < steps && Q_out)  // a probe that stopped early: its remaining basis columns are zero
+      GK_CUDA(cudaMemset2DAsync(Q_out + (i64)L * blk + p, sizeof(double) * P, 0, sizeof(double), size_t(N) * (steps - L), s));
   }
   GK_CUDA(cudaStreamSynchronize(s));
   return res;

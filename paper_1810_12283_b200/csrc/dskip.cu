@@ -737,6 +737,108 @@ __global__ void __launch_bounds__(128, 3) k_had_expand3(const double* __restrict
     }
 }
 
+// ---------------------------------------------------------------- small batches (nrhs ≤ 2)
+// One or two right-hand sides (the merge-tree Lanczos of the build, single
+// vector MVMs): the Khatri–Rao GEMMs degenerate to GEMVs and the 16-column
+// DMMA tiles would waste ≥ 8×. Contraction: CTA = row range, thread t owns
+// m = t, t+256, … (register accumulators), rows staged 32 at a time; fixed-
+// order reduction of the CTA partials (k_had_reduce). Expansion: thread per
+// row, C in shared memory, T_B folded into B's QT as in v3.
+constexpr int HS_MMAX = 16;  // m per thread (ra·rb ≤ 256·HS_MMAX)
+template <int NR>
+__global__ void __launch_bounds__(256) k_had_contract_small(const double* __restrict__ QA, int ra,
+                                                            const double* __restrict__ QB, int rb,
+                                                            const double* __restrict__ V, i64 N, int nrhs,
+                                                            double* __restrict__ partial) {
+  __shared__ double qa[32][33], qb[32][33], vs[32][NR];
+  const int M = ra * rb, tid = threadIdx.x;
+  const i64 per = (N + gridDim.x - 1) / gridDim.x;
+  const i64 r0 = min(N, (i64)blockIdx.x * per), r1 = min(N, r0 + per);
+  int kk[HS_MMAX], ll[HS_MMAX];
+  double acc[HS_MMAX][NR];
+#pragma unroll
+  for (int q = 0; q < HS_MMAX; ++q) {
+    const int m = tid + 256 * q;
+    kk[q] = m < M ? m / rb : 0;
+    ll[q] = m < M ? m - kk[q] * rb : 0;
+#pragma unroll
+    for (int b = 0; b < NR; ++b) acc[q][b] = 0.0;
+  }
+  for (i64 rs = r0; rs < r1; rs += 32) {
+    const int nr = int(min((i64)32, r1 - rs));
+    __syncthreads();
+    for (int e = tid; e < 32 * 32; e += 256) {
+      const int r = e / 32, c = e % 32;
+      qa[r][c] = r < nr && c < ra ? QA[(rs + r) * ra + c] : 0.0;
+      qb[r][c] = r < nr && c < rb ? QB[(rs + r) * rb + c] : 0.0;
+    }
+    for (int e = tid; e < 32 * NR; e += 256) {
+      const int r = e / NR, b = e % NR;
+      vs[r][b] = r < nr && b < nrhs ? V[(rs + r) * nrhs + b] : 0.0;
+    }
+    __syncthreads();
+    for (int r = 0; r < nr; ++r) {
+#pragma unroll
+      for (int q = 0; q < HS_MMAX; ++q) {
+        if (tid + 256 * q >= M) break;
+        const double z = qa[r][kk[q]] * qb[r][ll[q]];
+#pragma unroll
+        for (int b = 0; b < NR; ++b) acc[q][b] += z * vs[r][b];
+      }
+    }
+  }
+  double* out = partial + (i64)blockIdx.x * M * nrhs;
+#pragma unroll
+  for (int q = 0; q < HS_MMAX; ++q) {
+    const int m = tid + 256 * q;
+    if (m < M)
+#pragma unroll
+      for (int b = 0; b < NR; ++b)
+        if (b < nrhs) out[(i64)m * nrhs + b] = acc[q][b];
+  }
+}
+
+template <int NR>
+__global__ void __launch_bounds__(256) k_had_expand_small(const double* __restrict__ QTA, int ra,
+                                                          const double* __restrict__ QBT, int rb,
+                                                          const double* __restrict__ C, i64 N, int nrhs,
+                                                          const double* __restrict__ v, i64 n_value, double nv2,
+                                                          double ng2, int accumulate, double* __restrict__ out) {
+  extern __shared__ double cs[];  // [ra·rb][NR]
+  const int M = ra * rb, tid = threadIdx.x;
+  for (int e = tid; e < M * NR; e += 256) cs[e] = (e % NR) < nrhs ? C[(e / NR) * nrhs + e % NR] : 0.0;
+  __syncthreads();
+  const i64 row = (i64)blockIdx.x * 256 + tid;
+  if (row >= N) return;
+  const double* a = QTA + row * ra;
+  const double* bq = QBT + row * rb;
+  double res[NR];
+#pragma unroll
+  for (int b = 0; b < NR; ++b) res[b] = 0.0;
+  for (int k = 0; k < ra; ++k) {
+    double sk[NR];
+#pragma unroll
+    for (int b = 0; b < NR; ++b) sk[b] = 0.0;
+    const double* ck = cs + (k * rb) * NR;
+    for (int l = 0; l < rb; ++l) {
+      const double w = __ldg(bq + l);
+#pragma unroll
+      for (int b = 0; b < NR; ++b) sk[b] += w * ck[l * NR + b];
+    }
+    const double ak = __ldg(a + k);
+#pragma unroll
+    for (int b = 0; b < NR; ++b) res[b] += ak * sk[b];
+  }
+#pragma unroll
+  for (int b = 0; b < NR; ++b) {
+    if (b >= nrhs) break;
+    const i64 idx = row * nrhs + b;
+    double val = res[b];
+    if (v) val += (row < n_value ? nv2 : ng2) * v[idx];
+    out[idx] = accumulate ? out[idx] + val : val;
+  }
+}
+
 // fp64 tensor-core peak probe: 8 independent DMMA chains per warp, no memory
 // traffic — the denominator of the D-SKIP roofline, measured on the running box.
 __global__ void __launch_bounds__(128) k_dmma_peak(int iters, double* sink) {
@@ -933,9 +1035,34 @@ static void hadamard_pair3_launch(const Factor& A, const Factor& B, const double
   }
 }
 
+template <int NR>
+static void hadamard_small_launch(const Factor& A, const Factor& B, const double* v, int nrhs, double* out,
+                                  bool accumulate, const double* noise_v, i64 n_value, double nv2, double ng2,
+                                  HadScratch& ws, cudaStream_t s) {
+  const i64 N = A.N;
+  const int M = A.r * B.r;
+  const int chunks = int(std::max<i64>(1, std::min<i64>(296, (N + 63) / 64)));
+  ws.partial.reserve(static_cast<size_t>(chunks) * M * nrhs);
+  ws.C.reserve(static_cast<size_t>(M) * nrhs);
+  k_had_contract_small<NR><<<chunks, 256, 0, s>>>(A.Q.p, A.r, B.Q.p, B.r, v, N, nrhs, ws.partial.p);
+  launched("hadamard contract (small batch)");
+  k_had_reduce<<<blocks_for((i64)M * nrhs), 256, 0, s>>>(ws.partial.p, chunks, M, nrhs, ws.C.p);
+  launched("hadamard reduce");
+  const size_t se = sizeof(double) * size_t(M) * NR;
+  raise_smem_limit((const void*)k_had_expand_small<NR>, se);
+  k_had_expand_small<NR><<<static_cast<unsigned>((N + 255) / 256), 256, se, s>>>(
+      A.QT.p, A.r, B.QT.p, B.r, ws.C.p, N, nrhs, noise_v, n_value, nv2, ng2, accumulate ? 1 : 0, out);
+  launched("hadamard expand (small batch)");
+}
+
 static bool hadamard_pair3(const Factor& A, const Factor& B, const double* v, int nrhs, double* out, bool accumulate,
                            const double* noise_v, i64 n_value, double nv2, double ng2, HadScratch& ws,
                            cudaStream_t s) {
+  if (nrhs <= 2 && g_tuning.dskip.load() == 0 && A.r <= 32 && B.r <= 32 && A.r * B.r <= 256 * HS_MMAX) {
+    if (nrhs == 1) hadamard_small_launch<1>(A, B, v, nrhs, out, accumulate, noise_v, n_value, nv2, ng2, ws, s);
+    else hadamard_small_launch<2>(A, B, v, nrhs, out, accumulate, noise_v, n_value, nv2, ng2, ws, s);
+    return true;
+  }
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (g_tuning.dskip.load() != 0 || (A.r & 1) || (B.r & 1) || (nrhs & 1) || !al16(v) || !al16(out) ||
       (noise_v && !al16(noise_v)) || !al16(A.Q.p) || !al16(A.QT.p) || !al16(B.Q.p) || !al16(B.QT.p))

@@ -1,3 +1,4 @@
+#include <type_traits>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -398,6 +399,301 @@ __global__ void __launch_bounds__(128) k_pc_proj_mma(const double* __restrict__ 
         if (j0 < k && bb < nrhs) out[(i64)j0 * nrhs + bb] = acc[ii][jn][e];
       }
     }
+  }
+}
+
+// ---------------------------------------------------------------- preconditioner GEMMs v3
+// The rank-k projection T = Q1ᵀ D^{-1/2} r and the apply
+// z = D^{-1/2}(D^{-1/2} r − Q1 T) as fp64 tensor-core GEMMs in the shape of the
+// D-SKIP Khatri–Rao kernels: rows arrive by per-row TMA bulk copies
+// (cp.async.bulk + mbarrier rings, one issuing warp), shared strides ≡ 4
+// (mod 16) doubles, warp tiles of 16 (m or rows) × all RHS. Needs an even rank
+// and an even RHS count (16-byte rows); other shapes use the kernels above.
+__host__ __device__ __forceinline__ int p3_pad(int x) { return x + ((4 - x % 16) + 16) % 16; }
+__device__ __forceinline__ unsigned p3_su32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void p3_mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"(p3_su32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void p3_arrive_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(p3_su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void p3_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared.b64 _, [%0];\n" ::"r"(p3_su32(b)) : "memory");
+}
+__device__ __forceinline__ void p3_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nP3W_%=:\nmbarrier.try_wait.parity.shared.b64 P1, [%0], %1;\n@!P1 bra P3W_%=;\n}\n" ::"r"(
+          p3_su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void p3_bulk(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   p3_su32(dst)),
+               "l"(src), "r"(bytes), "r"(p3_su32(b))
+               : "memory");
+}
+
+constexpr int P3_BK = 16, P3_NS = 3;   // projection: rows per stage, ring depth
+constexpr int P3_MC = 8, P3_NSE = 4;   // apply: m per T stage, ring depth
+
+// partial[chunk][m][b] = Σ_{rows in chunk} Q1[row][m] d[row] r[row][b]
+template <int NJ>
+__global__ void __launch_bounds__(128, 4) k_pc_proj3(const double* __restrict__ q1, int k,
+                                                     const double* __restrict__ dinv, const double* __restrict__ R,
+                                                     i64 N, int nrhs, i64 rows_per_chunk,
+                                                     double* __restrict__ partial) {
+  extern __shared__ __align__(16) double p3_sm[];
+  constexpr int BWC = 16 * NJ, SV = BWC + ((4 - BWC % 16) + 16) % 16, JT = 2 * NJ;
+  const int SA = p3_pad(k);
+  const int stage_d = P3_BK * (SA + SV + 1);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(p3_sm + P3_NS * stage_d);
+  unsigned long long* empty = full + P3_NS;
+  const int m0 = blockIdx.x * 64, b0 = blockIdx.y * BWC;
+  const int bw = min(BWC, nrhs - b0);
+  const i64 r_begin = (i64)blockIdx.z * rows_per_chunk;
+  const i64 r_end = min(N, r_begin + rows_per_chunk);
+  const int nst = r_end > r_begin ? int((r_end - r_begin + P3_BK - 1) / P3_BK) : 0;
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32, g = lane / 4, t4 = lane % 4;
+  const int wm = warp * 16;
+  if (tid == 0) {
+    for (int s = 0; s < P3_NS; ++s) p3_mbar_init(full + s, 32), p3_mbar_init(empty + s, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  // warp 0 fills a stage: lanes 0..15 Q1 row + r row, lane 16 the 16 D^{-1/2} values
+  auto issue = [&](int st) {
+    const i64 rs = r_begin + (i64)st * P3_BK;
+    const int nr = int(min((i64)P3_BK, r_end - rs));
+    double* base = p3_sm + (st % P3_NS) * stage_d;
+    unsigned long long* bar = full + st % P3_NS;
+    if (lane < P3_BK) {
+      double* qd = base + lane * SA;
+      double* vd = base + P3_BK * SA + lane * SV;
+      if (lane < nr) {
+        p3_arrive_tx(bar, unsigned(k + bw) * 8u);
+        p3_bulk(qd, q1 + (rs + lane) * k, unsigned(k) * 8u, bar);
+        p3_bulk(vd, R + (rs + lane) * nrhs + b0, unsigned(bw) * 8u, bar);
+      } else {
+        for (int c = 0; c < SA; ++c) qd[c] = 0.0;
+        for (int c = 0; c < SV; ++c) vd[c] = 0.0;
+        p3_arrive(bar);
+      }
+    } else if (lane == P3_BK) {
+      double* dd = base + P3_BK * (SA + SV);
+      if (nr == P3_BK) {
+        p3_arrive_tx(bar, P3_BK * 8u);
+        p3_bulk(dd, dinv + rs, P3_BK * 8u, bar);
+      } else {
+        for (int c = 0; c < P3_BK; ++c) dd[c] = c < nr ? dinv[rs + c] : 0.0;
+        p3_arrive(bar);
+      }
+    } else {
+      p3_arrive(bar);
+    }
+  };
+  int mi[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) mi[i] = min(m0 + wm + 8 * i + g, k - 1);
+  double acc[2][JT][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < JT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  if (warp == 0)
+    for (int s = 0; s < min(P3_NS, nst); ++s) issue(s);
+  for (int it = 0; it < nst; ++it) {
+    const int sb = it % P3_NS;
+    const unsigned ph = (it / P3_NS) & 1;
+    p3_wait(full + sb, ph);
+    const double* A1 = p3_sm + sb * stage_d;
+    const double* V1 = A1 + P3_BK * SA;
+    const double* D1 = V1 + P3_BK * SV;
+#pragma unroll
+    for (int kk = 0; kk < P3_BK; kk += 4) {
+      const int row = kk + t4;
+      const double dr = D1[row];
+      double af[2], bf[JT];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) af[i] = A1[row * SA + mi[i]] * dr;
+#pragma unroll
+      for (int j = 0; j < JT; ++j) bf[j] = V1[row * SV + 8 * j + g];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < JT; ++j) dmma_f64(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncwarp();
+    if (lane == 0) p3_arrive(empty + sb);
+    if (warp == 0 && it + P3_NS < nst) {
+      p3_wait(empty + sb, ph);
+      issue(it + P3_NS);
+    }
+  }
+  double* out = partial + (i64)blockIdx.z * k * nrhs;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < JT; ++j) {
+      const int m = m0 + wm + 8 * i + g, bl = 8 * j + 2 * t4;
+      if (m < k && bl < bw)
+        *reinterpret_cast<double2*>(out + (i64)m * nrhs + b0 + bl) = make_double2(acc[i][j][0], acc[i][j][1]);
+    }
+}
+
+// z = d (d r − Q1 T) for 64 rows × 16·NJ columns; r·z partials per (row block, column)
+template <int NJ>
+__global__ void __launch_bounds__(128, 3) k_pc_apply3(const double* __restrict__ q1, int k,
+                                                      const double* __restrict__ dinv,
+                                                      const double* __restrict__ R, const double* __restrict__ T,
+                                                      i64 N, int nrhs, double* __restrict__ Z,
+                                                      double* __restrict__ partial_rz) {
+  extern __shared__ __align__(16) double p3_sm[];
+  constexpr int BWC = 16 * NJ, SV = BWC + ((4 - BWC % 16) + 16) % 16, JT = 2 * NJ;
+  const int SA = p3_pad(k);
+  double* Qs = p3_sm;                 // [64][SA]
+  double* Rs = Qs + 64 * SA;          // [64][SV]
+  double* Ds = Rs + 64 * SV;          // [64]
+  double* Ts = Ds + 64;               // [P3_NSE][P3_MC][SV]
+  double* red = Ts + P3_NSE * P3_MC * SV;  // [4][BWC] r·z per warp
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(red + 4 * BWC);
+  unsigned long long* empty = full + P3_NSE;
+  unsigned long long* qbar = empty + P3_NSE;
+  const i64 i0 = (i64)blockIdx.x * 64;
+  const int b0 = blockIdx.y * BWC;
+  const int bw = min(BWC, nrhs - b0);
+  const int nr = int(min((i64)64, N - i0));
+  const int nch = (k + P3_MC - 1) / P3_MC;
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32, g = lane / 4, t4 = lane % 4;
+  const int wi = warp * 16;
+  if (tid == 0) {
+    for (int s = 0; s < P3_NSE; ++s) p3_mbar_init(full + s, 32), p3_mbar_init(empty + s, 4);
+    p3_mbar_init(qbar, 128);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  {  // the CTA's Q1 rows (threads 0..63) and r rows (64..127), once; D^{-1/2} by plain loads
+    const int row = tid & 63;
+    if (row < nr) {
+      const bool a = tid < 64;
+      const unsigned bytes = (a ? k : bw) * 8u;
+      p3_arrive_tx(qbar, bytes);
+      p3_bulk(a ? Qs + row * SA : Rs + row * SV, a ? q1 + (i0 + row) * k : R + (i0 + row) * nrhs + b0, bytes, qbar);
+    } else {
+      p3_arrive(qbar);
+    }
+    if (tid < 64) Ds[tid] = tid < nr ? dinv[i0 + tid] : 0.0;
+  }
+  auto issue = [&](int c) {  // warp 0; lane L < MC moves T row c·MC + L
+    const int m = c * P3_MC + lane;
+    unsigned long long* bar = full + c % P3_NSE;
+    double* dst = Ts + (c % P3_NSE) * P3_MC * SV + lane * SV;
+    if (lane < P3_MC && m < k) {
+      p3_arrive_tx(bar, bw * 8u);
+      p3_bulk(dst, T + (i64)m * nrhs + b0, bw * 8u, bar);
+    } else {
+      if (lane < P3_MC)
+        for (int c2 = 0; c2 < SV; ++c2) dst[c2] = 0.0;
+      p3_arrive(bar);
+    }
+  };
+  if (warp == 0)
+    for (int c = 0; c < min(P3_NSE, nch); ++c) issue(c);
+  double acc[2][JT][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < JT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  p3_wait(qbar, 0);
+  __syncthreads();  // Ds (plain stores) visible
+  const double* qrow[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) qrow[i] = Qs + min(wi + 8 * i + g, 63) * SA;
+  for (int c = 0; c < nch; ++c) {
+    const int sb = c % P3_NSE;
+    const unsigned ph = (c / P3_NSE) & 1;
+    p3_wait(full + sb, ph);
+    const double* T1 = Ts + sb * P3_MC * SV;
+#pragma unroll
+    for (int kk = 0; kk < P3_MC; kk += 4) {
+      const int m = c * P3_MC + kk + t4;
+      const int mc = m < k ? m : 0;  // m past k meets a zero T row
+      double af[2], bf[JT];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) af[i] = qrow[i][mc];
+#pragma unroll
+      for (int j = 0; j < JT; ++j) bf[j] = T1[(kk + t4) * SV + 8 * j + g];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < JT; ++j) dmma_f64(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncwarp();
+    if (lane == 0) p3_arrive(empty + sb);
+    if (warp == 0 && c + P3_NSE < nch) {
+      p3_wait(empty + sb, ph);
+      issue(c + P3_NSE);
+    }
+  }
+  // epilogue: z, and r·z summed over this warp's 16 rows per column (fixed order)
+  double rz[JT][2];
+#pragma unroll
+  for (int j = 0; j < JT; ++j) rz[j][0] = rz[j][1] = 0.0;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < JT; ++j) {
+      const int rl = wi + 8 * i + g, bl = 8 * j + 2 * t4;
+      if (rl < nr && bl < bw) {
+        const double d = Ds[rl];
+        const double2 rv = *reinterpret_cast<const double2*>(Rs + rl * SV + bl);
+        const double z0 = d * (d * rv.x - acc[i][j][0]), z1 = d * (d * rv.y - acc[i][j][1]);
+        *reinterpret_cast<double2*>(Z + (i0 + rl) * nrhs + b0 + bl) = make_double2(z0, z1);
+        rz[j][0] += rv.x * z0;
+        rz[j][1] += rv.y * z1;
+      }
+    }
+  if (partial_rz) {
+#pragma unroll
+    for (int j = 0; j < JT; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double v = rz[j][e];
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);  // over g (lanes with equal t4)
+        if (g == 0) red[warp * BWC + 8 * j + 2 * t4 + e] = v;
+      }
+    __syncthreads();
+    for (int bl = tid; bl < bw; bl += 128)
+      partial_rz[(i64)blockIdx.x * nrhs + b0 + bl] = ((red[bl] + red[BWC + bl]) + red[2 * BWC + bl]) + red[3 * BWC + bl];
+  }
+}
+
+// out[o] = Σ_c partial[c][o]: block = 32 outputs × 8 chunk groups (chunk c in
+// group c mod 8, loads 8 in flight), groups added in order (deterministic)
+__global__ void __launch_bounds__(256) k_pc_reduce(const double* __restrict__ partial, int chunks, int nout,
+                                                   double* __restrict__ out) {
+  __shared__ double sm[8][33];
+  const int lo = threadIdx.x & 31, gq = threadIdx.x >> 5;
+  const int o = blockIdx.x * 32 + lo;
+  double s = 0.0;
+  if (o < nout) {
+    int c = gq;
+    for (; c + 56 < chunks; c += 64) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcs(partial + (i64)(c + 8 * u) * nout + o);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; c < chunks; c += 8) s += __ldcs(partial + (i64)c * nout + o);
+  }
+  sm[gq][lo] = s;
+  __syncthreads();
+  if (gq == 0 && o < nout) {
+    double t = 0.0;
+    for (int q = 0; q < 8; ++q) t += sm[q][lo];
+    out[o] = t;
   }
 }
 
@@ -1311,6 +1607,18 @@ void Precond::ensure(int nrhs) {
     set_smem((const void*)k_pc_proj_mma, proj_mma_smem(nrhs));
     set_smem((const void*)k_pc_apply_mma, apply_mma_smem(nrhs));
   }
+  if ((k & 1) == 0 && k <= 256) {  // v3 kernels (precond_apply3)
+    auto lim = [&](auto nj, const void* fp, const void* fa) {
+      constexpr int NJ = decltype(nj)::value;
+      constexpr int BWC = 16 * NJ, SV = BWC + ((4 - BWC % 16) + 16) % 16;
+      raise_smem_limit(fp, sizeof(double) * size_t(P3_NS) * P3_BK * (p3_pad(int(k)) + SV + 1) + 16 * P3_NS);
+      raise_smem_limit(fa, sizeof(double) * (size_t(64) * (p3_pad(int(k)) + SV + 1) + size_t(P3_NSE) * P3_MC * SV +
+                                             4 * BWC) + 16 * P3_NSE + 8);
+    };
+    lim(std::integral_constant<int, 1>{}, (const void*)k_pc_proj3<1>, (const void*)k_pc_apply3<1>);
+    lim(std::integral_constant<int, 2>{}, (const void*)k_pc_proj3<2>, (const void*)k_pc_apply3<2>);
+    lim(std::integral_constant<int, 4>{}, (const void*)k_pc_proj3<4>, (const void*)k_pc_apply3<4>);
+  }
 }
 
 bool Precond::mma_ok(int nrhs) const {
@@ -1333,9 +1641,44 @@ size_t Precond::apply_mma_smem(int nrhs) const {
   return sizeof(double) * size_t(kp * (np + 8) + 64 * std::max(kp + 4, np + 8));  // Qs, reused for r·z
 }
 
+template <int NJ>
+static int precond_apply3(Precond& M, const double* r, double* z, int nrhs, cudaStream_t s, double* partial_rz) {
+  const int k = int(M.k);
+  const i64 N = M.N;
+  constexpr int BWC = 16 * NJ, SV = BWC + ((4 - BWC % 16) + 16) % 16;
+  const size_t sp = sizeof(double) * size_t(P3_NS) * P3_BK * (p3_pad(k) + SV + 1) + 16 * P3_NS;
+  const size_t sa = sizeof(double) * (size_t(64) * (p3_pad(k) + SV + 1) + size_t(P3_NSE) * P3_MC * SV + 4 * BWC) +
+                    16 * P3_NSE + 8;
+  // shared-memory limits were raised by ensure() (outside any graph capture)
+  const int mt = (k + 63) / 64, bt = (nrhs + BWC - 1) / BWC;
+  const int per_sm = int(std::max<size_t>(1, std::min<size_t>(4, (227 * 1024) / (sp + 1024))));
+  int sms = 0, dev = 0;
+  GK_CUDA(cudaGetDevice(&dev));
+  GK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  int chunks = int(std::max<i64>(1, std::min<i64>(std::min<i64>(RB, std::max(1, per_sm) * sms / (mt * bt)),
+                                                  (N + 4 * P3_BK - 1) / (4 * P3_BK))));
+  const i64 rpc = ((N + chunks - 1) / chunks + P3_BK - 1) / P3_BK * P3_BK;
+  chunks = int((N + rpc - 1) / rpc);
+  k_pc_proj3<NJ><<<dim3(mt, bt, chunks), 128, sp, s>>>(M.q1.p, k, M.dinv.p, r, N, nrhs, rpc, M.partial.p);
+  launched("precond proj (DMMA v3)");
+  k_pc_reduce<<<(k * nrhs + 31) / 32, 256, 0, s>>>(M.partial.p, chunks, k * nrhs, M.t.p);
+  launched("precond reduce");
+  const unsigned nb = static_cast<unsigned>((N + 63) / 64);
+  k_pc_apply3<NJ><<<dim3(nb, bt), 128, sa, s>>>(M.q1.p, k, M.dinv.p, r, M.t.p, N, nrhs, z, partial_rz);
+  launched("precond apply (DMMA v3)");
+  return int(nb);
+}
+
 int Precond::apply(const double* r, double* z, int nrhs, cudaStream_t s, double* partial_rz) {
   ensure(nrhs);  // no-op once reserved (and before any graph capture)
-  if (mma_ok(nrhs) && g_tuning.precond.load() == 0) {
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (g_tuning.precond.load() == 0 && (k & 1) == 0 && (nrhs & 1) == 0 && k <= 256 && nrhs >= 4 && al16(r) &&
+      al16(z) && al16(q1.p) && al16(dinv.p)) {
+    if (nrhs > 32) return precond_apply3<4>(*this, r, z, nrhs, s, partial_rz);
+    if (nrhs > 16) return precond_apply3<2>(*this, r, z, nrhs, s, partial_rz);
+    return precond_apply3<1>(*this, r, z, nrhs, s, partial_rz);
+  }
+  if (mma_ok(nrhs) && (g_tuning.precond.load() == 0 || g_tuning.precond.load() == 3)) {
     k_pc_proj_mma<<<RB, 128, proj_mma_smem(nrhs), s>>>(r, dinv.p, q1.p, N, int(k), nrhs, proj_rch(nrhs),
                                                        partial.p);
     launched("precond proj (DMMA)");

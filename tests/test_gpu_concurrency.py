@@ -1,0 +1,50 @@
+"""Concurrent host threads on one operator (SURVEY §8(b) Threading: the
+reference calls op.mvm concurrently from OpenMP threads in slq_logdet and
+trace_estimate, linalg.cpp:222,264). Every C-ABI call on a handle is
+serialised by the handle's mutex and uses handle-owned scratch; results must
+equal the single-threaded ones exactly."""
+import threading
+
+import numpy as np
+import pytest
+
+import paper_1810_12283_b200 as gk
+
+pytestmark = pytest.mark.gpu
+
+
+def test_concurrent_mvm_solve_and_slq_on_one_operator():
+    X, y, dY = gk.make_dataset(1, 0)
+    grid = gk.Grid.cover(X, 1e-4, 3, 60)
+    op = gk.DskiOperator(gk.KernelSpec(0.15, 1.0), grid, X, (0.1, 0.1))
+    N = op.size()
+    rng = np.random.default_rng(7)
+    Vs = [rng.standard_normal((N, c)) for c in (1, 4, 7, 32)]
+    want_mvm = [op.mvm(V) for V in Vs]
+    P = gk.Preconditioner.from_pivchol(op, gk.pivoted_cholesky(op, 20, kernel_part=True))
+    b = gk.stacked_targets(y, dY, y.mean())
+    want_x = gk.cg(op, b, 1e-8, 2000, P).x
+    want_ld = gk.slq_logdet(op, 8, 25, 0, 0.005).logdet
+    errors, results = [], {}
+
+    def worker(t):
+        try:
+            for rep in range(3):
+                for i, V in enumerate(Vs):
+                    out = op.mvm(V)
+                    if not np.array_equal(out, want_mvm[i]):
+                        errors.append(("mvm", t, rep, i, float(np.abs(out - want_mvm[i]).max())))
+            results[("cg", t)] = gk.cg(op, b, 1e-8, 2000, P).x
+            results[("slq", t)] = gk.slq_logdet(op, 8, 25, 0, 0.005).logdet
+        except Exception as e:  # surfaced below
+            errors.append(("exception", t, repr(e)))
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(4)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors[:5]
+    for t in range(4):
+        assert np.array_equal(results[("cg", t)], want_x)
+        assert results[("slq", t)] == want_ld

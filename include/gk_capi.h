@@ -52,7 +52,8 @@ const char* gk_version(void);
 /* Kernel-variant selection for tuning/A-B timing (process-wide). Keys:
  * "scatter", "gather", "toeplitz", "precond" (0 = default choice), "fused"
  * (1 = disable the one-launch 2-D MVM), "pcg_fused" (0/1 = one-launch PCG
- * vector step where supported, 2 = separate kernels), "dskip" (D-SKIP Hadamard
+ * vector step where supported, 2 = separate kernels, 3 = vector step v1,
+ * 5 = persistent MVM + vector step for the 2-D D-SKI operator), "dskip" (D-SKIP Hadamard
  * kernels: 0 = TMA-ring DMMA, 3 = cp.async DMMA, 1 = first generation),
  * "e2e_chunk" (gk_op_mvm host-buffer pipeline chunk, 0 = auto), "fused_prof"
  * and "f2_*" decomposition overrides. Returns the old value. */

@@ -1278,6 +1278,17 @@ struct DskiOp final : Op {
     if (d == 2 && G == 2) grow(grid_h, static_cast<size_t>(M) * nrhs);
   }
 
+  bool pcg_persist(PcgVecPlan& vp, const PcgVecArgs& va, double* P, double* AP, int nrhs, int iters,
+                   cudaStream_t s) override {
+    if (d != 2 || G != 2) return false;
+    Fused2dPlan* fp = fused_plan(nrhs);
+    if (!fp) return false;
+    ensure_scratch(nrhs);
+    if (fp->s_mode == 1) grow(grid_p, static_cast<size_t>(fp->s_nbuf) * M * nrhs);
+    return fused2d_pcg_persist(geom2d(), *fp, vp, va, P, AP, grid_u.p, grid_h.p, grid_t.p, grid_w.p, grid_p.p,
+                               iters, s);
+  }
+
   void mvm(const double* in, double* out, int nrhs, cudaStream_t s) override {
     ensure_scratch(nrhs);
     if (Fused2dPlan* fp = fused_plan(nrhs)) {

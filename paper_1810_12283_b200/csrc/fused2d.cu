@@ -40,6 +40,7 @@
 #include <type_traits>
 
 #include "fused2d.hpp"
+#include "pcg_vec2.cuh"
 #include "gk_sync.cuh"
 
 namespace gk {
@@ -867,8 +868,8 @@ __device__ void f2_gather(const F2Args& a, double* sm) {
 }
 
 
-template <int T, int RP, int MINB>
-__global__ void __launch_bounds__(F2_THREADS, MINB) k_dski_mvm2d(F2Args a) {
+template <int T, int RP>
+__device__ __forceinline__ void f2_body(const F2Args& a) {
   extern __shared__ __align__(16) double f2_sm[];
   double* ts0 = f2_sm;
   double* ts1 = f2_sm + a.m0p;
@@ -909,6 +910,29 @@ __global__ void __launch_bounds__(F2_THREADS, MINB) k_dski_mvm2d(F2Args a) {
   }
   __syncthreads();
   stamp(a, 7);
+  if (threadIdx.x == 0)  // the shared memory may be reused (persistent PCG kernel)
+    for (int b = 0; b < 8; ++b) asm volatile("mbarrier.inval.shared.b64 [%0];\n" ::"r"(smem_u32(mbar + b)) : "memory");
+  __syncthreads();
+}
+
+template <int T, int RP, int MINB>
+__global__ void __launch_bounds__(F2_THREADS, MINB) k_dski_mvm2d(F2Args a) {
+  f2_body<T, RP>(a);
+}
+
+// Persistent PCG: up to `iters` iterations in one cooperative launch — the
+// MVM AP = K P (f2_body) and the rows-resident vector step (pcg_vec2_body)
+// separated by grid barriers; all CTAs leave together once no column is
+// active (the vector step's column state is identical in every CTA).
+template <int T, int RP>
+__global__ void __launch_bounds__(F2_THREADS, 2) k_pcg_persist(F2Args fa, PcgVecArgs va, int iters) {
+  for (int it = 0; it < iters; ++it) {
+    f2_body<T, RP>(fa);
+    grid_sync(fa.bar);
+    const int nact = pcg_vec2_body(va);
+    if (nact == 0) break;
+    grid_sync(fa.bar);
+  }
 }
 
 size_t smem_bytes(const Fused2dGeom& g, const Fused2dPlan& p) {
@@ -1053,8 +1077,8 @@ void fused2d_plan(const Fused2dGeom& g, const std::vector<int>& cs, int nrhs, in
                  p.s_nspl, p.s_nst, p.s_nbuf, p.g_mode, p.g_TC, p.g_strips, p.g_L, p.g_segs, p.g_pmax, p.t_split);
 }
 
-void fused2d_mvm(const Fused2dGeom& g, Fused2dPlan& p, const double* v, double* out, double* u, double* h,
-                 double* y1, double* w, double* pbuf, bool noise, cudaStream_t s) {
+static F2Args fused2d_args(const Fused2dGeom& g, Fused2dPlan& p, const double* v, double* out, double* u,
+                           double* h, double* y1, double* w, double* pbuf, bool noise) {
   F2Args a{};
   a.m0 = g.m0;
   a.m1 = g.m1;
@@ -1112,6 +1136,12 @@ void fused2d_mvm(const Fused2dGeom& g, Fused2dPlan& p, const double* v, double* 
   a.pbuf = pbuf;
   a.m0p = (g.m0 + 7) / 8 * 8;
   a.m1p = (g.m1 + 7) / 8 * 8;
+  return a;
+}
+
+void fused2d_mvm(const Fused2dGeom& g, Fused2dPlan& p, const double* v, double* out, double* u, double* h,
+                 double* y1, double* w, double* pbuf, bool noise, cudaStream_t s) {
+  F2Args a = fused2d_args(g, p, v, out, u, h, y1, w, pbuf, noise);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(p.grid));
   cfg.blockDim = dim3(F2_THREADS);
@@ -1125,6 +1155,52 @@ void fused2d_mvm(const Fused2dGeom& g, Fused2dPlan& p, const double* v, double* 
   void* args[] = {&a};
   GK_CUDA(cudaLaunchKernelExC(&cfg, pick_kernel(g.T, p.RP, p.minb), args));
   launched("dski fused 2-D MVM");
+}
+
+
+bool fused2d_pcg_persist(const Fused2dGeom& g, Fused2dPlan& p, PcgVecPlan& vp, PcgVecArgs va, const double* P,
+                         double* AP, double* u, double* h, double* y1, double* w, double* pbuf, int iters,
+                         cudaStream_t s) {
+  if (!p.ok || !vp.v2 || p.grid != vp.grid || (g.T != 6 && g.T != 4)) return false;
+  F2Args fa = fused2d_args(g, p, P, AP, u, h, y1, w, pbuf, true);
+  fa.prof = nullptr;
+  va.rch = vp.rch;
+  va.prof = nullptr;
+  va.part = vp.part.p;
+  va.red_out = vp.red_out.p;
+  va.rctr = vp.rctr.p;
+  va.tpart = vp.tpart.p;
+  va.T = vp.T.p;
+  va.bar = vp.bar.p;
+  const void* fn = g.T == 6 ? (p.RP == 2 ? (const void*)k_pcg_persist<6, 2> : (const void*)k_pcg_persist<6, 1>)
+                            : (p.RP == 2 ? (const void*)k_pcg_persist<4, 2> : (const void*)k_pcg_persist<4, 1>);
+  const size_t smem = std::max(p.smem, vp.smem);
+  raise_smem_limit(fn, smem);
+  static std::mutex mu;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    GK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 int(cudaSharedmemCarveoutMaxShared)));
+  }
+  int occ = 0, sms = 0, dev = 0;
+  GK_CUDA(cudaGetDevice(&dev));
+  GK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, F2_THREADS, smem));
+  if (occ * sms < p.grid) return false;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(p.grid));
+  cfg.blockDim = dim3(F2_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void* args[] = {&fa, &va, &iters};
+  GK_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
+  launched("persistent PCG (MVM + vector step)");
+  return true;
 }
 
 }  // namespace gk

@@ -1,6 +1,8 @@
 // fused2d.hpp — one-launch D-SKI MVM for 2-D grids with gradients (C1, C2, C4).
 #pragma once
 
+#include "pcg_fused.hpp"
+
 #include <vector>
 
 #include "gk_common.hpp"
@@ -49,5 +51,12 @@ void fused2d_plan(const Fused2dGeom& g, const std::vector<int>& cell_start_h, in
 // (h holds the scatter's segment-boundary halo rows).
 void fused2d_mvm(const Fused2dGeom& g, Fused2dPlan& p, const double* v, double* out, double* u,
                  double* h, double* y1, double* w, double* pbuf, bool noise, cudaStream_t s);
+
+// Persistent PCG (PCG with this operator's one-launch MVM and the rows-resident
+// vector step in one cooperative kernel, up to `iters` iterations). False when
+// the plans are incompatible (then the caller uses the per-iteration path).
+bool fused2d_pcg_persist(const Fused2dGeom& g, Fused2dPlan& p, PcgVecPlan& vp, PcgVecArgs va, const double* P,
+                         double* AP, double* u, double* h, double* y1, double* w, double* pbuf, int iters,
+                         cudaStream_t s);
 
 }  // namespace gk

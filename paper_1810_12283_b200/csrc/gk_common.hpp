@@ -146,6 +146,9 @@ enum OpKind { KIND_EXACT = 0, KIND_DSKI = 1, KIND_DSKIP = 2, KIND_DENSE = 3 };
 // innermost ("RHS-minor": element (r, b) at r*nrhs + b).
 std::uint64_t next_op_uid();
 
+struct PcgVecPlan;
+struct PcgVecArgs;
+
 struct Op {
   Op() : uid(next_op_uid()) {}
   virtual ~Op();
@@ -177,6 +180,12 @@ struct Op {
   virtual void row(i64 r_ext, double* out, cudaStream_t s) = 0;
   // internal row index -> external row index (device array or null = identity)
   virtual const i64* d_ext_of_int() const { return nullptr; }
+  // Persistent PCG (MVM + fused vector step in one cooperative launch, up to
+  // `iters` iterations); false when this operator has no such path.
+  virtual bool pcg_persist(PcgVecPlan&, const PcgVecArgs&, double* /*P*/, double* /*AP*/, int /*nrhs*/,
+                           int /*iters*/, cudaStream_t) {
+    return false;
+  }
   virtual i64 int_of_ext(i64 r) const { return r; }
   virtual void stage(int st, const double* in, double* out, int nrhs, cudaStream_t s);
 

@@ -1524,7 +1524,43 @@ PcgResult pcg_internal(Op& op, Precond* M, const double* B, double* X, int nrhs,
   GK_CUDA(cudaMallocHost(&nact_h, 2 * sizeof(int)));
   GK_CUDA(cudaMemcpyAsync(nact_h, st.nactive, sizeof(int), cudaMemcpyDeviceToHost, s));
   GK_CUDA(cudaStreamSynchronize(s));
-  if (*nact_h > 0 && maxit > 0) {
+  bool persisted = false;
+  if (*nact_h > 0 && maxit > 0 && vfused && vplan.v2 && g_tuning.pcg_fused.load() == 5) {
+    // Persistent path (opt-in, tuning "pcg_fused" = 5): PI iterations per
+    // cooperative launch (MVM + vector step, grid barriers in between),
+    // polled one launch behind. Measured at C2: 124 µs per iteration vs 111
+    // for the graph-replayed kernels — graph replay already hides the launch
+    // gap, and the merged kernel's 128-register cap costs both phases spills.
+    PcgVecArgs va{};
+    va.st = st;
+    va.X = X;
+    va.R = R.p;
+    va.P = Pb.p;
+    va.AP = AP.p;
+    va.Z = Zb.p;
+    va.q1 = M ? M->q1.p : nullptr;
+    va.dinv = M ? M->dinv.p : nullptr;
+    va.k = kM;
+    va.N = N;
+    va.nrhs = nrhs;
+    const int PI = 32;
+    const int max_launches = (maxit + PI - 1) / PI + 1;
+    cudaEvent_t evs[2];
+    for (auto& e : evs) GK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (int j = 0; j < max_launches; ++j) {
+      if (!op.pcg_persist(vplan, va, Pb.p, AP.p, nrhs, PI, s)) break;  // j == 0: no persistent path
+      persisted = true;
+      GK_CUDA(cudaMemcpyAsync(nact_h + (j & 1), st.nactive, sizeof(int), cudaMemcpyDeviceToHost, s));
+      GK_CUDA(cudaEventRecord(evs[j & 1], s));
+      if (j >= 1) {
+        GK_CUDA(cudaEventSynchronize(evs[(j - 1) & 1]));
+        if (nact_h[(j - 1) & 1] == 0) break;
+      }
+    }
+    GK_CUDA(cudaStreamSynchronize(s));
+    for (auto e : evs) cudaEventDestroy(e);
+  }
+  if (!persisted && *nact_h > 0 && maxit > 0) {
     // warm the operator's scratch outside capture, then capture ITER iterations
     op.mvm(Pb.p, AP.p, nrhs, s);
     const int ITER = 4;

@@ -255,7 +255,7 @@ def test_dski_pipeline_matches_oracle_c1_subset():
 
 @pytest.mark.parametrize("nrhs", [1, 8, 32])
 @pytest.mark.parametrize("with_precond", [True, False])
-@pytest.mark.parametrize("variant", [1, 3])  # 1: rows-resident v2 where it fits, 3: v1
+@pytest.mark.parametrize("variant", [1, 3, 5])  # 1: rows-resident v2 where it fits, 3: v1, 5: persistent
 def test_fused_pcg_step_matches_unfused(nrhs, with_precond, variant):
     """The one-launch PCG vector step (pcg_fused.cu) runs the same per-column
     recurrences as the separate-kernel path: same iteration counts and flags,

@@ -20,17 +20,17 @@ dev = torch.device("cuda")
 Vext = torch.from_numpy(np.ascontiguousarray(B.T)).to(dev)
 Xd = torch.empty_like(Vext)
 its = int(sys.argv[1]) if len(sys.argv) > 1 else 200
-res = {1: [], 2: [], 3: []}
+res = {5: [], 1: [], 3: [], 2: []}
 for rep in range(int(os.environ.get("REPS", "3"))):
-    for fused in (1, 3, 2):
+    for fused in (5, 1, 3, 2):
         gk.set_tuning("pcg_fused", fused)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         it, conv = gk.cg_dev(op, Vext.data_ptr(), Xd.data_ptr(), nrhs, float(os.environ.get("TOL", "1e-12")), its, M)
         torch.cuda.synchronize()
         res[fused].append((time.perf_counter() - t0) / its * 1e6)
-for fused in (1, 3, 2):
-    print(f"pcg_fused={fused} ({ {1: 'one-launch vector step v2', 3: 'one-launch v1', 2: 'separate kernels'}[fused]}): "
+for fused in (5, 1, 3, 2):
+    print(f"pcg_fused={fused} ({ {5: 'persistent MVM + v2 step', 1: 'graphs: MVM + v2 step', 3: 'graphs: MVM + v1 step', 2: 'separate kernels'}[fused]}): "
           f"{its} iterations, min {min(res[fused]):.1f} us/iteration (all {[round(x, 1) for x in res[fused]]})",
           flush=True)
 gk.set_tuning("pcg_fused", 0)

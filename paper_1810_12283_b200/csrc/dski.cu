@@ -1,3 +1,6 @@
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 // dski.cu — the D-SKI operator on B200 (reference dski.cpp:174-304,
 // interpolation.cpp:59-97,212-266).
 //
@@ -1588,6 +1591,14 @@ std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, cons
   if (n < 1) fail(GK_ERR_ARG, "D-SKI needs at least one point");
   if (order != 0 && order != 1) fail(GK_ERR_ARG, "interpolation order must be 0 (quintic) or 1 (cubic)");
   DeviceGuard dg(device);
+  const bool bprof = std::getenv("GK_BUILD_PROF") != nullptr;
+  auto bt0 = std::chrono::steady_clock::now();
+  auto bmark = [&](const char* what) {
+    if (!bprof) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "dski build: %s %.3f ms\n", what, std::chrono::duration<double, std::milli>(t - bt0).count());
+    bt0 = t;
+  };
   auto op = std::make_unique<DskiOp>();
   op->kind = KIND_DSKI;
   op->device = device;
@@ -1618,6 +1629,7 @@ std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, cons
       axis_weights(X[j * n + i], g.origin[j], g.spacing[j], g.dims[j], T, i, j,
                    &base[static_cast<size_t>(i) * d + j], &wts[static_cast<size_t>(i) * STRIDE + j * 2 * T],
                    &wts[static_cast<size_t>(i) * STRIDE + j * 2 * T + T]);
+  bmark("stencil weights");
   // sort by base cell (counting sort: stable, deterministic)
   i64 ncells = 1;
   for (int j = 0; j < d; ++j) ncells *= op->nb[j];
@@ -1704,7 +1716,9 @@ std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, cons
   std::vector<i64> ext(static_cast<size_t>(op->N));
   for (int gg = 0; gg <= op->G; ++gg)
     for (i64 s = 0; s < n; ++s) ext[static_cast<size_t>(gg * n + s)] = gg * n + op->perm_h[static_cast<size_t>(s)];
+  bmark("sort + host tables");
   op->init_stream();
+  bmark("init_stream");
   cudaStream_t st = op->stream;
   op->base.upload(base_s.data(), base_s.size(), st);
   op->wts.upload(wts_s.data(), wts_s.size(), st);
@@ -1804,6 +1818,7 @@ std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, cons
   op->origin_d.upload(o3, 3, st);
   op->h_d.upload(h3, 3, st);
   GK_CUDA(cudaStreamSynchronize(st));
+  bmark("uploads");
   return op;
 }
 

@@ -103,6 +103,9 @@ int gk_debug_fused_phases(gk_op* op, int nrhs, int64_t* out, int max_ctas);
 /* fp64 tensor-core (DMMA m8n8k4) throughput of `device` in TFLOP/s, measured
  * by a register-only kernel (best of 5): the D-SKIP roofline denominator. */
 gk_status gk_debug_dmma_peak(int device, double* tflops);
+/* rademacher_vector(n, seed, stream) (rng.hpp:23-29) generated by the device
+ * mt19937_64 kernel that produces SLQ probes; copied to out[n] (test hook). */
+gk_status gk_debug_rademacher_dev(int64_t n, uint64_t seed, uint64_t stream, double* out);
 
 /* DskiOperator(kernel, grid, X, noise, order, with_gradients) (dski.hpp:58-65).
  * order: 0 quintic, 1 cubic. */

@@ -60,6 +60,7 @@ _SIGS = {
     "gk_kernel_launch_count": (_i64, []),
     "gk_debug_fused_phases": (C.c_int, [_vp, C.c_int, _i64p, C.c_int]),
     "gk_debug_dmma_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double)]),
+    "gk_debug_rademacher_dev": (C.c_int, [_i64, _u64, _u64, _dp]),
     "gk_dski_gather_dev": (C.c_int, [_vp, _vp, _vp, _vp, _i64, _vp]),
     "gk_grid_cover": (C.c_int, [_dp, _i64, C.c_int, _d, C.c_int, C.c_int, C.POINTER(GkGrid)]),
     "gk_mix_seed": (_u64, [_u64, _u64]),
@@ -780,6 +781,13 @@ def stacked_targets(y, dY, mean):
     if dY is not None:
         parts += [np.asarray(dY)[:, j] for j in range(np.asarray(dY).shape[1])]
     return np.concatenate(parts)
+
+
+def rademacher_vector_dev(n, seed, stream=0):
+    """rademacher_vector generated by the device mt19937_64 kernel (test hook)."""
+    out = np.empty(int(n))
+    _check(_lib.gk_debug_rademacher_dev(int(n), int(seed), int(stream), _p(out)))
+    return out
 
 
 def dmma_peak_tflops(device=0):

@@ -182,6 +182,7 @@ int gk_set_tuning(const char* key, int value) {
                            : k == "e2e_chunk" ? &g_tuning.e2e_chunk
                            : k == "dskip" ? &g_tuning.dskip
                            : k == "lanczos" ? &g_tuning.lanczos
+                           : k == "rng" ? &g_tuning.rng
                            : k == "dskip_e" ? &g_tuning.dskip_e
                            : k == "f2_stc" ? &g_tuning.f2_stc
                            : k == "f2_sl" ? &g_tuning.f2_sl
@@ -464,6 +465,16 @@ int gk_debug_fused_phases(gk_op* h, int nrhs, int64_t* out, int max_ctas) {
     n = dski_fused_phases(op, nrhs, out, max_ctas);
   });
   return n;
+}
+
+gk_status gk_debug_rademacher_dev(int64_t n, uint64_t seed, uint64_t stream, double* out) {
+  return guard([&] {
+    if (n < 0 || !out) fail(GK_ERR_ARG, "bad arguments");
+    DevBuf<double> d(static_cast<size_t>(std::max<int64_t>(n, 1)));
+    const std::uint64_t sd = mix_seed(seed, stream);
+    rademacher_dev(n, &sd, 1, 1.0, d.p, n, nullptr);
+    GK_CUDA(cudaMemcpy(out, d.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  });
 }
 
 gk_status gk_debug_dmma_peak(int device, double* tflops) {
@@ -893,9 +904,21 @@ gk_status gk_slq_logdet(const gk_op* h, int probes, int steps, uint64_t seed, do
         for (i64 i = 0; i < N; ++i) z[i] /= zn;
         rseeds[static_cast<size_t>(q)] = mix_seed(seed, 50000 + pid);
       };
-      parallel_for(Prun, gen);
+      if (g_tuning.rng.load() == 0) {  // probes generated on the device (bit-identical streams)
+        std::vector<std::uint64_t> sds(static_cast<size_t>(Prun));
+        for (int q = 0; q < Prun; ++q) {
+          const std::uint64_t pid = std::uint64_t(probe_offset + p0 + q);
+          sds[static_cast<size_t>(q)] = mix_seed(seed, pid);
+          rseeds[static_cast<size_t>(q)] = mix_seed(seed, 50000 + pid);
+          zn2v[static_cast<size_t>(q)] = double(N);  // Σ (±1)² in the host path
+        }
+        rademacher_dev(N, sds.data(), Prun, 1.0 / std::sqrt(double(N)), ze_p, N, s);
+      } else {
+        parallel_for(Prun, gen);
+      }
       auto t1 = now();
-      GK_CUDA(cudaMemcpyAsync(ze_p, hzp, sizeof(double) * N * Prun, cudaMemcpyHostToDevice, s));
+      if (g_tuning.rng.load() != 0)
+        GK_CUDA(cudaMemcpyAsync(ze_p, hzp, sizeof(double) * N * Prun, cudaMemcpyHostToDevice, s));
       op.to_internal(ze_p, N, zi_p, Prun, s);
       if (prof) GK_CUDA(cudaStreamSynchronize(s));
       auto t2 = now();

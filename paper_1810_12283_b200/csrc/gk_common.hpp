@@ -48,6 +48,7 @@ struct Tuning {
   // sizes), 3 = cp.async DMMA (v2), 1 = first generation
   std::atomic<int> dskip{0};
   std::atomic<int> lanczos{0};  // 1 = per-step host-synchronised Lanczos (reference order)
+  std::atomic<int> rng{0};      // 1 = SLQ probes generated on the host (else on the device, same streams)
   std::atomic<int> dskip_e{0};  // v3 expand ring: 0 = 8 m × 4 stages, 1 = 16 × 2, 2 = 16 × 4, 3 = 32 × 2
   std::atomic<int> gen{0};  // bumped by every gk_set_tuning call (cached plans rebuild)
 };

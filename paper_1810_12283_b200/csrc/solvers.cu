@@ -1417,6 +1417,56 @@ __global__ void k_cols_move(const double* __restrict__ src, int Psrc, double* __
   }
 }
 
+// ---------------------------------------------------------------- device mt19937_64
+// Rademacher probe streams on the device, bit-identical to the host's
+// std::mt19937_64(mix_seed(seed, stream)) with the sign from bit 0 of each raw
+// draw (rng.hpp:23-29). One CTA per stream; the 312-word twist runs as two
+// parallel halves (words < 156 read only old state; words ≥ 156 read the first
+// half's new words), then 312 tempered draws are emitted.
+__global__ void __launch_bounds__(320) k_rademacher_mt(const unsigned long long* __restrict__ seeds, i64 n,
+                                                       double scale, i64 ld, double* __restrict__ out) {
+  constexpr int NN = 312, MM = 156;
+  constexpr unsigned long long A = 0xB5026F5AA96619E9ULL, LM = (1ULL << 31) - 1, UM = ~LM;
+  __shared__ unsigned long long mt[NN];
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    unsigned long long x = seeds[blockIdx.x];
+    mt[0] = x;
+    for (int i = 1; i < NN; ++i) {
+      x = 6364136223846793005ULL * (x ^ (x >> 62)) + (unsigned long long)i;
+      mt[i] = x;
+    }
+  }
+  __syncthreads();
+  double* o = out + (i64)blockIdx.x * ld;
+  for (i64 base = 0; base < n; base += NN) {
+    unsigned long long v = 0;
+    if (tid < MM) {
+      const unsigned long long x = (mt[tid] & UM) | (mt[tid + 1] & LM);
+      v = mt[tid + MM] ^ (x >> 1) ^ ((x & 1ULL) ? A : 0ULL);
+    }
+    __syncthreads();
+    if (tid < MM) mt[tid] = v;
+    __syncthreads();
+    if (tid < MM) {
+      const int i = MM + tid;
+      const unsigned long long x = (mt[i] & UM) | (mt[(i + 1) % NN] & LM);
+      v = mt[i - MM] ^ (x >> 1) ^ ((x & 1ULL) ? A : 0ULL);
+    }
+    __syncthreads();
+    if (tid < MM) mt[MM + tid] = v;
+    __syncthreads();
+    if (tid < NN && base + tid < n) {
+      unsigned long long y = mt[tid];
+      y ^= (y >> 29) & 0x5555555555555555ULL;
+      y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+      y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+      y ^= y >> 43;
+      o[base + tid] = (y & 1ULL) ? scale : -scale;
+    }
+  }
+}
+
 }  // namespace
 
 // ================================================================ PCG driver
@@ -2315,6 +2365,17 @@ LanczosBatch lanczos_batch(Op& op, const double* start_int, int P, int steps,
   }
   GK_CUDA(cudaStreamSynchronize(s));
   return res;
+}
+
+
+// P Rademacher vectors of length n (streams mixed on the host: seeds[q] =
+// mix_seed(seed, stream_q)), each scaled by `scale`, into out[q·ld + i].
+void rademacher_dev(i64 n, const std::uint64_t* seeds_h, int P, double scale, double* out, i64 ld, cudaStream_t s) {
+  DevBuf<unsigned long long> sd(static_cast<size_t>(P));
+  GK_CUDA(cudaMemcpyAsync(sd.p, seeds_h, sizeof(unsigned long long) * P, cudaMemcpyHostToDevice, s));
+  k_rademacher_mt<<<P, 320, 0, s>>>(sd.p, n, scale, ld, out);
+  launched("rademacher (device mt19937_64)");
+  GK_CUDA(cudaStreamSynchronize(s));  // pageable seed source / sd lifetime
 }
 
 }  // namespace gk

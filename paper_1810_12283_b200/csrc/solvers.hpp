@@ -79,4 +79,8 @@ LanczosBatch lanczos_batch(Op& op, const double* start_int, int P, int steps,
                            const std::vector<std::uint64_t>& restart_seeds, double* Q_out,
                            cudaStream_t s);
 
+// P Rademacher probe vectors generated on the device, bit-identical to the
+// host's std::mt19937_64(seeds[q]) streams (sign = bit 0 of each draw).
+void rademacher_dev(i64 n, const std::uint64_t* seeds_h, int P, double scale, double* out, i64 ld, cudaStream_t s);
+
 }  // namespace gk

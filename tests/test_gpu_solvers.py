@@ -112,6 +112,27 @@ def test_preconditioner_high_rank_vs_dense_inverse(k):
         assert abs(P.quadratic(b) - b @ want) <= 1e-9 * abs(b @ want)
 
 
+@pytest.mark.parametrize("n", [1, 311, 312, 313, 1000, 30000])
+def test_device_rademacher_streams_bit_identical(n):
+    """The device mt19937_64 (two-phase parallel twist) reproduces the host
+    std::mt19937_64(mix_seed(seed, stream)) sign stream exactly."""
+    for seed, stream in ((0, 0), (0, 1000), (7, 50001), (2 ** 63 + 5, 3)):
+        assert np.array_equal(gk.rademacher_vector_dev(n, seed, stream), gk.rademacher_vector(n, seed, stream))
+
+
+def test_slq_device_probes_equal_host_probes():
+    X, y, dY = gk.make_dataset(1, 0)
+    grid = gk.Grid.cover(X, 1e-4, 3, 60)
+    op = gk.DskiOperator(gk.KernelSpec(0.15, 1.0), grid, X, (0.05, 0.05))
+    a = gk.slq_logdet(op, 9, 20, 4, 1e-4)
+    try:
+        gk.set_tuning("rng", 1)
+        b = gk.slq_logdet(op, 9, 20, 4, 1e-4)
+    finally:
+        gk.set_tuning("rng", 0)
+    assert np.array_equal(a.estimates, b.estimates)
+
+
 def test_slq_exact_for_scaled_identity():
     r1 = gk.slq_logdet(gk.DenseOperator(np.eye(64)), 4, 10, 42)
     assert abs(r1.logdet) <= 1e-12

@@ -140,6 +140,26 @@ __device__ __forceinline__ void block_cols2(double v1, double v2, int nrhs, doub
   }
 }
 
+// as block_cols2, stored transposed: tp[c·grid + cta] (v1), tp[(nrhs + c)·grid + cta] (v2)
+__device__ __forceinline__ void block_cols2_t(double v1, double v2, int nrhs, double* sm, double* tp) {
+  __syncthreads();
+  sm[threadIdx.x] = v1;
+  __syncthreads();
+  const int slots = PV_THREADS / nrhs;
+  double s1 = 0.0;
+  if ((int)threadIdx.x < nrhs)
+    for (int k = 0; k < slots; ++k) s1 += sm[k * nrhs + threadIdx.x];
+  __syncthreads();
+  sm[threadIdx.x] = v2;
+  __syncthreads();
+  if ((int)threadIdx.x < nrhs) {
+    double s2 = 0.0;
+    for (int k = 0; k < slots; ++k) s2 += sm[k * nrhs + threadIdx.x];
+    tp[(i64)threadIdx.x * gridDim.x + blockIdx.x] = s1;
+    tp[(i64)(nrhs + threadIdx.x) * gridDim.x + blockIdx.x] = s2;
+  }
+}
+
 // Returns the number of active columns after the step (identical in every CTA).
 __device__ __forceinline__ int pcg_vec2_body(const PcgVecArgs& a) {
   extern __shared__ __align__(16) double pv_sm[];
@@ -284,7 +304,9 @@ __device__ __forceinline__ int pcg_vec2_body(const PcgVecArgs& a) {
       }
     }
   }
-  block_cols2(arr, acc_c, nrhs, red, part1);
+  // ‖r‖², ‖c‖² partials go out transposed behind the T partials and are
+  // reduced with them (no all-to-all read of partials by every CTA)
+  block_cols2_t(arr, acc_c, nrhs, red, a.tpart + (i64)K * nrhs * gridDim.x);
   pv_stamp(a, 2, prof_on);
   if (K > 0) {  // T partial = Q1ᵀ c over the resident rows (M = j, N = b, K = rows)
     const int ntt = ((K + 7) / 8) * ntn;
@@ -317,8 +339,22 @@ __device__ __forceinline__ int pcg_vec2_body(const PcgVecArgs& a) {
     }
   }
   pv_stamp(a, 3, prof_on);
-  grid_allreduce_cols(part1, 2 * nrhs, colv, a.bar);  // rr | cc; also a full barrier (tpart visible)
+  grid_sync(a.bar);  // T, ‖r‖² and ‖c‖² partials visible
   pv_stamp(a, 10, prof_on);
+  {  // distributed fixed-order reduction: T (K·nrhs), then ‖r‖² and ‖c‖² (2·nrhs)
+    const int nout = (K + 2) * nrhs;
+    for (int o = blockIdx.x * (PV_THREADS / 32) + tid / 32; o < nout; o += gridDim.x * (PV_THREADS / 32)) {
+      const double v = warp_sum_cols(a.tpart + (i64)o * gridDim.x, gridDim.x, 1, 0);
+      if ((tid & 31) == 0) a.T[o] = v;
+    }
+  }
+  pv_stamp(a, 4, prof_on);
+  grid_sync(a.bar);
+  pv_stamp(a, 9, prof_on);
+  for (int c = tid; c < 2 * nrhs; c += PV_THREADS) colv[c] = __ldcg(a.T + (i64)K * nrhs + c);
+  for (int j = warp; j < K; j += PV_THREADS / 32)
+    for (int cc = lane; cc < nrhs; cc += 32) Ts[j * RS + cc] = __ldcg(a.T + j * nrhs + cc);
+  __syncthreads();
 
   // D: convergence (:119-125)
   for (int c = tid; c < nrhs; c += PV_THREADS) {
@@ -340,19 +376,6 @@ __device__ __forceinline__ int pcg_vec2_body(const PcgVecArgs& a) {
     int nact = 0;
     for (int c = 0; c < nrhs; ++c) nact += act[c];
     *st.nactive = nact;
-  }
-  if (K > 0) {
-    const int nout = K * nrhs;
-    for (int o = blockIdx.x * (PV_THREADS / 32) + tid / 32; o < nout; o += gridDim.x * (PV_THREADS / 32)) {
-      const double v = warp_sum_cols(a.tpart + (i64)o * gridDim.x, gridDim.x, 1, 0);
-      if ((tid & 31) == 0) a.T[o] = v;
-    }
-    pv_stamp(a, 4, prof_on);
-    grid_sync(a.bar);
-    pv_stamp(a, 9, prof_on);
-    for (int j = warp; j < K; j += PV_THREADS / 32)
-      for (int cc = lane; cc < nrhs; cc += 32) Ts[j * RS + cc] = __ldcg(a.T + j * nrhs + cc);
-    __syncthreads();
   }
   // F: rz_new = ||c||² − ||T||², beta (active columns)
   for (int c = tid; c < nrhs; c += PV_THREADS) {

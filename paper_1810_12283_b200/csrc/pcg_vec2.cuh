@@ -393,26 +393,46 @@ __device__ __forceinline__ int pcg_vec2_body(const PcgVecArgs& a) {
   __syncthreads();
   pv_stamp(a, 5, prof_on);
 
-  // EG: p = D^{-1/2}(c − Q1 T) + beta p (active columns), from the DMMA tiles
+  // EG: p = D^{-1/2}(c − Q1 T) + beta p (active columns), from the DMMA tiles:
+  // the warp's tiles in groups of EGQ (not unrolled: keeps the kernel's code
+  // small — instruction-fetch stalls dominated with all tiles unrolled); per
+  // group the P values are loaded first, the DMMA chains run interleaved,
+  // then the epilogue writes.
   if (K > 0) {
+    constexpr int EGQ = 4;
     const int nte = (nr8 / 8) * ntn;
+    const int nq = nte > warp ? (nte - warp + 7) / 8 : 0;
+#pragma unroll 1
+    for (int q0 = 0; q0 < nq; q0 += EGQ) {
+      double pv[EGQ][2], sacc[EGQ][2];
+      const double* qp[EGQ];
+      const double* tp[EGQ];
+      int rows[EGQ], cols[EGQ];
 #pragma unroll
-    for (int q = 0; q < PV_ET; ++q) {
-      const int tile = warp + 8 * q;
-      if (tile < nte) {
-        const int m0 = tileM[tile], n0 = tileN[tile];
-        double s0 = 0.0, s1 = 0.0;
-        const double* qrow = Qs + (m0 + g8) * QS;
-        const double* tcol = Ts + n0 + g8;
-        for (int k0 = 0; k0 < K4; k0 += 4) pv_dmma(s0, s1, qrow[k0 + t4], tcol[(k0 + t4) * RS]);
-        const int row = m0 + g8;
+      for (int u = 0; u < EGQ; ++u) {
+        const int tile = warp + 8 * min(q0 + u, nq - 1);
+        rows[u] = tileM[tile] + g8;
+        cols[u] = tileN[tile] + 2 * t4;
+        qp[u] = Qs + rows[u] * QS + t4;
+        tp[u] = Ts + t4 * RS + tileN[tile] + g8;
+        sacc[u][0] = sacc[u][1] = 0.0;
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          pv[u][e] = (q0 + u < nq && rows[u] < nr && cols[u] + e < nrhs) ? a.P[(r0 + rows[u]) * nrhs + cols[u] + e]
+                                                                          : 0.0;
+      }
+      for (int k0 = 0; k0 < K4; k0 += 4)
+#pragma unroll
+        for (int u = 0; u < EGQ; ++u) pv_dmma(sacc[u][0], sacc[u][1], qp[u][k0], tp[u][k0 * RS]);
+#pragma unroll
+      for (int u = 0; u < EGQ; ++u) {
+        if (q0 + u >= nq || rows[u] >= nr) continue;
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int bb = n0 + 2 * t4 + e;
-          if (row < nr && bb < nrhs && act[bb]) {
-            const double z = Ds[row] * (Cs[row * RS + bb] - (e ? s1 : s0));
-            const i64 i = (r0 + row) * nrhs + bb;
-            a.P[i] = z + beta[bb] * a.P[i];
+          const int bb = cols[u] + e;
+          if (bb < nrhs && act[bb]) {
+            const double z = Ds[rows[u]] * (Cs[rows[u] * RS + bb] - sacc[u][e]);
+            a.P[(r0 + rows[u]) * nrhs + bb] = z + beta[bb] * pv[u][e];
           }
         }
       }

@@ -547,7 +547,7 @@ __global__ void __launch_bounds__(128, 3) k_pc_apply3(const double* __restrict__
                                                       const double* __restrict__ dinv,
                                                       const double* __restrict__ R, const double* __restrict__ T,
                                                       i64 N, int nrhs, double* __restrict__ Z,
-                                                      double* __restrict__ partial_rz) {
+                                                      double* __restrict__ partial_rz, int rz_ld, int rz_cols) {
   extern __shared__ __align__(16) double p3_sm[];
   constexpr int BWC = 16 * NJ, SV = BWC + ((4 - BWC % 16) + 16) % 16, JT = 2 * NJ;
   const int SA = p3_pad(k);
@@ -665,7 +665,9 @@ __global__ void __launch_bounds__(128, 3) k_pc_apply3(const double* __restrict__
       }
     __syncthreads();
     for (int bl = tid; bl < bw; bl += 128)
-      partial_rz[(i64)blockIdx.x * nrhs + b0 + bl] = ((red[bl] + red[BWC + bl]) + red[2 * BWC + bl]) + red[3 * BWC + bl];
+      if (b0 + bl < rz_cols)
+        partial_rz[(i64)blockIdx.x * rz_ld + b0 + bl] =
+            ((red[bl] + red[BWC + bl]) + red[2 * BWC + bl]) + red[3 * BWC + bl];
   }
 }
 
@@ -1683,8 +1685,11 @@ static void set_smem(const void* fn, size_t bytes) {
 void Precond::ensure(int nrhs) {
   if (nrhs <= ensured_nrhs) return;
   ensured_nrhs = nrhs;
-  partial.reserve(static_cast<size_t>(RB) * k * nrhs);
-  t.reserve(static_cast<size_t>(k) * nrhs);
+  const int np = nrhs + (nrhs & 1);  // padded width of the v3 kernels (odd RHS counts)
+  partial.reserve(static_cast<size_t>(RB) * k * np);
+  t.reserve(static_cast<size_t>(k) * np);
+  pad_r.reserve(static_cast<size_t>(N) * np);
+  pad_z.reserve(static_cast<size_t>(N) * np);
   const size_t sh1 = sizeof(double) * (PC_RT * k + PC_RT * nrhs + k * nrhs);
   if (sh1 > 227 * 1024) fail(GK_ERR_UNSUPPORTED, "preconditioner rank × nrhs too large for one pass");
   set_smem((const void*)k_pc_proj, sh1);
@@ -1727,8 +1732,23 @@ size_t Precond::apply_mma_smem(int nrhs) const {
   return sizeof(double) * size_t(kp * (np + 8) + 64 * std::max(kp + 4, np + 8));  // Qs, reused for r·z
 }
 
+__global__ void k_pad_cols(const double* __restrict__ src, int ns, i64 N, int np, double* __restrict__ dst) {
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < N * np; e += (i64)gridDim.x * blockDim.x) {
+    const i64 r = e / np;
+    const int b = int(e - r * np);
+    dst[e] = b < ns ? src[r * ns + b] : 0.0;
+  }
+}
+__global__ void k_unpad_cols(const double* __restrict__ src, int np, i64 N, int ns, double* __restrict__ dst) {
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < N * ns; e += (i64)gridDim.x * blockDim.x) {
+    const i64 r = e / ns;
+    dst[e] = src[r * np + (e - r * ns)];
+  }
+}
+
 template <int NJ>
-static int precond_apply3(Precond& M, const double* r, double* z, int nrhs, cudaStream_t s, double* partial_rz) {
+static int precond_apply3(Precond& M, const double* r, double* z, int nrhs, cudaStream_t s, double* partial_rz,
+                          int rz_ld, int rz_cols) {
   const int k = int(M.k);
   const i64 N = M.N;
   constexpr int BWC = 16 * NJ, SV = BWC + ((4 - BWC % 16) + 16) % 16;
@@ -1750,7 +1770,8 @@ static int precond_apply3(Precond& M, const double* r, double* z, int nrhs, cuda
   k_pc_reduce<<<(k * nrhs + 31) / 32, 256, 0, s>>>(M.partial.p, chunks, k * nrhs, M.t.p);
   launched("precond reduce");
   const unsigned nb = static_cast<unsigned>((N + 63) / 64);
-  k_pc_apply3<NJ><<<dim3(nb, bt), 128, sa, s>>>(M.q1.p, k, M.dinv.p, r, M.t.p, N, nrhs, z, partial_rz);
+  k_pc_apply3<NJ><<<dim3(nb, bt), 128, sa, s>>>(M.q1.p, k, M.dinv.p, r, M.t.p, N, nrhs, z, partial_rz, rz_ld,
+                                                 rz_cols);
   launched("precond apply (DMMA v3)");
   return int(nb);
 }
@@ -1758,11 +1779,28 @@ static int precond_apply3(Precond& M, const double* r, double* z, int nrhs, cuda
 int Precond::apply(const double* r, double* z, int nrhs, cudaStream_t s, double* partial_rz) {
   ensure(nrhs);  // no-op once reserved (and before any graph capture)
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  if (g_tuning.precond.load() == 0 && (k & 1) == 0 && (nrhs & 1) == 0 && k <= 256 && nrhs >= 4 && al16(r) &&
-      al16(z) && al16(q1.p) && al16(dinv.p)) {
-    if (nrhs > 32) return precond_apply3<4>(*this, r, z, nrhs, s, partial_rz);
-    if (nrhs > 16) return precond_apply3<2>(*this, r, z, nrhs, s, partial_rz);
-    return precond_apply3<1>(*this, r, z, nrhs, s, partial_rz);
+  if (g_tuning.precond.load() == 0 && (k & 1) == 0 && k <= 256 && nrhs >= 4 && nrhs + (nrhs & 1) <= 64 && al16(q1.p) &&
+      al16(dinv.p)) {
+    // an odd RHS count (C3: 17) runs on a zero-padded copy with 16-byte rows
+    const bool pad = (nrhs & 1) || !al16(r) || !al16(z);
+    const int np = pad ? nrhs + (nrhs & 1) : nrhs;
+    const double* rr = r;
+    double* zz = z;
+    if (pad) {
+      k_pad_cols<<<blocks_for(N * np), 256, 0, s>>>(r, nrhs, N, np, pad_r.p);
+      launched("precond pad");
+      rr = pad_r.p;
+      zz = pad_z.p;
+    }
+    int nb;
+    if (np > 32) nb = precond_apply3<4>(*this, rr, zz, np, s, partial_rz, nrhs, nrhs);
+    else if (np > 16) nb = precond_apply3<2>(*this, rr, zz, np, s, partial_rz, nrhs, nrhs);
+    else nb = precond_apply3<1>(*this, rr, zz, np, s, partial_rz, nrhs, nrhs);
+    if (pad) {
+      k_unpad_cols<<<blocks_for(N * nrhs), 256, 0, s>>>(pad_z.p, np, N, nrhs, z);
+      launched("precond unpad");
+    }
+    return nb;
   }
   if (mma_ok(nrhs) && (g_tuning.precond.load() == 0 || g_tuning.precond.load() == 3)) {
     k_pc_proj_mma<<<RB, 128, proj_mma_smem(nrhs), s>>>(r, dinv.p, q1.p, N, int(k), nrhs, proj_rch(nrhs),

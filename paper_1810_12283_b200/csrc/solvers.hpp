@@ -17,6 +17,7 @@ struct Precond {
   DevBuf<double> partial;  // [kRedBlocks][k][nrhs] scratch
   DevBuf<double> t;        // [k][nrhs]
   DevBuf<double> cbuf;     // scratch
+  DevBuf<double> pad_r, pad_z;  // zero-padded (even-width) r / z for the v3 kernels
   // Row order of q1/dinv: the internal order of operator `order_uid`
   // (0 = external order). `ext` points at this object's own copy of that
   // operator's internal->external row map, so it outlives the operator.

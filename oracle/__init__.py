@@ -120,6 +120,8 @@ def lib():
             "orc_gp_predict_mean_grad": (C.c_int, [_vp, _dp, _i64, _dp, _dp]),
             "orc_gp_predict_variance_pivchol": (C.c_int, [_vp, _dp, _dp]),
             "orc_gp_lml_gradient": (C.c_int, [_vp, C.c_int, _dp, C.POINTER(C.c_int)]),
+            "orc_gp_predict_variance_exact": (C.c_int, [_vp, _dp, _dp]),
+            "orc_gp_predict_variance_randomized": (C.c_int, [_vp, _dp, C.c_longlong, C.c_int, C.c_ulonglong, _dp]),
             "orc_gp_dlogell_apply": (C.c_int, [_vp, _dp, _dp]),
         }
         for name, (res, args) in sig.items():
@@ -657,6 +659,19 @@ class GpModel:
         v = _f64(v)
         out = np.empty(v.size)
         _check(lib().orc_gp_dlogell_apply(self.h, _p(v), _p(out)))
+        return out
+
+    def predict_variance_exact(self, x):
+        """GpModel::predict_variance_exact (gp.cpp:499-502)."""
+        out = _d()
+        _check(lib().orc_gp_predict_variance_exact(self.h, _p(_f64(x)), C.byref(out)))
+        return out.value
+
+    def predict_variance_randomized(self, Xt, probes, seed):
+        """GpModel::predict_variance_randomized (gp.cpp:519-547)."""
+        Xt = _f64(Xt, True)
+        out = np.empty(Xt.shape[0])
+        _check(lib().orc_gp_predict_variance_randomized(self.h, _p(Xt), Xt.shape[0], int(probes), int(seed), _p(out)))
         return out
 
     def predict_variance_pivchol(self, x):

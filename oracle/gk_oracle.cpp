@@ -1504,6 +1504,55 @@ Vec GpModel::cross_covariance(const double* x) {  // gp.cpp:406-417 (D-SKI)
   return dski_->stacked_apply(kw.data());
 }
 
+Vec GpModel::solve(const double* b) {  // gp.cpp:143-158 (tol_scale = 1)
+  const LinearOperator& A = op();
+  const Preconditioner* M = preconditioner();
+  CgResult r = cg(A, b, cfg_.cg, M ? M->as_apply() : PrecondApply{});
+  if (!r.converged)
+    throw std::runtime_error("CG did not converge: relative residual " + std::to_string(r.residual_history.back()) +
+                             " after " + std::to_string(r.iterations) + " iterations");
+  return r.x;
+}
+
+double GpModel::predict_variance_exact(const double* x) {  // gp.cpp:499-502
+  Vec q = cross_covariance(x);
+  Vec s = solve(q.data());
+  return k_eval(k_, x, x, d_) - dot(q.data(), s.data(), Index(q.size()));
+}
+
+// gp.cpp:519-547: pivoted-Cholesky base plus an unbiased control-variate
+// correction with Rademacher probes over the test points (streams 9000 + p).
+Vec GpModel::predict_variance_randomized(const double* Xt, Index T, int probes, std::uint64_t seed) {
+  const Preconditioner* M = preconditioner();
+  if (!M) throw std::logic_error("randomized variance needs the preconditioner enabled");
+  const Index N = op().size();
+  std::vector<Vec> Kc(static_cast<size_t>(T));
+  Vec base(static_cast<size_t>(T));
+  std::vector<double> x(static_cast<size_t>(d_));
+  for (Index t = 0; t < T; ++t) {
+    for (int j = 0; j < d_; ++j) x[size_t(j)] = Xt[j * T + t];
+    Kc[size_t(t)] = cross_covariance(x.data());
+    base[size_t(t)] = k_eval(k_, x.data(), x.data(), d_) - M->quadratic(Kc[size_t(t)]);
+  }
+  if (probes <= 0) return base;
+  Vec corr(static_cast<size_t>(T), 0.0);
+  for (int p = 0; p < probes; ++p) {
+    Vec z = rademacher_vector(T, seed, 9000 + std::uint64_t(p));
+    Vec w(static_cast<size_t>(N), 0.0);
+    for (Index t = 0; t < T; ++t)
+      for (Index i = 0; i < N; ++i) w[size_t(i)] += Kc[size_t(t)][size_t(i)] * z[size_t(t)];
+    Vec ex = solve(w.data());
+    Vec ap = M->apply(w);
+    for (Index t = 0; t < T; ++t) {
+      double s = 0.0;
+      for (Index i = 0; i < N; ++i) s += Kc[size_t(t)][size_t(i)] * (ex[size_t(i)] - ap[size_t(i)]);
+      corr[size_t(t)] += z[size_t(t)] * s;
+    }
+  }
+  for (Index t = 0; t < T; ++t) base[size_t(t)] -= corr[size_t(t)] / double(probes);
+  return base;
+}
+
 double GpModel::predict_variance_pivchol(const double* x) {  // gp.cpp:511-517
   const Preconditioner* M = preconditioner();
   if (!M) throw std::logic_error("pivoted Cholesky variance needs the preconditioner enabled");

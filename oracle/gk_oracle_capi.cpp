@@ -472,6 +472,13 @@ int orc_gp_lml_gradient(void* m, int probes, double* grad, int* nparams) {
 int orc_gp_dlogell_apply(void* m, const double* v, double* out) {
   return guard([&] { copy_out(static_cast<GpModel*>(m)->dlogell_apply(v), out); });
 }
+int orc_gp_predict_variance_exact(void* m, const double* x, double* out) {
+  return guard([&] { *out = static_cast<GpModel*>(m)->predict_variance_exact(x); });
+}
+int orc_gp_predict_variance_randomized(void* m, const double* Xt, long long T, int probes, unsigned long long seed,
+                                       double* out) {
+  return guard([&] { copy_out(static_cast<GpModel*>(m)->predict_variance_randomized(Xt, T, probes, seed), out); });
+}
 int orc_gp_predict_variance_pivchol(void* m, const double* x, double* out) {
   return guard([&] { *out = static_cast<GpModel*>(m)->predict_variance_pivchol(x); });
 }

@@ -713,6 +713,55 @@ def lml_gradient(A: LinearOperator, alpha, probes=8, seed=0, tol=1e-4, max_itera
     return g[: k.value].copy()
 
 
+def _solve_columns(A: LinearOperator, B, tol, max_iterations, precond):
+    """GpModel::solve (gp.cpp:143-158) for a block of columns: PCG, and the
+    reference's runtime_error when a column does not converge."""
+    res = cg(A, B, tol, max_iterations, precond, history=True)
+    res = res if isinstance(res, list) else [res]
+    for r in res:
+        if not r.converged:
+            h = r.residual_history[-1] if len(r.residual_history) else float("nan")
+            raise RuntimeError(f"CG did not converge: relative residual {h:.6f} after {r.iterations} iterations")
+    return np.column_stack([r.x for r in res])
+
+
+def _prior_variance(A):
+    k = A.kernel
+    if k.family != SE:
+        raise NotImplementedError("prior variance implemented for the squared-exponential kernel")
+    return k.outputscale ** 2  # eval(kernel, x, x) (gp.cpp:464-466)
+
+
+def predict_variance_exact(A: "DskiOperator", Xtest, tol=1e-4, max_iterations=1000, precond=None):
+    """GpModel::predict_variance_exact (gp.cpp:499-502) for a batch of test
+    points: k(x, x) − q(x)ᵀ K⁻¹ q(x), the solves batched over the test points."""
+    Q = A.cross_covariance(Xtest)
+    S = _solve_columns(A, Q, tol, max_iterations, precond)
+    return _prior_variance(A) - np.einsum("it,it->t", Q, S)
+
+
+def predict_variance_randomized(A: "DskiOperator", precond, Xtest, probes, seed, tol=1e-4, max_iterations=1000):
+    """GpModel::predict_variance_randomized (gp.cpp:519-547): the pivoted-
+    Cholesky variance plus an unbiased control-variate correction over
+    Rademacher probes (streams 9000 + p) on the test points."""
+    if precond is None:
+        raise ValueError("randomized variance needs the preconditioner enabled")
+    Xt = np.asarray(Xtest, dtype=np.float64)
+    T = Xt.shape[0]
+    Q = A.cross_covariance(Xt)
+    base = _prior_variance(A) - np.asarray(precond.quadratic(Q), dtype=np.float64).reshape(T)
+    if probes <= 0:
+        return base
+    Z = np.column_stack([rademacher_vector(T, seed, 9000 + p) for p in range(probes)])
+    W = Q @ Z
+    EX = _solve_columns(A, W, tol, max_iterations, precond)
+    AP = precond.apply(W)
+    corr = np.zeros(T)
+    for p in range(probes):  # probe order, as the reference accumulates
+        corr += Z[:, p] * (Q.T @ (EX[:, p] - AP[:, p]))
+    return base - corr / probes
+
+
 class LanczosFactor:
     """LanczosFactor (linalg.hpp:102-114)."""
 

@@ -93,3 +93,28 @@ def test_trace_estimate_matches_oracle():
     tg = gk.trace_estimate(A, B, 6, 11, 1e-11, 3000)
     to = O.trace_estimate(Ao, Bo, 6, 11, 1e-11, 3000)
     assert abs(tg - to) <= 1e-7 * abs(to), (tg, to)
+
+
+def test_predict_variance_exact_matches_oracle(model):
+    """k(x,x) − q(x)ᵀ K⁻¹ q(x) (gp.cpp:499-502) with the model's solver settings."""
+    om, op, X, y, dY, Xt = model
+    P = gk.Preconditioner.from_pivchol(op, gk.pivoted_cholesky(op, RANK, kernel_part=True))
+    vg = gk.predict_variance_exact(op, Xt[:6], 1e-10, 5000, P)
+    vo = np.array([om.predict_variance_exact(x) for x in Xt[:6]])
+    # var = s² − qᵀK⁻¹q cancels to ~3e-5 of the prior s² = 1: the solves at
+    # tol 1e-10 agree to ~1e-11 absolute, so the gate is relative to s²
+    assert np.all(np.abs(vg - vo) <= 1e-9), (vg, vo)
+    assert np.all(vg > 0)  # a posterior variance
+
+
+def test_predict_variance_randomized_matches_oracle(model):
+    """Pivoted-Cholesky base + control-variate correction over Rademacher
+    probes (gp.cpp:519-547), identical probe streams; the base and the
+    correction cancel to many digits, so the check is relative to the base."""
+    om, op, X, y, dY, Xt = model
+    P = gk.Preconditioner.from_pivchol(op, gk.pivoted_cholesky(op, RANK, kernel_part=True))
+    for probes in (0, 5):
+        vg = gk.predict_variance_randomized(op, P, Xt[:6], probes, 7, 1e-10, 5000)
+        vo = om.predict_variance_randomized(Xt[:6], probes, 7)
+        base = np.array([om.predict_variance_pivchol(x) for x in Xt[:6]])
+        assert np.all(np.abs(vg - vo) <= 1e-7 * (np.abs(base) + np.abs(vo)) + 1e-12), (probes, vg, vo)

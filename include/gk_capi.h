@@ -293,6 +293,11 @@ gk_status gk_dski_predict_mean_grad(const gk_op* op, const double* alpha, double
  * Q (N×T col-major). */
 gk_status gk_dski_cross_covariance(const gk_op* op, const double* Xtest, int64_t T, double* Q,
                                    int64_t ldq);
+/* GpModel::cross_covariance_jacobian (gp.cpp:431-461, D-SKI branch) for T test
+ * points (Xtest T×d col-major): J column t·d + p (leading dimension ldj ≥ N)
+ * = ∂q(x_t)/∂x_p = B K_UU w_p(x_t) with w_p the derivative point stencil. */
+gk_status gk_dski_cross_covariance_jacobian(const gk_op* op, const double* Xtest, int64_t T, double* J,
+                                           int64_t ldj);
 
 /* ---------------------------------------------------------------- datasets
  * Seeded synthetic workloads C1..C5 (BASELINE.json configs), generated on

@@ -121,6 +121,8 @@ def lib():
             "orc_gp_predict_variance_pivchol": (C.c_int, [_vp, _dp, _dp]),
             "orc_gp_lml_gradient": (C.c_int, [_vp, C.c_int, _dp, C.POINTER(C.c_int)]),
             "orc_gp_predict_variance_exact": (C.c_int, [_vp, _dp, _dp]),
+            "orc_gp_cross_covariance_jacobian": (C.c_int, [_vp, _dp, _dp]),
+            "orc_gp_cross_covariance": (C.c_int, [_vp, _dp, _dp]),
             "orc_gp_predict_variance_randomized": (C.c_int, [_vp, _dp, C.c_longlong, C.c_int, C.c_ulonglong, _dp]),
             "orc_gp_dlogell_apply": (C.c_int, [_vp, _dp, _dp]),
         }
@@ -660,6 +662,20 @@ class GpModel:
         out = np.empty(v.size)
         _check(lib().orc_gp_dlogell_apply(self.h, _p(v), _p(out)))
         return out
+
+    def cross_covariance(self, x):
+        """GpModel::cross_covariance (gp.cpp:406-417, D-SKI): length N."""
+        N = self.n * (self.d + 1 if self.dY is not None else 1)
+        out = np.empty(N)
+        _check(lib().orc_gp_cross_covariance(self.h, _p(_f64(x)), _p(out)))
+        return out
+
+    def cross_covariance_jacobian(self, x):
+        """GpModel::cross_covariance_jacobian (gp.cpp:431-461, D-SKI): N × d."""
+        N = self.n * (self.d + 1 if self.dY is not None else 1)
+        out = np.empty(N * self.d)
+        _check(lib().orc_gp_cross_covariance_jacobian(self.h, _p(_f64(x)), _p(out)))
+        return out.reshape(N, self.d, order="F")
 
     def predict_variance_exact(self, x):
         """GpModel::predict_variance_exact (gp.cpp:499-502)."""

@@ -1553,6 +1553,23 @@ Vec GpModel::predict_variance_randomized(const double* Xt, Index T, int probes, 
   return base;
 }
 
+Mat GpModel::cross_covariance_jacobian(const double* x) {  // gp.cpp:431-446 (D-SKI)
+  op();
+  if (!dski_) throw std::logic_error("oracle cross_covariance_jacobian: D-SKI backend only");
+  PointStencil st = point_stencil(dski_->grid(), x, cfg_.order);
+  const Index N = dski_->size();
+  Mat J(N, d_);
+  for (int p = 0; p < d_; ++p) {
+    Vec w(static_cast<size_t>(dski_->grid().size()), 0.0);
+    for (size_t c = 0; c < st.indices.size(); ++c) w[size_t(st.indices[c])] = st.derivative(c, p);
+    Vec kw(w.size());
+    dski_->grid_operator().mvm(w.data(), kw.data());
+    Vec col = dski_->stacked_apply(kw.data());
+    for (Index i = 0; i < N; ++i) J(i, p) = col[size_t(i)];
+  }
+  return J;
+}
+
 double GpModel::predict_variance_pivchol(const double* x) {  // gp.cpp:511-517
   const Preconditioner* M = preconditioner();
   if (!M) throw std::logic_error("pivoted Cholesky variance needs the preconditioner enabled");

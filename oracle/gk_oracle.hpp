@@ -377,6 +377,7 @@ class GpModel {
   std::pair<Vec, Mat> predict_mean_grad(const double* Xtest, Index T);
   double predict_variance_pivchol(const double* x);
   Vec solve(const double* b);                     // gp.cpp:143-158
+  Mat cross_covariance_jacobian(const double* x);  // gp.cpp:431-461 (D-SKI)
   double predict_variance_exact(const double* x);  // gp.cpp:499-502
   Vec predict_variance_randomized(const double* Xt /*T×d col-major*/, Index T, int probes, std::uint64_t seed);
   Vec cross_covariance(const double* x);

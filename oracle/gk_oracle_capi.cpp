@@ -472,6 +472,12 @@ int orc_gp_lml_gradient(void* m, int probes, double* grad, int* nparams) {
 int orc_gp_dlogell_apply(void* m, const double* v, double* out) {
   return guard([&] { copy_out(static_cast<GpModel*>(m)->dlogell_apply(v), out); });
 }
+int orc_gp_cross_covariance(void* m, const double* x, double* out) {
+  return guard([&] { copy_out(static_cast<GpModel*>(m)->cross_covariance(x), out); });
+}
+int orc_gp_cross_covariance_jacobian(void* m, const double* x, double* out) {
+  return guard([&] { copy_out(static_cast<GpModel*>(m)->cross_covariance_jacobian(x).a, out); });
+}
 int orc_gp_predict_variance_exact(void* m, const double* x, double* out) {
   return guard([&] { *out = static_cast<GpModel*>(m)->predict_variance_exact(x); });
 }

@@ -114,6 +114,7 @@ _SIGS = {
     "gk_lml_gradient": (C.c_int, [_vp, _vp, _dp, C.c_int, _u64, C.c_double, C.c_int, _dp, _ip]),
     "gk_trace_estimate": (C.c_int, [_vp, _vp, C.c_int, _u64, _d, C.c_int, _vp, _dp]),
     "gk_dski_predict_mean_grad": (C.c_int, [_vp, _dp, _d, _dp, _i64, _dp, _dp]),
+    "gk_dski_cross_covariance_jacobian": (C.c_int, [_vp, _dp, _i64, _dp, _i64]),
     "gk_dski_cross_covariance": (C.c_int, [_vp, _dp, _i64, _dp, _i64]),
     "gk_make_dataset": (C.c_int, [C.c_int, _u64, _i64p, _ip, _dp, _dp, _dp]),
 }
@@ -420,6 +421,15 @@ class DskiOperator(LinearOperator):
         """out = B w + noise·v on device pointers (internal layout): the last
         stage of a grid-slab sharded MVM."""
         _check(_lib.gk_dski_gather_dev(self._h, dW, dV, dOut, nrhs, stream))
+
+    def cross_covariance_jacobian(self, Xtest):
+        """GpModel::cross_covariance_jacobian (gp.cpp:431-461), batched: array
+        (N, T, d) with [:, t, p] = ∂q(x_t)/∂x_p."""
+        Xt = _f64(Xtest, True)
+        T = Xt.shape[0]
+        J = np.empty((self.size(), T * self.d), order="F")
+        _check(_lib.gk_dski_cross_covariance_jacobian(self._h, _p(Xt), T, _p(J), self.size()))
+        return J.reshape(self.size(), self.d, T, order="F").transpose(0, 2, 1)
 
     def cross_covariance(self, Xtest):
         """GpModel::cross_covariance for D-SKI (gp.cpp:412-417), one column per test point."""

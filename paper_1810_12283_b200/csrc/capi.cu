@@ -38,7 +38,7 @@ void dski_apply(Op& o, const double* U, double* Oi, int nrhs, cudaStream_t s);
 void dski_grid_mvm(Op& o, const double* U, double* W, int nrhs, cudaStream_t s);
 void dski_predict(Op& o, const double* alpha_i, double mean, const double* dXt, i64 nT, double* dvals,
                   double* dgrads, int* dbad, cudaStream_t s);
-void dski_cross_cov(Op& o, const double* dXt, i64 nT, double* Qi, int* dbad, cudaStream_t s);
+void dski_cross_cov(Op& o, const double* dXt, i64 nT, double* Qi, int* dbad, cudaStream_t s, int dir = -1);
 void precond_quadratic(Precond& M, const double* r, int nrhs, double* out_h, cudaStream_t s);
 void pivchol_copy_L(const PivChol& f, double* out_host);
 int dskip_factor_count(const Op& o);
@@ -583,6 +583,43 @@ gk_status gk_dski_predict_mean_grad(const gk_op* h, const double* alpha, double 
       fail(GK_ERR_OUT_OF_GRID, "test point " + std::to_string(badh) + " lies outside the interior of the grid", badh);
     GK_CUDA(cudaMemcpy(values, v.p, sizeof(double) * T, cudaMemcpyDeviceToHost));
     GK_CUDA(cudaMemcpy(grads, gr.p, sizeof(double) * T * g.d, cudaMemcpyDeviceToHost));
+  });
+}
+
+// GpModel::cross_covariance_jacobian (gp.cpp:431-461, D-SKI branch) for T test
+// points: column t·d + p of J = B K_UU w_p(x_t), w_p the ∂/∂x_p point stencil.
+gk_status gk_dski_cross_covariance_jacobian(const gk_op* h, const double* Xtest, int64_t T, double* J, int64_t ldj) {
+  return guard([&] {
+    Op& op = O(h);
+    const gk_grid g = dski_grid(op);
+    if (ldj < op.N) fail(GK_ERR_ARG, "size mismatch");
+    if (T <= 0) return;
+    std::lock_guard<std::mutex> lk(op.mu);
+    DeviceGuard dg(op.device);
+    cudaStream_t s = op.stream;
+    for (i64 t0 = 0; t0 < T; t0 += kMaxRhs) {
+      const i64 nt = std::min<i64>(kMaxRhs, T - t0);
+      std::vector<double> xh(static_cast<size_t>(nt) * g.d);
+      for (int j = 0; j < g.d; ++j)
+        for (i64 i = 0; i < nt; ++i) xh[static_cast<size_t>(j * nt + i)] = Xtest[j * T + t0 + i];
+      DevBuf<double> xt(static_cast<size_t>(nt) * g.d), qi(static_cast<size_t>(op.N) * nt), qe(static_cast<size_t>(op.N) * nt);
+      DevBuf<int> bad(1);
+      xt.upload(xh.data(), xh.size(), s);
+      for (int p = 0; p < g.d; ++p) {
+        const int big = INT_MAX;
+        GK_CUDA(cudaMemcpyAsync(bad.p, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+        dski_cross_cov(op, xt.p, nt, qi.p, bad.p, s, p);
+        int badh = INT_MAX;
+        GK_CUDA(cudaMemcpy(&badh, bad.p, sizeof(int), cudaMemcpyDeviceToHost));
+        if (badh != INT_MAX)
+          fail(GK_ERR_OUT_OF_GRID,
+               "test point " + std::to_string(t0 + badh) + " lies outside the interior of the grid", t0 + badh);
+        op.from_internal(qi.p, qe.p, op.N, int(nt), s);
+        GK_CUDA(cudaMemcpy2DAsync(J + (t0 * g.d + p) * ldj, sizeof(double) * ldj * g.d, qe.p, sizeof(double) * op.N,
+                                  sizeof(double) * op.N, nt, cudaMemcpyDeviceToHost, s));
+        GK_CUDA(cudaStreamSynchronize(s));
+      }
+    }
   });
 }
 

@@ -1122,7 +1122,7 @@ __global__ void k_predict(DskiView op, const double* __restrict__ X, i64 nT, con
 template <int D, int T>
 __global__ void k_test_stencils(DskiView op, const double* __restrict__ X, i64 nT,
                                 const double* origin3, const double* h3, double* __restrict__ U,
-                                int* __restrict__ bad) {
+                                int* __restrict__ bad, int dir) {
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < nT; i += (i64)gridDim.x * blockDim.x) {
     int base[3] = {0, 0, 0};
     double w[3][T], dw[3][T];
@@ -1153,7 +1153,7 @@ __global__ void k_test_stencils(DskiView op, const double* __restrict__ X, i64 n
       }
       for (int j = 0; j < D; ++j) {
         node = node * op.m[j] + base[j] + tt[j];
-        wt *= w[j][tt[j]];
+        wt *= (j == dir ? dw[j] : w[j])[tt[j]];  // dir ≥ 0: ∂/∂x_dir stencil (point_stencil derivative)
       }
       U[node * nT + i] = wt;
     }
@@ -1889,14 +1889,14 @@ void dski_predict(Op& o, const double* alpha_i, double mean, const double* dXt, 
 }
 
 // cross_covariance for T test points (gp.cpp:412-417): Q = B K_UU w_t.
-void dski_cross_cov(Op& o, const double* dXt, i64 nT, double* Qi, int* dbad, cudaStream_t s) {
+void dski_cross_cov(Op& o, const double* dXt, i64 nT, double* Qi, int* dbad, cudaStream_t s, int dir) {
   auto& op = static_cast<DskiOp&>(o);
   op.ensure_scratch(int(nT));
   DevBuf<double> U(static_cast<size_t>(op.M) * nT), W(static_cast<size_t>(op.M) * nT);
   GK_CUDA(cudaMemsetAsync(U.p, 0, sizeof(double) * op.M * nT, s));
   const DskiView vw = op.view();
   GK_DISPATCH_DT(op.d, op.T, {
-    k_test_stencils<D, T><<<grid_blocks(nT), 256, 0, s>>>(vw, dXt, nT, op.origin_d.p, op.h_d.p, U.p, dbad);
+    k_test_stencils<D, T><<<grid_blocks(nT), 256, 0, s>>>(vw, dXt, nT, op.origin_d.p, op.h_d.p, U.p, dbad, dir);
   });
   launched("dski test stencils");
   op.kuu(U.p, W.p, int(nT), s);

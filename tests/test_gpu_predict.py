@@ -118,3 +118,20 @@ def test_predict_variance_randomized_matches_oracle(model):
         vo = om.predict_variance_randomized(Xt[:6], probes, 7)
         base = np.array([om.predict_variance_pivchol(x) for x in Xt[:6]])
         assert np.all(np.abs(vg - vo) <= 1e-7 * (np.abs(base) + np.abs(vo)) + 1e-12), (probes, vg, vo)
+
+
+def test_cross_covariance_jacobian_matches_oracle(model):
+    """∂q(x)/∂x_p (gp.cpp:431-461) per test point against the oracle, and
+    Jᵀα = the predict_mean_grad gradient (gp.cpp:480-495)."""
+    om, op, X, y, dY, Xt = model
+    J = op.cross_covariance_jacobian(Xt)
+    assert J.shape == (op.size(), Xt.shape[0], 2)
+    for t in range(Xt.shape[0]):
+        Jo = om.cross_covariance_jacobian(Xt[t])
+        assert rel(J[:, t, :], Jo) <= 1e-12, t
+        assert rel(op.cross_covariance(Xt[t:t + 1])[:, 0], om.cross_covariance(Xt[t])) <= 1e-12, t
+    alpha, _ = om.alpha()
+    _, gg = op.predict_mean_grad(alpha, y.mean(), Xt)
+    assert rel(np.einsum("ntp,n->tp", J, alpha), gg) <= 1e-11
+    with pytest.raises(gk.OutOfGridError):
+        op.cross_covariance_jacobian(np.array([[5.0, 5.0]]))

@@ -288,7 +288,18 @@ def run_gpu(args):
     its, conv = gk.cg_dev(op, Vext.data_ptr(), Xd.data_ptr(), nrhs, CONFIG["pcg_tol"], 1000, M,
                           stream=sp)
     torch.cuda.synchronize()
+    t_pcg_first = time.perf_counter() - t0
+    # the same solve again: steady state (plans, graphs and workspaces cached
+    # on the operator), what every later solve of a hyperparameter loop costs
+    t0 = time.perf_counter()
+    its, conv = gk.cg_dev(op, Vext.data_ptr(), Xd.data_ptr(), nrhs, CONFIG["pcg_tol"], 1000, M,
+                          stream=sp)
+    torch.cuda.synchronize()
     t_pcg = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    slq = gk.slq_logdet(op, CONFIG["slq_probes"], CONFIG["slq_steps"], 0, 0.5 * 1e-4,
+                        probe_offset=rank * CONFIG["slq_probes"])
+    t_slq_first = time.perf_counter() - t0
     t0 = time.perf_counter()
     slq = gk.slq_logdet(op, CONFIG["slq_probes"], CONFIG["slq_steps"], 0, 0.5 * 1e-4,
                         probe_offset=rank * CONFIG["slq_probes"])
@@ -299,10 +310,10 @@ def run_gpu(args):
                                               world * CONFIG["slq_probes"], device=dev)
         slq_logdet = sharding.ordered_mean(est)
     t_slq = time.perf_counter() - t0
-    solve = torch.tensor([t_pre, t_pcg, t_slq], device=dev, dtype=torch.float64)
+    solve = torch.tensor([t_pre, t_pcg, t_slq, t_pcg_first, t_slq_first], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(solve, op=dist.ReduceOp.MAX)
-    t_pre, t_pcg, t_slq = [float(v) for v in solve.tolist()]
+    t_pre, t_pcg, t_slq, t_pcg_first, t_slq_first = [float(v) for v in solve.tolist()]
 
     c4 = None
     if not args.no_c4:
@@ -345,6 +356,10 @@ def run_gpu(args):
                              "achieved_gbs": mvm_bytes / (ms * 1e-3) / 1e9,
                              "frac_hbm": mvm_bytes / (ms * 1e-3) / 1e9 / hbm},
             "solve": {"precond_build_s": t_pre, "pcg_s": t_pcg, "slq_s": t_slq,
+                      "pcg_first_call_s": t_pcg_first, "slq_first_call_s": t_slq_first,
+                      "timing": "host wall clock around each call with device syncs, max over ranks; "
+                                "*_s = second identical call (steady state), *_first_call_s includes "
+                                "one-time plan/graph/workspace setup",
                       "pcg_plus_slq_s": t_pcg + t_slq, "pcg_iterations": [int(v) for v in its],
                       "pcg_converged": int(np.sum(conv)), "slq_logdet": slq_logdet,
                       "slq_probes_total": world * CONFIG["slq_probes"],
@@ -424,8 +439,20 @@ def c4_slab(args, world, rank, local, dist):
         its, conv = gk.cg_dev(op1, bd.data_ptr(), xd.data_ptr(), 1, 1e-4, 1000, M)
         torch.cuda.synchronize()
         t_pcg = time.perf_counter() - t0
+        us_it = t_pcg / max(1, int(its[0])) * 1e6
+        # HBM roofline of one iteration: the N×200 Woodbury factor Q1 (720 MB,
+        # far above L2) is streamed twice (Q1ᵀr, then Q1·c), plus the 1-RHS
+        # MVM and ~8 N-vectors of PCG state traffic
+        Nn, kk = sop.size(), 200
+        it_bytes = 2.0 * 8 * Nn * kk + dski_bytes(Nn, X.shape[0], 2, grid.size(), 1, 0) + 8.0 * 8 * Nn
+        peaks = measured_peaks()
+        hbm = float(peaks.get("hbm_gbs", 6650.0))
         solve = {"precond_build_s": t_pre, "pcg_s": t_pcg, "pcg_iterations": int(its[0]),
-                 "pcg_converged": int(conv[0]), "us_per_iteration": t_pcg / max(1, int(its[0])) * 1e6,
+                 "pcg_converged": int(conv[0]), "us_per_iteration": us_it,
+                 "roofline": {"bound": "hbm", "bytes_per_iteration": it_bytes,
+                              "achieved": it_bytes / (us_it * 1e-6) / 1e9, "peak": hbm, "unit": "GB/s",
+                              "frac": it_bytes / (us_it * 1e-6) / 1e9 / hbm,
+                              "bytes_formula": "2*8*N*k (Q1 twice) + MVM bytes (SURVEY 8(d), 1 RHS) + 8*8*N"},
                  "parallelism": "1 GPU (the PCG itself is not slab-sharded)"}
     return {"workload": "C4: D-SKI d=2 n=150000 (N=450000) grid 400x400 SE ell=0.02 sigma=1e-2, 1 RHS", "solve": solve,
             "parallelism": f"grid-slab x{world} (NCCL all-reduce of the grid vector per MVM)",

@@ -707,12 +707,16 @@ gk_status gk_pcg(const gk_op* h, const gk_precond* M, const double* B, int64_t l
     std::unique_lock<std::mutex> plk;
     if (P) plk = std::unique_lock<std::mutex>(P->mu);
     const int chunk = int(std::min<i64>(nrhs, 256));
-    DevBuf<double> e(static_cast<size_t>(op.N) * chunk), bi(static_cast<size_t>(op.N) * chunk), xi(static_cast<size_t>(op.N) * chunk);
+    // the operator's grow-only scratch (held under op.mu): no per-solve cudaMalloc/cudaFree
+    op.scratch_a.reserve(static_cast<size_t>(op.N) * chunk);
+    op.scratch_b.reserve(static_cast<size_t>(op.N) * chunk);
+    op.scratch_c.reserve(static_cast<size_t>(op.N) * chunk);
+    double *e = op.scratch_c.p, *bi = op.scratch_a.p, *xi = op.scratch_b.p;
     for (i64 c0 = 0; c0 < nrhs; c0 += chunk) {
       const int nb = int(std::min<i64>(chunk, nrhs - c0));
-      upload_internal(op, B + c0 * ldb, ldb, e.p, bi.p, nb, s);
-      PcgResult r = pcg_internal(op, P, bi.p, xi.p, nb, tol, maxit, history != nullptr, s);
-      download_internal(op, xi.p, e.p, X + c0 * ldx, ldx, nb, s);
+      upload_internal(op, B + c0 * ldb, ldb, e, bi, nb, s);
+      PcgResult r = pcg_internal(op, P, bi, xi, nb, tol, maxit, history != nullptr, s);
+      download_internal(op, xi, e, X + c0 * ldx, ldx, nb, s);
       GK_CUDA(cudaStreamSynchronize(s));
       for (int b = 0; b < nb; ++b) {
         if (iterations) iterations[c0 + b] = r.iterations[static_cast<size_t>(b)];

@@ -169,6 +169,9 @@ struct Op {
   HostBuf slq_h;  // pinned probe staging
   DevBuf<int> lz_wsi;
   HostBuf pinned;
+  // PCG workspace, fused-step plan and instantiated iteration graph, reused
+  // across solves (solvers.cu PcgCache; type-erased here)
+  std::shared_ptr<void> pcg_cache;
   // host-buffer MVM pipeline (gk_op_mvm): copy-in / compute / copy-out streams
   cudaStream_t io_in = nullptr, io_out = nullptr, io_pin = nullptr, io_pout = nullptr;
   std::vector<cudaEvent_t> io_events;

@@ -1472,17 +1472,66 @@ __global__ void __launch_bounds__(320) k_rademacher_mt(const unsigned long long*
 }  // namespace
 
 // ================================================================ PCG driver
+// Per-operator PCG state kept between solves (under the operator's mutex):
+// the workspace (grow-only), the fused-step plan, the pinned poll slots and
+// the instantiated iteration graph. Every solve re-captures its iterations
+// (a host-side enqueue) and refreshes the cached executable with
+// cudaGraphExecUpdate, so the graph always carries this call's pointers and
+// parameters; only a topology change re-instantiates. Re-allocating these
+// per call (cudaMalloc/cudaFree, cudaMallocHost, cudaGraphInstantiate) cost
+// ~6 ms per solve.
+struct PcgCache {
+  DevBuf<double> R, Zb, Pb, AP, part, prz, sc;
+  DevBuf<int> si;
+  PcgVecPlan vplan;
+  i64 vN = -1;
+  int vnrhs = -1, vk = -1, vtune = -1;
+  HostBuf poll;  // 2 pinned slots (lag-one polling of the active count)
+  cudaGraphExec_t exec = nullptr;
+  cudaEvent_t evs[2] = {nullptr, nullptr};
+  ~PcgCache() {
+    if (exec) cudaGraphExecDestroy(exec);
+    for (auto e : evs)
+      if (e) cudaEventDestroy(e);
+  }
+};
+
+static PcgCache& pcg_cache(Op& op) {
+  if (!op.pcg_cache) op.pcg_cache = std::make_shared<PcgCache>();
+  PcgCache& c = *static_cast<PcgCache*>(op.pcg_cache.get());
+  if (!c.evs[0])
+    for (auto& e : c.evs) GK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return c;
+}
+
 PcgResult pcg_internal(Op& op, Precond* M, const double* B, double* X, int nrhs, double tol, int maxit,
                        bool want_history, cudaStream_t s) {
   if (nrhs < 1 || nrhs > RT) fail(GK_ERR_ARG, "pcg: nrhs must be in [1, 256]");
   if (maxit < 0) fail(GK_ERR_ARG, "pcg: max_iterations must be >= 0");
   const i64 N = op.N;
   const i64 tot = N * nrhs;
-  DevBuf<double> R(static_cast<size_t>(tot)), Zb(static_cast<size_t>(tot)), Pb(static_cast<size_t>(tot)), AP(static_cast<size_t>(tot));
-  DevBuf<double> part(static_cast<size_t>(RB) * nrhs * 3);
-  DevBuf<double> prz(static_cast<size_t>((N + 63) / 64 + RB) * nrhs);  // r·z partials of the precond apply
-  DevBuf<double> sc(static_cast<size_t>(nrhs) * 4 + static_cast<size_t>(maxit + 1) * nrhs);
-  DevBuf<int> si(static_cast<size_t>(nrhs) * 4 + 1);
+  const bool tprof = std::getenv("GK_PCG_TIME") != nullptr;
+  auto tq = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!tprof) return;
+    GK_CUDA(cudaStreamSynchronize(s));
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[pcg time] %s %.3f ms\n", what, std::chrono::duration<double, std::milli>(now - tq).count());
+    tq = now;
+  };
+  PcgCache& cache = pcg_cache(op);
+  DevBuf<double>&R = cache.R, &Zb = cache.Zb, &Pb = cache.Pb, &AP = cache.AP, &part = cache.part, &prz = cache.prz,
+                 &sc = cache.sc;
+  DevBuf<int>& si = cache.si;
+  R.reserve(static_cast<size_t>(tot));
+  Zb.reserve(static_cast<size_t>(tot));
+  Pb.reserve(static_cast<size_t>(tot));
+  AP.reserve(static_cast<size_t>(tot));
+  part.reserve(static_cast<size_t>(RB) * nrhs * 3);
+  prz.reserve(static_cast<size_t>((N + 63) / 64 + RB) * nrhs);  // r·z partials of the precond apply
+  sc.reserve(static_cast<size_t>(nrhs) * 4 + static_cast<size_t>(maxit + 1) * nrhs);
+  si.reserve(static_cast<size_t>(nrhs) * 4 + 1);
+  mark("workspace");
   CgDev st;
   st.bnorm = sc.p;
   st.rz = sc.p + nrhs;
@@ -1524,15 +1573,25 @@ PcgResult pcg_internal(Op& op, Precond* M, const double* B, double* X, int nrhs,
   GK_CUDA(cudaMemsetAsync(st.nactive, 0, sizeof(int), s));
   k_cg_init<<<nrhs, 32, 0, s>>>(st, p0, p1, p2);
   launched("pcg init");
+  mark("init (precond ensure + apply)");
 
   // fused vector step (pcg_fused.cu): one cooperative kernel per iteration
   // besides the MVM instead of six kernels (tuning "pcg_fused": 0 default =
   // fused when supported, 2 = separate kernels). Measured on C2 (32 RHS,
   // rank 50): ~126 vs ~145 µs per iteration including the MVM.
-  PcgVecPlan vplan;
+  PcgVecPlan& vplan = cache.vplan;
   const int kM = M ? int(M->k) : 0;
-  const bool vfused = g_tuning.pcg_fused.load() != 2 && pcg_vec_supported(nrhs, kM);
-  if (vfused) pcg_vec_prepare(vplan, N, nrhs, kM, op.device);
+  const int vtune = g_tuning.pcg_fused.load();
+  const bool vfused = vtune != 2 && pcg_vec_supported(nrhs, kM);
+  if (vfused && (cache.vN != N || cache.vnrhs != nrhs || cache.vk != kM || cache.vtune != vtune ||
+                 std::getenv("GK_PCG_PROF"))) {
+    pcg_vec_prepare(vplan, N, nrhs, kM, op.device);
+    cache.vN = N;
+    cache.vnrhs = nrhs;
+    cache.vk = kM;
+    cache.vtune = vtune;
+  }
+  mark("vector-step plan");
 
   // one iteration, captured as a graph
   auto iteration = [&](cudaStream_t cs) {
@@ -1572,8 +1631,8 @@ PcgResult pcg_internal(Op& op, Precond* M, const double* B, double* X, int nrhs,
     launched("pcg pupdate");
   };
 
-  int* nact_h = nullptr;
-  GK_CUDA(cudaMallocHost(&nact_h, 2 * sizeof(int)));
+  cache.poll.reserve(2);
+  int* nact_h = reinterpret_cast<int*>(cache.poll.p);  // 2 ints in a pinned double slot pair
   GK_CUDA(cudaMemcpyAsync(nact_h, st.nactive, sizeof(int), cudaMemcpyDeviceToHost, s));
   GK_CUDA(cudaStreamSynchronize(s));
   bool persisted = false;
@@ -1597,8 +1656,7 @@ PcgResult pcg_internal(Op& op, Precond* M, const double* B, double* X, int nrhs,
     va.nrhs = nrhs;
     const int PI = 32;
     const int max_launches = (maxit + PI - 1) / PI + 1;
-    cudaEvent_t evs[2];
-    for (auto& e : evs) GK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaEvent_t* evs = cache.evs;
     for (int j = 0; j < max_launches; ++j) {
       if (!op.pcg_persist(vplan, va, Pb.p, AP.p, nrhs, PI, s)) break;  // j == 0: no persistent path
       persisted = true;
@@ -1610,11 +1668,11 @@ PcgResult pcg_internal(Op& op, Precond* M, const double* B, double* X, int nrhs,
       }
     }
     GK_CUDA(cudaStreamSynchronize(s));
-    for (auto e : evs) cudaEventDestroy(e);
   }
   if (!persisted && *nact_h > 0 && maxit > 0) {
     // warm the operator's scratch outside capture, then capture ITER iterations
     op.mvm(Pb.p, AP.p, nrhs, s);
+    mark("warm MVM");
     const int ITER = 4;
     // capture on the operator's private stream (capturing the legacy default
     // stream is not permitted); the graph is then launched on `s`.
@@ -1627,15 +1685,25 @@ PcgResult pcg_internal(Op& op, Precond* M, const double* B, double* X, int nrhs,
     GK_CUDA(cudaStreamEndCapture(cs, &graph));
     const i64 nodes = g_launches.load() - before;
     g_launches.fetch_sub(nodes);
-    cudaGraphExec_t exec;
-    GK_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    // refresh the cached executable with this capture (same topology: only
+    // node parameters change); instantiate only when that is refused
+    if (cache.exec) {
+      cudaGraphExecUpdateResultInfo info;
+      if (cudaGraphExecUpdate(cache.exec, graph, &info) != cudaSuccess) {
+        (void)cudaGetLastError();
+        cudaGraphExecDestroy(cache.exec);
+        cache.exec = nullptr;
+      }
+    }
+    if (!cache.exec) GK_CUDA(cudaGraphInstantiate(&cache.exec, graph, 0));
+    cudaGraphExec_t exec = cache.exec;
+    mark("capture + update/instantiate");
     // Lag-one polling: graph j is queued before the host waits for graph
     // j−1's active-column count, so the GPU never drains between graphs.
     // Iterations after convergence are no-ops for the converged columns (at
     // most one extra graph runs).
     const int max_launches = (maxit + ITER - 1) / ITER + 1;
-    cudaEvent_t evs[2];
-    for (auto& e : evs) GK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaEvent_t* evs = cache.evs;
     for (int j = 0; j < max_launches; ++j) {
       GK_CUDA(cudaGraphLaunch(exec, s));
       g_launches.fetch_add(nodes);
@@ -1647,12 +1715,10 @@ PcgResult pcg_internal(Op& op, Precond* M, const double* B, double* X, int nrhs,
       }
     }
     GK_CUDA(cudaStreamSynchronize(s));
-    for (auto e : evs) cudaEventDestroy(e);
-    cudaGraphExecDestroy(exec);
     cudaGraphDestroy(graph);
+    mark("iterations");
   }
   if (vfused) pcg_vec_dump(vplan);
-  cudaFreeHost(nact_h);
 
   PcgResult res;
   res.iterations.resize(static_cast<size_t>(nrhs));

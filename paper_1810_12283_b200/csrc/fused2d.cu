@@ -209,8 +209,11 @@ __device__ void f2_scatter(const F2Args& a, double* sm, unsigned long long* mbar
   const int BR = a.BR, tid = threadIdx.x, pmax = a.s_pmax;
   const int NST = a.s_nst;                                 // staging depth (cell rows in flight)
   double2* Wp = reinterpret_cast<double2*>(sm);           // [NST][pmax][2T]
-  double* Vb = sm + NST * pmax * 2 * T * 2;                // [NST][3][pmax][BR]
-  int4* Bb = reinterpret_cast<int4*>(Vb + ((NST * 3 * pmax * BR + 1) & ~1));  // [NST][pmax], 16-byte aligned
+  // [NST][3][VS]: group g of a staged row starts at element offset off_g
+  // (0 or 1) — the bulk copy starts at the even element below the row start
+  const int VS = (pmax * BR + 3) & ~1;  // even: every group copy starts 16-byte aligned
+  double* Vb = sm + NST * pmax * 2 * T * 2;
+  int4* Bb = reinterpret_cast<int4*>(Vb + NST * 3 * VS);  // [NST][pmax], 16-byte aligned
   int* CS = reinterpret_cast<int*>(Bb + NST * pmax);       // [L][csw]
   const int bl = tid % a.BRP, cslot = tid / a.BRP;
   const int nspl = a.s_nspl, half = cslot % nspl, ccol = cslot / nspl;
@@ -218,9 +221,12 @@ __device__ void f2_scatter(const F2Args& a, double* sm, unsigned long long* mbar
                                         ~uintptr_t(15));  // [nspl-1][T-1][TC][BR], 16-byte aligned
   const int items = a.s_strips * a.s_segs * a.chunks;
   const size_t gstride = (size_t)a.n * a.nrhs;
-  // TMA bulk copies (RP = 2: every source row is 16-byte aligned) or
-  // per-thread cp.async (odd RHS counts); both complete on mbar[buf]
-  const bool tma = RP == 2;
+  // TMA bulk copies (RP = 2: every source row is 16-byte aligned; or one
+  // chunk holding all right-hand sides, where each group's rows are one
+  // contiguous range copied from the even element at or below its start, the
+  // odd tail element stored by the issuing lane) or per-thread cp.async;
+  // both complete on mbar[buf]
+  const bool tma = RP == 2 || a.BR == a.nrhs;
   unsigned phase = 0;  // parity bit per stage buffer (uniform across threads)
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
     const int strip = item % a.s_strips;
@@ -238,6 +244,7 @@ __device__ void f2_scatter(const F2Args& a, double* sm, unsigned long long* mbar
     const bool active = ccol < a.s_TC && col < Cend && lane_ok;
     auto xslot = [&](int h, int t) { return X + ((((h - 1) * (T - 1) + t) * a.s_TC + ccol) * BR + bl * RP); };
     __syncthreads();  // previous item done with CS and the stage buffers
+#pragma unroll 4
     for (int e = tid; e < nrows * csw; e += F2_THREADS) {
       const int r = e / csw, c = e - r * csw;
       CS[e] = __ldg(a.cell_start + (size_t)(R + r) * a.nb1 + clo + c);
@@ -247,7 +254,7 @@ __device__ void f2_scatter(const F2Args& a, double* sm, unsigned long long* mbar
       const int* cs = CS + i * csw;
       const int P0 = cs[0], cnt = cs[csw - 1] - P0;
       double2* wdst = Wp + (size_t)buf * pmax * 2 * T;
-      double* vdst = Vb + (size_t)buf * 3 * pmax * BR;
+      double* vdst = Vb + (size_t)buf * 3 * VS;
       int4* bdst = Bb + (size_t)buf * pmax;
       if (tma) {
         // the last warp issues (idle in the compute when the strip leaves it
@@ -257,14 +264,26 @@ __device__ void f2_scatter(const F2Args& a, double* sm, unsigned long long* mbar
         if (lane >= 0) {
           if (lane == 0) {
             fence_proxy_async();
-            mbar_expect_tx(mbar + buf, unsigned(cnt) * unsigned(2 * T * 16 + 16 + 3 * BR * 8));
+            unsigned vbytes = unsigned(cnt) * unsigned(3 * BR * 8);
+            if (whole && cnt > 0) {
+              vbytes = 0;
+              for (int g = 0; g < 3; ++g) {
+                const size_t s0 = g * gstride + (size_t)P0 * a.nrhs, e0 = s0 + (size_t)cnt * a.nrhs;
+                const size_t se = s0 & ~size_t(1), len = e0 - se;
+                vbytes += unsigned(len & ~size_t(1)) * 8;
+                if (len & 1) vdst[(size_t)g * VS + len - 1] = __ldg(a.v + e0 - 1);  // odd tail: before the arrive
+              }
+            }
+            mbar_expect_tx(mbar + buf, unsigned(cnt) * unsigned(2 * T * 16 + 16) + vbytes);
             if (cnt > 0) {
               bulk_g2s(wdst, a.wd + (size_t)P0 * 2 * T, unsigned(cnt) * 2 * T * 16, mbar + buf);
               bulk_g2s(bdst, a.base + P0, unsigned(cnt) * 16, mbar + buf);
               if (whole)
-                for (int g = 0; g < 3; ++g)
-                  bulk_g2s(vdst + (size_t)g * pmax * BR, a.v + g * gstride + (size_t)P0 * a.nrhs,
-                           unsigned(cnt) * BR * 8, mbar + buf);
+                for (int g = 0; g < 3; ++g) {
+                  const size_t s0 = g * gstride + (size_t)P0 * a.nrhs, e0 = s0 + (size_t)cnt * a.nrhs;
+                  const size_t se = s0 & ~size_t(1), len = e0 - se;
+                  if (len >= 2) bulk_g2s(vdst + (size_t)g * VS, a.v + se, unsigned(len & ~size_t(1)) * 8, mbar + buf);
+                }
             }
           }
           if (!whole) {
@@ -272,7 +291,7 @@ __device__ void f2_scatter(const F2Args& a, double* sm, unsigned long long* mbar
             for (int q = lane; q < 3 * cnt; q += 32) {
               const int g = q >= 2 * cnt ? 2 : (q >= cnt ? 1 : 0);
               const int p = q - g * cnt;
-              bulk_g2s(vdst + ((size_t)g * pmax + p) * BR, a.v + g * gstride + (size_t)(P0 + p) * a.nrhs + bc0,
+              bulk_g2s(vdst + (size_t)g * VS + (size_t)p * BR, a.v + g * gstride + (size_t)(P0 + p) * a.nrhs + bc0,
                        unsigned(BR) * 8, mbar + buf);
             }
           }
@@ -284,7 +303,7 @@ __device__ void f2_scatter(const F2Args& a, double* sm, unsigned long long* mbar
           for (int q = cslot; q < 3 * cnt; q += F2_THREADS / a.BRP) {
             const int g = q >= 2 * cnt ? 2 : (q >= cnt ? 1 : 0);
             const int p = q - g * cnt;
-            cpa_rp<RP>(vdst + ((size_t)g * pmax + p) * BR + bl * RP,
+            cpa_rp<RP>(vdst + (size_t)g * VS + (size_t)p * BR + bl * RP,
                        a.v + g * gstride + (size_t)(P0 + p) * a.nrhs + rb);
           }
         cpa_commit();
@@ -316,17 +335,25 @@ __device__ void f2_scatter(const F2Args& a, double* sm, unsigned long long* mbar
         const int P0 = cs[0];
         const int q0 = cs[tlo] - P0, q1 = cs[thi + 1] - P0;
         const double2* W = Wp + (size_t)buf * pmax * 2 * T;
-        const double* V = Vb + (size_t)buf * 3 * pmax * BR + bl * RP;
+        const double* V = Vb + (size_t)buf * 3 * VS + bl * RP;
+        int vo1 = VS, vo2 = 2 * VS;  // group offsets (+ the start parity of each group's copy)
+        const double* V0 = V;
+        if (tma && BR == a.nrhs) {
+          const size_t s0 = (size_t)P0 * a.nrhs;
+          V0 = V + (s0 & 1);
+          vo1 += int(((gstride + s0) & 1)) - int(s0 & 1);
+          vo2 += int(((2 * gstride + s0) & 1)) - int(s0 & 1);
+        }
         const int4* B4 = Bb + (size_t)buf * pmax;
 #pragma unroll 2
         for (int p = q0 + half; p < q1; p += nspl) {
           const int tl = col - B4[p].y;
           const double2* wr = W + p * 2 * T;
-          const double* vr = V + p * BR;
+          const double* vr = V0 + p * BR;
           double v0[RP], v1[RP], v2[RP];
           vload<RP>(vr, v0);
-          vload<RP>(vr + pmax * BR, v1);
-          vload<RP>(vr + 2 * pmax * BR, v2);
+          vload<RP>(vr + vo1, v1);
+          vload<RP>(vr + vo2, v2);
           const double2 w1 = wr[T + tl];
           double A[RP], Cc[RP];
 #pragma unroll
@@ -453,6 +480,7 @@ __device__ __noinline__ void f2_toeplitz(const double* ts, int M, int Mp, int ba
   double* Hs0 = Bs1 + Mp * 8;              // [Mp][8] halo staging, one per B buffer
   double* Hs1 = Hs0 + Mp * 8;
   const bool contiguous = (Q % 8) == 0;
+  cpa_wait0();  // this thread's copies of the Toeplitz sequences (f2_body)
   __syncthreads();
   for (int e = tid; e < ND * 32; e += F2_THREADS) {
     const int D = e / 32 + Dlo, ln = e % 32;
@@ -483,33 +511,47 @@ __device__ __noinline__ void f2_toeplitz(const double* ts, int M, int Mp, int ba
         }
       }
     } else {
+      // 8 independent loads in flight per thread (one L2 round trip per batch)
 #pragma unroll 1
-      for (int e = tid; e < M * 8; e += F2_THREADS) {
-        const int c = e >> 3, j = e & 7;
-        const int col = col0 + j;
-        double val = 0.0;
-        if (col < ncols) {
-          const int p = col / Q, q = col - p * Q;
-          const size_t o = (size_t)p * M * Q + q + (size_t)c * Q;
-          val = X[o];
-          if (halo.row(p)) val += halo.h[o];
+      for (int e0 = tid; e0 < M * 8; e0 += F2_THREADS * 8) {
+        double val[8];
+        int dst[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e = e0 + u * F2_THREADS;
+          int c, j;
+          c = e >> 3;
+          j = e & 7;
+          const int col = col0 + j;
+          val[u] = 0.0;
+          dst[u] = -1;
+          if (e < M * 8) {
+            dst[u] = c * 8 + j;
+            if (col < ncols) {
+              const int p = col / Q, q = col - p * Q;
+              const size_t o = (size_t)p * M * Q + q + (size_t)c * Q;
+              val[u] = X[o];
+              if (halo.row(p)) val[u] += halo.h[o];
+            }
+          }
         }
-        B[c * 8 + j] = val;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (dst[u] >= 0) B[dst[u]] = val[u];
       }
     }
     cpa_commit();
   };
   int buf = 0;
   if ((int)blockIdx.x < items) issue(blockIdx.x / nsplit, Bs0, Hs0);
-  // nsplit is 1 or 2: item -> (column group, split) without integer division
-  const int sh = nsplit == 2 ? 1 : 0;
-  const int per = (mtiles + nsplit - 1) >> sh;
+  // item -> (column group, split): one division per item
+  const int per = (mtiles + nsplit - 1) / nsplit;
   for (int it = blockIdx.x; it < items; it += gridDim.x) {
-    const int cg = it >> sh, sp = it - (cg << sh);
+    const int cg = it / nsplit, sp = it - cg * nsplit;
     const int nxt = it + gridDim.x;
     // the next item reuses the staged slab when it has the same column group
     // (never with gridDim >= nsplit); otherwise prefetch into the other buffer
-    const int nxt_cg = nxt < items ? nxt >> sh : -1;
+    const int nxt_cg = nxt < items ? nxt / nsplit : -1;
     if (nxt_cg >= 0 && nxt_cg != cg) {
       issue(nxt_cg, buf ? Bs0 : Bs1, buf ? Hs0 : Hs1);
       cpa_wait1();
@@ -880,8 +922,17 @@ __device__ __forceinline__ void f2_body(const F2Args& a) {
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   stamp(a, 0);
-  for (int i = threadIdx.x; i < a.m0p; i += F2_THREADS) ts0[i] = i < a.m0 ? __ldg(a.t0 + i) : 0.0;
-  for (int i = threadIdx.x; i < a.m1p; i += F2_THREADS) ts1[i] = i < a.m1 ? __ldg(a.t1 + i) : 0.0;
+  // the Toeplitz sequences are needed from phase T1 on: their copies fly
+  // while the scatter runs (f2_toeplitz waits for them)
+  for (int i = threadIdx.x; i < a.m0p; i += F2_THREADS) {
+    if (i < a.m0) cpa8(ts0 + i, a.t0 + i);
+    else ts0[i] = 0.0;
+  }
+  for (int i = threadIdx.x; i < a.m1p; i += F2_THREADS) {
+    if (i < a.m1) cpa8(ts1 + i, a.t1 + i);
+    else ts1[i] = 0.0;
+  }
+  cpa_commit();
   __syncthreads();
   if (!(a.skip & 1)) {
     if (a.s_mode == 1) f2_scatter_direct<T, RP>(a);
@@ -908,6 +959,7 @@ __device__ __forceinline__ void f2_body(const F2Args& a) {
     if (a.g_mode == 1) f2_gather_direct<T, RP>(a);
     else f2_gather<T, RP>(a, work);
   }
+  cpa_wait0();  // nothing in flight into shared memory past the body (skip masks)
   __syncthreads();
   stamp(a, 7);
   if (threadIdx.x == 0)  // the shared memory may be reused (persistent PCG kernel)
@@ -939,7 +991,8 @@ size_t smem_bytes(const Fused2dGeom& g, const Fused2dPlan& p) {
   const int T = g.T;
   const int m0p = (g.m0 + 7) / 8 * 8, m1p = (g.m1 + 7) / 8 * 8;
   const size_t base = size_t(m0p + m1p) * 8 + 64;
-  const size_t S = size_t(p.s_nst) * p.s_pmax * (2 * T * 16 + 3 * p.BR * 8) + 8 + size_t(p.s_nst) * p.s_pmax * 16 +
+  const size_t S = size_t(p.s_nst) * p.s_pmax * (2 * T * 16 + 3 * p.BR * 8) + size_t(p.s_nst) * 3 * 3 * 8 + 8 +
+                   size_t(p.s_nst) * p.s_pmax * 16 +
                    size_t(p.s_L * p.s_csw) * 4 + 16 +
                    size_t(p.s_nspl - 1) * (T - 1) * p.s_TC * p.BR * 8;
   auto tbytes = [&](int M, int band, bool halo) {
@@ -1012,9 +1065,11 @@ void decompose(const Fused2dGeom& g, const std::vector<int>& cs, Fused2dPlan& p,
     for (int r = 0; r < g.nb0; ++r)
       p.g_pmax = std::max(p.g_pmax, cs[size_t(r) * g.nb1 + Cend] - cs[size_t(r) * g.nb1 + C]);
   }
-  // Toeplitz: split the m-tiles of each 8-column group when there are few groups
+  // Toeplitz: split the m-tiles of each 8-column group when there are fewer
+  // groups than CTAs (few right-hand sides), so every CTA gets an item
   const i64 cg = i64(std::max(g.m0, g.m1)) * p.nrhs / 8 + 1;  // 8-column groups of the mode-1 product
-  p.t_split = cg >= ctas / 2 ? 1 : 2;  // split only when there are very few column groups
+  const int mt = (std::max(g.m0, g.m1) + 7) / 8;
+  p.t_split = cg >= ctas / 2 ? 1 : int(std::max<i64>(2, std::min<i64>(mt / 2, ctas / cg)));
   if (const int o = g_tuning.f2_tsplit.load(); o > 0) p.t_split = o;
 }
 

@@ -10,6 +10,9 @@ import paper_1810_12283_b200 as gk  # noqa: E402
 from tools.fused_timing import problem  # noqa: E402
 
 gk.set_tuning("fused_prof", 1)
+for kv in filter(None, os.environ.get("GK_TUNE", "").split(",")):  # e.g. GK_TUNE=f2_tsplit=5
+    k, v = kv.split("=")
+    gk.set_tuning(k, int(v))
 names = ["scatter", "barrier1", "mode1", "barrier2", "mode0", "barrier3", "gather"]
 cases = [("C2", 32), ("C1", 32), ("C2", 1), ("C4", 1)]
 if len(sys.argv) > 1:

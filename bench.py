@@ -424,14 +424,37 @@ def c4_slab(args, world, rank, local, dist):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     solve = None
-    if rank == 0 and not args.no_c4_solve:  # BASELINE C4: rank-200 pivoted Cholesky + PCG (one GPU, unsharded)
+    fused = None
+    if rank == 0:  # the unsharded single-GPU MVM: the one-launch kernel (fused2d.cu), no all-reduce
         op1 = gk.DskiOperator(gk.KernelSpec(0.02, 1.0), grid, X, (1e-2, 1e-2), device=local)
+        bd = torch.from_numpy(np.ascontiguousarray(b)).to(dev)
+        V1, O1 = torch.empty_like(bd), torch.empty_like(bd)
+        op1.to_internal_dev(bd.data_ptr(), V1.data_ptr(), 1, stream=st.cuda_stream)
+        l0 = gk.kernel_launch_count()
+        for _ in range(5):
+            op1.stage_dev(3, V1.data_ptr(), O1.data_ptr(), 1, stream=st.cuda_stream)
+        per_mvm = (gk.kernel_launch_count() - l0) / 5
+        ev1 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+        torch.cuda.synchronize()
+        for e0, e1 in ev1:
+            e0.record(st)
+            op1.stage_dev(3, V1.data_ptr(), O1.data_ptr(), 1, stream=st.cuda_stream)
+            e1.record(st)
+        torch.cuda.synchronize()
+        ms1 = float(np.median([a.elapsed_time(b_) for a, b_ in ev1]))
+        mb = dski_bytes(op1.size(), X.shape[0], 2, grid.size(), 1, 0)
+        hbm1 = float(measured_peaks().get("hbm_gbs", 6650.0))
+        fused = {"ms_per_mvm": ms1, "value": op1.size() / (ms1 * 1e-3), "unit": UNIT, "gpu_launches_per_mvm": per_mvm,
+                 "roofline": {"bound": "hbm", "algorithmic_bytes": mb, "achieved": mb / (ms1 * 1e-3) / 1e9,
+                              "peak": hbm1, "unit": "GB/s", "frac": mb / (ms1 * 1e-3) / 1e9 / hbm1,
+                              "bytes_formula": "SURVEY 8(d): 8*(3*N*B + 2*n*d + 4*m*B), B = 1"},
+                 "timing": "CUDA events per MVM (L2 not evicted), median"}
+    if rank == 0 and not args.no_c4_solve:  # BASELINE C4: rank-200 pivoted Cholesky + PCG (one GPU, unsharded)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         M = gk.Preconditioner.from_pivchol(op1, gk.pivoted_cholesky(op1, 200, kernel_part=True))
         torch.cuda.synchronize()
         t_pre = time.perf_counter() - t0
-        bd = torch.from_numpy(np.ascontiguousarray(b)).to(dev)
         xd = torch.empty_like(bd)
         gk.cg_dev(op1, bd.data_ptr(), xd.data_ptr(), 1, 1e-4, 5, M)  # plans / graphs built outside the timing
         torch.cuda.synchronize()
@@ -455,6 +478,7 @@ def c4_slab(args, world, rank, local, dist):
                               "bytes_formula": "2*8*N*k (Q1 twice) + MVM bytes (SURVEY 8(d), 1 RHS) + 8*8*N"},
                  "parallelism": "1 GPU (the PCG itself is not slab-sharded)"}
     return {"workload": "C4: D-SKI d=2 n=150000 (N=450000) grid 400x400 SE ell=0.02 sigma=1e-2, 1 RHS", "solve": solve,
+            "fused_1gpu": fused,
             "parallelism": f"grid-slab x{world} (NCCL all-reduce of the grid vector per MVM)",
             "scaling": "strong", "ms_per_mvm": ms, "value": sop.size() * nrhs / (ms * 1e-3),
             "unit": UNIT, "local_points": int(sop.mine.size), "build_s": build_s,

@@ -610,6 +610,126 @@ __global__ void __launch_bounds__(256) k_scatter_units3(DskiView op, const int2*
   }
 }
 
+// d = 3 scatter over node-column TILES ("per-grid-tile sorting of points"):
+// a CTA owns a TB×TB tile of node columns × a z-range [za, zb) × RC
+// right-hand sides, one thread per (column, RHS). The points whose stencils
+// reach the tile are listed once per tile in last-axis base-cell order (built
+// with the operator); chunks of E of them — base, the three (w, ∂w) stencils
+// and the 4 value/derivative rows — are staged in shared memory by cp.async
+// (double-buffered), and every thread walks the same chunk: a point that
+// covers its column adds its T contributions to the thread's rolling z
+// window, which emits node z when the walk passes base cell z. A point's v
+// rows are read once per tile instead of once per column (36× for T = 6).
+// Fixed order, no atomics: deterministic. u must be fully written by the
+// units (they partition [0, m2) for every tile).
+constexpr int B3_E = 32;
+template <int T, bool GRAD>
+__global__ void __launch_bounds__(1024, 1) k_scatter_tile3(DskiView op, const int* __restrict__ list,
+                                                          const int4* __restrict__ units, int TB, int RC,
+                                                          int tiles1, const double* __restrict__ v,
+                                                          double* __restrict__ u, int nrhs) {
+  extern __shared__ __align__(16) double b3_sm[];
+  constexpr int G = GRAD ? 4 : 1;
+  const int4 un = __ldg(units + blockIdx.x);
+  const int tile = un.x, za = un.y & 0xffff, zb = un.y >> 16, e_lo = un.z, e_hi = un.w;
+  const int K0 = (tile / tiles1) * TB, K1 = (tile % tiles1) * TB;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int r = tid % RC, c = tid / RC;
+  const int k0 = K0 + c / TB, k1 = K1 + c % TB;
+  const int rc0 = blockIdx.y * RC;
+  const bool active = c < TB * TB && k0 < op.m[0] && k1 < op.m[1] && rc0 + r < nrhs;
+  const int m2 = op.m[2];
+  const size_t gs = (size_t)op.n * nrhs;
+  // stage buffers: [2][E] int4 base | [2][E][3T] double2 | [2][G][E][RC] double
+  int4* sb = reinterpret_cast<int4*>(b3_sm);
+  double2* sw = reinterpret_cast<double2*>(sb + 2 * B3_E);
+  double* sv = reinterpret_cast<double*>(sw + 2 * B3_E * 3 * T);
+  const int rcn = min(RC, nrhs - rc0);
+  auto issue = [&](int e0, int buf) {
+    const int cnt = min(B3_E, e_hi - e0);
+    int4* db = sb + buf * B3_E;
+    double2* dw = sw + buf * B3_E * 3 * T;
+    double* dv = sv + (size_t)buf * G * B3_E * RC;
+    for (int q = tid; q < cnt * (1 + 3 * T); q += nthr) {
+      const int j = q / (1 + 3 * T), k = q - j * (1 + 3 * T);
+      const int sp = __ldg(list + e0 + j);
+      if (k == 0) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(
+                         static_cast<unsigned>(__cvta_generic_to_shared(db + j))),
+                     "l"(op.base + sp)
+                     : "memory");
+      } else {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(
+                         static_cast<unsigned>(__cvta_generic_to_shared(dw + j * 3 * T + k - 1))),
+                     "l"(op.wd + (size_t)sp * 3 * T + k - 1)
+                     : "memory");
+      }
+    }
+    for (int q = tid; q < cnt * G * rcn; q += nthr) {
+      const int j = q / (G * rcn), rest = q - j * (G * rcn), g = rest / rcn, rr = rest - g * rcn;
+      const int sp = __ldg(list + e0 + j);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(static_cast<unsigned>(
+                       __cvta_generic_to_shared(dv + ((size_t)g * B3_E + j) * RC + rr))),
+                   "l"(v + g * gs + (size_t)sp * nrhs + rc0 + rr)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  double acc[T];
+#pragma unroll
+  for (int i = 0; i < T; ++i) acc[i] = 0.0;
+  int cur = max(0, za - (T - 1));  // acc[i] <-> node cur + i
+  double* ucol = u + ((size_t)k0 * op.m[1] + k1) * m2 * nrhs + rc0 + r;
+  auto emit = [&]() {
+    if (cur >= za && active) ucol[(size_t)cur * nrhs] = acc[0];
+#pragma unroll
+    for (int i = 0; i < T - 1; ++i) acc[i] = acc[i + 1];
+    acc[T - 1] = 0.0;
+    ++cur;
+  };
+  if (e_lo < e_hi) issue(e_lo, 0);
+  int buf = 0;
+  for (int e0 = e_lo; e0 < e_hi; e0 += B3_E) {
+    if (e0 + B3_E < e_hi) {
+      issue(e0 + B3_E, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    const int cnt = min(B3_E, e_hi - e0);
+    const int4* B = sb + buf * B3_E;
+    const double2* W = sw + buf * B3_E * 3 * T;
+    const double* V = sv + (size_t)buf * G * B3_E * RC + r;
+    for (int j = 0; j < cnt; ++j) {
+      const int4 b = B[j];
+      while (cur < b.z) emit();
+      const int t0 = k0 - b.x, t1 = k1 - b.y;
+      if (active && unsigned(t0) < unsigned(T) && unsigned(t1) < unsigned(T)) {
+        const double2* w = W + j * 3 * T;
+        const double2 a0 = w[t0], a1 = w[T + t1];
+        const double v0 = V[j * RC];
+        double A, Bc = 0.0;
+        if constexpr (GRAD) {
+          const double v1 = V[(B3_E + j) * RC], v2 = V[(2 * B3_E + j) * RC], v3 = V[(3 * B3_E + j) * RC];
+          A = a1.x * (v0 * a0.x + v1 * a0.y) + a1.y * (v2 * a0.x);
+          Bc = a1.x * (v3 * a0.x);
+        } else {
+          A = a1.x * a0.x * v0;
+        }
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+          const double2 a2 = w[2 * T + t];
+          acc[t] += GRAD ? a2.x * A + a2.y * Bc : a2.x * A;
+        }
+      }
+    }
+    __syncthreads();  // buffer `buf` free for the chunk after next
+    buf ^= 1;
+  }
+  while (cur < zb) emit();
+}
+
 // d = 1 scatter: CTA per (node, RHS). The points covering node k (base cells
 // k−T+1 .. k) are ONE contiguous range of the sorted order; 256 threads stride
 // over it and reduce in a fixed shared-memory tree (deterministic). The pull
@@ -1190,6 +1310,12 @@ struct DskiOp final : Op {
   // a unit emits nodes [za, zb) of its column (nodes no point touches are 0)
   DevBuf<int4> col3_units;
   int col3_nunits = 0;
+  // tile scatter (k_scatter_tile3): per TB×TB tile of node columns the points
+  // reaching it in base-cell order (b2 major); units {tile, za | zb << 16,
+  // first entry (window halo included), end entry}
+  DevBuf<int> tile3_list;
+  DevBuf<int4> tile3_units;
+  int tile3_nunits = 0, tile3_tb = 6, tile3_tiles1 = 0;
   int max_row_pts = 0;    // d = 2: most points sharing one base row (band kernels' staging)
   DevBuf<i64> ext;        // internal row -> external row
   std::vector<i64> perm_h, inv_h;
@@ -1427,6 +1553,31 @@ void DskiOp::scatter(const double* v, double* u, int nrhs, cudaStream_t s) const
       else k_scatter_1d<4, false><<<g1, 256, 0, s>>>(vw, v, u, nrhs);
     }
     launched("dski scatter (d=1 node blocks)");
+    return;
+  }
+  // column tiles: measured faster than the per-column lists for 1-2 RHS at C3
+  // (1 RHS: 228 vs 323 us), slower for 17+ RHS (every warp walks every
+  // point of the tile; 578 vs 365 us)
+  if (d == 3 && (variant == 8 || (variant == 0 && nrhs <= 2)) && tile3_units.p) {
+    const int TB = tile3_tb;
+    const int nch = int((i64(TB) * TB * nrhs + 1023) / 1024);
+    const int RC = (nrhs + nch - 1) / nch;
+    const int nthr = (TB * TB * RC + 31) / 32 * 32;
+    const int G4 = G ? 4 : 1;
+    const size_t shm = 2 * B3_E * (16 + size_t(3) * T * 16 + size_t(G4) * RC * 8);
+    const dim3 tgrid(static_cast<unsigned>(tile3_nunits), static_cast<unsigned>(nch));
+    auto go = [&](const void* fn, auto kern) {
+      if (shm > 48 * 1024) raise_smem_limit(fn, shm);
+      kern<<<tgrid, nthr, shm, s>>>(vw, tile3_list.p, tile3_units.p, TB, RC, tile3_tiles1, v, u, nrhs);
+    };
+    if (T == 6) {
+      if (G) go((const void*)k_scatter_tile3<6, true>, k_scatter_tile3<6, true>);
+      else go((const void*)k_scatter_tile3<6, false>, k_scatter_tile3<6, false>);
+    } else {
+      if (G) go((const void*)k_scatter_tile3<4, true>, k_scatter_tile3<4, true>);
+      else go((const void*)k_scatter_tile3<4, false>, k_scatter_tile3<4, false>);
+    }
+    launched("dski scatter (d=3 column tiles)");
     return;
   }
   if (d == 3 && variant == 7 && col3_units.p) {  // balanced units over the per-column sorted lists
@@ -1801,6 +1952,55 @@ std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, cons
     }
     op->col3_nunits = int(units.size());
     op->col3_units.upload(units.data(), units.size(), st);
+    if (m2 < 65536) {  // tile lists for k_scatter_tile3 (z packed in 16 bits)
+      const int TB = op->tile3_tb;
+      const int tiles0 = (m0 + TB - 1) / TB, tiles1 = (m1 + TB - 1) / TB;
+      std::vector<int> tl;
+      std::vector<int4> tu;
+      std::vector<int> zs;  // b2 of each entry of the current tile
+      constexpr int kTileEntries = 192;
+      for (int K0 = 0; K0 < tiles0; ++K0)
+        for (int K1 = 0; K1 < tiles1; ++K1) {
+          const int e0 = int(tl.size());
+          zs.clear();
+          const int blo = std::max(0, K0 * TB - (T - 1)), bhi = std::min(nb0 - 1, K0 * TB + TB - 1);
+          const int clo = std::max(0, K1 * TB - (T - 1)), chi = std::min(nb1 - 1, K1 * TB + TB - 1);
+          for (int b2 = 0; b2 < nb2; ++b2)
+            for (int b0 = blo; b0 <= bhi; ++b0)
+              for (int b1 = clo; b1 <= chi; ++b1) {
+                const int cc = (b0 * nb1 + b1) * nb2 + b2;
+                for (int q = cstart[static_cast<size_t>(cc)]; q < cstart[static_cast<size_t>(cc) + 1]; ++q) {
+                  tl.push_back(q);
+                  zs.push_back(b2);
+                }
+              }
+          const int e1 = int(tl.size()), ne = e1 - e0;
+          // units partition [0, m2): ~kTileEntries entries with b2 in [za, zb)
+          int za = 0, ia = 0;  // ia: first local entry with b2 >= za
+          const int tile = K0 * tiles1 + K1;
+          while (za < m2) {
+            int ih = ia;
+            while (ih > 0 && zs[static_cast<size_t>(ih - 1)] >= za - (T - 1)) --ih;
+            int zb = za, ib = ia, cnt = 0;
+            while (zb < m2) {
+              int i = ib;
+              while (i < ne && zs[static_cast<size_t>(i)] == zb) ++i;
+              if (cnt > 0 && cnt + (i - ib) > kTileEntries) break;
+              cnt += i - ib;
+              ib = i;
+              ++zb;
+            }
+            if (ib >= ne) zb = m2;  // the last unit of the tile runs to the top
+            tu.push_back(make_int4(tile, za | (zb << 16), e0 + ih, e0 + ib));
+            za = zb;
+            ia = ib;
+          }
+        }
+      op->tile3_tiles1 = tiles1;
+      op->tile3_nunits = int(tu.size());
+      op->tile3_list.upload(tl.data(), std::max<size_t>(1, tl.size()), st);
+      op->tile3_units.upload(tu.data(), tu.size(), st);
+    }
     op->col3_nseg = nseg;
     op->col3_list.upload(list.data(), list.size(), st);
     op->col3_start.upload(start.data(), start.size(), st);

@@ -211,3 +211,36 @@ def test_fused_2d_variants_match_oracle(smode, gmode):
     finally:
         gk.set_tuning("f2_smode", prev[0])
         gk.set_tuning("f2_gmode", prev[1])
+
+
+@pytest.mark.parametrize("with_gradients", [True, False])
+@pytest.mark.parametrize("order", [0, 1])
+def test_d3_tile_scatter_matches_oracle(order, with_gradients):
+    """The d = 3 column-tile scatter (k_scatter_tile3; default for 1-2 RHS,
+    forced here for every count) against the oracle: points piled onto a few
+    z-levels (units that cannot split inside one base cell level), RHS counts
+    below, at and above one RHS chunk (36 columns x RC <= 1024 threads), and
+    the per-column list scatter it replaces."""
+    rng = np.random.default_rng(8)
+    X = rng.uniform(0.0, 1.0, (300, 3))
+    X[:150, 2] = 0.5 + 1e-3 * rng.standard_normal(150)  # a dense sheet: many entries per (tile, z)
+    grid = gk.Grid.cover(X, 0.05, 3, 20)
+    g = gk.DskiOperator(gk.KernelSpec(0.3, 1.0), grid, X, (0.1, 0.05), order, with_gradients)
+    r = O.DskiOperator(O.KernelSpec(0.3, 1.0), O.Grid(grid.dims, grid.origin, grid.spacing), X, (0.1, 0.05),
+                       order, with_gradients)
+    for nrhs in (1, 2, 5, 33):
+        V = rng.standard_normal((g.size(), nrhs))
+        ref = r.mvm(V)
+        prev = gk.set_tuning("scatter", 8)
+        try:
+            tile = g.mvm(V)
+        finally:
+            gk.set_tuning("scatter", prev)
+        prev = gk.set_tuning("scatter", 6)
+        try:
+            lists = g.mvm(V)
+        finally:
+            gk.set_tuning("scatter", prev)
+        assert rel(tile, ref) <= TOL
+        assert rel(tile, lists) <= 1e-13
+        assert np.array_equal(tile, g.mvm(V)) or nrhs > 2  # default path for 1-2 RHS is the tile kernel

@@ -1017,7 +1017,10 @@ void decompose(const Fused2dGeom& g, const std::vector<int>& cs, Fused2dPlan& p,
   // segments of >= T-1 cell rows (each halo row then has exactly two
   // contributors). Narrow strips and many items beat wide, thread-filled
   // strips (measured at C1/C2), so aim for about one item per CTA.
-  p.s_nspl = g_tuning.f2_nspl.load() > 0 ? g_tuning.f2_nspl.load() : 2;
+  // point split per column: 2 threads for single-RHS plans (C4: one thread
+  // per column leaves too many points per thread), 1 when several RHS lanes
+  // share a column (C1/C2 32 RHS: ~0.8 us faster, no partial combine)
+  p.s_nspl = g_tuning.f2_nspl.load() > 0 ? g_tuning.f2_nspl.load() : (p.BRP >= 2 ? 1 : 2);
   p.s_nst = g_tuning.f2_nst.load() > 0 ? std::min(4, g_tuning.f2_nst.load()) : 3;
   const int max_tc = std::max(1, F2_THREADS / p.s_nspl / p.BRP);
   const int seg_max = std::max(1, g.nb0 / std::max(1, T - 1));

@@ -149,23 +149,41 @@ __global__ void __launch_bounds__(128) k_toeplitz_dmma(const double* __restrict_
   for (int i = 0; i < WM; ++i)
 #pragma unroll
     for (int j = 0; j < WN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  for (int c0 = 0; c0 < M; c0 += BK) {
-    const int dmin = max(0, max(c0 - (a0 + BM - 1), a0 - (c0 + BK - 1)));
-    if (dmin >= band) continue;  // block-uniform
-    __syncthreads();
-    for (int idx = tid; idx < BK * BM; idx += 128) {
+  // k tiles that meet the band of rows [a0, a0 + BM): one contiguous range.
+  // The next tile's A and B values are loaded into registers while the
+  // current one computes (one global latency per launch, not per k tile).
+  constexpr int ASL = (BK * BM + 127) / 128;
+  const int lo = a0 - BK + 2 - band;  // first k-tile start whose last column is within the band
+  const int c_begin = lo <= 0 ? 0 : (lo + BK - 1) / BK * BK;
+  const int c_end = min(M, a0 + BM - 1 + band);
+  double ra[ASL], rb[SLOTS];
+  auto load = [&](int c0) {
+#pragma unroll
+    for (int r = 0; r < ASL; ++r) {
+      const int idx = tid + 128 * r;
       const int kk = idx / BM, mm = idx % BM;
       const int a = a0 + mm, c = c0 + kk;
-      As[kk * SA + mm] = (a < M && c < M) ? __ldg(t + (a > c ? a - c : c - a)) : 0.0;
+      ra[r] = (idx < BK * BM && a < M && c < M) ? __ldg(t + (a > c ? a - c : c - a)) : 0.0;
     }
 #pragma unroll
     for (int r = 0; r < SLOTS; ++r) {
-      if (tid + 128 * r < BK * BN) {
-        const int c = c0 + skk[r];
-        Bs[skk[r] * SB + scc[r]] = (sval[r] && c < M) ? __ldg(X + soff[r] + (i64)c * Q) : 0.0;
-      }
+      const int c = c0 + skk[r];
+      rb[r] = (sval[r] && c < M) ? __ldg(X + soff[r] + (i64)c * Q) : 0.0;
     }
+  };
+  if (c_begin < c_end) load(c_begin);
+  for (int c0 = c_begin; c0 < c_end; c0 += BK) {
     __syncthreads();
+#pragma unroll
+    for (int r = 0; r < ASL; ++r) {
+      const int idx = tid + 128 * r;
+      if (idx < BK * BM) As[(idx / BM) * SA + idx % BM] = ra[r];
+    }
+#pragma unroll
+    for (int r = 0; r < SLOTS; ++r)
+      if (tid + 128 * r < BK * BN) Bs[skk[r] * SB + scc[r]] = rb[r];
+    __syncthreads();
+    if (c0 + BK < c_end) load(c0 + BK);
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       double af[WM], bf[WN];

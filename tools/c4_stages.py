@@ -46,3 +46,11 @@ prev = gk.set_tuning("fused", 1)
 for name, s, a, b in (("scatter", 0, Vi, U), ("kuu", 1, U, W), ("gather", 2, W, Oi), ("staged", 3, Vi, Oi)):
     print(f"{name}: {t(lambda: op.stage_dev(s, a.data_ptr(), b.data_ptr(), nrhs, stream=st)):.1f} us")
 gk.set_tuning("fused", prev)
+prev = gk.set_tuning("fused", 1)
+for var in (0, 1, 2, 3):
+    gk.set_tuning("scatter", var)
+    U.fill_(0.0)
+    us = t(lambda: op.stage_dev(0, Vi.data_ptr(), U.data_ptr(), nrhs, stream=st))
+    print(f"staged scatter variant {var}: {us:.1f} us, checksum {float(U.sum()):.12e}")
+gk.set_tuning("scatter", 0)
+gk.set_tuning("fused", prev)

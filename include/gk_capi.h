@@ -299,6 +299,44 @@ gk_status gk_dski_cross_covariance(const gk_op* op, const double* Xtest, int64_t
 gk_status gk_dski_cross_covariance_jacobian(const gk_op* op, const double* Xtest, int64_t T, double* J,
                                            int64_t ldj);
 
+/* GpModel::solve (gp.cpp:143-158): PCG over nrhs columns (x0 = 0); a column
+ * that does not converge is GK_ERR_RUNTIME with the reference's message
+ * "CG did not converge: relative residual R after K iterations (tol T)".
+ * iterations (nrhs, may be NULL) receives the per-column counts. */
+gk_status gk_gp_solve(const gk_op* op, const gk_precond* precond, const double* B, int64_t ldb,
+                      int64_t nrhs, double tol, int max_iterations, double* X, int64_t ldx,
+                      int* iterations);
+/* GpModel::logdet (gp.cpp:165-179), D-SKI/D-SKIP branch: slq_logdet with the
+ * model's eigen floor 0.5·min(σ₁, σ₂)² (0.5·σ₁² without gradients). */
+gk_status gk_gp_logdet(const gk_op* op, int probes, int lanczos_steps, uint64_t seed,
+                       double noise_value, double noise_gradient, int has_gradients,
+                       double* logdet);
+/* GpModel::log_marginal_likelihood (gp.cpp:181-187): targets = stacked
+ * targets with the mean subtracted (observations.hpp:29-35, gp.cpp:43);
+ * alpha = solve(targets) (throws like gk_gp_solve), lml = −½(tᵀα + logdet +
+ * N log 2π). fit_term, logdet and alpha (N) may be NULL. */
+gk_status gk_gp_log_marginal_likelihood(const gk_op* op, const gk_precond* precond,
+                                        const double* targets, double tol, int max_iterations,
+                                        int probes, int lanczos_steps, uint64_t seed,
+                                        double noise_value, double noise_gradient,
+                                        int has_gradients, double* lml, double* fit_term,
+                                        double* logdet, double* alpha);
+/* GpModel::predict_variance_exact (gp.cpp:499-502) for T test points (Xtest
+ * T×d col-major): var[t] = prior − q_tᵀ K⁻¹ q_t; cross-covariances, the
+ * batched solve (GpModel::solve semantics) and the dots all on the device. */
+gk_status gk_dski_predict_variance_exact(const gk_op* op, const gk_precond* precond,
+                                         const double* Xtest, int64_t T, double prior,
+                                         double tol, int max_iterations, double* var);
+/* GpModel::predict_variance_randomized (gp.cpp:519-547): the pivoted-Cholesky
+ * variance minus the control-variate correction over `probes` Rademacher
+ * probes z_p = rademacher_vector(T, seed, 9000+p) (accumulated in probe
+ * order). K'z, the solves, M⁻¹ and K'ᵀ(·) run on the device. precond is
+ * required (std::logic_error → GK_ERR_LOGIC otherwise). */
+gk_status gk_dski_predict_variance_randomized(const gk_op* op, const gk_precond* precond,
+                                              const double* Xtest, int64_t T, double prior,
+                                              int probes, uint64_t seed, double tol,
+                                              int max_iterations, double* var);
+
 /* ---------------------------------------------------------------- datasets
  * Seeded synthetic workloads C1..C5 (BASELINE.json configs), generated on
  * the host with std::mt19937_64 + libstdc++ distributions like

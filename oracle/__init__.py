@@ -125,6 +125,9 @@ def lib():
             "orc_gp_cross_covariance": (C.c_int, [_vp, _dp, _dp]),
             "orc_gp_predict_variance_randomized": (C.c_int, [_vp, _dp, C.c_longlong, C.c_int, C.c_ulonglong, _dp]),
             "orc_gp_dlogell_apply": (C.c_int, [_vp, _dp, _dp]),
+            "orc_dskip_from_factors": (_vp, [_i64, C.c_int, _d, _d, C.c_int, _i64p, C.POINTER(_dp),
+                                             C.POINTER(_dp), C.POINTER(_dp)]),
+            "orc_make_dataset": (C.c_int, [C.c_int, _u64, _i64p, _ip, _dp, _dp, _dp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -171,6 +174,30 @@ def gaussian_vector(n, seed, stream=0):
 
 def mt19937_64_nth(seed, nth):
     return lib().orc_mt19937_64_nth(seed, nth)
+
+
+# ------------------------------------------------------------------ workloads
+def make_dataset(config, seed=0):
+    """Seeded synthetic workload C1..C5 (BASELINE.json configs), generated by the
+    oracle library itself (datasets.cpp). Returns X (n×d, col-major), y, dY."""
+    n, d = _i64(), C.c_int()
+    if lib().orc_make_dataset(int(config), int(seed), C.byref(n), C.byref(d), None, None, None) != 0:
+        raise ValueError("unknown dataset config")
+    n, d = n.value, d.value
+    X = np.empty((n, d), order="F")
+    y = np.empty(n)
+    dY = np.empty((n, d), order="F")
+    lib().orc_make_dataset(int(config), int(seed), None, None, _p(X), _p(y), _p(dY))
+    return X, y, dY
+
+
+def stacked_targets(y, dY, mean):
+    """ObservationSet::stacked_targets (observations.hpp:29-35): [y - mean; ∂1y; …; ∂dy]."""
+    parts = [np.asarray(y, dtype=np.float64) - mean]
+    if dY is not None:
+        dY = np.asarray(dY, dtype=np.float64)
+        parts += [dY[:, j] for j in range(dY.shape[1])]
+    return np.concatenate(parts)
 
 
 # ------------------------------------------------------------------ kernels / interpolation
@@ -420,6 +447,24 @@ class DskipOperator(Operator):
             msg = lib().orc_last_error().decode()
             raise (ValueError if "separable" in msg or "positive" in msg else RuntimeError)(msg)
         super().__init__(h, (X,))
+
+    @staticmethod
+    def from_factors(factors, n, groups, noise=(0.0, 0.0)):
+        """Hadamard operator over given factors [(Q, alpha, beta), ...]."""
+        op = DskipOperator.__new__(DskipOperator)
+        op.n, op.d, op.noise = n, groups, noise
+        nf = len(factors)
+        Qs = [_f64(f[0], True) for f in factors]
+        As = [_f64(f[1]) for f in factors]
+        Bs = [_f64(f[2]) if np.asarray(f[2]).size else np.zeros(1) for f in factors]
+        ranks = (_i64 * nf)(*[q.shape[1] for q in Qs])
+        arr = lambda xs: (_dp * nf)(*[_p(x) for x in xs])  # noqa: E731
+        h = lib().orc_dskip_from_factors(n, groups, float(noise[0]), float(noise[1]), nf, ranks, arr(Qs),
+                                         arr(As), arr(Bs))
+        if not h:
+            raise ValueError(lib().orc_last_error().decode())
+        Operator.__init__(op, h, (Qs, As, Bs))
+        return op
 
     def factors(self):
         out = []

@@ -328,6 +328,10 @@ class DskipOperator final : public LinearOperator {  // dskip.cpp:162-274
  public:
   DskipOperator(const KernelSpec& k, const double* X, Index n, int d, NoiseLevels noise,
                 const DskipConfig& cfg = {});
+  // Over given Lanczos factors (e.g. the device build's), for Hadamard-MVM
+  // parity with identical factors at full size.
+  DskipOperator(Index n, int groups, NoiseLevels noise, std::vector<LanczosFactor> factors)
+      : n_(n), d_(groups), groups_(groups), noise_(noise), factors_(std::move(factors)) {}
   Index size() const override { return n_ * (groups_ + 1); }
   void mvm(const double* v, double* out) const override;
   bool has_diagonal() const override { return true; }

@@ -200,6 +200,26 @@ void* orc_dskip_create(int family, double ell, double s, const double* X, long l
   return st == OK ? out : nullptr;
 }
 
+void* orc_dskip_from_factors(long long n, int groups, double nv, double ng, int nf, const long long* ranks,
+                             const double* const* Q, const double* const* alpha, const double* const* beta) {
+  LinearOperator* out = nullptr;
+  int st = guard([&] {
+    const Index N = n * (groups + 1);
+    std::vector<LanczosFactor> fs;
+    for (int f = 0; f < nf; ++f) {
+      LanczosFactor F;
+      const Index r = ranks[f];
+      F.Q = Mat(N, r);
+      std::copy(Q[f], Q[f] + N * r, F.Q.a.begin());
+      F.alpha.assign(alpha[f], alpha[f] + r);
+      F.beta.assign(beta[f], beta[f] + std::max<Index>(r - 1, 0));
+      fs.push_back(std::move(F));
+    }
+    out = new DskipOperator(n, groups, NoiseLevels{nv, ng}, std::move(fs));
+  });
+  return st == OK ? out : nullptr;
+}
+
 // Factor data of a D-SKIP operator: number of factors, their ranks, and Q/alpha/beta.
 int orc_dskip_factor_count(void* h) {
   auto* op = dynamic_cast<DskipOperator*>(static_cast<LinearOperator*>(h));

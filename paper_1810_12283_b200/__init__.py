@@ -117,6 +117,13 @@ _SIGS = {
     "gk_dski_cross_covariance_jacobian": (C.c_int, [_vp, _dp, _i64, _dp, _i64]),
     "gk_dski_cross_covariance": (C.c_int, [_vp, _dp, _i64, _dp, _i64]),
     "gk_make_dataset": (C.c_int, [C.c_int, _u64, _i64p, _ip, _dp, _dp, _dp]),
+    "gk_gp_solve": (C.c_int, [_vp, _vp, _dp, _i64, _i64, _d, C.c_int, _dp, _i64, _ip]),
+    "gk_gp_logdet": (C.c_int, [_vp, C.c_int, C.c_int, _u64, _d, _d, C.c_int, _dp]),
+    "gk_gp_log_marginal_likelihood": (C.c_int, [_vp, _vp, _dp, _d, C.c_int, C.c_int, C.c_int, _u64, _d, _d,
+                                                C.c_int, _dp, _dp, _dp, _dp]),
+    "gk_dski_predict_variance_exact": (C.c_int, [_vp, _vp, _dp, _i64, _d, _d, C.c_int, _dp]),
+    "gk_dski_predict_variance_randomized": (C.c_int, [_vp, _vp, _dp, _i64, _d, C.c_int, _u64, _d, C.c_int,
+                                                      _dp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -723,18 +730,6 @@ def lml_gradient(A: LinearOperator, alpha, probes=8, seed=0, tol=1e-4, max_itera
     return g[: k.value].copy()
 
 
-def _solve_columns(A: LinearOperator, B, tol, max_iterations, precond):
-    """GpModel::solve (gp.cpp:143-158) for a block of columns: PCG, and the
-    reference's runtime_error when a column does not converge."""
-    res = cg(A, B, tol, max_iterations, precond, history=True)
-    res = res if isinstance(res, list) else [res]
-    for r in res:
-        if not r.converged:
-            h = r.residual_history[-1] if len(r.residual_history) else float("nan")
-            raise RuntimeError(f"CG did not converge: relative residual {h:.6f} after {r.iterations} iterations")
-    return np.column_stack([r.x for r in res])
-
-
 def _prior_variance(A):
     k = A.kernel
     if k.family != SE:
@@ -742,34 +737,204 @@ def _prior_variance(A):
     return k.outputscale ** 2  # eval(kernel, x, x) (gp.cpp:464-466)
 
 
+def gp_solve(A: LinearOperator, B, tol=1e-4, max_iterations=1000, precond=None):
+    """GpModel::solve (gp.cpp:143-158) for a block of columns: PCG, and the
+    reference's RuntimeError when a column does not converge."""
+    b = np.asarray(B, dtype=np.float64)
+    vec = b.ndim == 1
+    Bm = np.asfortranarray(b.reshape(-1, 1) if vec else b)
+    X = np.empty_like(Bm, order="F")
+    its = np.zeros(Bm.shape[1], np.int32)
+    _check(_lib.gk_gp_solve(A.handle, precond.handle if precond is not None else None, _p(Bm), Bm.shape[0],
+                            Bm.shape[1], float(tol), int(max_iterations), _p(X), X.shape[0],
+                            its.ctypes.data_as(_ip)))
+    return X[:, 0] if vec else X
+
+
 def predict_variance_exact(A: "DskiOperator", Xtest, tol=1e-4, max_iterations=1000, precond=None):
     """GpModel::predict_variance_exact (gp.cpp:499-502) for a batch of test
-    points: k(x, x) − q(x)ᵀ K⁻¹ q(x), the solves batched over the test points."""
-    Q = A.cross_covariance(Xtest)
-    S = _solve_columns(A, Q, tol, max_iterations, precond)
-    return _prior_variance(A) - np.einsum("it,it->t", Q, S)
+    points: k(x, x) − q(x)ᵀ K⁻¹ q(x); cross-covariances, the batched solve and
+    the dots run on the device (gk_dski_predict_variance_exact)."""
+    Xt = _f64(Xtest, True)
+    if Xt.ndim == 1:
+        Xt = Xt.reshape(1, -1, order="F")
+    out = np.empty(Xt.shape[0])
+    _check(_lib.gk_dski_predict_variance_exact(A.handle, precond.handle if precond is not None else None, _p(Xt),
+                                               Xt.shape[0], _prior_variance(A), float(tol), int(max_iterations),
+                                               _p(out)))
+    return out
 
 
 def predict_variance_randomized(A: "DskiOperator", precond, Xtest, probes, seed, tol=1e-4, max_iterations=1000):
     """GpModel::predict_variance_randomized (gp.cpp:519-547): the pivoted-
     Cholesky variance plus an unbiased control-variate correction over
-    Rademacher probes (streams 9000 + p) on the test points."""
+    Rademacher probes (streams 9000 + p) on the test points; all reductions
+    on the device (gk_dski_predict_variance_randomized)."""
     if precond is None:
         raise ValueError("randomized variance needs the preconditioner enabled")
-    Xt = np.asarray(Xtest, dtype=np.float64)
-    T = Xt.shape[0]
-    Q = A.cross_covariance(Xt)
-    base = _prior_variance(A) - np.asarray(precond.quadratic(Q), dtype=np.float64).reshape(T)
-    if probes <= 0:
-        return base
-    Z = np.column_stack([rademacher_vector(T, seed, 9000 + p) for p in range(probes)])
-    W = Q @ Z
-    EX = _solve_columns(A, W, tol, max_iterations, precond)
-    AP = precond.apply(W)
-    corr = np.zeros(T)
-    for p in range(probes):  # probe order, as the reference accumulates
-        corr += Z[:, p] * (Q.T @ (EX[:, p] - AP[:, p]))
-    return base - corr / probes
+    Xt = _f64(Xtest, True)
+    out = np.empty(Xt.shape[0])
+    _check(_lib.gk_dski_predict_variance_randomized(A.handle, precond.handle, _p(Xt), Xt.shape[0],
+                                                    _prior_variance(A), int(probes), int(seed), float(tol),
+                                                    int(max_iterations), _p(out)))
+    return out
+
+
+class GpModel:
+    """GpModel (gp.hpp:64-145; gp.cpp) over the device operators: the hot-path
+    members (op, preconditioner, solve, alpha, logdet, log_marginal_likelihood,
+    lml_gradient, predictions). Backends "dski" and "dskip" (the reference's
+    dense-LLT "exact" backend is not on the path; ExactOperator provides the
+    matrix-free exact K∇ MVM). The optimiser `fit` is out of scope."""
+
+    def __init__(self, kernel: KernelSpec, X, y, dY=None, noise=(1e-2, 1e-2), backend="dski", grid_ratio=0.2,
+                 max_grid_nodes=128, dskip_rank=100, dskip_grid_ratio=0.1, dskip_max_grid_nodes=512, tol=1e-4,
+                 max_iterations=1000, use_preconditioner=True, precond_rank=100, slq_probes=10, slq_steps=50,
+                 gradient_probes=8, seed=0, interpolation=0, device=0):
+        if backend not in ("dski", "dskip"):
+            raise ValueError(f"unknown or unsupported backend '{backend}'")
+        self.kernel = kernel
+        self.X = _f64(X, True)
+        self.y = _f64(y)
+        self.dY = _f64(dY, True) if dY is not None else None
+        self.n, self.d = self.X.shape
+        nv, ng = float(noise[0]), float(noise[1])
+        if not nv > 0:  # gp.cpp:38-41
+            raise ValueError("value noise must be positive")
+        if self.dY is not None and not ng > 0:
+            raise ValueError("gradient noise must be positive")
+        self.noise = (nv, ng)
+        self.backend = backend
+        self.cfg = dict(grid_ratio=grid_ratio, max_grid_nodes=max_grid_nodes, dskip_rank=dskip_rank,
+                        dskip_grid_ratio=dskip_grid_ratio, dskip_max_grid_nodes=dskip_max_grid_nodes, tol=tol,
+                        max_iterations=max_iterations, use_preconditioner=use_preconditioner,
+                        precond_rank=precond_rank, slq_probes=slq_probes, slq_steps=slq_steps,
+                        gradient_probes=gradient_probes, seed=seed, interpolation=interpolation)
+        self.device = device
+        self.mean = float(self.y.mean())  # gp.cpp:43
+        self._invalidate()
+
+    def _invalidate(self):  # gp.cpp:55-64
+        self._op = self._M = self._alpha = None
+
+    def set_hyperparameters(self, kernel: KernelSpec, noise_value, noise_gradient):
+        if not noise_value > 0:
+            raise ValueError("value noise must be positive")
+        self.kernel, self.noise = kernel, (float(noise_value), float(noise_gradient))
+        self._invalidate()
+
+    @property
+    def has_gradients(self):
+        return self.dY is not None
+
+    def outputs(self):
+        return self.n * (self.d + 1 if self.has_gradients else 1)
+
+    def stacked_targets(self):
+        return stacked_targets(self.y, self.dY, self.mean)
+
+    def op(self):
+        """GpModel::build_operator (gp.cpp:66-110)."""
+        if self._op is None:
+            c = self.cfg
+            if self.backend == "dski":
+                grid = Grid.cover(self.X, c["grid_ratio"] * self.kernel.lengthscale, 3, c["max_grid_nodes"])
+                self._op = DskiOperator(self.kernel, grid, self.X, self.noise, c["interpolation"],
+                                        self.has_gradients, self.device)
+            else:
+                self._op = DskipOperator(self.kernel, self.X, self.noise, c["dskip_rank"], c["dskip_grid_ratio"],
+                                         c["dskip_max_grid_nodes"], c["seed"], track_dlogell=True,
+                                         with_gradients=self.has_gradients, device=self.device)
+        return self._op
+
+    def preconditioner(self):
+        """GpModel::preconditioner (gp.cpp:117-141): rank-k pivoted Cholesky of
+        the kernel part, noise in D."""
+        if not self.cfg["use_preconditioner"]:
+            return None
+        if self._M is None:
+            A = self.op()
+            f = pivoted_cholesky(A, min(self.cfg["precond_rank"], A.size()), kernel_part=True)
+            if f.rank() == 0:
+                raise RuntimeError("pivoted Cholesky produced an empty preconditioner factor")
+            self._M = Preconditioner.from_pivchol(A, f)
+        return self._M
+
+    def solve(self, b, tol_scale=1.0):
+        return gp_solve(self.op(), b, self.cfg["tol"] * tol_scale, self.cfg["max_iterations"],
+                        self.preconditioner())
+
+    def alpha(self):
+        if self._alpha is None:
+            self._alpha = self.solve(self.stacked_targets())
+        return self._alpha
+
+    def logdet(self):
+        """GpModel::logdet (gp.cpp:165-179): SLQ with floor ½·min(σ₁, σ₂)²."""
+        out = _d()
+        _check(_lib.gk_gp_logdet(self.op().handle, int(self.cfg["slq_probes"]), int(self.cfg["slq_steps"]),
+                                 int(self.cfg["seed"]), self.noise[0], self.noise[1], int(self.has_gradients),
+                                 C.byref(out)))
+        return out.value
+
+    def log_marginal_likelihood(self):
+        """GpModel::log_marginal_likelihood (gp.cpp:181-187)."""
+        A, M = self.op(), self.preconditioner()
+        t = self.stacked_targets()
+        lml, fit, ld = _d(), _d(), _d()
+        a = np.empty(t.size)
+        _check(_lib.gk_gp_log_marginal_likelihood(A.handle, M.handle if M is not None else None, _p(t),
+                                                  float(self.cfg["tol"]), int(self.cfg["max_iterations"]),
+                                                  int(self.cfg["slq_probes"]), int(self.cfg["slq_steps"]),
+                                                  int(self.cfg["seed"]), self.noise[0], self.noise[1],
+                                                  int(self.has_gradients), C.byref(lml), C.byref(fit),
+                                                  C.byref(ld), _p(a)))
+        self._alpha = a
+        return lml.value
+
+    def lml_gradient(self):
+        """GpModel::lml_gradient (gp.cpp:220-292), stochastic-trace branch."""
+        return lml_gradient(self.op(), self.alpha(), self.cfg["gradient_probes"], self.cfg["seed"],
+                            self.cfg["tol"], self.cfg["max_iterations"], self.preconditioner())
+
+    def predict_mean_grad(self, Xtest):
+        if self.backend != "dski":
+            raise NotImplementedError("predict_mean_grad implemented for the D-SKI backend")
+        return self.op().predict_mean_grad(self.alpha(), self.mean, Xtest)
+
+    def predict_mean(self, Xtest):
+        return self.predict_mean_grad(Xtest)[0]
+
+    def cross_covariance(self, Xtest):
+        return self.op().cross_covariance(Xtest)
+
+    def cross_covariance_jacobian(self, Xtest):
+        return self.op().cross_covariance_jacobian(Xtest)
+
+    def prior_variance(self):
+        return self.kernel.outputscale ** 2
+
+    def predict_variance_exact(self, Xtest):
+        return predict_variance_exact(self.op(), Xtest, self.cfg["tol"], self.cfg["max_iterations"],
+                                      self.preconditioner())
+
+    def predict_variance_pivchol(self, Xtest):
+        """GpModel::predict_variance_pivchol (gp.cpp:506-511)."""
+        M = self.preconditioner()
+        if M is None:
+            raise LogicError("pivoted Cholesky variance needs the preconditioner enabled")
+        Q = self.cross_covariance(Xtest)
+        return self.prior_variance() - np.asarray(M.quadratic(Q), dtype=np.float64).reshape(Q.shape[1])
+
+    def predict_variance_randomized(self, Xtest, probes, seed):
+        M = self.preconditioner()
+        if M is None:
+            raise LogicError("randomized variance needs the preconditioner enabled")
+        return predict_variance_randomized(self.op(), M, Xtest, probes, seed, self.cfg["tol"],
+                                           self.cfg["max_iterations"])
+
+    def dlogell_apply(self, v):
+        return self.op().dlogell_apply(v)
 
 
 class LanczosFactor:

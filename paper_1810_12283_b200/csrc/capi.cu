@@ -72,7 +72,10 @@ void parallel_for(int n, F&& f) {
 
 struct gk_precond {
   std::unique_ptr<Precond> impl;
-  // cached copies reordered for an operator's internal row order (keyed by Op::uid)
+  // cached copies reordered for an operator's internal row order (keyed by
+  // Op::uid); the lookup/insert is guarded by reorder_mu (one external-order
+  // preconditioner may be bound to several operators from several threads)
+  std::mutex reorder_mu;
   std::vector<std::pair<std::uint64_t, std::unique_ptr<Precond>>> reordered;
 };
 struct gk_pivchol {
@@ -109,6 +112,23 @@ Op& O(const gk_op* op) {
 
 cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 
+// One C-ABI call's exclusive use of an operator: holds op.mu, orders the
+// call's device work after the previous call's (whatever stream that used)
+// through op.last_use, and records op.last_use on this call's stream at exit.
+// Construct after the DeviceGuard (the event belongs to op.device).
+struct OpSession {
+  Op& op;
+  cudaStream_t s;
+  std::unique_lock<std::mutex> lk;
+  OpSession(Op& o, cudaStream_t st) : op(o), s(st), lk(o.mu) {
+    if (!op.last_use) GK_CUDA(cudaEventCreateWithFlags(&op.last_use, cudaEventDisableTiming));
+    else GK_CUDA(cudaStreamWaitEvent(s, op.last_use, 0));
+  }
+  ~OpSession() { cudaEventRecord(op.last_use, s); }
+  OpSession(const OpSession&) = delete;
+  OpSession& operator=(const OpSession&) = delete;
+};
+
 // Host block (N×nrhs col-major, ld) -> device internal layout.
 void upload_internal(Op& op, const double* V, i64 ldv, double* d_ext, double* d_int, int nrhs, cudaStream_t s) {
   GK_CUDA(cudaMemcpy2DAsync(d_ext, sizeof(double) * op.N, V, sizeof(double) * ldv, sizeof(double) * op.N, nrhs,
@@ -132,6 +152,7 @@ Precond& precond_for(const gk_precond* M, const Op& op) {
   if (base.order_uid == 0 && ext == nullptr) return base;  // both in external order
   if (base.order_uid != 0)
     fail(GK_ERR_UNSUPPORTED, "preconditioner was built for another operator's row order");
+  std::lock_guard<std::mutex> rlk(mm->reorder_mu);
   for (auto& pr : mm->reordered)
     if (pr.first == op.uid) return *pr.second;
   // external-ordered preconditioner -> reorder rows for op: new[r] = old[ext[r]]
@@ -298,9 +319,9 @@ gk_status gk_op_mvm(const gk_op* h, const double* V, int64_t ldv, double* Out, i
     Op& op = O(h);
     if (nrhs < 0 || ldv < op.N || ldo < op.N) fail(GK_ERR_ARG, "MVM size mismatch");
     if (nrhs == 0) return;
-    std::lock_guard<std::mutex> lk(op.mu);
     DeviceGuard dg(op.device);
     cudaStream_t s = op.stream;
+    OpSession ss(op, s);
     // Host buffers: column chunks pipelined over five streams, one per
     // resource stage — H2D (copy engine), to-internal permute, MVM,
     // from-internal permute, D2H (the other copy engine). Each stage of chunk
@@ -364,9 +385,9 @@ gk_status gk_op_mvm_dev(const gk_op* h, const double* dV, int64_t ldv, double* d
     Op& op = O(h);
     if (nrhs < 0 || ldv < op.N || ldo < op.N) fail(GK_ERR_ARG, "MVM size mismatch");
     if (nrhs == 0) return;
-    std::lock_guard<std::mutex> lk(op.mu);
     DeviceGuard dg(op.device);
     cudaStream_t s = S(stream);
+    OpSession ss(op, s);
     const int chunk = int(std::min<i64>(nrhs, kMaxRhs));
     op.scratch_a.reserve(static_cast<size_t>(op.N) * chunk);
     op.scratch_b.reserve(static_cast<size_t>(op.N) * chunk);
@@ -384,6 +405,7 @@ gk_status gk_op_stage_dev(const gk_op* h, int stage, const double* dIn, double* 
     Op& op = O(h);
     if (nrhs < 1 || nrhs > 256) fail(GK_ERR_ARG, "stage: nrhs must be in [1, 256]");
     DeviceGuard dg(op.device);
+    OpSession ss(op, S(stream));
     op.stage(stage, dIn, dOut, int(nrhs), S(stream));
   });
 }
@@ -394,6 +416,7 @@ gk_status gk_dski_gather_dev(const gk_op* h, const double* dW, const double* dV,
     Op& op = O(h);
     if (nrhs < 1 || nrhs > 256) fail(GK_ERR_ARG, "gather: nrhs must be in [1, 256]");
     DeviceGuard dg(op.device);
+    OpSession ss(op, S(stream));
     dski_gather_noise(op, dW, dV, dOut, int(nrhs), S(stream));
   });
 }
@@ -403,6 +426,7 @@ gk_status gk_op_to_internal_dev(const gk_op* h, const double* dV, int64_t ldv, d
   return guard([&] {
     Op& op = O(h);
     DeviceGuard dg(op.device);
+    OpSession ss(op, S(stream));
     op.to_internal(dV, ldv, dI, int(nrhs), S(stream));
   });
 }
@@ -412,6 +436,7 @@ gk_status gk_op_from_internal_dev(const gk_op* h, const double* dI, double* dV, 
   return guard([&] {
     Op& op = O(h);
     DeviceGuard dg(op.device);
+    OpSession ss(op, S(stream));
     op.from_internal(dI, dV, ldv, int(nrhs), S(stream));
   });
 }
@@ -419,9 +444,9 @@ gk_status gk_op_from_internal_dev(const gk_op* h, const double* dI, double* dV, 
 gk_status gk_op_diagonal(const gk_op* h, double* out) {
   return guard([&] {
     Op& op = O(h);
-    std::lock_guard<std::mutex> lk(op.mu);
     DeviceGuard dg(op.device);
     cudaStream_t s = op.stream;
+    OpSession ss(op, s);
     op.scratch_a.reserve(static_cast<size_t>(op.N));
     op.scratch_b.reserve(static_cast<size_t>(op.N));
     op.diagonal(op.scratch_a.p, s);
@@ -435,9 +460,9 @@ gk_status gk_op_row(const gk_op* h, int64_t r, double* out) {
   return guard([&] {
     Op& op = O(h);
     if (r < 0 || r >= op.N) fail(GK_ERR_RANGE, "row index out of range");
-    std::lock_guard<std::mutex> lk(op.mu);
     DeviceGuard dg(op.device);
     cudaStream_t s = op.stream;
+    OpSession ss(op, s);
     op.scratch_a.reserve(static_cast<size_t>(op.N));
     op.scratch_b.reserve(static_cast<size_t>(op.N));
     op.row(r, op.scratch_a.p, s);
@@ -461,7 +486,7 @@ int gk_debug_fused_phases(gk_op* h, int nrhs, int64_t* out, int max_ctas) {
     if (!out || max_ctas < 0) fail(GK_ERR_ARG, "null output");
     Op& op = O(h);
     DeviceGuard dg(op.device);
-    std::lock_guard<std::mutex> lk(op.mu);
+    OpSession ss(op, op.stream);
     n = dski_fused_phases(op, nrhs, out, max_ctas);
   });
   return n;
@@ -502,9 +527,9 @@ namespace {
 template <class F>
 void grid_call(Op& op, const double* In, i64 ldi, i64 rows_in, double* Out, i64 ldo, i64 rows_out, i64 nrhs,
                bool in_is_grid, bool out_is_grid, F&& f) {
-  std::lock_guard<std::mutex> lk(op.mu);
   DeviceGuard dg(op.device);
   cudaStream_t s = op.stream;
+  OpSession ss(op, s);
   const int chunk = int(std::min<i64>(nrhs, kMaxRhs));
   DevBuf<double> ein(static_cast<size_t>(rows_in) * chunk), iin(static_cast<size_t>(rows_in) * chunk), iout(static_cast<size_t>(rows_out) * chunk),
       eout(static_cast<size_t>(rows_out) * chunk);
@@ -566,9 +591,9 @@ gk_status gk_dski_predict_mean_grad(const gk_op* h, const double* alpha, double 
     Op& op = O(h);
     const gk_grid g = dski_grid(op);
     if (T <= 0) return;
-    std::lock_guard<std::mutex> lk(op.mu);
     DeviceGuard dg(op.device);
     cudaStream_t s = op.stream;
+    OpSession ss(op, s);
     DevBuf<double> ae(static_cast<size_t>(op.N)), ai(static_cast<size_t>(op.N)), xt(static_cast<size_t>(T) * g.d), v(static_cast<size_t>(T)), gr(static_cast<size_t>(T) * g.d);
     DevBuf<int> bad(1);
     const int big = INT_MAX;
@@ -594,9 +619,9 @@ gk_status gk_dski_cross_covariance_jacobian(const gk_op* h, const double* Xtest,
     const gk_grid g = dski_grid(op);
     if (ldj < op.N) fail(GK_ERR_ARG, "size mismatch");
     if (T <= 0) return;
-    std::lock_guard<std::mutex> lk(op.mu);
     DeviceGuard dg(op.device);
     cudaStream_t s = op.stream;
+    OpSession ss(op, s);
     for (i64 t0 = 0; t0 < T; t0 += kMaxRhs) {
       const i64 nt = std::min<i64>(kMaxRhs, T - t0);
       std::vector<double> xh(static_cast<size_t>(nt) * g.d);
@@ -629,9 +654,9 @@ gk_status gk_dski_cross_covariance(const gk_op* h, const double* Xtest, int64_t 
     const gk_grid g = dski_grid(op);
     if (ldq < op.N) fail(GK_ERR_ARG, "size mismatch");
     if (T <= 0) return;
-    std::lock_guard<std::mutex> lk(op.mu);
     DeviceGuard dg(op.device);
     cudaStream_t s = op.stream;
+    OpSession ss(op, s);
     for (i64 t0 = 0; t0 < T; t0 += kMaxRhs) {
       const i64 nt = std::min<i64>(kMaxRhs, T - t0);
       std::vector<double> xh(static_cast<size_t>(nt) * g.d);
@@ -700,9 +725,9 @@ gk_status gk_pcg(const gk_op* h, const gk_precond* M, const double* B, int64_t l
     Op& op = O(h);
     if (ldb < op.N || ldx < op.N) fail(GK_ERR_ARG, "cg: rhs size mismatch");
     if (nrhs <= 0) return;
-    std::lock_guard<std::mutex> lk(op.mu);
     DeviceGuard dg(op.device);
     cudaStream_t s = op.stream;
+    OpSession ss(op, s);
     Precond* P = M ? &precond_for(M, op) : nullptr;
     std::unique_lock<std::mutex> plk;
     if (P) plk = std::unique_lock<std::mutex>(P->mu);
@@ -736,9 +761,9 @@ gk_status gk_pcg_dev(const gk_op* h, const gk_precond* M, const double* dB, int6
     Op& op = O(h);
     if (ldb < op.N || ldx < op.N) fail(GK_ERR_ARG, "cg: rhs size mismatch");
     if (nrhs <= 0) return;
-    std::lock_guard<std::mutex> lk(op.mu);
     DeviceGuard dg(op.device);
     cudaStream_t s = S(stream);
+    OpSession ss(op, s);
     Precond* P = M ? &precond_for(M, op) : nullptr;
     std::unique_lock<std::mutex> plk;
     if (P) plk = std::unique_lock<std::mutex>(P->mu);
@@ -763,8 +788,8 @@ gk_status gk_pivoted_cholesky(const gk_op* h, int kernel_part, int64_t max_rank,
                               gk_pivchol** out) {
   return guard([&] {
     Op& op = O(h);
-    std::lock_guard<std::mutex> lk(op.mu);
     DeviceGuard dg(op.device);
+    OpSession ss(op, op.stream);
     auto f = std::make_unique<gk_pivchol>();
     f->impl = pivchol_run(op, kernel_part != 0, max_rank, trace_tol);
     *out = f.release();
@@ -812,10 +837,10 @@ gk_status gk_precond_from_pivchol(const gk_op* h, const gk_pivchol* f, gk_precon
     const PivChol& p = *f->impl;
     if (p.k == 0) fail(GK_ERR_RUNTIME, "pivoted Cholesky produced an empty preconditioner factor");
     if (p.order_uid != op.uid) fail(GK_ERR_ARG, "pivoted Cholesky factor belongs to another operator");
-    std::lock_guard<std::mutex> lk(op.mu);
     DeviceGuard dg(op.device);
     cudaStream_t s;
     GK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    OpSession ss(op, s);
     std::vector<double> nh(static_cast<size_t>(op.N));
     for (i64 r = 0; r < op.N; ++r) nh[static_cast<size_t>(r)] = r < op.n_value ? op.nv2 : op.ng2;
     if (op.nv2 <= 0.0 || (op.N > op.n_value && op.ng2 <= 0.0))
@@ -908,9 +933,9 @@ gk_status gk_slq_logdet(const gk_op* h, int probes, int steps, uint64_t seed, do
     *logdet = 0.0;
     if (clamped) *clamped = 0;
     if (probes <= 0) return;
-    std::lock_guard<std::mutex> lk(op.mu);
     DeviceGuard dg(op.device);
     cudaStream_t s = op.stream;
+    OpSession ss(op, s);
     const i64 N = op.N;
     const int chunk = std::min(probes, 64);
     std::vector<double> est(static_cast<size_t>(probes), 0.0);
@@ -1002,9 +1027,9 @@ gk_status gk_lanczos(const gk_op* h, int64_t steps, uint64_t seed, const double*
     const i64 N = op.N;
     if (!start && (steps <= 0 || steps > N)) fail(GK_ERR_ARG, "Lanczos rank must lie in [1, N]");
     steps = std::min<i64>(steps, N);
-    std::lock_guard<std::mutex> lk(op.mu);
     DeviceGuard dg(op.device);
     cudaStream_t s = op.stream;
+    OpSession ss(op, s);
     std::vector<double> q(static_cast<size_t>(N));
     std::uint64_t rs = restart_seed;
     if (start) {
@@ -1145,6 +1170,215 @@ gk_status gk_lml_gradient(const gk_op* hA, const gk_precond* M, const double* al
       }
     }
     for (int p = 0; p < np; ++p) grad[p] = 0.5 * (data[static_cast<size_t>(p)] - tr[static_cast<size_t>(p)]);
+  });
+}
+
+// ---------------------------------------------------------------- GpModel glue
+}  // extern "C"
+
+namespace {
+// GpModel::solve's error text (gp.cpp:151-156).
+[[noreturn]] void cg_not_converged(double relres, int its, double tol) {
+  fail(GK_ERR_RUNTIME, "CG did not converge: relative residual " + std::to_string(relres) + " after " +
+                           std::to_string(its) + " iterations (tol " + std::to_string(tol) + ")");
+}
+// GpModel::solve (gp.cpp:143-158) on an internal block: PCG, then the
+// reference's runtime_error for the first column that did not converge.
+void gp_solve_internal(Op& op, Precond* P, const double* Bi, double* Xi, int nb, double tol, int maxit,
+                       cudaStream_t s, int* its_out) {
+  PcgResult r = pcg_internal(op, P, Bi, Xi, nb, tol, maxit, true, s);
+  for (int b = 0; b < nb; ++b) {
+    if (its_out) its_out[b] = r.iterations[static_cast<size_t>(b)];
+    if (!r.converged[static_cast<size_t>(b)]) {
+      const int hl = r.hist_len[static_cast<size_t>(b)];
+      const double rr = hl > 0 ? r.history[static_cast<size_t>(hl - 1) * nb + b] : 0.0;
+      cg_not_converged(rr, r.iterations[static_cast<size_t>(b)], tol);
+    }
+  }
+}
+// Test points [t0, t0+nt) of a T×d col-major host block, re-packed nt×d col-major.
+std::vector<double> test_chunk(const double* Xtest, i64 T, int d, i64 t0, i64 nt) {
+  std::vector<double> xh(static_cast<size_t>(nt) * d);
+  for (int j = 0; j < d; ++j)
+    for (i64 i = 0; i < nt; ++i) xh[static_cast<size_t>(j * nt + i)] = Xtest[j * T + t0 + i];
+  return xh;
+}
+// cross_covariance (gp.cpp:412-417) of nt test points into Qi (internal, N×nt).
+void cross_cov_chunk(Op& op, const gk_grid& g, const double* Xtest, i64 T, i64 t0, i64 nt, double* Qi,
+                     cudaStream_t s) {
+  std::vector<double> xh = test_chunk(Xtest, T, g.d, t0, nt);
+  DevBuf<double> xt(xh.size());
+  DevBuf<int> bad(1);
+  const int big = INT_MAX;
+  GK_CUDA(cudaMemcpyAsync(bad.p, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+  xt.upload(xh.data(), xh.size(), s);
+  dski_cross_cov(op, xt.p, nt, Qi, bad.p, s);
+  int badh = INT_MAX;
+  GK_CUDA(cudaMemcpy(&badh, bad.p, sizeof(int), cudaMemcpyDeviceToHost));
+  if (badh != INT_MAX)
+    fail(GK_ERR_OUT_OF_GRID, "test point " + std::to_string(t0 + badh) + " lies outside the interior of the grid",
+         t0 + badh);
+}
+}  // namespace
+
+extern "C" {
+
+gk_status gk_gp_solve(const gk_op* h, const gk_precond* M, const double* B, int64_t ldb, int64_t nrhs, double tol,
+                      int maxit, double* X, int64_t ldx, int* iterations) {
+  return guard([&] {
+    Op& op = O(h);
+    if (ldb < op.N || ldx < op.N) fail(GK_ERR_ARG, "cg: rhs size mismatch");
+    if (nrhs <= 0) return;
+    DeviceGuard dg(op.device);
+    cudaStream_t s = op.stream;
+    OpSession ss(op, s);
+    Precond* P = M ? &precond_for(M, op) : nullptr;
+    std::unique_lock<std::mutex> plk;
+    if (P) plk = std::unique_lock<std::mutex>(P->mu);
+    const int chunk = int(std::min<i64>(nrhs, 256));
+    DevBuf<double> e(static_cast<size_t>(op.N) * chunk), bi(e.n), xi(e.n);
+    for (i64 c0 = 0; c0 < nrhs; c0 += chunk) {
+      const int nb = int(std::min<i64>(chunk, nrhs - c0));
+      upload_internal(op, B + c0 * ldb, ldb, e.p, bi.p, nb, s);
+      gp_solve_internal(op, P, bi.p, xi.p, nb, tol, maxit, s, iterations ? iterations + c0 : nullptr);
+      download_internal(op, xi.p, e.p, X + c0 * ldx, ldx, nb, s);
+      GK_CUDA(cudaStreamSynchronize(s));
+    }
+  });
+}
+
+gk_status gk_gp_logdet(const gk_op* h, int probes, int steps, uint64_t seed, double noise_value,
+                       double noise_gradient, int has_gradients, double* logdet) {
+  const double f2 = has_gradients ? std::min(noise_value, noise_gradient) : noise_value;  // gp.cpp:174-177
+  int clamped = 0;
+  return gk_slq_logdet(h, probes, steps, seed, 0.5 * f2 * f2, 0, logdet, &clamped, nullptr);
+}
+
+gk_status gk_gp_log_marginal_likelihood(const gk_op* h, const gk_precond* M, const double* targets, double tol,
+                                        int maxit, int probes, int steps, uint64_t seed, double noise_value,
+                                        double noise_gradient, int has_gradients, double* lml, double* fit_term,
+                                        double* logdet, double* alpha) {
+  return guard([&] {  // gp.cpp:181-187
+    Op& op = O(h);
+    if (!targets || !lml) fail(GK_ERR_ARG, "null argument");
+    std::vector<double> a(static_cast<size_t>(op.N));
+    int its = 0;
+    gk_status st = gk_gp_solve(h, M, targets, op.N, 1, tol, maxit, a.data(), op.N, &its);
+    if (st != GK_OK) fail(st, g_err);
+    double fit = 0.0;
+    for (i64 i = 0; i < op.N; ++i) fit += targets[i] * a[static_cast<size_t>(i)];
+    double ld = 0.0;
+    st = gk_gp_logdet(h, probes, steps, seed, noise_value, noise_gradient, has_gradients, &ld);
+    if (st != GK_OK) fail(st, g_err);
+    const double pi = 3.14159265358979323846;
+    *lml = -0.5 * (fit + ld + double(op.N) * std::log(2.0 * pi));
+    if (fit_term) *fit_term = fit;
+    if (logdet) *logdet = ld;
+    if (alpha) std::copy(a.begin(), a.end(), alpha);
+  });
+}
+
+gk_status gk_dski_predict_variance_exact(const gk_op* h, const gk_precond* M, const double* Xtest, int64_t T,
+                                         double prior, double tol, int maxit, double* var) {
+  return guard([&] {  // gp.cpp:499-502, batched over test points
+    Op& op = O(h);
+    const gk_grid g = dski_grid(op);
+    if (T <= 0) return;
+    DeviceGuard dg(op.device);
+    cudaStream_t s = op.stream;
+    OpSession ss(op, s);
+    Precond* P = M ? &precond_for(M, op) : nullptr;
+    std::unique_lock<std::mutex> plk;
+    if (P) plk = std::unique_lock<std::mutex>(P->mu);
+    const int chunk = int(std::min<i64>(T, kMaxRhs));
+    DevBuf<double> Qi(static_cast<size_t>(op.N) * chunk), Si(Qi.n), dots(static_cast<size_t>(chunk)), part;
+    std::vector<double> dh(static_cast<size_t>(chunk));
+    for (i64 t0 = 0; t0 < T; t0 += chunk) {
+      const int nt = int(std::min<i64>(chunk, T - t0));
+      cross_cov_chunk(op, g, Xtest, T, t0, nt, Qi.p, s);
+      gp_solve_internal(op, P, Qi.p, Si.p, nt, tol, maxit, s, nullptr);
+      col_dots_dev(Qi.p, Si.p, op.N, nt, dots.p, part, s);
+      GK_CUDA(cudaMemcpyAsync(dh.data(), dots.p, sizeof(double) * nt, cudaMemcpyDeviceToHost, s));
+      GK_CUDA(cudaStreamSynchronize(s));
+      for (int i = 0; i < nt; ++i) var[t0 + i] = prior - dh[static_cast<size_t>(i)];
+    }
+  });
+}
+
+gk_status gk_dski_predict_variance_randomized(const gk_op* h, const gk_precond* M, const double* Xtest, int64_t T,
+                                              double prior, int probes, uint64_t seed, double tol, int maxit,
+                                              double* var) {
+  return guard([&] {  // gp.cpp:519-547
+    Op& op = O(h);
+    const gk_grid g = dski_grid(op);
+    if (!M) fail(GK_ERR_LOGIC, "randomized variance needs the preconditioner enabled");
+    if (T <= 0) return;
+    DeviceGuard dg(op.device);
+    cudaStream_t s = op.stream;
+    OpSession ss(op, s);
+    Precond* P = &precond_for(M, op);
+    std::unique_lock<std::mutex> plk(P->mu);
+    const i64 N = op.N;
+    const int chunk = int(std::min<i64>(T, kMaxRhs));
+    const int nchunks = int((T + chunk - 1) / chunk);
+    // K' (N×T) kept on the device as per-chunk internal blocks
+    DevBuf<double> Kc(static_cast<size_t>(N) * T);
+    std::vector<double> base(static_cast<size_t>(T));
+    for (int c = 0; c < nchunks; ++c) {
+      const i64 t0 = i64(c) * chunk;
+      const int nt = int(std::min<i64>(chunk, T - t0));
+      double* Qi = Kc.p + N * t0;
+      cross_cov_chunk(op, g, Xtest, T, t0, nt, Qi, s);
+      precond_quadratic(*P, Qi, nt, base.data() + t0, s);
+      for (int i = 0; i < nt; ++i) base[static_cast<size_t>(t0 + i)] = prior - base[static_cast<size_t>(t0 + i)];
+    }
+    if (probes <= 0) {
+      std::copy(base.begin(), base.end(), var);
+      return;
+    }
+    // z_p = rademacher_vector(T, seed, 9000 + p), row-major Z[t][p]
+    std::vector<double> Z(static_cast<size_t>(T) * probes), zc(static_cast<size_t>(T));
+    for (int p = 0; p < probes; ++p) {
+      rademacher(T, seed, 9000 + std::uint64_t(p), zc.data());
+      for (i64 t = 0; t < T; ++t) Z[static_cast<size_t>(t * probes + p)] = zc[static_cast<size_t>(t)];
+    }
+    std::vector<double> G(static_cast<size_t>(T) * probes);  // G[t][p] = q_tᵀ (K⁻¹ − M⁻¹) w_p
+    const int pchunk = std::min(probes, kMaxRhs);
+    DevBuf<double> Zd, W(static_cast<size_t>(N) * pchunk), EX(W.n), AP(W.n), Gd(static_cast<size_t>(chunk) * pchunk),
+        part;
+    std::vector<double> Zsub;
+    for (int p0 = 0; p0 < probes; p0 += pchunk) {
+      const int np = std::min(pchunk, probes - p0);
+      // W = K' Z[:, p0:p0+np], summed over the test-point chunks
+      for (int c = 0; c < nchunks; ++c) {
+        const i64 t0 = i64(c) * chunk;
+        const int nt = int(std::min<i64>(chunk, T - t0));
+        Zsub.assign(static_cast<size_t>(nt) * np, 0.0);
+        for (int t = 0; t < nt; ++t)
+          for (int q = 0; q < np; ++q) Zsub[static_cast<size_t>(t * np + q)] = Z[static_cast<size_t>((t0 + t) * probes + p0 + q)];
+        Zd.upload(Zsub.data(), Zsub.size(), s);
+        rows_gemm_dev(Kc.p + N * t0, nt, Zd.p, np, N, W.p, c > 0, s);
+        GK_CUDA(cudaStreamSynchronize(s));  // Zd reused by the next chunk
+      }
+      gp_solve_internal(op, P, W.p, EX.p, np, tol, maxit, s, nullptr);
+      P->apply(W.p, AP.p, np, s);
+      sub_dev(EX.p, AP.p, EX.p, N * np, s);
+      for (int c = 0; c < nchunks; ++c) {
+        const i64 t0 = i64(c) * chunk;
+        const int nt = int(std::min<i64>(chunk, T - t0));
+        cross_dev(Kc.p + N * t0, nt, EX.p, np, N, Gd.p, part, s);
+        std::vector<double> gh(static_cast<size_t>(nt) * np);
+        GK_CUDA(cudaMemcpyAsync(gh.data(), Gd.p, sizeof(double) * gh.size(), cudaMemcpyDeviceToHost, s));
+        GK_CUDA(cudaStreamSynchronize(s));
+        for (int t = 0; t < nt; ++t)
+          for (int q = 0; q < np; ++q) G[static_cast<size_t>((t0 + t) * probes + p0 + q)] = gh[static_cast<size_t>(t * np + q)];
+      }
+    }
+    for (i64 t = 0; t < T; ++t) {
+      double corr = 0.0;  // accumulated in probe order (gp.cpp:538-544)
+      for (int p = 0; p < probes; ++p) corr += Z[static_cast<size_t>(t * probes + p)] * G[static_cast<size_t>(t * probes + p)];
+      var[t] = base[static_cast<size_t>(t)] - corr / double(probes);
+    }
   });
 }
 

@@ -160,6 +160,11 @@ struct Op {
   i64 n_value = 0;      // rows [0, n_value) carry sigma_1^2, the rest sigma_2^2
   double nv2 = 0.0, ng2 = 0.0;
   std::mutex mu;        // serialises host-API calls that use the scratch below
+  // Recorded at the end of every C-ABI call on the stream that call used; the
+  // next call (any stream: op.stream or a caller's) waits on it first, so
+  // device work of successive calls that share op-owned scratch, plans and
+  // grid-barrier counters never overlaps (OpSession in capi.cu).
+  cudaEvent_t last_use = nullptr;
   cudaStream_t stream = nullptr;  // own stream for host-API calls
   cudaStream_t cap_stream = nullptr;  // private stream used only for CUDA-graph capture
   DevBuf<double> scratch_a, scratch_b, scratch_c;

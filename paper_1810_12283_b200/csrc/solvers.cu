@@ -1987,6 +1987,73 @@ std::unique_ptr<Precond> precond_build(const double* F_int, i64 N, i64 k, const 
   return M;
 }
 
+// ================================================================ small block products (GP glue)
+// C[r][j] (+)= Σ_t A[r][t]·Bm[t][j]: RHS-minor block (rows × ka) times a small
+// host-sized matrix (ka × nb, row-major); one thread per output element.
+__global__ void k_rows_gemm(const double* __restrict__ A, int ka, const double* __restrict__ Bm, int nb, i64 rows,
+                            double* __restrict__ Cm, int accumulate) {
+  for (i64 e = (i64)blockIdx.x * blockDim.x + threadIdx.x; e < rows * nb; e += (i64)gridDim.x * blockDim.x) {
+    const i64 r = e / nb;
+    const int j = int(e - r * nb);
+    const double* a = A + r * ka;
+    double acc = 0.0;
+    for (int t = 0; t < ka; ++t) acc += a[t] * Bm[(i64)t * nb + j];
+    Cm[e] = accumulate ? Cm[e] + acc : acc;
+  }
+}
+
+// partial[block][t*nb + j] = Σ_{r in block's range} A[r][t]·D[r][j] (fixed order).
+__global__ void __launch_bounds__(256) k_cross_partial(const double* __restrict__ A, int ka,
+                                                       const double* __restrict__ D, int nb, i64 rows,
+                                                       double* __restrict__ partial) {
+  i64 r0, r1;
+  row_range(rows, r0, r1);
+  const int nout = ka * nb;
+  for (int o = threadIdx.x; o < nout; o += blockDim.x) {
+    const int t = o / nb, j = o - (o / nb) * nb;
+    double acc = 0.0;
+    for (i64 r = r0; r < r1; ++r) acc += A[r * ka + t] * D[r * nb + j];
+    partial[(i64)blockIdx.x * nout + o] = acc;
+  }
+}
+
+__global__ void k_sub(const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ c, i64 n) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) c[i] = a[i] - b[i];
+}
+
+void rows_gemm_dev(const double* A, int ka, const double* Bm_dev, int nb, i64 rows, double* C, bool accumulate,
+                   cudaStream_t s) {
+  if (rows * nb == 0) return;
+  k_rows_gemm<<<blocks_for(rows * nb), 256, 0, s>>>(A, ka, Bm_dev, nb, rows, C, accumulate ? 1 : 0);
+  launched("rows gemm");
+}
+
+void cross_dev(const double* A, int ka, const double* D, int nb, i64 rows, double* out_dev, DevBuf<double>& part,
+               cudaStream_t s) {
+  const int nout = ka * nb;
+  part.reserve(static_cast<size_t>(RB) * nout);
+  k_cross_partial<<<RB, 256, 0, s>>>(A, ka, D, nb, rows, part.p);
+  launched("cross partial");
+  k_fin_cols<<<fin_blocks(nout), 256, 0, s>>>(part.p, nout, out_dev);
+  launched("cross fin");
+}
+
+void col_dots_dev(const double* X, const double* Y, i64 rows, int nrhs, double* out_dev, DevBuf<double>& part,
+                  cudaStream_t s) {
+  if (nrhs < 1 || nrhs > RT) fail(GK_ERR_ARG, "column dots: nrhs must be in [1, 256]");
+  part.reserve(static_cast<size_t>(RB) * nrhs);
+  k_dot_partial<<<RB, RT, 0, s>>>(X, Y, rows, nrhs, part.p);
+  launched("column dots");
+  k_fin_cols<<<fin_blocks(nrhs), 256, 0, s>>>(part.p, nrhs, out_dev);
+  launched("column dots fin");
+}
+
+void sub_dev(const double* a, const double* b, double* c, i64 n, cudaStream_t s) {
+  if (n == 0) return;
+  k_sub<<<blocks_for(n), 256, 0, s>>>(a, b, c, n);
+  launched("sub");
+}
+
 // ================================================================ pivoted Cholesky
 std::unique_ptr<PivChol> pivchol_run(Op& op, bool kernel_part, i64 max_rank, double trace_tol) {
   cudaStream_t s = op.stream;

@@ -84,4 +84,17 @@ LanczosBatch lanczos_batch(Op& op, const double* start_int, int P, int steps,
 // host's std::mt19937_64(seeds[q]) streams (sign = bit 0 of each draw).
 void rademacher_dev(i64 n, const std::uint64_t* seeds_h, int P, double scale, double* out, i64 ld, cudaStream_t s);
 
+// Small block products used by the GP glue (internal RHS-minor layouts; all
+// results deterministic, fixed summation order).
+//   C = A·Bm (rows×ka times ka×nb, Bm on the device, row-major)
+void rows_gemm_dev(const double* A, int ka, const double* Bm_dev, int nb, i64 rows, double* C, bool accumulate,
+                   cudaStream_t s);
+//   out[t][j] = Σ_r A[r][t]·D[r][j]  (ka×nb, device)
+void cross_dev(const double* A, int ka, const double* D, int nb, i64 rows, double* out_dev, DevBuf<double>& part,
+               cudaStream_t s);
+//   out[b] = Σ_r X[r][b]·Y[r][b]  (device)
+void col_dots_dev(const double* X, const double* Y, i64 rows, int nrhs, double* out_dev, DevBuf<double>& part,
+                  cudaStream_t s);
+void sub_dev(const double* a, const double* b, double* c, i64 n, cudaStream_t s);
+
 }  // namespace gk

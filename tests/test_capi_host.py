@@ -89,3 +89,13 @@ def test_errors_map_to_reference_exception_types():
         gk.KernelSpec(-1.0, 1.0)
     with pytest.raises(ValueError):
         gk.make_dataset(9)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_oracle_datasets_bit_identical_to_product(cfg):
+    # the reference arm of bench.py and the oracle-side fixtures generate their
+    # inputs with the oracle library only; both sides must see the same workload
+    Xa, ya, dYa = gk.make_dataset(cfg, 0)
+    Xb, yb, dYb = O.make_dataset(cfg, 0)
+    assert np.array_equal(Xa, Xb) and np.array_equal(ya, yb) and np.array_equal(dYa, dYb)
+    assert np.array_equal(gk.stacked_targets(ya, dYa, ya.mean()), O.stacked_targets(yb, dYb, yb.mean()))

@@ -48,3 +48,48 @@ def test_concurrent_mvm_solve_and_slq_on_one_operator():
     for t in range(4):
         assert np.array_equal(results[("cg", t)], want_x)
         assert results[("slq", t)] == want_ld
+
+
+def test_dev_entry_points_ordered_against_host_calls():
+    """device-pointer calls on a caller's side stream (stage_dev /
+    mvm_dev, asynchronous) interleaved, without any host synchronisation, with
+    host-API calls on the same handle (mvm, diagonal, cg) that reuse the
+    handle's scratch, plans and grid-barrier counter. Every call waits on the
+    handle's last-use event, so all results equal the serial ones."""
+    import torch
+    X, y, dY = gk.make_dataset(2, 0)
+    grid = gk.Grid.cover(X, 1e-4, 3, 100)
+    op = gk.DskiOperator(gk.KernelSpec(0.2, 1.0), grid, X, (1e-2, 1e-2))
+    N = op.size()
+    rng = np.random.default_rng(3)
+    B32 = rng.standard_normal((N, 32))
+    want32 = op.mvm(B32)
+    want_diag = op.diagonal()
+    b = gk.stacked_targets(y, dY, y.mean())
+    want_x = gk.cg(op, b, 1e-3, 40).x
+    side = torch.cuda.Stream()
+    Vext = torch.from_numpy(np.ascontiguousarray(B32.T)).cuda()
+    Vi = torch.empty(N * 32, dtype=torch.float64, device="cuda")
+    outs = [torch.empty_like(Vi) for _ in range(6)]
+    Oext = [torch.empty_like(Vext) for _ in range(6)]
+    torch.cuda.synchronize()
+    s = side.cuda_stream
+    op.to_internal_dev(Vext.data_ptr(), Vi.data_ptr(), 32, stream=s)
+    diags, xs = [], []
+    for k in range(6):
+        op.stage_dev(3, Vi.data_ptr(), outs[k].data_ptr(), 32, stream=s)  # async on the side stream
+        op.from_internal_dev(outs[k].data_ptr(), Oext[k].data_ptr(), 32, stream=s)
+        if k % 2 == 0:
+            diags.append(op.diagonal())  # host API on the handle's own stream
+        else:
+            xs.append(gk.cg(op, b, 1e-3, 40).x)
+        if k == 5:  # the external-layout device entry point as well
+            op.mvm_dev(Vext.data_ptr(), Oext[k].data_ptr(), 32, stream=s)
+    side.synchronize()
+    for k in range(6):
+        got = Oext[k].cpu().numpy().T
+        assert np.linalg.norm(got - want32) <= 1e-13 * np.linalg.norm(want32), k
+    for d in diags:
+        assert np.array_equal(d, want_diag)
+    for x in xs:
+        assert np.array_equal(x, want_x)

@@ -8,9 +8,12 @@ all five configs").
   30-step SLQ ≤1e-8 per probe (linalg.cpp:215-253).
 - C3: the 17-RHS d = 3 MVM (targets + 16 probes), ≤1e-12.
 - C4: the 1- and 8-RHS MVMs (400² grid, n = 150,000), ≤1e-12.
-- C1: the whole GpModel pipeline at its stated settings (60² grid, rank-20
-  pivoted Cholesky, PCG tol 1e-8, SLQ 8 × 25): pivots bit-exact, iterations
-  ±1, α to the solver tolerance, log-det and LML ≤1e-8 (gp.cpp:117-187).
+- C1: the GpModel pipeline at its stated settings (60² grid, rank-20
+  pivoted Cholesky, PCG tol 1e-8, SLQ 8 × 25): pivots bit-exact, the
+  reference's own non-convergence reproduced (same exception), early PCG
+  history ≤1e-8, log-det ≤1e-8; and at σ = 0.5, where the reference solve
+  converges, LML/log-det ≤1e-8 and iterations inside the oracle's band ±1
+  (gp.cpp:117-187).
 - C5: the 64-RHS Hadamard MVM at full N with identical factors (the device
   build's, evaluated by the oracle's hadamard_mvm, dskip.cpp:24-36), ≤1e-12;
   and the device D-SKIP build pinned step by step (Lanczos α/β of the leaf
@@ -107,32 +110,69 @@ def test_c4_mvm(nrhs):
     assert col_rel(op.mvm(B), want) <= 1e-12
 
 
-def test_c1_gp_pipeline():
-    """C1 at its stated settings through GpModel on both sides."""
+def c1_models(noise, tol, maxit):
     X, y, dY = O.make_dataset(1, 0)
-    kw = dict(noise=NOISE, backend="dski", grid_ratio=1e-3, max_grid_nodes=60, tol=1e-8, max_iterations=2000,
+    kw = dict(noise=noise, backend="dski", grid_ratio=1e-3, max_grid_nodes=60, tol=tol, max_iterations=maxit,
               precond_rank=20, slq_probes=8, slq_steps=25, seed=0)
-    ref = O.GpModel(O.KernelSpec(0.15, 1.0), X, y, dY, **kw)
-    gm = gk.GpModel(gk.KernelSpec(0.15, 1.0), X, y, dY, **kw)
+    return O.GpModel(O.KernelSpec(0.15, 1.0), X, y, dY, **kw), gk.GpModel(gk.KernelSpec(0.15, 1.0), X, y, dY, **kw)
+
+
+def test_c1_stated_settings():
+    """C1 as BASELINE states it (σ = 1e-2, rank 20, tol 1e-8, SLQ 8 × 25). The
+    reference algorithm does not reach tol 1e-8 here: the oracle's PCG stops
+    at max_iterations with relres ≈ 0.14 and GpModel::solve throws
+    (gp.cpp:151-156). Parity: pivots bit-exact, the same exception, the PCG
+    residual history of the first 20 iterations ≤1e-8, SLQ log-det with the
+    model's floor ½σ² ≤1e-8 per probe."""
+    ref, gm = c1_models(NOISE, 1e-8, 2000)
     A = gm.op()
     assert list(A.grid.dims) == [60, 60]
-    # GpModel::preconditioner: rank-20 pivots bit-exact
     f = gk.pivoted_cholesky(A, 20, kernel_part=True)
     assert [int(p) for p in f.pivots] == [int(p) for p in ref.pivots(20)]
-    # GpModel::solve / alpha: PCG at tol 1e-8, iterations ±1, solution to tol
-    a_ref, its_ref = ref.alpha()
+    with pytest.raises(RuntimeError, match="CG did not converge"):
+        ref.alpha()
+    with pytest.raises(RuntimeError, match="CG did not converge: relative residual .* after 2000 iterations"):
+        gm.alpha()
     t = gm.stacked_targets()
-    sol = gk.cg(A, t, 1e-8, 2000, gm.preconditioner())
-    assert sol.converged and abs(sol.iterations - its_ref) <= 1, (sol.iterations, its_ref)
-    a = gm.alpha()
-    assert np.linalg.norm(a - a_ref) <= 1e-6 * np.linalg.norm(a_ref)
-    assert np.linalg.norm(A.mvm(a) - t) <= 1.01e-8 * np.linalg.norm(t)
-    # logdet and LML (identical probe seeds) ≤ 1e-8 relative
-    got_ld = gm.logdet()
+    og = O.Grid(A.grid.dims, A.grid.origin, A.grid.spacing)
+    rop = O.DskiOperator(O.KernelSpec(0.15, 1.0), og, gm.X, NOISE)
+    fr = O.pivoted_cholesky(rop, 20, noise_diag=rop.noise_diagonal())
+    Pr = O.Preconditioner(fr.L, rop.noise_diagonal())
+    hr = O.cg(rop, t, 1e-8, 20, Pr).residual_history
+    hg = gk.cg(A, t, 1e-8, 20, gm.preconditioner()).residual_history
+    assert np.max(np.abs(np.asarray(hg) - hr) / hr) <= 1e-8
+    want = O.slq_logdet(rop, 8, 25, 0, 0.5 * 1e-4)
+    got = gk.slq_logdet(A, 8, 25, 0, 0.5 * 1e-4)
+    assert np.max(np.abs(got.estimates - want.estimates) / np.abs(want.estimates)) <= 1e-8
+    assert abs(gm.logdet() - want.logdet) <= 1e-8 * abs(want.logdet)
+
+
+def test_c1_lml_where_the_solve_converges():
+    """The C1 pipeline (data, 60² grid, ℓ, rank-20 preconditioner, SLQ 8 × 25)
+    at σ = 0.5, where the reference's PCG converges (tol 1e-10, ~600
+    iterations): LML and log-det ≤1e-8, α to the solver tolerance, iteration
+    count inside the oracle's own ulp-perturbation band ±1 (CG counts at
+    hundreds of iterations move under 1e-16 perturbations of b,
+    test_gpu_solvers.oracle_iteration_band)."""
+    from test_gpu_solvers import oracle_iteration_band
+    ref, gm = c1_models((0.5, 0.5), 1e-10, 3000)
     r = ref.log_marginal_likelihood()
-    assert abs(got_ld - r["logdet"]) <= 1e-8 * abs(r["logdet"])
     lml = gm.log_marginal_likelihood()
     assert abs(lml - r["lml"]) <= 1e-8 * abs(r["lml"]), (lml, r["lml"])
+    assert abs(gm.logdet() - r["logdet"]) <= 1e-8 * abs(r["logdet"])
+    a_ref, its_ref = ref.alpha()
+    a = gm.alpha()
+    assert np.linalg.norm(a - a_ref) <= 1e-6 * np.linalg.norm(a_ref)
+    A, t = gm.op(), gm.stacked_targets()
+    og = O.Grid(A.grid.dims, A.grid.origin, A.grid.spacing)
+    rop = O.DskiOperator(O.KernelSpec(0.15, 1.0), og, gm.X, (0.5, 0.5))
+    fr = O.pivoted_cholesky(rop, 20, noise_diag=rop.noise_diagonal())
+    lo, hi = oracle_iteration_band(rop, t, 1e-10, 3000, O.Preconditioner(fr.L, rop.noise_diagonal()), k=2)
+    its = gk.cg(A, t, 1e-10, 3000, gm.preconditioner()).iterations
+    # ±1 against the oracle GpModel's own solve (measured: 616 vs 616); the
+    # band of the free-function oracle PCG (its preconditioner differs from
+    # GpModel's at roundoff: 608-609) is accepted as well
+    assert abs(its - its_ref) <= 1 or lo - 1 <= its <= hi + 1, (its, its_ref, lo, hi)
 
 
 def test_c1_gp_solve_raises_reference_error():

@@ -33,6 +33,7 @@
 #include <sstream>
 
 #include "fused2d.hpp"
+#include "lean2d.hpp"
 #include "gk_common.hpp"
 #include "gk_kernels.cuh"
 
@@ -1323,6 +1324,7 @@ struct DskiOp final : Op {
   DevBuf<double> grid_u, grid_w, grid_t, grid_h, grid_p;  // per-MVM grid scratch (guarded by mu / caller)
   std::vector<int> cell_start_h;          // host copy (fused-plan sizing)
   std::vector<std::unique_ptr<Fused2dPlan>> fplans;  // one-launch d = 2 MVM plans, per nrhs
+  std::vector<std::unique_ptr<Lean2dPlan>> lplans;   // lean one-launch d = 2 MVM plans, per nrhs
 
   Fused2dGeom geom2d() const {
     Fused2dGeom g;
@@ -1359,6 +1361,30 @@ struct DskiOp final : Op {
     fused2d_plan(geom2d(), cell_start_h, nrhs, device, *p);
     fplans.push_back(std::move(p));
     return fplans.back()->ok ? fplans.back().get() : nullptr;
+  }
+
+  // The lean one-launch MVM (lean2d.cu): d = 2 with gradients, grids up to
+  // 128² and up to 64 right-hand sides. Chosen where it measured faster than
+  // fused2d on B200 (tools/lean_timing.py): odd RHS counts ≥ 3 (C1 9 RHS 31.8
+  // vs 33.7 µs, C2 31 RHS 56.3 vs 62.4 µs) and more than 32 RHS (C2 64 RHS
+  // 74.9 vs 87.0 µs). Tuning "lean": 0 = this policy, 1 = never, 2 = always.
+  Lean2dPlan* lean_plan(int nrhs) {
+    const int pol = g_tuning.lean.load();
+    if (d != 2 || G != 2 || g_tuning.fused.load() != 0 || pol == 1 || n >= (i64(1) << 31)) return nullptr;
+    if (pol == 0 && !((nrhs % 2 == 1 && nrhs >= 3) || nrhs > 32)) return nullptr;
+    const int gen = g_tuning.gen.load();
+    for (auto it = lplans.begin(); it != lplans.end(); ++it)
+      if ((*it)->nrhs == nrhs) {
+        if ((*it)->tuning_gen == gen) return (*it)->ok ? it->get() : nullptr;
+        lplans.erase(it);
+        ++epoch;
+        break;
+      }
+    auto p = std::make_unique<Lean2dPlan>();
+    p->tuning_gen = gen;
+    lean2d_plan(geom2d(), nrhs, device, *p);
+    lplans.push_back(std::move(p));
+    return lplans.back()->ok ? lplans.back().get() : nullptr;
   }
 
   DskiView view() const {
@@ -1420,6 +1446,11 @@ struct DskiOp final : Op {
 
   void mvm(const double* in, double* out, int nrhs, cudaStream_t s) override {
     ensure_scratch(nrhs);
+    if (Lean2dPlan* lp = lean_plan(nrhs)) {
+      grow(grid_p, static_cast<size_t>(2) * M * nrhs);
+      lean2d_mvm(geom2d(), *lp, in, out, grid_p.p, grid_t.p, grid_w.p, true, s);
+      return;
+    }
     if (Fused2dPlan* fp = fused_plan(nrhs)) {
       if (fp->s_mode == 1) grow(grid_p, static_cast<size_t>(fp->s_nbuf) * M * nrhs);
       fused2d_mvm(geom2d(), *fp, in, out, grid_u.p, grid_h.p, grid_t.p, grid_w.p, grid_p.p, true, s);
@@ -2111,6 +2142,16 @@ namespace gk {
 int dski_fused_phases(Op& o, int nrhs, i64* out, int max_ctas) {
   if (o.kind != KIND_DSKI) fail(GK_ERR_ARG, "operator is not a D-SKI operator");
   auto& op = static_cast<DskiOp&>(o);
+  for (auto& p : op.lplans)
+    if (p->nrhs == nrhs && p->ok && p->prof.p) {
+      const int n = std::min(p->grid, max_ctas);
+      std::vector<i64> h(p->prof.n);
+      GK_CUDA(cudaDeviceSynchronize());
+      GK_CUDA(cudaMemcpy(h.data(), p->prof.p, sizeof(i64) * h.size(), cudaMemcpyDeviceToHost));
+      for (int c = 0; c < n; ++c)
+        for (int k = 0; k < 8; ++k) out[size_t(c) * 8 + k] = h[size_t(c) * 8 + k];
+      return n;
+    }
   for (auto& p : op.fplans)
     if (p->nrhs == nrhs && p->ok && p->prof.p) {
       const int n = std::min(p->grid, max_ctas);

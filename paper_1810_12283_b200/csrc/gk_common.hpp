@@ -37,6 +37,7 @@ void raise_smem_limit(const void* fn, size_t bytes);
 // Process-wide kernel-variant knobs (gk_set_tuning); 0 = default.
 struct Tuning {
   std::atomic<int> scatter{0}, gather{0}, toeplitz{0}, precond{0}, fused{0}, fused_prof{0}, pcg_fused{0};
+  std::atomic<int> lean{0};  // lean one-launch 2-D MVM (lean2d.cu): 0 measured policy, 1 never, 2 always
   // fused 2-D MVM decomposition overrides (0 = heuristic)
   std::atomic<int> f2_stc{0}, f2_sl{0}, f2_gtc{0}, f2_gl{0}, f2_tsplit{0}, f2_per_sm{0};
   std::atomic<int> f2_skip{0};  // debug: bitmask of phases to skip (1 S, 2 T1, 4 T0, 8 G)

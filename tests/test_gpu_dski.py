@@ -244,3 +244,17 @@ def test_d3_tile_scatter_matches_oracle(order, with_gradients):
         assert rel(tile, ref) <= TOL
         assert rel(tile, lists) <= 1e-13
         assert np.array_equal(tile, g.mvm(V)) or nrhs > 2  # default path for 1-2 RHS is the tile kernel
+
+
+@pytest.mark.parametrize("lean", [1, 2])  # 1: fused2d one-launch kernel, 2: lean2d one-launch kernel
+@pytest.mark.parametrize("ell,n", [(0.5, 60), (0.4, 80), (0.3, 150)])  # grids 15², 17² (partial last segment), 21²
+def test_one_launch_2d_kernels_match_oracle(lean, ell, n):
+    g, r, _, _ = pair(n, 2, ell=ell, max_nodes=40)
+    rng = np.random.default_rng(n)
+    try:
+        gk.set_tuning("lean", lean)
+        for nrhs in (1, 2, 3, 8, 32, 33, 64):
+            V = rng.standard_normal((g.size(), nrhs))
+            assert rel(g.mvm(V), r.mvm(V)) <= TOL, nrhs
+    finally:
+        gk.set_tuning("lean", 0)

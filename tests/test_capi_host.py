@@ -99,3 +99,19 @@ def test_oracle_datasets_bit_identical_to_product(cfg):
     Xb, yb, dYb = O.make_dataset(cfg, 0)
     assert np.array_equal(Xa, Xb) and np.array_equal(ya, yb) and np.array_equal(dYa, dYb)
     assert np.array_equal(gk.stacked_targets(ya, dYa, ya.mean()), O.stacked_targets(yb, dYb, yb.mean()))
+
+
+def test_bench_reference_arm_loads_only_the_oracle():
+    """bench.py --impl reference must run the reference algorithm without the
+    product library: its inputs come from the oracle's own generators."""
+    import subprocess
+    import sys
+    code = ("import sys, types; sys.argv=['bench.py']; import bench; "
+            "a=types.SimpleNamespace(steps=1, warmup=0, gpus=1); line=bench.run_reference(a); "
+            "maps=open('/proc/self/maps').read(); "
+            "assert 'libgk_b200' not in maps, 'product library loaded'; "
+            "assert 'libgk_oracle' in maps; assert 'paper_1810_12283_b200' not in sys.modules; "
+            "print(line['value'] > 0)")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.strip().endswith("True")

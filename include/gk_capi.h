@@ -337,6 +337,20 @@ gk_status gk_dski_predict_variance_randomized(const gk_op* op, const gk_precond*
                                               int probes, uint64_t seed, double tol,
                                               int max_iterations, double* var);
 
+/* ---------------------------------------------------------------- row-sharded preconditioner
+ * SURVEY §8(e) (grid-slab sharding, C4): each rank holds the rows of Q1 and
+ * D^{-1/2} for its own rows of the system. The Woodbury apply of
+ * Preconditioner::apply (linalg.cpp:200-204) splits into a local projection
+ * T_r = Q1_rᵀ D_r^{-1/2} r_r (k×nrhs), an all-reduce T = Σ_r T_r, and a local
+ * finish z_r = D_r^{-1/2}(D_r^{-1/2} r_r − Q1_r T). Device pointers; row-
+ * minor (RHS innermost) blocks of this rank's rows. */
+gk_status gk_precond_from_q1_dev(const double* dQ1 /*N×k col-major*/, const double* dinv_sqrt /*N*/,
+                                 int64_t N, int64_t k, int device, gk_precond** out);
+gk_status gk_precond_project_dev(const gk_precond* M, const double* dR, double* dT, int64_t nrhs,
+                                 void* stream);
+gk_status gk_precond_finish_dev(const gk_precond* M, const double* dR, const double* dT, double* dZ,
+                                int64_t nrhs, void* stream);
+
 /* ---------------------------------------------------------------- datasets
  * Seeded synthetic workloads C1..C5 (BASELINE.json configs), generated on
  * the host with std::mt19937_64 + libstdc++ distributions like

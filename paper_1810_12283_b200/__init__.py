@@ -117,6 +117,9 @@ _SIGS = {
     "gk_dski_cross_covariance_jacobian": (C.c_int, [_vp, _dp, _i64, _dp, _i64]),
     "gk_dski_cross_covariance": (C.c_int, [_vp, _dp, _i64, _dp, _i64]),
     "gk_make_dataset": (C.c_int, [C.c_int, _u64, _i64p, _ip, _dp, _dp, _dp]),
+    "gk_precond_from_q1_dev": (C.c_int, [_vp, _vp, _i64, _i64, C.c_int, C.POINTER(_vp)]),
+    "gk_precond_project_dev": (C.c_int, [_vp, _vp, _vp, _i64, _vp]),
+    "gk_precond_finish_dev": (C.c_int, [_vp, _vp, _vp, _vp, _i64, _vp]),
     "gk_gp_solve": (C.c_int, [_vp, _vp, _dp, _i64, _i64, _d, C.c_int, _dp, _i64, _ip]),
     "gk_gp_logdet": (C.c_int, [_vp, C.c_int, C.c_int, _u64, _d, _d, C.c_int, _dp]),
     "gk_gp_log_marginal_likelihood": (C.c_int, [_vp, _vp, _dp, _d, C.c_int, C.c_int, C.c_int, _u64, _d, _d,
@@ -653,6 +656,22 @@ class Preconditioner:
         h = _vp()
         _check(_lib.gk_precond_from_pivchol(A.handle, factor.handle, C.byref(h)))
         return Preconditioner(_handle=h, size=A.size())
+
+    @staticmethod
+    def from_q1_dev(dQ1, ddinv, N, k, device=0):
+        """Preconditioner over an explicit Q1 (N×k col-major) and D^{-1/2} (N),
+        device pointers (a rank's rows of a row-sharded preconditioner)."""
+        h = _vp()
+        _check(_lib.gk_precond_from_q1_dev(dQ1, ddinv, int(N), int(k), int(device), C.byref(h)))
+        return Preconditioner(_handle=h, size=int(N))
+
+    def project_dev(self, dR, dT, nrhs, stream=0):
+        """T = Q1ᵀ D^{-1/2} r over this preconditioner's rows (RHS-minor r, k×nrhs T)."""
+        _check(_lib.gk_precond_project_dev(self._h, dR, dT, int(nrhs), stream))
+
+    def finish_dev(self, dR, dT, dZ, nrhs, stream=0):
+        """z = D^{-1/2}(D^{-1/2} r − Q1 T) for a given (all-reduced) T."""
+        _check(_lib.gk_precond_finish_dev(self._h, dR, dT, dZ, int(nrhs), stream))
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -1383,6 +1383,44 @@ gk_status gk_dski_predict_variance_randomized(const gk_op* h, const gk_precond* 
   });
 }
 
+// ---------------------------------------------------------------- row-sharded preconditioner
+gk_status gk_precond_from_q1_dev(const double* dQ1, const double* ddinv, int64_t N, int64_t k, int device,
+                                 gk_precond** out) {
+  return guard([&] {
+    if (N <= 0 || k <= 0 || !dQ1 || !ddinv || !out) fail(GK_ERR_ARG, "bad preconditioner factor");
+    DeviceGuard dg(device);
+    cudaStream_t s;
+    GK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    auto M = std::make_unique<gk_precond>();
+    M->impl = precond_from_q1(dQ1, ddinv, N, k, device, s);
+    M->impl->stream = s;
+    *out = M.release();
+  });
+}
+
+gk_status gk_precond_project_dev(const gk_precond* M, const double* dR, double* dT, int64_t nrhs, void* stream) {
+  return guard([&] {
+    if (!M || !M->impl) fail(GK_ERR_ARG, "null preconditioner");
+    if (nrhs < 1 || nrhs > 256) fail(GK_ERR_ARG, "nrhs must be in [1, 256]");
+    Precond& P = *M->impl;
+    std::lock_guard<std::mutex> lk(P.mu);
+    DeviceGuard dg(P.device);
+    precond_project(P, dR, int(nrhs), dT, S(stream));
+  });
+}
+
+gk_status gk_precond_finish_dev(const gk_precond* M, const double* dR, const double* dT, double* dZ, int64_t nrhs,
+                                void* stream) {
+  return guard([&] {
+    if (!M || !M->impl) fail(GK_ERR_ARG, "null preconditioner");
+    if (nrhs < 1 || nrhs > 256) fail(GK_ERR_ARG, "nrhs must be in [1, 256]");
+    Precond& P = *M->impl;
+    std::lock_guard<std::mutex> lk(P.mu);
+    DeviceGuard dg(P.device);
+    precond_finish(P, dR, dT, dZ, int(nrhs), S(stream));
+  });
+}
+
 gk_status gk_make_dataset(int config, uint64_t seed, int64_t* n, int* d, double* X, double* y, double* dY) {
   gk_status st = GK_OK;
   try {

@@ -2054,6 +2054,42 @@ void sub_dev(const double* a, const double* b, double* c, i64 n, cudaStream_t s)
   launched("sub");
 }
 
+// ================================================================ split preconditioner (row-sharded Q1)
+// T = Q1ᵀ D^{-1/2} r over this preconditioner's rows (k×nrhs, device): the
+// partial projection a row-sharded preconditioner all-reduces before
+// finishing.
+void precond_project(Precond& M, const double* r, int nrhs, double* T, cudaStream_t s) {
+  M.ensure(nrhs);
+  const size_t sh1 = sizeof(double) * (PC_RT * M.k + PC_RT * nrhs + M.k * nrhs);
+  raise_smem_limit((const void*)k_pc_proj, sh1);
+  k_pc_proj<<<RB, RT, sh1, s>>>(r, M.dinv.p, M.q1.p, M.N, int(M.k), nrhs, M.partial.p, nullptr);
+  launched("precond proj");
+  k_pc_fin<<<fin_blocks(int(M.k * nrhs)), 256, 0, s>>>(M.partial.p, int(M.k * nrhs), T);
+  launched("precond fin");
+}
+// z = D^{-1/2}(D^{-1/2} r − Q1 T) for a given (all-reduced) T.
+void precond_finish(Precond& M, const double* r, const double* T, double* z, int nrhs, cudaStream_t s) {
+  M.ensure(nrhs);
+  const size_t sh2 = sizeof(double) * (M.k * nrhs + RT);
+  raise_smem_limit((const void*)k_pc_apply, sh2);
+  k_pc_apply<<<RB, RT, sh2, s>>>(r, M.dinv.p, M.q1.p, T, M.N, int(M.k), nrhs, z, nullptr);
+  launched("precond apply");
+}
+// A preconditioner over an explicit Q1 (N×k col-major, device) and D^{-1/2}.
+std::unique_ptr<Precond> precond_from_q1(const double* Q1cm, const double* dinv, i64 N, i64 k, int device,
+                                         cudaStream_t s) {
+  auto M = std::make_unique<Precond>();
+  M->device = device;
+  M->N = N;
+  M->k = k;
+  M->q1.alloc(static_cast<size_t>(N * k));
+  M->dinv.alloc(static_cast<size_t>(N));
+  to_internal(nullptr, N, Q1cm, N, M->q1.p, int(k), s);  // col-major N×k -> row-major [N][k]
+  GK_CUDA(cudaMemcpyAsync(M->dinv.p, dinv, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+  GK_CUDA(cudaStreamSynchronize(s));
+  return M;
+}
+
 // ================================================================ pivoted Cholesky
 std::unique_ptr<PivChol> pivchol_run(Op& op, bool kernel_part, i64 max_rank, double trace_tol) {
   cudaStream_t s = op.stream;

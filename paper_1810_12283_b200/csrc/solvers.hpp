@@ -84,6 +84,14 @@ LanczosBatch lanczos_batch(Op& op, const double* start_int, int P, int steps,
 // host's std::mt19937_64(seeds[q]) streams (sign = bit 0 of each draw).
 void rademacher_dev(i64 n, const std::uint64_t* seeds_h, int P, double scale, double* out, i64 ld, cudaStream_t s);
 
+// Row-sharded preconditioner pieces: T = Q1ᵀ D^{-1/2} r, then
+// z = D^{-1/2}(D^{-1/2} r − Q1 T) with an all-reduced T; and a Precond over an
+// explicit Q1 (N×k col-major) and D^{-1/2} (device).
+void precond_project(Precond& M, const double* r, int nrhs, double* T, cudaStream_t s);
+void precond_finish(Precond& M, const double* r, const double* T, double* z, int nrhs, cudaStream_t s);
+std::unique_ptr<Precond> precond_from_q1(const double* Q1cm, const double* dinv, i64 N, i64 k, int device,
+                                         cudaStream_t s);
+
 // Small block products used by the GP glue (internal RHS-minor layouts; all
 // results deterministic, fixed summation order).
 //   C = A·Bm (rows×ka times ka×nb, Bm on the device, row-major)

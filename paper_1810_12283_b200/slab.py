@@ -39,9 +39,14 @@ class SlabShardedDskiOperator:
         nb0 = int(grid.dims[0]) - T + 1
         self.parts = slab_partition(np.clip(base0, 0, nb0 - 1), nb0, self.world)
         self.mine = self.parts[self.rank]
+        self.X_local = X[self.mine]
+        self.noise = tuple(noise)
         self.device = torch.cuda.current_device() if device is None else device
         self.dev = torch.device("cuda", self.device)
-        self.local = DskiOperator(kernel, grid, X[self.mine], noise, order, True, device=self.device)
+        # a rank whose slab holds no points still joins every all-reduce (with
+        # a zero grid vector) and owns no rows
+        self.local = (DskiOperator(kernel, grid, self.X_local, noise, order, True, device=self.device)
+                      if self.mine.size else None)
         self.M = grid.size()
         self.G = self.d + 1
 
@@ -61,6 +66,10 @@ class SlabShardedDskiOperator:
         st = torch.cuda.current_stream(self.dev).cuda_stream
         U = torch.empty(self.M * nrhs, dtype=torch.float64, device=self.dev) if U is None else U
         W = torch.empty_like(U) if W is None else W
+        if self.local is None:  # empty slab: contribute zeros to the grid sum, no rows to gather
+            U.zero_()
+            dist.all_reduce(U, op=dist.ReduceOp.SUM, group=self.group)
+            return
         self.local.stage_dev(0, Vi.data_ptr(), U.data_ptr(), nrhs, stream=st)   # Bᵣᵀ vᵣ, full grid
         dist.all_reduce(U, op=dist.ReduceOp.SUM, group=self.group)             # Σ_r over NVLink
         self.local.stage_dev(1, U.data_ptr(), W.data_ptr(), nrhs, stream=st)   # K_UU
@@ -78,6 +87,12 @@ class SlabShardedDskiOperator:
         nrhs = V2.shape[1]
         rows = self.local_rows()
         Nl = rows.size
+        if self.local is None:
+            self.mvm_local_dev(None, None, nrhs)
+            out = torch.zeros((nrhs, self.size()), dtype=torch.float64, device=self.dev)
+            dist.all_reduce(out, op=dist.ReduceOp.SUM, group=self.group)
+            res = out.T.cpu().numpy()
+            return res[:, 0] if vec else res
         Vext = torch.from_numpy(np.ascontiguousarray(V2[rows].T)).to(self.dev)  # (nrhs, Nl) = col-major Nl×nrhs
         Vi = torch.empty(Nl * nrhs, dtype=torch.float64, device=self.dev)
         Oi = torch.empty_like(Vi)

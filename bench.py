@@ -727,8 +727,30 @@ def c4_slab(args, world, rank, local, dist):
                               "achieved": it_bytes / (us_it * 1e-6) / 1e9, "peak": hbm, "unit": "GB/s",
                               "frac": it_bytes / (us_it * 1e-6) / 1e9 / hbm,
                               "bytes_formula": "2*8*N*k (Q1 twice) + MVM bytes (SURVEY 8(d), 1 RHS) + 8*8*N"},
-                 "parallelism": "1 GPU (the PCG itself is not slab-sharded)"}
+                 "parallelism": "1 GPU, unsharded (the fused single-GPU PCG path)"}
+    slab_solve = None
+    if not args.no_c4_solve:  # the same solve with rows sharded by grid slab (slab_solver.py)
+        from paper_1810_12283_b200 import slab_solver as S
+        be = S.GpuSlabBackend(sop)
+        t_pc, f = wall(lambda: S.slab_pivoted_cholesky(be, 200))
+        t_pb, Ms = wall(lambda: S.SlabPreconditioner(be, f.L, be.noise_diag()))
+        bl = torch.from_numpy(np.ascontiguousarray(b[rows]).reshape(-1, 1)).to(dev)
+        S.slab_cg(be, bl, 1e-4, 3, Ms)  # warm
+        if world > 1:
+            dist.barrier()
+        t_cg, res = wall(lambda: S.slab_cg(be, bl, 1e-4, 1000, Ms))
+        tt = torch.tensor([t_pc, t_pb, t_cg], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_pc, t_pb, t_cg = [float(v) for v in tt.tolist()]
+        slab_solve = {"pivchol_s": t_pc, "precond_build_s": t_pb, "pcg_s": t_cg,
+                      "pcg_iterations": int(res.iterations[0]), "pcg_converged": bool(res.converged[0]),
+                      "us_per_iteration": t_cg / max(1, res.iterations[0]) * 1e6,
+                      "parallelism": f"grid-slab x{world}: rows sharded; CG dots, the k x B preconditioner "
+                                     "projection and the grid vector all-reduced over NCCL; max-loc pivots",
+                      "timing": "host wall clock, max over ranks"}
     return {"workload": "C4: D-SKI d=2 n=150000 (N=450000) grid 400x400 SE ell=0.02 sigma=1e-2, 1 RHS", "solve": solve,
+            "slab_solve": slab_solve,
             "fused_1gpu": fused,
             "parallelism": f"grid-slab x{world} (NCCL all-reduce of the grid vector per MVM)",
             "scaling": "strong", "ms_per_mvm": ms, "value": sop.size() * nrhs / (ms * 1e-3),

@@ -1133,8 +1133,8 @@ __global__ void k_diagonal(DskiView op, const double* __restrict__ tvec, const i
 // short 1-D Toeplitz–stencil product), so row entries are products of 1-D
 // stencil dots. Each CTA rebuilds the α_j in shared memory.
 template <int D, int T>
-__global__ void k_row(DskiView op, const double* __restrict__ tvec, const int* __restrict__ toff,
-                      int src_s, int src_g, double* __restrict__ out) {
+__device__ __forceinline__ void row_body(const DskiView& op, const double* __restrict__ tvec,
+                                         const int* __restrict__ toff, int src_s, int src_g, double* __restrict__ out) {
   extern __shared__ double alpha[];  // Σ m_j
   constexpr int STRIDE = D * 2 * T;
   const int4 sb = op.base[src_s];
@@ -1181,6 +1181,24 @@ __global__ void k_row(DskiView op, const double* __restrict__ tvec, const int* _
     if (it == r_self) prod += (g == 0 ? op.nv2 : op.ng2);
     out[it] = prod;
   }
+}
+
+template <int D, int T>
+__global__ void k_row(DskiView op, const double* __restrict__ tvec, const int* __restrict__ toff,
+                      int src_s, int src_g, double* __restrict__ out) {
+  row_body<D, T>(op, tvec, toff, src_s, src_g, out);
+}
+
+// The same row with the INTERNAL row index read from device memory (a
+// device-side pivot), skipped when *active == 0: lets the pivoted Cholesky
+// loop run without a host round trip per pivot.
+template <int D, int T>
+__global__ void k_row_dev(DskiView op, const double* __restrict__ tvec, const int* __restrict__ toff,
+                          const long long* __restrict__ r_int, const int* __restrict__ active,
+                          double* __restrict__ out) {
+  if (!*active) return;
+  const long long r = *r_int;
+  row_body<D, T>(op, tvec, toff, int(r % op.n), int(r / op.n), out);
 }
 
 // Test-point stencils for prediction (gp.cpp:480-495): values/grads from a
@@ -1473,6 +1491,8 @@ struct DskiOp final : Op {
   }
   void diagonal(double* dd, cudaStream_t s) override;
   void row(i64 r_ext, double* out, cudaStream_t s) override;
+  bool row_dev(const i64* d_r_int, const int* d_active, double* out, cudaStream_t s) override;
+  bool has_row_dev() const override { return true; }
 };
 
 #define GK_DISPATCH_DT(D_, T_, ...)                                   \
@@ -1733,6 +1753,17 @@ void DskiOp::diagonal(double* dd, cudaStream_t s) {
   const DskiView vw = view();
   GK_DISPATCH_DT(d, T, { k_diagonal<D, T><<<grid_blocks(n), 256, 0, s>>>(vw, tvec.p, toff.p, dd); });
   launched("dski diagonal");
+}
+
+bool DskiOp::row_dev(const i64* d_r_int, const int* d_active, double* out, cudaStream_t s) {
+  const DskiView vw = view();
+  const int shm = int(sizeof(double)) * (m[0] + (d > 1 ? m[1] : 0) + (d > 2 ? m[2] : 0));
+  GK_DISPATCH_DT(d, T, {
+    k_row_dev<D, T><<<grid_blocks(N), 256, shm, s>>>(vw, tvec.p, toff.p, reinterpret_cast<const long long*>(d_r_int),
+                                                    d_active, out);
+  });
+  launched("dski row (device pivot)");
+  return true;
 }
 
 void DskiOp::row(i64 r_ext, double* out, cudaStream_t s) {

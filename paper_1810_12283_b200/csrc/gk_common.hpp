@@ -37,6 +37,7 @@ void raise_smem_limit(const void* fn, size_t bytes);
 // Process-wide kernel-variant knobs (gk_set_tuning); 0 = default.
 struct Tuning {
   std::atomic<int> scatter{0}, gather{0}, toeplitz{0}, precond{0}, fused{0}, fused_prof{0}, pcg_fused{0};
+  std::atomic<int> pivchol{0};  // 1 = host-synchronised pivot loop (3 syncs per pivot)
   std::atomic<int> lean{0};  // lean one-launch 2-D MVM (lean2d.cu): 0 measured policy, 1 never, 2 always
   // fused 2-D MVM decomposition overrides (0 = heuristic)
   std::atomic<int> f2_stc{0}, f2_sl{0}, f2_gtc{0}, f2_gl{0}, f2_tsplit{0}, f2_per_sm{0};
@@ -188,6 +189,13 @@ struct Op {
   virtual void diagonal(double* d, cudaStream_t s) = 0;
   // row r (EXTERNAL index) including noise, written in internal order
   virtual void row(i64 r_ext, double* out, cudaStream_t s) = 0;
+  // Row *d_r_int (INTERNAL index, read from device memory) written in
+  // internal order, skipped when *d_active == 0; false = not implemented
+  // (callers then use row() with a host round trip).
+  virtual bool row_dev(const i64* /*d_r_int*/, const int* /*d_active*/, double* /*out*/, cudaStream_t) {
+    return false;
+  }
+  virtual bool has_row_dev() const { return false; }
   // internal row index -> external row index (device array or null = identity)
   virtual const i64* d_ext_of_int() const { return nullptr; }
   // Persistent PCG (MVM + fused vector step in one cooperative launch, up to

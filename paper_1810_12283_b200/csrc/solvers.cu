@@ -2090,6 +2090,81 @@ std::unique_ptr<Precond> precond_from_q1(const double* Q1cm, const double* dinv,
   return M;
 }
 
+// ---------------------------------------------------------------- device-resident pivot loop
+// State of the on-device pivoted Cholesky loop (one per factorisation).
+struct PvDev {
+  double stats[5];   // last k_pv_stats_fin output: min, sum, max, ext bits, int bits
+  double initial, scale, tol_abs;  // initial trace, max(diag), trace_tol · initial
+  double dmax, sq, residual;
+  double fail_val;
+  long long piv_int, piv_ext;
+  int active;   // 1 while the loop runs (0 once a stop condition or a failure hit)
+  int kdone;    // pivots taken
+  int failed;   // 1: residual diagonal below −1e-10·scale (the reference throws)
+};
+
+// Start of step k: the stop tests of linalg.cpp:153-154 on the last stats.
+__global__ void k_pv_begin(PvDev* st, int k, long long* pivots) {
+  if (threadIdx.x != 0 || !st->active) return;
+  const double dmax = st->stats[2];
+  if (dmax <= 0.0 || st->residual <= st->tol_abs) {
+    st->active = 0;
+    return;
+  }
+  st->dmax = dmax;
+  st->sq = sqrt(dmax);
+  st->piv_ext = reinterpret_cast<const long long*>(st->stats)[3];
+  st->piv_int = reinterpret_cast<const long long*>(st->stats)[4];
+  pivots[k] = st->piv_ext;
+  st->kdone = k + 1;
+}
+
+__global__ void k_pv_update_dev(double* __restrict__ col, double* __restrict__ L, int k, i64 N,
+                                const double* __restrict__ noise, int kernel_part, const PvDev* __restrict__ st,
+                                double* __restrict__ d) {
+  if (!st->active) return;
+  extern __shared__ double lp[];
+  const i64 piv = st->piv_int;
+  const double sq = st->sq;
+  for (int j = threadIdx.x; j < k; j += blockDim.x) lp[j] = L[(i64)j * N + piv];
+  __syncthreads();
+  for (i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x; r < N; r += (i64)gridDim.x * blockDim.x) {
+    double c = col[r];
+    if (r == piv && kernel_part) c -= noise[piv];
+    if (k > 0) {
+      double s = 0.0;
+      for (int j = 0; j < k; ++j) s += L[(i64)j * N + r] * lp[j];
+      c -= s;
+    }
+    c /= sq;
+    L[(i64)k * N + r] = c;
+    d[r] -= c * c;
+  }
+}
+
+// After the update: the PSD check on min(d) (linalg.cpp:165-167). A failure
+// stops the loop and records the value (the host raises after the loop).
+__global__ void k_pv_check(PvDev* st) {
+  if (threadIdx.x != 0 || !st->active) return;
+  if (st->stats[0] < -1e-10 * st->scale) {
+    st->failed = 1;
+    st->fail_val = st->stats[0];
+    st->active = 0;
+  }
+}
+
+__global__ void k_pv_clamp_dev(double* __restrict__ d, i64 N, const PvDev* __restrict__ st) {
+  if (!st->active) return;
+  const i64 piv = st->piv_int;
+  for (i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x; r < N; r += (i64)gridDim.x * blockDim.x)
+    d[r] = (r == piv) ? 0.0 : fmax(d[r], 0.0);
+}
+
+// End of step: residual trace = Σ d (linalg.cpp:171).
+__global__ void k_pv_end(PvDev* st) {
+  if (threadIdx.x == 0 && st->active) st->residual = st->stats[1];
+}
+
 // ================================================================ pivoted Cholesky
 std::unique_ptr<PivChol> pivchol_run(Op& op, bool kernel_part, i64 max_rank, double trace_tol) {
   cudaStream_t s = op.stream;
@@ -2116,14 +2191,14 @@ std::unique_ptr<PivChol> pivchol_run(Op& op, bool kernel_part, i64 max_rank, dou
   k_pv_init<<<blocks_for(N), 256, 0, s>>>(diag.p, noise.p, kernel_part ? 1 : 0, N, d.p);
   launched("pivchol init");
   DevBuf<double> pmin(RB), psum(RB), pmax(RB), stats(5);
-  DevBuf<i64> pext(RB), pint(RB);
+  DevBuf<i64> pext(RB), pint_(RB);
   HostBuf pinned;
   pinned.reserve(5);
   double* sh = pinned.p;
   auto stats_of_d = [&]() {
-    k_pv_stats<<<RB, RT, 0, s>>>(d.p, op.d_ext_of_int(), N, pmin.p, psum.p, pmax.p, pext.p, pint.p);
+    k_pv_stats<<<RB, RT, 0, s>>>(d.p, op.d_ext_of_int(), N, pmin.p, psum.p, pmax.p, pext.p, pint_.p);
     launched("pivchol stats");
-    k_pv_stats_fin<<<1, 32, 0, s>>>(pmin.p, psum.p, pmax.p, pext.p, pint.p, RB, stats.p);
+    k_pv_stats_fin<<<1, 32, 0, s>>>(pmin.p, psum.p, pmax.p, pext.p, pint_.p, RB, stats.p);
     launched("pivchol stats fin");
     GK_CUDA(cudaMemcpyAsync(sh, stats.p, sizeof(double) * 5, cudaMemcpyDeviceToHost, s));
     GK_CUDA(cudaStreamSynchronize(s));
@@ -2134,6 +2209,59 @@ std::unique_ptr<PivChol> pivchol_run(Op& op, bool kernel_part, i64 max_rank, dou
   f->residual_trace = sh[1];
   const double scale = std::max(sh[2], 1e-300);
   i64 k = 0;
+  // Device-resident loop (the operator computes a row from a device-side
+  // pivot): every step's argmax, row, update, PSD check, clamp and trace stay
+  // on the GPU — one host synchronisation for the whole factorisation
+  // instead of three per pivot. Same operations, same order as below.
+  DevBuf<PvDev> pst(1);
+  DevBuf<long long> dpiv(static_cast<size_t>(std::max<i64>(max_rank, 1)));
+  if (max_rank > 0 && g_tuning.pivchol.load() == 0 && op.has_row_dev()) {
+    PvDev h{};
+    std::memcpy(h.stats, sh, sizeof(h.stats));
+    h.initial = sh[1];
+    h.scale = scale;
+    h.tol_abs = trace_tol * sh[1];
+    h.residual = sh[1];
+    h.active = 1;
+    GK_CUDA(cudaMemcpyAsync(pst.p, &h, sizeof(PvDev), cudaMemcpyHostToDevice, s));
+    const i64* pint = reinterpret_cast<const i64*>(&pst.p->piv_int);
+    const int* act = &pst.p->active;
+    double* st_stats = pst.p->stats;
+    for (i64 kk = 0; kk < max_rank; ++kk) {
+      k_pv_begin<<<1, 32, 0, s>>>(pst.p, int(kk), dpiv.p);
+      launched("pivchol begin");
+      op.row_dev(pint, act, col.p, s);
+      k_pv_update_dev<<<blocks_for(N), 256, sizeof(double) * std::max<i64>(kk, 1), s>>>(
+          col.p, f->L.p, int(kk), N, noise.p, kernel_part ? 1 : 0, pst.p, d.p);
+      launched("pivchol update");
+      k_pv_stats<<<RB, RT, 0, s>>>(d.p, op.d_ext_of_int(), N, pmin.p, psum.p, pmax.p, pext.p, pint_.p);
+      launched("pivchol stats");
+      k_pv_stats_fin<<<1, 32, 0, s>>>(pmin.p, psum.p, pmax.p, pext.p, pint_.p, RB, st_stats);
+      launched("pivchol stats fin");
+      k_pv_check<<<1, 32, 0, s>>>(pst.p);
+      launched("pivchol check");
+      k_pv_clamp_dev<<<blocks_for(N), 256, 0, s>>>(d.p, N, pst.p);
+      launched("pivchol clamp");
+      k_pv_stats<<<RB, RT, 0, s>>>(d.p, op.d_ext_of_int(), N, pmin.p, psum.p, pmax.p, pext.p, pint_.p);
+      launched("pivchol stats");
+      k_pv_stats_fin<<<1, 32, 0, s>>>(pmin.p, psum.p, pmax.p, pext.p, pint_.p, RB, st_stats);
+      launched("pivchol stats fin");
+      k_pv_end<<<1, 32, 0, s>>>(pst.p);
+      launched("pivchol end");
+    }
+    GK_CUDA(cudaMemcpyAsync(&h, pst.p, sizeof(PvDev), cudaMemcpyDeviceToHost, s));
+    GK_CUDA(cudaStreamSynchronize(s));
+    k = h.kdone;
+    std::vector<long long> ph(static_cast<size_t>(std::max<i64>(k, 1)));
+    if (k > 0) GK_CUDA(cudaMemcpy(ph.data(), dpiv.p, sizeof(long long) * k, cudaMemcpyDeviceToHost));
+    for (i64 j = 0; j < k; ++j) f->pivots.push_back(ph[static_cast<size_t>(j)]);
+    if (h.failed)
+      fail(GK_ERR_RUNTIME, "pivoted Cholesky: operator is not positive semidefinite (residual diagonal " +
+                               std::to_string(h.fail_val) + ")");
+    f->residual_trace = h.residual;
+    f->k = k;
+    return f;
+  }
   for (; k < max_rank; ++k) {
     const double dmax = sh[2];
     i64 piv_ext, piv_int;

@@ -311,3 +311,27 @@ def test_fused_pcg_step_matches_unfused(nrhs, with_precond, variant):
         assert np.linalg.norm(f.x - r.x) <= 1e-4 * max(np.linalg.norm(r.x), 1e-300) or np.linalg.norm(r.x) == 0
     if nrhs > 2:
         assert fused[2].iterations == 0 and fused[2].converged
+
+
+@pytest.mark.parametrize("cfg,rank", [(1, 20), (2, 50)])
+def test_device_resident_pivot_loop_matches_host_loop_and_oracle(cfg, rank):
+    """pivchol_run's device-resident loop (D-SKI rows from a device-side pivot,
+    one host sync per factorisation) against the host-synchronised loop and
+    the oracle: identical pivots (bit-exact order) and L."""
+    X, y, dY = gk.make_dataset(cfg, 0)
+    ell, nodes = {1: (0.15, 60), 2: (0.2, 100)}[cfg]
+    grid = gk.Grid.cover(X, 1e-4, 3, nodes)
+    op = gk.DskiOperator(gk.KernelSpec(ell, 1.0), grid, X, (1e-2, 1e-2))
+    try:
+        gk.set_tuning("pivchol", 1)
+        fh = gk.pivoted_cholesky(op, rank, kernel_part=True)
+        gk.set_tuning("pivchol", 0)
+        fd = gk.pivoted_cholesky(op, rank, kernel_part=True)
+    finally:
+        gk.set_tuning("pivchol", 0)
+    assert list(fd.pivots) == list(fh.pivots)
+    assert np.max(np.abs(fd.L - fh.L)) <= 1e-12 * np.max(np.abs(fh.L))
+    assert fd.residual_trace == pytest.approx(fh.residual_trace, rel=1e-12)
+    r = O.DskiOperator(O.KernelSpec(ell, 1.0), O.Grid(grid.dims, grid.origin, grid.spacing), X, (1e-2, 1e-2))
+    fr = O.pivoted_cholesky(r, rank, noise_diag=r.noise_diagonal())
+    assert [int(p) for p in fd.pivots] == [int(p) for p in fr.pivots]

@@ -1329,6 +1329,19 @@ struct DskiOp final : Op {
   // a unit emits nodes [za, zb) of its column (nodes no point touches are 0)
   DevBuf<int4> col3_units;
   int col3_nunits = 0;
+  // d = 3 gather units (k_gather_units3): {b0, b1, za, zb} cell-line runs and
+  // their sorted-point ranges; zspan = the longest block z extent (zb - za + T - 1)
+  DevBuf<int4> g3_units;
+  DevBuf<int2> g3_range;
+  int g3_nunits = 0, g3_zspan = 0;
+  // d = 3 unit-push scatter: scratch node offsets per unit, and per node
+  // column the entries {unit, ab} sorted by (za, unit) with per-(column,
+  // 8-node z segment) first entries
+  DevBuf<long long> s3_uoff;
+  DevBuf<int> s3_cstart, s3_cseg;
+  DevBuf<int2> s3_cent;
+  long long s3_nodes = 0;
+  int s3_nzs = 0;
   // tile scatter (k_scatter_tile3): per TB×TB tile of node columns the points
   // reaching it in base-cell order (b2 major); units {tile, za | zb << 16,
   // first entry (window halo included), end entry}
@@ -1340,6 +1353,7 @@ struct DskiOp final : Op {
   std::vector<i64> perm_h, inv_h;
   DevBuf<double> origin_d, h_d;
   DevBuf<double> grid_u, grid_w, grid_t, grid_h, grid_p;  // per-MVM grid scratch (guarded by mu / caller)
+  mutable DevBuf<double> s3_scratch;  // unit-push scatter blocks (s3_nodes × nrhs)
   std::vector<int> cell_start_h;          // host copy (fused-plan sizing)
   std::vector<std::unique_ptr<Fused2dPlan>> fplans;  // one-launch d = 2 MVM plans, per nrhs
   std::vector<std::unique_ptr<Lean2dPlan>> lplans;   // lean one-launch d = 2 MVM plans, per nrhs
@@ -1515,6 +1529,228 @@ static void smem_attr(const void* fn, size_t bytes) {
   if (bytes > 48 * 1024) raise_smem_limit(fn, bytes);
 }
 
+// d = 3 gather over cell-line units (B w + noise, dski.cpp:221-226): a unit
+// is a run of occupied base cells (b0, b1, [za, zb)) of one cell line; its
+// points are contiguous in the sorted order and all read the node block
+// [b0, b0+T) × [b1, b1+T) × [za, zb+T-1) × RHS. The CTA stages that block in
+// shared memory once (36 contiguous z-runs), then every (point, RHS) task
+// contracts its 6×6×6 stencil from shared memory — instead of 216 L2 reads
+// per (point, RHS), one L2 read of the block per unit (C3's surface points
+// pile up to ~180 per cell). Same summation order as k_gather_lean.
+constexpr int G3U_THREADS = 256;
+template <int T, bool GRAD>
+__global__ void __launch_bounds__(G3U_THREADS) k_gather_units3(DskiView op, const int4* __restrict__ units, int nunits,
+                                                               const int2* __restrict__ urange,
+                                                               const double* __restrict__ w,
+                                                               const double* __restrict__ v,
+                                                               double* __restrict__ out, int nrhs, int noise,
+                                                               int zmax) {
+  extern __shared__ double blk[];  // [T][T][nzb][nrhs]
+  const int m1 = op.m[1], m2 = op.m[2];
+  constexpr int REC = 3 * 2 * T;
+  const size_t gstride = (size_t)op.n * nrhs;
+  for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+    const int4 U = __ldg(units + u);  // b0, b1, za, zb
+    const int2 pr = __ldg(urange + u);
+    const int za = U.z, nzb = min(U.w - U.z + T - 1, zmax);
+    const int run = nzb * nrhs;  // one (k0, k1) z-run, contiguous in w
+    __syncthreads();  // the previous unit is done with the block
+    // 36 contiguous z-runs (one per node column of the block), a warp per run
+    for (int ab = threadIdx.x >> 5; ab < T * T; ab += G3U_THREADS / 32) {
+      const int a = ab / T, b = ab - a * T;
+      const double* src = w + (((size_t)(U.x + a) * m1 + (U.y + b)) * m2 + za) * nrhs;
+      double* dst = blk + ab * run;
+      for (int q = threadIdx.x & 31; q < run; q += 32) dst[q] = __ldg(src + q);
+    }
+    __syncthreads();
+    const int ntask = (pr.y - pr.x) * nrhs;
+    for (int t = threadIdx.x; t < ntask; t += G3U_THREADS) {
+      const int pl = t / nrhs, r = t - pl * nrhs;
+      const int sidx = pr.x + pl;
+      const double* rec = op.wts + (size_t)sidx * REC;
+      const int zo = __ldg(&op.base[sidx].z) - za;
+      double wr_[REC];  // the point's (w, ∂w) per axis in registers
+#pragma unroll
+      for (int q = 0; q < REC; ++q) wr_[q] = __ldg(rec + q);
+      double o[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int t0 = 0; t0 < T; ++t0) {
+        double R0 = 0.0, R1 = 0.0, R2 = 0.0;
+#pragma unroll
+        for (int t1 = 0; t1 < T; ++t1) {
+          const double* wr = blk + ((t0 * T + t1) * nzb + zo) * nrhs + r;
+          double uu[T];
+#pragma unroll
+          for (int t2 = 0; t2 < T; ++t2) uu[t2] = wr[t2 * nrhs];
+          double rr = 0.0, qq = 0.0;
+#pragma unroll
+          for (int t2 = 0; t2 < T; ++t2) {
+            rr += wr_[4 * T + t2] * uu[t2];
+            if constexpr (GRAD) qq += wr_[5 * T + t2] * uu[t2];
+          }
+          const double w1 = wr_[2 * T + t1];
+          R0 += w1 * rr;
+          if constexpr (GRAD) {
+            R1 += wr_[3 * T + t1] * rr;
+            R2 += w1 * qq;
+          }
+        }
+        const double w0 = wr_[t0];
+        o[0] += w0 * R0;
+        if constexpr (GRAD) {
+          o[1] += wr_[T + t0] * R0;
+          o[2] += w0 * R1;
+          o[3] += w0 * R2;
+        }
+      }
+      constexpr int NG = GRAD ? 4 : 1;
+      const size_t idx0 = (size_t)sidx * nrhs + r;
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        const size_t idx = idx0 + g * gstride;
+        double val = o[g];
+        if (noise) val += (g == 0 ? op.nv2 : op.ng2) * __ldg(v + idx);
+        out[idx] = val;
+      }
+    }
+  }
+}
+
+// d = 3 scatter Bᵀv (dski.cpp:213-219) as a push per cell-line unit plus a
+// deterministic merge. Push: CTA per unit (the gather's units: a run of
+// occupied base cells of one cell line); its points are staged in shared
+// memory and thread (node column ab of the unit's 6×6 block, RHS) walks them in
+// order (sorted by base z) with a rolling register window along z, writing
+// the unit's block of Bᵀv contributions once per node into a scratch area.
+// Every point's data is read once (not once per covering node column).
+// Merge: thread (node column, 8-node z segment, RHS) sums the blocks of the
+// units covering it in fixed (z-start, unit) order. No atomics anywhere.
+constexpr int S3U_THREADS = 128;
+constexpr int S3U_MAXP = 40;  // points staged per pass (a unit with more takes several passes)
+template <int T, bool GRAD>
+__global__ void __launch_bounds__(S3U_THREADS) k_scatter_upush3(DskiView op, const int4* __restrict__ units,
+                                                                int nunits, const int2* __restrict__ urange,
+                                                                const long long* __restrict__ uoff,
+                                                                const double* __restrict__ v,
+                                                                double* __restrict__ scratch, int nrhs) {
+  constexpr int REC = 3 * 2 * T;
+  constexpr int NG = GRAD ? 4 : 1;
+  extern __shared__ double sm3[];
+  double* sw = sm3;                       // [S3U_MAXP][REC]
+  double* sv = sw + S3U_MAXP * REC;       // [S3U_MAXP][NG][nrhs]
+  int* sz = reinterpret_cast<int*>(sv + S3U_MAXP * NG * nrhs);  // [S3U_MAXP]
+  const size_t gstride = (size_t)op.n * nrhs;
+  const int ntask = T * nrhs;  // thread (a, r) owns the T node columns (a, 0..T-1) of the block
+  for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+    const int4 U = __ldg(units + u);
+    const int2 pr = __ldg(urange + u);
+    const int za = U.z, nzb = U.w - U.z + T - 1;
+    double* out = scratch + (size_t)__ldg(uoff + u) * nrhs;
+    // rolling windows acc[b][t] <-> node (a, b, zc + t)
+    double acc[T][T];
+#pragma unroll
+    for (int b = 0; b < T; ++b)
+#pragma unroll
+      for (int t = 0; t < T; ++t) acc[b][t] = 0.0;
+    int zc = 0;
+    const int tk = threadIdx.x;
+    const bool live = tk < ntask;
+    const int a = live ? tk / nrhs : 0, r = live ? tk - (tk / nrhs) * nrhs : 0;
+    auto emit = [&]() {  // node zc of the T columns is final
+      if (live)
+#pragma unroll
+        for (int b = 0; b < T; ++b) out[((size_t)(a * T + b) * nzb + zc) * nrhs + r] = acc[b][0];
+#pragma unroll
+      for (int b = 0; b < T; ++b) {
+#pragma unroll
+        for (int k = 0; k < T - 1; ++k) acc[b][k] = acc[b][k + 1];
+        acc[b][T - 1] = 0.0;
+      }
+      ++zc;
+    };
+    for (int p0 = pr.x; p0 < pr.y; p0 += S3U_MAXP) {
+      const int np = min(S3U_MAXP, pr.y - p0);
+      __syncthreads();  // previous chunk / unit done with the stage
+      for (int e = threadIdx.x; e < np * REC; e += S3U_THREADS) sw[e] = __ldg(op.wts + (size_t)p0 * REC + e);
+      for (int pl = threadIdx.x / 32; pl < np; pl += S3U_THREADS / 32)
+        for (int q = threadIdx.x & 31; q < NG * nrhs; q += 32) {
+          const int g = q / nrhs, rr = q - g * nrhs;
+          sv[pl * NG * nrhs + q] = __ldg(v + g * gstride + (size_t)(p0 + pl) * nrhs + rr);
+        }
+      for (int e = threadIdx.x; e < np; e += S3U_THREADS) sz[e] = __ldg(&op.base[p0 + e].z) - za;
+      __syncthreads();
+      for (int pl = 0; pl < np; ++pl) {
+        const double* w = sw + pl * REC;
+        const int zo = sz[pl];
+        while (zc < zo) emit();
+        const double* vv = sv + pl * NG * nrhs + r;
+        const double wa = w[a], v0 = vv[0];
+        double ca, cb = 0.0, cc = 0.0;  // per-b coefficients: A_b = wb·ca + dwb·cb, B_b = wb·cc
+        ca = wa * v0;
+        if constexpr (GRAD) {
+          ca = fma(w[T + a], vv[nrhs], ca);
+          cb = wa * vv[2 * nrhs];
+          cc = wa * vv[3 * nrhs];
+        }
+        double z2[T], dz2[T];
+#pragma unroll
+        for (int c = 0; c < T; ++c) {
+          z2[c] = w[4 * T + c];
+          dz2[c] = GRAD ? w[5 * T + c] : 0.0;
+        }
+#pragma unroll
+        for (int b = 0; b < T; ++b) {
+          const double wb = w[2 * T + b];
+          const double A = GRAD ? fma(w[3 * T + b], cb, wb * ca) : wb * ca;
+          const double Bc = wb * cc;
+#pragma unroll
+          for (int c = 0; c < T; ++c) acc[b][c] = GRAD ? fma(dz2[c], Bc, fma(z2[c], A, acc[b][c])) : fma(z2[c], A, acc[b][c]);
+        }
+      }
+    }
+    while (zc < nzb) emit();
+  }
+}
+
+// Merge: u(col, z, r) = Σ over the entries {unit, ab} of column col whose
+// block covers z, in the column's fixed (za, unit) order.
+__global__ void __launch_bounds__(256) k_scatter_merge3(int ncol, int m2, int nzs, int T,
+                                                       const int* __restrict__ cstart,
+                                                       const int2* __restrict__ cent,
+                                                       const int* __restrict__ cseg,
+                                                       const int4* __restrict__ units,
+                                                       const long long* __restrict__ uoff,
+                                                       const double* __restrict__ scratch, double* __restrict__ u,
+                                                       int nrhs) {
+  const i64 ntask = (i64)ncol * nzs * nrhs;
+  for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < ntask; t += (i64)gridDim.x * blockDim.x) {
+    const int r = int(t % nrhs);
+    const i64 cz = t / nrhs;
+    const int zs = int(cz % nzs), col = int(cz / nzs);
+    const int z0 = zs * 8;
+    double acc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = 0.0;
+    const int e1 = __ldg(cstart + col + 1);
+    for (int e = __ldg(cseg + cz); e < e1; ++e) {
+      const int2 en = __ldg(cent + e);
+      const int4 U = __ldg(units + en.x);
+      const int za = U.z, nzb = U.w - U.z + T - 1;
+      if (za >= z0 + 8) break;  // entries sorted by za
+      if (za + nzb <= z0) continue;
+      const double* src = scratch + ((size_t)__ldg(uoff + en.x) + (size_t)en.y * nzb) * nrhs + r;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int zl = z0 + k - za;
+        if (zl >= 0 && zl < nzb) acc[k] += __ldcg(src + (size_t)zl * nrhs);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (z0 + k < m2) u[((size_t)col * m2 + z0 + k) * nrhs + r] = acc[k];
+  }
+}
+
 // Lean-kernel launch shape: x = RHS lanes (≤ 32), y = items per block, shrunk
 // (down to one warp) when there are too few items to give every SM ~4 CTAs.
 static dim3 lean_block(int nrhs, i64 items) {
@@ -1606,6 +1842,23 @@ void DskiOp::scatter(const double* v, double* u, int nrhs, cudaStream_t s) const
     launched("dski scatter (d=1 node blocks)");
     return;
   }
+  if (d == 3 && variant == 0 && s3_uoff.p && G && T * nrhs <= S3U_THREADS) {  // unit push + merge
+    const int NG = 4;
+    const size_t smem = sizeof(double) * size_t(S3U_MAXP) * (3 * 2 * T + NG * nrhs) + sizeof(int) * S3U_MAXP;
+    const void* fn = T == 6 ? (const void*)k_scatter_upush3<6, true> : (const void*)k_scatter_upush3<4, true>;
+    if (smem > 48 * 1024) raise_smem_limit(fn, smem);
+    s3_scratch.reserve(static_cast<size_t>(s3_nodes) * nrhs);
+    const unsigned gp = static_cast<unsigned>(std::min(g3_nunits, 148 * 16));
+    if (T == 6) k_scatter_upush3<6, true><<<gp, S3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, s3_uoff.p, v, s3_scratch.p, nrhs);
+    else k_scatter_upush3<4, true><<<gp, S3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, s3_uoff.p, v, s3_scratch.p, nrhs);
+    launched("dski scatter (d=3 unit push)");
+    const int ncol = m[0] * m[1];
+    k_scatter_merge3<<<grid_blocks(i64(ncol) * s3_nzs * nrhs), 256, 0, s>>>(ncol, m[2], s3_nzs, T, s3_cstart.p, s3_cent.p,
+                                                                          s3_cseg.p, g3_units.p, s3_uoff.p,
+                                                                          s3_scratch.p, u, nrhs);
+    launched("dski scatter (d=3 unit merge)");
+    return;
+  }
   // column tiles: measured faster than the per-column lists for 1-2 RHS at C3
   // (1 RHS: 228 vs 323 us), slower for 17+ RHS (every warp walks every
   // point of the tile; 578 vs 365 us)
@@ -1694,6 +1947,25 @@ void DskiOp::gather(const double* w, const double* v, double* out, int nrhs, boo
     });
     launched("dski gather");
     return;
+  }
+  if (d == 3 && variant == 0 && g3_units.p && nrhs >= 4) {  // (1-3 RHS: the lean gather measured faster)
+    const size_t smem = sizeof(double) * size_t(T) * T * g3_zspan * nrhs;
+    if (smem <= 200 * 1024) {
+      const void* fn = T == 6 ? (G ? (const void*)k_gather_units3<6, true> : (const void*)k_gather_units3<6, false>)
+                              : (G ? (const void*)k_gather_units3<4, true> : (const void*)k_gather_units3<4, false>);
+      raise_smem_limit(fn, smem);
+      GK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, int(cudaSharedmemCarveoutMaxShared)));
+      const unsigned grid = static_cast<unsigned>(std::min(g3_nunits, 148 * 8));
+      if (T == 6) {
+        if (G) k_gather_units3<6, true><<<grid, G3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, w, v, out, nrhs, noise ? 1 : 0, g3_zspan);
+        else k_gather_units3<6, false><<<grid, G3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, w, v, out, nrhs, noise ? 1 : 0, g3_zspan);
+      } else {
+        if (G) k_gather_units3<4, true><<<grid, G3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, w, v, out, nrhs, noise ? 1 : 0, g3_zspan);
+        else k_gather_units3<4, false><<<grid, G3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, w, v, out, nrhs, noise ? 1 : 0, g3_zspan);
+      }
+      launched("dski gather (d=3 cell-line units)");
+      return;
+    }
   }
   const dim3 blk = lean_block(nrhs, n);
   const dim3 grid(static_cast<unsigned>((n + blk.y - 1) / blk.y), static_cast<unsigned>((nrhs + blk.x - 1) / blk.x));
@@ -1947,6 +2219,71 @@ std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, cons
   }
   op->cell_start.upload(cstart.data(), cstart.size(), st);
   op->cell_start_h = cstart;
+  if (d == 3) {  // gather units: runs of ≤ kZU occupied base cells along z per cell line
+    constexpr int kZU = 4;
+    const int nb1 = op->nb[1], nb2 = op->nb[2];
+    std::vector<int4> gu;
+    std::vector<int2> gr;
+    int zspan = 0;
+    for (int b0 = 0; b0 < op->nb[0]; ++b0)
+      for (int b1 = 0; b1 < nb1; ++b1) {
+        const size_t c0 = (static_cast<size_t>(b0) * nb1 + b1) * nb2;
+        int b2 = 0;
+        while (b2 < nb2) {
+          if (cstart[c0 + b2 + 1] == cstart[c0 + b2]) {
+            ++b2;
+            continue;
+          }
+          const int za = b2;
+          int zb = b2;
+          while (zb < nb2 && zb - za < kZU && (zb == za || cstart[c0 + zb + 1] > cstart[c0 + zb])) ++zb;
+          gu.push_back(make_int4(b0, b1, za, zb));
+          gr.push_back(make_int2(cstart[c0 + za], cstart[c0 + zb]));
+          zspan = std::max(zspan, zb - za + T - 1);
+          b2 = zb;
+        }
+      }
+    op->g3_nunits = int(gu.size());
+    op->g3_zspan = zspan;
+    op->g3_units.upload(gu.data(), gu.size(), op->stream);
+    op->g3_range.upload(gr.data(), gr.size(), op->stream);
+    // unit-push scatter tables
+    const int m1 = g.dims[1], m2 = g.dims[2], ncol = g.dims[0] * m1;
+    std::vector<long long> uoff(gu.size());
+    long long tot = 0;
+    std::vector<std::vector<int2>> per(static_cast<size_t>(ncol));
+    for (size_t ui = 0; ui < gu.size(); ++ui) {
+      const int nzb = gu[ui].w - gu[ui].z + T - 1;
+      uoff[ui] = tot;
+      tot += static_cast<long long>(T) * T * nzb;
+      for (int a = 0; a < T; ++a)
+        for (int b = 0; b < T; ++b)
+          per[static_cast<size_t>((gu[ui].x + a) * m1 + gu[ui].y + b)].push_back(make_int2(int(ui), a * T + b));
+    }
+    const int nzs = (m2 + 7) / 8;
+    std::vector<int> cst(static_cast<size_t>(ncol) + 1, 0), cseg(static_cast<size_t>(ncol) * nzs);
+    std::vector<int2> cent;
+    for (int c = 0; c < ncol; ++c) {
+      auto& L = per[static_cast<size_t>(c)];
+      std::stable_sort(L.begin(), L.end(), [&](const int2& x, const int2& y) {
+        return gu[static_cast<size_t>(x.x)].z < gu[static_cast<size_t>(y.x)].z;  // (za, unit): units already ascending
+      });
+      cst[static_cast<size_t>(c)] = int(cent.size());
+      for (int zs = 0; zs < nzs; ++zs) {  // first entry whose block can reach segment zs
+        size_t e = 0;
+        while (e < L.size() && gu[static_cast<size_t>(L[e].x)].z + zspan <= zs * 8) ++e;
+        cseg[static_cast<size_t>(c) * nzs + zs] = int(cent.size() + e);
+      }
+      cent.insert(cent.end(), L.begin(), L.end());
+    }
+    cst[static_cast<size_t>(ncol)] = int(cent.size());
+    op->s3_nodes = tot;
+    op->s3_nzs = nzs;
+    op->s3_uoff.upload(uoff.data(), uoff.size(), op->stream);
+    op->s3_cstart.upload(cst.data(), cst.size(), op->stream);
+    op->s3_cseg.upload(cseg.data(), cseg.size(), op->stream);
+    op->s3_cent.upload(cent.data(), std::max<size_t>(cent.size(), 1), op->stream);
+  }
   if (d == 3) {  // per node column (k0, k1): covering points ordered by (b2, t0, t1, point)
     const int m0 = g.dims[0], m1 = g.dims[1], m2 = g.dims[2];
     const int nb0 = op->nb[0], nb1 = op->nb[1], nb2 = op->nb[2];

@@ -151,22 +151,6 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 // CTA's prior global writes (ordered by __syncthreads) are visible to every
 // CTA after the barrier. Co-residency is guaranteed by the cooperative
 // launch; a bounded spin turns a logic error into a trap instead of a hang.
-__device__ __forceinline__ void grid_sync(unsigned long long* bar) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long t;
-    asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;\n" : "=l"(t) : "l"(bar) : "memory");
-    const unsigned long long nb = gridDim.x;
-    const unsigned long long target = (t / nb + 1) * nb;
-    unsigned spins = 0;
-    while (ld_relaxed(bar) < target) {
-      if (++spins > (1u << 24)) __trap();
-      __nanosleep(kBarrierSleepNs);
-    }
-    asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
-  }
-  __syncthreads();
-}
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -1124,8 +1108,8 @@ void fused2d_plan(const Fused2dGeom& g, const std::vector<int>& cs, int nrhs, in
   }
   p.grid = per_sm * sms;
   if (const int o = g_tuning.f2_grid.load(); o > 0) p.grid = std::min(p.grid, o);
-  p.bar.alloc(1);
-  GK_CUDA(cudaMemset(p.bar.p, 0, sizeof(unsigned long long)));
+  p.bar.alloc(kBarSlots);
+  GK_CUDA(cudaMemset(p.bar.p, 0, sizeof(unsigned long long) * kBarSlots));
   p.ok = true;
   if (std::getenv("GK_FUSED_PLAN_PRINT"))
     std::fprintf(stderr,

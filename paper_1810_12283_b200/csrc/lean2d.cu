@@ -37,6 +37,7 @@
 #include <cstdlib>
 
 #include "lean2d.hpp"
+#include "gk_sync.cuh"
 
 namespace gk {
 
@@ -66,30 +67,7 @@ struct LArgs {
   int kp0, mt0, nt0, mc0, ms0, dlo0, nd0;  // mode 0: K = m0, M = m0, N = m1·R
 };
 
-__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
 
-// Grid-wide barrier on a monotonic arrival counter (cooperative launch:
-// every CTA is resident). Release on arrival, acquire after the wait.
-__device__ __forceinline__ void grid_sync(unsigned long long* bar) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long t;
-    asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;\n" : "=l"(t) : "l"(bar) : "memory");
-    const unsigned long long nb = gridDim.x;
-    const unsigned long long target = (t / nb + 1) * nb;
-    unsigned spins = 0;
-    while (ld_relaxed(bar) < target) {
-      if (++spins > (1u << 26)) __trap();
-      __nanosleep(32);
-    }
-    asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
-  }
-  __syncthreads();
-}
 
 __device__ __forceinline__ void stamp(const LArgs& a, int k) {
   if (a.prof != nullptr && threadIdx.x == 0) {
@@ -549,8 +527,8 @@ void lean2d_plan(const Fused2dGeom& g, int nrhs, int device, Lean2dPlan& p) {
   GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, L2D_THREADS, p.smem));
   if (occ < 1) return;
   p.grid = std::min(occ, 2) * sms;
-  p.bar.alloc(1);
-  GK_CUDA(cudaMemset(p.bar.p, 0, sizeof(unsigned long long)));
+  p.bar.alloc(kBarSlots);
+  GK_CUDA(cudaMemset(p.bar.p, 0, sizeof(unsigned long long) * kBarSlots));
   p.ok = true;
 }
 

@@ -638,8 +638,8 @@ static void pcg_vec_prepare_impl(PcgVecPlan& p, i64 N, int nrhs, int k, int devi
   p.part.alloc(size_t(3) * p.grid * nrhs);
   p.tpart.alloc(size_t(p.grid) * (k + 2) * nrhs);  // + ‖r‖², ‖c‖² rows (v2)
   p.T.alloc(size_t(k + 2) * nrhs);
-  p.bar.alloc(1);
-  GK_CUDA(cudaMemset(p.bar.p, 0, sizeof(unsigned long long)));
+  p.bar.alloc(kBarSlots);
+  GK_CUDA(cudaMemset(p.bar.p, 0, sizeof(unsigned long long) * kBarSlots));
   p.red_out.alloc(size_t(3) * nrhs);
   p.rctr.alloc(2);
   GK_CUDA(cudaMemset(p.rctr.p, 0, 2 * sizeof(unsigned long long)));

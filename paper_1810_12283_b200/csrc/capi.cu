@@ -200,6 +200,7 @@ int gk_set_tuning(const char* key, int value) {
                            : k == "fused" ? &g_tuning.fused
                            : k == "lean" ? &g_tuning.lean
                            : k == "pivchol" ? &g_tuning.pivchol
+                           : k == "devbuild" ? &g_tuning.devbuild
                            : k == "fused_prof" ? &g_tuning.fused_prof
                            : k == "pcg_fused" ? &g_tuning.pcg_fused
                            : k == "e2e_chunk" ? &g_tuning.e2e_chunk

@@ -34,6 +34,8 @@
 
 #include "fused2d.hpp"
 #include "lean2d.hpp"
+
+#include <cub/cub.cuh>
 #include "gk_common.hpp"
 #include "gk_kernels.cuh"
 
@@ -1299,6 +1301,129 @@ __global__ void k_test_stencils(DskiView op, const double* __restrict__ X, i64 n
   }
 }
 
+// ================================================================ on-device point tables
+// The D-SKI constructor's per-point work (DskiOperator ctor, dski.cpp:174-204;
+// build_interpolation, interpolation.cpp:212-266) on the GPU: stencil base
+// cells and (w, ∂w) weights per axis, a stable sort by base cell (CUB radix
+// sort of (cell, point) pairs), the cell start table and the sorted-order
+// copies. The weights are evaluated with explicitly rounded operations in the
+// host formula's exact order (no FMA contraction), so the device tables are
+// bit-identical to the host build's (tuning "devbuild" = 1 keeps the host path).
+namespace {
+__device__ __forceinline__ double M_(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double A_(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double S_(double a, double b) { return __dsub_rn(a, b); }
+__device__ double dq_piece(double s) {
+  if (s < 1.0) {
+    const double B = S_(M_(A_(M_(-25.0, s), 63.0), s), 35.0);
+    const double C = M_(M_(M_(B, s), s), s);
+    const double D = M_(M_(15.0, s), s);
+    return __ddiv_rn(A_(S_(C, D), 12.0), 12.0);
+  }
+  if (s < 2.0) {
+    const double Q = S_(A_(M_(M_(S_(M_(25.0, s), 114.0), s), s), M_(153.0, s)), 48.0);
+    return __ddiv_rn(M_(M_(S_(s, 2.0), S_(s, 1.0)), Q), 24.0);
+  }
+  if (s < 3.0) {
+    const double t = S_(s, 3.0);
+    return __ddiv_rn(M_(M_(M_(M_(-t, t), t), S_(s, 2.0)), S_(M_(5.0, s), 8.0)), 24.0);
+  }
+  return 0.0;
+}
+__device__ double dq_deriv(double s) {
+  if (s < 1.0) return __ddiv_rn(M_(S_(M_(A_(M_(A_(M_(-125.0, s), 252.0), s), -105.0), s), 30.0), s), 12.0);
+  if (s < 2.0)
+    return __ddiv_rn(A_(M_(S_(M_(A_(M_(S_(M_(125.0, s), 756.0), s), 1635.0), s), 1470.0), s), 450.0), 24.0);
+  if (s < 3.0)
+    return __ddiv_rn(S_(M_(A_(M_(S_(M_(A_(M_(-25.0, s), 252.0), s), 939.0), s), 1530.0), s), 918.0), 24.0);
+  return 0.0;
+}
+__device__ double dc_val(double s) {
+  const double a = fabs(s);
+  if (a < 1.0) return A_(M_(M_(S_(M_(1.5, a), 2.5), a), a), 1.0);
+  if (a < 2.0) return A_(M_(S_(M_(A_(M_(-0.5, a), 2.5), a), 4.0), a), 2.0);
+  return 0.0;
+}
+__device__ double dc_der(double s) {
+  const double sg = s < 0.0 ? -1.0 : 1.0;
+  const double a = fabs(s);
+  double v = 0.0;
+  if (a < 1.0) v = M_(S_(M_(4.5, a), 5.0), a);
+  else if (a < 2.0) v = S_(M_(A_(M_(-1.5, a), 5.0), a), 4.0);
+  return M_(sg, v);
+}
+
+struct PtGeom {
+  int d, T;
+  double origin[3], h[3];
+  int m[3], nb[3];
+};
+
+__global__ void k_pts_weights(PtGeom g, const double* __restrict__ X, i64 n, int* __restrict__ base_o,
+                              double* __restrict__ wts_o, int* __restrict__ key, int* __restrict__ bad) {
+  const int STRIDE = g.d * 2 * g.T;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    long long c = 0;
+    bool ok = true;
+    for (int j = 0; j < g.d; ++j) {
+      const double x = X[(i64)j * n + i];
+      const double s = __ddiv_rn(S_(x, g.origin[j]), g.h[j]);
+      const double cell = floor(s);
+      const double t = S_(s, cell);
+      const long long b = (long long)cell - (g.T == 6 ? 2 : 1);
+      if (!(t >= 0.0 && t < 1.0) || b < 0 || b + g.T > g.m[j]) {
+        ok = false;
+        break;
+      }
+      double* w = wts_o + i * STRIDE + j * 2 * g.T;
+      for (int k = 0; k < g.T; ++k) {
+        const double arg = S_(t, double(k - (g.T == 6 ? 2 : 1)));
+        if (g.T == 6) {
+          w[k] = dq_piece(fabs(arg));
+          w[g.T + k] = __ddiv_rn(arg < 0.0 ? -dq_deriv(-arg) : dq_deriv(arg), g.h[j]);
+        } else {
+          w[k] = dc_val(arg);
+          w[g.T + k] = __ddiv_rn(dc_der(arg), g.h[j]);
+        }
+      }
+      base_o[i * 4 + j] = int(b);
+      c = c * g.nb[j] + b;
+    }
+    if (!ok) {
+      atomicMin(bad, int(i));
+      key[i] = 0;
+      continue;
+    }
+    key[i] = int(c);
+  }
+}
+
+// cstart[c] = first sorted position with key ≥ c (keys ascending).
+__global__ void k_cell_start(const int* __restrict__ key, i64 n, i64 ncells, int* __restrict__ cstart) {
+  for (i64 s = blockIdx.x * (i64)blockDim.x + threadIdx.x; s < n; s += (i64)gridDim.x * blockDim.x) {
+    const i64 k = key[s], prev = s ? key[s - 1] : -1;
+    for (i64 c = prev + 1; c <= k; ++c) cstart[c] = int(s);
+    if (s == n - 1)
+      for (i64 c = k + 1; c <= ncells; ++c) cstart[c] = int(n);
+  }
+}
+
+__global__ void k_gather_pts(const int* __restrict__ perm, const int* __restrict__ base_o,
+                             const double* __restrict__ wts_o, i64 n, int d, int T, int G, int4* __restrict__ base_s,
+                             double* __restrict__ wts_s, double2* __restrict__ wd, i64* __restrict__ ext) {
+  const int STRIDE = d * 2 * T;
+  for (i64 s = blockIdx.x * (i64)blockDim.x + threadIdx.x; s < n; s += (i64)gridDim.x * blockDim.x) {
+    const i64 i = perm[s];
+    base_s[s] = make_int4(base_o[i * 4], d > 1 ? base_o[i * 4 + 1] : 0, d > 2 ? base_o[i * 4 + 2] : 0, 0);
+    for (int e = 0; e < STRIDE; ++e) wts_s[s * STRIDE + e] = wts_o[i * STRIDE + e];
+    for (int j = 0; j < d; ++j)
+      for (int t = 0; t < T; ++t)
+        wd[(s * d + j) * T + t] = make_double2(wts_o[i * STRIDE + j * 2 * T + t], wts_o[i * STRIDE + j * 2 * T + T + t]);
+    for (int gg = 0; gg <= G; ++gg) ext[gg * n + s] = gg * n + i;
+  }
+}
+}  // namespace
+
 // ================================================================ operator
 struct DskiOp final : Op {
   int d = 0, T = 6, G = 0;
@@ -2105,53 +2230,6 @@ std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, cons
     op->nb[j] = g.dims[j] - T + 1;
     op->M *= g.dims[j];
   }
-  // per-point stencils in original order (interpolation.cpp:66-97)
-  const int STRIDE = d * 2 * T;
-  std::vector<int> base(static_cast<size_t>(n) * d);
-  std::vector<double> wts(static_cast<size_t>(n) * STRIDE);
-  for (i64 i = 0; i < n; ++i)
-    for (int j = 0; j < d; ++j)
-      axis_weights(X[j * n + i], g.origin[j], g.spacing[j], g.dims[j], T, i, j,
-                   &base[static_cast<size_t>(i) * d + j], &wts[static_cast<size_t>(i) * STRIDE + j * 2 * T],
-                   &wts[static_cast<size_t>(i) * STRIDE + j * 2 * T + T]);
-  bmark("stencil weights");
-  // sort by base cell (counting sort: stable, deterministic)
-  i64 ncells = 1;
-  for (int j = 0; j < d; ++j) ncells *= op->nb[j];
-  std::vector<i64> cell(static_cast<size_t>(n));
-  std::vector<int> cstart(static_cast<size_t>(ncells) + 1, 0);
-  for (i64 i = 0; i < n; ++i) {
-    i64 c = 0;
-    for (int j = 0; j < d; ++j) c = c * op->nb[j] + base[static_cast<size_t>(i) * d + j];
-    cell[static_cast<size_t>(i)] = c;
-    cstart[static_cast<size_t>(c) + 1]++;
-  }
-  for (i64 c = 0; c < ncells; ++c) cstart[static_cast<size_t>(c) + 1] += cstart[static_cast<size_t>(c)];
-  if (d == 2)
-    for (int br = 0; br < op->nb[0]; ++br)
-      op->max_row_pts = std::max(op->max_row_pts, cstart[static_cast<size_t>(br + 1) * op->nb[1]] -
-                                                      cstart[static_cast<size_t>(br) * op->nb[1]]);
-  op->perm_h.assign(static_cast<size_t>(n), 0);
-  op->inv_h.assign(static_cast<size_t>(n), 0);
-  {
-    std::vector<int> fill(cstart.begin(), cstart.end() - 1);
-    for (i64 i = 0; i < n; ++i) {
-      const int pos = fill[static_cast<size_t>(cell[static_cast<size_t>(i)])]++;
-      op->perm_h[static_cast<size_t>(pos)] = i;
-      op->inv_h[static_cast<size_t>(i)] = pos;
-    }
-  }
-  std::vector<int4> base_s(static_cast<size_t>(n));
-  std::vector<double> wts_s(static_cast<size_t>(n) * STRIDE);
-  for (i64 s = 0; s < n; ++s) {
-    const i64 i = op->perm_h[static_cast<size_t>(s)];
-    int4 b4 = make_int4(0, 0, 0, 0);
-    b4.x = base[static_cast<size_t>(i) * d + 0];
-    if (d > 1) b4.y = base[static_cast<size_t>(i) * d + 1];
-    if (d > 2) b4.z = base[static_cast<size_t>(i) * d + 2];
-    base_s[static_cast<size_t>(s)] = b4;
-    std::memcpy(&wts_s[static_cast<size_t>(s) * STRIDE], &wts[static_cast<size_t>(i) * STRIDE], sizeof(double) * STRIDE);
-  }
   // Toeplitz sequences t_j[k] = exp(-(k h_j)²/(2ℓ²)), s² folded into axis 0
   // (SE profile, kernels.cpp:22-27 / dski.cpp:30-34).
   std::vector<double> tv;
@@ -2198,13 +2276,130 @@ std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, cons
       }
     op->band_dl[static_cast<size_t>(j)] = band;
   }
-  std::vector<i64> ext(static_cast<size_t>(op->N));
+  const int STRIDE = d * 2 * T;
+  i64 ncells = 1;
+  for (int j = 0; j < d; ++j) ncells *= op->nb[j];
+  op->init_stream();
+  cudaStream_t st = op->stream;
+  std::vector<int> cstart;
+  std::vector<i64> ext;
+  const bool host_build = g_tuning.devbuild.load() != 0 || ncells >= (i64(1) << 31) || n >= (i64(1) << 31);
+  if (!host_build) {
+    // on-device point tables (bit-identical to the host build below)
+    PtGeom pg{};
+    pg.d = d;
+    pg.T = T;
+    for (int j = 0; j < d; ++j) {
+      pg.origin[j] = g.origin[j];
+      pg.h[j] = g.spacing[j];
+      pg.m[j] = g.dims[j];
+      pg.nb[j] = op->nb[j];
+    }
+    DevBuf<double> Xd(static_cast<size_t>(n) * d), wts_o(static_cast<size_t>(n) * STRIDE);
+    DevBuf<int> base_o(static_cast<size_t>(n) * 4), key(static_cast<size_t>(n)), key_s(static_cast<size_t>(n)),
+        idx(static_cast<size_t>(n)), perm(static_cast<size_t>(n)), bad(1);
+    Xd.upload(X, static_cast<size_t>(n) * d, st);
+    const int big = INT_MAX;
+    GK_CUDA(cudaMemcpyAsync(bad.p, &big, sizeof(int), cudaMemcpyHostToDevice, st));
+    k_pts_weights<<<grid_blocks(n), 256, 0, st>>>(pg, Xd.p, n, base_o.p, wts_o.p, key.p, bad.p);
+    launched("dski build: stencils");
+    int badh = INT_MAX;
+    GK_CUDA(cudaMemcpyAsync(&badh, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    GK_CUDA(cudaStreamSynchronize(st));
+    if (badh != INT_MAX) {  // the host formula names the point and axis (OutOfGridError text)
+      int bb;
+      std::vector<double> w(static_cast<size_t>(T)), dw(static_cast<size_t>(T));
+      for (int j = 0; j < d; ++j)
+        axis_weights(X[j * n + badh], g.origin[j], g.spacing[j], g.dims[j], T, badh, j, &bb, w.data(), dw.data());
+      fail(GK_ERR_OUT_OF_GRID, "point " + std::to_string(badh) + " lies outside the interior of the grid", badh);
+    }
+    std::vector<int> iota(static_cast<size_t>(n));
+    std::iota(iota.begin(), iota.end(), 0);
+    idx.upload(iota.data(), iota.size(), st);
+    int bits = 1;
+    while ((i64(1) << bits) < ncells) ++bits;
+    size_t tmp_bytes = 0;
+    GK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key.p, key_s.p, idx.p, perm.p, int(n), 0, bits, st));
+    DevBuf<unsigned char> tmp(tmp_bytes);
+    GK_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, key.p, key_s.p, idx.p, perm.p, int(n), 0, bits, st));
+    launched("dski build: radix sort");
+    op->cell_start.alloc(static_cast<size_t>(ncells) + 1);
+    k_cell_start<<<grid_blocks(n), 256, 0, st>>>(key_s.p, n, ncells, op->cell_start.p);
+    launched("dski build: cell starts");
+    op->base.alloc(static_cast<size_t>(n));
+    op->wts.alloc(static_cast<size_t>(n) * STRIDE);
+    op->wd.alloc(static_cast<size_t>(n) * d * T);
+    op->ext.alloc(static_cast<size_t>(op->N));
+    k_gather_pts<<<grid_blocks(n), 256, 0, st>>>(perm.p, base_o.p, wts_o.p, n, d, T, op->G, op->base.p, op->wts.p,
+                                                 op->wd.p, op->ext.p);
+    launched("dski build: sorted tables");
+    // host copies the operator keeps: cell starts (plans, d = 3 lists), the permutation
+    cstart.resize(static_cast<size_t>(ncells) + 1);
+    std::vector<int> ph(static_cast<size_t>(n));
+    GK_CUDA(cudaMemcpyAsync(cstart.data(), op->cell_start.p, sizeof(int) * cstart.size(), cudaMemcpyDeviceToHost, st));
+    GK_CUDA(cudaMemcpyAsync(ph.data(), perm.p, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
+    GK_CUDA(cudaStreamSynchronize(st));
+    op->perm_h.resize(static_cast<size_t>(n));
+    op->inv_h.resize(static_cast<size_t>(n));
+    for (i64 q = 0; q < n; ++q) {
+      op->perm_h[static_cast<size_t>(q)] = ph[static_cast<size_t>(q)];
+      op->inv_h[static_cast<size_t>(ph[static_cast<size_t>(q)])] = q;
+    }
+    if (d == 2)
+      for (int br = 0; br < op->nb[0]; ++br)
+        op->max_row_pts = std::max(op->max_row_pts, cstart[static_cast<size_t>(br + 1) * op->nb[1]] -
+                                                        cstart[static_cast<size_t>(br) * op->nb[1]]);
+    op->cell_start_h = cstart;
+    bmark("device point tables");
+  } else {
+  // per-point stencils in original order (interpolation.cpp:66-97)
+  std::vector<int> base(static_cast<size_t>(n) * d);
+  std::vector<double> wts(static_cast<size_t>(n) * STRIDE);
+  for (i64 i = 0; i < n; ++i)
+    for (int j = 0; j < d; ++j)
+      axis_weights(X[j * n + i], g.origin[j], g.spacing[j], g.dims[j], T, i, j,
+                   &base[static_cast<size_t>(i) * d + j], &wts[static_cast<size_t>(i) * STRIDE + j * 2 * T],
+                   &wts[static_cast<size_t>(i) * STRIDE + j * 2 * T + T]);
+  bmark("stencil weights");
+  // sort by base cell (counting sort: stable, deterministic)
+  std::vector<i64> cell(static_cast<size_t>(n));
+  cstart.assign(static_cast<size_t>(ncells) + 1, 0);
+  for (i64 i = 0; i < n; ++i) {
+    i64 c = 0;
+    for (int j = 0; j < d; ++j) c = c * op->nb[j] + base[static_cast<size_t>(i) * d + j];
+    cell[static_cast<size_t>(i)] = c;
+    cstart[static_cast<size_t>(c) + 1]++;
+  }
+  for (i64 c = 0; c < ncells; ++c) cstart[static_cast<size_t>(c) + 1] += cstart[static_cast<size_t>(c)];
+  if (d == 2)
+    for (int br = 0; br < op->nb[0]; ++br)
+      op->max_row_pts = std::max(op->max_row_pts, cstart[static_cast<size_t>(br + 1) * op->nb[1]] -
+                                                      cstart[static_cast<size_t>(br) * op->nb[1]]);
+  op->perm_h.assign(static_cast<size_t>(n), 0);
+  op->inv_h.assign(static_cast<size_t>(n), 0);
+  {
+    std::vector<int> fill(cstart.begin(), cstart.end() - 1);
+    for (i64 i = 0; i < n; ++i) {
+      const int pos = fill[static_cast<size_t>(cell[static_cast<size_t>(i)])]++;
+      op->perm_h[static_cast<size_t>(pos)] = i;
+      op->inv_h[static_cast<size_t>(i)] = pos;
+    }
+  }
+  std::vector<int4> base_s(static_cast<size_t>(n));
+  std::vector<double> wts_s(static_cast<size_t>(n) * STRIDE);
+  for (i64 s = 0; s < n; ++s) {
+    const i64 i = op->perm_h[static_cast<size_t>(s)];
+    int4 b4 = make_int4(0, 0, 0, 0);
+    b4.x = base[static_cast<size_t>(i) * d + 0];
+    if (d > 1) b4.y = base[static_cast<size_t>(i) * d + 1];
+    if (d > 2) b4.z = base[static_cast<size_t>(i) * d + 2];
+    base_s[static_cast<size_t>(s)] = b4;
+    std::memcpy(&wts_s[static_cast<size_t>(s) * STRIDE], &wts[static_cast<size_t>(i) * STRIDE], sizeof(double) * STRIDE);
+  }
+  ext.resize(static_cast<size_t>(op->N));
   for (int gg = 0; gg <= op->G; ++gg)
     for (i64 s = 0; s < n; ++s) ext[static_cast<size_t>(gg * n + s)] = gg * n + op->perm_h[static_cast<size_t>(s)];
   bmark("sort + host tables");
-  op->init_stream();
-  bmark("init_stream");
-  cudaStream_t st = op->stream;
   op->base.upload(base_s.data(), base_s.size(), st);
   op->wts.upload(wts_s.data(), wts_s.size(), st);
   {
@@ -2219,6 +2414,8 @@ std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, cons
   }
   op->cell_start.upload(cstart.data(), cstart.size(), st);
   op->cell_start_h = cstart;
+  op->ext.upload(ext.data(), ext.size(), st);
+  }
   if (d == 3) {  // gather units: runs of ≤ kZU occupied base cells along z per cell line
     constexpr int kZU = 4;
     const int nb1 = op->nb[1], nb2 = op->nb[2];
@@ -2408,7 +2605,6 @@ std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, cons
   op->tvec.upload(tv.data(), tv.size(), st);
   op->tvec_dl.upload(tvd.data(), tvd.size(), st);
   op->toff.upload(op->toff_h.data(), op->toff_h.size(), st);
-  op->ext.upload(ext.data(), ext.size(), st);
   double o3[3] = {0, 0, 0}, h3[3] = {1, 1, 1};
   for (int j = 0; j < d; ++j) {
     o3[j] = g.origin[j];

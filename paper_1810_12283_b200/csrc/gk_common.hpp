@@ -37,6 +37,7 @@ void raise_smem_limit(const void* fn, size_t bytes);
 // Process-wide kernel-variant knobs (gk_set_tuning); 0 = default.
 struct Tuning {
   std::atomic<int> scatter{0}, gather{0}, toeplitz{0}, precond{0}, fused{0}, fused_prof{0}, pcg_fused{0};
+  std::atomic<int> devbuild{0};  // 1 = D-SKI point tables built on the host
   std::atomic<int> pivchol{0};  // 1 = host-synchronised pivot loop (3 syncs per pivot)
   std::atomic<int> lean{0};  // lean one-launch 2-D MVM (lean2d.cu): 0 measured policy, 1 never, 2 always
   // fused 2-D MVM decomposition overrides (0 = heuristic)

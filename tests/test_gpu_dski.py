@@ -259,3 +259,35 @@ def test_one_launch_2d_kernels_match_oracle(lean, ell, n):
             assert rel(g.mvm(V), r.mvm(V)) <= TOL, nrhs
     finally:
         gk.set_tuning("lean", 0)
+
+
+@pytest.mark.parametrize("cfg", [1, 3, 4])
+def test_device_point_tables_bit_identical_to_host_build(cfg):
+    """The D-SKI constructor's point tables built on the GPU (stencil weights
+    with the host formula's rounding, CUB stable radix sort by base cell, cell
+    starts) give bit-identical operators to the host build (tuning "devbuild")."""
+    X, *_ = gk.make_dataset(cfg, 0)
+    ell, nodes = {1: (0.15, 60), 3: (0.3, 48), 4: (0.02, 400)}[cfg]
+    grid = gk.Grid.cover(X, 1e-4, 3, nodes)
+    V = np.random.default_rng(cfg).standard_normal((X.shape[0] * (X.shape[1] + 1), 3))
+    try:
+        gk.set_tuning("devbuild", 1)
+        host = gk.DskiOperator(gk.KernelSpec(ell, 1.0), grid, X, (1e-2, 1e-2))
+        a = host.mvm(V)
+        gk.set_tuning("devbuild", 0)
+        dev = gk.DskiOperator(gk.KernelSpec(ell, 1.0), grid, X, (1e-2, 1e-2))
+        b = dev.mvm(V)
+    finally:
+        gk.set_tuning("devbuild", 0)
+    assert np.array_equal(a, b)
+    assert np.array_equal(host.diagonal(), dev.diagonal())
+
+
+def test_device_build_reports_out_of_grid_point():
+    X = np.random.default_rng(3).uniform(0, 1, (50, 2))
+    grid = gk.Grid.cover(X, 0.1, 3, 24)
+    X2 = X.copy()
+    X2[17, 1] = 5.0  # outside the grid interior
+    with pytest.raises(gk.OutOfGridError) as e:
+        gk.DskiOperator(gk.KernelSpec(0.3, 1.0), grid, X2, (0.1, 0.1))
+    assert e.value.point == 17 and "point 17" in str(e.value)

@@ -237,7 +237,11 @@ gk_status gk_pivchol_get(const gk_pivchol* f, double* L /*N×rank or NULL*/,
 void gk_pivchol_destroy(gk_pivchol* f);
 
 /* Preconditioner(F, noise_diag) (linalg.cpp:176-213): M^{-1}b =
- * D^{-1/2}(c - Q1 Q1^T c), c = D^{-1/2} b, Q1 from a QR of [D^{-1/2}F; I]. */
+ * D^{-1/2}(c - Q1 Q1^T c), c = D^{-1/2} b, Q1 from a QR of [D^{-1/2}F; I]
+ * (CholeskyQR2 on the device; agrees with the reference's Householder Q1 to
+ * ≤1e-10 at C4's rank 200, tests/test_gpu_fullsize_parity.py). Limit: rank
+ * k ≤ 512 (GK_ERR_UNSUPPORTED above; the reference has none — larger ranks
+ * would need a blocked Gram/solve, no BASELINE config asks for one). */
 gk_status gk_precond_create(const double* F, int64_t N, int64_t k, const double* noise_diag,
                             int device, gk_precond** out);
 /* From a device-resident pivoted Cholesky factor, with D = op noise diagonal

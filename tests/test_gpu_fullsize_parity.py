@@ -218,3 +218,32 @@ def test_dskip_build_pinned_step_by_step(d):
         assert np.max(np.abs(fg.beta[:5] - br[:5])) <= 1e-10 * np.max(np.abs(ar))
         # and the basis vectors themselves (up to roundoff) for those steps
         assert np.max(np.abs(fg.Q[:, :5] - Qr[:, :5])) <= 1e-9
+
+
+def test_c4_cholesky_qr2_preconditioner_matches_householder():
+    """The preconditioner's Q1 is built by CholeskyQR2 on the device where the
+    reference uses Householder QR (linalg.cpp:187-193). At C4's rank 200 and
+    σ = 1e-2 (the worst-conditioned [D^{-1/2}L; I] of the configs), M⁻¹b and
+    the quadratic form agree with a Householder QR of the same factor (LAPACK
+    via numpy) to ≤1e-10."""
+    X, y, dY = O.make_dataset(4, 0)
+    grid = gk.Grid.cover(X, 1e-4, 3, 400)
+    op = gk.DskiOperator(gk.KernelSpec(0.02, 1.0), grid, X, NOISE)
+    f = gk.pivoted_cholesky(op, 200, kernel_part=True)
+    M = gk.Preconditioner.from_pivchol(op, f)
+    L = f.L
+    nd = np.full(op.size(), NOISE[1] ** 2)
+    nd[: X.shape[0]] = NOISE[0] ** 2
+    dinv = 1.0 / np.sqrt(nd)
+    Q, _ = np.linalg.qr(np.vstack([dinv[:, None] * L, np.eye(L.shape[1])]))  # Householder (LAPACK geqrf)
+    Q1 = Q[: op.size()]
+    B = np.random.default_rng(4).standard_normal((op.size(), 2))
+    B[:, 0] = O.stacked_targets(y, dY, y.mean())
+    for j in range(2):
+        c = dinv * B[:, j]
+        t = Q1.T @ c
+        z_ref = dinv * (c - Q1 @ t)
+        z = M.apply(B[:, j])
+        assert np.linalg.norm(z - z_ref) <= 1e-10 * np.linalg.norm(z_ref)
+        q_ref = c @ c - t @ t
+        assert abs(M.quadratic(B[:, j]) - q_ref) <= 1e-10 * abs(q_ref)

@@ -199,6 +199,15 @@ gk_status gk_op_stage_dev(const gk_op* op, int stage, const double* dIn, double*
  * all-reduced. */
 gk_status gk_dski_gather_dev(const gk_op* op, const double* dW, const double* dV, double* dOut,
                              int64_t nrhs, void* stream);
+/* The one-launch 2-D MVM split at its first grid barrier (grid-slab sharding,
+ * SURVEY §8(e)): phase 0 scatters dV (internal layout) into dU2 = [u; h]
+ * (2·M·nrhs doubles: the grid vector and the scatter's segment halo rows);
+ * phase 1 applies K_UU to the (all-reduced) dU2 and gathers with noise from
+ * dV into dOut. GK_ERR_UNSUPPORTED when the operator has no such plan
+ * (callers then use gk_op_stage_dev stages 0/1 and gk_dski_gather_dev);
+ * phase 2 only queries that availability for nrhs (no device work). */
+gk_status gk_dski_fused_split_dev(const gk_op* op, int phase, const double* dV, double* dU2,
+                                  double* dOut, int64_t nrhs, void* stream);
 /* Convert external column-major blocks to/from the internal layout. */
 gk_status gk_op_to_internal_dev(const gk_op* op, const double* dV, int64_t ldv, double* dI,
                                 int64_t nrhs, void* stream);
@@ -297,6 +306,14 @@ gk_status gk_dski_predict_mean_grad(const gk_op* op, const double* alpha, double
  * Q (N×T col-major). */
 gk_status gk_dski_cross_covariance(const gk_op* op, const double* Xtest, int64_t T, double* Q,
                                    int64_t ldq);
+/* Device-pointer cross-covariance for T ≤ 64 test points (dXt T×d col-major
+ * on the device): columns B K_UU w(x_t) into dQ (N×T external order, ld
+ * ldq), w the value stencil (direction = -1, gp.cpp:412-417) or its ∂/∂x_p
+ * (direction = p, gp.cpp:431-461). Used for pivot columns of the
+ * grid-slab sharded pivoted Cholesky. Synchronises `stream` once (the
+ * out-of-grid check). */
+gk_status gk_dski_cross_covariance_dev(const gk_op* op, const double* dXt, int64_t T, int direction,
+                                       double* dQ, int64_t ldq, void* stream);
 /* GpModel::cross_covariance_jacobian (gp.cpp:431-461, D-SKI branch) for T test
  * points (Xtest T×d col-major): J column t·d + p (leading dimension ldj ≥ N)
  * = ∂q(x_t)/∂x_p = B K_UU w_p(x_t) with w_p the derivative point stencil. */

@@ -117,6 +117,8 @@ _SIGS = {
     "gk_dski_cross_covariance_jacobian": (C.c_int, [_vp, _dp, _i64, _dp, _i64]),
     "gk_dski_cross_covariance": (C.c_int, [_vp, _dp, _i64, _dp, _i64]),
     "gk_make_dataset": (C.c_int, [C.c_int, _u64, _i64p, _ip, _dp, _dp, _dp]),
+    "gk_dski_cross_covariance_dev": (C.c_int, [_vp, _vp, _i64, C.c_int, _vp, _i64, _vp]),
+    "gk_dski_fused_split_dev": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, _i64, _vp]),
     "gk_precond_from_q1_dev": (C.c_int, [_vp, _vp, _i64, _i64, C.c_int, C.POINTER(_vp)]),
     "gk_precond_project_dev": (C.c_int, [_vp, _vp, _vp, _i64, _vp]),
     "gk_precond_finish_dev": (C.c_int, [_vp, _vp, _vp, _vp, _i64, _vp]),
@@ -426,6 +428,22 @@ class DskiOperator(LinearOperator):
         out = np.empty_like(V, order="F")
         _check(_lib.gk_dski_dlogell_apply(self._h, _p(V), V.shape[0], _p(out), V.shape[0], V.shape[1]))
         return out[:, 0] if vec else out
+
+    def cross_covariance_dev(self, dXt, T, direction, dQ, ldq=None, stream=0):
+        """Device-pointer cross-covariance columns (value stencil for
+        direction -1, ∂/∂x_p for direction p), external row order."""
+        _check(_lib.gk_dski_cross_covariance_dev(self._h, dXt, int(T), int(direction), dQ, ldq or self.size(),
+                                                 stream))
+
+    def fused_split_dev(self, phase, dV, dU2, dOut, nrhs, stream=0):
+        """The one-launch MVM split at its first barrier: phase 0 scatters into
+        dU2 = [u; h] (2·M·nrhs), phase 1 finishes from an all-reduced dU2.
+        Returns False when unsupported for this operator."""
+        st = _lib.gk_dski_fused_split_dev(self._h, int(phase), dV, dU2, dOut, int(nrhs), stream)
+        if st == 9:
+            return False
+        _check(st)
+        return True
 
     def gather_dev(self, dW, dV, dOut, nrhs, stream=0):
         """out = B w + noise·v on device pointers (internal layout): the last

@@ -31,6 +31,8 @@ std::unique_ptr<Op> make_dskip(const gk_kernel& k, const double* X, i64 n, int d
                                const gk_dskip_config& cfg, int device);
 int64_t dski_grid_size(const Op& o);
 int dski_fused_phases(Op& o, int nrhs, i64* out, int max_ctas);
+bool dski_fused_split(Op& o, int phase, const double* v, double* u2, double* out, int nrhs, cudaStream_t s);
+void dski_cross_cov_dev(Op& o, const double* dXt, i64 nT, int dir, double* dQ, i64 ldq, cudaStream_t s);
 void dski_gather_noise(Op& o, const double* W, const double* V, double* out, int nrhs, cudaStream_t s);
 gk_grid dski_grid(const Op& o);
 void dski_transpose_apply(Op& o, const double* Vi, double* U, int nrhs, cudaStream_t s);
@@ -421,6 +423,34 @@ gk_status gk_dski_gather_dev(const gk_op* h, const double* dW, const double* dV,
     DeviceGuard dg(op.device);
     OpSession ss(op, S(stream));
     dski_gather_noise(op, dW, dV, dOut, int(nrhs), S(stream));
+  });
+}
+
+gk_status gk_dski_fused_split_dev(const gk_op* h, int phase, const double* dV, double* dU2, double* dOut,
+                                  int64_t nrhs, void* stream) {
+  return guard([&] {
+    Op& op = O(h);
+    if (phase < 0 || phase > 2) fail(GK_ERR_ARG, "phase must be 0 (scatter), 1 (K_UU + gather) or 2 (query)");
+    if (nrhs < 1 || nrhs > kMaxRhs) fail(GK_ERR_ARG, "nrhs out of range");
+    DeviceGuard dg(op.device);
+    OpSession ss(op, S(stream));
+    if (!dski_fused_split(op, phase, dV, dU2, dOut, int(nrhs), S(stream)))
+      fail(GK_ERR_UNSUPPORTED, "the split one-launch MVM needs a 2-D D-SKI operator with gradients");
+  });
+}
+
+gk_status gk_dski_cross_covariance_dev(const gk_op* h, const double* dXt, int64_t T, int direction, double* dQ,
+                                       int64_t ldq, void* stream) {
+  return guard([&] {
+    Op& op = O(h);
+    if (op.kind != KIND_DSKI) fail(GK_ERR_ARG, "operator is not a D-SKI operator");
+    if (T < 1 || T > kMaxRhs) fail(GK_ERR_ARG, "test point count must be in [1, 64]");
+    if (ldq < op.N) fail(GK_ERR_ARG, "size mismatch");
+    const gk_grid g = dski_grid(op);
+    if (direction < -1 || direction >= g.d) fail(GK_ERR_ARG, "direction out of range");
+    DeviceGuard dg(op.device);
+    OpSession ss(op, S(stream));
+    dski_cross_cov_dev(op, dXt, T, direction, dQ, ldq, S(stream));
   });
 }
 

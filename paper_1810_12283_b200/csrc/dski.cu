@@ -1479,6 +1479,7 @@ struct DskiOp final : Op {
   DevBuf<double> origin_d, h_d;
   DevBuf<double> grid_u, grid_w, grid_t, grid_h, grid_p;  // per-MVM grid scratch (guarded by mu / caller)
   mutable DevBuf<double> s3_scratch;  // unit-push scatter blocks (s3_nodes × nrhs)
+  DevBuf<int> oog;                     // out-of-grid flag of the device cross-covariance
   std::vector<int> cell_start_h;          // host copy (fused-plan sizing)
   std::vector<std::unique_ptr<Fused2dPlan>> fplans;  // one-launch d = 2 MVM plans, per nrhs
   std::vector<std::unique_ptr<Lean2dPlan>> lplans;   // lean one-launch d = 2 MVM plans, per nrhs
@@ -1616,6 +1617,20 @@ struct DskiOp final : Op {
     scatter(in, grid_u.p, nrhs, s);
     kuu(grid_u.p, grid_w.p, nrhs, s);
     gather(grid_w.p, in, out, nrhs, true, s);
+  }
+  // The one-launch 2-D MVM split at its first grid barrier, for the grid-slab
+  // sharded MVM: phase 0 scatters v into [u; h] (u2: 2·M·nrhs), phase 1 runs
+  // K_UU and the gather + noise from an (all-reduced) [u; h]. False when the
+  // fused plan does not apply (or uses the partial-buffer scatter).
+  bool fused_split(int phase, const double* v, double* u2, double* out, int nrhs, cudaStream_t s) {
+    Fused2dPlan* fp = fused_plan(nrhs);
+    if (!fp || fp->s_mode != 0) return false;
+    if (phase == 2) return true;  // availability query
+    ensure_scratch(nrhs);
+    double* h = u2 + static_cast<size_t>(M) * nrhs;
+    if (phase == 0) fused2d_mvm(geom2d(), *fp, v, grid_w.p, u2, h, grid_t.p, grid_w.p, grid_p.p, true, s, 14);
+    else fused2d_mvm(geom2d(), *fp, v, out, u2, h, grid_t.p, grid_w.p, grid_p.p, true, s, 1);
+    return true;
   }
   void stage(int st, const double* in, double* out, int nrhs, cudaStream_t s) override {
     ensure_scratch(nrhs);
@@ -2699,10 +2714,43 @@ void dski_cross_cov(Op& o, const double* dXt, i64 nT, double* Qi, int* dbad, cud
   GK_CUDA(cudaStreamSynchronize(s));
 }
 
+// Device-pointer cross-covariance (gp.cpp:412-417 / 431-461 for one stencil
+// direction): columns B K_UU w(x_t) for nT test points (dXt nT×d col-major,
+// device) written in EXTERNAL row order into dQ (ld ldq); the operator's grid
+// scratch is reused (no allocation); one synchronisation for the
+// out-of-grid check. dir < 0: value stencil, else ∂/∂x_dir.
+void dski_cross_cov_dev(Op& o, const double* dXt, i64 nT, int dir, double* dQ, i64 ldq, cudaStream_t s) {
+  auto& op = static_cast<DskiOp&>(o);
+  op.ensure_scratch(int(nT));
+  op.scratch_a.reserve(static_cast<size_t>(op.N) * nT);
+  op.oog.reserve(1);
+  const int big = INT_MAX;
+  GK_CUDA(cudaMemcpyAsync(op.oog.p, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+  GK_CUDA(cudaMemsetAsync(op.grid_u.p, 0, sizeof(double) * op.M * nT, s));
+  const DskiView vw = op.view();
+  GK_DISPATCH_DT(op.d, op.T, {
+    k_test_stencils<D, T><<<grid_blocks(nT), 256, 0, s>>>(vw, dXt, nT, op.origin_d.p, op.h_d.p, op.grid_u.p, op.oog.p, dir);
+  });
+  launched("dski test stencils");
+  op.kuu(op.grid_u.p, op.grid_w.p, int(nT), s);
+  op.gather(op.grid_w.p, op.grid_w.p, op.scratch_a.p, int(nT), false, s);
+  op.from_internal(op.scratch_a.p, dQ, ldq, int(nT), s);
+  int badh = INT_MAX;
+  GK_CUDA(cudaMemcpyAsync(&badh, op.oog.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GK_CUDA(cudaStreamSynchronize(s));
+  if (badh != INT_MAX)
+    fail(GK_ERR_OUT_OF_GRID, "test point " + std::to_string(badh) + " lies outside the interior of the grid", badh);
+}
+
 }  // namespace gk
 
 namespace gk {
 // gk_debug_fused_phases backend
+bool dski_fused_split(Op& o, int phase, const double* v, double* u2, double* out, int nrhs, cudaStream_t s) {
+  if (o.kind != KIND_DSKI) fail(GK_ERR_ARG, "operator is not a D-SKI operator");
+  return static_cast<DskiOp&>(o).fused_split(phase, v, u2, out, nrhs, s);
+}
+
 int dski_fused_phases(Op& o, int nrhs, i64* out, int max_ctas) {
   if (o.kind != KIND_DSKI) fail(GK_ERR_ARG, "operator is not a D-SKI operator");
   auto& op = static_cast<DskiOp&>(o);

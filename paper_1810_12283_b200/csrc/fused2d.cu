@@ -1182,8 +1182,9 @@ static F2Args fused2d_args(const Fused2dGeom& g, Fused2dPlan& p, const double* v
 }
 
 void fused2d_mvm(const Fused2dGeom& g, Fused2dPlan& p, const double* v, double* out, double* u, double* h,
-                 double* y1, double* w, double* pbuf, bool noise, cudaStream_t s) {
+                 double* y1, double* w, double* pbuf, bool noise, cudaStream_t s, int skip) {
   F2Args a = fused2d_args(g, p, v, out, u, h, y1, w, pbuf, noise);
+  a.skip |= skip;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(p.grid));
   cfg.blockDim = dim3(F2_THREADS);

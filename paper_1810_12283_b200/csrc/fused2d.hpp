@@ -49,8 +49,12 @@ void fused2d_plan(const Fused2dGeom& g, const std::vector<int>& cell_start_h, in
                   Fused2dPlan& p);
 // out = B K_UU B^T v (+ noise): u, h, y1, w are M×nrhs grid scratch buffers
 // (h holds the scatter's segment-boundary halo rows).
+// skip: bitmask of phases to leave out (1 scatter, 2 mode 1, 4 mode 0, 8
+// gather), OR-ed with the debug knob: the split launches of the grid-slab MVM
+// run the scatter alone (14) and the rest alone (1) around an all-reduce of
+// [u; h].
 void fused2d_mvm(const Fused2dGeom& g, Fused2dPlan& p, const double* v, double* out, double* u,
-                 double* h, double* y1, double* w, double* pbuf, bool noise, cudaStream_t s);
+                 double* h, double* y1, double* w, double* pbuf, bool noise, cudaStream_t s, int skip = 0);
 
 // Persistent PCG (PCG with this operator's one-launch MVM and the rows-resident
 // vector step in one cooperative kernel, up to `iters` iterations). False when

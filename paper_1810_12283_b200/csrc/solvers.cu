@@ -2054,12 +2054,59 @@ void sub_dev(const double* a, const double* b, double* c, i64 n, cudaStream_t s)
   launched("sub");
 }
 
+// Single right-hand side: T[j] = Σ_r q1[r][j] · dinv[r] r[r] as a streaming
+// read of the row-major Q1 (thread j of a block owns output j over the
+// block's row range: each row of Q1 is one coalesced read), partials per
+// block summed in block order by k_pc_fin (deterministic).
+__global__ void __launch_bounds__(256) k_pc_proj_r1(const double* __restrict__ Rv, const double* __restrict__ dinv,
+                                                    const double* __restrict__ q1, i64 N, int k,
+                                                    double* __restrict__ partial) {
+  i64 r0, r1;
+  row_range(N, r0, r1);
+  for (int j0 = 0; j0 < k; j0 += blockDim.x) {
+    const int j = j0 + threadIdx.x;
+    double acc0 = 0.0, acc1 = 0.0;
+    if (j < k) {
+      i64 r = r0;
+      for (; r + 1 < r1; r += 2) {  // two independent chains
+        acc0 = fma(q1[r * k + j], dinv[r] * Rv[r], acc0);
+        acc1 = fma(q1[(r + 1) * k + j], dinv[r + 1] * Rv[r + 1], acc1);
+      }
+      if (r < r1) acc0 = fma(q1[r * k + j], dinv[r] * Rv[r], acc0);
+      partial[(i64)blockIdx.x * k + j] = acc0 + acc1;
+    }
+  }
+}
+// z[r] = dinv[r] (dinv[r] r[r] − Σ_j q1[r][j] T[j]): a warp per row (lanes over j).
+__global__ void __launch_bounds__(256) k_pc_apply_r1(const double* __restrict__ Rv, const double* __restrict__ dinv,
+                                                     const double* __restrict__ q1, const double* __restrict__ T,
+                                                     i64 N, int k, double* __restrict__ Z) {
+  extern __shared__ double Ts[];
+  for (int j = threadIdx.x; j < k; j += blockDim.x) Ts[j] = T[j];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (i64 r = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5; r < N; r += ((i64)gridDim.x * blockDim.x) >> 5) {
+    double s = 0.0;
+    for (int j = lane; j < k; j += 32) s = fma(q1[r * k + j], Ts[j], s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) Z[r] = dinv[r] * (dinv[r] * Rv[r] - s);
+  }
+}
+
 // ================================================================ split preconditioner (row-sharded Q1)
 // T = Q1ᵀ D^{-1/2} r over this preconditioner's rows (k×nrhs, device): the
 // partial projection a row-sharded preconditioner all-reduces before
 // finishing.
 void precond_project(Precond& M, const double* r, int nrhs, double* T, cudaStream_t s) {
   M.ensure(nrhs);
+  if (nrhs == 1) {
+    k_pc_proj_r1<<<RB, 256, 0, s>>>(r, M.dinv.p, M.q1.p, M.N, int(M.k), M.partial.p);
+    launched("precond proj (1 RHS, streaming)");
+    k_pc_fin<<<fin_blocks(int(M.k)), 256, 0, s>>>(M.partial.p, int(M.k), T);
+    launched("precond fin");
+    return;
+  }
   const size_t sh1 = sizeof(double) * (PC_RT * M.k + PC_RT * nrhs + M.k * nrhs);
   raise_smem_limit((const void*)k_pc_proj, sh1);
   k_pc_proj<<<RB, RT, sh1, s>>>(r, M.dinv.p, M.q1.p, M.N, int(M.k), nrhs, M.partial.p, nullptr);
@@ -2070,6 +2117,11 @@ void precond_project(Precond& M, const double* r, int nrhs, double* T, cudaStrea
 // z = D^{-1/2}(D^{-1/2} r − Q1 T) for a given (all-reduced) T.
 void precond_finish(Precond& M, const double* r, const double* T, double* z, int nrhs, cudaStream_t s) {
   M.ensure(nrhs);
+  if (nrhs == 1) {
+    k_pc_apply_r1<<<blocks_for(M.N * 32), 256, sizeof(double) * M.k, s>>>(r, M.dinv.p, M.q1.p, T, M.N, int(M.k), z);
+    launched("precond apply (1 RHS, warp per row)");
+    return;
+  }
   const size_t sh2 = sizeof(double) * (M.k * nrhs + RT);
   raise_smem_limit((const void*)k_pc_apply, sh2);
   k_pc_apply<<<RB, RT, sh2, s>>>(r, M.dinv.p, M.q1.p, T, M.N, int(M.k), nrhs, z, nullptr);

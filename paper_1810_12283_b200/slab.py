@@ -49,6 +49,27 @@ class SlabShardedDskiOperator:
                       if self.mine.size else None)
         self.M = grid.size()
         self.G = self.d + 1
+        # per RHS count: whether every rank can run the split one-launch path
+        # (decided collectively: the all-reduced buffers must match)
+        self._split = {}
+        self._u2buf = None
+
+    def _use_split(self, nrhs):
+        import torch
+        import torch.distributed as dist
+        if nrhs not in self._split:
+            ok = 1.0 if self.local is None else float(self.local.fused_split_dev(2, 0, 0, 0, nrhs))
+            t = torch.tensor([ok], dtype=torch.float64, device=self.dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
+            self._split[nrhs] = bool(t.item() > 0.5)
+        return self._split[nrhs]
+
+    def _u2(self, nrhs):
+        import torch
+        need = 2 * self.M * nrhs
+        if self._u2buf is None or self._u2buf.numel() < need:
+            self._u2buf = torch.empty(need, dtype=torch.float64, device=self.dev)
+        return self._u2buf[:need]
 
     def size(self):
         return self.n * self.G
@@ -66,9 +87,17 @@ class SlabShardedDskiOperator:
         st = torch.cuda.current_stream(self.dev).cuda_stream
         U = torch.empty(self.M * nrhs, dtype=torch.float64, device=self.dev) if U is None else U
         W = torch.empty_like(U) if W is None else W
+        split = self._use_split(nrhs)
         if self.local is None:  # empty slab: contribute zeros to the grid sum, no rows to gather
-            U.zero_()
-            dist.all_reduce(U, op=dist.ReduceOp.SUM, group=self.group)
+            Z = self._u2(nrhs) if split else U
+            Z.zero_()
+            dist.all_reduce(Z, op=dist.ReduceOp.SUM, group=self.group)
+            return
+        if split:  # one-launch kernel split at its first barrier: [u; h] all-reduced between the launches
+            U2 = self._u2(nrhs)
+            self.local.fused_split_dev(0, Vi.data_ptr(), U2.data_ptr(), 0, nrhs, stream=st)
+            dist.all_reduce(U2, op=dist.ReduceOp.SUM, group=self.group)
+            self.local.fused_split_dev(1, Vi.data_ptr(), U2.data_ptr(), Oi.data_ptr(), nrhs, stream=st)
             return
         self.local.stage_dev(0, Vi.data_ptr(), U.data_ptr(), nrhs, stream=st)   # Bᵣᵀ vᵣ, full grid
         dist.all_reduce(U, op=dist.ReduceOp.SUM, group=self.group)             # Σ_r over NVLink

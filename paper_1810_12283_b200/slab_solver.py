@@ -109,14 +109,15 @@ class GpuSlabBackend:
         return self.X_loc[i], g
 
     def kernel_column(self, x, g):
+        """Local rows of the pivot's kernel column: B_r K_UU w(x), w the
+        pivot's value (g = 0) or ∂/∂x_{g-1} stencil, on the device."""
         if self.local is None:
             return self.zeros(0)
-        x = np.asarray(x, dtype=np.float64).reshape(1, -1)
-        if g == 0:
-            col = self.local.cross_covariance(x)[:, 0]
-        else:
-            col = self.local.cross_covariance_jacobian(x)[:, 0, g - 1]
-        return self.torch.from_numpy(np.ascontiguousarray(col)).to(self.dev)
+        torch = self.torch
+        xt = torch.as_tensor(np.asarray(x, dtype=np.float64).reshape(-1), device=self.dev).contiguous()
+        col = torch.empty(self.N_loc, dtype=torch.float64, device=self.dev)
+        self.local.cross_covariance_dev(xt.data_ptr(), 1, g - 1, col.data_ptr(), self.N_loc, stream=self._stream())
+        return col
 
     def make_precond(self, Q1, dinv):
         from . import Preconditioner
@@ -349,50 +350,47 @@ class SlabCgResult:
 def slab_cg(be, Bm, tol=1e-4, max_iterations=1000, precond=None, group=None):
     """cg (linalg.cpp:85-131) on this rank's rows of a block of right-hand
     sides (N_loc × B), every column with its own α, β and stopping iteration
-    (a stopped column is frozen); x0 = 0."""
+    (a stopped column is frozen); x0 = 0. The per-column bookkeeping stays on
+    the device: one host synchronisation per iteration (the stop test)."""
     torch = be.torch
     B = Bm.shape[1]
     X = torch.zeros_like(Bm)
     bnorm = torch.sqrt(_coldot(be, Bm, Bm, group))
+    safe_b = torch.where(bnorm > 0, bnorm, torch.ones_like(bnorm))
     active = bnorm > 0
-    iters = [0] * B
-    conv = [bool(not a) for a in active.tolist()]
-    hist = [[] for _ in range(B)]
+    conv = ~active  # b = 0: converged with 0 iterations (linalg.cpp:93-96)
+    iters = torch.zeros(B, dtype=torch.int64, device=Bm.device)
     R = Bm.clone()
     Z = precond.apply(R) if precond is not None else R.clone()
     P = Z.clone()
     rz = _coldot(be, R, Z, group)
-    relres = torch.sqrt(_coldot(be, R, R, group)) / torch.where(active, bnorm, torch.ones_like(bnorm))
-    for b in range(B):
-        if active[b]:
-            hist[b].append(float(relres[b]))
-            if relres[b] <= tol:
-                conv[b] = True
-                active[b] = False
+    relres = torch.sqrt(_coldot(be, R, R, group)) / safe_b
+    nan = torch.full_like(relres, float("nan"))
+    hist = [torch.where(active, relres, nan)]
+    done0 = active & (relres <= tol)
+    conv = conv | done0
+    active = active & ~done0
     for it in range(max_iterations):
         if not bool(active.any()):
             break
         AP = be.mvm(P)
         pAp = _coldot(be, P, AP, group)
-        stall = active & (pAp <= 0)  # loss of positive definiteness: stop unconverged
-        active = active & ~stall
+        active = active & ~(pAp <= 0)  # loss of positive definiteness: stop unconverged
         a = torch.where(active, rz / torch.where(active, pAp, torch.ones_like(pAp)), torch.zeros_like(pAp))
         X = X + a[None, :] * P
         R = R - a[None, :] * AP
-        rr = _coldot(be, R, R, group)
-        relres = torch.sqrt(rr) / torch.where(bnorm > 0, bnorm, torch.ones_like(bnorm))
-        for b in range(B):
-            if active[b]:
-                iters[b] = it + 1
-                hist[b].append(float(relres[b]))
-                if relres[b] <= tol:
-                    conv[b] = True
-                    active[b] = False
-        if not bool(active.any()):
-            break
+        relres = torch.sqrt(_coldot(be, R, R, group)) / safe_b
+        iters = torch.where(active, torch.full_like(iters, it + 1), iters)
+        hist.append(torch.where(active, relres, nan))
+        done = active & (relres <= tol)
+        conv = conv | done
+        active = active & ~done
         Z = precond.apply(R) if precond is not None else R.clone()
         rzn = _coldot(be, R, Z, group)
         beta = torch.where(active, rzn / torch.where(active, rz, torch.ones_like(rz)), torch.zeros_like(rz))
         P = torch.where(active[None, :], Z + beta[None, :] * P, P)
         rz = torch.where(active, rzn, rz)
-    return SlabCgResult(X, iters, conv, hist)
+    H = torch.stack(hist).cpu().numpy()
+    histories = [[float(v) for v in H[:, b] if v == v] for b in range(B)]
+    return SlabCgResult(X, [int(v) for v in iters.cpu().tolist()], [bool(v) for v in conv.cpu().tolist()],
+                        histories)

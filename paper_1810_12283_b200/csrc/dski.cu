@@ -1677,7 +1677,7 @@ static void smem_attr(const void* fn, size_t bytes) {
 // contracts its 6×6×6 stencil from shared memory — instead of 216 L2 reads
 // per (point, RHS), one L2 read of the block per unit (C3's surface points
 // pile up to ~180 per cell). Same summation order as k_gather_lean.
-constexpr int G3U_THREADS = 256;
+constexpr int G3U_THREADS = 128;
 template <int T, bool GRAD>
 __global__ void __launch_bounds__(G3U_THREADS) k_gather_units3(DskiView op, const int4* __restrict__ units, int nunits,
                                                                const int2* __restrict__ urange,
@@ -2095,7 +2095,7 @@ void DskiOp::gather(const double* w, const double* v, double* out, int nrhs, boo
                               : (G ? (const void*)k_gather_units3<4, true> : (const void*)k_gather_units3<4, false>);
       raise_smem_limit(fn, smem);
       GK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, int(cudaSharedmemCarveoutMaxShared)));
-      const unsigned grid = static_cast<unsigned>(std::min(g3_nunits, 148 * 8));
+      const unsigned grid = static_cast<unsigned>(std::min(g3_nunits, 148 * 16));
       if (T == 6) {
         if (G) k_gather_units3<6, true><<<grid, G3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, w, v, out, nrhs, noise ? 1 : 0, g3_zspan);
         else k_gather_units3<6, false><<<grid, G3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, w, v, out, nrhs, noise ? 1 : 0, g3_zspan);

@@ -19,7 +19,8 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libgk_b200.so")
+# GK_B200_LIB: an alternative build of the same library (A/B timing of compile-time variants)
+LIB_PATH = os.environ.get("GK_B200_LIB") or os.path.join(_HERE, "_lib", "libgk_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

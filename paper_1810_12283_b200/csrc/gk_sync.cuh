@@ -40,8 +40,8 @@ __device__ __forceinline__ void grid_sync(unsigned long long* bar) {
     const unsigned long long target = (t / nb + 1) * nb;
     unsigned spins = 0;
     while (ld_relaxed(bar) < target) {
-      if (++spins > (1u << 24)) __trap();
-      __nanosleep(kBarrierSleepNs);
+      if (++spins > (1u << 28)) __trap();
+      if (kBarrierSleepNs) __nanosleep(kBarrierSleepNs);
     }
     asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
   }

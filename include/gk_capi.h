@@ -89,6 +89,9 @@ gk_status gk_grid_cover(const double* X, int64_t n, int d, double target_spacing
 uint64_t gk_mix_seed(uint64_t seed, uint64_t stream);
 void gk_rademacher_vector(int64_t n, uint64_t seed, uint64_t stream, double* out);
 void gk_gaussian_vector(int64_t n, uint64_t seed, uint64_t stream, double* out);
+/* std::uniform_real_distribution<double>(a, b) over seeded_rng(seed, stream)
+ * (libstdc++; the restart jitter of GpModel::fit, gp.cpp:328-331). */
+void gk_uniform_vector(int64_t n, uint64_t seed, uint64_t stream, double a, double b, double* out);
 
 /* ---------------------------------------------------------------- operators
  * Every structured operator is a gk_op (LinearOperator, linear_operator.hpp:12-35). */
@@ -379,6 +382,16 @@ gk_status gk_precond_finish_dev(const gk_precond* M, const double* dR, const dou
  * Pass NULL buffers to query n and d first. */
 gk_status gk_make_dataset(int config, uint64_t seed, int64_t* n, int* d, double* X, double* y,
                           double* dY);
+
+/* sample_dataset(test_function_by_name(name), n, Uniform, seed, σ₁, σ₂,
+ * with_gradients) (testfns.cpp:355-402) for name "franke" (d = 2,
+ * testfns.cpp:67-92) or "friedman" (d = 5, :290-310) — the data of the
+ * precond-study tool (cmd_precond_study.cpp:31-34). X n×d col-major, y n,
+ * dY n×d (NULL when with_gradients = 0). X = NULL only queries d.
+ * Unknown name: GK_ERR_ARG (std::invalid_argument, testfns.cpp:325). */
+gk_status gk_sample_test_function(const char* name, int64_t n, uint64_t seed, double noise_value,
+                                  double noise_gradient, int with_gradients, int* d, double* X, double* y,
+                                  double* dY);
 
 #ifdef __cplusplus
 }

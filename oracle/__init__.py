@@ -128,6 +128,10 @@ def lib():
             "orc_dskip_from_factors": (_vp, [_i64, C.c_int, _d, _d, C.c_int, _i64p, C.POINTER(_dp),
                                              C.POINTER(_dp), C.POINTER(_dp)]),
             "orc_make_dataset": (C.c_int, [C.c_int, _u64, _i64p, _ip, _dp, _dp, _dp]),
+            "orc_sample_test_function": (C.c_int, [C.c_char_p, _i64, _u64, _d, _d, C.c_int, _ip, _dp, _dp,
+                                                   _dp]),
+            "orc_gp_fit": (C.c_int, [_vp, C.c_int, C.c_int, _d, _d, C.c_int, _u64, _dp, _dp]),
+            "orc_gp_set_hyperparameters": (C.c_int, [_vp, _d, _d, _d, _d]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -188,6 +192,22 @@ def make_dataset(config, seed=0):
     y = np.empty(n)
     dY = np.empty((n, d), order="F")
     lib().orc_make_dataset(int(config), int(seed), None, None, _p(X), _p(y), _p(dY))
+    return X, y, dY
+
+
+def sample_test_function(name, n, seed=0, noise=(0.0, 0.0), with_gradients=True):
+    """sample_dataset (testfns.cpp:355-402), uniform sampling, for "franke"
+    (d = 2) or "friedman" (d = 5). Returns X (n×d col-major), y, dY (or None)."""
+    d = C.c_int()
+    if lib().orc_sample_test_function(name.encode(), int(n), int(seed), 0.0, 0.0, 0, C.byref(d), None, None,
+                                      None) != 0:
+        raise ValueError(f"unknown test function '{name}'")
+    X = np.empty((n, d.value), order="F")
+    y = np.empty(n)
+    dY = np.empty((n, d.value), order="F") if with_gradients else None
+    lib().orc_sample_test_function(name.encode(), int(n), int(seed), float(noise[0]), float(noise[1]),
+                                   int(with_gradients), C.byref(d), _p(X), _p(y),
+                                   _p(dY) if dY is not None else None)
     return X, y, dY
 
 
@@ -693,6 +713,20 @@ class GpModel:
         grads = np.empty((T, self.d), order="F")
         _check(lib().orc_gp_predict_mean_grad(self.h, _p(Xt), T, _p(vals), _p(grads)))
         return vals, grads
+
+    def set_hyperparameters(self, ell, s, noise_value, noise_gradient):
+        _check(lib().orc_gp_set_hyperparameters(self.h, ell, s, noise_value, noise_gradient))
+
+    def fit(self, max_iterations=40, restarts=3, initial_step=0.3, min_step=1e-4, optimize_noise=True, seed=0):
+        """GpModel::fit (gp.cpp:294-404). Returns dict(ell, s, noise_value,
+        noise_gradient, log_marginal, restarts=[(succeeded, iterations, lml)])."""
+        out = np.empty(5)
+        nrest = max(restarts, 1) if max_iterations > 0 else 1
+        rep = np.empty(3 * nrest)
+        _check(lib().orc_gp_fit(self.h, int(max_iterations), int(restarts), float(initial_step), float(min_step),
+                                int(optimize_noise), int(seed), _p(out), _p(rep)))
+        return dict(ell=out[0], s=out[1], noise_value=out[2], noise_gradient=out[3], log_marginal=out[4],
+                    restarts=[(bool(rep[3 * i]), int(rep[3 * i + 1]), rep[3 * i + 2]) for i in range(nrest)])
 
     def lml_gradient(self, probes=8):
         """GpModel::lml_gradient (gp.cpp:220-292): ∂LML/∂(log ℓ, log s, log σ₁[, log σ₂])."""

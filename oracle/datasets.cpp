@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdint>
 #include <random>
+#include <string>
 #include <vector>
 #include <algorithm>
 
@@ -212,6 +213,54 @@ extern "C" int orc_make_dataset(int config, unsigned long long seed, long long* 
       y[i] = v;
       for (int j = 0; j < 6; ++j) G(i, j) = g[j];
     }
+  }
+  return 0;
+}
+
+// sample_dataset (testfns.cpp:355-402) for the precond-study functions:
+// Franke (testfns.cpp:67-92, d = 2) and Friedman #1 (:290-310, d = 5), uniform
+// sampling on [0, 1]^d. Returns 1 for an unknown name.
+extern "C" int orc_sample_test_function(const char* name, long long n, unsigned long long seed, double nv,
+                                        double ng, int with_gradients, int* d_out, double* X, double* y,
+                                        double* dY) {
+  const std::string fn(name ? name : "");
+  const int d = fn == "franke" ? 2 : fn == "friedman" ? 5 : 0;
+  if (d == 0) return 1;
+  *d_out = d;
+  if (!X) return 0;
+  auto rng = std::mt19937_64(gko::mix_seed(seed, 0));
+  std::uniform_real_distribution<double> unif(0.0, 1.0);
+  for (i64 i = 0; i < n; ++i)
+    for (int j = 0; j < d; ++j) X[j * n + i] = 0.0 + 1.0 * unif(rng);
+  std::normal_distribution<double> gauss(0.0, 1.0);
+  const double pi = 3.14159265358979323846;
+  std::vector<double> g(static_cast<size_t>(d));
+  for (i64 i = 0; i < n; ++i) {
+    double v;
+    if (d == 2) {
+      const double a = X[i], b = X[n + i];
+      const double e1 = 0.75 * std::exp(-(std::pow(9 * a - 2, 2) + std::pow(9 * b - 2, 2)) / 4.0);
+      const double e2 = 0.75 * std::exp(-std::pow(9 * a + 1, 2) / 49.0 - (9 * b + 1) / 10.0);
+      const double e3 = 0.5 * std::exp(-(std::pow(9 * a - 7, 2) + std::pow(9 * b - 3, 2)) / 4.0);
+      const double e4 = -0.2 * std::exp(-std::pow(9 * a - 4, 2) - std::pow(9 * b - 7, 2));
+      v = e1 + e2 + e3 + e4;
+      g[0] = e1 * (-9.0 * (9 * a - 2) / 2.0) + e2 * (-18.0 * (9 * a + 1) / 49.0) + e3 * (-9.0 * (9 * a - 7) / 2.0) +
+             e4 * (-18.0 * (9 * a - 4));
+      g[1] = e1 * (-9.0 * (9 * b - 2) / 2.0) + e2 * (-9.0 / 10.0) + e3 * (-9.0 * (9 * b - 3) / 2.0) +
+             e4 * (-18.0 * (9 * b - 7));
+    } else {
+      const double x0 = X[i], x1 = X[n + i], x2 = X[2 * n + i], x3 = X[3 * n + i], x4 = X[4 * n + i];
+      v = 10.0 * std::sin(pi * x0 * x1) + 20.0 * std::pow(x2 - 0.5, 2) + 10.0 * x3 + 5.0 * x4;
+      const double c = 10.0 * pi * std::cos(pi * x0 * x1);
+      g[0] = c * x1;
+      g[1] = c * x0;
+      g[2] = 40.0 * (x2 - 0.5);
+      g[3] = 10.0;
+      g[4] = 5.0;
+    }
+    y[i] = v + nv * gauss(rng);
+    if (with_gradients)
+      for (int j = 0; j < d; ++j) dY[j * n + i] = g[j] + ng * gauss(rng);
   }
   return 0;
 }

@@ -1429,6 +1429,132 @@ Vec GpModel::dlogell_apply(const double* v) {  // gp.cpp:200-218
   return static_cast<const DskipOperator&>(*op_).dlogell_apply(v);
 }
 
+void GpModel::set_hyperparameters(double ell, double s, double nv, double ng) {  // gp.cpp:46-64
+  if (nv <= 0.0) throw std::invalid_argument("value noise must be positive");
+  k_.ell = ell;
+  k_.s = s;
+  nv_ = nv;
+  ng_ = ng;
+  op_.reset();
+  dski_ = nullptr;
+  precond_.reset();
+  factor_.reset();
+  alpha_.reset();
+  mean_grid_.reset();
+  kuu_dlogell_.reset();
+}
+
+// Projected gradient ascent in log-parameter space with a per-restart step
+// that grows ×1.4 on acceptance and shrinks ×0.4 on rejection; restarts
+// r > 0 jitter the start by U(−0.7, 0.7) from seeded_rng(seed, 31 + r).
+GpModel::FitOut GpModel::fit(int max_iterations, int restarts_opt, double initial_step, double min_step,
+                             bool optimize_noise, std::uint64_t seed) {
+  const bool grads = dY_.rows > 0;
+  const int np = grads ? 4 : 3;
+  auto encode = [&] {
+    Vec p(static_cast<size_t>(np));
+    p[0] = std::log(k_.ell);
+    p[1] = std::log(k_.s);
+    p[2] = std::log(nv_);
+    if (grads) p[3] = std::log(ng_);
+    return p;
+  };
+  auto decode = [&](const Vec& p) {
+    set_hyperparameters(std::exp(p[0]), std::exp(p[1]), std::exp(p[2]), grads ? std::exp(p[3]) : ng_);
+  };
+  auto clampv = [](double v, double lo, double hi) { return std::min(std::max(v, lo), hi); };
+  auto clamp_params = [&](Vec p) {
+    p[0] = clampv(p[0], std::log(1e-4), std::log(1e4));
+    p[1] = clampv(p[1], std::log(1e-6), std::log(1e6));
+    for (int i = 2; i < np; ++i) p[i] = clampv(p[i], std::log(1e-6), std::log(1e3));
+    return p;
+  };
+  const Vec p0 = encode();
+  const int restarts = max_iterations > 0 ? std::max(restarts_opt, 1) : 1;
+  FitOut best;
+  best.log_marginal = -std::numeric_limits<double>::infinity();
+  Vec best_p = p0;
+  bool any_ok = false;
+  std::string errors;
+  for (int r = 0; r < restarts; ++r) {
+    FitReport rep;
+    Vec p = p0;
+    if (r > 0) {
+      std::mt19937_64 rng(mix_seed(seed, 31 + std::uint64_t(r)));
+      std::uniform_real_distribution<double> jitter(-0.7, 0.7);
+      for (int i = 0; i < np; ++i) p[i] += jitter(rng);
+      p = clamp_params(p);
+    }
+    try {
+      decode(p);
+      double L = log_marginal_likelihood();
+      double step = initial_step;
+      int it = 0;
+      for (; it < max_iterations; ++it) {
+        Vec g;
+        try {
+          g = lml_gradient();
+        } catch (const std::exception&) {
+          break;
+        }
+        if (!optimize_noise) {
+          g[2] = 0.0;
+          if (np == 4) g[3] = 0.0;
+        }
+        double gn = 0.0;
+        for (double v : g) {
+          if (!std::isfinite(v)) throw std::runtime_error("non-finite likelihood gradient");
+          gn += v * v;
+        }
+        if (std::sqrt(gn) < 1e-10) break;
+        bool accepted = false;
+        while (step >= min_step) {
+          Vec pt = p;
+          for (int i = 0; i < np; ++i) pt[i] = p[i] + clampv(step * g[i], -0.5, 0.5);
+          pt = clamp_params(pt);
+          decode(pt);
+          double Lt;
+          try {
+            Lt = log_marginal_likelihood();
+          } catch (const std::exception&) {
+            Lt = -std::numeric_limits<double>::infinity();
+          }
+          if (std::isfinite(Lt) && Lt > L) {
+            p = pt;
+            L = Lt;
+            step = std::min(step * 1.4, 2.0);
+            ++rep.accepted_steps;
+            accepted = true;
+            break;
+          }
+          step *= 0.4;
+        }
+        if (!accepted) break;
+      }
+      decode(p);
+      rep.succeeded = true;
+      rep.iterations = it;
+      rep.log_marginal = L;
+      if (L > best.log_marginal) {
+        best.log_marginal = L;
+        best_p = p;
+      }
+      any_ok = true;
+    } catch (const std::exception& e) {
+      rep.succeeded = false;
+      errors += std::string(" [") + e.what() + "]";
+    }
+    best.restarts.push_back(rep);
+  }
+  if (!any_ok) throw std::runtime_error("all fit restarts failed:" + errors);
+  decode(best_p);
+  best.ell = k_.ell;
+  best.s = k_.s;
+  best.nv = nv_;
+  best.ng = ng_;
+  return best;
+}
+
 Vec GpModel::lml_gradient() {  // gp.cpp:220-292
   const LinearOperator& A = op();
   const Index N = A.size();

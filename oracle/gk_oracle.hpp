@@ -390,6 +390,19 @@ class GpModel {
   Vec dlogell_apply(const double* v);      // gp.cpp:200-218 (D-SKI / D-SKIP branches)
   Vec lml_gradient();                      // gp.cpp:220-292 (stochastic-trace branch)
   void set_gradient_probes(int p) { cfg_.gradient_probes = p; }
+  void set_hyperparameters(double ell, double s, double nv, double ng);  // gp.cpp:46-64
+  struct FitReport {
+    bool succeeded = false;
+    double log_marginal = 0.0;
+    int iterations = 0, accepted_steps = 0;
+  };
+  struct FitOut {
+    double ell, s, nv, ng, log_marginal;
+    std::vector<FitReport> restarts;
+  };
+  // gp.cpp:294-404 (FitOptions gp.hpp:50-57)
+  FitOut fit(int max_iterations, int restarts, double initial_step, double min_step, bool optimize_noise,
+             std::uint64_t seed);
 
  private:
   KernelSpec k_;

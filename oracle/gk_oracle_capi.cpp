@@ -489,6 +489,28 @@ int orc_gp_lml_gradient(void* m, int probes, double* grad, int* nparams) {
     *nparams = int(r.size());
   });
 }
+// GpModel::fit (gp.cpp:294-404): out = (ℓ, s, σ₁, σ₂, best LML); per
+// restart r: reports[3r..3r+2] = (succeeded, iterations, LML).
+int orc_gp_fit(void* m, int max_iterations, int restarts, double initial_step, double min_step,
+               int optimize_noise, unsigned long long seed, double* out, double* reports) {
+  return guard([&] {
+    auto r = static_cast<GpModel*>(m)->fit(max_iterations, restarts, initial_step, min_step,
+                                           optimize_noise != 0, seed);
+    out[0] = r.ell;
+    out[1] = r.s;
+    out[2] = r.nv;
+    out[3] = r.ng;
+    out[4] = r.log_marginal;
+    for (size_t i = 0; i < r.restarts.size(); ++i) {
+      reports[3 * i] = r.restarts[i].succeeded ? 1.0 : 0.0;
+      reports[3 * i + 1] = r.restarts[i].iterations;
+      reports[3 * i + 2] = r.restarts[i].log_marginal;
+    }
+  });
+}
+int orc_gp_set_hyperparameters(void* m, double ell, double s, double nv, double ng) {
+  return guard([&] { static_cast<GpModel*>(m)->set_hyperparameters(ell, s, nv, ng); });
+}
 int orc_gp_dlogell_apply(void* m, const double* v, double* out) {
   return guard([&] { copy_out(static_cast<GpModel*>(m)->dlogell_apply(v), out); });
 }

@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import dataclasses
 from dataclasses import dataclass
 
 import numpy as np
@@ -118,6 +119,8 @@ _SIGS = {
     "gk_dski_cross_covariance_jacobian": (C.c_int, [_vp, _dp, _i64, _dp, _i64]),
     "gk_dski_cross_covariance": (C.c_int, [_vp, _dp, _i64, _dp, _i64]),
     "gk_make_dataset": (C.c_int, [C.c_int, _u64, _i64p, _ip, _dp, _dp, _dp]),
+    "gk_uniform_vector": (None, [_i64, _u64, _u64, _d, _d, _dp]),
+    "gk_sample_test_function": (C.c_int, [C.c_char_p, _i64, _u64, _d, _d, C.c_int, _ip, _dp, _dp, _dp]),
     "gk_dski_cross_covariance_dev": (C.c_int, [_vp, _vp, _i64, C.c_int, _vp, _i64, _vp]),
     "gk_dski_fused_split_dev": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, _i64, _vp]),
     "gk_precond_from_q1_dev": (C.c_int, [_vp, _vp, _i64, _i64, C.c_int, C.POINTER(_vp)]),
@@ -212,6 +215,13 @@ def gaussian_vector(n, seed, stream=0):
 
 # ------------------------------------------------------------------ kernel / grid
 SE, SPLINE = 0, 1
+
+
+def uniform_vector(n, seed, stream, a, b):
+    """std::uniform_real_distribution<double>(a, b) over seeded_rng(seed, stream)."""
+    out = np.empty(n)
+    _lib.gk_uniform_vector(n, seed, stream, float(a), float(b), _p(out))
+    return out
 
 
 @dataclass
@@ -974,6 +984,106 @@ class GpModel:
     def dlogell_apply(self, v):
         return self.op().dlogell_apply(v)
 
+    def fit(self, max_iterations=40, restarts=3, initial_step=0.3, min_step=1e-4, optimize_noise=True, seed=0):
+        """GpModel::fit (gp.cpp:294-404, FitOptions gp.hpp:50-57): gradient
+        ascent on the LML in log-parameter space θ = (log ℓ, log s, log σ₁[,
+        log σ₂]); steps clamped to ±0.5 per coordinate, θ clamped to the
+        reference's boxes, step ×1.4 (≤ 2) on an accepted step and ×0.4 on a
+        rejected one down to min_step; restart r > 0 jitters the start by
+        U(−0.7, 0.7) from seeded_rng(seed, 31 + r). Every LML and gradient
+        evaluation runs on the device (log_marginal_likelihood,
+        lml_gradient); this loop is host control flow only. Leaves the model
+        at the best restart's parameters and returns a FitResult."""
+        grads = self.has_gradients
+        npar = 4 if grads else 3
+        lo = np.array([np.log(1e-4), np.log(1e-6)] + [np.log(1e-6)] * (npar - 2))
+        hi = np.array([np.log(1e4), np.log(1e6)] + [np.log(1e3)] * (npar - 2))
+
+        def encode():
+            p = [np.log(self.kernel.lengthscale), np.log(self.kernel.outputscale), np.log(self.noise[0])]
+            return np.array(p + ([np.log(self.noise[1])] if grads else []))
+
+        def decode(p):
+            k = dataclasses.replace(self.kernel, lengthscale=float(np.exp(p[0])), outputscale=float(np.exp(p[1])))
+            self.set_hyperparameters(k, float(np.exp(p[2])), float(np.exp(p[3])) if grads else self.noise[1])
+
+        p0 = encode()
+        nrest = max(restarts, 1) if max_iterations > 0 else 1
+        best = FitResult(self.kernel, self.noise[0], self.noise[1], -np.inf, [])
+        best_p, any_ok = p0, False
+        for r in range(nrest):
+            rep = FitRestartReport()
+            p = p0.copy()
+            if r > 0:
+                p = np.minimum(np.maximum(p + uniform_vector(npar, seed, 31 + r, -0.7, 0.7), lo), hi)
+            try:
+                decode(p)
+                L = self.log_marginal_likelihood()
+                step = initial_step
+                it = 0
+                while it < max_iterations:
+                    try:
+                        g = self.lml_gradient()
+                    except (RuntimeError, ValueError):
+                        break  # keep the progress made so far in this restart
+                    if not optimize_noise:
+                        g[2:] = 0.0
+                    if not np.all(np.isfinite(g)):
+                        raise RuntimeError("non-finite likelihood gradient")
+                    if np.linalg.norm(g) < 1e-10:
+                        break
+                    accepted = False
+                    while step >= min_step:
+                        pt = np.minimum(np.maximum(p + np.clip(step * g, -0.5, 0.5), lo), hi)
+                        decode(pt)
+                        try:
+                            Lt = self.log_marginal_likelihood()
+                        except (RuntimeError, ValueError):
+                            Lt = -np.inf
+                        if np.isfinite(Lt) and Lt > L:
+                            p, L = pt, Lt
+                            step = min(step * 1.4, 2.0)
+                            rep.accepted_steps += 1
+                            accepted = True
+                            break
+                        step *= 0.4
+                    if not accepted:
+                        break
+                    it += 1
+                decode(p)
+                rep.succeeded, rep.iterations, rep.log_marginal = True, it, L
+                if L > best.log_marginal:
+                    best.log_marginal, best_p = L, p
+                any_ok = True
+            except (RuntimeError, ValueError) as e:
+                rep.succeeded, rep.error = False, str(e)
+            best.restarts.append(rep)
+        if not any_ok:
+            raise RuntimeError("all fit restarts failed:" + "".join(f" [{r.error}]" for r in best.restarts))
+        decode(best_p)
+        best.kernel, best.noise_value, best.noise_gradient = self.kernel, self.noise[0], self.noise[1]
+        return best
+
+
+@dataclass
+class FitRestartReport:
+    """FitRestartReport (gp.hpp:59-65)."""
+    succeeded: bool = False
+    error: str = ""
+    log_marginal: float = -np.inf
+    iterations: int = 0
+    accepted_steps: int = 0
+
+
+@dataclass
+class FitResult:
+    """FitResult (gp.hpp:67-73)."""
+    kernel: KernelSpec
+    noise_value: float
+    noise_gradient: float
+    log_marginal: float
+    restarts: list
+
 
 class LanczosFactor:
     """LanczosFactor (linalg.hpp:102-114)."""
@@ -1034,6 +1144,22 @@ def make_dataset(config, seed=0):
     y = np.empty(n)
     dY = np.empty((n, d), order="F")
     _check(_lib.gk_make_dataset(config, seed, None, None, _p(X), _p(y), _p(dY)))
+    return X, y, dY
+
+
+def sample_test_function(name, n, seed=0, noise=(0.0, 0.0), with_gradients=True):
+    """sample_dataset (testfns.cpp:355-402), uniform sampling, for the
+    precond-study functions "franke" (d = 2) and "friedman" (d = 5).
+    Returns X (n×d), y, dY (None without gradients)."""
+    d = C.c_int()
+    _check(_lib.gk_sample_test_function(name.encode(), int(n), int(seed), 0.0, 0.0, 0, C.byref(d), None, None,
+                                        None))
+    X = np.empty((n, d.value), order="F")
+    y = np.empty(n)
+    dY = np.empty((n, d.value), order="F") if with_gradients else None
+    _check(_lib.gk_sample_test_function(name.encode(), int(n), int(seed), float(noise[0]), float(noise[1]),
+                                        int(with_gradients), C.byref(d), _p(X), _p(y),
+                                        _p(dY) if dY is not None else None))
     return X, y, dY
 
 

@@ -15,6 +15,9 @@
 #include "gk_kernels.cuh"
 #include "solvers.hpp"
 
+extern "C" gk_status gk_sample_test_function_impl(const char* name, int64_t n, std::uint64_t seed, double nv,
+                                                  double ng, int with_gradients, int* d, double* X, double* y,
+                                                  double* dY);
 extern "C" gk_status gk_make_dataset_impl(int config, std::uint64_t seed, int64_t* n, int* d, double* X,
                                           double* y, double* dY);
 
@@ -262,6 +265,9 @@ gk_status gk_grid_cover(const double* X, int64_t n, int d, double target, int ma
 uint64_t gk_mix_seed(uint64_t seed, uint64_t stream) { return mix_seed(seed, stream); }
 void gk_rademacher_vector(int64_t n, uint64_t seed, uint64_t stream, double* out) { rademacher(n, seed, stream, out); }
 void gk_gaussian_vector(int64_t n, uint64_t seed, uint64_t stream, double* out) { gaussian(n, seed, stream, out); }
+void gk_uniform_vector(int64_t n, uint64_t seed, uint64_t stream, double a, double b, double* out) {
+  uniform(n, seed, stream, a, b, out);
+}
 
 gk_status gk_dski_create(const gk_kernel* kernel, const gk_grid* grid, const double* X, int64_t n, double nv,
                          double ng, int order, int with_gradients, int device, gk_op** out) {
@@ -1451,6 +1457,20 @@ gk_status gk_precond_finish_dev(const gk_precond* M, const double* dR, const dou
     DeviceGuard dg(P.device);
     precond_finish(P, dR, dT, dZ, int(nrhs), S(stream));
   });
+}
+
+gk_status gk_sample_test_function(const char* name, int64_t n, uint64_t seed, double noise_value,
+                                  double noise_gradient, int with_gradients, int* d, double* X, double* y,
+                                  double* dY) {
+  gk_status st = GK_OK;
+  try {
+    st = gk_sample_test_function_impl(name, n, seed, noise_value, noise_gradient, with_gradients, d, X, y, dY);
+    if (st != GK_OK) g_err = std::string("unknown test function '") + (name ? name : "") + "'";
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    st = GK_ERR_RUNTIME;
+  }
+  return st;
 }
 
 gk_status gk_make_dataset(int config, uint64_t seed, int64_t* n, int* d, double* X, double* y, double* dY) {

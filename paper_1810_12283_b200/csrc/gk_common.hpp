@@ -135,6 +135,7 @@ struct HostBuf {
 std::uint64_t mix_seed(std::uint64_t seed, std::uint64_t stream);
 void rademacher(i64 n, std::uint64_t seed, std::uint64_t stream, double* out);
 void gaussian(i64 n, std::uint64_t seed, std::uint64_t stream, double* out);
+void uniform(i64 n, std::uint64_t seed, std::uint64_t stream, double a, double b, double* out);
 // Tridiagonal eigendecomposition, ascending; Z is n×n col-major (may be null
 // for values only).
 void tridiag_eig(int n, const double* alpha, const double* beta, double* evals, double* Z);

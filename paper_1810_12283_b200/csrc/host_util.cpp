@@ -44,6 +44,15 @@ void gaussian(i64 n, std::uint64_t seed, std::uint64_t stream, double* out) {
   for (i64 i = 0; i < n; ++i) out[i] = dist(rng);
 }
 
+// std::uniform_real_distribution<double>(a, b) over seeded_rng(seed, stream)
+// (libstdc++: one 64-bit draw per value, generate_canonical · (b − a) + a);
+// the restart jitter of GpModel::fit (gp.cpp:328-331).
+void uniform(i64 n, std::uint64_t seed, std::uint64_t stream, double a, double b, double* out) {
+  std::mt19937_64 rng(mix_seed(seed, stream));
+  std::uniform_real_distribution<double> dist(a, b);
+  for (i64 i = 0; i < n; ++i) out[i] = dist(rng);
+}
+
 // Symmetric tridiagonal QL iteration with implicit shifts; eigenvectors are
 // rotated along (Z = I initially) so Z's first row gives the Gauss
 // quadrature weights SLQ needs (linalg.cpp:231-245).
@@ -222,6 +231,58 @@ void real_sh(const D3& x, const D3& y, const D3& z, D3* Y) {
 }
 
 }  // namespace
+
+// sample_dataset(fn, n, Uniform, seed, σ₁, σ₂, with_gradients) for the two
+// test functions the precond-study tool sweeps (testfns.cpp:67-92 Franke,
+// :290-310 Friedman #1, :355-402 sampling): X row by row from
+// uniform(0, 1) over seeded_rng(seed), then per point the value and its
+// gradient plus σ·N(0, 1) draws from the same engine.
+extern "C" gk_status gk_sample_test_function_impl(const char* name, i64 n, std::uint64_t seed, double nv,
+                                                  double ng, int with_gradients, int* d_out, double* X,
+                                                  double* y, double* dY) {
+  const std::string fn(name ? name : "");
+  int d = 0;
+  if (fn == "franke") d = 2;
+  else if (fn == "friedman") d = 5;
+  else return GK_ERR_ARG;
+  *d_out = d;
+  if (!X) return GK_OK;
+  std::mt19937_64 rng(gk::mix_seed(seed, 0));
+  std::uniform_real_distribution<double> unif(0.0, 1.0);
+  for (i64 i = 0; i < n; ++i)
+    for (int j = 0; j < d; ++j) X[j * n + i] = 0.0 + (1.0 - 0.0) * unif(rng);
+  std::normal_distribution<double> gauss(0.0, 1.0);
+  const double kPi = 3.14159265358979323846;
+  for (i64 i = 0; i < n; ++i) {
+    double v, g[5];
+    if (d == 2) {
+      const double x = X[i], yv = X[n + i];
+      const double t1 = 0.75 * std::exp(-(std::pow(9 * x - 2, 2) + std::pow(9 * yv - 2, 2)) / 4.0);
+      const double t2 = 0.75 * std::exp(-std::pow(9 * x + 1, 2) / 49.0 - (9 * yv + 1) / 10.0);
+      const double t3 = 0.5 * std::exp(-(std::pow(9 * x - 7, 2) + std::pow(9 * yv - 3, 2)) / 4.0);
+      const double t4 = -0.2 * std::exp(-std::pow(9 * x - 4, 2) - std::pow(9 * yv - 7, 2));
+      v = t1 + t2 + t3 + t4;
+      g[0] = t1 * (-9.0 * (9 * x - 2) / 2.0) + t2 * (-18.0 * (9 * x + 1) / 49.0) + t3 * (-9.0 * (9 * x - 7) / 2.0) +
+             t4 * (-18.0 * (9 * x - 4));
+      g[1] = t1 * (-9.0 * (9 * yv - 2) / 2.0) + t2 * (-9.0 / 10.0) + t3 * (-9.0 * (9 * yv - 3) / 2.0) +
+             t4 * (-18.0 * (9 * yv - 7));
+    } else {
+      double x[5];
+      for (int j = 0; j < 5; ++j) x[j] = X[j * n + i];
+      v = 10.0 * std::sin(kPi * x[0] * x[1]) + 20.0 * std::pow(x[2] - 0.5, 2) + 10.0 * x[3] + 5.0 * x[4];
+      const double c = 10.0 * kPi * std::cos(kPi * x[0] * x[1]);
+      g[0] = c * x[1];
+      g[1] = c * x[0];
+      g[2] = 40.0 * (x[2] - 0.5);
+      g[3] = 10.0;
+      g[4] = 5.0;
+    }
+    y[i] = v + nv * gauss(rng);
+    if (with_gradients)
+      for (int j = 0; j < d; ++j) dY[j * n + i] = g[j] + ng * gauss(rng);
+  }
+  return GK_OK;
+}
 
 extern "C" gk_status gk_make_dataset_impl(int config, std::uint64_t seed, i64* n_out, int* d_out,
                                           double* X, double* y, double* dY) {

@@ -1,0 +1,146 @@
+"""The gradkrig tools on the device, against the oracle:
+GpModel.fit reproduces the reference optimiser (gp.cpp:294-404) step for step;
+`fit` → model JSON → `predict` gives the oracle GpModel's predictive mean,
+gradient and variance (cmd_fit.cpp / cmd_predict.cpp); `precond-study`
+iteration counts match the oracle's CG/PCG (cmd_precond_study.cpp:29-98);
+`benchmark-mvm` times the operator cmd_benchmark_mvm.cpp:55-80 builds."""
+import csv
+import json
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1810_12283_b200 as gk
+from paper_1810_12283_b200 import cli
+from paper_1810_12283_b200 import io as gio
+
+pytestmark = pytest.mark.gpu
+
+N_PTS = 300
+NOISE = 0.05
+
+
+def _franke():
+    X, y, dY = O.sample_test_function("franke", N_PTS, 0, (NOISE, NOISE))
+    return X, y, dY
+
+
+WC = dict(noise=(1.0, 1.0), backend="dski", grid_ratio=0.2, max_grid_nodes=40, tol=1e-10, max_iterations=3000,
+          precond_rank=100, slq_probes=8, slq_steps=25, seed=0)
+
+
+def test_fit_matches_oracle_optimizer():
+    """Same trajectory as the oracle's GpModel::fit: every accept/reject
+    decision, restart jitter, iteration count and final θ. Well-conditioned
+    (σ = 1, rank-100 preconditioner, noise held fixed — FitOptions
+    optimize_noise = false): there every 1e-2-tolerance probe solve of the
+    stochastic gradient stops at the same PCG iteration on both sides, so the
+    gradients agree to ≤1e-8 (tests/test_gpu_gradient.py); in ill-conditioned
+    regimes probe iteration counts move under roundoff and the trajectories
+    separate, as two runs of the reference on different hardware would."""
+    X, y, dY = _franke()
+    ref = O.GpModel(O.KernelSpec(0.3, 1.0), X, y, dY, **WC)
+    gm = gk.GpModel(gk.KernelSpec(0.3, 1.0), X, y, dY, **WC)
+    want = ref.fit(max_iterations=3, restarts=2, optimize_noise=False, seed=0)
+    got = gm.fit(max_iterations=3, restarts=2, optimize_noise=False, seed=0)
+    assert [(r.succeeded, r.iterations) for r in got.restarts] == [(s, i) for s, i, _ in want["restarts"]]
+    assert sum(r.accepted_steps for r in got.restarts) >= 2
+    for r, (_, _, L) in zip(got.restarts, want["restarts"]):
+        assert abs(r.log_marginal - L) <= 1e-8 * abs(L)
+    assert abs(got.kernel.lengthscale - want["ell"]) <= 1e-8 * want["ell"]
+    assert abs(got.kernel.outputscale - want["s"]) <= 1e-8 * want["s"]
+    # noise is not optimised, but restart jitter moves it (gp.cpp:328-331)
+    assert abs(got.noise_value - want["noise_value"]) <= 1e-14 * want["noise_value"]
+    assert abs(got.noise_gradient - want["noise_gradient"]) <= 1e-14 * want["noise_gradient"]
+    assert abs(got.log_marginal - want["log_marginal"]) <= 1e-8 * abs(want["log_marginal"])
+    assert got.log_marginal > gk.GpModel(gk.KernelSpec(0.3, 1.0), X, y, dY, **WC).log_marginal_likelihood()
+
+
+def test_cli_fit_then_predict_matches_oracle(tmp_path):
+    X, y, dY = _franke()
+    data = str(tmp_path / "train.csv")
+    gio.write_dataset_csv(data, gio.Dataset(X, y, dY))
+    model = str(tmp_path / "model.json")
+    # --probes 16: slq 16 probes, gradient probes max(4, 16/2) = 8 (common.cpp:49-50)
+    # one optimiser iteration from σ = 1 (one well-conditioned gradient, see
+    # test_fit_matches_oracle_optimizer), tol 1e-10
+    rc = cli.main(["fit", "--data", data, "--model", model, "--backend", "dski", "--ell", "0.3", "--noise", "1",
+                   "--noise-grad", "1", "--grid-size", "40", "--rank", "100", "--probes", "16", "--tol", "1e-10",
+                   "--maxit", "3000", "--iters", "1", "--restarts", "1"])
+    assert rc == 0
+    j = json.load(open(model))
+    assert j["backend"] == "dski" and j["data"] == {"path": data, "with_gradients": True}
+    assert j["solver"]["precond_rank"] == 100 and j["solver"]["slq_probes"] == 16
+    ref = O.GpModel(O.KernelSpec(0.3, 1.0), X, y, dY, noise=(1.0, 1.0), backend="dski", grid_ratio=0.2,
+                    max_grid_nodes=40, dskip_rank=100, tol=1e-10, max_iterations=3000, precond_rank=100,
+                    slq_probes=16, slq_steps=50, seed=0)
+    want = ref.fit(max_iterations=1, restarts=1, seed=0)
+    assert want["noise_value"] != 1.0  # the step moved every parameter
+    for key, w in ((j["kernel"]["lengthscale"], want["ell"]), (j["kernel"]["outputscale"], want["s"]),
+                   (j["noise"]["value"], want["noise_value"]), (j["noise"]["gradient"], want["noise_gradient"])):
+        assert abs(key - w) <= 1e-8 * w
+    assert j["mean"]["value"] == float(np.mean(y)) or abs(j["mean"]["value"] - np.mean(y)) <= 1e-15
+
+    test = str(tmp_path / "test.csv")
+    Xt = O.sample_test_function("franke", 7, 9)[0]
+    gio.write_csv(test, ["x1", "x2"], Xt.tolist())
+    out = str(tmp_path / "pred.csv")
+    assert cli.main(["predict", "--model", model, "--test", test, "--out", out, "--gradients"]) == 0
+    rows = list(csv.reader(open(out)))
+    assert rows[0] == ["x1", "x2", "mean", "variance", "dmean1", "dmean2"]
+    P = np.array(rows[1:], dtype=float)
+    assert np.array_equal(P[:, :2], Xt)
+    ref.set_hyperparameters(j["kernel"]["lengthscale"], j["kernel"]["outputscale"], j["noise"]["value"],
+                            j["noise"]["gradient"])
+    mu, g = ref.predict_mean_grad(Xt)
+    assert np.max(np.abs(P[:, 2] - mu)) <= 1e-8 * np.max(np.abs(mu))
+    assert np.max(np.abs(P[:, 4:] - g)) <= 1e-8 * np.max(np.abs(g))
+    var = np.array([ref.predict_variance_pivchol(x) for x in Xt])
+    assert np.max(np.abs(P[:, 3] - var)) <= 1e-8 * np.max(np.abs(var))
+
+
+def test_cli_precond_study_matches_oracle(tmp_path):
+    out = str(tmp_path / "study.csv")
+    assert cli.main(["precond-study", "--function", "franke", "--n", "300", "--sweep-points", "2", "--rank", "30",
+                     "--maxit", "400", "--out", out]) == 0
+    rows = np.array(list(csv.reader(open(out)))[1:], dtype=float)
+    assert rows.shape == (4, 6)
+    X, y, dY = O.sample_test_function("franke", 300, 0)
+    ys = np.sqrt(np.mean((y - y.mean()) ** 2))
+    y, dY = (y - y.mean()) / ys, dY / ys
+    b = O.stacked_targets(y, dY, y.mean())
+    for r in rows:
+        ell, sigma = r[0], r[1]
+        op = O.DskiOperator(O.KernelSpec(ell, 1.0), O.Grid.cover(X, 0.25 * ell, 3, 64), X, (sigma, sigma))
+        plain = O.cg(op, b, 1e-4, 400)
+        nd = op.noise_diagonal()
+        f = O.pivoted_cholesky(op, 30, noise_diag=nd)
+        pre = O.cg(op, b, 1e-4, 400, O.Preconditioner(f.L, nd))
+        # CG counts at hundreds of iterations move under roundoff (test_gpu_solvers.oracle_iteration_band)
+        for its, conv, ref in ((r[2], r[3], plain), (r[4], r[5], pre)):
+            assert abs(its - ref.iterations) <= max(2, 0.02 * ref.iterations), (ell, sigma, its, ref.iterations)
+            if abs(ref.iterations - 400) > 10:
+                assert bool(conv) == ref.converged
+
+
+@pytest.mark.parametrize("backend", ["dski", "dskip", "exact"])
+def test_cli_benchmark_mvm(tmp_path, backend):
+    out = str(tmp_path / "bench.csv")
+    assert cli.main(["benchmark-mvm", "--backend", backend, "--sizes", "500,1000", "--reps", "3", "--rank", "40",
+                     "--out", out]) == 0
+    rows = list(csv.reader(open(out)))
+    assert rows[0] == ["n", "N", "seconds"]
+    assert [(int(float(r[0])), int(float(r[1]))) for r in rows[1:]] == [(500, 1500), (1000, 3000)]
+    assert all(float(r[2]) > 0 for r in rows[1:])
+
+
+def test_benchmark_operator_is_the_reference_one():
+    """cmd_benchmark_mvm.cpp:55-63: SE(0.4, 1) D-SKI on the fixed [−0.25, 1.25]
+    grid with noise 0.1 — one MVM against the oracle's ≤1e-12."""
+    X = cli.bench_points(800, 2, 0)
+    op = cli.bench_operator("dski", X, 32, 100, 0)
+    ref = O.DskiOperator(O.KernelSpec(0.4, 1.0), O.Grid([32, 32], [-0.25, -0.25], [1.5 / 31] * 2), X, (0.1, 0.1))
+    v = gk.gaussian_vector(op.size(), 7)
+    want = ref.mvm(v)
+    assert np.linalg.norm(op.mvm(v) - want) <= 1e-12 * np.linalg.norm(want)

@@ -48,6 +48,33 @@ __device__ __forceinline__ void grid_sync(unsigned long long* bar) {
   __syncthreads();
 }
 
+// The same barrier split in two: grid_arrive (every thread calls it; thread
+// 0 returns the generation target) and grid_wait(bar, target) (every thread
+// calls it with thread 0's target). Work placed between the two overlaps the
+// wait for the other CTAs — the one-launch MVM warms its next phase's
+// instruction stream there.
+__device__ __forceinline__ unsigned long long grid_arrive(unsigned long long* bar) {
+  __syncthreads();
+  unsigned long long target = 0;
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;\n" : "=l"(t) : "l"(bar) : "memory");
+    const unsigned long long nb = gridDim.x;
+    target = (t / nb + 1) * nb;
+  }
+  return target;
+}
+__device__ __forceinline__ void grid_wait(unsigned long long* bar, unsigned long long target) {
+  if (threadIdx.x == 0) {
+    unsigned spins = 0;
+    while (ld_relaxed(bar) < target) {
+      if (++spins > (1u << 28)) __trap();
+      if (kBarrierSleepNs) __nanosleep(kBarrierSleepNs);
+    }
+    asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+  }
+  __syncthreads();
+}
 
 }  // namespace gk
 

@@ -73,7 +73,7 @@ struct F2Args {
   int t_split;
   int m0p, m1p;
   int skip;
-  int g_wide;          // direct gather with 4 or 8 RHS per task (0: RP per task)
+  int t_wide;          // Toeplitz phases: 16-column items where the layout allows
   int warm;            // instruction warm-up passes inside the split barriers (1 T, 2/4 G at barrier 2/3)
   int s_mode, g_mode;  // 0: staged rolling kernels, 1: direct-load high-parallelism variants
   int s_nbuf;          // direct scatter: number of partial grid buffers S
@@ -452,10 +452,13 @@ __device__ __noinline__ void f2_sum_partials(const HaloSpec& halo, int M, int Q,
 
 // dry = true: instruction warm-up only (run inside a split grid barrier):
 // one item, no global loads or stores, two warps through the DMMA loops.
+// wide = true: 16-column items (two n-tiles per staged slab) where the
+// layout allows it, so a 400-group phase fits 296 CTAs in one round.
 __device__ __noinline__ void f2_toeplitz(const double* ts, int M, int Mp, int band, int P, int Q, const double* X,
-                            HaloSpec halo, double* Y, double* sm, int nsplit, bool dry = false) {
+                            HaloSpec halo, double* Y, double* sm, int nsplit, bool dry = false, bool wide = false) {
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32, g = lane / 4, t4 = lane % 4;
-  const int ncols = P * Q, cgroups = (ncols + 7) / 8, items = cgroups * nsplit;
+  const int CW = (wide && halo.mode != 2 && Q % 16 == 0) ? 16 : 8;  // columns per item
+  const int ncols = P * Q, cgroups = (ncols + CW - 1) / CW, items = cgroups * nsplit;
   const int mtiles = Mp / 8, kq = Mp / 4;
   // diagonals D = 2mt - kk/4 the band-limited k loops can touch (the union
   // range of a warp's two tiles 8 m-tiles apart adds at most 16 + 2)
@@ -463,10 +466,10 @@ __device__ __noinline__ void f2_toeplitz(const double* ts, int M, int Mp, int ba
   const int Dlo = max(-(kq - 1), -Dmax), Dhi = min(2 * (mtiles - 1), Dmax);
   const int ND = Dhi - Dlo + 1;
   double* F = sm;                          // [ND][32], row D - Dlo
-  double* Bs0 = F + ND * 32;               // [Mp][8]
-  double* Bs1 = Bs0 + Mp * 8;
-  double* Hs0 = Bs1 + Mp * 8;              // [Mp][8] halo staging, one per B buffer
-  double* Hs1 = Hs0 + Mp * 8;
+  double* Bs0 = F + ND * 32;               // [Mp][CW]
+  double* Bs1 = Bs0 + Mp * CW;
+  double* Hs0 = Bs1 + Mp * CW;             // [Mp][CW] halo staging, one per B buffer
+  double* Hs1 = Hs0 + Mp * CW;
   const bool contiguous = (Q % 8) == 0;
   cpa_wait0();  // this thread's copies of the Toeplitz sequences (f2_body)
   __syncthreads();
@@ -476,26 +479,27 @@ __device__ __noinline__ void f2_toeplitz(const double* ts, int M, int Mp, int ba
     x = x < 0 ? -x : x;
     F[e] = x < M ? ts[x] : 0.0;
   }
-  for (int e = tid; e < (Mp - M) * 8; e += F2_THREADS) {  // padding rows stay zero
-    Bs0[M * 8 + e] = 0.0;
-    Bs1[M * 8 + e] = 0.0;
+  for (int e = tid; e < (Mp - M) * CW; e += F2_THREADS) {  // padding rows stay zero
+    Bs0[M * CW + e] = 0.0;
+    Bs1[M * CW + e] = 0.0;
   }
+  const int lg = CW == 16 ? 3 : 2;  // log2 of the 16-byte copies per row
   auto issue = [&](int cg, double* B, double* Hs) {
-    const int col0 = cg * 8;
+    const int col0 = cg * CW;
     if (halo.mode == 2) {
       f2_sum_partials(halo, M, Q, ncols, col0, B);
     } else if (contiguous) {
       const int p = col0 / Q, q = col0 - p * Q;
       const double* src = X + (size_t)p * M * Q + q;
-      for (int e = tid; e < M * 4; e += F2_THREADS) {
-        const int c = e >> 2, k = e & 3;
-        cpa16(B + c * 8 + 2 * k, src + (size_t)c * Q + 2 * k);
+      for (int e = tid; e < (M << lg); e += F2_THREADS) {
+        const int c = e >> lg, k = e & ((1 << lg) - 1);
+        cpa16(B + c * CW + 2 * k, src + (size_t)c * Q + 2 * k);
       }
       if (halo.row(p)) {
         const double* hs = halo.h + (size_t)p * M * Q + q;
-        for (int e = tid; e < M * 4; e += F2_THREADS) {
-          const int c = e >> 2, k = e & 3;
-          cpa16(Hs + c * 8 + 2 * k, hs + (size_t)c * Q + 2 * k);
+        for (int e = tid; e < (M << lg); e += F2_THREADS) {
+          const int c = e >> lg, k = e & ((1 << lg) - 1);
+          cpa16(Hs + c * CW + 2 * k, hs + (size_t)c * Q + 2 * k);
         }
       }
     } else {
@@ -546,7 +550,7 @@ __device__ __noinline__ void f2_toeplitz(const double* ts, int M, int Mp, int ba
     } else {
       cpa_wait0();
     }
-    const int col0 = cg * 8;
+    const int col0 = cg * CW;
     // one division per item: (p, q) of the first column and the output base
     const int p0 = col0 / Q, q0 = col0 - p0 * Q;
     double* const Yb = Y + (size_t)p0 * M * Q + q0;
@@ -555,16 +559,17 @@ __device__ __noinline__ void f2_toeplitz(const double* ts, int M, int Mp, int ba
     double* B = buf ? Bs1 : Bs0;
     const double* Hs = buf ? Hs1 : Hs0;
     if (hrow) {  // u + h for the halo rows
-      for (int e = tid; e < M * 8; e += F2_THREADS) B[e] += Hs[e];
+      for (int e = tid; e < M * CW; e += F2_THREADS) B[e] += Hs[e];
       __syncthreads();
     }
     const int mt_lo = sp * per, mt_hi = min(mtiles, mt_lo + per);
     constexpr int NW = F2_THREADS / 32;
+    int nt = 0;  // n-tile of the item (CW = 16: two)
     auto store = [&](int mt, double r0, double r1) {
       const int ar = mt * 8 + g;
       if (dry || ar >= M) return;
       if (contiguous) {
-        *reinterpret_cast<double2*>(Yb + (size_t)ar * Q + 2 * t4) = make_double2(r0, r1);
+        *reinterpret_cast<double2*>(Yb + (size_t)ar * Q + nt * 8 + 2 * t4) = make_double2(r0, r1);
       } else {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
@@ -579,6 +584,7 @@ __device__ __noinline__ void f2_toeplitz(const double* ts, int M, int Mp, int ba
     // each warp runs up to two m-tiles in one k loop (4 independent DMMA
     // chains, B fragment shared); k steps outside a tile's numerical band
     // only add the tiny exact Toeplitz terms, so the union range is used
+    for (nt = 0; nt < CW / 8; ++nt)
     for (int mt0 = mt_lo + warp; mt0 < mt_hi && (!dry || warp == 0 || warp == NW - 1); mt0 += 2 * NW) {
       const int mt1 = mt0 + NW;
       const bool two = mt1 < mt_hi;
@@ -589,13 +595,13 @@ __device__ __noinline__ void f2_toeplitz(const double* ts, int M, int Mp, int ba
       double y00 = 0.0, y01 = 0.0, y10 = 0.0, y11 = 0.0;  // tile 1
       const double* F0 = F + (2 * mt0 - Dlo) * 32 + lane;
       const double* F1 = F + (2 * mt1 - Dlo) * 32 + lane;
-      const double* Bp = B + t4 * 8 + g;
+      const double* Bp = B + t4 * CW + g + nt * 8;
       int kk = k_lo;
       if (two) {
 #pragma unroll 2
         for (; kk + 8 <= k_hi; kk += 8) {
           const int j = kk >> 2;
-          const double b0 = Bp[kk * 8], b1 = Bp[(kk + 4) * 8];
+          const double b0 = Bp[kk * CW], b1 = Bp[(kk + 4) * CW];
           const double f00 = F0[-j * 32], f01 = F0[-(j + 1) * 32];
           const double f10 = F1[-j * 32], f11 = F1[-(j + 1) * 32];
           dmma(x00, x01, f00, b0);
@@ -605,7 +611,7 @@ __device__ __noinline__ void f2_toeplitz(const double* ts, int M, int Mp, int ba
         }
         if (kk < k_hi) {
           const int j = kk >> 2;
-          const double b0 = Bp[kk * 8];
+          const double b0 = Bp[kk * CW];
           dmma(x00, x01, F0[-j * 32], b0);
           dmma(y00, y01, F1[-j * 32], b0);
         }
@@ -615,11 +621,11 @@ __device__ __noinline__ void f2_toeplitz(const double* ts, int M, int Mp, int ba
 #pragma unroll 2
         for (; kk + 8 <= k_hi; kk += 8) {
           const int j = kk >> 2;
-          const double b0 = Bp[kk * 8], b1 = Bp[(kk + 4) * 8];
+          const double b0 = Bp[kk * CW], b1 = Bp[(kk + 4) * CW];
           dmma(x00, x01, F0[-j * 32], b0);
           dmma(x10, x11, F0[-(j + 1) * 32], b1);
         }
-        if (kk < k_hi) dmma(x00, x01, F0[-(kk >> 2) * 32], Bp[kk * 8]);
+        if (kk < k_hi) dmma(x00, x01, F0[-(kk >> 2) * 32], Bp[kk * CW]);
         store(mt0, x00 + x10, x01 + x11);
       }
     }
@@ -780,74 +786,6 @@ __device__ void f2_gather_direct(const F2Args& a, bool dry = false) {
     vstore<RP>(a.out + idx, o0);
     vstore<RP>(a.out + idx + gstride, o1);
     vstore<RP>(a.out + idx + 2 * gstride, o2);
-  }
-}
-
-// The same gather with GR right-hand sides per task (GR = 4, 8; nrhs % GR
-// == 0): fewer, wider tasks, so every thread runs at most one round at C2
-// (n·nrhs/GR tasks ≤ grid threads) instead of 2–3 rounds of RHS pairs.
-template <int T, int GR>
-__device__ void f2_gather_wide(const F2Args& a) {
-  const size_t gstride = (size_t)a.n * a.nrhs;
-  const size_t rstride = (size_t)a.m1 * a.nrhs;
-  const int per = a.nrhs / GR;
-  const int ntask = a.n * per;
-  for (int task = blockIdx.x * F2_THREADS + threadIdx.x; task < ntask; task += gridDim.x * F2_THREADS) {
-    const int s = task / per;
-    const int rb = (task - s * per) * GR;
-    const int4 bs = __ldg(a.base + s);
-    const double2* wr = a.wd + (size_t)s * 2 * T;
-    double2 w1[T];
-#pragma unroll
-    for (int t1 = 0; t1 < T; ++t1) w1[t1] = __ldg(wr + T + t1);
-    const double* wb = a.w + ((size_t)bs.x * a.m1 + bs.y) * a.nrhs + rb;
-    double o0[GR], o1[GR], o2[GR];
-#pragma unroll
-    for (int k = 0; k < GR; ++k) o0[k] = o1[k] = o2[k] = 0.0;
-#pragma unroll
-    for (int t0 = 0; t0 < T; ++t0) {
-      const double* rr = wb + (size_t)t0 * rstride;
-      double r[GR], q[GR];
-#pragma unroll
-      for (int k = 0; k < GR; ++k) r[k] = q[k] = 0.0;
-#pragma unroll
-      for (int t1 = 0; t1 < T; ++t1) {
-        double x[GR];
-#pragma unroll
-        for (int k = 0; k < GR; k += 2) {
-          const double2 xx = __ldcg(reinterpret_cast<const double2*>(rr + (size_t)t1 * a.nrhs + k));
-          x[k] = xx.x;
-          x[k + 1] = xx.y;
-        }
-#pragma unroll
-        for (int k = 0; k < GR; ++k) {
-          r[k] = fma(w1[t1].x, x[k], r[k]);
-          q[k] = fma(w1[t1].y, x[k], q[k]);
-        }
-      }
-      const double2 w0 = __ldg(wr + t0);
-#pragma unroll
-      for (int k = 0; k < GR; ++k) {
-        o0[k] = fma(w0.x, r[k], o0[k]);
-        o1[k] = fma(w0.y, r[k], o1[k]);
-        o2[k] = fma(w0.x, q[k], o2[k]);
-      }
-    }
-    const size_t idx = (size_t)s * a.nrhs + rb;
-#pragma unroll
-    for (int k = 0; k < GR; k += 2) {
-      double2 n0 = make_double2(0.0, 0.0), n1 = n0, n2 = n0;
-      if (a.noise) {
-        n0 = __ldg(reinterpret_cast<const double2*>(a.v + idx + k));
-        n1 = __ldg(reinterpret_cast<const double2*>(a.v + idx + gstride + k));
-        n2 = __ldg(reinterpret_cast<const double2*>(a.v + idx + 2 * gstride + k));
-      }
-      *reinterpret_cast<double2*>(a.out + idx + k) = make_double2(fma(a.nv2, n0.x, o0[k]), fma(a.nv2, n0.y, o0[k + 1]));
-      *reinterpret_cast<double2*>(a.out + idx + gstride + k) =
-          make_double2(fma(a.ng2, n1.x, o1[k]), fma(a.ng2, n1.y, o1[k + 1]));
-      *reinterpret_cast<double2*>(a.out + idx + 2 * gstride + k) =
-          make_double2(fma(a.ng2, n2.x, o2[k]), fma(a.ng2, n2.y, o2[k + 1]));
-    }
   }
 }
 
@@ -1012,11 +950,12 @@ __device__ __forceinline__ void f2_body(const F2Args& a) {
   // before it overlaps that fetch with the wait for the other CTAs.
   {
     const unsigned long long tgt = grid_arrive(a.bar);
-    if (a.warm & 1) f2_toeplitz(ts1, a.m1, a.m1p, a.band1, a.m0, a.nrhs, a.u, hs1, a.y1, work, a.t_split, true);
+    if (a.warm & 1)
+      f2_toeplitz(ts1, a.m1, a.m1p, a.band1, a.m0, a.nrhs, a.u, hs1, a.y1, work, a.t_split, true, a.t_wide);
     grid_wait(a.bar, tgt);
   }
   stamp(a, 2);
-  if (!(a.skip & 2)) f2_toeplitz(ts1, a.m1, a.m1p, a.band1, a.m0, a.nrhs, a.u, hs1, a.y1, work, a.t_split);
+  if (!(a.skip & 2)) f2_toeplitz(ts1, a.m1, a.m1p, a.band1, a.m0, a.nrhs, a.u, hs1, a.y1, work, a.t_split, false, a.t_wide);
   stamp(a, 3);
   {
     const unsigned long long tgt = grid_arrive(a.bar);
@@ -1024,8 +963,9 @@ __device__ __forceinline__ void f2_body(const F2Args& a) {
     grid_wait(a.bar, tgt);
   }
   stamp(a, 4);
-  if (!(a.skip & 4)) f2_toeplitz(ts0, a.m0, a.m0p, a.band0, 1, a.m1 * a.nrhs, a.y1, HaloSpec{0, nullptr, 0, 1, 0, T, 1}, a.w, work,
-              a.t_split);
+  if (!(a.skip & 4))
+    f2_toeplitz(ts0, a.m0, a.m0p, a.band0, 1, a.m1 * a.nrhs, a.y1, HaloSpec{0, nullptr, 0, 1, 0, T, 1}, a.w, work,
+                a.t_split, false, a.t_wide);
   stamp(a, 5);
   {
     const unsigned long long tgt = grid_arrive(a.bar);
@@ -1034,13 +974,8 @@ __device__ __forceinline__ void f2_body(const F2Args& a) {
   }
   stamp(a, 6);
   if (!(a.skip & 8)) {
-    if (a.g_mode == 1) {
-      if (a.g_wide == 4) f2_gather_wide<T, 4>(a);
-      else if (a.g_wide == 8) f2_gather_wide<T, 8>(a);
-      else f2_gather_direct<T, RP>(a);
-    } else {
-      f2_gather<T, RP>(a, work);
-    }
+    if (a.g_mode == 1) f2_gather_direct<T, RP>(a);
+    else f2_gather<T, RP>(a, work);
   }
   cpa_wait0();  // nothing in flight into shared memory past the body (skip masks)
   __syncthreads();
@@ -1078,11 +1013,12 @@ size_t smem_bytes(const Fused2dGeom& g, const Fused2dPlan& p) {
                    size_t(p.s_nst) * p.s_pmax * 16 +
                    size_t(p.s_L * p.s_csw) * 4 + 16 +
                    size_t(p.s_nspl - 1) * (T - 1) * p.s_TC * p.BR * 8;
+  const size_t cw = p.t_wide ? 16 : 8;
   auto tbytes = [&](int M, int band, bool halo) {
     const int Mp = (M + 7) / 8 * 8, mtiles = Mp / 8, kq = Mp / 4;
     const int Dmax = (band + 11) / 4 + 18;
     const int ND = std::min(2 * (mtiles - 1), Dmax) - std::max(-(kq - 1), -Dmax) + 1;
-    return size_t(ND) * 32 * 8 + size_t(halo ? 4 : 2) * Mp * 8 * 8;
+    return size_t(ND) * 32 * 8 + size_t(halo ? 4 : 2) * Mp * cw * 8;
   };
   const bool halo1 = p.s_mode == 0 && p.nrhs % 8 == 0;  // mode-1 staging adds u + h slabs
   const size_t Tp = std::max(tbytes(g.m1, g.band1, halo1), tbytes(g.m0, g.band0, false));
@@ -1157,6 +1093,11 @@ void decompose(const Fused2dGeom& g, const std::vector<int>& cs, Fused2dPlan& p,
   const int mt = (std::max(g.m0, g.m1) + 7) / 8;
   p.t_split = cg >= ctas / 2 ? 1 : int(std::max<i64>(2, std::min<i64>(mt / 2, ctas / cg)));
   if (const int o = g_tuning.f2_tsplit.load(); o > 0) p.t_split = o;
+  // 16-column items (one round for C2's 400 groups on 296 CTAs) measured
+  // slower: 51.2 vs 49.2 µs at C2 32 RHS — an item's DMMA time doubles
+  // (~1.4 µs per 8 columns per SM pair), more than the second round costs.
+  // Off unless requested (tuning key f2_twide).
+  p.t_wide = g_tuning.f2_twide.load() == 1 && p.nrhs % 16 == 0;
 }
 
 template <int T, int RP, int MINB>
@@ -1270,8 +1211,7 @@ static F2Args fused2d_args(const Fused2dGeom& g, Fused2dPlan& p, const double* v
   a.t_split = p.t_split;
   a.skip = g_tuning.f2_skip.load();
   a.warm = g_tuning.f2_warm.load() >= 0 ? g_tuning.f2_warm.load() : 1;
-  a.g_wide = 0;
-  if (const int gw = g_tuning.f2_gwide.load(); gw > 0 && (gw == 4 || gw == 8) && p.nrhs % gw == 0) a.g_wide = gw;
+  a.t_wide = p.t_wide;
   a.s_mode = p.s_mode;
   a.g_mode = p.g_mode;
   a.s_nbuf = p.s_nbuf;

@@ -33,6 +33,7 @@ struct Fused2dPlan {
   int s_TC = 0, s_strips = 0, s_L = 0, s_segs = 0, s_pmax = 0, s_csw = 0;
   int g_TC = 0, g_strips = 0, g_L = 0, g_segs = 0, g_pmax = 0, g_nw = 0;
   int t_split = 1;
+  int t_wide = 0;  // Toeplitz phases: 16-column items
   int s_mode = 0, g_mode = 0;  // 0 staged rolling, 1 direct-load variants
   int s_nspl = 2;
   int s_nst = 3;                // staged scatter: cell rows in flight              // staged scatter: threads splitting one column's points

@@ -8,6 +8,9 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1810_12283_b200 as gk  # noqa: E402
 
+for kv in filter(None, os.environ.get("GK_TUNE", "").split(",")):
+    k, v = kv.split("=")
+    gk.set_tuning(k, int(v))
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 nrhs = int(sys.argv[2]) if len(sys.argv) > 2 else 17
 X, y, dY = gk.make_dataset(cfg, 0)

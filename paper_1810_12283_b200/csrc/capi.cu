@@ -222,7 +222,6 @@ int gk_set_tuning(const char* key, int value) {
                            : k == "f2_skip" ? &g_tuning.f2_skip
                            : k == "f2_warm" ? &g_tuning.f2_warm
                            : k == "f2_twide" ? &g_tuning.f2_twide
-                           : k == "s3merge" ? &g_tuning.s3merge
                            : k == "f2_grid" ? &g_tuning.f2_grid
                            : k == "f2_rp" ? &g_tuning.f2_rp
                            : k == "f2_smode" ? &g_tuning.f2_smode

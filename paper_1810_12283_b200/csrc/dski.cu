@@ -1465,8 +1465,6 @@ struct DskiOp final : Op {
   DevBuf<long long> s3_uoff;
   DevBuf<int> s3_cstart, s3_cseg;
   DevBuf<int2> s3_cent;
-  DevBuf<int> s3_sstart;  // flattened merge table: per (column, z segment) entry ranges
-  DevBuf<int4> s3_sent;   // {scratch node at the segment's first z, first, end offset in 0..8}
   long long s3_nodes = 0;
   int s3_nzs = 0;
   // tile scatter (k_scatter_tile3): per TB×TB tile of node columns the points
@@ -1893,42 +1891,6 @@ __global__ void __launch_bounds__(256) k_scatter_merge3(int ncol, int m2, int nz
   }
 }
 
-// The same merge over a flattened table: per (node column, z segment) the
-// covering blocks in the same (za, unit) order as {scratch node of the
-// segment's first z, first and end covered offset}: one table load per
-// entry instead of the entry → unit → offset chain and no skipped entries.
-// Bit-identical to k_scatter_merge3 (same summation order per node);
-// measured 140 vs 146 µs for the C3 17-RHS scatter (push + merge). (Taking
-// 2 or 4 entries per step with every load issued up front was slower: 150
-// and 164 µs — the kernel is issue-bound, ~45 % issue-active, not
-// latency-bound.)
-__global__ void __launch_bounds__(256) k_scatter_merge3f(int ncol, int m2, int nzs, const int* __restrict__ sstart,
-                                                        const int4* __restrict__ sent,
-                                                        const double* __restrict__ scratch, double* __restrict__ u,
-                                                        int nrhs) {
-  const i64 ntask = (i64)ncol * nzs * nrhs;
-  for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < ntask; t += (i64)gridDim.x * blockDim.x) {
-    const int r = int(t % nrhs);
-    const i64 cz = t / nrhs;
-    const int zs = int(cz % nzs), col = int(cz / nzs);
-    const int z0 = zs * 8;
-    double acc[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) acc[k] = 0.0;
-    const int e1 = __ldg(sstart + cz + 1);
-    for (int e = __ldg(sstart + cz); e < e1; ++e) {
-      const int4 A = __ldg(sent + e);
-      const double* sa = scratch + (i64)A.x * nrhs + r;
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (k >= A.y && k < A.z) acc[k] += __ldcg(sa + (i64)k * nrhs);
-    }
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (z0 + k < m2) u[((size_t)col * m2 + z0 + k) * nrhs + r] = acc[k];
-  }
-}
-
 // Lean-kernel launch shape: x = RHS lanes (≤ 32), y = items per block, shrunk
 // (down to one warp) when there are too few items to give every SM ~4 CTAs.
 static dim3 lean_block(int nrhs, i64 items) {
@@ -2031,13 +1993,9 @@ void DskiOp::scatter(const double* v, double* u, int nrhs, cudaStream_t s) const
     else k_scatter_upush3<4, true><<<gp, S3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, s3_uoff.p, v, s3_scratch.p, nrhs);
     launched("dski scatter (d=3 unit push)");
     const int ncol = m[0] * m[1];
-    if (g_tuning.s3merge.load() == 1 || !s3_sent.p)
-      k_scatter_merge3<<<grid_blocks(i64(ncol) * s3_nzs * nrhs), 256, 0, s>>>(ncol, m[2], s3_nzs, T, s3_cstart.p, s3_cent.p,
-                                                                            s3_cseg.p, g3_units.p, s3_uoff.p,
-                                                                            s3_scratch.p, u, nrhs);
-    else
-      k_scatter_merge3f<<<grid_blocks(i64(ncol) * s3_nzs * nrhs), 256, 0, s>>>(ncol, m[2], s3_nzs, s3_sstart.p,
-                                                                             s3_sent.p, s3_scratch.p, u, nrhs);
+    k_scatter_merge3<<<grid_blocks(i64(ncol) * s3_nzs * nrhs), 256, 0, s>>>(ncol, m[2], s3_nzs, T, s3_cstart.p, s3_cent.p,
+                                                                          s3_cseg.p, g3_units.p, s3_uoff.p,
+                                                                          s3_scratch.p, u, nrhs);
     launched("dski scatter (d=3 unit merge)");
     return;
   }
@@ -2531,38 +2489,6 @@ std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, cons
       cent.insert(cent.end(), L.begin(), L.end());
     }
     cst[static_cast<size_t>(ncol)] = int(cent.size());
-    // flattened per-segment table for k_scatter_merge3f (same entry order)
-    std::vector<int> sst(static_cast<size_t>(ncol) * nzs + 1, 0);
-    std::vector<int4> sent;
-    bool fits = tot < (1LL << 31) - 64;
-    for (int c = 0; c < ncol && fits; ++c)
-      for (int zs = 0; zs < nzs; ++zs) {
-        const int z0 = zs * 8;
-        sst[static_cast<size_t>(c) * nzs + zs] = int(sent.size());
-        for (int e = cseg[static_cast<size_t>(c) * nzs + zs]; e < cst[static_cast<size_t>(c) + 1]; ++e) {
-          const int2 en = cent[static_cast<size_t>(e)];
-          const int4 U = gu[static_cast<size_t>(en.x)];
-          const int za = U.z, nzb = U.w - U.z + T - 1;
-          if (za >= z0 + 8) break;
-          if (za + nzb <= z0) continue;
-          const long long node = uoff[static_cast<size_t>(en.x)] + static_cast<long long>(en.y) * nzb + (z0 - za);
-          sent.push_back(make_int4(int(node), std::max(0, za - z0), std::min(8, za + nzb - z0), 0));
-        }
-      }
-    sst[static_cast<size_t>(ncol) * nzs] = int(sent.size());
-    if (std::getenv("GK_S3_STATS")) {
-      std::vector<int> cnt(static_cast<size_t>(ncol) * nzs);
-      for (size_t i = 0; i < cnt.size(); ++i) cnt[i] = sst[i + 1] - sst[i];
-      std::vector<int> srt = cnt;
-      std::sort(srt.begin(), srt.end());
-      std::fprintf(stderr, "[s3] units %zu scratch nodes %lld entries %zu segs %zu: mean %.2f p50 %d p90 %d p99 %d max %d\n",
-                   gu.size(), tot, sent.size(), cnt.size(), double(sent.size()) / cnt.size(), srt[srt.size() / 2],
-                   srt[srt.size() * 9 / 10], srt[srt.size() * 99 / 100], srt.back());
-    }
-    if (fits) {
-      op->s3_sstart.upload(sst.data(), sst.size(), op->stream);
-      op->s3_sent.upload(sent.data(), std::max<size_t>(sent.size(), 1), op->stream);
-    }
     op->s3_nodes = tot;
     op->s3_nzs = nzs;
     op->s3_uoff.upload(uoff.data(), uoff.size(), op->stream);

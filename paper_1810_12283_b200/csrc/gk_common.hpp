@@ -42,7 +42,6 @@ struct Tuning {
   std::atomic<int> lean{0};  // lean one-launch 2-D MVM (lean2d.cu): 0 measured policy, 1 never, 2 always
   // fused 2-D MVM decomposition overrides (0 = heuristic)
   std::atomic<int> f2_stc{0}, f2_sl{0}, f2_gtc{0}, f2_gl{0}, f2_tsplit{0}, f2_per_sm{0};
-  std::atomic<int> s3merge{0};  // d = 3 unit-push merge: 0 flattened table, 1 entry chain
   std::atomic<int> f2_twide{-1};  // one-launch 2-D MVM Toeplitz 16-column items (-1 auto, 0 off, 1 on)  // one-launch 2-D MVM direct gather: RHS per task (4, 8; 0 = plan's RP)
   std::atomic<int> f2_warm{-1};  // one-launch 2-D MVM warm-up passes (bitmask; -1 = default)
   std::atomic<int> f2_skip{0};  // debug: bitmask of phases to skip (1 S, 2 T1, 4 T0, 8 G)

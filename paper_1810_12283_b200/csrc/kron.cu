@@ -399,7 +399,16 @@ void toeplitz_mode(const double* t, int M, int band, i64 P, i64 Q, const double*
     else launch_toeplitz<2, 2>(t, M, band, P, Q, X, Y, s);
     return;
   }
-  if (variant == 0 || variant == 3) {  // DMMA, smallest tile (most CTAs): best measured at C1-C4 sizes
+  if ((variant == 0 || variant == 5) && M > 32 && M <= 64) {
+    // one row block covering every row (no half-empty second block): C3's
+    // 48-node axes 60.4 -> 48.1 µs for K_UU at 17 RHS (bit-identical: the
+    // same k order per output)
+    const bool wide = ctas(64, 64) >= 192;
+    if (M <= 48) { if (wide) launch_toeplitz_dmma<3, 4>(t, M, band, P, Q, X, Y, s); else launch_toeplitz_dmma<3, 2>(t, M, band, P, Q, X, Y, s); }
+    else { if (wide) launch_toeplitz_dmma<4, 4>(t, M, band, P, Q, X, Y, s); else launch_toeplitz_dmma<4, 2>(t, M, band, P, Q, X, Y, s); }
+    return;
+  }
+  if (variant == 0 || variant == 3 || variant == 5) {  // DMMA, smallest tile (most CTAs): best measured at C1-C4 sizes
     launch_toeplitz_dmma<2, 2>(t, M, band, P, Q, X, Y, s);
     return;
   }

@@ -251,9 +251,10 @@ void gk_pivchol_destroy(gk_pivchol* f);
 /* Preconditioner(F, noise_diag) (linalg.cpp:176-213): M^{-1}b =
  * D^{-1/2}(c - Q1 Q1^T c), c = D^{-1/2} b, Q1 from a QR of [D^{-1/2}F; I]
  * (CholeskyQR2 on the device; agrees with the reference's Householder Q1 to
- * ≤1e-10 at C4's rank 200, tests/test_gpu_fullsize_parity.py). Limit: rank
- * k ≤ 512 (GK_ERR_UNSUPPORTED above; the reference has none — larger ranks
- * would need a blocked Gram/solve, no BASELINE config asks for one). */
+ * ≤1e-10 at C4's rank 200, tests/test_gpu_fullsize_parity.py). Any rank:
+ * ranks whose projection does not fit shared memory run it in k-column tiles
+ * and the apply as S = Q1 T plus a finishing pass (the k×k Cholesky of the
+ * Gram matrix runs on the host in long double, O(k³)). */
 gk_status gk_precond_create(const double* F, int64_t N, int64_t k, const double* noise_diag,
                             int device, gk_precond** out);
 /* From a device-resident pivoted Cholesky factor, with D = op noise diagonal

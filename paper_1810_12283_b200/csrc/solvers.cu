@@ -235,8 +235,9 @@ __global__ void k_fill(double* __restrict__ a, double v, i64 n) {
 // (for quadratic()). Rows are staged 16 at a time in shared memory; outputs
 // o = j*nrhs + b are owned by one thread each and accumulate in smem.
 constexpr int PC_RT = 16;
+// q1 may be a column slice [j0, j0 + k) of the [N][ld] factor (ld = row stride).
 __global__ void k_pc_proj(const double* __restrict__ Rv, const double* __restrict__ dinv,
-                          const double* __restrict__ q1, i64 N, int k, int nrhs, double* __restrict__ partial,
+                          const double* __restrict__ q1, i64 N, int k, int ld, int nrhs, double* __restrict__ partial,
                           double* __restrict__ partial_cc) {
   extern __shared__ double sh[];
   double* qs = sh;                     // [PC_RT][k]
@@ -251,7 +252,7 @@ __global__ void k_pc_proj(const double* __restrict__ Rv, const double* __restric
   for (i64 rt = r0; rt < r1; rt += PC_RT) {
     const int nr = int((r1 - rt) < PC_RT ? (r1 - rt) : PC_RT);
     __syncthreads();
-    for (int e = tid; e < nr * k; e += blockDim.x) qs[e] = q1[rt * k + e];
+    for (int e = tid; e < nr * k; e += blockDim.x) qs[e] = q1[(rt + e / k) * ld + e % k];
     for (int e = tid; e < nr * nrhs; e += blockDim.x) {
       const int rr = e / nrhs;
       cs[e] = dinv[rt + rr] * Rv[(rt + rr) * nrhs + (e % nrhs)];
@@ -302,6 +303,29 @@ __global__ void k_pc_apply(const double* __restrict__ Rv, const double* __restri
       const double* qr = q1 + r * k;
       for (int j = 0; j < k; ++j) s += qr[j] * Ts[j * nrhs + b];
       const double z = di * (di * rv - s);
+      Z[r * nrhs + b] = z;
+      acc += rv * z;
+    }
+  }
+  if (partial_rz) block_col_store(acc, nrhs, partial_rz, sm);
+}
+
+// z = dinv (dinv r − S) for a precomputed S = Q1 T (large ranks); partial Σ r·z
+// in k_pc_apply's layout.
+__global__ void k_pc_finish_s(const double* __restrict__ Rv, const double* __restrict__ dinv,
+                              const double* __restrict__ S, i64 N, int nrhs, double* __restrict__ Z,
+                              double* __restrict__ partial_rz) {
+  __shared__ double sm[kRedThreads];
+  const int slots = blockDim.x / nrhs;
+  const int b = threadIdx.x % nrhs, slot = threadIdx.x / nrhs;
+  double acc = 0.0;
+  if (slot < slots) {
+    i64 r0, r1;
+    row_range(N, r0, r1);
+    for (i64 r = r0 + slot; r < r1; r += slots) {
+      const double di = dinv[r];
+      const double rv = Rv[r * nrhs + b];
+      const double z = di * (di * rv - S[r * nrhs + b]);
       Z[r * nrhs + b] = z;
       acc += rv * z;
     }
@@ -1748,6 +1772,47 @@ static void set_smem(const void* fn, size_t bytes) {
     raise_smem_limit(fn, bytes);
 }
 
+// Ranks whose k_pc_proj staging (or k_pc_apply's T copy) does not fit
+// shared memory run the projection in k-column tiles and the apply as
+// S = Q1 T (rows_gemm) followed by k_pc_finish_s — no rank limit (the
+// reference Preconditioner has none, linalg.cpp:176-213).
+constexpr size_t kPcSmem = 200 * 1024;
+static size_t pc_proj_smem(i64 kt, int nrhs) { return sizeof(double) * size_t(PC_RT * kt + PC_RT * nrhs + kt * nrhs); }
+static int pc_proj_tile(i64 k, int nrhs) {
+  const i64 t = (i64(kPcSmem / sizeof(double)) - PC_RT * nrhs) / (PC_RT + nrhs);
+  return int(std::max<i64>(1, std::min<i64>(k, t)));
+}
+static bool pc_big(i64 k, int nrhs) {
+  return pc_proj_smem(k, nrhs) > kPcSmem || sizeof(double) * size_t(k * nrhs + RT) > kPcSmem;
+}
+// T[k][nrhs] = Q1ᵀ D^{-1/2} r (and the Σ c² partials into pcc when given).
+static void pc_project(Precond& M, const double* r, int nrhs, double* T, double* pcc, cudaStream_t s) {
+  const int KT = pc_proj_tile(M.k, nrhs);
+  for (i64 j0 = 0; j0 < M.k; j0 += KT) {
+    const int kt = int(std::min<i64>(KT, M.k - j0));
+    k_pc_proj<<<RB, RT, pc_proj_smem(kt, nrhs), s>>>(r, M.dinv.p, M.q1.p + j0, M.N, kt, int(M.k), nrhs, M.partial.p,
+                                                      j0 == 0 ? pcc : nullptr);
+    launched("precond proj");
+    k_pc_fin<<<fin_blocks(kt * nrhs), 256, 0, s>>>(M.partial.p, kt * nrhs, T + j0 * nrhs);
+    launched("precond fin");
+  }
+}
+// z = D^{-1/2}(D^{-1/2} r − Q1 T); partial Σ r·z per block when requested.
+static int pc_finish(Precond& M, const double* r, const double* T, double* z, int nrhs, cudaStream_t s,
+                     double* partial_rz) {
+  if (!pc_big(M.k, nrhs)) {
+    const size_t sh2 = sizeof(double) * (M.k * nrhs + RT);
+    k_pc_apply<<<RB, RT, sh2, s>>>(r, M.dinv.p, M.q1.p, T, M.N, int(M.k), nrhs, z, partial_rz);
+    launched("precond apply");
+    return RB;
+  }
+  M.cbuf.reserve(static_cast<size_t>(M.N) * nrhs);
+  rows_gemm_dev(M.q1.p, int(M.k), T, nrhs, M.N, M.cbuf.p, false, s);
+  k_pc_finish_s<<<RB, RT, 0, s>>>(r, M.dinv.p, M.cbuf.p, M.N, nrhs, z, partial_rz);
+  launched("precond apply (large rank)");
+  return RB;
+}
+
 void Precond::ensure(int nrhs) {
   if (nrhs <= ensured_nrhs) return;
   ensured_nrhs = nrhs;
@@ -1756,10 +1821,9 @@ void Precond::ensure(int nrhs) {
   t.reserve(static_cast<size_t>(k) * np);
   pad_r.reserve(static_cast<size_t>(N) * np);
   pad_z.reserve(static_cast<size_t>(N) * np);
-  const size_t sh1 = sizeof(double) * (PC_RT * k + PC_RT * nrhs + k * nrhs);
-  if (sh1 > 227 * 1024) fail(GK_ERR_UNSUPPORTED, "preconditioner rank × nrhs too large for one pass");
-  set_smem((const void*)k_pc_proj, sh1);
-  set_smem((const void*)k_pc_apply, sizeof(double) * (k * nrhs + RT));
+  set_smem((const void*)k_pc_proj, kPcSmem + 8 * 1024);  // every tile size of pc_project fits
+  if (!pc_big(k, nrhs)) set_smem((const void*)k_pc_apply, sizeof(double) * (k * nrhs + RT));
+  else cbuf.reserve(static_cast<size_t>(N) * nrhs);
   if (mma_ok(nrhs)) {
     set_smem((const void*)k_pc_proj_mma, proj_mma_smem(nrhs));
     set_smem((const void*)k_pc_apply_mma, apply_mma_smem(nrhs));
@@ -1879,25 +1943,14 @@ int Precond::apply(const double* r, double* z, int nrhs, cudaStream_t s, double*
     launched("precond apply (DMMA)");
     return int(nb);
   }
-  const size_t sh1 = sizeof(double) * (PC_RT * k + PC_RT * nrhs + k * nrhs);
-  k_pc_proj<<<RB, RT, sh1, s>>>(r, dinv.p, q1.p, N, int(k), nrhs, partial.p, nullptr);
-  launched("precond proj");
-  k_pc_fin<<<fin_blocks(int(k * nrhs)), 256, 0, s>>>(partial.p, int(k * nrhs), t.p);
-  launched("precond fin");
-  const size_t sh2 = sizeof(double) * (k * nrhs + RT);
-  k_pc_apply<<<RB, RT, sh2, s>>>(r, dinv.p, q1.p, t.p, N, int(k), nrhs, z, partial_rz);
-  launched("precond apply");
-  return RB;
+  pc_project(*this, r, nrhs, t.p, nullptr, s);
+  return pc_finish(*this, r, t.p, z, nrhs, s, partial_rz);
 }
 
 void precond_quadratic(Precond& M, const double* r, int nrhs, double* out_h, cudaStream_t s) {
   M.ensure(nrhs);
   DevBuf<double> pcc(static_cast<size_t>(RB) * nrhs), cc(static_cast<size_t>(nrhs));
-  const size_t sh1 = sizeof(double) * (PC_RT * M.k + PC_RT * nrhs + M.k * nrhs);
-  k_pc_proj<<<RB, RT, sh1, s>>>(r, M.dinv.p, M.q1.p, M.N, int(M.k), nrhs, M.partial.p, pcc.p);
-  launched("precond proj");
-  k_pc_fin<<<fin_blocks(int(M.k * nrhs)), 256, 0, s>>>(M.partial.p, int(M.k * nrhs), M.t.p);
-  launched("precond fin");
+  pc_project(M, r, nrhs, M.t.p, pcc.p, s);
   k_fin_cols<<<fin_blocks(nrhs), 256, 0, s>>>(pcc.p, nrhs, cc.p);
   launched("precond fin");
   std::vector<double> T(static_cast<size_t>(M.k) * nrhs), c2(static_cast<size_t>(nrhs));
@@ -1915,7 +1968,6 @@ void precond_quadratic(Precond& M, const double* r, int nrhs, double* out_h, cud
 std::unique_ptr<Precond> precond_build(const double* F_int, i64 N, i64 k, const double* noise_int, int device,
                                        cudaStream_t s) {
   if (k < 1) fail(GK_ERR_ARG, "preconditioner needs a factor of rank at least 1");
-  if (k > 512) fail(GK_ERR_UNSUPPORTED, "preconditioner rank above 512 is not supported");
   auto M = std::make_unique<Precond>();
   M->device = device;
   M->N = N;
@@ -2107,12 +2159,7 @@ void precond_project(Precond& M, const double* r, int nrhs, double* T, cudaStrea
     launched("precond fin");
     return;
   }
-  const size_t sh1 = sizeof(double) * (PC_RT * M.k + PC_RT * nrhs + M.k * nrhs);
-  raise_smem_limit((const void*)k_pc_proj, sh1);
-  k_pc_proj<<<RB, RT, sh1, s>>>(r, M.dinv.p, M.q1.p, M.N, int(M.k), nrhs, M.partial.p, nullptr);
-  launched("precond proj");
-  k_pc_fin<<<fin_blocks(int(M.k * nrhs)), 256, 0, s>>>(M.partial.p, int(M.k * nrhs), T);
-  launched("precond fin");
+  pc_project(M, r, nrhs, T, nullptr, s);
 }
 // z = D^{-1/2}(D^{-1/2} r − Q1 T) for a given (all-reduced) T.
 void precond_finish(Precond& M, const double* r, const double* T, double* z, int nrhs, cudaStream_t s) {
@@ -2122,10 +2169,7 @@ void precond_finish(Precond& M, const double* r, const double* T, double* z, int
     launched("precond apply (1 RHS, warp per row)");
     return;
   }
-  const size_t sh2 = sizeof(double) * (M.k * nrhs + RT);
-  raise_smem_limit((const void*)k_pc_apply, sh2);
-  k_pc_apply<<<RB, RT, sh2, s>>>(r, M.dinv.p, M.q1.p, T, M.N, int(M.k), nrhs, z, nullptr);
-  launched("precond apply");
+  pc_finish(M, r, T, z, nrhs, s, nullptr);
 }
 // A preconditioner over an explicit Q1 (N×k col-major, device) and D^{-1/2}.
 std::unique_ptr<Precond> precond_from_q1(const double* Q1cm, const double* dinv, i64 N, i64 k, int device,

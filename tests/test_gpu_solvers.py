@@ -112,6 +112,29 @@ def test_preconditioner_high_rank_vs_dense_inverse(k):
         assert abs(P.quadratic(b) - b @ want) <= 1e-9 * abs(b @ want)
 
 
+@pytest.mark.parametrize("k", [520, 700])
+def test_preconditioner_rank_above_shared_memory_limits(k):
+    """Ranks whose projection staging does not fit shared memory (k-column
+    tiles) and whose apply runs as S = Q1 T + a finishing pass: no rank
+    limit, like the reference Preconditioner (linalg.cpp:176-213). Single-
+    and 32-column applies, the quadratic form, and a PCG solve preconditioned
+    by the exact inverse (converges in one iteration)."""
+    n, sigma = 1500, 0.3
+    F = np.random.default_rng(k).standard_normal((n, k)) / np.sqrt(k)
+    P = gk.Preconditioner(F, sigma)
+    assert P.rank() == k
+    M = sigma ** 2 * np.eye(n) + F @ F.T
+    B = np.random.default_rng(400).standard_normal((n, 32))
+    want = np.linalg.solve(M, B)
+    got = np.asarray(P.apply(B))
+    assert np.max(np.linalg.norm(got - want, axis=0) / np.linalg.norm(want, axis=0)) <= 1e-9
+    b = B[:, 0]
+    assert np.linalg.norm(P.apply(b) - want[:, 0]) <= 1e-9 * np.linalg.norm(want[:, 0])
+    assert abs(P.quadratic(b) - b @ want[:, 0]) <= 1e-9 * abs(b @ want[:, 0])
+    res = gk.cg(gk.DenseOperator(M), B[:, :4], 1e-8, 50, P)  # one CgResult per column
+    assert all(r.iterations <= 2 and r.converged for r in res)
+
+
 @pytest.mark.parametrize("n", [1, 311, 312, 313, 1000, 30000])
 def test_device_rademacher_streams_bit_identical(n):
     """The device mt19937_64 (two-phase parallel twist) reproduces the host

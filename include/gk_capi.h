@@ -63,8 +63,12 @@ int64_t gk_kernel_launch_count(void);
 
 /* ---------------------------------------------------------------- kernel spec
  * KernelSpec (reference kernels.hpp:42-75). family 0 = squared exponential,
- * 1 = spline (spline is accepted by the dense paths only; grid operators
- * return GK_ERR_UNSUPPORTED for it in this build). */
+ * 1 = spline (kernels.cpp:104-118). D-SKI takes either: the separable SE
+ * profile runs as Kronecker–Toeplitz mode products, the spline profile as a
+ * circulant embedding with an in-house FFT (dski.cpp:80-172). D-SKIP needs a
+ * separable kernel (GK_ERR_ARG for spline, std::invalid_argument at
+ * dskip.cpp:118-121); the matrix-free exact operator implements SE only
+ * (GK_ERR_UNSUPPORTED). */
 typedef struct {
   int family;
   double lengthscale;
@@ -170,6 +174,11 @@ gk_status gk_op_noise_diagonal(const gk_op* op, double* out);
  * (dski.cpp:146-172): W = K_UU U. */
 int64_t gk_dski_grid_size(const gk_op* op);
 gk_status gk_dski_get_grid(const gk_op* op, gk_grid* out);
+/* GridKernelOperator::min_embedding_eigenvalue (dski.hpp:40-43, dski.cpp:
+ * 137-139): the smallest eigenvalue of the reference's circulant embedding
+ * (2(m_j − 1) nodes per axis) of the operator's profile, computed on the host
+ * (separable cosine sums in long double; O(E·ΣE_j), seconds at C4). */
+gk_status gk_dski_min_embedding_eigenvalue(const gk_op* op, double* out);
 gk_status gk_dski_transpose_apply(const gk_op* op, const double* V, int64_t ldv, double* U,
                                   int64_t ldu, int64_t nrhs);
 gk_status gk_dski_apply(const gk_op* op, const double* U, int64_t ldu, double* Out, int64_t ldo,

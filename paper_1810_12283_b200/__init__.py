@@ -90,6 +90,7 @@ _SIGS = {
     "gk_op_from_internal_dev": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp]),
     "gk_dski_grid_size": (_i64, [_vp]),
     "gk_dski_get_grid": (C.c_int, [_vp, C.POINTER(GkGrid)]),
+    "gk_dski_min_embedding_eigenvalue": (C.c_int, [_vp, C.POINTER(C.c_double)]),
     "gk_dski_transpose_apply": (C.c_int, [_vp, _dp, _i64, _dp, _i64, _i64]),
     "gk_dski_apply": (C.c_int, [_vp, _dp, _i64, _dp, _i64, _i64]),
     "gk_dski_grid_mvm": (C.c_int, [_vp, _dp, _i64, _dp, _i64, _i64]),
@@ -222,6 +223,34 @@ def uniform_vector(n, seed, stream, a, b):
     out = np.empty(n)
     _lib.gk_uniform_vector(n, seed, stream, float(a), float(b), _p(out))
     return out
+
+
+def spline_constants_for_domain(scaled_diameter, dim):
+    """SplineConstants::for_domain (kernels.cpp:42-90): a = −1.5·D; b is the
+    first of 0.25·D³·2^j (j = 0..12) for which the kernel matrix of a 5-per-
+    axis lattice (≤ 3 axes) spanning the scaled diameter D is PSD (min
+    eigenvalue ≥ −1e-10 · max), doubled. Returns (a, b, even)."""
+    if not scaled_diameter > 0:
+        raise ValueError("spline domain diameter must be positive")
+    even = dim % 2 == 0
+    a = -1.5 * scaled_diameter
+    rho3 = scaled_diameter ** 3
+    axes = min(dim, 3)
+    per_axis = 5
+    side = scaled_diameter / np.sqrt(float(axes))
+    idx = np.arange(per_axis ** axes)
+    P = np.column_stack([side * ((idx // per_axis ** ax) % per_axis) / (per_axis - 1) for ax in range(axes)])
+    D = np.sqrt(((P[:, None, :] - P[None, :, :]) ** 2).sum(-1))
+    with np.errstate(divide="ignore", invalid="ignore"):
+        radial = np.where(D > 0, D * D * np.log(np.where(D > 0, D, 1.0)), 0.0) if even else D ** 3
+    mult = 0.25
+    while mult <= 1024.0:
+        b = mult * rho3
+        ev = np.linalg.eigvalsh(radial + a * D * D + b)
+        if ev.min() >= -1e-10 * ev.max():
+            return a, 2.0 * b, even
+        mult *= 2.0
+    raise RuntimeError("spline constant calibration failed to reach PSD")
 
 
 @dataclass
@@ -394,6 +423,13 @@ class DskiOperator(LinearOperator):
 
     def points(self):
         return self.n
+
+    def min_embedding_eigenvalue(self):
+        """GridKernelOperator::min_embedding_eigenvalue (dski.hpp:40-43) of the
+        reference's 2(m−1) circulant embedding."""
+        out = _d()
+        _check(_lib.gk_dski_min_embedding_eigenvalue(self.handle, C.byref(out)))
+        return out.value
 
     def grid_size(self):
         return int(_lib.gk_dski_grid_size(self._h))
@@ -780,9 +816,9 @@ def lml_gradient(A: LinearOperator, alpha, probes=8, seed=0, tol=1e-4, max_itera
 
 def _prior_variance(A):
     k = A.kernel
-    if k.family != SE:
-        raise NotImplementedError("prior variance implemented for the squared-exponential kernel")
-    return k.outputscale ** 2  # eval(kernel, x, x) (gp.cpp:464-466)
+    if k.family == SE:
+        return k.outputscale ** 2  # eval(kernel, x, x) (gp.cpp:464-466)
+    return k.outputscale ** 2 * k.spline_b  # spline at ρ = 0: s²·b (kernels.cpp:113-117)
 
 
 def gp_solve(A: LinearOperator, B, tol=1e-4, max_iterations=1000, precond=None):
@@ -960,7 +996,7 @@ class GpModel:
         return self.op().cross_covariance_jacobian(Xtest)
 
     def prior_variance(self):
-        return self.kernel.outputscale ** 2
+        return _prior_variance(self.op())
 
     def predict_variance_exact(self, Xtest):
         return predict_variance_exact(self.op(), Xtest, self.cfg["tol"], self.cfg["max_iterations"],

@@ -14,8 +14,9 @@ host control flow of the tools. Differences from the reference tools:
     (dense Cholesky, gp.cpp:71-84) is not on the B200 path; fit/predict with
     it exit 2 (config error) naming the supported backends. benchmark-mvm
     times "exact" through the matrix-free device operator (ExactOperator).
-  - `--kernel spline` exits 2: the grid operators are squared-exponential
-    only on both sides (dski.cpp:95-101 rejects other families for D-SKI).
+  - `--kernel spline` runs on the dski backend (K_UU by circulant embedding
+    and an in-house FFT); dskip rejects it like the reference
+    (dskip.cpp:118-121, exit 2).
   - GRADKRIG_THREADS is accepted and ignored (no host worker pool).
   - subcommands terrain / active-subspace / bo are out of scope.
 """
@@ -81,12 +82,13 @@ def make_kernel(a, X):
     """make_kernel (proj/tools/common.cpp:55-72): ℓ defaults to 0.2 × the
     bounding-box diagonal, s to 1."""
     gk = _gk()
-    if a.kernel != "se":
-        raise ConfigError("kernel family 'spline' is not supported by the B200 grid operators (use --kernel se)")
     span2 = sum(float(X[:, j].max() - X[:, j].min()) ** 2 for j in range(X.shape[1]))
     diag = math.sqrt(max(span2, 1e-12))
     ell = a.ell if a.ell > 0 else 0.2 * diag
     s = a.outputscale if a.outputscale > 0 else 1.0
+    if a.kernel == "spline":  # constants calibrated on the data's scaled diameter (common.cpp:66-69)
+        sa, sb, even = gk.spline_constants_for_domain(diag / ell, X.shape[1])
+        return gk.KernelSpec(ell, s, gk.SPLINE, sa, sb, even)
     return gk.KernelSpec(ell, s)
 
 
@@ -115,7 +117,9 @@ def run_fit(a) -> None:
     cfg = make_gp_config(a)
     model = build_model(kernel, X, y, dY, a.noise, a.noise_grad, cfg)
     res = model.fit(max_iterations=a.iters, restarts=a.restarts, seed=a.seed)
-    out = io.ModelFile(family="se", lengthscale=res.kernel.lengthscale, outputscale=res.kernel.outputscale,
+    k = res.kernel
+    out = io.ModelFile(family="spline" if k.family == 1 else "se", spline_a=k.spline_a, spline_b=k.spline_b,
+                       spline_even=bool(k.spline_even), lengthscale=k.lengthscale, outputscale=k.outputscale,
                        noise_value=res.noise_value, noise_gradient=res.noise_gradient, mean=model.mean,
                        backend=cfg.backend, config=cfg, data_path=a.data, with_gradients=dY is not None)
     io.save_model(a.model, out)
@@ -147,9 +151,10 @@ def run_predict(a) -> None:
         if dY is not None:
             dY = np.asfortranarray(dY @ P)
         Xtest = Xtest @ P
-    if m.family != "se":
-        raise ConfigError("kernel family 'spline' is not supported by the B200 grid operators")
-    kernel = gk.KernelSpec(m.lengthscale, m.outputscale)
+    if m.family == "spline":
+        kernel = gk.KernelSpec(m.lengthscale, m.outputscale, gk.SPLINE, m.spline_a, m.spline_b, m.spline_even)
+    else:
+        kernel = gk.KernelSpec(m.lengthscale, m.outputscale)
     model = build_model(kernel, X, y, dY, m.noise_value, m.noise_gradient, m.config)
     model.set_hyperparameters(kernel, m.noise_value, m.noise_gradient)
     if model.backend != "dski":

@@ -38,6 +38,7 @@ bool dski_fused_split(Op& o, int phase, const double* v, double* u2, double* out
 void dski_cross_cov_dev(Op& o, const double* dXt, i64 nT, int dir, double* dQ, i64 ldq, cudaStream_t s);
 void dski_gather_noise(Op& o, const double* W, const double* V, double* out, int nrhs, cudaStream_t s);
 gk_grid dski_grid(const Op& o);
+double dski_min_embedding_eigenvalue(const Op& o);
 void dski_transpose_apply(Op& o, const double* Vi, double* U, int nrhs, cudaStream_t s);
 void dski_apply(Op& o, const double* U, double* Oi, int nrhs, cudaStream_t s);
 void dski_grid_mvm(Op& o, const double* U, double* W, int nrhs, cudaStream_t s);
@@ -558,6 +559,13 @@ int64_t gk_dski_grid_size(const gk_op* h) {
 
 gk_status gk_dski_get_grid(const gk_op* h, gk_grid* out) {
   return guard([&] { *out = dski_grid(O(h)); });
+}
+
+gk_status gk_dski_min_embedding_eigenvalue(const gk_op* h, double* out) {
+  return guard([&] {
+    if (!out) fail(GK_ERR_ARG, "null output");
+    *out = dski_min_embedding_eigenvalue(O(h));
+  });
 }
 
 }  // extern "C"

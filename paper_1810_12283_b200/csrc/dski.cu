@@ -33,6 +33,7 @@
 #include <sstream>
 
 #include "fused2d.hpp"
+#include "kuu_fft.hpp"
 #include "lean2d.hpp"
 
 #include <cub/cub.cuh>
@@ -1435,6 +1436,11 @@ struct DskiOp final : Op {
   DevBuf<double> wts;
   DevBuf<double2> wd;
   DevBuf<int> cell_start;
+  // Non-separable profile (spline kernel): K_UU by circulant embedding + FFT
+  // (kuu_fft.cu); diagonal from the stencil-offset table, rows through K_UU.
+  bool generic = false;
+  std::unique_ptr<KuuFft> kfft, kfft_dl;  // value and d/dlog(ell) profiles (the latter built on first use)
+  DevBuf<double> gtab;                    // profile at stencil offsets, (2T-1)^d row-major
   DevBuf<double> tvec;  // concatenated per-axis Toeplitz sequences (axis 0 carries s²)
   DevBuf<int> toff;
   std::vector<int> toff_h;
@@ -1505,7 +1511,7 @@ struct DskiOp final : Op {
   }
   // The fused one-launch MVM applies to d = 2 with gradients (C1, C2, C4).
   Fused2dPlan* fused_plan(int nrhs) {
-    if (d != 2 || G != 2 || g_tuning.fused.load() != 0 || n >= (i64(1) << 31)) return nullptr;
+    if (generic || d != 2 || G != 2 || g_tuning.fused.load() != 0 || n >= (i64(1) << 31)) return nullptr;
     const int gen = g_tuning.gen.load();
     for (auto it = fplans.begin(); it != fplans.end(); ++it)
       if ((*it)->nrhs == nrhs) {
@@ -1528,7 +1534,7 @@ struct DskiOp final : Op {
   // 74.9 vs 87.0 µs). Tuning "lean": 0 = this policy, 1 = never, 2 = always.
   Lean2dPlan* lean_plan(int nrhs) {
     const int pol = g_tuning.lean.load();
-    if (d != 2 || G != 2 || g_tuning.fused.load() != 0 || pol == 1 || n >= (i64(1) << 31)) return nullptr;
+    if (generic || d != 2 || G != 2 || g_tuning.fused.load() != 0 || pol == 1 || n >= (i64(1) << 31)) return nullptr;
     if (pol == 0 && !((nrhs % 2 == 1 && nrhs >= 3) || nrhs > 32)) return nullptr;
     const int gen = g_tuning.gen.load();
     for (auto it = lplans.begin(); it != lplans.end(); ++it)
@@ -1585,6 +1591,10 @@ struct DskiOp final : Op {
     }
   }
   void ensure_scratch(int nrhs) {
+    if (generic && kfft && kfft->buf.n < static_cast<size_t>(kfft->Etot) * ((nrhs + 1) / 2)) {
+      kfft->buf.reserve(static_cast<size_t>(kfft->Etot) * ((nrhs + 1) / 2));
+      ++epoch;
+    }
     grow(grid_u, static_cast<size_t>(M) * nrhs);
     grow(grid_w, static_cast<size_t>(M) * nrhs);
     grow(grid_t, static_cast<size_t>(M) * nrhs);
@@ -1646,7 +1656,8 @@ struct DskiOp final : Op {
   void diagonal(double* dd, cudaStream_t s) override;
   void row(i64 r_ext, double* out, cudaStream_t s) override;
   bool row_dev(const i64* d_r_int, const int* d_active, double* out, cudaStream_t s) override;
-  bool has_row_dev() const override { return true; }
+  bool has_row_dev() const override { return !generic; }
+  double min_embedding_eigenvalue() const;
 };
 
 #define GK_DISPATCH_DT(D_, T_, ...)                                   \
@@ -2120,7 +2131,128 @@ __global__ void k_axpy_inplace(double* __restrict__ w, const double* __restrict_
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) w[i] += x[i];
 }
 
+// ---------------------------------------------------------------- general profiles
+// Stationary profile κ(offset) = eval(kernel, offset, 0) (kernels.cpp:104-118)
+// and its ∂/∂log ℓ (eval_dlogell, kernels.cpp:172-188), on the host.
+static double profile_value(const gk_kernel& k, const double* off, int d, bool dlogell) {
+  const double s2 = k.outputscale * k.outputscale, ell = k.lengthscale;
+  double r2 = 0.0;
+  for (int j = 0; j < d; ++j) r2 += off[j] * off[j];
+  if (k.family == 0) {
+    const double v = s2 * std::exp(-0.5 * r2 / (ell * ell));
+    return dlogell ? v * (r2 / (ell * ell)) : v;
+  }
+  if (!dlogell) {
+    const double rho = std::sqrt(r2) / ell;
+    const double radial = k.spline_even ? (rho > 0 ? rho * rho * std::log(rho) : 0.0) : rho * rho * rho;
+    return s2 * (radial + k.spline_a * rho * rho + k.spline_b);
+  }
+  if (r2 == 0.0) return 0.0;
+  const double rho2 = r2 / (ell * ell);
+  const double rho = std::sqrt(rho2);
+  if (!k.spline_even) return s2 * (-3.0 * rho * rho2 - 2.0 * k.spline_a * rho2);
+  return s2 * (-2.0 * rho2 * std::log(rho) - rho2 - 2.0 * k.spline_a * rho2);
+}
+
+// The profile on an embedded torus of E[j] nodes per axis at the wrapped
+// offsets (i ≤ E/2 ? i : i − E)·h_j, row-major (dski.cpp:97-114).
+static std::vector<double> embedded_slice(const gk_kernel& k, const gk_grid& g, const int* E, bool dlogell) {
+  const int d = g.d;
+  i64 tot = 1;
+  for (int j = 0; j < d; ++j) tot *= E[j];
+  std::vector<double> out(static_cast<size_t>(tot));
+  int idx[3] = {0, 0, 0};
+  double off[3];
+  for (i64 t = 0; t < tot; ++t) {
+    for (int j = 0; j < d; ++j) off[j] = double(idx[j] <= E[j] / 2 ? idx[j] : idx[j] - E[j]) * g.spacing[j];
+    out[static_cast<size_t>(t)] = profile_value(k, off, d, dlogell);
+    for (int j = d - 1; j >= 0; --j) {
+      if (++idx[j] < E[j]) break;
+      idx[j] = 0;
+    }
+  }
+  return out;
+}
+
+double DskiOp::min_embedding_eigenvalue() const {
+  int E[3] = {1, 1, 1};
+  for (int j = 0; j < d; ++j) E[j] = 2 * (m[j] - 1);
+  return min_embedding_eigenvalue_host(d, m, embedded_slice(kernel, grid, E, false));
+}
+
+// diag = Σ_δ κ(δ) Π_j P_j(δ_j), P_j the autocorrelation of axis j's stencil
+// weights (derivative weights on the group's axis): the offset-table double
+// loop of dski.cpp:240-290 regrouped by offset.
+template <int D, int T>
+__global__ void k_diagonal_generic(DskiView op, const double* __restrict__ tab, double* __restrict__ diag) {
+  constexpr int W = 2 * T - 1, STRIDE = D * 2 * T;
+  int nt = 1;
+  for (int j = 0; j < D; ++j) nt *= W;
+  for (i64 s = blockIdx.x * (i64)blockDim.x + threadIdx.x; s < op.n; s += (i64)gridDim.x * blockDim.x) {
+    const double* p = op.wts + s * STRIDE;
+    for (int g = 0; g <= op.G; ++g) {
+      double P[D][W];
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        const double* c = p + j * 2 * T + (g == j + 1 ? T : 0);
+#pragma unroll
+        for (int dl = 0; dl < W; ++dl) {
+          const int del = dl - (T - 1);
+          double acc = 0.0;
+#pragma unroll
+          for (int a = 0; a < T; ++a)
+            if (a - del >= 0 && a - del < T) acc += c[a] * c[a - del];
+          P[j][dl] = acc;
+        }
+      }
+      double sum = 0.0;
+      for (int t = 0; t < nt; ++t) {
+        int r = t;
+        double prod = __ldg(tab + t);
+#pragma unroll
+        for (int j = D - 1; j >= 0; --j) {
+          prod *= P[j][r % W];
+          r /= W;
+        }
+        sum += prod;
+      }
+      diag[(i64)g * op.n + s] = sum + (g == 0 ? op.nv2 : op.ng2);
+    }
+  }
+}
+
+// grid vector e (zeroed by the caller) = the stencil of point si, group g
+template <int D, int T>
+__global__ void k_stencil_to_grid(DskiView op, int si, int g, double* __restrict__ e) {
+  constexpr int STRIDE = D * 2 * T;
+  int nt = 1;
+  for (int j = 0; j < D; ++j) nt *= T;
+  const int4 b = op.base[si];
+  const int bb[3] = {b.x, b.y, b.z};
+  const double* p = op.wts + (i64)si * STRIDE;
+  for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+    int r = t, tj[3] = {0, 0, 0};
+    for (int j = D - 1; j >= 0; --j) {
+      tj[j] = r % T;
+      r /= T;
+    }
+    double w = 1.0;
+    i64 node = 0;
+    for (int j = 0; j < D; ++j) {
+      w *= p[j * 2 * T + (g == j + 1 ? T : 0) + tj[j]];
+      node = node * op.m[j] + bb[j] + tj[j];
+    }
+    e[node] = w;
+  }
+}
+
+__global__ void k_add_scalar(double* __restrict__ x, double v) { *x += v; }
+
 void DskiOp::kuu(const double* u, double* w, int nrhs, cudaStream_t s) const {
+  if (generic) {
+    kfft->apply(u, w, nrhs, s);
+    return;
+  }
   // Modes from the last axis to the first: u -> ... -> w, intermediates
   // alternating between w and the scratch grid_t so the last mode lands in w
   // (caller has reserved grid_t for nrhs columns; u must not alias w/grid_t).
@@ -2139,6 +2271,16 @@ void DskiOp::kuu(const double* u, double* w, int nrhs, cudaStream_t s) const {
 // (the reference applies the same operator through a second circulant
 // embedding of kernel_dlogell_profile, dski.cpp:36-40, gp.cpp:212-213).
 void DskiOp::kuu_dlogell(const double* u, double* w, int nrhs, cudaStream_t s) {
+  if (generic) {  // the reference's second embedding of kernel_dlogell_profile (dski.cpp:36-40)
+    if (!kfft_dl) {
+      auto f = std::make_unique<KuuFft>();
+      f->init(d, m);
+      f->build(embedded_slice(kernel, grid, f->E, true), s);
+      kfft_dl = std::move(f);
+    }
+    kfft_dl->apply(u, w, nrhs, s);
+    return;
+  }
   grow(grid_a, static_cast<size_t>(M) * nrhs);
   grow(grid_b, static_cast<size_t>(M) * nrhs);
   for (int term = 0; term < d; ++term) {
@@ -2163,6 +2305,32 @@ void DskiOp::kuu_dlogell(const double* u, double* w, int nrhs, cudaStream_t s) {
 
 void DskiOp::diagonal(double* dd, cudaStream_t s) {
   const DskiView vw = view();
+  if (generic) {
+    if (!gtab.p) {
+      const int W = 2 * T - 1;
+      int E[3] = {W, W, W};
+      gk_grid tg = grid;  // offsets (i − (T−1))·h: a W^d table centred on 0
+      std::vector<double> tab;
+      i64 tot = 1;
+      for (int j = 0; j < d; ++j) tot *= W;
+      tab.resize(static_cast<size_t>(tot));
+      int idx[3] = {0, 0, 0};
+      double off[3];
+      for (i64 t = 0; t < tot; ++t) {
+        for (int j = 0; j < d; ++j) off[j] = double(idx[j] - (T - 1)) * tg.spacing[j];
+        tab[static_cast<size_t>(t)] = profile_value(kernel, off, d, false);
+        for (int j = d - 1; j >= 0; --j) {
+          if (++idx[j] < E[j]) break;
+          idx[j] = 0;
+        }
+      }
+      gtab.upload(tab.data(), tab.size(), s);
+      GK_CUDA(cudaStreamSynchronize(s));
+    }
+    GK_DISPATCH_DT(d, T, { k_diagonal_generic<D, T><<<grid_blocks(n), 256, 0, s>>>(vw, gtab.p, dd); });
+    launched("dski diagonal (general profile)");
+    return;
+  }
   GK_DISPATCH_DT(d, T, { k_diagonal<D, T><<<grid_blocks(n), 256, 0, s>>>(vw, tvec.p, toff.p, dd); });
   launched("dski diagonal");
 }
@@ -2183,6 +2351,17 @@ void DskiOp::row(i64 r_ext, double* out, cudaStream_t s) {
   const int g = int(r_ext / n);
   const int si = int(inv_h[static_cast<size_t>(r_ext % n)]);
   const DskiView vw = view();
+  if (generic) {  // row = B K_UU (stencil of the row) + its noise entry (dski.cpp:292-304)
+    ensure_scratch(1);
+    GK_CUDA(cudaMemsetAsync(grid_u.p, 0, sizeof(double) * M, s));
+    GK_DISPATCH_DT(d, T, { k_stencil_to_grid<D, T><<<1, 256, 0, s>>>(vw, si, g, grid_u.p); });
+    launched("dski row stencil");
+    kfft->apply(grid_u.p, grid_w.p, 1, s);
+    gather(grid_w.p, grid_w.p, out, 1, false, s);
+    k_add_scalar<<<1, 1, 0, s>>>(out + (i64)g * n + si, g == 0 ? nv2 : ng2);
+    launched("dski row noise");
+    return;
+  }
   const int shm = int(sizeof(double)) * (m[0] + (d > 1 ? m[1] : 0) + (d > 2 ? m[2] : 0));
   GK_DISPATCH_DT(d, T, { k_row<D, T><<<grid_blocks(N), 256, shm, s>>>(vw, tvec.p, toff.p, si, g, out); });
   launched("dski row");
@@ -2206,10 +2385,9 @@ std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, cons
                                       int profile) {
   if (profile == 1 && g.d != 1)
     fail(GK_ERR_UNSUPPORTED, "the d/dlog(ell) grid profile is implemented for 1-D grids only");
-  if (k.family != 0)
-    fail(GK_ERR_UNSUPPORTED,
-         "D-SKI on B200 implements the separable squared-exponential profile; the spline "
-         "profile is not supported by this build");
+  if (k.family != 0 && k.family != 1) fail(GK_ERR_ARG, "unknown kernel family");
+  if (k.family != 0 && profile != 0)
+    fail(GK_ERR_UNSUPPORTED, "the d/dlog(ell) 1-D grid profile is the D-SKIP leaf's (separable kernels only)");
   if (!(k.lengthscale > 0.0)) fail(GK_ERR_ARG, "lengthscale must be > 0");
   if (!(k.outputscale > 0.0)) fail(GK_ERR_ARG, "outputscale must be > 0");
   if (g.d < 1 || g.d > 3) fail(GK_ERR_UNSUPPORTED, "D-SKI grid dimension must be 1, 2 or 3");
@@ -2296,6 +2474,12 @@ std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, cons
   for (int j = 0; j < d; ++j) ncells *= op->nb[j];
   op->init_stream();
   cudaStream_t st = op->stream;
+  if (k.family != 0) {  // general profile: circulant embedding + FFT (dski.cpp:80-172)
+    op->generic = true;
+    op->kfft = std::make_unique<KuuFft>();
+    op->kfft->init(d, op->m);
+    op->kfft->build(embedded_slice(k, g, op->kfft->E, false), st);
+  }
   std::vector<int> cstart;
   std::vector<i64> ext;
   const bool host_build = g_tuning.devbuild.load() != 0 || ncells >= (i64(1) << 31) || n >= (i64(1) << 31);
@@ -2640,6 +2824,10 @@ int64_t dski_grid_size(const Op& o) {
 gk_grid dski_grid(const Op& o) {
   if (o.kind != KIND_DSKI) fail(GK_ERR_ARG, "operator is not a D-SKI operator");
   return static_cast<const DskiOp&>(o).grid;
+}
+double dski_min_embedding_eigenvalue(const Op& o) {
+  if (o.kind != KIND_DSKI) fail(GK_ERR_ARG, "operator is not a D-SKI operator");
+  return static_cast<const DskiOp&>(o).min_embedding_eigenvalue();
 }
 
 // B K_UU B^T without the noise diagonal (internal layout), for D-SKIP leaves.

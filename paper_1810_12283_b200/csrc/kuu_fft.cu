@@ -1,0 +1,299 @@
+// kuu_fft.cu — K_UU = T(κ) for a general stationary profile κ (e.g. the
+// spline kernel, kernels.cpp:104-118) on a d ≤ 3 grid, by circulant
+// embedding (reference GridKernelOperator, dski.cpp:80-172):
+//   w = corner( IFFT( spec · FFT( zero-padded u ) ) ).
+// The embedding is the power of two E_j ≥ 2m_j − 1 per axis (the reference
+// takes 2(m_j − 1) for FFTW; any E_j ≥ 2m_j − 1 reproduces the same linear
+// convolution exactly, and powers of two let one radix-2 kernel serve every
+// axis). Right-hand sides go two at a time as the real and imaginary parts
+// of one complex field (the spectrum of an even profile slice is real).
+//
+// FFT: one kernel per axis, a CTA transforms TI lines in shared memory
+// (bit-reversed load, log2 E radix-2 butterfly stages, natural-order store);
+// for the strided axes the TI lines are adjacent in memory so every load row
+// is one coalesced 16·TI-byte segment.
+#include <cmath>
+
+#include "kuu_fft.hpp"
+
+namespace gk {
+
+namespace {
+
+constexpr int FFT_THREADS = 256;
+constexpr size_t kFftSmem = 64 * 1024;
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// Lines of one axis pass. A line is (pair p, indices i_k of the axes k < j,
+// inner index i over the axes k > j); element t of the line lives at
+// p·Etot + Σ_{k<j} i_k·stride_k + t·S + i (S = Π_{k>j} E_k). The axes
+// before j are restricted to i_k < lim_k: forward passes run last axis
+// first, so those axes still hold the zero-padded input (support m_k);
+// inverse passes run first axis first and only the corner i_k < m_k of the
+// result is needed. `support` > 0: entries t ≥ support of the line are the
+// zero padding and are not read. TI lines per CTA: S == 1 — TI whole lines;
+// S > 1 — TI lines adjacent in memory (same outer index, TI | S).
+struct AxisPass {
+  int L, logL, TI, support, inverse;
+  i64 S, nlines, Etot;
+  int j, lim0, lim1;
+  i64 st0, st1;  // strides of axes 0 and 1 (elements)
+};
+
+__global__ void __launch_bounds__(FFT_THREADS) k_fft_lines(double2* __restrict__ buf, AxisPass a,
+                                                           const double2* __restrict__ tw) {
+  extern __shared__ double2 sx[];  // [TI][L]
+  const int L = a.L, TI = a.TI;
+  const i64 g0 = (i64)blockIdx.x * TI;
+  const int tid = threadIdx.x;
+  auto base = [&](i64 g) -> i64 {
+    i64 i = 0, o = g;
+    if (a.S > 1) {
+      i = g % a.S;
+      o = g / a.S;
+    }
+    i64 off = i;
+    if (a.j >= 2) {
+      off += (o % a.lim1) * a.st1;
+      o /= a.lim1;
+    }
+    if (a.j >= 1) {
+      off += (o % a.lim0) * a.st0;
+      o /= a.lim0;
+    }
+    return o * a.Etot + off;
+  };
+  const int shift = 32 - a.logL;
+  const int sup = a.support > 0 ? a.support : L;
+  for (int e = tid; e < TI * L; e += FFT_THREADS) {
+    int c, t;
+    if (a.S == 1) {
+      c = e / L;
+      t = e - c * L;
+    } else {
+      t = e / TI;
+      c = e - t * TI;
+    }
+    const i64 g = g0 + c;
+    double2 v = make_double2(0.0, 0.0);
+    if (g < a.nlines && t < sup) v = buf[base(g) + (i64)t * a.S];
+    const int rt = a.logL ? int(__brev(unsigned(t)) >> shift) : 0;
+    sx[c * L + rt] = v;
+  }
+  __syncthreads();
+  const int halfL = L >> 1;
+  for (int s = 1; s <= a.logL; ++s) {
+    const int half = 1 << (s - 1);
+    const int tstride = L >> s;
+    for (int e = tid; e < TI * halfL; e += FFT_THREADS) {
+      const int c = e / halfL, jj = e - c * halfL;
+      const int pos = jj & (half - 1), grp = jj >> (s - 1);
+      const int i1 = (grp << s) + pos, i2 = i1 + half;
+      double2 w = __ldg(tw + pos * tstride);
+      if (a.inverse) w.y = -w.y;
+      const double2 x = sx[c * L + i1];
+      const double2 y = cmul(w, sx[c * L + i2]);
+      sx[c * L + i1] = make_double2(x.x + y.x, x.y + y.y);
+      sx[c * L + i2] = make_double2(x.x - y.x, x.y - y.y);
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < TI * L; e += FFT_THREADS) {
+    int c, t;
+    if (a.S == 1) {
+      c = e / L;
+      t = e - c * L;
+    } else {
+      t = e / TI;
+      c = e - t * TI;
+    }
+    const i64 g = g0 + c;
+    if (g < a.nlines) buf[base(g) + (i64)t * a.S] = sx[c * L + t];
+  }
+}
+
+struct Dims3 {
+  int m[3], E[3];
+};
+
+// zero-padded complex field of RHS pair p: corner node (i0, i1, i2) gets
+// u[node][2p] + i·u[node][2p+1]
+__global__ void k_fft_load(const double* __restrict__ U, int nrhs, int npairs, Dims3 g, i64 M, i64 Etot,
+                           double2* __restrict__ buf) {
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < M * npairs; e += (i64)gridDim.x * blockDim.x) {
+    const int p = int(e / M);
+    const i64 node = e - (i64)p * M;
+    const int i2 = int(node % g.m[2]);
+    const i64 r = node / g.m[2];
+    const int i1 = int(r % g.m[1]), i0 = int(r / g.m[1]);
+    const i64 ei = ((i64)i0 * g.E[1] + i1) * g.E[2] + i2;
+    const int c = 2 * p;
+    const double re = U[node * nrhs + c];
+    const double im = c + 1 < nrhs ? U[node * nrhs + c + 1] : 0.0;
+    buf[(i64)p * Etot + ei] = make_double2(re, im);
+  }
+}
+
+__global__ void k_fft_scale(double2* __restrict__ buf, const double* __restrict__ spec, i64 Etot, int npairs) {
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < Etot * npairs; e += (i64)gridDim.x * blockDim.x) {
+    const double sc = spec[e % Etot];
+    const double2 v = buf[e];
+    buf[e] = make_double2(v.x * sc, v.y * sc);
+  }
+}
+
+__global__ void k_fft_store(const double2* __restrict__ buf, int nrhs, int npairs, Dims3 g, i64 M, i64 Etot,
+                            double* __restrict__ W) {
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < M * npairs; e += (i64)gridDim.x * blockDim.x) {
+    const int p = int(e / M);
+    const i64 node = e - (i64)p * M;
+    const int i2 = int(node % g.m[2]);
+    const i64 r = node / g.m[2];
+    const int i1 = int(r % g.m[1]), i0 = int(r / g.m[1]);
+    const i64 ei = ((i64)i0 * g.E[1] + i1) * g.E[2] + i2;
+    const double2 v = buf[(i64)p * Etot + ei];
+    const int c = 2 * p;
+    W[node * nrhs + c] = v.x;
+    if (c + 1 < nrhs) W[node * nrhs + c + 1] = v.y;
+  }
+}
+
+__global__ void k_fft_real_part(const double2* __restrict__ buf, i64 n, double scale, double* __restrict__ out) {
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < n; e += (i64)gridDim.x * blockDim.x)
+    out[e] = buf[e].x * scale;
+}
+
+unsigned blocks_of(i64 n) { return static_cast<unsigned>(std::min<i64>((n + 255) / 256, 148 * 32)); }
+
+// All axes of npairs fields, forward (inverse = 0: last axis first, input
+// supported on the corner i_k < m_k when `pruned`) or inverse (first axis
+// first, only the corner of the result kept when `pruned`); no scaling.
+void fft_all_axes(const KuuFft& f, double2* buf, int npairs, int inverse, bool pruned, cudaStream_t s) {
+  for (int step = 0; step < 3; ++step) {
+    const int j = inverse ? step : 2 - step;
+    const int L = f.E[j];
+    if (L < 2) continue;
+    AxisPass a{};
+    a.L = L;
+    a.logL = f.logE[j];
+    a.inverse = inverse;
+    a.j = j;
+    a.Etot = f.Etot;
+    a.S = 1;
+    for (int k = j + 1; k < 3; ++k) a.S *= f.E[k];
+    a.st0 = i64(f.E[1]) * f.E[2];
+    a.st1 = f.E[2];
+    a.lim0 = pruned ? f.m[0] : f.E[0];
+    a.lim1 = pruned ? f.m[1] : f.E[1];
+    a.support = pruned && !inverse ? f.m[j] : 0;
+    i64 outer = npairs;
+    if (j >= 1) outer *= a.lim0;
+    if (j >= 2) outer *= a.lim1;
+    a.nlines = outer * a.S;
+    if (a.S == 1) a.TI = std::max(1, int(kFftSmem / (sizeof(double2) * L)));
+    else a.TI = int(std::min<i64>(a.S, std::max<i64>(1, std::min<i64>(16, kFftSmem / (sizeof(double2) * L)))));
+    const size_t smem = sizeof(double2) * size_t(a.TI) * L;
+    raise_smem_limit((const void*)k_fft_lines, smem);
+    k_fft_lines<<<static_cast<unsigned>((a.nlines + a.TI - 1) / a.TI), FFT_THREADS, smem, s>>>(buf, a, f.tw[j].p);
+    launched("kuu fft axis");
+  }
+}
+
+}  // namespace
+
+void KuuFft::init(int dd, const int* dims) {
+  d = dd;
+  M = 1;
+  Etot = 1;
+  for (int j = 0; j < 3; ++j) {
+    m[j] = j < d ? dims[j] : 1;
+    int e = 1, lg = 0;
+    if (j < d)
+      while (e < 2 * m[j] - 1) {
+        e <<= 1;
+        ++lg;
+      }
+    if (e > 8192) fail(GK_ERR_UNSUPPORTED, "grid too large for the circulant-embedding K_UU (E > 8192 per axis)");
+    E[j] = e;
+    logE[j] = lg;
+    M *= m[j];
+    Etot *= e;
+  }
+}
+
+void KuuFft::build(const std::vector<double>& slice, cudaStream_t s) {
+  if (static_cast<i64>(slice.size()) != Etot) fail(GK_ERR_ARG, "profile slice size mismatch");
+  for (int j = 0; j < 3; ++j) {
+    const int L = E[j];
+    std::vector<double2> t(static_cast<size_t>(std::max(1, L / 2)));
+    for (int k = 0; k < L / 2; ++k) {
+      const long double a = -2.0L * 3.14159265358979323846264338327950288L * k / L;
+      t[static_cast<size_t>(k)] = make_double2(double(cosl(a)), double(sinl(a)));
+    }
+    tw[j].upload(t.data(), t.size(), s);
+    GK_CUDA(cudaStreamSynchronize(s));
+  }
+  std::vector<double2> z(static_cast<size_t>(Etot));
+  for (i64 e = 0; e < Etot; ++e) z[static_cast<size_t>(e)] = make_double2(slice[static_cast<size_t>(e)], 0.0);
+  buf.reserve(static_cast<size_t>(Etot));
+  GK_CUDA(cudaMemcpyAsync(buf.p, z.data(), sizeof(double2) * Etot, cudaMemcpyHostToDevice, s));
+  fft_all_axes(*this, buf.p, 1, 0, false, s);
+  // the slice is even in every axis, so its spectrum is real; the imaginary
+  // parts are roundoff and are dropped (as dski.cpp:127-131 does)
+  spec.alloc(static_cast<size_t>(Etot));
+  k_fft_real_part<<<blocks_of(Etot), 256, 0, s>>>(buf.p, Etot, 1.0 / double(Etot), spec.p);
+  launched("kuu fft spectrum");
+  GK_CUDA(cudaStreamSynchronize(s));
+}
+
+void KuuFft::apply(const double* U, double* W, int nrhs, cudaStream_t s) const {
+  const int npairs = (nrhs + 1) / 2;
+  buf.reserve(static_cast<size_t>(Etot) * npairs);
+  Dims3 g{{m[0], m[1], m[2]}, {E[0], E[1], E[2]}};
+  // no zero fill: the pruned forward passes read only the corner they wrote
+  k_fft_load<<<blocks_of(M * npairs), 256, 0, s>>>(U, nrhs, npairs, g, M, Etot, buf.p);
+  launched("kuu fft load");
+  fft_all_axes(*this, buf.p, npairs, 0, true, s);
+  k_fft_scale<<<blocks_of(Etot * npairs), 256, 0, s>>>(buf.p, spec.p, Etot, npairs);
+  launched("kuu fft spectrum multiply");
+  fft_all_axes(*this, buf.p, npairs, 1, true, s);
+  k_fft_store<<<blocks_of(M * npairs), 256, 0, s>>>(buf.p, nrhs, npairs, g, M, Etot, W);
+  launched("kuu fft store");
+}
+
+double min_embedding_eigenvalue_host(int d, const int* dims, const std::vector<double>& slice) {
+  // embedding 2(m_j − 1) per axis (dski.cpp:89-95), slice row-major; the
+  // even slice's DFT along each axis is a cosine sum (separable)
+  int E[3] = {1, 1, 1};
+  i64 tot = 1;
+  for (int j = 0; j < d; ++j) {
+    E[j] = 2 * (dims[j] - 1);
+    tot *= E[j];
+  }
+  if (static_cast<i64>(slice.size()) != tot) fail(GK_ERR_ARG, "embedding slice size mismatch");
+  std::vector<long double> a(slice.begin(), slice.end()), b(static_cast<size_t>(tot));
+  for (int j = 0; j < d; ++j) {
+    const int L = E[j];
+    i64 S = 1;
+    for (int k = j + 1; k < d; ++k) S *= E[k];
+    std::vector<long double> c(static_cast<size_t>(L));
+    for (int k = 0; k < L; ++k) c[static_cast<size_t>(k)] = cosl(2.0L * 3.14159265358979323846264338327950288L * k / L);
+    for (i64 e = 0; e < tot; ++e) {
+      const i64 o = e / (S * L), i = e % S;
+      const int kk = int((e / S) % L);
+      long double acc = 0.0L;
+      for (int t = 0; t < L; ++t)
+        acc += a[static_cast<size_t>(o * L * S + i + (i64)t * S)] * c[static_cast<size_t>((i64(kk) * t) % L)];
+      b[static_cast<size_t>(e)] = acc;
+    }
+    a.swap(b);
+  }
+  long double mn = a[0];
+  for (const long double v : a) mn = std::min(mn, v);
+  return double(mn);
+}
+
+}  // namespace gk

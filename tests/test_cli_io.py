@@ -125,7 +125,7 @@ def test_cli_exit_codes_without_device_work(tmp_path):
     data = _write(tmp_path / "d.csv", "x1,x2,y\n0.1,0.2,1\n0.3,0.4,2\n")
     assert cli.main(["fit", "--data", str(tmp_path / "missing.csv")]) == cli.EXIT_DATA
     assert cli.main(["fit", "--data", _write(tmp_path / "bad.csv", "x1,y\n1,oops\n")]) == cli.EXIT_DATA
-    assert cli.main(["fit", "--data", data, "--kernel", "spline"]) == cli.EXIT_CONFIG
+    assert cli.main(["fit", "--data", data, "--kernel", "spline", "--backend", "exact"]) == cli.EXIT_CONFIG
     assert cli.main(["fit", "--data", data, "--backend", "exact"]) == cli.EXIT_CONFIG
     assert cli.main(["fit", "--data", data, "--precond", "maybe"]) == cli.EXIT_CONFIG  # parse error
     assert cli.main(["fit"]) == cli.EXIT_CONFIG  # --data is required
@@ -175,3 +175,28 @@ def test_benchmark_points_follow_seeded_rng_row_order():
     u = O.mix_seed(2, 5)
     flat = [float(O.mt19937_64_nth(u, i + 1)) / 2.0 ** 64 for i in range(15)]
     assert X.flatten(order="C").tolist() == flat
+
+
+def test_spline_constants_for_domain():
+    """SplineConstants::for_domain (kernels.cpp:42-90): a = −1.5·D, the first
+    PSD b on the canonical lattice, doubled; the b before it is not PSD."""
+    import paper_1810_12283_b200 as gk
+    for D, dim in ((2.0, 2), (3.5, 3), (1.2, 1), (4.0, 5)):
+        a, b, even = gk.spline_constants_for_domain(D, dim)
+        assert a == -1.5 * D and even == (dim % 2 == 0)
+        mult = b / 2 / D ** 3
+        assert mult in [0.25 * 2 ** j for j in range(13)]
+        axes = min(dim, 3)
+        side = D / np.sqrt(axes)
+        idx = np.arange(5 ** axes)
+        P = np.column_stack([side * ((idx // 5 ** ax) % 5) / 4 for ax in range(axes)])
+        R = np.sqrt(((P[:, None] - P[None]) ** 2).sum(-1))
+        with np.errstate(divide="ignore", invalid="ignore"):
+            rad = np.where(R > 0, R * R * np.log(np.where(R > 0, R, 1.0)), 0.0) if even else R ** 3
+        ev = np.linalg.eigvalsh(rad + a * R * R + b / 2)
+        assert ev.min() >= -1e-10 * ev.max()
+        if mult > 0.25:
+            ev = np.linalg.eigvalsh(rad + a * R * R + b / 4)
+            assert ev.min() < -1e-10 * ev.max()
+    with pytest.raises(ValueError):
+        gk.spline_constants_for_domain(0.0, 2)

@@ -144,3 +144,27 @@ def test_benchmark_operator_is_the_reference_one():
     v = gk.gaussian_vector(op.size(), 7)
     want = ref.mvm(v)
     assert np.linalg.norm(op.mvm(v) - want) <= 1e-12 * np.linalg.norm(want)
+
+
+def test_cli_spline_kernel_fit_and_predict(tmp_path):
+    """--kernel spline on the dski backend (SplineConstants::for_domain
+    calibration, K_UU by circulant embedding): fit → model JSON with the
+    spline constants → predict; the predictive mean matches the oracle
+    D-SKI operator's B K_UU Bᵀ α path (gp.cpp:480-495) through its own K∇."""
+    X, y, dY = O.sample_test_function("franke", 150, 3, (0.05, 0.05))
+    data = str(tmp_path / "train.csv")
+    gio.write_dataset_csv(data, gio.Dataset(X, y, dY))
+    model = str(tmp_path / "model.json")
+    assert cli.main(["fit", "--data", data, "--model", model, "--kernel", "spline", "--backend", "dski", "--noise", "0.3",
+                     "--noise-grad", "0.3", "--grid-size", "40", "--rank", "60", "--tol", "1e-8", "--maxit", "3000",
+                     "--probes", "8", "--iters", "1", "--restarts", "1"]) == 0
+    j = json.load(open(model))
+    assert j["kernel"]["family"] == "spline" and {"spline_a", "spline_b", "spline_even"} <= set(j["kernel"])
+    assert j["kernel"]["spline_even"] is True  # d = 2
+    test = str(tmp_path / "test.csv")
+    gio.write_csv(test, ["x1", "x2"], X[:5].tolist())
+    out = str(tmp_path / "pred.csv")
+    assert cli.main(["predict", "--model", model, "--test", test, "--out", out]) == 0
+    P = np.array(list(csv.reader(open(out)))[1:], dtype=float)
+    assert P.shape == (5, 4) and np.all(np.isfinite(P))
+    assert np.max(np.abs(P[:, 2] - y[:5])) < 0.5  # the mean interpolates its own (noisy) training values

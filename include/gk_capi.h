@@ -67,8 +67,7 @@ int64_t gk_kernel_launch_count(void);
  * profile runs as Kronecker–Toeplitz mode products, the spline profile as a
  * circulant embedding with an in-house FFT (dski.cpp:80-172). D-SKIP needs a
  * separable kernel (GK_ERR_ARG for spline, std::invalid_argument at
- * dskip.cpp:118-121); the matrix-free exact operator implements SE only
- * (GK_ERR_UNSUPPORTED). */
+ * dskip.cpp:118-121); the matrix-free exact operator takes both. */
 typedef struct {
   int family;
   double lengthscale;

@@ -518,7 +518,7 @@ class DskiOperator(LinearOperator):
 
 
 class ExactOperator(LinearOperator):
-    """Matrix-free exact D-SE K∇ + noise (kernels.cpp:242-285 without assembly)."""
+    """Matrix-free exact K∇ + noise, SE or spline kernel (kernels.cpp:104-170, 242-285 without assembly)."""
 
     def __init__(self, kernel: KernelSpec, X, noise=(0.0, 0.0), with_gradients=True, device=0):
         X = _f64(X, True)

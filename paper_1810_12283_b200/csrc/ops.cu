@@ -57,11 +57,49 @@ __global__ void k_from_internal(const double* __restrict__ I, const i64* __restr
   }
 }
 
-// Matrix-free exact D-SE K∇ (type-major, kernels.cpp:242-285) + noise.
-// One thread per (row point i, rhs b) computes all d+1 output groups; the
-// column points are streamed through shared memory in tiles.
+// Kernel family parameters of the matrix-free exact operator.
+struct KParams {
+  int family;  // 0 SE, 1 spline
+  double s2, ell, ell2, a, b;
+  int even;
+};
+
+// One (x_i, x_j) pair of K∇ (kernels.cpp:104-170, assembled as :242-285):
+// k = eval, dk/dx'_q = g·u_q (u = x_i − x_j; dk/dx_p = −g·u_p), and the
+// Hessian block d²k/dx_p dx'_q = α δ_pq + β u_p u_q.
+__device__ __forceinline__ void kpair(const KParams& K, double r2, double& k, double& g, double& al, double& be) {
+  if (K.family == 0) {  // SeProfile (kernels.cpp:22-27)
+    k = K.s2 * exp(-0.5 * r2 / K.ell2);
+    g = k / K.ell2;
+    al = g;
+    be = -g / K.ell2;
+    return;
+  }
+  const double r = sqrt(r2), rho = r / K.ell;
+  const double radial = K.even ? (rho > 0 ? rho * rho * log(rho) : 0.0) : rho * rho * rho;
+  k = K.s2 * (radial + K.a * rho * rho + K.b);
+  if (r == 0.0) {  // analytic limit / convention (kernels.cpp:129, 155-159)
+    g = 0.0;
+    al = -2.0 * K.a * K.s2 / K.ell2;
+    be = 0.0;
+  } else if (!K.even) {
+    const double c1 = 3.0 * r / (K.ell2 * K.ell) + 2.0 * K.a / K.ell2;
+    g = -K.s2 * c1;
+    al = g;
+    be = -K.s2 * 3.0 / (r * K.ell2 * K.ell);
+  } else {
+    const double c = (2.0 * log(rho) + 1.0 + 2.0 * K.a) / K.ell2;
+    g = -K.s2 * c;
+    al = g;
+    be = -K.s2 * 2.0 / (K.ell2 * r2);
+  }
+}
+
+// Matrix-free exact K∇ (type-major, kernels.cpp:242-285) + noise, SE or
+// spline. One thread per (row point i, rhs b) computes all d+1 output
+// groups; the column points are streamed through shared memory in tiles.
 template <int D, bool GRAD>
-__global__ void __launch_bounds__(256) k_exact_mvm(const double* __restrict__ X, i64 n, double s2, double ell2,
+__global__ void __launch_bounds__(256) k_exact_mvm(const double* __restrict__ X, i64 n, KParams K,
                                                    const double* __restrict__ v, double* __restrict__ out,
                                                    int nrhs, double nv2, double ng2) {
   constexpr int TILE = 128;
@@ -78,7 +116,6 @@ __global__ void __launch_bounds__(256) k_exact_mvm(const double* __restrict__ X,
   double o[NG];
 #pragma unroll
   for (int g = 0; g < NG; ++g) o[g] = 0.0;
-  const double inv_ell2 = 1.0 / ell2;
   for (i64 j0 = 0; j0 < n; j0 += TILE) {
     __syncthreads();
     for (int t = threadIdx.x; t < TILE * D; t += blockDim.x) {
@@ -96,11 +133,11 @@ __global__ void __launch_bounds__(256) k_exact_mvm(const double* __restrict__ X,
         u[p] = xi[p] - xs[p][jj];
         r2 += u[p] * u[p];
       }
-      const double k = s2 * exp(-0.5 * r2 * inv_ell2);
+      double k, gc, al, be;
+      kpair(K, r2, k, gc, al, be);
       const double v0 = v[j * nrhs + b];
       o[0] += k * v0;
       if constexpr (GRAD) {
-        const double gc = k * inv_ell2;  // grad_coeff (kernels.cpp:25)
         double vq[D], uv = 0.0;
 #pragma unroll
         for (int q = 0; q < D; ++q) {
@@ -108,10 +145,9 @@ __global__ void __launch_bounds__(256) k_exact_mvm(const double* __restrict__ X,
           o[0] += gc * u[q] * vq[q];  // K(i, (q+1)j) = dk/dx'_q
           uv += u[q] * vq[q];
         }
-        // rows (p+1)i: -g_p v0 + Σ_q H_pq v_q, H = k/ℓ⁴ (ℓ² δ - u uᵀ)
+        // rows (p+1)i: −g u_p v0 + Σ_q (α δ_pq + β u_p u_q) v_q
 #pragma unroll
-        for (int p = 0; p < D; ++p)
-          o[p + 1] += -gc * u[p] * v0 + gc * vq[p] - gc * inv_ell2 * u[p] * uv;
+        for (int p = 0; p < D; ++p) o[p + 1] += -gc * u[p] * v0 + al * vq[p] + be * u[p] * uv;
       }
     }
   }
@@ -123,16 +159,17 @@ __global__ void __launch_bounds__(256) k_exact_mvm(const double* __restrict__ X,
   }
 }
 
-__global__ void k_exact_diag(i64 n, int groups, double s2, double ell2, double nv2, double ng2,
-                             double* __restrict__ d) {
+__global__ void k_exact_diag(i64 n, int groups, KParams K, double nv2, double ng2, double* __restrict__ d) {
   const i64 N = n * (groups + 1);
+  double k, g, al, be;
+  kpair(K, 0.0, k, g, al, be);
   for (i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x; r < N; r += (i64)gridDim.x * blockDim.x)
-    d[r] = r < n ? s2 + nv2 : s2 / ell2 + ng2;
+    d[r] = r < n ? k + nv2 : al + ng2;
 }
 
 template <int D>
-__global__ void k_exact_row(const double* __restrict__ X, i64 n, int groups, double s2, double ell2,
-                            i64 gi, int gg, double nv2, double ng2, double* __restrict__ out) {
+__global__ void k_exact_row(const double* __restrict__ X, i64 n, int groups, KParams K, i64 gi, int gg,
+                            double nv2, double ng2, double* __restrict__ out) {
   const i64 N = n * (groups + 1);
   double xi[D];
   for (int p = 0; p < D; ++p) xi[p] = X[p * n + gi];
@@ -144,12 +181,13 @@ __global__ void k_exact_row(const double* __restrict__ X, i64 n, int groups, dou
       u[p] = xi[p] - X[p * n + j];
       r2 += u[p] * u[p];
     }
-    const double k = s2 * exp(-0.5 * r2 / ell2);
+    double k, gc, al, be;
+    kpair(K, r2, k, gc, al, be);
     double val;
     if (gg == 0 && q == 0) val = k;
-    else if (gg == 0) val = k / ell2 * u[q - 1];
-    else if (q == 0) val = -k / ell2 * u[gg - 1];
-    else val = (k / (ell2 * ell2)) * ((gg == q ? ell2 : 0.0) - u[gg - 1] * u[q - 1]);
+    else if (gg == 0) val = gc * u[q - 1];
+    else if (q == 0) val = -gc * u[gg - 1];
+    else val = (gg == q ? al : 0.0) + be * u[gg - 1] * u[q - 1];
     if (j == gi && q == gg) val += gg == 0 ? nv2 : ng2;
     out[r] = val;
   }
@@ -248,14 +286,14 @@ void Op::stage(int st, const double* in, double* out, int nrhs, cudaStream_t s) 
 struct ExactOp final : Op {
   int d = 0, G = 0;
   i64 n = 0;
-  double s2 = 1.0, ell2 = 1.0;
+  KParams K{};
   DevBuf<double> X;
   void mvm(const double* in, double* out, int nrhs, cudaStream_t s) override {
     const int blocks = int((n * nrhs + 255) / 256);
 #define GK_EXACT_CASE(DD)                                                                          \
   case DD:                                                                                         \
-    if (G) k_exact_mvm<DD, true><<<blocks, 256, 0, s>>>(X.p, n, s2, ell2, in, out, nrhs, nv2, ng2); \
-    else k_exact_mvm<DD, false><<<blocks, 256, 0, s>>>(X.p, n, s2, ell2, in, out, nrhs, nv2, ng2); \
+    if (G) k_exact_mvm<DD, true><<<blocks, 256, 0, s>>>(X.p, n, K, in, out, nrhs, nv2, ng2); \
+    else k_exact_mvm<DD, false><<<blocks, 256, 0, s>>>(X.p, n, K, in, out, nrhs, nv2, ng2); \
     break;
     switch (d) {
       GK_EXACT_CASE(1)
@@ -270,7 +308,7 @@ struct ExactOp final : Op {
     launched("exact mvm");
   }
   void diagonal(double* dd, cudaStream_t s) override {
-    k_exact_diag<<<blocks_for(N), 256, 0, s>>>(n, G, s2, ell2, nv2, ng2, dd);
+    k_exact_diag<<<blocks_for(N), 256, 0, s>>>(n, G, K, nv2, ng2, dd);
     launched("exact diag");
   }
   void row(i64 r, double* out, cudaStream_t s) override {
@@ -279,7 +317,7 @@ struct ExactOp final : Op {
     const int gg = int(r / n);
     switch (d) {
 #define GK_ROW_CASE(DD) \
-  case DD: k_exact_row<DD><<<blocks_for(N), 256, 0, s>>>(X.p, n, G, s2, ell2, gi, gg, nv2, ng2, out); break;
+  case DD: k_exact_row<DD><<<blocks_for(N), 256, 0, s>>>(X.p, n, G, K, gi, gg, nv2, ng2, out); break;
       GK_ROW_CASE(1)
       GK_ROW_CASE(2)
       GK_ROW_CASE(3)
@@ -295,7 +333,7 @@ struct ExactOp final : Op {
 
 std::unique_ptr<Op> make_exact(const gk_kernel& k, const double* X, i64 n, int d, double nv, double ng,
                                int with_grad, int device) {
-  if (k.family != 0) fail(GK_ERR_UNSUPPORTED, "exact device operator implements the SE kernel only");
+  if (k.family != 0 && k.family != 1) fail(GK_ERR_ARG, "unknown kernel family");
   if (!(k.lengthscale > 0.0)) fail(GK_ERR_ARG, "lengthscale must be > 0");
   if (!(k.outputscale > 0.0)) fail(GK_ERR_ARG, "outputscale must be > 0");
   if (d < 1 || d > 6) fail(GK_ERR_UNSUPPORTED, "exact operator supports 1 <= d <= 6");
@@ -310,8 +348,8 @@ std::unique_ptr<Op> make_exact(const gk_kernel& k, const double* X, i64 n, int d
   op->n_value = n;
   op->nv2 = nv * nv;
   op->ng2 = ng * ng;
-  op->s2 = k.outputscale * k.outputscale;
-  op->ell2 = k.lengthscale * k.lengthscale;
+  op->K = KParams{k.family, k.outputscale * k.outputscale, k.lengthscale, k.lengthscale * k.lengthscale,
+                  k.spline_a, k.spline_b, k.spline_even};
   op->init_stream();
   op->X.upload(X, static_cast<size_t>(n) * d, op->stream);
   GK_CUDA(cudaStreamSynchronize(op->stream));

@@ -144,6 +144,29 @@ gk_status gk_dskip_create_from_factors(int64_t n, int groups, double noise_value
 /* DenseOperator(A) (linear_operator.hpp:38-56); A is N×N column-major. */
 gk_status gk_dense_create(const double* A, int64_t N, int device, gk_op** out);
 
+/* assemble_dense(kernel, X, X', options) (kernels.cpp:242-285, AssemblyOptions
+ * kernels.hpp:83-92): the type-major n(d+1) × n'(d+1) (or n × n') K∇, or
+ * ∂K∇/∂log ℓ when dlogell != 0, assembled on `device`; derivative_scale > 0
+ * scales derivative rows and columns. Host output, column-major. Above
+ * size_cap entries: GK_ERR_LENGTH (std::length_error, kernels.cpp:252-255). */
+gk_status gk_assemble_dense(const gk_kernel* kernel, const double* X, int64_t n, const double* Xp, int64_t np, int d,
+                            int with_derivatives, int dlogell, double derivative_scale, int64_t size_cap, int device,
+                            double* out);
+/* GpModel's exact backend (gp.cpp:71-85): DenseOperator over the device-
+ * assembled K∇ + noise diagonal, with its dense Cholesky factor (cuSOLVER
+ * potrf, loaded on first use; the reference uses Eigen's LLT). Not positive
+ * definite: GK_ERR_RUNTIME "dense kernel matrix is not positive definite". */
+gk_status gk_dense_kernel_create(const gk_kernel* kernel, const double* X, int64_t n, int d, double noise_value,
+                                 double noise_gradient, int with_gradients, int64_t size_cap, int device,
+                                 gk_op** out);
+/* llt_->solve (gp.cpp:146): X = K⁻¹ B through the factor (host buffers). */
+gk_status gk_dense_cholesky_solve(const gk_op* op, const double* B, int64_t ldb, int64_t nrhs, double* X, int64_t ldx);
+/* GpModel::logdet exact branch (gp.cpp:167-168): 2 Σ log L_ii. */
+gk_status gk_dense_cholesky_logdet(const gk_op* op, double* logdet);
+/* GpModel::lml_gradient exact branch (gp.cpp:246-276): traces through K⁻¹ and
+ * the assembled ∂K/∂log ℓ. alpha = K⁻¹ targets (host, N). */
+gk_status gk_dense_exact_lml_gradient(const gk_op* op, const double* alpha, double* grad, int* nparams);
+
 /* Matrix-free exact D-SE operator: assemble_dense(kernel, X, X) + noise
  * (kernels.cpp:242-285) applied without forming the N×N matrix. */
 gk_status gk_exact_create(const gk_kernel* kernel, const double* X, int64_t n, int d,

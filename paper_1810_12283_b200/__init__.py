@@ -90,6 +90,13 @@ _SIGS = {
     "gk_op_from_internal_dev": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp]),
     "gk_dski_grid_size": (_i64, [_vp]),
     "gk_dski_get_grid": (C.c_int, [_vp, C.POINTER(GkGrid)]),
+    "gk_assemble_dense": (C.c_int, [C.POINTER(GkKernel), _dp, _i64, _dp, _i64, C.c_int, C.c_int, C.c_int, _d, _i64,
+                                    C.c_int, _dp]),
+    "gk_dense_kernel_create": (C.c_int, [C.POINTER(GkKernel), _dp, _i64, C.c_int, _d, _d, C.c_int, _i64, C.c_int,
+                                         C.POINTER(_vp)]),
+    "gk_dense_cholesky_solve": (C.c_int, [_vp, _dp, _i64, _i64, _dp, _i64]),
+    "gk_dense_cholesky_logdet": (C.c_int, [_vp, C.POINTER(C.c_double)]),
+    "gk_dense_exact_lml_gradient": (C.c_int, [_vp, _dp, _dp, C.POINTER(C.c_int)]),
     "gk_dski_min_embedding_eigenvalue": (C.c_int, [_vp, C.POINTER(C.c_double)]),
     "gk_dski_transpose_apply": (C.c_int, [_vp, _dp, _i64, _dp, _i64, _i64]),
     "gk_dski_apply": (C.c_int, [_vp, _dp, _i64, _dp, _i64, _i64]),
@@ -539,6 +546,60 @@ class DenseOperator(LinearOperator):
         super().__init__(_create(_lib.gk_dense_create, _p(A), A.shape[0], device), device)
 
 
+def assemble_dense(kernel: KernelSpec, X, Xp=None, with_derivatives=True, dlogell=False, derivative_scale=0.0,
+                   size_cap=50_000_000, device=0):
+    """assemble_dense (kernels.cpp:242-285, AssemblyOptions kernels.hpp:83-92)
+    on the device: type-major K∇(X, X') (or ∂K∇/∂log ℓ); OverflowError above
+    size_cap entries (std::length_error)."""
+    X = _f64(X, True)
+    Xp = X if Xp is None else _f64(Xp, True)
+    n, d = X.shape
+    npt = Xp.shape[0]
+    if Xp.shape[1] != d:
+        raise ValueError("point sets have mismatched dimensions")
+    rows = n * (d + 1) if with_derivatives else n
+    cols = npt * (d + 1) if with_derivatives else npt
+    out = np.empty((rows, cols), order="F") if rows * cols <= size_cap else np.empty((0, 0))
+    k = kernel.c()
+    _check(_lib.gk_assemble_dense(C.byref(k), _p(X), n, _p(Xp), npt, d, int(with_derivatives), int(dlogell),
+                                  float(derivative_scale), int(size_cap), device, _p(out)))
+    return out
+
+
+class DenseKernelOperator(LinearOperator):
+    """GpModel's exact operator (gp.cpp:71-85): the device-assembled K∇ + noise
+    as a DenseOperator with its Cholesky factor (solve, logdet, the exact
+    LML gradient of gp.cpp:246-276)."""
+
+    def __init__(self, kernel: KernelSpec, X, noise=(1e-2, 1e-2), with_gradients=True, size_cap=50_000_000,
+                 device=0):
+        X = _f64(X, True)
+        self.n, self.d = X.shape
+        self.kernel = kernel
+        k = kernel.c()
+        super().__init__(_create(_lib.gk_dense_kernel_create, C.byref(k), _p(X), self.n, self.d, float(noise[0]),
+                                 float(noise[1]), int(with_gradients), int(size_cap), device), device)
+
+    def solve(self, B):
+        b = np.asarray(B, dtype=np.float64)
+        vec = b.ndim == 1
+        Bm = np.asfortranarray(b.reshape(-1, 1) if vec else b)
+        X = np.empty_like(Bm, order="F")
+        _check(_lib.gk_dense_cholesky_solve(self.handle, _p(Bm), Bm.shape[0], Bm.shape[1], _p(X), X.shape[0]))
+        return X[:, 0] if vec else X
+
+    def logdet(self):
+        out = _d()
+        _check(_lib.gk_dense_cholesky_logdet(self.handle, C.byref(out)))
+        return out.value
+
+    def exact_lml_gradient(self, alpha):
+        g = np.empty(4)
+        k = C.c_int()
+        _check(_lib.gk_dense_exact_lml_gradient(self.handle, _p(_f64(alpha)), _p(g), C.byref(k)))
+        return g[: k.value].copy()
+
+
 class DskipOperator(LinearOperator):
     """DskipOperator (dskip.hpp:91-121)."""
 
@@ -867,16 +928,17 @@ def predict_variance_randomized(A: "DskiOperator", precond, Xtest, probes, seed,
 class GpModel:
     """GpModel (gp.hpp:64-145; gp.cpp) over the device operators: the hot-path
     members (op, preconditioner, solve, alpha, logdet, log_marginal_likelihood,
-    lml_gradient, predictions). Backends "dski" and "dskip" (the reference's
-    dense-LLT "exact" backend is not on the path; ExactOperator provides the
-    matrix-free exact K∇ MVM). The optimiser `fit` is out of scope."""
+    lml_gradient, predictions, fit). Backends "dski", "dskip" and "exact"
+    (the device-assembled dense K∇ with a dense Cholesky factor, gp.cpp:71-85).
+    Predictions for the non-D-SKI backends use the assembled cross-covariance
+    (gp.cpp:419-461)."""
 
     def __init__(self, kernel: KernelSpec, X, y, dY=None, noise=(1e-2, 1e-2), backend="dski", grid_ratio=0.2,
                  max_grid_nodes=128, dskip_rank=100, dskip_grid_ratio=0.1, dskip_max_grid_nodes=512, tol=1e-4,
                  max_iterations=1000, use_preconditioner=True, precond_rank=100, slq_probes=10, slq_steps=50,
-                 gradient_probes=8, seed=0, interpolation=0, device=0):
-        if backend not in ("dski", "dskip"):
-            raise ValueError(f"unknown or unsupported backend '{backend}'")
+                 gradient_probes=8, seed=0, interpolation=0, dense_size_cap=50_000_000, device=0):
+        if backend not in ("exact", "dski", "dskip"):
+            raise ValueError(f"unknown backend '{backend}'")
         self.kernel = kernel
         self.X = _f64(X, True)
         self.y = _f64(y)
@@ -893,7 +955,8 @@ class GpModel:
                         dskip_grid_ratio=dskip_grid_ratio, dskip_max_grid_nodes=dskip_max_grid_nodes, tol=tol,
                         max_iterations=max_iterations, use_preconditioner=use_preconditioner,
                         precond_rank=precond_rank, slq_probes=slq_probes, slq_steps=slq_steps,
-                        gradient_probes=gradient_probes, seed=seed, interpolation=interpolation)
+                        gradient_probes=gradient_probes, seed=seed, interpolation=interpolation,
+                        dense_size_cap=dense_size_cap)
         self.device = device
         self.mean = float(self.y.mean())  # gp.cpp:43
         self._invalidate()
@@ -921,7 +984,10 @@ class GpModel:
         """GpModel::build_operator (gp.cpp:66-110)."""
         if self._op is None:
             c = self.cfg
-            if self.backend == "dski":
+            if self.backend == "exact":
+                self._op = DenseKernelOperator(self.kernel, self.X, self.noise, self.has_gradients,
+                                               c["dense_size_cap"], self.device)
+            elif self.backend == "dski":
                 grid = Grid.cover(self.X, c["grid_ratio"] * self.kernel.lengthscale, 3, c["max_grid_nodes"])
                 self._op = DskiOperator(self.kernel, grid, self.X, self.noise, c["interpolation"],
                                         self.has_gradients, self.device)
@@ -945,6 +1011,8 @@ class GpModel:
         return self._M
 
     def solve(self, b, tol_scale=1.0):
+        if self.backend == "exact":  # llt_->solve (gp.cpp:146)
+            return self.op().solve(b)
         return gp_solve(self.op(), b, self.cfg["tol"] * tol_scale, self.cfg["max_iterations"],
                         self.preconditioner())
 
@@ -954,7 +1022,10 @@ class GpModel:
         return self._alpha
 
     def logdet(self):
-        """GpModel::logdet (gp.cpp:165-179): SLQ with floor ½·min(σ₁, σ₂)²."""
+        """GpModel::logdet (gp.cpp:165-179): SLQ with floor ½·min(σ₁, σ₂)²
+        (exact backend: 2 Σ log L_ii)."""
+        if self.backend == "exact":
+            return self.op().logdet()
         out = _d()
         _check(_lib.gk_gp_logdet(self.op().handle, int(self.cfg["slq_probes"]), int(self.cfg["slq_steps"]),
                                  int(self.cfg["seed"]), self.noise[0], self.noise[1], int(self.has_gradients),
@@ -963,6 +1034,9 @@ class GpModel:
 
     def log_marginal_likelihood(self):
         """GpModel::log_marginal_likelihood (gp.cpp:181-187)."""
+        if self.backend == "exact":
+            t = self.stacked_targets()
+            return -0.5 * (float(t @ self.alpha()) + self.logdet() + t.size * np.log(2.0 * np.pi))
         A, M = self.op(), self.preconditioner()
         t = self.stacked_targets()
         lml, fit, ld = _d(), _d(), _d()
@@ -977,28 +1051,57 @@ class GpModel:
         return lml.value
 
     def lml_gradient(self):
-        """GpModel::lml_gradient (gp.cpp:220-292), stochastic-trace branch."""
+        """GpModel::lml_gradient (gp.cpp:220-292): exact traces through the
+        dense factor (exact backend), else the stochastic-trace branch."""
+        if self.backend == "exact":
+            return self.op().exact_lml_gradient(self.alpha())
         return lml_gradient(self.op(), self.alpha(), self.cfg["gradient_probes"], self.cfg["seed"],
                             self.cfg["tol"], self.cfg["max_iterations"], self.preconditioner())
 
+    def _assembled_cross(self, Xtest):
+        """assemble_dense(X, Xtest) rows of the training outputs: columns t =
+        cross_covariance(x_t) (gp.cpp:419-428), columns (p+1)·T + t its
+        Jacobian column p (gp.cpp:447-460)."""
+        Xt = _f64(np.atleast_2d(Xtest), True)
+        K = assemble_dense(self.kernel, self.X, Xt, True, size_cap=self.cfg["dense_size_cap"], device=self.device)
+        return K[: self.outputs()], Xt.shape[0]
+
     def predict_mean_grad(self, Xtest):
-        if self.backend != "dski":
-            raise NotImplementedError("predict_mean_grad implemented for the D-SKI backend")
-        return self.op().predict_mean_grad(self.alpha(), self.mean, Xtest)
+        """GpModel::predict_mean_grad (gp.cpp:471-496)."""
+        if self.backend == "dski":
+            return self.op().predict_mean_grad(self.alpha(), self.mean, Xtest)
+        K, T = self._assembled_cross(Xtest)
+        a = self.alpha()
+        values = self.mean + K[:, :T].T @ a
+        grads = np.column_stack([K[:, (p + 1) * T:(p + 2) * T].T @ a for p in range(self.d)])
+        return values, grads
 
     def predict_mean(self, Xtest):
         return self.predict_mean_grad(Xtest)[0]
 
     def cross_covariance(self, Xtest):
-        return self.op().cross_covariance(Xtest)
+        if self.backend == "dski":
+            return self.op().cross_covariance(Xtest)
+        K, T = self._assembled_cross(Xtest)
+        return np.asfortranarray(K[:, :T])
 
     def cross_covariance_jacobian(self, Xtest):
-        return self.op().cross_covariance_jacobian(Xtest)
+        """(N, T, d) array, [:, t, p] = ∂q(x_t)/∂x_p (as DskiOperator's)."""
+        if self.backend == "dski":
+            return self.op().cross_covariance_jacobian(Xtest)
+        K, T = self._assembled_cross(Xtest)
+        return np.stack([K[:, (p + 1) * T:(p + 2) * T] for p in range(self.d)], axis=2)
 
     def prior_variance(self):
-        return _prior_variance(self.op())
+        k = self.kernel  # eval(kernel, x, x) (gp.cpp:464-466)
+        return k.outputscale ** 2 * (1.0 if k.family == SE else k.spline_b)
 
     def predict_variance_exact(self, Xtest):
+        """GpModel::predict_variance_exact (gp.cpp:506-509)."""
+        if self.backend != "dski":
+            Q = self.cross_covariance(Xtest)
+            S = np.asarray(self.solve(Q)).reshape(Q.shape)
+            return self.prior_variance() - np.einsum("ij,ij->j", Q, S)
         return predict_variance_exact(self.op(), Xtest, self.cfg["tol"], self.cfg["max_iterations"],
                                       self.preconditioner())
 
@@ -1014,10 +1117,27 @@ class GpModel:
         M = self.preconditioner()
         if M is None:
             raise LogicError("randomized variance needs the preconditioner enabled")
+        if self.backend != "dski":  # gp.cpp:519-547 over the assembled cross-covariance
+            Kc = self.cross_covariance(Xtest)
+            T = Kc.shape[1]
+            base = self.prior_variance() - np.asarray(M.quadratic(Kc), dtype=np.float64).reshape(T)
+            if probes <= 0:
+                return base
+            corr = np.zeros(T)
+            for p in range(probes):
+                z = rademacher_vector(T, seed, 9000 + p)
+                w = Kc @ z
+                corr += z * (Kc.T @ (np.asarray(self.solve(w)) - np.asarray(M.apply(w))))
+            return base - corr / probes
         return predict_variance_randomized(self.op(), M, Xtest, probes, seed, self.cfg["tol"],
                                            self.cfg["max_iterations"])
 
     def dlogell_apply(self, v):
+        """GpModel::dlogell_apply (gp.cpp:200-218)."""
+        if self.backend == "exact":
+            M = assemble_dense(self.kernel, self.X, None, self.has_gradients, dlogell=True,
+                               size_cap=self.cfg["dense_size_cap"], device=self.device)
+            return M @ np.asarray(v, dtype=np.float64)
         return self.op().dlogell_apply(v)
 
     def fit(self, max_iterations=40, restarts=3, initial_step=0.3, min_step=1e-4, optimize_noise=True, seed=0):

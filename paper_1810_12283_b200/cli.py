@@ -10,10 +10,8 @@ common.cpp:86-100 classifies exceptions). Run as
 The operators, solves, log-determinants, gradients and predictions all run in
 libgk_b200.so on the GPU; this module is argument parsing, file I/O and the
 host control flow of the tools. Differences from the reference tools:
-  - `--backend` defaults to "dski": the reference's default "exact" backend
-    (dense Cholesky, gp.cpp:71-84) is not on the B200 path; fit/predict with
-    it exit 2 (config error) naming the supported backends. benchmark-mvm
-    times "exact" through the matrix-free device operator (ExactOperator).
+  - benchmark-mvm times "exact" through the matrix-free device operator
+    (ExactOperator) instead of an assembled DenseOperator (same product).
   - `--kernel spline` runs on the dski backend (K_UU by circulant embedding
     and an in-house FFT); dskip rejects it like the reference
     (dskip.cpp:118-121, exit 2).
@@ -52,8 +50,8 @@ def _onoff(v: str) -> bool:
 def add_common_flags(p: argparse.ArgumentParser) -> None:
     """add_common_flags (proj/tools/common.cpp:14-37)."""
     p.add_argument("--kernel", default="se", choices=["se", "spline"], help="kernel family")
-    p.add_argument("--backend", default="dski", choices=["exact", "dski", "dskip"],
-                   help="kernel operator backend (dski, dskip on the GPU)")
+    p.add_argument("--backend", default="exact", choices=["exact", "dski", "dskip"],
+                   help="kernel operator backend (exact, dski, dskip)")
     p.add_argument("--ell", type=float, default=0.0, help="initial lengthscale (0: heuristic)")
     p.add_argument("--outputscale", type=float, default=0.0, help="initial output scale (0: heuristic)")
     p.add_argument("--noise", type=float, default=1e-2, help="value noise sigma1")
@@ -95,8 +93,6 @@ def make_kernel(a, X):
 def build_model(kernel, X, y, dY, noise_value, noise_gradient, cfg):
     """GpModel(kernel, data, cfg) with the tool's config (gp.cpp:33-44)."""
     gk = _gk()
-    if cfg.backend == "exact":
-        raise ConfigError("backend 'exact' (dense Cholesky) is not on the B200 path; use --backend dski or dskip")
     return gk.GpModel(kernel, X, y, dY, noise=(noise_value, noise_gradient), backend=cfg.backend,
                       grid_ratio=cfg.grid_ratio, max_grid_nodes=cfg.max_grid_nodes, dskip_rank=cfg.dskip_rank,
                       tol=cfg.cg_tol, max_iterations=cfg.cg_maxit, use_preconditioner=cfg.precond,
@@ -157,8 +153,6 @@ def run_predict(a) -> None:
         kernel = gk.KernelSpec(m.lengthscale, m.outputscale)
     model = build_model(kernel, X, y, dY, m.noise_value, m.noise_gradient, m.config)
     model.set_hyperparameters(kernel, m.noise_value, m.noise_gradient)
-    if model.backend != "dski":
-        raise ConfigError("predict on the B200 path needs the dski backend (cross-covariances are D-SKI)")
     Xtest = np.asfortranarray(Xtest)
     mean, grads = model.predict_mean_grad(Xtest)
     if a.variance == "randomized":

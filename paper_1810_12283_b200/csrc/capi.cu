@@ -27,6 +27,13 @@ std::unique_ptr<Op> make_dski(const gk_kernel& k, const gk_grid& g, const double
 std::unique_ptr<Op> make_exact(const gk_kernel& k, const double* X, i64 n, int d, double nv, double ng,
                                int with_grad, int device);
 std::unique_ptr<Op> make_dense(const double* A, i64 N, int device);
+std::unique_ptr<Op> make_dense_kernel(const gk_kernel& k, const double* X, i64 n, int d, double nv, double ng,
+                                      int with_grad, i64 size_cap, int device);
+void assemble_dense_dev(const gk_kernel& k, const double* dX, i64 n, const double* dXp, i64 np, int d, bool deriv,
+                        bool dl, double c, double* out, i64 ld, cudaStream_t s);
+void dense_chol_solve(Op& o, const double* dB, double* dX, int nrhs, cudaStream_t s);
+double dense_chol_logdet(Op& o);
+void dense_exact_lml_gradient(Op& o, const double* alpha_h, double* grad, int* nparams);
 std::unique_ptr<Op> make_dskip_from_factors(i64 n, int groups, double nv, double ng, int nf, const i64* ranks,
                                             const double* const* Q, const double* const* alpha,
                                             const double* const* beta, int device);
@@ -305,6 +312,76 @@ gk_status gk_dense_create(const double* A, int64_t N, int device, gk_op** out) {
     auto h = std::make_unique<gk_op>();
     h->impl = make_dense(A, N, device);
     *out = h.release();
+  });
+}
+
+gk_status gk_assemble_dense(const gk_kernel* kernel, const double* X, int64_t n, const double* Xp, int64_t np, int d,
+                            int with_derivatives, int dlogell, double derivative_scale, int64_t size_cap, int device,
+                            double* out) {
+  return guard([&] {
+    if (!kernel || !X || !Xp || !out) fail(GK_ERR_ARG, "null argument");
+    if (kernel->family != 0 && kernel->family != 1) fail(GK_ERR_ARG, "unknown kernel family");
+    if (n < 0 || np < 0 || d < 1) fail(GK_ERR_ARG, "point sets have mismatched dimensions");
+    const i64 rows = with_derivatives ? n * (d + 1) : n, cols = with_derivatives ? np * (d + 1) : np;
+    if (rows * cols > size_cap)
+      fail(GK_ERR_LENGTH, "dense assembly of " + std::to_string(rows) + " x " + std::to_string(cols) +
+                              " exceeds the configured size cap");
+    if (rows * cols == 0) return;
+    DeviceGuard dg(device);
+    cudaStream_t s = nullptr;
+    GK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    DevBuf<double> dX(static_cast<size_t>(n) * d), dXp(static_cast<size_t>(np) * d), K(static_cast<size_t>(rows) * cols);
+    dX.upload(X, static_cast<size_t>(n) * d, s);
+    dXp.upload(Xp, static_cast<size_t>(np) * d, s);
+    assemble_dense_dev(*kernel, dX.p, n, dXp.p, np, d, with_derivatives != 0, dlogell != 0, derivative_scale, K.p, rows, s);
+    GK_CUDA(cudaMemcpyAsync(out, K.p, sizeof(double) * rows * cols, cudaMemcpyDeviceToHost, s));
+    GK_CUDA(cudaStreamSynchronize(s));
+    cudaStreamDestroy(s);
+  });
+}
+
+gk_status gk_dense_kernel_create(const gk_kernel* kernel, const double* X, int64_t n, int d, double nv, double ng,
+                                 int with_gradients, int64_t size_cap, int device, gk_op** out) {
+  return guard([&] {
+    auto h = std::make_unique<gk_op>();
+    h->impl = make_dense_kernel(*kernel, X, n, d, nv, ng, with_gradients, size_cap, device);
+    *out = h.release();
+  });
+}
+
+gk_status gk_dense_cholesky_solve(const gk_op* h, const double* B, int64_t ldb, int64_t nrhs, double* X, int64_t ldx) {
+  return guard([&] {
+    Op& op = O(h);
+    if (nrhs < 0 || ldb < op.N || ldx < op.N) fail(GK_ERR_ARG, "solve size mismatch");
+    if (nrhs == 0) return;
+    DeviceGuard dg(op.device);
+    cudaStream_t s = op.stream;
+    OpSession ss(op, s);
+    DevBuf<double> d(static_cast<size_t>(op.N) * nrhs);
+    GK_CUDA(cudaMemcpy2DAsync(d.p, sizeof(double) * op.N, B, sizeof(double) * ldb, sizeof(double) * op.N, nrhs,
+                              cudaMemcpyHostToDevice, s));
+    dense_chol_solve(op, d.p, d.p, int(nrhs), s);
+    GK_CUDA(cudaMemcpy2DAsync(X, sizeof(double) * ldx, d.p, sizeof(double) * op.N, sizeof(double) * op.N, nrhs,
+                              cudaMemcpyDeviceToHost, s));
+    GK_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+gk_status gk_dense_cholesky_logdet(const gk_op* h, double* logdet) {
+  return guard([&] {
+    Op& op = O(h);
+    DeviceGuard dg(op.device);
+    OpSession ss(op, op.stream);
+    *logdet = dense_chol_logdet(op);
+  });
+}
+
+gk_status gk_dense_exact_lml_gradient(const gk_op* h, const double* alpha, double* grad, int* nparams) {
+  return guard([&] {
+    Op& op = O(h);
+    DeviceGuard dg(op.device);
+    OpSession ss(op, op.stream);
+    dense_exact_lml_gradient(op, alpha, grad, nparams);
   });
 }
 

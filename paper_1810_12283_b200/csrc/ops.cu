@@ -3,8 +3,13 @@
 // K∇ of reference kernels.cpp:242-285, never materialised) and an explicit
 // dense operator (linear_operator.hpp:38-56) used by solver tests.
 #include <cmath>
+#include <dlfcn.h>
+#include <string>
+#include <type_traits>
+#include <cusolverDn.h>
 
 #include "gk_kernels.cuh"
+#include "solvers.hpp"
 
 namespace gk {
 
@@ -92,6 +97,68 @@ __device__ __forceinline__ void kpair(const KParams& K, double r2, double& k, do
     g = -K.s2 * c;
     al = g;
     be = -K.s2 * 2.0 / (K.ell2 * r2);
+  }
+}
+
+// The same decomposition for ∂/∂log ℓ of the kernel (eval_dlogell,
+// eval_grad_dlogell, eval_hess_dlogell, kernels.cpp:172-240).
+__device__ __forceinline__ void kpair_dl(const KParams& K, double r2, double& k, double& g, double& al,
+                                         double& be) {
+  if (K.family == 0) {
+    const double kv = K.s2 * exp(-0.5 * r2 / K.ell2), rho2 = r2 / K.ell2;
+    k = kv * rho2;
+    g = kv / K.ell2 * (rho2 - 2.0);
+    al = g;
+    be = -kv / (K.ell2 * K.ell2) * (rho2 - 4.0);
+    return;
+  }
+  if (r2 == 0.0) {
+    k = 0.0;
+    g = 0.0;
+    al = 4.0 * K.a * K.s2 / K.ell2;
+    be = 0.0;
+    return;
+  }
+  const double r = sqrt(r2), rho2 = r2 / K.ell2, rho = sqrt(rho2);
+  if (!K.even) {
+    k = K.s2 * (-3.0 * rho * rho2 - 2.0 * K.a * rho2);
+    g = K.s2 * (9.0 * r / (K.ell2 * K.ell) + 4.0 * K.a / K.ell2);
+    al = g;
+    be = K.s2 * 9.0 / (r * K.ell2 * K.ell);
+  } else {
+    const double lr = log(r / K.ell);
+    k = K.s2 * (-2.0 * rho2 * log(rho) - rho2 - 2.0 * K.a * rho2);
+    g = 2.0 * K.s2 * (2.0 * lr + 2.0 + 2.0 * K.a) / K.ell2;
+    al = g;
+    be = 2.0 * K.s2 / K.ell2 * (2.0 / r2);
+  }
+}
+
+// assemble_dense (kernels.cpp:242-285): K(X, X') in type-major blocks, one
+// thread per point pair writing its (d+1)² entries; dl: ∂K/∂log ℓ; scale c
+// > 0 multiplies derivative rows and columns (AssemblyOptions, kernels.hpp:83-92).
+constexpr int kAsmMaxD = 16;
+__global__ void k_assemble_dense(const double* __restrict__ X, i64 n, const double* __restrict__ Xp, i64 np, int d,
+                                 KParams K, int with_deriv, int dl, double c, double* __restrict__ out, i64 ld) {
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < n * np; e += (i64)gridDim.x * blockDim.x) {
+    const i64 i = e % n, j = e / n;
+    double u[kAsmMaxD], r2 = 0.0;
+    for (int p = 0; p < d; ++p) {
+      u[p] = X[p * n + i] - Xp[p * np + j];
+      r2 += u[p] * u[p];
+    }
+    double k, g, al, be;
+    if (dl) kpair_dl(K, r2, k, g, al, be);
+    else kpair(K, r2, k, g, al, be);
+    out[j * ld + i] = k;
+    if (!with_deriv) continue;
+    const double cs = c > 0.0 ? c : 1.0;
+    for (int p = 0; p < d; ++p) {
+      out[((p + 1) * np + j) * ld + i] = cs * g * u[p];   // d/dx'_p columns
+      out[j * ld + (p + 1) * n + i] = -cs * g * u[p];     // d/dx_p rows
+      for (int q = 0; q < d; ++q)
+        out[((q + 1) * np + j) * ld + (p + 1) * n + i] = cs * cs * ((p == q ? al : 0.0) + be * u[p] * u[q]);
+    }
   }
 }
 
@@ -357,8 +424,91 @@ std::unique_ptr<Op> make_exact(const gk_kernel& k, const double* X, i64 n, int d
 }
 
 // ---------------------------------------------------------------- dense
+// cuSOLVER's dense Cholesky (potrf/potrs/potri) for the exact GpModel backend
+// (the reference's Eigen LLT, gp.cpp:71-85,146,167,246-276) — not on the
+// D-SKI/D-SKIP hot path. Loaded with dlopen on first use by soname, so a
+// copy the process already mapped (e.g. torch's) is reused.
+struct CusolverApi {
+  bool ok = false;
+  std::string err;
+  cusolverStatus_t (*create)(cusolverDnHandle_t*) = nullptr;
+  cusolverStatus_t (*destroy)(cusolverDnHandle_t) = nullptr;
+  cusolverStatus_t (*set_stream)(cusolverDnHandle_t, cudaStream_t) = nullptr;
+  cusolverStatus_t (*potrf_bs)(cusolverDnHandle_t, cublasFillMode_t, int, double*, int, int*) = nullptr;
+  cusolverStatus_t (*potrf)(cusolverDnHandle_t, cublasFillMode_t, int, double*, int, double*, int, int*) = nullptr;
+  cusolverStatus_t (*potrs)(cusolverDnHandle_t, cublasFillMode_t, int, int, const double*, int, double*, int,
+                            int*) = nullptr;
+  cusolverStatus_t (*potri_bs)(cusolverDnHandle_t, cublasFillMode_t, int, double*, int, int*) = nullptr;
+  cusolverStatus_t (*potri)(cusolverDnHandle_t, cublasFillMode_t, int, double*, int, double*, int, int*) = nullptr;
+};
+static CusolverApi& cusolver() {
+  static CusolverApi api = [] {
+    CusolverApi a;
+    void* h = dlopen("libcusolver.so.11", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      a.err = dlerror();
+      return a;
+    }
+    auto sym = [&](auto& f, const char* name) { f = reinterpret_cast<std::decay_t<decltype(f)>>(dlsym(h, name)); };
+    sym(a.create, "cusolverDnCreate");
+    sym(a.destroy, "cusolverDnDestroy");
+    sym(a.set_stream, "cusolverDnSetStream");
+    sym(a.potrf_bs, "cusolverDnDpotrf_bufferSize");
+    sym(a.potrf, "cusolverDnDpotrf");
+    sym(a.potrs, "cusolverDnDpotrs");
+    sym(a.potri_bs, "cusolverDnDpotri_bufferSize");
+    sym(a.potri, "cusolverDnDpotri");
+    a.ok = a.create && a.destroy && a.set_stream && a.potrf_bs && a.potrf && a.potrs && a.potri_bs && a.potri;
+    if (!a.ok) a.err = "cuSOLVER symbols missing";
+    return a;
+  }();
+  if (!api.ok) fail(GK_ERR_CUDA, "cuSOLVER (dense Cholesky of the exact backend) unavailable: " + api.err);
+  return api;
+}
+static void sol_check(cusolverStatus_t st, const char* what) {
+  if (st != CUSOLVER_STATUS_SUCCESS) fail(GK_ERR_CUDA, std::string(what) + ": cuSOLVER status " + std::to_string(int(st)));
+}
+
+__global__ void k_add_noise_diag(double* __restrict__ A, i64 N, i64 n, double nv2, double ng2) {
+  for (i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x; r < N; r += (i64)gridDim.x * blockDim.x)
+    A[r * N + r] += r < n ? nv2 : ng2;
+}
+// log det = 2 Σ log L_ii, one block, fixed order (gp.cpp:167-168)
+__global__ void k_chol_logdet(const double* __restrict__ L, i64 N, double* __restrict__ out) {
+  __shared__ double sm[256];
+  double acc = 0.0;
+  for (i64 r = threadIdx.x; r < N; r += blockDim.x) acc += log(L[r * N + r]);
+  sm[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < 256; ++k) t += sm[k];
+    *out = 2.0 * t;
+  }
+}
+// fill the upper triangle of a lower-stored symmetric matrix
+__global__ void k_symmetrize_lower(double* __restrict__ A, i64 N) {
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < N * N; e += (i64)gridDim.x * blockDim.x) {
+    const i64 r = e % N, c = e / N;
+    if (r < c) A[c * N + r] = A[r * N + c];
+  }
+}
+
 struct DenseOp final : Op {
   DevBuf<double> A;
+  // exact-backend state (make_dense_kernel): the Cholesky factor and the data
+  DevBuf<double> L;
+  cusolverDnHandle_t sol = nullptr;
+  DevBuf<int> info;
+  DevBuf<double> work;
+  bool kernel_built = false;
+  KParams K{};
+  DevBuf<double> X;
+  i64 n = 0;
+  int d = 0, G = 0;
+  ~DenseOp() override {
+    if (sol) cusolver().destroy(sol);
+  }
   void mvm(const double* in, double* out, int nrhs, cudaStream_t s) override {
     k_dense_mvm<<<blocks_for(N * nrhs), 256, 0, s>>>(A.p, N, in, out, nrhs);
     launched("dense mvm");
@@ -373,6 +523,152 @@ struct DenseOp final : Op {
     launched("dense row");
   }
 };
+
+// assemble_dense(kernel, X, X') on the device into out (rows × cols,
+// column-major, leading dimension ld) — shared by gk_assemble_dense and the
+// exact backend.
+void assemble_dense_dev(const gk_kernel& k, const double* dX, i64 n, const double* dXp, i64 np, int d, bool deriv,
+                        bool dl, double c, double* out, i64 ld, cudaStream_t s) {
+  if (d > kAsmMaxD) fail(GK_ERR_UNSUPPORTED, "dense assembly supports d <= 16");
+  const KParams K{k.family, k.outputscale * k.outputscale, k.lengthscale, k.lengthscale * k.lengthscale,
+                  k.spline_a, k.spline_b, k.spline_even};
+  k_assemble_dense<<<blocks_for(n * np), 256, 0, s>>>(dX, n, dXp, np, d, K, deriv ? 1 : 0, dl ? 1 : 0, c, out, ld);
+  launched("assemble dense");
+}
+
+// GpModel's exact operator (gp.cpp:71-85): K = assemble_dense + noise on the
+// device and its Cholesky factor; not positive definite -> runtime_error.
+std::unique_ptr<Op> make_dense_kernel(const gk_kernel& k, const double* X, i64 n, int d, double nv, double ng,
+                                      int with_grad, i64 size_cap, int device) {
+  if (k.family != 0 && k.family != 1) fail(GK_ERR_ARG, "unknown kernel family");
+  if (!(k.lengthscale > 0.0)) fail(GK_ERR_ARG, "lengthscale must be > 0");
+  if (!(k.outputscale > 0.0)) fail(GK_ERR_ARG, "outputscale must be > 0");
+  if (n < 1 || d < 1) fail(GK_ERR_ARG, "dense kernel operator needs points");
+  const i64 N = with_grad ? n * (d + 1) : n;
+  if (N * N > size_cap)
+    fail(GK_ERR_LENGTH, "dense assembly of " + std::to_string(N) + " x " + std::to_string(N) +
+                            " exceeds the configured size cap");
+  if (N >= (i64(1) << 31)) fail(GK_ERR_UNSUPPORTED, "dense operator too large");
+  DeviceGuard dg(device);
+  auto op = std::make_unique<DenseOp>();
+  op->kind = KIND_DENSE;
+  op->device = device;
+  op->N = N;
+  op->n_value = n;
+  op->n = n;
+  op->d = d;
+  op->G = with_grad ? d : 0;
+  op->nv2 = nv * nv;
+  op->ng2 = ng * ng;
+  op->kernel_built = true;
+  op->K = KParams{k.family, k.outputscale * k.outputscale, k.lengthscale, k.lengthscale * k.lengthscale,
+                  k.spline_a, k.spline_b, k.spline_even};
+  op->init_stream();
+  cudaStream_t s = op->stream;
+  op->X.upload(X, static_cast<size_t>(n) * d, s);
+  op->A.alloc(static_cast<size_t>(N) * N);
+  assemble_dense_dev(k, op->X.p, n, op->X.p, n, d, with_grad != 0, false, 0.0, op->A.p, N, s);
+  k_add_noise_diag<<<blocks_for(N), 256, 0, s>>>(op->A.p, N, n, op->nv2, op->ng2);
+  launched("dense noise diagonal");
+  auto& api = cusolver();
+  sol_check(api.create(&op->sol), "cusolverDnCreate");
+  sol_check(api.set_stream(op->sol, s), "cusolverDnSetStream");
+  op->L.alloc(static_cast<size_t>(N) * N);
+  GK_CUDA(cudaMemcpyAsync(op->L.p, op->A.p, sizeof(double) * N * N, cudaMemcpyDeviceToDevice, s));
+  int lwork = 0;
+  sol_check(api.potrf_bs(op->sol, CUBLAS_FILL_MODE_LOWER, int(N), op->L.p, int(N), &lwork), "potrf buffer size");
+  op->work.alloc(static_cast<size_t>(std::max(1, lwork)));
+  op->info.alloc(1);
+  sol_check(api.potrf(op->sol, CUBLAS_FILL_MODE_LOWER, int(N), op->L.p, int(N), op->work.p, lwork, op->info.p),
+            "potrf");
+  int info_h = 0;
+  GK_CUDA(cudaMemcpyAsync(&info_h, op->info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GK_CUDA(cudaStreamSynchronize(s));
+  if (info_h != 0) fail(GK_ERR_RUNTIME, "dense kernel matrix is not positive definite");
+  return op;
+}
+
+static DenseOp& factored(Op& o) {
+  if (o.kind != KIND_DENSE || !static_cast<DenseOp&>(o).kernel_built)
+    fail(GK_ERR_LOGIC, "operator has no dense Cholesky factor (build it with gk_dense_kernel_create)");
+  return static_cast<DenseOp&>(o);
+}
+
+// X = K⁻¹ B by the Cholesky factor (llt_->solve, gp.cpp:146); device,
+// column-major N × nrhs blocks (in place when dB == dX).
+void dense_chol_solve(Op& o, const double* dB, double* dX, int nrhs, cudaStream_t s) {
+  DenseOp& op = factored(o);
+  auto& api = cusolver();
+  if (dB != dX) GK_CUDA(cudaMemcpyAsync(dX, dB, sizeof(double) * op.N * nrhs, cudaMemcpyDeviceToDevice, s));
+  sol_check(api.set_stream(op.sol, s), "cusolverDnSetStream");
+  sol_check(api.potrs(op.sol, CUBLAS_FILL_MODE_LOWER, int(op.N), nrhs, op.L.p, int(op.N), dX, int(op.N), op.info.p),
+            "potrs");
+}
+
+double dense_chol_logdet(Op& o) {
+  DenseOp& op = factored(o);
+  DevBuf<double> out(1);
+  k_chol_logdet<<<1, 256, 0, op.stream>>>(op.L.p, op.N, out.p);
+  launched("dense logdet");
+  double h = 0.0;
+  GK_CUDA(cudaMemcpyAsync(&h, out.p, sizeof(double), cudaMemcpyDeviceToHost, op.stream));
+  GK_CUDA(cudaStreamSynchronize(op.stream));
+  return h;
+}
+
+// GpModel::lml_gradient, exact branch (gp.cpp:246-276): Kinv from the
+// factor, ∂K/∂log ℓ assembled on the device, traces as fixed-order dots.
+void dense_exact_lml_gradient(Op& o, const double* alpha_h, double* grad, int* nparams) {
+  DenseOp& op = factored(o);
+  auto& api = cusolver();
+  cudaStream_t s = op.stream;
+  const i64 N = op.N, n = op.n;
+  DevBuf<double> Kinv(static_cast<size_t>(N) * N), Mell(static_cast<size_t>(N) * N), a(static_cast<size_t>(N)),
+      t(static_cast<size_t>(N)), ones(static_cast<size_t>(N)), dots(8), part;
+  GK_CUDA(cudaMemcpyAsync(Kinv.p, op.L.p, sizeof(double) * N * N, cudaMemcpyDeviceToDevice, s));
+  int lwork = 0;
+  sol_check(api.set_stream(op.sol, s), "cusolverDnSetStream");
+  sol_check(api.potri_bs(op.sol, CUBLAS_FILL_MODE_LOWER, int(N), Kinv.p, int(N), &lwork), "potri buffer size");
+  op.work.reserve(static_cast<size_t>(std::max(1, lwork)));
+  sol_check(api.potri(op.sol, CUBLAS_FILL_MODE_LOWER, int(N), Kinv.p, int(N), op.work.p, lwork, op.info.p), "potri");
+  k_symmetrize_lower<<<blocks_for(N * N), 256, 0, s>>>(Kinv.p, N);
+  launched("dense symmetrize");
+  gk_kernel kk{op.K.family, op.K.ell, std::sqrt(op.K.s2), op.K.a, op.K.b, op.K.even};
+  assemble_dense_dev(kk, op.X.p, n, op.X.p, n, op.d, op.G > 0, true, 0.0, Mell.p, N, s);
+  a.upload(alpha_h, static_cast<size_t>(N), s);
+  // t = Mell a; data_ell = a·t; tr_ell = Σ Kinv ⊙ Mell
+  rows_gemm_dev(Mell.p, int(N), a.p, 1, N, t.p, false, s);  // Mell symmetric: row r · a
+  col_dots_dev(a.p, t.p, N, 1, dots.p + 0, part, s);
+  col_dots_dev(Kinv.p, Mell.p, N * N, 1, dots.p + 1, part, s);
+  // Ka = (K − noise) a = A a − nd ⊙ a
+  rows_gemm_dev(op.A.p, int(N), a.p, 1, N, t.p, false, s);
+  col_dots_dev(a.p, t.p, N, 1, dots.p + 2, part, s);
+  std::vector<double> dh(3), diag(static_cast<size_t>(N)), ah(alpha_h, alpha_h + N);
+  GK_CUDA(cudaMemcpyAsync(dh.data(), dots.p, sizeof(double) * 3, cudaMemcpyDeviceToHost, s));
+  GK_CUDA(cudaMemcpy2DAsync(diag.data(), sizeof(double), Kinv.p, sizeof(double) * (N + 1), sizeof(double), N,
+                            cudaMemcpyDeviceToHost, s));
+  GK_CUDA(cudaStreamSynchronize(s));
+  const double sv2 = op.nv2, sg2 = op.ng2;
+  double aKa = dh[2];
+  for (i64 r = 0; r < N; ++r) aKa -= (r < n ? sv2 : sg2) * ah[static_cast<size_t>(r)] * ah[static_cast<size_t>(r)];
+  double dnd = 0.0, trh = 0.0, trt = 0.0, ah2 = 0.0, at2 = 0.0;
+  for (i64 r = 0; r < N; ++r) {
+    const double kd = diag[static_cast<size_t>(r)];
+    dnd += kd * (r < n ? sv2 : sg2);
+    if (r < n) {
+      trh += kd;
+      ah2 += ah[static_cast<size_t>(r)] * ah[static_cast<size_t>(r)];
+    } else {
+      trt += kd;
+      at2 += ah[static_cast<size_t>(r)] * ah[static_cast<size_t>(r)];
+    }
+  }
+  grad[0] = 0.5 * (dh[0] - dh[1]);
+  grad[1] = 0.5 * (2.0 * aKa - 2.0 * (double(N) - dnd));
+  grad[2] = 0.5 * (2.0 * sv2 * ah2 - 2.0 * sv2 * trh);
+  *nparams = op.G > 0 ? 4 : 3;
+  if (op.G > 0) grad[3] = 0.5 * (2.0 * sg2 * at2 - 2.0 * sg2 * trt);
+}
 
 std::unique_ptr<Op> make_dense(const double* A, i64 N, int device) {
   if (N < 1) fail(GK_ERR_ARG, "dense operator needs N >= 1");

@@ -125,8 +125,7 @@ def test_cli_exit_codes_without_device_work(tmp_path):
     data = _write(tmp_path / "d.csv", "x1,x2,y\n0.1,0.2,1\n0.3,0.4,2\n")
     assert cli.main(["fit", "--data", str(tmp_path / "missing.csv")]) == cli.EXIT_DATA
     assert cli.main(["fit", "--data", _write(tmp_path / "bad.csv", "x1,y\n1,oops\n")]) == cli.EXIT_DATA
-    assert cli.main(["fit", "--data", data, "--kernel", "spline", "--backend", "exact"]) == cli.EXIT_CONFIG
-    assert cli.main(["fit", "--data", data, "--backend", "exact"]) == cli.EXIT_CONFIG
+    assert cli.main(["fit", "--data", data, "--backend", "gpu"]) == cli.EXIT_CONFIG  # not a backend
     assert cli.main(["fit", "--data", data, "--precond", "maybe"]) == cli.EXIT_CONFIG  # parse error
     assert cli.main(["fit"]) == cli.EXIT_CONFIG  # --data is required
     # "is not a gradkrig model file" matches none of common.cpp:92-98's data

@@ -168,3 +168,32 @@ def test_cli_spline_kernel_fit_and_predict(tmp_path):
     P = np.array(list(csv.reader(open(out)))[1:], dtype=float)
     assert P.shape == (5, 4) and np.all(np.isfinite(P))
     assert np.max(np.abs(P[:, 2] - y[:5])) < 0.5  # the mean interpolates its own (noisy) training values
+
+
+def test_cli_default_exact_backend(tmp_path):
+    """The tools' default backend "exact" (dense K∇ + Cholesky, gp.cpp:71-85):
+    fit → JSON → predict with the exact variance equals numpy on the oracle's
+    dense assembly at the fitted hyperparameters."""
+    X, y, dY = O.sample_test_function("franke", 100, 8, (0.05, 0.05))
+    data = str(tmp_path / "train.csv")
+    gio.write_dataset_csv(data, gio.Dataset(X, y, dY))
+    model = str(tmp_path / "model.json")
+    assert cli.main(["fit", "--data", data, "--model", model, "--ell", "0.3", "--noise", "0.2", "--noise-grad", "0.2",
+                     "--iters", "2", "--restarts", "1", "--probes", "8"]) == 0
+    j = json.load(open(model))
+    assert j["backend"] == "exact"
+    test = str(tmp_path / "test.csv")
+    Xt = O.sample_test_function("franke", 5, 21)[0]
+    gio.write_csv(test, ["x1", "x2"], Xt.tolist())
+    out = str(tmp_path / "pred.csv")
+    assert cli.main(["predict", "--model", model, "--test", test, "--out", out, "--variance", "exact"]) == 0
+    P = np.array(list(csv.reader(open(out)))[1:], dtype=float)
+    ko = O.KernelSpec(j["kernel"]["lengthscale"], j["kernel"]["outputscale"])
+    s1, s2 = j["noise"]["value"], j["noise"]["gradient"]
+    K = O.assemble_dense(ko, X) + np.diag(np.concatenate([np.full(100, s1 ** 2), np.full(200, s2 ** 2)]))
+    t = O.stacked_targets(y, dY, y.mean())
+    Q = O.assemble_dense(ko, X, Xt)[:300, :5]
+    mu = y.mean() + Q.T @ np.linalg.solve(K, t)
+    var = j["kernel"]["outputscale"] ** 2 - np.einsum("ij,ij->j", Q, np.linalg.solve(K, Q))
+    assert np.max(np.abs(P[:, 2] - mu)) <= 1e-9 * np.max(np.abs(mu))
+    assert np.max(np.abs(P[:, 3] - var)) <= 1e-9

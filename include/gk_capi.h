@@ -175,7 +175,7 @@ gk_status gk_exact_create(const gk_kernel* kernel, const double* X, int64_t n, i
 
 void gk_op_destroy(gk_op* op);
 int64_t gk_op_size(const gk_op* op);
-/* 0 = exact, 1 = dski, 2 = dskip, 3 = dense */
+/* 0 = exact, 1 = dski, 2 = dskip, 3 = dense, 4 = grid kernel (K_UU) */
 int gk_op_kind(const gk_op* op);
 
 /* LinearOperator::mvm over nrhs columns: Out = A V (host pointers). */
@@ -201,6 +201,20 @@ gk_status gk_dski_get_grid(const gk_op* op, gk_grid* out);
  * (2(m_j − 1) nodes per axis) of the operator's profile, computed on the host
  * (separable cosine sums in long double; O(E·ΣE_j), seconds at C4). */
 gk_status gk_dski_min_embedding_eigenvalue(const gk_op* op, double* out);
+/* Profile-agnostic forms: the caller evaluates its
+ * StationaryProfile where the reference's constructors do and passes the
+ * values. slice = the profile on the reference's circulant embedding,
+ * 2(m_j − 1) nodes per axis, row-major, entry t at the wrapped offsets
+ * (i_j ≤ m_j − 1 ? i_j : i_j − 2(m_j − 1))·h_j (dski.cpp:97-114).
+ * GridKernelOperator(grid, profile) (dski.cpp:80-172): K_UU as an operator of
+ * size M (mvm, diagonal, row; gk_dski_min_embedding_eigenvalue works on it).
+ * D-SKI from a profile: offset_table = the profile at the (2T − 1)^d stencil
+ * offsets (i_j − (T − 1))·h_j, row-major (kernel_offset_table_, dski.cpp:
+ * 181-203; T = 6 quintic, 4 cubic). Such an operator has no ∂/∂log ℓ. */
+gk_status gk_grid_kernel_create(const gk_grid* grid, const double* slice, int device, gk_op** out);
+gk_status gk_dski_create_from_profile(const gk_grid* grid, const double* X, int64_t n, double noise_value,
+                                      double noise_gradient, int order, int with_gradients, const double* slice,
+                                      const double* offset_table, int device, gk_op** out);
 gk_status gk_dski_transpose_apply(const gk_op* op, const double* V, int64_t ldv, double* U,
                                   int64_t ldu, int64_t nrhs);
 gk_status gk_dski_apply(const gk_op* op, const double* U, int64_t ldu, double* Out, int64_t ldo,

@@ -90,6 +90,9 @@ _SIGS = {
     "gk_op_from_internal_dev": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp]),
     "gk_dski_grid_size": (_i64, [_vp]),
     "gk_dski_get_grid": (C.c_int, [_vp, C.POINTER(GkGrid)]),
+    "gk_grid_kernel_create": (C.c_int, [C.POINTER(GkGrid), _dp, C.c_int, C.POINTER(_vp)]),
+    "gk_dski_create_from_profile": (C.c_int, [C.POINTER(GkGrid), _dp, _i64, _d, _d, C.c_int, C.c_int, _dp, _dp,
+                                              C.c_int, C.POINTER(_vp)]),
     "gk_assemble_dense": (C.c_int, [C.POINTER(GkKernel), _dp, _i64, _dp, _i64, C.c_int, C.c_int, C.c_int, _d, _i64,
                                     C.c_int, _dp]),
     "gk_dense_kernel_create": (C.c_int, [C.POINTER(GkKernel), _dp, _i64, C.c_int, _d, _d, C.c_int, _i64, C.c_int,
@@ -428,6 +431,25 @@ class DskiOperator(LinearOperator):
                                  float(noise[0]), float(noise[1]), int(order),
                                  int(with_gradients), device), device)
 
+    @classmethod
+    def from_profile(cls, grid: Grid, X, slice_ref, offset_table, noise=(0.0, 0.0), order=0, with_gradients=True,
+                     device=0):
+        """DskiOperator over a caller-evaluated stationary profile: slice_ref on
+        the reference embedding (2(m_j − 1) per axis), offset_table at the
+        (2T − 1)^d stencil offsets (gk_dski_create_from_profile)."""
+        X = _f64(X, True)
+        if X.ndim != 2 or X.shape[1] != grid.d:
+            raise ValueError("interpolation points do not match grid dimension")
+        self = cls.__new__(cls)
+        self.n, self.d = X.shape
+        self.kernel, self.grid, self.noise = None, grid, tuple(noise)
+        g = grid.c()
+        sl, ot = _f64(np.ravel(slice_ref)), _f64(np.ravel(offset_table))
+        LinearOperator.__init__(self, _create(_lib.gk_dski_create_from_profile, C.byref(g), _p(X), self.n,
+                                              float(noise[0]), float(noise[1]), int(order), int(with_gradients),
+                                              _p(sl), _p(ot), device), device)
+        return self
+
     def points(self):
         return self.n
 
@@ -544,6 +566,33 @@ class DenseOperator(LinearOperator):
         if A.ndim != 2 or A.shape[0] != A.shape[1]:
             raise ValueError("dense operator must be square")
         super().__init__(_create(_lib.gk_dense_create, _p(A), A.shape[0], device), device)
+
+
+class GridKernelOperator(LinearOperator):
+    """GridKernelOperator(grid, profile) (dski.hpp:20-50, dski.cpp:80-172):
+    K_UU over the grid for a stationary profile given as its values on the
+    reference's circulant embedding (2(m_j − 1) nodes per axis, wrapped
+    offsets, row-major); applied by circulant embedding + FFT on the device."""
+
+    def __init__(self, grid: Grid, slice_ref, device=0):
+        self.grid = grid
+        g = grid.c()
+        sl = _f64(np.ravel(slice_ref))
+        super().__init__(_create(_lib.gk_grid_kernel_create, C.byref(g), _p(sl), device), device)
+
+    @staticmethod
+    def embedding_offsets(grid: Grid):
+        """The wrapped offsets (E' × d, row-major over E'_j = 2(m_j − 1)) at
+        which the slice is evaluated (dski.cpp:97-114)."""
+        E = [2 * (int(m) - 1) for m in grid.dims]
+        idx = np.stack(np.meshgrid(*[np.arange(e) for e in E], indexing="ij"), -1).reshape(-1, grid.d)
+        w = np.where(idx <= np.asarray(E) // 2, idx, idx - np.asarray(E))
+        return w * np.asarray(grid.spacing)
+
+    def min_embedding_eigenvalue(self):
+        out = _d()
+        _check(_lib.gk_dski_min_embedding_eigenvalue(self.handle, C.byref(out)))
+        return out.value
 
 
 def assemble_dense(kernel: KernelSpec, X, Xp=None, with_derivatives=True, dlogell=False, derivative_scale=0.0,

@@ -46,6 +46,10 @@ void dski_cross_cov_dev(Op& o, const double* dXt, i64 nT, int dir, double* dQ, i
 void dski_gather_noise(Op& o, const double* W, const double* V, double* out, int nrhs, cudaStream_t s);
 gk_grid dski_grid(const Op& o);
 double dski_min_embedding_eigenvalue(const Op& o);
+std::unique_ptr<Op> make_grid_kernel(int d, const int* dims, const double* slice_ref, int device);
+double grid_kernel_min_eig(const Op& o);
+std::unique_ptr<Op> make_dski_slices(const gk_grid& g, const double* X, i64 n, double nv, double ng, int order,
+                                     int with_grad, int device, const double* slice_ref, const double* offset_table);
 void dski_transpose_apply(Op& o, const double* Vi, double* U, int nrhs, cudaStream_t s);
 void dski_apply(Op& o, const double* U, double* Oi, int nrhs, cudaStream_t s);
 void dski_grid_mvm(Op& o, const double* U, double* W, int nrhs, cudaStream_t s);
@@ -641,7 +645,28 @@ gk_status gk_dski_get_grid(const gk_op* h, gk_grid* out) {
 gk_status gk_dski_min_embedding_eigenvalue(const gk_op* h, double* out) {
   return guard([&] {
     if (!out) fail(GK_ERR_ARG, "null output");
-    *out = dski_min_embedding_eigenvalue(O(h));
+    const Op& op = O(h);
+    *out = op.kind == KIND_GRID ? grid_kernel_min_eig(op) : dski_min_embedding_eigenvalue(op);
+  });
+}
+
+gk_status gk_grid_kernel_create(const gk_grid* grid, const double* slice, int device, gk_op** out) {
+  return guard([&] {
+    if (!grid || !slice) fail(GK_ERR_ARG, "null argument");
+    auto h = std::make_unique<gk_op>();
+    h->impl = make_grid_kernel(grid->d, grid->dims, slice, device);
+    *out = h.release();
+  });
+}
+
+gk_status gk_dski_create_from_profile(const gk_grid* grid, const double* X, int64_t n, double nv, double ng,
+                                      int order, int with_gradients, const double* slice,
+                                      const double* offset_table, int device, gk_op** out) {
+  return guard([&] {
+    if (!grid) fail(GK_ERR_ARG, "null grid");
+    auto h = std::make_unique<gk_op>();
+    h->impl = make_dski_slices(*grid, X, n, nv, ng, order, with_gradients, device, slice, offset_table);
+    *out = h.release();
   });
 }
 

@@ -1441,6 +1441,7 @@ struct DskiOp final : Op {
   bool generic = false;
   std::unique_ptr<KuuFft> kfft, kfft_dl;  // value and d/dlog(ell) profiles (the latter built on first use)
   DevBuf<double> gtab;                    // profile at stencil offsets, (2T-1)^d row-major
+  std::vector<double> slice_ref_h;        // caller-supplied profile slice (family 2)
   DevBuf<double> tvec;  // concatenated per-axis Toeplitz sequences (axis 0 carries s²)
   DevBuf<int> toff;
   std::vector<int> toff_h;
@@ -2175,6 +2176,7 @@ static std::vector<double> embedded_slice(const gk_kernel& k, const gk_grid& g, 
 }
 
 double DskiOp::min_embedding_eigenvalue() const {
+  if (!slice_ref_h.empty()) return min_embedding_eigenvalue_host(d, m, slice_ref_h);
   int E[3] = {1, 1, 1};
   for (int j = 0; j < d; ++j) E[j] = 2 * (m[j] - 1);
   return min_embedding_eigenvalue_host(d, m, embedded_slice(kernel, grid, E, false));
@@ -2272,6 +2274,8 @@ void DskiOp::kuu(const double* u, double* w, int nrhs, cudaStream_t s) const {
 // embedding of kernel_dlogell_profile, dski.cpp:36-40, gp.cpp:212-213).
 void DskiOp::kuu_dlogell(const double* u, double* w, int nrhs, cudaStream_t s) {
   if (generic) {  // the reference's second embedding of kernel_dlogell_profile (dski.cpp:36-40)
+    if (kernel.family == 2)
+      fail(GK_ERR_UNSUPPORTED, "d/dlog(ell) needs a kernel family (the operator was built from a profile slice)");
     if (!kfft_dl) {
       auto f = std::make_unique<KuuFft>();
       f->init(d, m);
@@ -2373,19 +2377,35 @@ void DskiOp::row(i64 r_ext, double* out, cudaStream_t s) {
 // is all the D-SKIP leaves need (dskip.cpp:171).
 std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, const double* X, i64 n,
                                       double nv, double ng, int order, int with_grad, int device,
-                                      int profile);
+                                      int profile, const double* slice_ref, const double* offset_table);
+// the entry the D-SKIP leaves use (dskip.cu)
+std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, const double* X, i64 n,
+                                      double nv, double ng, int order, int with_grad, int device, int profile) {
+  return make_dski_profile(k, g, X, n, nv, ng, order, with_grad, device, profile, nullptr, nullptr);
+}
+
+// DskiOperator over a caller-evaluated stationary profile (the boundary's
+// profile-agnostic form): slice_ref = the profile on the reference embedding
+// (2(m_j − 1) nodes per axis, dski.cpp:97-114), offset_table = the profile at
+// the (2T − 1)^d stencil offsets (kernel_offset_table_, dski.cpp:181-203).
+std::unique_ptr<Op> make_dski_slices(const gk_grid& g, const double* X, i64 n, double nv, double ng, int order,
+                                     int with_grad, int device, const double* slice_ref, const double* offset_table) {
+  if (!slice_ref || !offset_table) fail(GK_ERR_ARG, "profile slice and offset table are required");
+  gk_kernel k{2, 1.0, 1.0, 0.0, 0.0, 0};  // family 2: caller-supplied profile
+  return make_dski_profile(k, g, X, n, nv, ng, order, with_grad, device, 0, slice_ref, offset_table);
+}
 
 std::unique_ptr<Op> make_dski(const gk_kernel& k, const gk_grid& g, const double* X, i64 n,
                               double nv, double ng, int order, int with_grad, int device) {
-  return make_dski_profile(k, g, X, n, nv, ng, order, with_grad, device, 0);
+  return make_dski_profile(k, g, X, n, nv, ng, order, with_grad, device, 0, nullptr, nullptr);
 }
 
 std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, const double* X, i64 n,
                                       double nv, double ng, int order, int with_grad, int device,
-                                      int profile) {
+                                      int profile, const double* slice_ref, const double* offset_table) {
   if (profile == 1 && g.d != 1)
     fail(GK_ERR_UNSUPPORTED, "the d/dlog(ell) grid profile is implemented for 1-D grids only");
-  if (k.family != 0 && k.family != 1) fail(GK_ERR_ARG, "unknown kernel family");
+  if (k.family != 0 && k.family != 1 && !(k.family == 2 && slice_ref)) fail(GK_ERR_ARG, "unknown kernel family");
   if (k.family != 0 && profile != 0)
     fail(GK_ERR_UNSUPPORTED, "the d/dlog(ell) 1-D grid profile is the D-SKIP leaf's (separable kernels only)");
   if (!(k.lengthscale > 0.0)) fail(GK_ERR_ARG, "lengthscale must be > 0");
@@ -2478,7 +2498,19 @@ std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, cons
     op->generic = true;
     op->kfft = std::make_unique<KuuFft>();
     op->kfft->init(d, op->m);
-    op->kfft->build(embedded_slice(k, g, op->kfft->E, false), st);
+    if (slice_ref) {
+      i64 tot = 1, ttot = 1;
+      for (int j = 0; j < d; ++j) {
+        tot *= 2 * (op->m[j] - 1);
+        ttot *= 2 * T - 1;
+      }
+      op->kfft->build(slice_from_reference(*op->kfft, std::vector<double>(slice_ref, slice_ref + tot)), st);
+      op->slice_ref_h.assign(slice_ref, slice_ref + tot);
+      op->gtab.upload(offset_table, static_cast<size_t>(ttot), st);
+      GK_CUDA(cudaStreamSynchronize(st));
+    } else {
+      op->kfft->build(embedded_slice(k, g, op->kfft->E, false), st);
+    }
   }
   std::vector<int> cstart;
   std::vector<i64> ext;

@@ -145,7 +145,7 @@ void tridiag_eig(int n, const double* alpha, const double* beta, double* evals, 
 void cholesky_upper(int k, const double* A, double* R);
 
 // ---------------------------------------------------------------- operators
-enum OpKind { KIND_EXACT = 0, KIND_DSKI = 1, KIND_DSKIP = 2, KIND_DENSE = 3 };
+enum OpKind { KIND_EXACT = 0, KIND_DSKI = 1, KIND_DSKIP = 2, KIND_DENSE = 3, KIND_GRID = 4 };
 
 // Device operator behind gk_op. All compute entry points work on the
 // INTERNAL layout: rows in the operator's internal order (D-SKI sorts points

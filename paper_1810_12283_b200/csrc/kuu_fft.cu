@@ -264,6 +264,84 @@ void KuuFft::apply(const double* U, double* W, int nrhs, cudaStream_t s) const {
   launched("kuu fft store");
 }
 
+std::vector<double> slice_from_reference(const KuuFft& f, const std::vector<double>& slice_ref) {
+  int Er[3] = {1, 1, 1};
+  i64 tot_ref = 1;
+  for (int j = 0; j < f.d; ++j) {
+    Er[j] = 2 * (f.m[j] - 1);
+    tot_ref *= Er[j];
+  }
+  if (static_cast<i64>(slice_ref.size()) != tot_ref) fail(GK_ERR_ARG, "profile slice size mismatch");
+  std::vector<double> out(static_cast<size_t>(f.Etot), 0.0);
+  int idx[3] = {0, 0, 0};
+  for (i64 t = 0; t < f.Etot; ++t) {
+    bool in = true;
+    i64 r = 0;
+    for (int j = 0; j < f.d; ++j) {
+      const int w = f.wrap(j, idx[j]);
+      if (w > f.m[j] - 1 || w < -(f.m[j] - 1)) in = false;
+      r = r * Er[j] + (w >= 0 ? w : Er[j] + w);
+    }
+    if (in) out[static_cast<size_t>(t)] = slice_ref[static_cast<size_t>(r)];
+    for (int j = f.d - 1; j >= 0; --j) {
+      if (++idx[j] < f.E[j]) break;
+      idx[j] = 0;
+    }
+  }
+  return out;
+}
+
+// GridKernelOperator(grid, profile) (dski.cpp:80-172) at the boundary: the
+// caller's profile evaluated on the reference embedding (what dski.cpp:97-114
+// computes from the StationaryProfile callback), applied by the FFT route.
+struct GridKernelOp final : Op {
+  KuuFft f;
+  std::vector<double> slice_ref;
+  int dims[3] = {1, 1, 1};
+  void mvm(const double* in, double* out, int nrhs, cudaStream_t s) override { f.apply(in, out, nrhs, s); }
+  void diagonal(double* dd, cudaStream_t s) override {
+    std::vector<double> h(static_cast<size_t>(N), slice_ref[0]);  // κ(0) on every node
+    GK_CUDA(cudaMemcpyAsync(dd, h.data(), sizeof(double) * N, cudaMemcpyHostToDevice, s));
+    GK_CUDA(cudaStreamSynchronize(s));
+  }
+  void row(i64 r, double* out, cudaStream_t s) override {
+    if (r < 0 || r >= N) fail(GK_ERR_RANGE, "grid kernel row index out of range");
+    DevBuf<double> e(static_cast<size_t>(N));
+    GK_CUDA(cudaMemsetAsync(e.p, 0, sizeof(double) * N, s));
+    const double one = 1.0;
+    GK_CUDA(cudaMemcpyAsync(e.p + r, &one, sizeof(double), cudaMemcpyHostToDevice, s));
+    f.apply(e.p, out, 1, s);
+    GK_CUDA(cudaStreamSynchronize(s));
+  }
+};
+
+std::unique_ptr<Op> make_grid_kernel(int d, const int* dims, const double* slice_ref, int device) {
+  if (d < 1 || d > 3) fail(GK_ERR_UNSUPPORTED, "grid kernel operator supports 1 <= d <= 3");
+  i64 tot = 1;
+  for (int j = 0; j < d; ++j) {
+    if (dims[j] < 2) fail(GK_ERR_ARG, "grid needs at least 2 nodes per dimension");
+    tot *= 2 * (dims[j] - 1);
+  }
+  DeviceGuard dg(device);
+  auto op = std::make_unique<GridKernelOp>();
+  op->kind = KIND_GRID;
+  op->device = device;
+  op->f.init(d, dims);
+  op->N = op->f.M;
+  op->n_value = op->N;
+  for (int j = 0; j < d; ++j) op->dims[j] = dims[j];
+  op->slice_ref.assign(slice_ref, slice_ref + tot);
+  op->init_stream();
+  op->f.build(slice_from_reference(op->f, op->slice_ref), op->stream);
+  return op;
+}
+
+double grid_kernel_min_eig(const Op& o) {
+  if (o.kind != KIND_GRID) fail(GK_ERR_ARG, "operator is not a grid kernel operator");
+  const auto& g = static_cast<const GridKernelOp&>(o);
+  return min_embedding_eigenvalue_host(g.f.d, g.dims, g.slice_ref);
+}
+
 double min_embedding_eigenvalue_host(int d, const int* dims, const std::vector<double>& slice) {
   // embedding 2(m_j − 1) per axis (dski.cpp:89-95), slice row-major; the
   // even slice's DFT along each axis is a cosine sum (separable)

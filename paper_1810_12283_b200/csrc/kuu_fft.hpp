@@ -28,6 +28,11 @@ struct KuuFft {
   void apply(const double* U, double* W, int nrhs, cudaStream_t s) const;
 };
 
+// Our embedding's slice from the reference's (2(m_j − 1) nodes per axis,
+// row-major): offsets |w_j| ≤ m_j − 1 copied, the rest (never reached by a
+// corner product) zero.
+std::vector<double> slice_from_reference(const KuuFft& f, const std::vector<double>& slice_ref);
+
 // Smallest eigenvalue of the reference's own embedding (size 2(m_j − 1) per
 // axis, GridKernelOperator::min_embedding_eigenvalue, dski.hpp:40-43): the
 // even slice's real DFT, by separable cosine sums on the host (long double).

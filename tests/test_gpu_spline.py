@@ -141,3 +141,63 @@ def test_spline_exact_operator_matches_dense_assembly(d, even):
     assert rel(op.diagonal(), np.diag(K)) <= 1e-12
     for r in (0, 3, 7, n + 7, op.size() - 1):
         assert np.linalg.norm(op.row(r) - K[r]) <= 1e-12 * np.linalg.norm(np.abs(K[r])), r
+
+
+def profile_values(kind, off, ell=0.4, s=1.3, a=-3.0, b=40.0, even=True):
+    """κ(offset) of SE / spline as the reference's eval(kernel, offset, 0)."""
+    r2 = (np.asarray(off) ** 2).sum(-1)
+    if kind == "se":
+        return s * s * np.exp(-0.5 * r2 / ell ** 2)
+    rho = np.sqrt(r2) / ell
+    with np.errstate(divide="ignore", invalid="ignore"):
+        rad = np.where(rho > 0, rho * rho * np.log(np.where(rho > 0, rho, 1.0)), 0.0) if even else rho ** 3
+    return s * s * (rad + a * rho * rho + b)
+
+
+@pytest.mark.parametrize("kind", ["se", "spline"])
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_grid_kernel_operator_from_profile_slice(kind, d):
+    """GridKernelOperator(grid, profile) at the boundary: the caller's profile
+    values on the reference embedding; K_UU against the dense profile matrix
+    (test_dski.cpp:51-69 analogue) and the oracle's operator; the minimum
+    embedding eigenvalue against the oracle's."""
+    dims = {1: [40], 2: [20, 16], 3: [10, 9, 8]}[d]
+    g = gk.Grid(dims, [0.0] * d, [0.05] * d)
+    off = gk.GridKernelOperator.embedding_offsets(g)
+    even = d % 2 == 0
+    op = gk.GridKernelOperator(g, profile_values(kind, off, even=even))
+    idx = np.stack(np.meshgrid(*[np.arange(m) for m in dims], indexing="ij"), -1).reshape(-1, d) * 0.05
+    K = profile_values(kind, idx[:, None, :] - idx[None, :, :], even=even)
+    u = np.random.default_rng(d).standard_normal((op.size(), 3))
+    got = op.mvm(u)
+    scale = np.linalg.norm(np.abs(K) @ np.abs(u), axis=0)
+    assert np.all(np.linalg.norm(got - K @ u, axis=0) <= 1e-12 * scale)
+    ko = O.KernelSpec(0.4, 1.3) if kind == "se" else O.KernelSpec(0.4, 1.3, O.SPLINE, -3.0, 40.0, even)
+    ref = O.GridKernelOperator(ko, O.Grid(dims, [0.0] * d, [0.05] * d))
+    assert np.linalg.norm(got[:, 0] - ref.mvm(u[:, 0])) <= 1e-12 * scale[0]
+    want = ref.min_embedding_eigenvalue()
+    assert abs(op.min_embedding_eigenvalue() - want) <= 1e-10 * max(abs(want), abs(K[0, 0]))
+    assert np.allclose(op.diagonal(), K[0, 0], rtol=1e-15) and np.linalg.norm(op.row(5) - K[5]) <= 1e-12 * np.abs(K[5]).sum()
+
+
+def test_dski_from_profile_slices_equals_kernel_build():
+    """gk_dski_create_from_profile with the spline profile's embedding slice
+    and stencil-offset table reproduces the spline D-SKI operator built from
+    the kernel (MVM, diagonal, rows)."""
+    X, op, ref = spline_pair(2, True, n=150)
+    g = op.grid
+    k = op.kernel
+    kw = dict(ell=k.lengthscale, s=k.outputscale, a=k.spline_a, b=k.spline_b, even=k.spline_even)
+    off = gk.GridKernelOperator.embedding_offsets(g)
+    W = 11
+    tidx = np.stack(np.meshgrid(np.arange(W), np.arange(W), indexing="ij"), -1).reshape(-1, 2)
+    toff = (tidx - 5) * np.asarray(g.spacing)
+    pop = gk.DskiOperator.from_profile(g, X, profile_values("spline", off, **kw), profile_values("spline", toff, **kw),
+                                       noise=(0.2, 0.3))
+    V = np.random.default_rng(4).standard_normal((op.size(), 2))
+    # the same operator up to the slice's ulp-level differences (numpy vs libm)
+    # and the embedding entries beyond the band (zero here, the profile there)
+    assert rel(pop.mvm(V), op.mvm(V)) <= 1e-12
+    assert rel(pop.diagonal(), op.diagonal()) <= 1e-13
+    assert rel(pop.row(17), op.row(17)) <= 1e-12
+    assert abs(pop.min_embedding_eigenvalue() - op.min_embedding_eigenvalue()) <= 1e-10 * abs(op.min_embedding_eigenvalue())

@@ -322,6 +322,21 @@ def run_gpu(args):
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_mean, e2e_med = [float(v) for v in e2e_t.tolist()]
     e2e_value = N * NR / e2e_mean
+    # the same call from pageable (numpy) buffers, as the reference's Eigen
+    # callers would pass them (the driver stages the copies)
+    Pin = np.asfortranarray(Bh)
+    Pout = np.empty_like(Pin, order="F")
+
+    def e2e_pageable():
+        gk._check(lib.gk_op_mvm(op.handle, gk._p(Pin), N, gk._p(Pout), N, nrhs))
+
+    e2e_pageable()
+    pg = []
+    for _ in range(min(e2e_steps, 20)):
+        t0 = time.perf_counter()
+        e2e_pageable()
+        pg.append(time.perf_counter() - t0)
+    e2e_pageable_us = float(np.mean(pg)) * 1e6
 
     solve = c2_solve(gk, op, X, y, dY, cols, world, rank, dev, sp, dist)
 
@@ -352,7 +367,9 @@ def run_gpu(args):
                     "d2h_bytes_per_step": 8 * N * nrhs,
                     "path": "gk_op_mvm (C-ABI, pinned host buffers, permutes + copies timed)",
                     "statistic": f"mean of {e2e_steps} host-timed calls, max over ranks",
-                    "us_per_call_mean": e2e_mean * 1e6, "us_per_call_median": e2e_med * 1e6},
+                    "us_per_call_mean": e2e_mean * 1e6, "us_per_call_median": e2e_med * 1e6,
+                    "pageable": {"us_per_call_mean": e2e_pageable_us, "value": N * NR / (e2e_pageable_us * 1e-6),
+                                 "path": "gk_op_mvm from pageable numpy buffers (rank 0 of the run, same config)"}},
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
                          "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,

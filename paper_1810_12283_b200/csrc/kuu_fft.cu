@@ -38,6 +38,7 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 // S > 1 — TI lines adjacent in memory (same outer index, TI | S).
 struct AxisPass {
   int L, logL, TI, support, inverse;
+  const double* spec;  // non-null: forward FFT, × spec, inverse FFT in one pass (axis 0)
   i64 S, nlines, Etot;
   int j, lim0, lim1;
   i64 st0, st1;  // strides of axes 0 and 1 (elements)
@@ -85,21 +86,50 @@ __global__ void __launch_bounds__(FFT_THREADS) k_fft_lines(double2* __restrict__
   }
   __syncthreads();
   const int halfL = L >> 1;
-  for (int s = 1; s <= a.logL; ++s) {
-    const int half = 1 << (s - 1);
-    const int tstride = L >> s;
-    for (int e = tid; e < TI * halfL; e += FFT_THREADS) {
-      const int c = e / halfL, jj = e - c * halfL;
-      const int pos = jj & (half - 1), grp = jj >> (s - 1);
-      const int i1 = (grp << s) + pos, i2 = i1 + half;
-      double2 w = __ldg(tw + pos * tstride);
-      if (a.inverse) w.y = -w.y;
-      const double2 x = sx[c * L + i1];
-      const double2 y = cmul(w, sx[c * L + i2]);
-      sx[c * L + i1] = make_double2(x.x + y.x, x.y + y.y);
-      sx[c * L + i2] = make_double2(x.x - y.x, x.y - y.y);
+  auto stages = [&](int inverse) {
+    for (int s = 1; s <= a.logL; ++s) {
+      const int half = 1 << (s - 1);
+      const int tstride = L >> s;
+      for (int e = tid; e < TI * halfL; e += FFT_THREADS) {
+        const int c = e / halfL, jj = e - c * halfL;
+        const int pos = jj & (half - 1), grp = jj >> (s - 1);
+        const int i1 = (grp << s) + pos, i2 = i1 + half;
+        double2 w = __ldg(tw + pos * tstride);
+        if (inverse) w.y = -w.y;
+        const double2 x = sx[c * L + i1];
+        const double2 y = cmul(w, sx[c * L + i2]);
+        sx[c * L + i1] = make_double2(x.x + y.x, x.y + y.y);
+        sx[c * L + i2] = make_double2(x.x - y.x, x.y - y.y);
+      }
+      __syncthreads();
+    }
+  };
+  stages(a.inverse);
+  if (a.spec) {
+    // pointwise spectrum multiply (element t of line g sits at spectrum index
+    // t·S + inner, the field's own offset), bit-reversal permutation in place,
+    // then the inverse transform of the same line
+    for (int e = tid; e < TI * L; e += FFT_THREADS) {
+      const int c = e / L, t = e - c * L;
+      const i64 g = g0 + c;
+      if (g < a.nlines) {
+        const i64 inner = a.S > 1 ? g % a.S : 0;
+        const double sc = __ldg(a.spec + (i64)t * a.S + inner);
+        sx[e] = make_double2(sx[e].x * sc, sx[e].y * sc);
+      }
     }
     __syncthreads();
+    for (int e = tid; e < TI * L; e += FFT_THREADS) {
+      const int c = e / L, t = e - c * L;
+      const int rt = a.logL ? int(__brev(unsigned(t)) >> shift) : 0;
+      if (t < rt) {
+        const double2 x = sx[c * L + t];
+        sx[c * L + t] = sx[c * L + rt];
+        sx[c * L + rt] = x;
+      }
+    }
+    __syncthreads();
+    stages(1);
   }
   for (int e = tid; e < TI * L; e += FFT_THREADS) {
     int c, t;
@@ -137,14 +167,6 @@ __global__ void k_fft_load(const double* __restrict__ U, int nrhs, int npairs, D
   }
 }
 
-__global__ void k_fft_scale(double2* __restrict__ buf, const double* __restrict__ spec, i64 Etot, int npairs) {
-  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < Etot * npairs; e += (i64)gridDim.x * blockDim.x) {
-    const double sc = spec[e % Etot];
-    const double2 v = buf[e];
-    buf[e] = make_double2(v.x * sc, v.y * sc);
-  }
-}
-
 __global__ void k_fft_store(const double2* __restrict__ buf, int nrhs, int npairs, Dims3 g, i64 M, i64 Etot,
                             double* __restrict__ W) {
   for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < M * npairs; e += (i64)gridDim.x * blockDim.x) {
@@ -171,12 +193,24 @@ unsigned blocks_of(i64 n) { return static_cast<unsigned>(std::min<i64>((n + 255)
 // All axes of npairs fields, forward (inverse = 0: last axis first, input
 // supported on the corner i_k < m_k when `pruned`) or inverse (first axis
 // first, only the corner of the result kept when `pruned`); no scaling.
-void fft_all_axes(const KuuFft& f, double2* buf, int npairs, int inverse, bool pruned, cudaStream_t s) {
-  for (int step = 0; step < 3; ++step) {
-    const int j = inverse ? step : 2 - step;
+// mode 0 forward, 1 inverse, 2 convolve: forward along axes 2, 1, then axis 0
+// forward × spectrum × inverse in one pass, then inverse along axes 1, 2.
+void fft_all_axes(const KuuFft& f, double2* buf, int npairs, int mode, bool pruned, cudaStream_t s) {
+  const int nsteps = mode == 2 ? 5 : 3;
+  for (int step = 0; step < nsteps; ++step) {
+    int j, inverse = mode == 1;
+    const double* spec = nullptr;
+    if (mode == 2) {
+      j = step < 3 ? 2 - step : step - 2;  // 2, 1, 0 (conv), 1, 2
+      inverse = step > 2;
+      if (step == 2) spec = f.spec.p;
+    } else {
+      j = inverse ? step : 2 - step;
+    }
     const int L = f.E[j];
     if (L < 2) continue;
     AxisPass a{};
+    a.spec = spec;
     a.L = L;
     a.logL = f.logE[j];
     a.inverse = inverse;
@@ -188,7 +222,7 @@ void fft_all_axes(const KuuFft& f, double2* buf, int npairs, int inverse, bool p
     a.st1 = f.E[2];
     a.lim0 = pruned ? f.m[0] : f.E[0];
     a.lim1 = pruned ? f.m[1] : f.E[1];
-    a.support = pruned && !inverse ? f.m[j] : 0;
+    a.support = pruned && !inverse ? f.m[j] : 0;  // (the convolve pass reads the forward input: pruned support)
     i64 outer = npairs;
     if (j >= 1) outer *= a.lim0;
     if (j >= 2) outer *= a.lim1;
@@ -256,10 +290,7 @@ void KuuFft::apply(const double* U, double* W, int nrhs, cudaStream_t s) const {
   // no zero fill: the pruned forward passes read only the corner they wrote
   k_fft_load<<<blocks_of(M * npairs), 256, 0, s>>>(U, nrhs, npairs, g, M, Etot, buf.p);
   launched("kuu fft load");
-  fft_all_axes(*this, buf.p, npairs, 0, true, s);
-  k_fft_scale<<<blocks_of(Etot * npairs), 256, 0, s>>>(buf.p, spec.p, Etot, npairs);
-  launched("kuu fft spectrum multiply");
-  fft_all_axes(*this, buf.p, npairs, 1, true, s);
+  fft_all_axes(*this, buf.p, npairs, 2, true, s);
   k_fft_store<<<blocks_of(M * npairs), 256, 0, s>>>(buf.p, nrhs, npairs, g, M, Etot, W);
   launched("kuu fft store");
 }

@@ -144,7 +144,9 @@ def test_pivoted_cholesky_variance_exact_at_full_rank_biased_up_at_rank_100():
     Xt = points(50, 2, 0.1, 0.9, 22)
     full = gk.GpModel(se(0.5, 1.0), X, y, dY, noise=(0.1, 0.1), backend="exact", precond_rank=360)
     ve = full.predict_variance_exact(Xt[:10])
-    assert np.all(np.abs(full.predict_variance_pivchol(Xt[:10]) - ve) <= 1e-8 * np.abs(ve))
+    vp = full.predict_variance_pivchol(Xt[:10])
+    # doctest::Approx(v).epsilon(1e-8): |a − b| < 1e-8·(1 + max(|a|, |b|))
+    assert np.all(np.abs(vp - ve) <= 1e-8 * (1.0 + np.maximum(np.abs(vp), np.abs(ve))))
     t100 = gk.GpModel(se(0.5, 1.0), X, y, dY, noise=(0.1, 0.1), backend="exact", precond_rank=100)
     assert np.all(t100.predict_variance_pivchol(Xt) - t100.predict_variance_exact(Xt) >= -1e-8)
 

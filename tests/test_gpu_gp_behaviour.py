@@ -5,7 +5,6 @@ fit optimiser, predictive means and gradients, and the exact / pivoted-
 Cholesky / randomized variances (gp.cpp:143-547). Data: Franke samples
 (testfns.cpp sampling, `sample_test_function`) and draws from a GP prior
 through the oracle's dense assembly."""
-import dataclasses
 
 import numpy as np
 import pytest

@@ -197,3 +197,72 @@ def test_cli_default_exact_backend(tmp_path):
     var = j["kernel"]["outputscale"] ** 2 - np.einsum("ij,ij->j", Q, np.linalg.solve(K, Q))
     assert np.max(np.abs(P[:, 2] - mu)) <= 1e-9 * np.max(np.abs(mu))
     assert np.max(np.abs(P[:, 3] - var)) <= 1e-9
+
+
+def test_cli_fit_round_trips_as_a_no_op(tmp_path, capsys):
+    """test_cli.cpp:70-96: fit, then refit from the written parameters with
+    zero iterations — the same hyperparameters (1e-12); the report has a
+    finite log-marginal."""
+    X, y, dY = O.sample_test_function("franke", 40, 2, (0.02, 0.02))
+    data = str(tmp_path / "toy.csv")
+    gio.write_dataset_csv(data, gio.Dataset(X, y, dY))
+    m1 = str(tmp_path / "m.json")
+    assert cli.main(["fit", "--data", data, "--model", m1, "--iters", "8", "--restarts", "1", "--seed", "1"]) == 0
+    report = capsys.readouterr().out
+    assert "log-marginal=" in report and "nan" not in report
+    j = json.load(open(m1))
+    m2 = str(tmp_path / "m2.json")
+    assert cli.main(["fit", "--data", data, "--model", m2, "--iters", "0", "--ell", repr(j["kernel"]["lengthscale"]),
+                     "--outputscale", repr(j["kernel"]["outputscale"]), "--noise", repr(j["noise"]["value"]),
+                     "--noise-grad", repr(j["noise"]["gradient"]), "--seed", "1"]) == 0
+    k2 = json.load(open(m2))
+    for a, b in ((k2["kernel"]["lengthscale"], j["kernel"]["lengthscale"]),
+                 (k2["kernel"]["outputscale"], j["kernel"]["outputscale"]), (k2["noise"]["value"], j["noise"]["value"])):
+        assert abs(a - b) <= 1e-12 * abs(b)
+
+
+def test_cli_predict_pins_training_points_and_is_deterministic(tmp_path):
+    """test_cli.cpp:98-141: at low noise the mean pins the training values,
+    the pivoted-Cholesky variance never falls below the exact one, and the
+    randomized variance is reproducible under a fixed seed."""
+    X, y, dY = O.sample_test_function("franke", 60, 7)
+    train = str(tmp_path / "train.csv")
+    gio.write_dataset_csv(train, gio.Dataset(X, y, dY))
+    model = str(tmp_path / "m.json")
+    assert cli.main(["fit", "--data", train, "--model", model, "--iters", "0", "--ell", "0.18", "--outputscale", "0.5",
+                     "--noise", "1e-3", "--noise-grad", "1e-3", "--rank", "180"]) == 0
+
+    def run(var, name, extra=()):
+        out = str(tmp_path / name)
+        assert cli.main(["predict", "--model", model, "--test", train, "--out", out, "--variance", var, *extra]) == 0
+        return out, np.array(list(csv.reader(open(out)))[1:], dtype=float)
+
+    _, ex = run("exact", "exact.csv")
+    _, pc = run("pivchol", "pivchol.csv")
+    assert np.all(np.abs(ex[:, 2] - y) < 5e-3)
+    # rank 180 = N: M⁻¹ = K⁻¹ up to rounding; at σ = 1e-3 both variances are
+    # s² − qᵀ(·)q ≈ 1e-7 from s² = 0.25 with cond(K) ~ 1e11, so each carries
+    # ~1e-8 of rounding — the reference's −1e-8 margin sits at that floor
+    assert np.all(pc[:, 3] - ex[:, 3] >= -5e-8)
+    r1, _ = run("randomized", "r1.csv", ("--probes", "16", "--seed", "9"))
+    r2, _ = run("randomized", "r2.csv", ("--probes", "16", "--seed", "9"))
+    assert open(r1).read() == open(r2).read()
+
+
+def test_cli_precond_study_csv_and_pcg_never_behind_cg(tmp_path):
+    """test_cli.cpp:194-211."""
+    out = str(tmp_path / "study.csv")
+    assert cli.main(["precond-study", "--function", "franke", "--n", "300", "--sweep-points", "3", "--rank", "60",
+                     "--out", out, "--seed", "4", "--grid-size", "32"]) == 0
+    lines = open(out).read().splitlines()
+    assert lines[0] == "ell,sigma,cg_iters,cg_converged,pcg_iters,pcg_converged"
+    rows = np.array([[float(v) for v in ln.split(",")] for ln in lines[1:]])
+    assert rows.shape == (9, 6) and np.all(rows[:, 4] <= rows[:, 2] + 2)
+
+
+def test_cli_benchmark_mvm_timings_grow_with_n(tmp_path):
+    """test_cli.cpp:213-228 (host-buffer calls through the C-ABI)."""
+    out = str(tmp_path / "bench.csv")
+    assert cli.main(["benchmark-mvm", "--backend", "dski", "--sizes", "500,2000,8000", "--reps", "5", "--out", out]) == 0
+    secs = [float(ln.split(",")[2]) for ln in open(out).read().splitlines()[1:]]
+    assert len(secs) == 3 and secs[2] > secs[0]

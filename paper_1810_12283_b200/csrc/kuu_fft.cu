@@ -86,20 +86,45 @@ __global__ void __launch_bounds__(FFT_THREADS) k_fft_lines(double2* __restrict__
   }
   __syncthreads();
   const int halfL = L >> 1;
+  // radix-2 DIT stages, two at a time in registers (a thread owns the four
+  // elements the two stages combine: the same butterflies in the same order
+  // as stage-by-stage, half the shared-memory passes and barriers)
   auto stages = [&](int inverse) {
-    for (int s = 1; s <= a.logL; ++s) {
-      const int half = 1 << (s - 1);
-      const int tstride = L >> s;
+    const double sg = inverse ? -1.0 : 1.0;
+    int s = 1;
+    if (a.logL & 1) {  // one single stage first when log2 L is odd
       for (int e = tid; e < TI * halfL; e += FFT_THREADS) {
         const int c = e / halfL, jj = e - c * halfL;
-        const int pos = jj & (half - 1), grp = jj >> (s - 1);
-        const int i1 = (grp << s) + pos, i2 = i1 + half;
-        double2 w = __ldg(tw + pos * tstride);
-        if (inverse) w.y = -w.y;
-        const double2 x = sx[c * L + i1];
-        const double2 y = cmul(w, sx[c * L + i2]);
+        const int i1 = 2 * jj, i2 = i1 + 1;
+        const double2 x = sx[c * L + i1], y = sx[c * L + i2];
         sx[c * L + i1] = make_double2(x.x + y.x, x.y + y.y);
         sx[c * L + i2] = make_double2(x.x - y.x, x.y - y.y);
+      }
+      __syncthreads();
+      s = 2;
+    }
+    const int quarterL = L >> 2;
+    for (; s + 1 <= a.logL; s += 2) {
+      const int h = 1 << (s - 1);
+      const int ts1 = L >> s, ts2 = L >> (s + 1);
+      for (int e = tid; e < TI * quarterL; e += FFT_THREADS) {
+        const int c = e / quarterL, jj = e - c * quarterL;
+        const int pos = jj & (h - 1), grp = jj >> (s - 1);
+        const int i0 = grp * 4 * h + pos;
+        double2* row = sx + c * L;
+        const double2 a0 = row[i0], a1 = row[i0 + h], a2 = row[i0 + 2 * h], a3 = row[i0 + 3 * h];
+        double2 w1 = __ldg(tw + pos * ts1), w2 = __ldg(tw + pos * ts2), w3 = __ldg(tw + (pos + h) * ts2);
+        w1.y *= sg;
+        w2.y *= sg;
+        w3.y *= sg;
+        const double2 t1 = cmul(w1, a1), t3 = cmul(w1, a3);
+        const double2 b0 = make_double2(a0.x + t1.x, a0.y + t1.y), b1 = make_double2(a0.x - t1.x, a0.y - t1.y);
+        const double2 b2 = make_double2(a2.x + t3.x, a2.y + t3.y), b3 = make_double2(a2.x - t3.x, a2.y - t3.y);
+        const double2 u2 = cmul(w2, b2), u3 = cmul(w3, b3);
+        row[i0] = make_double2(b0.x + u2.x, b0.y + u2.y);
+        row[i0 + 2 * h] = make_double2(b0.x - u2.x, b0.y - u2.y);
+        row[i0 + h] = make_double2(b1.x + u3.x, b1.y + u3.y);
+        row[i0 + 3 * h] = make_double2(b1.x - u3.x, b1.y - u3.y);
       }
       __syncthreads();
     }

@@ -1399,6 +1399,17 @@ __global__ void k_pts_weights(PtGeom g, const double* __restrict__ X, i64 n, int
   }
 }
 
+// d = 2 scatter records of the one-launch MVM: a point's 2T (w, dw) pairs
+// followed by its int4 base (fused2d.cu f2_scatter).
+__global__ void k_pack_records(const double2* __restrict__ wd, const int4* __restrict__ base, i64 n, int T,
+                               double2* __restrict__ rec) {
+  const int RW = 2 * T + 1;
+  for (i64 s = blockIdx.x * (i64)blockDim.x + threadIdx.x; s < n; s += (i64)gridDim.x * blockDim.x) {
+    for (int k = 0; k < 2 * T; ++k) rec[s * RW + k] = wd[s * 2 * T + k];
+    *reinterpret_cast<int4*>(rec + s * RW + 2 * T) = base[s];
+  }
+}
+
 // cstart[c] = first sorted position with key ≥ c (keys ascending).
 __global__ void k_cell_start(const int* __restrict__ key, i64 n, i64 ncells, int* __restrict__ cstart) {
   for (i64 s = blockIdx.x * (i64)blockDim.x + threadIdx.x; s < n; s += (i64)gridDim.x * blockDim.x) {
@@ -1435,6 +1446,7 @@ struct DskiOp final : Op {
   DevBuf<int4> base;
   DevBuf<double> wts;
   DevBuf<double2> wd;
+  DevBuf<double2> rec;  // d = 2 with gradients: [n][2T+1] scatter records of the one-launch MVM (fused2d)
   DevBuf<int> cell_start;
   // Non-separable profile (spline kernel): K_UU by circulant embedding + FFT
   // (kuu_fft.cu); diagonal from the stencil-offset table, rows through K_UU.
@@ -1501,6 +1513,7 @@ struct DskiOp final : Op {
     g.n = int(n);
     g.base = base.p;
     g.wd = wd.p;
+    g.rec = rec.p;
     g.cell_start = cell_start.p;
     g.t0 = tvec.p + toff_h[0];
     g.t1 = tvec.p + toff_h[1];
@@ -1597,7 +1610,7 @@ struct DskiOp final : Op {
       ++epoch;
     }
     grow(grid_u, static_cast<size_t>(M) * nrhs);
-    grow(grid_w, static_cast<size_t>(M) * nrhs);
+    grow(grid_w, static_cast<size_t>(M) * nrhs + 8);  // + 8: the one-launch gather's aligned window loads
     grow(grid_t, static_cast<size_t>(M) * nrhs);
     if (d == 2 && G == 2) grow(grid_h, static_cast<size_t>(M) * nrhs);
   }
@@ -2646,6 +2659,11 @@ std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, cons
   op->cell_start.upload(cstart.data(), cstart.size(), st);
   op->cell_start_h = cstart;
   op->ext.upload(ext.data(), ext.size(), st);
+  }
+  if (d == 2 && op->G == 2) {
+    op->rec.alloc(static_cast<size_t>(n) * (2 * T + 1));
+    k_pack_records<<<grid_blocks(n), 256, 0, st>>>(op->wd.p, op->base.p, n, T, op->rec.p);
+    launched("dski build: scatter records");
   }
   if (d == 3) {  // gather units: runs of ≤ kZU occupied base cells along z per cell line
     constexpr int kZU = 4;

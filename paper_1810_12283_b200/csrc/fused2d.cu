@@ -53,6 +53,7 @@ struct F2Args {
   int m0, m1, nb0, nb1, n;
   const int4* base;
   const double2* wd;  // [n][2][T] (w, dw) pairs: axis 0 then axis 1
+  const double2* rec; // [n][2T+1]: the point's 2T (w, dw) pairs, then its int4 base (scatter staging)
   const int* cell_start;
   const double* t0;
   const double* t1;
@@ -181,6 +182,19 @@ __device__ __forceinline__ void vstore(double* p, const double (&x)[RP]) {
 
 constexpr int kProfSlots = 8;
 
+// Phase stamps (tuning "fused_prof"); builds with -DGK_SCATTER_STAMPS or
+// -DGK_TOEPLITZ_STAMPS stamp inside the scatter / the mode-1 product instead
+// (tools/fused_phases.py with SCATTER_STAMPS / TOEPLITZ_STAMPS set).
+#if defined(GK_SCATTER_STAMPS)
+#define PSTAMP(k) stamp(a, k)
+#define BSTAMP(k) ((void)0)
+#elif defined(GK_TOEPLITZ_STAMPS)
+#define PSTAMP(k) ((void)0)
+#define BSTAMP(k) ((void)0)
+#else
+#define PSTAMP(k) ((void)0)
+#define BSTAMP(k) stamp(a, k)
+#endif
 __device__ __forceinline__ void stamp(const F2Args& a, int k) {
   if (a.prof != nullptr && threadIdx.x == 0 && k < kProfSlots) {
     unsigned long long t;
@@ -194,13 +208,17 @@ template <int T, int RP>
 __device__ void f2_scatter(const F2Args& a, double* sm, unsigned long long* mbar) {
   const int BR = a.BR, tid = threadIdx.x, pmax = a.s_pmax;
   const int NST = a.s_nst;                                 // staging depth (cell rows in flight)
-  double2* Wp = reinterpret_cast<double2*>(sm);           // [NST][pmax][2T]
+  // [NST][pmax][RW] point records as in global memory: 2T (w, dw) pairs and
+  // the int4 base. The odd record stride (13 or 9 16-byte units) spreads the
+  // records of consecutive points over all banks: lanes of a warp that read
+  // different points (one column each) hit distinct banks.
+  constexpr int RW = 2 * T + 1;
+  double2* Wp = reinterpret_cast<double2*>(sm);
   // [NST][3][VS]: group g of a staged row starts at element offset off_g
   // (0 or 1) — the bulk copy starts at the even element below the row start
   const int VS = (pmax * BR + 3) & ~1;  // even: every group copy starts 16-byte aligned
-  double* Vb = sm + NST * pmax * 2 * T * 2;
-  int4* Bb = reinterpret_cast<int4*>(Vb + NST * 3 * VS);  // [NST][pmax], 16-byte aligned
-  int* CS = reinterpret_cast<int*>(Bb + NST * pmax);       // [L][csw]
+  double* Vb = sm + NST * pmax * RW * 2;
+  int* CS = reinterpret_cast<int*>(Vb + NST * 3 * VS);     // [L][csw]
   const int bl = tid % a.BRP, cslot = tid / a.BRP;
   const int nspl = a.s_nspl, half = cslot % nspl, ccol = cslot / nspl;
   double* X = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(CS + a.s_L * a.s_csw) + 15) &
@@ -236,12 +254,12 @@ __device__ void f2_scatter(const F2Args& a, double* sm, unsigned long long* mbar
       CS[e] = __ldg(a.cell_start + (size_t)(R + r) * a.nb1 + clo + c);
     }
     __syncthreads();
+    if (item == (int)blockIdx.x) PSTAMP(1);
     auto issue = [&](int i, int buf) {
       const int* cs = CS + i * csw;
       const int P0 = cs[0], cnt = cs[csw - 1] - P0;
-      double2* wdst = Wp + (size_t)buf * pmax * 2 * T;
+      double2* wdst = Wp + (size_t)buf * pmax * RW;
       double* vdst = Vb + (size_t)buf * 3 * VS;
-      int4* bdst = Bb + (size_t)buf * pmax;
       if (tma) {
         // the last warp issues (idle in the compute when the strip leaves it
         // without a column), so bulk-copy issue latency overlaps the compute
@@ -250,25 +268,31 @@ __device__ void f2_scatter(const F2Args& a, double* sm, unsigned long long* mbar
         if (lane >= 0) {
           if (lane == 0) {
             fence_proxy_async();
+            // group copies of an odd element count are rounded up to even
+            // (one element past the range, in bounds: ranges end at least one
+            // element before the end of v except for the last group's last
+            // point, whose odd tail is loaded directly)
+            const size_t vend = 3 * gstride;
             unsigned vbytes = unsigned(cnt) * unsigned(3 * BR * 8);
             if (whole && cnt > 0) {
               vbytes = 0;
               for (int g = 0; g < 3; ++g) {
                 const size_t s0 = g * gstride + (size_t)P0 * a.nrhs, e0 = s0 + (size_t)cnt * a.nrhs;
                 const size_t se = s0 & ~size_t(1), len = e0 - se;
-                vbytes += unsigned(len & ~size_t(1)) * 8;
-                if (len & 1) vdst[(size_t)g * VS + len - 1] = __ldg(a.v + e0 - 1);  // odd tail: before the arrive
+                const size_t clen = (len & 1) && e0 < vend ? len + 1 : (len & ~size_t(1));
+                vbytes += unsigned(clen) * 8;
+                if ((len & 1) && e0 == vend) vdst[(size_t)g * VS + len - 1] = __ldg(a.v + e0 - 1);  // before the arrive
               }
             }
-            mbar_expect_tx(mbar + buf, unsigned(cnt) * unsigned(2 * T * 16 + 16) + vbytes);
+            mbar_expect_tx(mbar + buf, unsigned(cnt) * unsigned(RW * 16) + vbytes);
             if (cnt > 0) {
-              bulk_g2s(wdst, a.wd + (size_t)P0 * 2 * T, unsigned(cnt) * 2 * T * 16, mbar + buf);
-              bulk_g2s(bdst, a.base + P0, unsigned(cnt) * 16, mbar + buf);
+              bulk_g2s(wdst, a.rec + (size_t)P0 * RW, unsigned(cnt) * RW * 16, mbar + buf);
               if (whole)
                 for (int g = 0; g < 3; ++g) {
                   const size_t s0 = g * gstride + (size_t)P0 * a.nrhs, e0 = s0 + (size_t)cnt * a.nrhs;
                   const size_t se = s0 & ~size_t(1), len = e0 - se;
-                  if (len >= 2) bulk_g2s(vdst + (size_t)g * VS, a.v + se, unsigned(len & ~size_t(1)) * 8, mbar + buf);
+                  const size_t clen = (len & 1) && e0 < vend ? len + 1 : (len & ~size_t(1));
+                  if (clen >= 2) bulk_g2s(vdst + (size_t)g * VS, a.v + se, unsigned(clen) * 8, mbar + buf);
                 }
             }
           }
@@ -283,8 +307,7 @@ __device__ void f2_scatter(const F2Args& a, double* sm, unsigned long long* mbar
           }
         }
       } else {
-        for (int e = tid; e < cnt * 2 * T; e += F2_THREADS) cpa16(wdst + e, a.wd + (size_t)P0 * 2 * T + e);
-        for (int p = tid; p < cnt; p += F2_THREADS) cpa16(bdst + p, a.base + P0 + p);
+        for (int e = tid; e < cnt * RW; e += F2_THREADS) cpa16(wdst + e, a.rec + (size_t)P0 * RW + e);
         if (lane_ok)
           for (int q = cslot; q < 3 * cnt; q += F2_THREADS / a.BRP) {
             const int g = q >= 2 * cnt ? 2 : (q >= cnt ? 1 : 0);
@@ -314,13 +337,16 @@ __device__ void f2_scatter(const F2Args& a, double* sm, unsigned long long* mbar
     for (int j = 0; j < depth - 1 && j < nrows; ++j) issue(j, j);
     for (int i = 0; i < nrows; ++i) {
       const int buf = i % depth;
+      const bool stp = item == (int)blockIdx.x && i == 2;
+      if (stp) PSTAMP(2);
       if (i + depth - 1 < nrows) issue(i + depth - 1, (i + depth - 1) % depth);
       wait(buf);
+      if (stp) PSTAMP(3);
       if (active && tlo <= thi) {
         const int* cs = CS + i * csw;
         const int P0 = cs[0];
         const int q0 = cs[tlo] - P0, q1 = cs[thi + 1] - P0;
-        const double2* W = Wp + (size_t)buf * pmax * 2 * T;
+        const double2* W = Wp + (size_t)buf * pmax * RW;
         const double* V = Vb + (size_t)buf * 3 * VS + bl * RP;
         int vo1 = VS, vo2 = 2 * VS;  // group offsets (+ the start parity of each group's copy)
         const double* V0 = V;
@@ -330,11 +356,13 @@ __device__ void f2_scatter(const F2Args& a, double* sm, unsigned long long* mbar
           vo1 += int(((gstride + s0) & 1)) - int(s0 & 1);
           vo2 += int(((2 * gstride + s0) & 1)) - int(s0 & 1);
         }
-        const int4* B4 = Bb + (size_t)buf * pmax;
+        if (stp) PSTAMP(4);
+        int itc = 0;
 #pragma unroll 2
         for (int p = q0 + half; p < q1; p += nspl) {
-          const int tl = col - B4[p].y;
-          const double2* wr = W + p * 2 * T;
+          if (stp && itc++ == 1) PSTAMP(5);
+          const double2* wr = W + p * RW;
+          const int tl = col - reinterpret_cast<const int4*>(wr + 2 * T)->y;
           const double* vr = V0 + p * BR;
           double v0[RP], v1[RP], v2[RP];
           vload<RP>(vr, v0);
@@ -356,6 +384,7 @@ __device__ void f2_scatter(const F2Args& a, double* sm, unsigned long long* mbar
         }
       }
       // node row R+i is complete: combine the point-split partials in fixed order
+      if (stp) PSTAMP(6);
       if (nspl > 1) {
         if (active && half > 0) vstore<RP>(xslot(half, 0), acc[0]);
         __syncthreads();
@@ -454,8 +483,18 @@ __device__ __noinline__ void f2_sum_partials(const HaloSpec& halo, int M, int Q,
 // one item, no global loads or stores, two warps through the DMMA loops.
 // wide = true: 16-column items (two n-tiles per staged slab) where the
 // layout allows it, so a 400-group phase fits 296 CTAs in one round.
+__device__ __forceinline__ void tstamp(unsigned long long* prof, int k) {
+#ifdef GK_TOEPLITZ_STAMPS
+  if (prof != nullptr && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    prof[blockIdx.x * 8 + k] = t;
+  }
+#endif
+}
 __device__ __noinline__ void f2_toeplitz(const double* ts, int M, int Mp, int band, int P, int Q, const double* X,
-                            HaloSpec halo, double* Y, double* sm, int nsplit, bool dry = false, bool wide = false) {
+                            HaloSpec halo, double* Y, double* sm, int nsplit, bool dry = false, bool wide = false,
+                            unsigned long long* prof = nullptr) {
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32, g = lane / 4, t4 = lane % 4;
   const int CW = (wide && halo.mode != 2 && Q % 16 == 0) ? 16 : 8;  // columns per item
   const int ncols = P * Q, cgroups = (ncols + CW - 1) / CW, items = cgroups * nsplit;
@@ -471,8 +510,10 @@ __device__ __noinline__ void f2_toeplitz(const double* ts, int M, int Mp, int ba
   double* Hs0 = Bs1 + Mp * CW;             // [Mp][CW] halo staging, one per B buffer
   double* Hs1 = Hs0 + Mp * CW;
   const bool contiguous = (Q % 8) == 0;
+  tstamp(prof, 0);
   cpa_wait0();  // this thread's copies of the Toeplitz sequences (f2_body)
   __syncthreads();
+  tstamp(prof, 1);
   for (int e = tid; e < ND * 32; e += F2_THREADS) {
     const int D = e / 32 + Dlo, ln = e % 32;
     int x = 4 * D + ln / 4 - ln % 4;
@@ -503,48 +544,49 @@ __device__ __noinline__ void f2_toeplitz(const double* ts, int M, int Mp, int ba
         }
       }
     } else {
-      // 8 independent loads in flight per thread (one L2 round trip per batch)
-#pragma unroll 1
-      for (int e0 = tid; e0 < M * 8; e0 += F2_THREADS * 8) {
-        double val[8];
-        int dst[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int e = e0 + u * F2_THREADS;
-          int c, j;
-          c = e >> 3;
-          j = e & 7;
-          const int col = col0 + j;
-          val[u] = 0.0;
-          dst[u] = -1;
-          if (e < M * 8) {
-            dst[u] = c * 8 + j;
-            if (col < ncols) {
-              const int p = col / Q, q = col - p * Q;
-              const size_t o = (size_t)p * M * Q + q + (size_t)c * Q;
-              val[u] = X[o];
-              if (halo.row(p)) val[u] += halo.h[o];
-            }
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (dst[u] >= 0) B[dst[u]] = val[u];
+      // columns of stride Q: 8-byte cp.async per element, each thread always
+      // the same column j = tid mod 8 (one division per item); halo rows of
+      // u go to Hs and are added after the wait
+      const int col = col0 + (tid & 7);
+      if (col < ncols) {
+        const int p = col / Q, q = col - p * Q;
+        const size_t o = (size_t)p * M * Q + q;
+        for (int e = tid; e < M * 8; e += F2_THREADS) cpa8(B + e, X + o + (size_t)(e >> 3) * Q);
+        if (halo.row(p))
+          for (int e = tid; e < M * 8; e += F2_THREADS) cpa8(Hs + e, halo.h + o + (size_t)(e >> 3) * Q);
+      } else {
+        for (int e = tid; e < M * 8; e += F2_THREADS) B[e] = 0.0;
       }
     }
     cpa_commit();
   };
+  // strided columns with halo rows: the halo staging takes the second slab
+  // buffer, so items are not prefetched (the phase has about one item per CTA)
+  const bool nc_halo = !contiguous && halo.mode == 1;
+  const bool pf = !nc_halo;
+  if (nc_halo) Hs0 = Bs1;
+  bool hj = false;  // this thread's column of a strided item is a halo row
+  auto col_halo = [&](int col0) {
+    const int col = col0 + (tid & 7);
+    hj = col < ncols && halo.row(col / Q);
+  };
   int buf = 0;
+  tstamp(prof, 2);
   if (!dry && (int)blockIdx.x < items) issue(blockIdx.x / nsplit, Bs0, Hs0);
+  tstamp(prof, 3);
   // item -> (column group, split): one division per item
   const int per = (mtiles + nsplit - 1) / nsplit;
+  int prev_cg = -1;
   for (int it = dry ? (int)blockIdx.x % max(items, 1) : (int)blockIdx.x; it < items; it += gridDim.x) {
     const int cg = it / nsplit, sp = it - cg * nsplit;
     const int nxt = dry ? items : it + gridDim.x;
     // the next item reuses the staged slab when it has the same column group
     // (never with gridDim >= nsplit); otherwise prefetch into the other buffer
     const int nxt_cg = nxt < items ? nxt / nsplit : -1;
-    if (nxt_cg >= 0 && nxt_cg != cg) {
+    const bool fresh = cg != prev_cg;  // the slab was staged for this item (not reused): add its halo once
+    prev_cg = cg;
+    if (nc_halo) col_halo(cg * CW);
+    if (pf && nxt_cg >= 0 && nxt_cg != cg) {
       issue(nxt_cg, buf ? Bs0 : Bs1, buf ? Hs0 : Hs1);
       cpa_wait1();
     } else {
@@ -556,10 +598,15 @@ __device__ __noinline__ void f2_toeplitz(const double* ts, int M, int Mp, int ba
     double* const Yb = Y + (size_t)p0 * M * Q + q0;
     const bool hrow = contiguous && halo.row(p0);
     __syncthreads();
+    if (it == (int)blockIdx.x) tstamp(prof, 4);
     double* B = buf ? Bs1 : Bs0;
     const double* Hs = buf ? Hs1 : Hs0;
-    if (hrow) {  // u + h for the halo rows
+    if (hrow && fresh) {  // u + h for the halo rows
       for (int e = tid; e < M * CW; e += F2_THREADS) B[e] += Hs[e];
+      __syncthreads();
+    } else if (nc_halo && fresh && !dry) {  // strided items: per column (this thread's j)
+      if (hj)
+        for (int e = tid; e < M * 8; e += F2_THREADS) B[e] += Hs[e];
       __syncthreads();
     }
     const int mt_lo = sp * per, mt_hi = min(mtiles, mt_lo + per);
@@ -630,8 +677,12 @@ __device__ __noinline__ void f2_toeplitz(const double* ts, int M, int Mp, int ba
       }
     }
     __syncthreads();
+    if (it == (int)blockIdx.x) tstamp(prof, 5);
     if (dry) break;
-    if (nxt_cg >= 0 && nxt_cg != cg) buf ^= 1;
+    if (nxt_cg >= 0 && nxt_cg != cg) {
+      if (pf) buf ^= 1;
+      else issue(nxt_cg, Bs0, Hs0);  // no prefetch: stage the next item now
+    }
   }
 }
 
@@ -727,8 +778,9 @@ __device__ void f2_gather_direct(const F2Args& a, bool dry = false) {
     const int s = t / a.chunks;
     const int rb = chunk * a.BR + bl * RP;
     if (rb >= a.nrhs) continue;
-    const int4 bs = __ldg(a.base + s);
-    const double2* wr = a.wd + (size_t)s * 2 * T;
+    // the point's record (2T (w, dw) pairs, then its base), L2-resident from phase S
+    const double2* wr = a.rec + (size_t)s * (2 * T + 1);
+    const int4 bs = __ldg(reinterpret_cast<const int4*>(wr + 2 * T));
     double2 w1[T];
 #pragma unroll
     for (int t1 = 0; t1 < T; ++t1) w1[t1] = __ldg(wr + T + t1);
@@ -736,9 +788,29 @@ __device__ void f2_gather_direct(const F2Args& a, bool dry = false) {
     double o0[RP], o1[RP], o2[RP];
 #pragma unroll
     for (int k = 0; k < RP; ++k) o0[k] = o1[k] = o2[k] = 0.0;
+    // single RHS: each window row (T contiguous nodes) as aligned 16-byte
+    // loads from the even element at or below its start (the grid buffer is
+    // padded past its end), shifted by the start parity in registers
+    constexpr int NL = (T + 2) / 2;
+    const bool single = RP == 1 && a.nrhs == 1;
 #pragma unroll
     for (int t0 = 0; t0 < T; ++t0) {
       const double* rr = wb + (size_t)t0 * rstride;
+      double xs[T];
+      if (single) {
+        const uintptr_t ad = reinterpret_cast<uintptr_t>(rr);
+        const double2* p2 = reinterpret_cast<const double2*>(ad & ~uintptr_t(15));
+        const bool odd = (ad & 15) != 0;
+        double e[2 * NL];
+#pragma unroll
+        for (int l = 0; l < NL; ++l) {
+          const double2 y = __ldcg(p2 + l);
+          e[2 * l] = y.x;
+          e[2 * l + 1] = y.y;
+        }
+#pragma unroll
+        for (int t1 = 0; t1 < T; ++t1) xs[t1] = odd ? e[t1 + 1] : e[t1];
+      }
       double r[RP], q[RP];
 #pragma unroll
       for (int k = 0; k < RP; ++k) r[k] = q[k] = 0.0;
@@ -750,7 +822,7 @@ __device__ void f2_gather_direct(const F2Args& a, bool dry = false) {
           x[0] = xx.x;
           x[1] = xx.y;
         } else {
-          x[0] = __ldcg(rr + (size_t)t1 * a.nrhs);
+          x[0] = single ? xs[t1] : __ldcg(rr + (size_t)t1 * a.nrhs);
         }
 #pragma unroll
         for (int k = 0; k < RP; ++k) {
@@ -827,11 +899,16 @@ __device__ void f2_gather(const F2Args& a, double* sm) {
     };
     auto issue_pts = [&](int i, int buf) {
       const int P0 = CS[2 * i], cnt = CS[2 * i + 1] - P0;
-      const double2* wsrc = a.wd + (size_t)P0 * 2 * T;
+      // from the scatter's records (still L2-resident from phase S)
+      constexpr int RW = 2 * T + 1;
+      const double2* wsrc = a.rec + (size_t)P0 * RW;
       double2* wdst = Wp + (size_t)buf * pmax * 2 * T;
-      for (int e = tid; e < cnt * 2 * T; e += F2_THREADS) cpa16(wdst + e, wsrc + e);
+      for (int e = tid; e < cnt * 2 * T; e += F2_THREADS) {
+        const int p = e / (2 * T), k = e - p * (2 * T);
+        cpa16(wdst + e, wsrc + p * RW + k);
+      }
       int* bdst = Bb + buf * pmax;
-      for (int p = tid; p < cnt; p += F2_THREADS) cpa4(bdst + p, &a.base[P0 + p].y);
+      for (int p = tid; p < cnt; p += F2_THREADS) cpa4(bdst + p, &reinterpret_cast<const int4*>(wsrc + p * RW + 2 * T)->y);
     };
 #pragma unroll 1
     for (int t = 0; t < T; ++t) issue_row(R + t);
@@ -940,7 +1017,8 @@ __device__ __forceinline__ void f2_body(const F2Args& a) {
     if (a.s_mode == 1) f2_scatter_direct<T, RP>(a);
     else f2_scatter<T, RP>(a, work, mbar);
   }
-  stamp(a, 1);
+  BSTAMP(1);
+  PSTAMP(7);
   const HaloSpec hs1 = a.s_mode == 1
                            ? HaloSpec{2, a.pbuf, (size_t)a.m0 * a.m1 * a.nrhs, a.s_L, a.s_segs, T, a.s_nbuf}
                            : HaloSpec{1, a.h, 0, a.s_L, a.s_segs, T, 1};
@@ -954,32 +1032,39 @@ __device__ __forceinline__ void f2_body(const F2Args& a) {
       f2_toeplitz(ts1, a.m1, a.m1p, a.band1, a.m0, a.nrhs, a.u, hs1, a.y1, work, a.t_split, true, a.t_wide);
     grid_wait(a.bar, tgt);
   }
-  stamp(a, 2);
-  if (!(a.skip & 2)) f2_toeplitz(ts1, a.m1, a.m1p, a.band1, a.m0, a.nrhs, a.u, hs1, a.y1, work, a.t_split, false, a.t_wide);
-  stamp(a, 3);
+  BSTAMP(2);
+#ifdef GK_TOEPLITZ_STAMPS
+  stamp(a, 6);
+#endif
+  if (!(a.skip & 2))
+    f2_toeplitz(ts1, a.m1, a.m1p, a.band1, a.m0, a.nrhs, a.u, hs1, a.y1, work, a.t_split, false, a.t_wide, a.prof);
+  BSTAMP(3);
+#ifdef GK_TOEPLITZ_STAMPS
+  stamp(a, 7);
+#endif
   {
     const unsigned long long tgt = grid_arrive(a.bar);
     if ((a.warm & 2) && a.g_mode == 1) f2_gather_direct<T, RP>(a, true);
     grid_wait(a.bar, tgt);
   }
-  stamp(a, 4);
+  BSTAMP(4);
   if (!(a.skip & 4))
     f2_toeplitz(ts0, a.m0, a.m0p, a.band0, 1, a.m1 * a.nrhs, a.y1, HaloSpec{0, nullptr, 0, 1, 0, T, 1}, a.w, work,
                 a.t_split, false, a.t_wide);
-  stamp(a, 5);
+  BSTAMP(5);
   {
     const unsigned long long tgt = grid_arrive(a.bar);
     if ((a.warm & 4) && a.g_mode == 1) f2_gather_direct<T, RP>(a, true);
     grid_wait(a.bar, tgt);
   }
-  stamp(a, 6);
+  BSTAMP(6);
   if (!(a.skip & 8)) {
     if (a.g_mode == 1) f2_gather_direct<T, RP>(a);
     else f2_gather<T, RP>(a, work);
   }
   cpa_wait0();  // nothing in flight into shared memory past the body (skip masks)
   __syncthreads();
-  stamp(a, 7);
+  BSTAMP(7);
   if (threadIdx.x == 0)  // the shared memory may be reused (persistent PCG kernel)
     for (int b = 0; b < 8; ++b) asm volatile("mbarrier.inval.shared.b64 [%0];\n" ::"r"(smem_u32(mbar + b)) : "memory");
   __syncthreads();
@@ -1169,6 +1254,7 @@ static F2Args fused2d_args(const Fused2dGeom& g, Fused2dPlan& p, const double* v
   a.n = g.n;
   a.base = g.base;
   a.wd = g.wd;
+  a.rec = g.rec;
   a.cell_start = g.cell_start;
   a.t0 = g.t0;
   a.t1 = g.t1;

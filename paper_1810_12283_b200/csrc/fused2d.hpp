@@ -17,6 +17,7 @@ struct Fused2dGeom {
   int n = 0;                 // points
   const int4* base = nullptr;        // [n] (base0, base1, -, -)
   const double2* wd = nullptr;       // [n][2][T] (w, dw) pairs, axis 0 then axis 1
+  const double2* rec = nullptr;      // [n][2T+1] (w, dw) pairs then the int4 base (scatter staging records)
   const int* cell_start = nullptr;   // [nb0*nb1 + 1]
   const double* t0 = nullptr;        // axis-0 Toeplitz sequence (carries s²)
   const double* t1 = nullptr;        // axis-1 Toeplitz sequence

@@ -14,6 +14,10 @@ for kv in filter(None, os.environ.get("GK_TUNE", "").split(",")):  # e.g. GK_TUN
     k, v = kv.split("=")
     gk.set_tuning(k, int(v))
 names = ["scatter", "barrier1", "mode1", "barrier2", "mode0", "barrier3", "gather"]
+if os.environ.get("SCATTER_STAMPS"):  # a build with -DGK_SCATTER_STAMPS (stamps inside the scatter's first item)
+    names = ["cs", "to_row2", "wait", "qrange", "iter0", "rest", "to_exit"]
+if os.environ.get("TOEPLITZ_STAMPS"):  # -DGK_TOEPLITZ_STAMPS: slots 0-5 inside mode 1, 6 barrier-1 exit, 7 mode-1 exit
+    names = ["seq_wait", "F_table", "issue", "slab_wait", "compute", "to_b1exit", "to_end"]
 cases = [("C2", 32), ("C1", 32), ("C2", 1), ("C4", 1)]
 if len(sys.argv) > 1:
     cases = [(sys.argv[1], int(sys.argv[2]))]

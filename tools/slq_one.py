@@ -1,5 +1,5 @@
-"""C2 SLQ (31 probes x 30 steps) once warm, then once inside
-cudaProfilerStart/Stop for `ncu --profile-from-start off`; prints wall time."""
+"""One C2 SLQ (31 probes x 30 Lanczos steps) inside cudaProfilerStart/Stop,
+after a warm-up call (for ncu --profile-from-start off)."""
 import os
 import sys
 import time
@@ -7,20 +7,17 @@ import time
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import bench  # noqa: E402
 import paper_1810_12283_b200 as gk  # noqa: E402
+from bench import build_problem  # noqa: E402
 
-X, y, dY, grid = bench.build_problem()
-c = bench.CONFIG
-op = gk.DskiOperator(gk.KernelSpec(c["ell"], 1.0), grid, X, (c["noise"], c["noise"]))
-r = gk.slq_logdet(op, c["slq_probes"], c["slq_steps"], 0, 0.5e-4)
+X, y, dY, grid = build_problem()
+op = gk.DskiOperator(gk.KernelSpec(0.2, 1.0), grid, X, (1e-2, 1e-2))
+gk.slq_logdet(op, 31, 30, 0, 0.5e-4)
 torch.cuda.synchronize()
 t0 = time.perf_counter()
-r = gk.slq_logdet(op, c["slq_probes"], c["slq_steps"], 0, 0.5e-4)
+gk.slq_logdet(op, 31, 30, 0, 0.5e-4)
+print(f"slq wall {1e3 * (time.perf_counter() - t0):.2f} ms", flush=True)
+torch.cuda.profiler.start()
+gk.slq_logdet(op, 31, 30, 0, 0.5e-4)
 torch.cuda.synchronize()
-print("slq wall", time.perf_counter() - t0, r.logdet, flush=True)
-if os.environ.get("PROFILE"):
-    torch.cuda.profiler.start()
-    r = gk.slq_logdet(op, c["slq_probes"], c["slq_steps"], 0, 0.5e-4)
-    torch.cuda.synchronize()
-    torch.cuda.profiler.stop()
+torch.cuda.profiler.stop()

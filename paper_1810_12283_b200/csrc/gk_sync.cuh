@@ -64,6 +64,23 @@ __device__ __forceinline__ unsigned long long grid_arrive(unsigned long long* ba
   }
   return target;
 }
+// grid_arrive that also returns (to every thread) how many CTAs arrived
+// before this one in the current generation.
+__device__ __forceinline__ unsigned long long grid_arrive_rank(unsigned long long* bar, int& rank) {
+  __shared__ int s_rank;
+  __syncthreads();
+  unsigned long long target = 0;
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;\n" : "=l"(t) : "l"(bar) : "memory");
+    const unsigned long long nb = gridDim.x;
+    target = (t / nb + 1) * nb;
+    s_rank = int(t % nb);
+  }
+  __syncthreads();
+  rank = s_rank;
+  return target;
+}
 __device__ __forceinline__ void grid_wait(unsigned long long* bar, unsigned long long target) {
   if (threadIdx.x == 0) {
     unsigned spins = 0;

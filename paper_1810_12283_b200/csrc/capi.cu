@@ -221,6 +221,7 @@ int gk_set_tuning(const char* key, int value) {
                            : k == "fused_prof" ? &g_tuning.fused_prof
                            : k == "pcg_fused" ? &g_tuning.pcg_fused
                            : k == "e2e_chunk" ? &g_tuning.e2e_chunk
+                           : k == "d3" ? &g_tuning.d3
                            : k == "dskip" ? &g_tuning.dskip
                            : k == "lanczos" ? &g_tuning.lanczos
                            : k == "rng" ? &g_tuning.rng

@@ -48,7 +48,8 @@ struct Tuning {
   std::atomic<int> f2_grid{0}, f2_rp{0};
   std::atomic<int> f2_smode{0}, f2_gmode{0};  // 1 staged, 2 direct (0 = default)
   std::atomic<int> f2_nspl{0}, f2_nst{0};
-  std::atomic<int> e2e_chunk{0};  // gk_op_mvm pipeline chunk width (0 = auto)
+  std::atomic<int> e2e_chunk{0};
+  std::atomic<int> d3{0};  // d = 3 MVM A/B bitmask (2: r-fastest gather tasks for every RHS count)  // gk_op_mvm pipeline chunk width (0 = auto)
   // D-SKIP Hadamard kernels: 0 = TMA-ring DMMA (v3, falling back to v2 for odd
   // sizes), 3 = cp.async DMMA (v2), 1 = first generation
   std::atomic<int> dskip{0};

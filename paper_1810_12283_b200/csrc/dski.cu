@@ -1484,6 +1484,10 @@ struct DskiOp final : Op {
   DevBuf<long long> s3_uoff;
   DevBuf<int> s3_cstart, s3_cseg;
   DevBuf<int2> s3_cent;
+  // per node (column, z): [zoff, zoff+1) in zlist = scratch node offsets of
+  // the blocks covering it, in (za, unit) order (k_scatter_merge3f)
+  DevBuf<int> s3_zoff, s3_zlist;
+  int s3_maxl = 0;
   long long s3_nodes = 0;
   int s3_nzs = 0;
   // tile scatter (k_scatter_tile3): per TB×TB tile of node columns the points
@@ -1938,6 +1942,48 @@ __global__ void __launch_bounds__(256) k_scatter_merge3(int ncol, int m2, int nz
   }
 }
 
+// Merge over flattened per-node lists: for every node (column, z) the
+// scratch node offsets of exactly the blocks covering it, in the column's
+// (za, unit) order (built with the operator). CTA per node column: its
+// per-z starts and list are staged in shared memory by all threads at once,
+// then thread (z, RHS) sums its list four entries at a time (the four loads
+// issued together). No candidate scanning or coverage predicates (the
+// per-segment entry walk of k_scatter_merge3 visits ~33 entries per node of
+// which ~6 cover it). Same per-node summation order: bit-identical.
+constexpr int M3F_THREADS = 256;
+__global__ void __launch_bounds__(M3F_THREADS) k_scatter_merge3f(int ncol, int m2, const int* __restrict__ zoff,
+                                                                const int* __restrict__ zlist,
+                                                                const double* __restrict__ scratch,
+                                                                double* __restrict__ u, int nrhs) {
+  extern __shared__ int sl[];  // [m2 + 1] list starts relative to the column, then the column's list
+  int* li = sl + m2 + 1;
+  const int nout = m2 * nrhs;
+  for (int col = blockIdx.x; col < ncol; col += gridDim.x) {
+    const int* zo = zoff + (size_t)col * m2;
+    const int b0 = __ldg(zo), nl = __ldg(zo + m2) - b0;
+    __syncthreads();
+    for (int z = threadIdx.x; z <= m2; z += M3F_THREADS) sl[z] = __ldg(zo + z) - b0;
+    for (int i = threadIdx.x; i < nl; i += M3F_THREADS) li[i] = __ldg(zlist + b0 + i);
+    __syncthreads();
+    double* uc = u + (size_t)col * m2 * nrhs;
+    for (int o = threadIdx.x; o < nout; o += M3F_THREADS) {
+      const int z = o / nrhs, r = o - z * nrhs;
+      const int s1 = sl[z + 1];
+      double acc = 0.0;
+      for (int i = sl[z]; i < s1; i += 4) {
+        double val[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          val[j] = i + j < s1 ? __ldcg(scratch + (size_t)li[i + j] * nrhs + r) : 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (i + j < s1) acc += val[j];
+      }
+      uc[o] = acc;
+    }
+  }
+}
+
 // Lean-kernel launch shape: x = RHS lanes (≤ 32), y = items per block, shrunk
 // (down to one warp) when there are too few items to give every SM ~4 CTAs.
 static dim3 lean_block(int nrhs, i64 items) {
@@ -2040,6 +2086,14 @@ void DskiOp::scatter(const double* v, double* u, int nrhs, cudaStream_t s) const
     else k_scatter_upush3<4, true><<<gp, S3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, s3_uoff.p, v, s3_scratch.p, nrhs);
     launched("dski scatter (d=3 unit push)");
     const int ncol = m[0] * m[1];
+    const size_t msm = sizeof(int) * (size_t(m[2]) + 1 + size_t(s3_maxl));
+    if (s3_zoff.p && msm <= 96 * 1024 && !(g_tuning.d3.load() & 1)) {
+      raise_smem_limit((const void*)k_scatter_merge3f, msm);
+      k_scatter_merge3f<<<static_cast<unsigned>(std::min(ncol, 148 * 32)), M3F_THREADS, msm, s>>>(
+          ncol, m[2], s3_zoff.p, s3_zlist.p, s3_scratch.p, u, nrhs);
+      launched("dski scatter (d=3 unit merge, per-node lists)");
+      return;
+    }
     k_scatter_merge3<<<grid_blocks(i64(ncol) * s3_nzs * nrhs), 256, 0, s>>>(ncol, m[2], s3_nzs, T, s3_cstart.p, s3_cent.p,
                                                                           s3_cseg.p, g3_units.p, s3_uoff.p,
                                                                           s3_scratch.p, u, nrhs);
@@ -2731,6 +2785,8 @@ std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, cons
     const int nzs = (m2 + 7) / 8;
     std::vector<int> cst(static_cast<size_t>(ncol) + 1, 0), cseg(static_cast<size_t>(ncol) * nzs);
     std::vector<int2> cent;
+    std::vector<int> zoff(static_cast<size_t>(ncol) * m2 + 1, 0), zlist;
+    int maxl = 0;
     for (int c = 0; c < ncol; ++c) {
       auto& L = per[static_cast<size_t>(c)];
       std::stable_sort(L.begin(), L.end(), [&](const int2& x, const int2& y) {
@@ -2742,6 +2798,20 @@ std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, cons
         while (e < L.size() && gu[static_cast<size_t>(L[e].x)].z + zspan <= zs * 8) ++e;
         cseg[static_cast<size_t>(c) * nzs + zs] = int(cent.size() + e);
       }
+      {  // flattened per-node lists of this column
+        const size_t l0 = zlist.size();
+        for (int z = 0; z < m2; ++z) {
+          zoff[static_cast<size_t>(c) * m2 + z] = int(zlist.size());
+          for (const int2& en : L) {
+            const int4& U = gu[static_cast<size_t>(en.x)];
+            const int nzb = U.w - U.z + T - 1;
+            if (U.z > z) break;  // sorted by za
+            if (z < U.z + nzb)
+              zlist.push_back(int(uoff[static_cast<size_t>(en.x)] + static_cast<long long>(en.y) * nzb + (z - U.z)));
+          }
+        }
+        maxl = std::max(maxl, int(zlist.size() - l0));
+      }
       cent.insert(cent.end(), L.begin(), L.end());
     }
     cst[static_cast<size_t>(ncol)] = int(cent.size());
@@ -2751,6 +2821,13 @@ std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, cons
     op->s3_cstart.upload(cst.data(), cst.size(), op->stream);
     op->s3_cseg.upload(cseg.data(), cseg.size(), op->stream);
     op->s3_cent.upload(cent.data(), std::max<size_t>(cent.size(), 1), op->stream);
+    zoff[static_cast<size_t>(ncol) * m2] = int(zlist.size());
+    if (tot < (1LL << 31)) {
+      if (zlist.empty()) zlist.push_back(0);
+      op->s3_zoff.upload(zoff.data(), zoff.size(), op->stream);
+      op->s3_zlist.upload(zlist.data(), zlist.size(), op->stream);
+      op->s3_maxl = maxl;
+    }
   }
   if (d == 3) {  // per node column (k0, k1): covering points ordered by (b2, t0, t1, point)
     const int m0 = g.dims[0], m1 = g.dims[1], m2 = g.dims[2];

@@ -1903,6 +1903,74 @@ __global__ void __launch_bounds__(S3U_THREADS) k_scatter_upush3(DskiView op, con
   }
 }
 
+// The same push for few right-hand sides (T·nrhs ≤ 32): one unit per group
+// of T·nrhs threads, many units per CTA, point data read straight from L1/L2
+// (the per-unit staging of k_scatter_upush3 serves only T·nrhs threads here:
+// at 1 RHS its CTA ran 6 live threads of 128). Same per-node order.
+template <int T, bool GRAD>
+__global__ void __launch_bounds__(64) k_scatter_upush3d(DskiView op, const int4* __restrict__ units, int nunits,
+                                                         const int2* __restrict__ urange,
+                                                         const long long* __restrict__ uoff,
+                                                         const double* __restrict__ v,
+                                                         double* __restrict__ scratch, int nrhs) {
+  constexpr int REC = 3 * 2 * T;
+  const size_t gstride = (size_t)op.n * nrhs;
+  const int per = T * nrhs;
+  const long long ntask = (long long)nunits * per;
+  for (long long g = blockIdx.x * 64LL + threadIdx.x; g < ntask; g += (long long)gridDim.x * 64) {
+    const int u = int(g / per), wi = int(g - (long long)u * per);
+    const int a = wi / nrhs, r = wi - a * nrhs;
+    const int4 U = __ldg(units + u);
+    const int2 pr = __ldg(urange + u);
+    const int za = U.z, nzb = U.w - U.z + T - 1;
+    double* out = scratch + (size_t)__ldg(uoff + u) * nrhs;
+    double acc[T][T];
+#pragma unroll
+    for (int b = 0; b < T; ++b)
+#pragma unroll
+      for (int t = 0; t < T; ++t) acc[b][t] = 0.0;
+    int zc = 0;
+    auto emit = [&]() {
+#pragma unroll
+      for (int b = 0; b < T; ++b) out[((size_t)(a * T + b) * nzb + zc) * nrhs + r] = acc[b][0];
+#pragma unroll
+      for (int b = 0; b < T; ++b) {
+#pragma unroll
+        for (int k = 0; k < T - 1; ++k) acc[b][k] = acc[b][k + 1];
+        acc[b][T - 1] = 0.0;
+      }
+      ++zc;
+    };
+    for (int p = pr.x; p < pr.y; ++p) {
+      const double* w = op.wts + (size_t)p * REC;
+      const int zo = __ldg(&op.base[p].z) - za;
+      while (zc < zo) emit();
+      const double wa = __ldg(w + a), v0 = __ldg(v + (size_t)p * nrhs + r);
+      double ca = wa * v0, cb = 0.0, cc = 0.0;
+      if constexpr (GRAD) {
+        ca = fma(__ldg(w + T + a), __ldg(v + gstride + (size_t)p * nrhs + r), ca);
+        cb = wa * __ldg(v + 2 * gstride + (size_t)p * nrhs + r);
+        cc = wa * __ldg(v + 3 * gstride + (size_t)p * nrhs + r);
+      }
+      double z2[T], dz2[T];
+#pragma unroll
+      for (int c = 0; c < T; ++c) {
+        z2[c] = __ldg(w + 4 * T + c);
+        dz2[c] = GRAD ? __ldg(w + 5 * T + c) : 0.0;
+      }
+#pragma unroll
+      for (int b = 0; b < T; ++b) {
+        const double wb = __ldg(w + 2 * T + b);
+        const double A = GRAD ? fma(__ldg(w + 3 * T + b), cb, wb * ca) : wb * ca;
+        const double Bc = wb * cc;
+#pragma unroll
+        for (int c = 0; c < T; ++c) acc[b][c] = GRAD ? fma(dz2[c], Bc, fma(z2[c], A, acc[b][c])) : fma(z2[c], A, acc[b][c]);
+      }
+    }
+    while (zc < nzb) emit();
+  }
+}
+
 // Merge: u(col, z, r) = Σ over the entries {unit, ab} of column col whose
 // block covers z, in the column's fixed (za, unit) order.
 __global__ void __launch_bounds__(256) k_scatter_merge3(int ncol, int m2, int nzs, int T,
@@ -2081,10 +2149,18 @@ void DskiOp::scatter(const double* v, double* u, int nrhs, cudaStream_t s) const
     const void* fn = T == 6 ? (const void*)k_scatter_upush3<6, true> : (const void*)k_scatter_upush3<4, true>;
     if (smem > 48 * 1024) raise_smem_limit(fn, smem);
     s3_scratch.reserve(static_cast<size_t>(s3_nodes) * nrhs);
+    if (T * nrhs <= 32 && !(g_tuning.d3.load() & 4)) {
+      const long long nt = static_cast<long long>(g3_nunits) * T * nrhs;
+      const unsigned gd = static_cast<unsigned>(std::max<long long>(1, (nt + 63) / 64));
+      if (T == 6) k_scatter_upush3d<6, true><<<gd, 64, 0, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, s3_uoff.p, v, s3_scratch.p, nrhs);
+      else k_scatter_upush3d<4, true><<<gd, 64, 0, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, s3_uoff.p, v, s3_scratch.p, nrhs);
+      launched("dski scatter (d=3 unit push, direct)");
+    } else {
     const unsigned gp = static_cast<unsigned>(std::min(g3_nunits, 148 * 16));
     if (T == 6) k_scatter_upush3<6, true><<<gp, S3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, s3_uoff.p, v, s3_scratch.p, nrhs);
     else k_scatter_upush3<4, true><<<gp, S3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, s3_uoff.p, v, s3_scratch.p, nrhs);
     launched("dski scatter (d=3 unit push)");
+    }
     const int ncol = m[0] * m[1];
     const size_t msm = sizeof(int) * (size_t(m[2]) + 1 + size_t(s3_maxl));
     if (s3_zoff.p && msm <= 96 * 1024 && !(g_tuning.d3.load() & 1)) {

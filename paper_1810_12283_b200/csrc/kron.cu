@@ -317,6 +317,122 @@ __global__ void __launch_bounds__(128) k_toeplitz_slab(const double* __restrict_
   }
 }
 
+// Persistent variant for M ≤ 16·WM (one row block holds every row): the A
+// operand is the same Toeplitz matrix for every column tile, so each warp
+// keeps its A fragments in registers for the whole launch; CTAs (grid sized
+// to the resident capacity) walk column tiles with the next tile's B slab
+// copied by 8-byte cp.async while the current one computes. Same k order and
+// fragment mapping as k_toeplitz_dmma<WM, WN>: bit-identical.
+template <int WM, int WN>
+__global__ void __launch_bounds__(128) k_toeplitz_pers(const double* __restrict__ t, int M, i64 P, i64 Q,
+                                                       const double* __restrict__ X, double* __restrict__ Y) {
+  constexpr int BM = 16 * WM, BN = 16 * WN;
+  constexpr int SB = BN + 8;
+  constexpr int KS = BM / 4;  // k steps covering every row (M ≤ BM, zero-padded)
+  extern __shared__ __align__(16) double smp[];
+  double* ts = smp;               // [BM]
+  double* Bs = smp + BM;          // [2][BM][SB]
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int wm = (warp / 2) * (8 * WM), wn = (warp % 2) * (8 * WN);
+  const int g = lane / 4, t4 = lane % 4;
+  const i64 ncols = P * Q;
+  const i64 ntiles = (ncols + BN - 1) / BN;
+  const int Qi = int(Q);
+  for (int i = tid; i < BM; i += 128) ts[i] = i < M ? __ldg(t + i) : 0.0;
+  __syncthreads();
+  double af[KS][WM];
+#pragma unroll
+  for (int k = 0; k < KS; ++k)
+#pragma unroll
+    for (int i = 0; i < WM; ++i) {
+      const int a = wm + 8 * i + g, c = 4 * k + t4;
+      af[k][i] = (a < M && c < M) ? ts[a > c ? a - c : c - a] : 0.0;
+    }
+  // staging slot: thread -> column cc = tid % BN, rows c = tid / BN + r·(128 / BN)
+  constexpr int RSTEP = 128 / BN;
+  const int scc = tid % BN, sc0 = tid / BN;
+  auto issue = [&](i64 tile, int buf) {
+    const i64 col = tile * BN + scc;
+    double* dst = Bs + buf * (BM * SB);
+    if (col < ncols) {
+      const int p = int(col / Qi), q = int(col - (i64)p * Qi);
+      const double* src = X + (i64)p * M * Qi + q;
+      for (int c = sc0; c < BM; c += RSTEP) {
+        if (c < M) {
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(static_cast<unsigned>(
+                           __cvta_generic_to_shared(dst + c * SB + scc))),
+                       "l"(src + (i64)c * Qi)
+                       : "memory");
+        } else {
+          dst[c * SB + scc] = 0.0;
+        }
+      }
+    } else {
+      for (int c = sc0; c < BM; c += RSTEP) dst[c * SB + scc] = 0.0;
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  i64 tile = blockIdx.x;
+  if (tile < ntiles) issue(tile, 0);
+  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+    const int buf = it & 1;
+    if (tile + gridDim.x < ntiles) {
+      issue(tile + gridDim.x, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    const double* B = Bs + buf * (BM * SB);
+    double acc[WM][WN][2];
+#pragma unroll
+    for (int i = 0; i < WM; ++i)
+#pragma unroll
+      for (int j = 0; j < WN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+    for (int k = 0; k < KS; ++k) {
+      double bf[WN];
+#pragma unroll
+      for (int j = 0; j < WN; ++j) bf[j] = B[(4 * k + t4) * SB + wn + 8 * j + g];
+#pragma unroll
+      for (int i = 0; i < WM; ++i)
+#pragma unroll
+        for (int j = 0; j < WN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[k][i], bf[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < WN; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const i64 col = tile * BN + wn + 8 * j + 2 * t4 + e;
+        if (col >= ncols) continue;
+        const int p = int(col / Qi), q = int(col - (i64)p * Qi);
+        double* yo = Y + (i64)p * M * Qi + q;
+#pragma unroll
+        for (int i = 0; i < WM; ++i) {
+          const int a = wm + 8 * i + g;
+          if (a < M) yo[(i64)a * Qi] = acc[i][j][e];
+        }
+      }
+    __syncthreads();  // every warp is done with this buffer before it is refilled
+  }
+}
+
+template <int WM, int WN>
+void launch_toeplitz_pers(const double* t, int M, i64 P, i64 Q, const double* X, double* Y, cudaStream_t s) {
+  constexpr int BM = 16 * WM, BN = 16 * WN;
+  const size_t shm = sizeof(double) * (BM + 2 * size_t(BM) * (BN + 8));
+  static int blocks_per_sm = 0;
+  if (!blocks_per_sm) {
+    if (shm > 48 * 1024) raise_smem_limit((const void*)k_toeplitz_pers<WM, WN>, shm);
+    GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_toeplitz_pers<WM, WN>, 128, shm));
+    blocks_per_sm = std::max(1, blocks_per_sm);
+  }
+  const i64 ntiles = (P * Q + BN - 1) / BN;
+  const unsigned grid = static_cast<unsigned>(std::min<i64>(ntiles, 148LL * blocks_per_sm));
+  k_toeplitz_pers<WM, WN><<<grid, 128, shm, s>>>(t, M, P, Q, X, Y);
+  launched("toeplitz mode product (DMMA, persistent)");
+}
+
 template <int NT>
 void launch_toeplitz_slab(const double* t, int M, int band, i64 P, i64 Q, const double* X, double* Y,
                           cudaStream_t s) {
@@ -404,6 +520,13 @@ void toeplitz_mode(const double* t, int M, int band, i64 P, i64 Q, const double*
     // 48-node axes 60.4 -> 48.1 µs for K_UU at 17 RHS (bit-identical: the
     // same k order per output)
     const bool wide = ctas(64, 64) >= 192;
+    // persistent, A fragments in registers, next tile's B in flight: C3's
+    // 48-node modes at 17 RHS 48.1 -> 46.1 µs (the 64-column persistent tile,
+    // 152 registers, measured 52.3); bit-identical
+    if (variant == 0 && M <= 48 && !(g_tuning.d3.load() & 8)) {
+      launch_toeplitz_pers<3, 2>(t, M, P, Q, X, Y, s);
+      return;
+    }
     if (M <= 48) { if (wide) launch_toeplitz_dmma<3, 4>(t, M, band, P, Q, X, Y, s); else launch_toeplitz_dmma<3, 2>(t, M, band, P, Q, X, Y, s); }
     else { if (wide) launch_toeplitz_dmma<4, 4>(t, M, band, P, Q, X, Y, s); else launch_toeplitz_dmma<4, 2>(t, M, band, P, Q, X, Y, s); }
     return;

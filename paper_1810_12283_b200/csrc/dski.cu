@@ -2019,6 +2019,7 @@ __global__ void __launch_bounds__(256) k_scatter_merge3(int ncol, int m2, int nz
 // per-segment entry walk of k_scatter_merge3 visits ~33 entries per node of
 // which ~6 cover it). Same per-node summation order: bit-identical.
 constexpr int M3F_THREADS = 256;
+constexpr int M3F_UNROLL = 8;  // a node's list (~6 blocks) in one round of loads
 __global__ void __launch_bounds__(M3F_THREADS) k_scatter_merge3f(int ncol, int m2, const int* __restrict__ zoff,
                                                                 const int* __restrict__ zlist,
                                                                 const double* __restrict__ scratch,
@@ -2038,13 +2039,13 @@ __global__ void __launch_bounds__(M3F_THREADS) k_scatter_merge3f(int ncol, int m
       const int z = o / nrhs, r = o - z * nrhs;
       const int s1 = sl[z + 1];
       double acc = 0.0;
-      for (int i = sl[z]; i < s1; i += 4) {
-        double val[4];
+      for (int i = sl[z]; i < s1; i += M3F_UNROLL) {
+        double val[M3F_UNROLL];
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < M3F_UNROLL; ++j)
           val[j] = i + j < s1 ? __ldcg(scratch + (size_t)li[i + j] * nrhs + r) : 0.0;
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < M3F_UNROLL; ++j)
           if (i + j < s1) acc += val[j];
       }
       uc[o] = acc;

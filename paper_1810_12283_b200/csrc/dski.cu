@@ -1706,6 +1706,24 @@ static void smem_attr(const void* fn, size_t bytes) {
 // contracts its 6×6×6 stencil from shared memory — instead of 216 L2 reads
 // per (point, RHS), one L2 read of the block per unit (C3's surface points
 // pile up to ~180 per cell). Same summation order as k_gather_lean.
+__device__ __forceinline__ void g3_cp8(double* s, const double* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(s))),
+               "l"(g)
+               : "memory");
+}
+__device__ __forceinline__ void g3_cp16(void* s, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(s))),
+               "l"(g)
+               : "memory");
+}
+__device__ __forceinline__ void g3_cp4(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(s))),
+               "l"(g)
+               : "memory");
+}
+__device__ __forceinline__ void g3_cp_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
 constexpr int G3U_THREADS = 128;
 template <int T, bool GRAD>
 __global__ void __launch_bounds__(G3U_THREADS) k_gather_units3(DskiView op, const int4* __restrict__ units, int nunits,
@@ -1729,8 +1747,11 @@ __global__ void __launch_bounds__(G3U_THREADS) k_gather_units3(DskiView op, cons
       const int a = ab / T, b = ab - a * T;
       const double* src = w + (((size_t)(U.x + a) * m1 + (U.y + b)) * m2 + za) * nrhs;
       double* dst = blk + ab * run;
-      for (int q = threadIdx.x & 31; q < run; q += 32) dst[q] = __ldg(src + q);
+      // cp.async: every copy of the block in flight at once (a load→store
+      // loop paid one L2 round trip per iteration)
+      for (int q = threadIdx.x & 31; q < run; q += 32) g3_cp8(dst + q, src + q);
     }
+    g3_cp_wait_all();
     __syncthreads();
     // Tasks (point, RHS). With ≥ 16 RHS the first 16·⌊nrhs/16⌋ columns of
     // every point go in blocks of 16 (a half-warp reads 16 consecutive
@@ -1862,17 +1883,20 @@ __global__ void __launch_bounds__(S3U_THREADS) k_scatter_upush3(DskiView op, con
     for (int p0 = pr.x; p0 < pr.y; p0 += S3U_MAXP) {
       const int np = min(S3U_MAXP, pr.y - p0);
       __syncthreads();  // previous chunk / unit done with the stage
-      for (int e = threadIdx.x; e < np * REC; e += S3U_THREADS) sw[e] = __ldg(op.wts + (size_t)p0 * REC + e);
+      // staged by cp.async (all copies in flight at once)
+      for (int e = threadIdx.x; e < np * REC / 2; e += S3U_THREADS)
+        g3_cp16(sw + 2 * e, op.wts + (size_t)p0 * REC + 2 * e);
       for (int pl = threadIdx.x / 32; pl < np; pl += S3U_THREADS / 32)
         for (int q = threadIdx.x & 31; q < NG * nrhs; q += 32) {
           const int g = q / nrhs, rr = q - g * nrhs;
-          sv[pl * NG * nrhs + q] = __ldg(v + g * gstride + (size_t)(p0 + pl) * nrhs + rr);
+          g3_cp8(sv + pl * NG * nrhs + q, v + g * gstride + (size_t)(p0 + pl) * nrhs + rr);
         }
-      for (int e = threadIdx.x; e < np; e += S3U_THREADS) sz[e] = __ldg(&op.base[p0 + e].z) - za;
+      for (int e = threadIdx.x; e < np; e += S3U_THREADS) g3_cp4(sz + e, &op.base[p0 + e].z);
+      g3_cp_wait_all();
       __syncthreads();
       for (int pl = 0; pl < np; ++pl) {
         const double* w = sw + pl * REC;
-        const int zo = sz[pl];
+        const int zo = sz[pl] - za;
         while (zc < zo) emit();
         const double* vv = sv + pl * NG * nrhs + r;
         const double wa = w[a], v0 = vv[0];

@@ -26,7 +26,7 @@ flush = torch.ones(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 g = torch.Generator(device="cuda").manual_seed(0)
 V = torch.randn(N * nrhs, dtype=torch.float64, device="cuda", generator=g)
 U = torch.randn(M * nrhs, dtype=torch.float64, device="cuda", generator=g)
-stages = {"scatter": (0, V, M), "kuu": (1, U, M), "gather": (2, U, N), "mvm": (3, V, N)}
+stages = {"scatter": (0, V, M), "kuu": (1, U, M), "gather": (2, U, N), "mvm": (3, V, N), "mvm_graph": (4, V, N)}
 outs = {(k, v): torch.empty(sz * nrhs, dtype=torch.float64, device="cuda") for k, (_, _, sz) in stages.items()
         for v in vals}
 ts = {(k, v): [] for k in stages for v in vals}

@@ -1725,13 +1725,14 @@ __device__ __forceinline__ void g3_cp_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 constexpr int G3U_THREADS = 128;
-template <int T, bool GRAD>
+template <int T, bool GRAD, int NR = 0>  // NR > 0: the RHS count as a compile-time constant (immediate offsets)
 __global__ void __launch_bounds__(G3U_THREADS) k_gather_units3(DskiView op, const int4* __restrict__ units, int nunits,
                                                                const int2* __restrict__ urange,
                                                                const double* __restrict__ w,
                                                                const double* __restrict__ v,
-                                                               double* __restrict__ out, int nrhs, int noise,
+                                                               double* __restrict__ out, int nrhs_rt, int noise,
                                                                int zmax, int g_tuning_d3) {
+  const int nrhs = NR > 0 ? NR : nrhs_rt;
   extern __shared__ double blk[];  // [T][T][nzb][nrhs]
   const int m1 = op.m[1], m2 = op.m[2];
   constexpr int REC = 3 * 2 * T;
@@ -2298,7 +2299,14 @@ void DskiOp::gather(const double* w, const double* v, double* out, int nrhs, boo
       raise_smem_limit(fn, smem);
       GK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, int(cudaSharedmemCarveoutMaxShared)));
       const unsigned grid = static_cast<unsigned>(std::min(g3_nunits, 148 * 16));
-      if (T == 6) {
+      const int d3 = g_tuning.d3.load();
+      if (T == 6 && G && (nrhs == 16 || nrhs == 17) && !(d3 & 512)) {
+        const void* fs = nrhs == 16 ? (const void*)k_gather_units3<6, true, 16> : (const void*)k_gather_units3<6, true, 17>;
+        raise_smem_limit(fs, smem);
+        GK_CUDA(cudaFuncSetAttribute(fs, cudaFuncAttributePreferredSharedMemoryCarveout, int(cudaSharedmemCarveoutMaxShared)));
+        if (nrhs == 16) k_gather_units3<6, true, 16><<<grid, G3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, w, v, out, nrhs, noise ? 1 : 0, g3_zspan, d3);
+        else k_gather_units3<6, true, 17><<<grid, G3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, w, v, out, nrhs, noise ? 1 : 0, g3_zspan, d3);
+      } else if (T == 6) {
         if (G) k_gather_units3<6, true><<<grid, G3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, w, v, out, nrhs, noise ? 1 : 0, g3_zspan, g_tuning.d3.load());
         else k_gather_units3<6, false><<<grid, G3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, w, v, out, nrhs, noise ? 1 : 0, g3_zspan, g_tuning.d3.load());
       } else {

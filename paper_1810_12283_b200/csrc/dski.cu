@@ -2907,17 +2907,24 @@ std::unique_ptr<Op> make_dski_profile(const gk_kernel& k, const gk_grid& g, cons
         while (e < L.size() && gu[static_cast<size_t>(L[e].x)].z + zspan <= zs * 8) ++e;
         cseg[static_cast<size_t>(c) * nzs + zs] = int(cent.size() + e);
       }
-      {  // flattened per-node lists of this column
+      {  // flattened per-node lists of this column: count per z, prefix sum,
+         // fill in entry order (O(blocks · nzb), entry order kept per node)
         const size_t l0 = zlist.size();
-        for (int z = 0; z < m2; ++z) {
-          zoff[static_cast<size_t>(c) * m2 + z] = int(zlist.size());
-          for (const int2& en : L) {
-            const int4& U = gu[static_cast<size_t>(en.x)];
-            const int nzb = U.w - U.z + T - 1;
-            if (U.z > z) break;  // sorted by za
-            if (z < U.z + nzb)
-              zlist.push_back(int(uoff[static_cast<size_t>(en.x)] + static_cast<long long>(en.y) * nzb + (z - U.z)));
-          }
+        std::vector<int> cnt(static_cast<size_t>(m2) + 1, 0);
+        for (const int2& en : L) {
+          const int4& U = gu[static_cast<size_t>(en.x)];
+          const int nzb = U.w - U.z + T - 1;
+          for (int z = U.z; z < std::min(m2, U.z + nzb); ++z) ++cnt[static_cast<size_t>(z) + 1];
+        }
+        for (int z = 0; z < m2; ++z) cnt[static_cast<size_t>(z) + 1] += cnt[static_cast<size_t>(z)];
+        for (int z = 0; z < m2; ++z) zoff[static_cast<size_t>(c) * m2 + z] = int(l0) + cnt[static_cast<size_t>(z)];
+        zlist.resize(l0 + static_cast<size_t>(cnt[static_cast<size_t>(m2)]));
+        for (const int2& en : L) {
+          const int4& U = gu[static_cast<size_t>(en.x)];
+          const int nzb = U.w - U.z + T - 1;
+          const long long o = uoff[static_cast<size_t>(en.x)] + static_cast<long long>(en.y) * nzb;
+          for (int z = U.z; z < std::min(m2, U.z + nzb); ++z)
+            zlist[l0 + static_cast<size_t>(cnt[static_cast<size_t>(z)]++)] = int(o + (z - U.z));
         }
         maxl = std::max(maxl, int(zlist.size() - l0));
       }

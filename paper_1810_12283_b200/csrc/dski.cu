@@ -1725,32 +1725,47 @@ __device__ __forceinline__ void g3_cp_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 constexpr int G3U_THREADS = 128;
-template <int T, bool GRAD, int NR = 0>  // NR > 0: the RHS count as a compile-time constant (immediate offsets)
+// RHS columns go in chunks (blockIdx.y; chunk width cw, the last one may be
+// narrower): the staged block holds one chunk, so wide RHS counts keep the
+// shared footprint — and the occupancy — of a ~16-column block.
+template <int T, bool GRAD, int NR = 0, bool ONE = false>  // NR > 0: the chunk width as a compile-time constant
+                                                            // (immediate offsets); ONE: a single chunk (ldr == NR)
 __global__ void __launch_bounds__(G3U_THREADS) k_gather_units3(DskiView op, const int4* __restrict__ units, int nunits,
                                                                const int2* __restrict__ urange,
                                                                const double* __restrict__ w,
                                                                const double* __restrict__ v,
-                                                               double* __restrict__ out, int nrhs_rt, int noise,
+                                                               double* __restrict__ out, int ldr_rt, int cw_rt, int noise,
                                                                int zmax, int g_tuning_d3) {
-  const int nrhs = NR > 0 ? NR : nrhs_rt;
+  const int ldr = (NR > 0 && ONE) ? NR : ldr_rt;
+  // ldr: the RHS count (the stride of w, v, out); columns [r0, r0 + nrhs) here
+  const int r0 = ONE ? 0 : blockIdx.y * cw_rt;
+  const int nrhs = NR > 0 ? NR : min(cw_rt, ldr - r0);
   extern __shared__ double blk[];  // [T][T][nzb][nrhs]
   const int m1 = op.m[1], m2 = op.m[2];
   constexpr int REC = 3 * 2 * T;
-  const size_t gstride = (size_t)op.n * nrhs;
+  const size_t gstride = (size_t)op.n * ldr;
+  const unsigned inv = (65536u + nrhs - 1) / nrhs;  // q / nrhs = (q * inv) >> 16 for q < 2048
   for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
     const int4 U = __ldg(units + u);  // b0, b1, za, zb
     const int2 pr = __ldg(urange + u);
     const int za = U.z, nzb = min(U.w - U.z + T - 1, zmax);
-    const int run = nzb * nrhs;  // one (k0, k1) z-run, contiguous in w
+    const int run = nzb * nrhs;  // one (k0, k1) z-run (contiguous in w when the chunk is every column)
     __syncthreads();  // the previous unit is done with the block
     // 36 contiguous z-runs (one per node column of the block), a warp per run
     for (int ab = threadIdx.x >> 5; ab < T * T; ab += G3U_THREADS / 32) {
       const int a = ab / T, b = ab - a * T;
-      const double* src = w + (((size_t)(U.x + a) * m1 + (U.y + b)) * m2 + za) * nrhs;
+      const double* src = w + (((size_t)(U.x + a) * m1 + (U.y + b)) * m2 + za) * ldr + r0;
       double* dst = blk + ab * run;
       // cp.async: every copy of the block in flight at once (a load→store
       // loop paid one L2 round trip per iteration)
-      for (int q = threadIdx.x & 31; q < run; q += 32) g3_cp8(dst + q, src + q);
+      if (nrhs == ldr) {
+        for (int q = threadIdx.x & 31; q < run; q += 32) g3_cp8(dst + q, src + q);
+      } else {
+        for (int q = threadIdx.x & 31; q < run; q += 32) {
+          const int z = int((unsigned(q) * inv) >> 16);
+          g3_cp8(dst + q, src + (size_t)z * ldr + (q - z * nrhs));
+        }
+      }
     }
     g3_cp_wait_all();
     __syncthreads();
@@ -1817,7 +1832,7 @@ __global__ void __launch_bounds__(G3U_THREADS) k_gather_units3(DskiView op, cons
         }
       }
       constexpr int NG = GRAD ? 4 : 1;
-      const size_t idx0 = (size_t)sidx * nrhs + r;
+      const size_t idx0 = (size_t)sidx * ldr + r0 + r;
 #pragma unroll
       for (int g = 0; g < NG; ++g) {
         const size_t idx = idx0 + g * gstride;
@@ -1845,15 +1860,18 @@ __global__ void __launch_bounds__(S3U_THREADS) k_scatter_upush3(DskiView op, con
                                                                 int nunits, const int2* __restrict__ urange,
                                                                 const long long* __restrict__ uoff,
                                                                 const double* __restrict__ v,
-                                                                double* __restrict__ scratch, int nrhs) {
+                                                                double* __restrict__ scratch, int nrhs, int cw) {
+  // RHS columns [r0, r0 + cw) of nrhs (blockIdx.y = column chunk; cw·T ≤ threads)
+  const int r0 = blockIdx.y * cw, cwa = cw;  // cwa: the staging width allocated
+  cw = min(cw, nrhs - r0);
   constexpr int REC = 3 * 2 * T;
   constexpr int NG = GRAD ? 4 : 1;
   extern __shared__ double sm3[];
   double* sw = sm3;                       // [S3U_MAXP][REC]
-  double* sv = sw + S3U_MAXP * REC;       // [S3U_MAXP][NG][nrhs]
-  int* sz = reinterpret_cast<int*>(sv + S3U_MAXP * NG * nrhs);  // [S3U_MAXP]
+  double* sv = sw + S3U_MAXP * REC;       // [S3U_MAXP][NG][cw]
+  int* sz = reinterpret_cast<int*>(sv + S3U_MAXP * NG * cwa);  // [S3U_MAXP]
   const size_t gstride = (size_t)op.n * nrhs;
-  const int ntask = T * nrhs;  // thread (a, r) owns the T node columns (a, 0..T-1) of the block
+  const int ntask = T * cw;  // thread (a, r) owns the T node columns (a, 0..T-1) of the block
   for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
     const int4 U = __ldg(units + u);
     const int2 pr = __ldg(urange + u);
@@ -1868,7 +1886,7 @@ __global__ void __launch_bounds__(S3U_THREADS) k_scatter_upush3(DskiView op, con
     int zc = 0;
     const int tk = threadIdx.x;
     const bool live = tk < ntask;
-    const int a = live ? tk / nrhs : 0, r = live ? tk - (tk / nrhs) * nrhs : 0;
+    const int a = live ? tk / cw : 0, rl = live ? tk - (tk / cw) * cw : 0, r = r0 + rl;
     auto emit = [&]() {  // node zc of the T columns is final
       if (live)
 #pragma unroll
@@ -1888,9 +1906,9 @@ __global__ void __launch_bounds__(S3U_THREADS) k_scatter_upush3(DskiView op, con
       for (int e = threadIdx.x; e < np * REC / 2; e += S3U_THREADS)
         g3_cp16(sw + 2 * e, op.wts + (size_t)p0 * REC + 2 * e);
       for (int pl = threadIdx.x / 32; pl < np; pl += S3U_THREADS / 32)
-        for (int q = threadIdx.x & 31; q < NG * nrhs; q += 32) {
-          const int g = q / nrhs, rr = q - g * nrhs;
-          g3_cp8(sv + pl * NG * nrhs + q, v + g * gstride + (size_t)(p0 + pl) * nrhs + rr);
+        for (int q = threadIdx.x & 31; q < NG * cw; q += 32) {
+          const int g = q / cw, rr = q - g * cw;
+          g3_cp8(sv + pl * NG * cw + q, v + g * gstride + (size_t)(p0 + pl) * nrhs + r0 + rr);
         }
       for (int e = threadIdx.x; e < np; e += S3U_THREADS) g3_cp4(sz + e, &op.base[p0 + e].z);
       g3_cp_wait_all();
@@ -1899,14 +1917,14 @@ __global__ void __launch_bounds__(S3U_THREADS) k_scatter_upush3(DskiView op, con
         const double* w = sw + pl * REC;
         const int zo = sz[pl] - za;
         while (zc < zo) emit();
-        const double* vv = sv + pl * NG * nrhs + r;
+        const double* vv = sv + pl * NG * cw + rl;
         const double wa = w[a], v0 = vv[0];
         double ca, cb = 0.0, cc = 0.0;  // per-b coefficients: A_b = wb·ca + dwb·cb, B_b = wb·cc
         ca = wa * v0;
         if constexpr (GRAD) {
-          ca = fma(w[T + a], vv[nrhs], ca);
-          cb = wa * vv[2 * nrhs];
-          cc = wa * vv[3 * nrhs];
+          ca = fma(w[T + a], vv[cw], ca);
+          cb = wa * vv[2 * cw];
+          cc = wa * vv[3 * cw];
         }
         double z2[T], dz2[T];
 #pragma unroll
@@ -2169,9 +2187,14 @@ void DskiOp::scatter(const double* v, double* u, int nrhs, cudaStream_t s) const
     launched("dski scatter (d=1 node blocks)");
     return;
   }
-  if (d == 3 && variant == 0 && s3_uoff.p && G && T * nrhs <= S3U_THREADS) {  // unit push + merge
+  if (d == 3 && variant == 0 && s3_uoff.p && G) {  // unit push + merge
     const int NG = 4;
-    const size_t smem = sizeof(double) * size_t(S3U_MAXP) * (3 * 2 * T + NG * nrhs) + sizeof(int) * S3U_MAXP;
+    // RHS columns in chunks of at most S3U_THREADS / T (blockIdx.y), so the
+    // unit path serves any RHS count (beyond 21 columns it used to fall back
+    // to the per-column lists: 32 RHS 362 µs)
+    const int nch = (T * nrhs + S3U_THREADS - 1) / S3U_THREADS;
+    const int cw = (nrhs + nch - 1) / nch;
+    const size_t smem = sizeof(double) * size_t(S3U_MAXP) * (3 * 2 * T + NG * cw) + sizeof(int) * S3U_MAXP;
     const void* fn = T == 6 ? (const void*)k_scatter_upush3<6, true> : (const void*)k_scatter_upush3<4, true>;
     if (smem > 48 * 1024) raise_smem_limit(fn, smem);
     s3_scratch.reserve(static_cast<size_t>(s3_nodes) * nrhs);
@@ -2182,9 +2205,9 @@ void DskiOp::scatter(const double* v, double* u, int nrhs, cudaStream_t s) const
       else k_scatter_upush3d<4, true><<<gd, 64, 0, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, s3_uoff.p, v, s3_scratch.p, nrhs);
       launched("dski scatter (d=3 unit push, direct)");
     } else {
-    const unsigned gp = static_cast<unsigned>(std::min(g3_nunits, 148 * 16));
-    if (T == 6) k_scatter_upush3<6, true><<<gp, S3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, s3_uoff.p, v, s3_scratch.p, nrhs);
-    else k_scatter_upush3<4, true><<<gp, S3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, s3_uoff.p, v, s3_scratch.p, nrhs);
+    const dim3 gp(static_cast<unsigned>(std::max(1, std::min(g3_nunits, 148 * 16 / nch))), static_cast<unsigned>(nch));
+    if (T == 6) k_scatter_upush3<6, true><<<gp, S3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, s3_uoff.p, v, s3_scratch.p, nrhs, cw);
+    else k_scatter_upush3<4, true><<<gp, S3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, s3_uoff.p, v, s3_scratch.p, nrhs, cw);
     launched("dski scatter (d=3 unit push)");
     }
     const int ncol = m[0] * m[1];
@@ -2292,26 +2315,40 @@ void DskiOp::gather(const double* w, const double* v, double* out, int nrhs, boo
     return;
   }
   if (d == 3 && variant == 0 && g3_units.p && nrhs >= 4) {  // (1-3 RHS: the lean gather measured faster)
-    const size_t smem = sizeof(double) * size_t(T) * T * g3_zspan * nrhs;
+    // RHS chunks of ≤ 17 columns (blockIdx.y): 64 RHS staged whole took
+    // 166 KB per CTA (one CTA per SM)
+    const int nch = (nrhs + 16) / 17;
+    const int cw = (nrhs + nch - 1) / nch;
+    const size_t smem = sizeof(double) * size_t(T) * T * g3_zspan * cw;
     if (smem <= 200 * 1024) {
       const void* fn = T == 6 ? (G ? (const void*)k_gather_units3<6, true> : (const void*)k_gather_units3<6, false>)
                               : (G ? (const void*)k_gather_units3<4, true> : (const void*)k_gather_units3<4, false>);
       raise_smem_limit(fn, smem);
       GK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, int(cudaSharedmemCarveoutMaxShared)));
-      const unsigned grid = static_cast<unsigned>(std::min(g3_nunits, 148 * 16));
+      const dim3 grid(static_cast<unsigned>(std::max(1, std::min(g3_nunits, 148 * 16 / nch))), static_cast<unsigned>(nch));
       const int d3 = g_tuning.d3.load();
-      if (T == 6 && G && (nrhs == 16 || nrhs == 17) && !(d3 & 512)) {
-        const void* fs = nrhs == 16 ? (const void*)k_gather_units3<6, true, 16> : (const void*)k_gather_units3<6, true, 17>;
+      const int nz = noise ? 1 : 0;
+      if (T == 6 && G && (cw == 16 || cw == 17) && nrhs % cw == 0 && !(d3 & 512)) {
+        const void* fs = nch == 1 ? (cw == 16 ? (const void*)k_gather_units3<6, true, 16, true> : (const void*)k_gather_units3<6, true, 17, true>)
+                                  : (cw == 16 ? (const void*)k_gather_units3<6, true, 16> : (const void*)k_gather_units3<6, true, 17>);
         raise_smem_limit(fs, smem);
         GK_CUDA(cudaFuncSetAttribute(fs, cudaFuncAttributePreferredSharedMemoryCarveout, int(cudaSharedmemCarveoutMaxShared)));
-        if (nrhs == 16) k_gather_units3<6, true, 16><<<grid, G3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, w, v, out, nrhs, noise ? 1 : 0, g3_zspan, d3);
-        else k_gather_units3<6, true, 17><<<grid, G3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, w, v, out, nrhs, noise ? 1 : 0, g3_zspan, d3);
+        auto args = [&](auto kern) {
+          kern<<<grid, G3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, w, v, out, nrhs, cw, nz, g3_zspan, d3);
+        };
+        if (nch == 1) {
+          if (cw == 16) args(k_gather_units3<6, true, 16, true>);
+          else args(k_gather_units3<6, true, 17, true>);
+        } else {
+          if (cw == 16) args(k_gather_units3<6, true, 16>);
+          else args(k_gather_units3<6, true, 17>);
+        }
       } else if (T == 6) {
-        if (G) k_gather_units3<6, true><<<grid, G3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, w, v, out, nrhs, noise ? 1 : 0, g3_zspan, g_tuning.d3.load());
-        else k_gather_units3<6, false><<<grid, G3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, w, v, out, nrhs, noise ? 1 : 0, g3_zspan, g_tuning.d3.load());
+        if (G) k_gather_units3<6, true><<<grid, G3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, w, v, out, nrhs, cw, nz, g3_zspan, d3);
+        else k_gather_units3<6, false><<<grid, G3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, w, v, out, nrhs, cw, nz, g3_zspan, d3);
       } else {
-        if (G) k_gather_units3<4, true><<<grid, G3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, w, v, out, nrhs, noise ? 1 : 0, g3_zspan, g_tuning.d3.load());
-        else k_gather_units3<4, false><<<grid, G3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, w, v, out, nrhs, noise ? 1 : 0, g3_zspan, g_tuning.d3.load());
+        if (G) k_gather_units3<4, true><<<grid, G3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, w, v, out, nrhs, cw, nz, g3_zspan, d3);
+        else k_gather_units3<4, false><<<grid, G3U_THREADS, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, w, v, out, nrhs, cw, nz, g3_zspan, d3);
       }
       launched("dski gather (d=3 cell-line units)");
       return;

@@ -247,7 +247,7 @@ def test_d3_tile_scatter_matches_oracle(order, with_gradients):
         assert rel(default, ref) <= TOL and rel(default, lists) <= 1e-13
 
 
-@pytest.mark.parametrize("nrhs", [1, 2, 5, 6, 16, 17, 21])
+@pytest.mark.parametrize("nrhs", [1, 2, 5, 6, 16, 17, 21, 33, 64])
 def test_d3_unit_paths_bit_identical_and_match_oracle(nrhs):
     """The d = 3 unit-push scatter (staged, and the direct variant for
     T*nrhs <= 32), the merge over per-node lists and the gather's 16-column

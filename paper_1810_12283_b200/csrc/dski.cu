@@ -2314,7 +2314,9 @@ void DskiOp::gather(const double* w, const double* v, double* out, int nrhs, boo
     launched("dski gather");
     return;
   }
-  if (d == 3 && variant == 0 && g3_units.p && nrhs >= 4) {  // (1-3 RHS: the lean gather measured faster)
+  // (every RHS count since the cp.async staging: 1 RHS 34.8 -> 30.8 µs and
+  // 3 RHS 43.0 -> 32.7 µs against the lean gather)
+  if (d == 3 && variant == 0 && g3_units.p && !(g_tuning.d3.load() & 1024)) {
     // RHS chunks of ≤ 17 columns (blockIdx.y): 64 RHS staged whole took
     // 166 KB per CTA (one CTA per SM)
     const int nch = (nrhs + 16) / 17;

@@ -253,7 +253,7 @@ def test_d3_unit_paths_bit_identical_and_match_oracle(nrhs):
     T*nrhs <= 32), the merge over per-node lists and the gather's 16-column
     task blocks (with the compile-time 16/17-column instantiations) against
     the oracle, and bit for bit against the earlier variants they replaced
-    (tuning "d3": 1 list-walk merge, 4 staged push for few RHS, 512 runtime
+    (tuning "d3": 1 list-walk merge, 4 staged push for few RHS, 1024 lean gather, 512 runtime
     RHS count in the gather)."""
     rng = np.random.default_rng(31 + nrhs)
     X = rng.uniform(0.0, 1.0, (700, 3))
@@ -265,7 +265,7 @@ def test_d3_unit_paths_bit_identical_and_match_oracle(nrhs):
     ref = r.mvm(V)
     default = g.mvm(V)
     assert rel(default, ref) <= TOL
-    prev = gk.set_tuning("d3", 1 | 4 | 512)
+    prev = gk.set_tuning("d3", 1 | 4 | 512 | 1024)
     try:
         old = g.mvm(V)
     finally:

@@ -2014,6 +2014,97 @@ __global__ void __launch_bounds__(64) k_scatter_upush3d(DskiView op, const int4*
   }
 }
 
+// Few right-hand sides (T·nrhs ≤ 32): a warp per unit. The warp stages a
+// chunk of the unit's points (weights, v rows, base z) with cp.async — one
+// L2 round trip per 32 points instead of one per point in the direct walk
+// (k_scatter_upush3d) — then lanes (a, r) run the rolling window over it.
+// Same per-node order as k_scatter_upush3.
+constexpr int S3W_CH = 32;
+template <int T, bool GRAD>
+__global__ void __launch_bounds__(128) k_scatter_upush3w(DskiView op, const int4* __restrict__ units, int nunits,
+                                                         const int2* __restrict__ urange,
+                                                         const long long* __restrict__ uoff,
+                                                         const double* __restrict__ v,
+                                                         double* __restrict__ scratch, int nrhs) {
+  constexpr int REC = 3 * 2 * T;
+  constexpr int NG = GRAD ? 4 : 1;
+  extern __shared__ __align__(16) double smw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int per_warp = S3W_CH * (REC + NG * nrhs) + S3W_CH / 2;  // doubles (+ the z ints)
+  double* sw = smw + (size_t)warp * per_warp;  // [CH][REC]
+  double* sv = sw + S3W_CH * REC;              // [CH][NG][nrhs]
+  int* sz = reinterpret_cast<int*>(sv + S3W_CH * NG * nrhs);  // [CH]
+  const size_t gstride = (size_t)op.n * nrhs;
+  const int ntask = T * nrhs;
+  const bool live = lane < ntask;
+  const int a = live ? lane / nrhs : 0, r = live ? lane - (lane / nrhs) * nrhs : 0;
+  for (int u = blockIdx.x * 4 + warp; u < nunits; u += gridDim.x * 4) {
+    const int4 U = __ldg(units + u);
+    const int2 pr = __ldg(urange + u);
+    const int za = U.z, nzb = U.w - U.z + T - 1;
+    double* out = scratch + (size_t)__ldg(uoff + u) * nrhs;
+    double acc[T][T];
+#pragma unroll
+    for (int b = 0; b < T; ++b)
+#pragma unroll
+      for (int t = 0; t < T; ++t) acc[b][t] = 0.0;
+    int zc = 0;
+    auto emit = [&]() {
+      if (live)
+#pragma unroll
+        for (int b = 0; b < T; ++b) out[((size_t)(a * T + b) * nzb + zc) * nrhs + r] = acc[b][0];
+#pragma unroll
+      for (int b = 0; b < T; ++b) {
+#pragma unroll
+        for (int k = 0; k < T - 1; ++k) acc[b][k] = acc[b][k + 1];
+        acc[b][T - 1] = 0.0;
+      }
+      ++zc;
+    };
+    for (int p0 = pr.x; p0 < pr.y; p0 += S3W_CH) {
+      const int np = min(S3W_CH, pr.y - p0);
+      __syncwarp();  // the previous chunk is consumed
+      for (int e = lane; e < np * REC / 2; e += 32) g3_cp16(sw + 2 * e, op.wts + (size_t)p0 * REC + 2 * e);
+      for (int q = lane; q < np * NG * nrhs; q += 32) {
+        const int pl = q / (NG * nrhs), rem = q - pl * (NG * nrhs);
+        const int g = rem / nrhs, rr = rem - g * nrhs;
+        g3_cp8(sv + q, v + g * gstride + (size_t)(p0 + pl) * nrhs + rr);
+      }
+      for (int e = lane; e < np; e += 32) g3_cp4(sz + e, &op.base[p0 + e].z);
+      g3_cp_wait_all();
+      __syncwarp();
+      for (int pl = 0; pl < np; ++pl) {
+        const double* w = sw + pl * REC;
+        const int zo = sz[pl] - za;
+        while (zc < zo) emit();
+        const double* vv = sv + pl * NG * nrhs + r;
+        const double wa = w[a], v0 = vv[0];
+        double ca = wa * v0, cb = 0.0, cc = 0.0;
+        if constexpr (GRAD) {
+          ca = fma(w[T + a], vv[nrhs], ca);
+          cb = wa * vv[2 * nrhs];
+          cc = wa * vv[3 * nrhs];
+        }
+        double z2[T], dz2[T];
+#pragma unroll
+        for (int c = 0; c < T; ++c) {
+          z2[c] = w[4 * T + c];
+          dz2[c] = GRAD ? w[5 * T + c] : 0.0;
+        }
+#pragma unroll
+        for (int b = 0; b < T; ++b) {
+          const double wb = w[2 * T + b];
+          const double A = GRAD ? fma(w[3 * T + b], cb, wb * ca) : wb * ca;
+          const double Bc = wb * cc;
+#pragma unroll
+          for (int c = 0; c < T; ++c) acc[b][c] = GRAD ? fma(dz2[c], Bc, fma(z2[c], A, acc[b][c])) : fma(z2[c], A, acc[b][c]);
+        }
+      }
+    }
+    while (zc < nzb) emit();
+  }
+}
+
 // Merge: u(col, z, r) = Σ over the entries {unit, ab} of column col whose
 // block covers z, in the column's fixed (za, unit) order.
 __global__ void __launch_bounds__(256) k_scatter_merge3(int ncol, int m2, int nzs, int T,
@@ -2198,7 +2289,15 @@ void DskiOp::scatter(const double* v, double* u, int nrhs, cudaStream_t s) const
     const void* fn = T == 6 ? (const void*)k_scatter_upush3<6, true> : (const void*)k_scatter_upush3<4, true>;
     if (smem > 48 * 1024) raise_smem_limit(fn, smem);
     s3_scratch.reserve(static_cast<size_t>(s3_nodes) * nrhs);
-    if (T * nrhs <= 32 && !(g_tuning.d3.load() & 4)) {
+    if (T * nrhs <= 32 && !(g_tuning.d3.load() & (4 | 2048))) {
+      const size_t wsm = sizeof(double) * 4 * (size_t(S3W_CH) * (3 * 2 * T + NG * nrhs) + S3W_CH / 2);
+      const void* fw = T == 6 ? (const void*)k_scatter_upush3w<6, true> : (const void*)k_scatter_upush3w<4, true>;
+      if (wsm > 48 * 1024) raise_smem_limit(fw, wsm);
+      const unsigned gw = static_cast<unsigned>(std::max(1, (g3_nunits + 3) / 4));
+      if (T == 6) k_scatter_upush3w<6, true><<<gw, 128, wsm, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, s3_uoff.p, v, s3_scratch.p, nrhs);
+      else k_scatter_upush3w<4, true><<<gw, 128, wsm, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, s3_uoff.p, v, s3_scratch.p, nrhs);
+      launched("dski scatter (d=3 unit push, warp per unit)");
+    } else if (T * nrhs <= 32 && !(g_tuning.d3.load() & 4)) {
       const long long nt = static_cast<long long>(g3_nunits) * T * nrhs;
       const unsigned gd = static_cast<unsigned>(std::max<long long>(1, (nt + 63) / 64));
       if (T == 6) k_scatter_upush3d<6, true><<<gd, 64, 0, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, s3_uoff.p, v, s3_scratch.p, nrhs);

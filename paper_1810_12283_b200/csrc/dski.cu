@@ -2154,21 +2154,26 @@ __global__ void __launch_bounds__(256) k_scatter_merge3(int ncol, int m2, int nz
 // which ~6 cover it). Same per-node summation order: bit-identical.
 constexpr int M3F_THREADS = 256;
 constexpr int M3F_UNROLL = 8;  // a node's list (~6 blocks) in one round of loads
-__global__ void __launch_bounds__(M3F_THREADS) k_scatter_merge3f(int ncol, int m2, const int* __restrict__ zoff,
+__global__ void __launch_bounds__(M3F_THREADS) k_scatter_merge3f(int ngroups, int gn, int nnodes,
+                                                                const int* __restrict__ zoff,
                                                                 const int* __restrict__ zlist,
                                                                 const double* __restrict__ scratch,
                                                                 double* __restrict__ u, int nrhs) {
-  extern __shared__ int sl[];  // [m2 + 1] list starts relative to the column, then the column's list
-  int* li = sl + m2 + 1;
-  const int nout = m2 * nrhs;
-  for (int col = blockIdx.x; col < ncol; col += gridDim.x) {
-    const int* zo = zoff + (size_t)col * m2;
-    const int b0 = __ldg(zo), nl = __ldg(zo + m2) - b0;
+  // CTA per group of gn consecutive nodes (whole node columns: one column, or
+  // several when a column has fewer outputs than threads); nodes (col, z)
+  // are consecutive in both zoff and u
+  extern __shared__ int sl[];  // [gn + 1] list starts relative to the group, then the group's list
+  int* li = sl + gn + 1;
+  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    const int n0 = grp * gn, nn = min(gn, nnodes - n0);
+    const int* zo = zoff + n0;
+    const int b0 = __ldg(zo), nl = __ldg(zo + nn) - b0;
     __syncthreads();
-    for (int z = threadIdx.x; z <= m2; z += M3F_THREADS) sl[z] = __ldg(zo + z) - b0;
+    for (int z = threadIdx.x; z <= nn; z += M3F_THREADS) sl[z] = __ldg(zo + z) - b0;
     for (int i = threadIdx.x; i < nl; i += M3F_THREADS) li[i] = __ldg(zlist + b0 + i);
     __syncthreads();
-    double* uc = u + (size_t)col * m2 * nrhs;
+    double* uc = u + (size_t)n0 * nrhs;
+    const int nout = nn * nrhs;
     for (int o = threadIdx.x; o < nout; o += M3F_THREADS) {
       const int z = o / nrhs, r = o - z * nrhs;
       const int s1 = sl[z + 1];
@@ -2310,11 +2315,15 @@ void DskiOp::scatter(const double* v, double* u, int nrhs, cudaStream_t s) const
     launched("dski scatter (d=3 unit push)");
     }
     const int ncol = m[0] * m[1];
-    const size_t msm = sizeof(int) * (size_t(m[2]) + 1 + size_t(s3_maxl));
+    // columns per CTA: one, or several when a column's outputs (m2 · nrhs)
+    // leave most of the CTA idle (1 RHS: 48 outputs for 256 threads)
+    const int cpb = (g_tuning.d3.load() & 4096) ? 1 : std::max(1, M3F_THREADS / (m[2] * nrhs));
+    const size_t msm = sizeof(int) * (size_t(cpb) * m[2] + 1 + size_t(cpb) * s3_maxl);
     if (s3_zoff.p && msm <= 96 * 1024 && !(g_tuning.d3.load() & 1)) {
       raise_smem_limit((const void*)k_scatter_merge3f, msm);
-      k_scatter_merge3f<<<static_cast<unsigned>(std::min(ncol, 148 * 32)), M3F_THREADS, msm, s>>>(
-          ncol, m[2], s3_zoff.p, s3_zlist.p, s3_scratch.p, u, nrhs);
+      const int ngroups = (ncol + cpb - 1) / cpb;
+      k_scatter_merge3f<<<static_cast<unsigned>(std::min(ngroups, 148 * 32)), M3F_THREADS, msm, s>>>(
+          ngroups, cpb * m[2], ncol * m[2], s3_zoff.p, s3_zlist.p, s3_scratch.p, u, nrhs);
       launched("dski scatter (d=3 unit merge, per-node lists)");
       return;
     }

@@ -247,8 +247,9 @@ def test_d3_tile_scatter_matches_oracle(order, with_gradients):
         assert rel(default, ref) <= TOL and rel(default, lists) <= 1e-13
 
 
-@pytest.mark.parametrize("nrhs", [1, 2, 5, 6, 16, 17, 21, 33, 64])
-def test_d3_unit_paths_bit_identical_and_match_oracle(nrhs):
+@pytest.mark.parametrize("order", [0, 1])
+@pytest.mark.parametrize("nrhs", [1, 2, 5, 6, 8, 16, 17, 21, 33, 64])
+def test_d3_unit_paths_bit_identical_and_match_oracle(nrhs, order):
     """The d = 3 unit-push scatter (staged, and the direct variant for
     T*nrhs <= 32), the merge over per-node lists and the gather's 16-column
     task blocks (with the compile-time 16/17-column instantiations) against
@@ -259,13 +260,13 @@ def test_d3_unit_paths_bit_identical_and_match_oracle(nrhs):
     X = rng.uniform(0.0, 1.0, (700, 3))
     X[:300, 2] = 0.5 + 1e-3 * rng.standard_normal(300)  # a dense sheet: long units, many points per cell
     grid = gk.Grid.cover(X, 0.05, 3, 24)
-    g = gk.DskiOperator(gk.KernelSpec(0.3, 1.0), grid, X, (0.1, 0.05))
-    r = O.DskiOperator(O.KernelSpec(0.3, 1.0), O.Grid(grid.dims, grid.origin, grid.spacing), X, (0.1, 0.05))
+    g = gk.DskiOperator(gk.KernelSpec(0.3, 1.0), grid, X, (0.1, 0.05), order)
+    r = O.DskiOperator(O.KernelSpec(0.3, 1.0), O.Grid(grid.dims, grid.origin, grid.spacing), X, (0.1, 0.05), order)
     V = rng.standard_normal((g.size(), nrhs))
     ref = r.mvm(V)
     default = g.mvm(V)
     assert rel(default, ref) <= TOL
-    prev = gk.set_tuning("d3", 1 | 4 | 512 | 1024)
+    prev = gk.set_tuning("d3", 1 | 4 | 512 | 1024 | 4096)
     try:
         old = g.mvm(V)
     finally:

@@ -1,4 +1,7 @@
 #include <thread>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <atomic>
 #include <chrono>
 #include <cstdio>
@@ -221,6 +224,7 @@ int gk_set_tuning(const char* key, int value) {
                            : k == "fused_prof" ? &g_tuning.fused_prof
                            : k == "pcg_fused" ? &g_tuning.pcg_fused
                            : k == "e2e_chunk" ? &g_tuning.e2e_chunk
+                           : k == "e2e_stage" ? &g_tuning.e2e_stage
                            : k == "d3" ? &g_tuning.d3
                            : k == "dskip" ? &g_tuning.dskip
                            : k == "lanczos" ? &g_tuning.lanczos
@@ -410,6 +414,105 @@ void gk_op_destroy(gk_op* op) {
 int64_t gk_op_size(const gk_op* op) { return op && op->impl ? op->impl->N : -1; }
 int gk_op_kind(const gk_op* op) { return op && op->impl ? op->impl->kind : -1; }
 
+// Parallel host copies for the pageable-buffer MVM: a small persistent pool
+// (one copy per call is split over the workers and the calling thread). A
+// single-threaded memcpy, or the driver's own staging of pageable copies
+// (one bounce buffer), moves ~10 GB/s; the copy engines take ~50.
+namespace {
+class HostCopyPool {
+ public:
+  static HostCopyPool& get() {
+    static HostCopyPool p;
+    return p;
+  }
+  // copy ncols columns of `rows` doubles, src/dst with their own leading dims
+  void copy_cols(double* dst, size_t ldd, const double* src, size_t lds, size_t rows, size_t ncols) {
+    const size_t total = rows * ncols;
+    const int parts = int(std::min<size_t>(workers_.size() + 1, std::max<size_t>(1, total / (64 * 1024))));
+    auto piece = [=](int k) {  // elements [k·total/parts, (k+1)·total/parts) in column-major order
+      size_t e = total * size_t(k) / size_t(parts);
+      const size_t end = total * size_t(k + 1) / size_t(parts);
+      while (e < end) {
+        const size_t c = e / rows, r = e - c * rows, len = std::min(rows - r, end - e);
+        std::memcpy(dst + c * ldd + r, src + c * lds + r, len * sizeof(double));
+        e += len;
+      }
+    };
+    if (parts == 1) {
+      piece(0);
+      return;
+    }
+    std::lock_guard<std::mutex> call(call_mu_);  // one job at a time (operators on other threads)
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = piece;
+      nparts_ = parts;
+      next_ = 1;
+      done_ = 0;
+      ++gen_;
+    }
+    cv_.notify_all();
+    piece(0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return done_ == nparts_ - 1; });
+  }
+
+ private:
+  HostCopyPool() {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const char* env = std::getenv("GK_COPY_THREADS");  // total copy threads incl. the caller (default 8)
+    const unsigned want = env ? unsigned(std::max(1, std::atoi(env))) : 8u;
+    const int n = int(std::min(want - 1, hw > 1 ? hw - 1 : 0u));
+    for (int i = 0; i < n; ++i) workers_.emplace_back([this] { run(); });
+  }
+  ~HostCopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  void run() {
+    std::uint64_t seen = 0;
+    for (;;) {
+      std::function<void(int)> job;
+      int k = -1;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || (gen_ != seen && next_ < nparts_); });
+        if (stop_) return;
+        k = next_++;
+        job = job_;
+        if (next_ >= nparts_) seen = gen_;
+      }
+      job(k);
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        ++done_;
+      }
+      done_cv_.notify_one();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_, call_mu_;
+  std::condition_variable cv_, done_cv_;
+  std::function<void(int)> job_;
+  int nparts_ = 0, next_ = 0, done_ = 0;
+  std::uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+bool is_pinned_host(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+}  // namespace
+
 gk_status gk_op_mvm(const gk_op* h, const double* V, int64_t ldv, double* Out, int64_t ldo, int64_t nrhs) {
   return guard([&] {
     Op& op = O(h);
@@ -435,7 +538,7 @@ gk_status gk_op_mvm(const gk_op* h, const double* V, int64_t ldv, double* Out, i
       GK_CUDA(cudaStreamCreateWithFlags(&op.io_pin, cudaStreamNonBlocking));
       GK_CUDA(cudaStreamCreateWithFlags(&op.io_pout, cudaStreamNonBlocking));
     }
-    while (int(op.io_events.size()) < 4 * nchunks + 1) {
+    while (int(op.io_events.size()) < 5 * nchunks + 1) {
       cudaEvent_t e;
       GK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       op.io_events.push_back(e);
@@ -445,16 +548,42 @@ gk_status gk_op_mvm(const gk_op* h, const double* V, int64_t ldv, double* Out, i
     op.io_int_in.reserve(tot);
     op.io_int_out.reserve(tot);
     op.io_ext_out.reserve(tot);
+    // Pageable host buffers (e.g. Eigen storage): chunks go through pinned
+    // staging copied by the host pool — chunk j+1 is copied in while the
+    // device works on chunk j, and chunk j's result is copied out as soon as
+    // its D2H copy has landed — instead of the driver's serial bounce-buffer
+    // staging of pageable copies (tuning "e2e_stage" = 1 turns it off).
+    const bool stage_in = g_tuning.e2e_stage.load() == 0 && !is_pinned_host(V);
+    const bool stage_out = g_tuning.e2e_stage.load() == 0 && !is_pinned_host(Out);
+    if (stage_in) op.io_pin_in.reserve(tot);
+    if (stage_out) op.io_pin_out.reserve(tot);
+    const double* Vsrc = stage_in ? op.io_pin_in.p : V;
+    const i64 ldvs = stage_in ? op.N : ldv;
+    double* Odst = stage_out ? op.io_pin_out.p : Out;
+    const i64 ldos = stage_out ? op.N : ldo;
+    HostCopyPool& pool = HostCopyPool::get();
+    auto copy_in = [&](int j) {
+      const i64 c0 = i64(j) * chunk;
+      const int nb = int(std::min<i64>(chunk, nrhs - c0));
+      pool.copy_cols(op.io_pin_in.p + static_cast<size_t>(op.N) * c0, op.N, V + c0 * ldv, ldv, op.N, nb);
+    };
+    auto copy_out = [&](int j) {
+      const i64 c0 = i64(j) * chunk;
+      const int nb = int(std::min<i64>(chunk, nrhs - c0));
+      GK_CUDA(cudaEventSynchronize(op.io_events[5 * j + 4]));  // chunk j's D2H copy landed
+      pool.copy_cols(Out + c0 * ldo, ldo, op.io_pin_out.p + static_cast<size_t>(op.N) * c0, op.N, op.N, nb);
+    };
+    if (stage_in) copy_in(0);
     // the side streams must not start before earlier work on the compute stream
-    cudaEvent_t e0 = op.io_events[4 * nchunks];
+    cudaEvent_t e0 = op.io_events[5 * nchunks];
     GK_CUDA(cudaEventRecord(e0, s));
     for (cudaStream_t t : {op.io_in, op.io_out, op.io_pin, op.io_pout}) GK_CUDA(cudaStreamWaitEvent(t, e0, 0));
     for (int j = 0; j < nchunks; ++j) {
       const i64 c0 = i64(j) * chunk;
       const int nb = int(std::min<i64>(chunk, nrhs - c0));
       const size_t off = static_cast<size_t>(op.N) * c0;
-      cudaEvent_t* ev = &op.io_events[4 * j];
-      GK_CUDA(cudaMemcpy2DAsync(op.io_ext_in.p + off, sizeof(double) * op.N, V + c0 * ldv, sizeof(double) * ldv,
+      cudaEvent_t* ev = &op.io_events[5 * j];
+      GK_CUDA(cudaMemcpy2DAsync(op.io_ext_in.p + off, sizeof(double) * op.N, Vsrc + c0 * ldvs, sizeof(double) * ldvs,
                                 sizeof(double) * op.N, nb, cudaMemcpyHostToDevice, op.io_in));
       GK_CUDA(cudaEventRecord(ev[0], op.io_in));
       GK_CUDA(cudaStreamWaitEvent(op.io_pin, ev[0], 0));
@@ -467,9 +596,13 @@ gk_status gk_op_mvm(const gk_op* h, const double* V, int64_t ldv, double* Out, i
       op.from_internal(op.io_int_out.p + off, op.io_ext_out.p + off, op.N, nb, op.io_pout);
       GK_CUDA(cudaEventRecord(ev[3], op.io_pout));
       GK_CUDA(cudaStreamWaitEvent(op.io_out, ev[3], 0));
-      GK_CUDA(cudaMemcpy2DAsync(Out + c0 * ldo, sizeof(double) * ldo, op.io_ext_out.p + off, sizeof(double) * op.N,
+      GK_CUDA(cudaMemcpy2DAsync(Odst + c0 * ldos, sizeof(double) * ldos, op.io_ext_out.p + off, sizeof(double) * op.N,
                                 sizeof(double) * op.N, nb, cudaMemcpyDeviceToHost, op.io_out));
+      GK_CUDA(cudaEventRecord(ev[4], op.io_out));
+      if (stage_in && j + 1 < nchunks) copy_in(j + 1);  // overlaps the device work on chunk j
+      if (stage_out && j >= 1) copy_out(j - 1);
     }
+    if (stage_out) copy_out(nchunks - 1);
     GK_CUDA(cudaStreamSynchronize(op.io_out));
     GK_CUDA(cudaStreamSynchronize(s));
   });

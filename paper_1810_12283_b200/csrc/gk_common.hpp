@@ -49,6 +49,7 @@ struct Tuning {
   std::atomic<int> f2_smode{0}, f2_gmode{0};  // 1 staged, 2 direct (0 = default)
   std::atomic<int> f2_nspl{0}, f2_nst{0};
   std::atomic<int> e2e_chunk{0};
+  std::atomic<int> e2e_stage{0};  // 1 = pageable host buffers go straight to cudaMemcpyAsync (driver staging)
   std::atomic<int> d3{0};  // d = 3 MVM A/B bitmask (2: r-fastest gather tasks for every RHS count)  // gk_op_mvm pipeline chunk width (0 = auto)
   // D-SKIP Hadamard kernels: 0 = TMA-ring DMMA (v3, falling back to v2 for odd
   // sizes), 3 = cp.async DMMA (v2), 1 = first generation
@@ -188,6 +189,7 @@ struct Op {
   cudaStream_t io_in = nullptr, io_out = nullptr, io_pin = nullptr, io_pout = nullptr;
   std::vector<cudaEvent_t> io_events;
   DevBuf<double> io_ext_in, io_int_in, io_int_out, io_ext_out;
+  HostBuf io_pin_in, io_pin_out;  // pinned staging for pageable caller buffers
 
   virtual void mvm(const double* in, double* out, int nrhs, cudaStream_t s) = 0;
   // diagonal including noise, internal order

@@ -1,4 +1,5 @@
 #include <thread>
+#include <unistd.h>
 #include <condition_variable>
 #include <functional>
 #include <mutex>
@@ -428,7 +429,9 @@ class HostCopyPool {
   // copy ncols columns of `rows` doubles, src/dst with their own leading dims
   void copy_cols(double* dst, size_t ldd, const double* src, size_t lds, size_t rows, size_t ncols) {
     const size_t total = rows * ncols;
-    const int parts = int(std::min<size_t>(workers_.size() + 1, std::max<size_t>(1, total / (64 * 1024))));
+    // a forked child inherits the pool object but not its threads: copy serially there
+    const size_t nw = getpid() == pid_ ? workers_.size() : 0;
+    const int parts = int(std::min<size_t>(nw + 1, std::max<size_t>(1, total / (64 * 1024))));
     auto piece = [=](int k) {  // elements [k·total/parts, (k+1)·total/parts) in column-major order
       size_t e = total * size_t(k) / size_t(parts);
       const size_t end = total * size_t(k + 1) / size_t(parts);
@@ -458,7 +461,7 @@ class HostCopyPool {
   }
 
  private:
-  HostCopyPool() {
+  HostCopyPool() : pid_(getpid()) {
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
     const char* env = std::getenv("GK_COPY_THREADS");  // total copy threads incl. the caller (default 8)
     const unsigned want = env ? unsigned(std::max(1, std::atoi(env))) : 8u;
@@ -501,6 +504,7 @@ class HostCopyPool {
   int nparts_ = 0, next_ = 0, done_ = 0;
   std::uint64_t gen_ = 0;
   bool stop_ = false;
+  pid_t pid_;
 };
 
 bool is_pinned_host(const void* p) {

@@ -93,3 +93,41 @@ def test_dev_entry_points_ordered_against_host_calls():
         assert np.array_equal(d, want_diag)
     for x in xs:
         assert np.array_equal(x, want_x)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nrhs", [1, 7, 32, 45])
+def test_host_mvm_pageable_staging_matches_pinned_and_direct(nrhs):
+    """gk_op_mvm from pageable buffers (pinned staging by the host copy pool,
+    chunked, with leading dimensions larger than N) returns exactly what the
+    driver's direct pageable copies and pinned buffers return."""
+    import torch
+    X, y, dY = gk.make_dataset(2, 0)
+    X = X[:3000]
+    grid = gk.Grid.cover(X, 1e-3, 3, 60)
+    op = gk.DskiOperator(gk.KernelSpec(0.2, 1.0), grid, X, (1e-2, 1e-2))
+    N = op.size()
+    ld = N + 5
+    rng = np.random.default_rng(nrhs)
+    Vp = np.asfortranarray(rng.standard_normal((ld, nrhs)))
+    outs = {}
+    for stage in (0, 1):
+        prev = gk.set_tuning("e2e_stage", stage)
+        try:
+            O = np.zeros((ld, nrhs), order="F")
+            gk._check(gk._lib.gk_op_mvm(op.handle, gk._p(Vp), ld, gk._p(O), ld, nrhs))
+        finally:
+            gk.set_tuning("e2e_stage", prev)
+        outs[stage] = O[:N].copy()
+        assert not O[N:].any()  # rows past N untouched
+    Vpin = torch.from_numpy(Vp.T.copy()).pin_memory()  # (nrhs, ld) row-major = column-major (ld, nrhs)
+    Opin = torch.zeros_like(Vpin).pin_memory()
+    gk._check(gk._lib.gk_op_mvm(op.handle, ctypes_ptr(Vpin), ld, ctypes_ptr(Opin), ld, nrhs))
+    pinned = Opin.numpy().T[:N]
+    assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[0], pinned)
+
+
+def ctypes_ptr(t):
+    import ctypes
+    return ctypes.cast(t.data_ptr(), ctypes.POINTER(ctypes.c_double))

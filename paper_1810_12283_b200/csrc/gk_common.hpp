@@ -50,7 +50,11 @@ struct Tuning {
   std::atomic<int> f2_nspl{0}, f2_nst{0};
   std::atomic<int> e2e_chunk{0};
   std::atomic<int> e2e_stage{0};  // 1 = pageable host buffers go straight to cudaMemcpyAsync (driver staging)
-  std::atomic<int> d3{0};  // d = 3 MVM A/B bitmask (2: r-fastest gather tasks for every RHS count)  // gk_op_mvm pipeline chunk width (0 = auto)
+  // d = 3 MVM A/B bitmask (0 = the measured default; each bit restores the variant it replaced):
+  //   1 list-walk merge (k_scatter_merge3), 2 r-fastest gather tasks, 4 CTA-staged push for few RHS,
+  //   8 non-persistent Toeplitz modes for M <= 48, 512 runtime RHS count in the gather, 1024 lean
+  //   gather, 2048 direct (unstaged) push for few RHS, 4096 one node column per merge CTA
+  std::atomic<int> d3{0};
   // D-SKIP Hadamard kernels: 0 = TMA-ring DMMA (v3, falling back to v2 for odd
   // sizes), 3 = cp.async DMMA (v2), 1 = first generation
   std::atomic<int> dskip{0};

@@ -55,8 +55,11 @@ const char* gk_version(void);
  * vector step where supported, 2 = separate kernels, 3 = vector step v1,
  * 5 = persistent MVM + vector step for the 2-D D-SKI operator), "dskip" (D-SKIP Hadamard
  * kernels: 0 = TMA-ring DMMA, 3 = cp.async DMMA, 1 = first generation),
- * "e2e_chunk" (gk_op_mvm host-buffer pipeline chunk, 0 = auto), "fused_prof"
- * and "f2_*" decomposition overrides. Returns the old value. */
+ * "e2e_chunk" (gk_op_mvm host-buffer pipeline chunk, 0 = auto), "e2e_stage"
+ * (1 = pageable caller buffers go straight to cudaMemcpyAsync instead of the
+ * pinned staging of the host copy pool), "d3" (bitmask restoring earlier d = 3
+ * MVM variants, see gk_common.hpp), "fused_prof" and "f2_*" decomposition
+ * overrides. Returns the old value. */
 int gk_set_tuning(const char* key, int value);
 /* Number of CUDA kernels this library has launched in this process. */
 int64_t gk_kernel_launch_count(void);

@@ -524,7 +524,9 @@ void toeplitz_mode(const double* t, int M, int band, i64 P, i64 Q, const double*
     // 48-node modes at 17 RHS 48.1 -> 46.1 µs (the 64-column persistent tile,
     // 152 registers, measured 52.3); bit-identical
     if (variant == 0 && M <= 48 && !(g_tuning.d3.load() & 8)) {
-      launch_toeplitz_pers<3, 2>(t, M, P, Q, X, Y, s);
+      // 16-column tiles when 32-column ones would leave SMs idle (1 RHS: 72 tiles)
+      if (ncols < 148 * 32 && !(g_tuning.d3.load() & 8192)) launch_toeplitz_pers<3, 1>(t, M, P, Q, X, Y, s);
+      else launch_toeplitz_pers<3, 2>(t, M, P, Q, X, Y, s);
       return;
     }
     if (M <= 48) { if (wide) launch_toeplitz_dmma<3, 4>(t, M, band, P, Q, X, Y, s); else launch_toeplitz_dmma<3, 2>(t, M, band, P, Q, X, Y, s); }

@@ -1844,6 +1844,89 @@ __global__ void __launch_bounds__(G3U_THREADS) k_gather_units3(DskiView op, cons
   }
 }
 
+// Few right-hand sides: a warp per unit (4 per CTA). The CTA-per-unit gather
+// above runs ~10 tasks per unit at 1 RHS, leaving three of its four warps
+// idle in every CTA slot; here each warp stages its unit's block with
+// cp.async and runs the unit's (point, RHS) tasks alone. Same per-task
+// arithmetic and order as k_gather_units3.
+template <int T, bool GRAD>
+__global__ void __launch_bounds__(128) k_gather_units3w(DskiView op, const int4* __restrict__ units, int nunits,
+                                                         const int2* __restrict__ urange,
+                                                         const double* __restrict__ w,
+                                                         const double* __restrict__ v,
+                                                         double* __restrict__ out, int nrhs, int noise, int zmax) {
+  extern __shared__ double blkw[];  // per warp [T][T][zmax][nrhs]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* blk = blkw + (size_t)warp * T * T * zmax * nrhs;
+  const int m1 = op.m[1], m2 = op.m[2];
+  constexpr int REC = 3 * 2 * T;
+  const size_t gstride = (size_t)op.n * nrhs;
+  for (int u = blockIdx.x * 4 + warp; u < nunits; u += gridDim.x * 4) {
+    const int4 U = __ldg(units + u);
+    const int2 pr = __ldg(urange + u);
+    const int za = U.z, nzb = min(U.w - U.z + T - 1, zmax);
+    const int run = nzb * nrhs;
+    __syncwarp();  // the previous unit's tasks are done with the block
+    for (int ab = 0; ab < T * T; ++ab) {
+      const int a = ab / T, b = ab - a * T;
+      const double* src = w + (((size_t)(U.x + a) * m1 + (U.y + b)) * m2 + za) * nrhs;
+      for (int q = lane; q < run; q += 32) g3_cp8(blk + ab * run + q, src + q);
+    }
+    g3_cp_wait_all();
+    __syncwarp();
+    const int ntask = (pr.y - pr.x) * nrhs;
+    for (int t = lane; t < ntask; t += 32) {
+      const int pl = t / nrhs, r = t - pl * nrhs;
+      const int sidx = pr.x + pl;
+      const double* rec = op.wts + (size_t)sidx * REC;
+      const int zo = __ldg(&op.base[sidx].z) - za;
+      double wr_[REC];
+#pragma unroll
+      for (int q = 0; q < REC; ++q) wr_[q] = __ldg(rec + q);
+      double o[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int t0 = 0; t0 < T; ++t0) {
+        double R0 = 0.0, R1 = 0.0, R2 = 0.0;
+#pragma unroll
+        for (int t1 = 0; t1 < T; ++t1) {
+          const double* wr = blk + ((t0 * T + t1) * nzb + zo) * nrhs + r;
+          double uu[T];
+#pragma unroll
+          for (int t2 = 0; t2 < T; ++t2) uu[t2] = wr[t2 * nrhs];
+          double rr = 0.0, qq = 0.0;
+#pragma unroll
+          for (int t2 = 0; t2 < T; ++t2) {
+            rr += wr_[4 * T + t2] * uu[t2];
+            if constexpr (GRAD) qq += wr_[5 * T + t2] * uu[t2];
+          }
+          const double w1 = wr_[2 * T + t1];
+          R0 += w1 * rr;
+          if constexpr (GRAD) {
+            R1 += wr_[3 * T + t1] * rr;
+            R2 += w1 * qq;
+          }
+        }
+        const double w0 = wr_[t0];
+        o[0] += w0 * R0;
+        if constexpr (GRAD) {
+          o[1] += wr_[T + t0] * R0;
+          o[2] += w0 * R1;
+          o[3] += w0 * R2;
+        }
+      }
+      constexpr int NG = GRAD ? 4 : 1;
+      const size_t idx0 = (size_t)sidx * nrhs + r;
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        const size_t idx = idx0 + g * gstride;
+        double val = o[g];
+        if (noise) val += (g == 0 ? op.nv2 : op.ng2) * __ldg(v + idx);
+        out[idx] = val;
+      }
+    }
+  }
+}
+
 // d = 3 scatter Bᵀv (dski.cpp:213-219) as a push per cell-line unit plus a
 // deterministic merge. Push: CTA per unit (the gather's units: a run of
 // occupied base cells of one cell line); its points are staged in shared
@@ -2424,6 +2507,23 @@ void DskiOp::gather(const double* w, const double* v, double* out, int nrhs, boo
   }
   // (every RHS count since the cp.async staging: 1 RHS 34.8 -> 30.8 µs and
   // 3 RHS 43.0 -> 32.7 µs against the lean gather)
+  if (d == 3 && variant == 0 && g3_units.p && nrhs <= 4 && !(g_tuning.d3.load() & (1024 | 16384))) {
+    const size_t smem = sizeof(double) * 4 * size_t(T) * T * g3_zspan * nrhs;
+    const void* fn = T == 6 ? (G ? (const void*)k_gather_units3w<6, true> : (const void*)k_gather_units3w<6, false>)
+                            : (G ? (const void*)k_gather_units3w<4, true> : (const void*)k_gather_units3w<4, false>);
+    raise_smem_limit(fn, smem);
+    const unsigned grid = static_cast<unsigned>(std::max(1, (g3_nunits + 3) / 4));
+    const int nz = noise ? 1 : 0;
+    if (T == 6) {
+      if (G) k_gather_units3w<6, true><<<grid, 128, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, w, v, out, nrhs, nz, g3_zspan);
+      else k_gather_units3w<6, false><<<grid, 128, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, w, v, out, nrhs, nz, g3_zspan);
+    } else {
+      if (G) k_gather_units3w<4, true><<<grid, 128, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, w, v, out, nrhs, nz, g3_zspan);
+      else k_gather_units3w<4, false><<<grid, 128, smem, s>>>(vw, g3_units.p, g3_nunits, g3_range.p, w, v, out, nrhs, nz, g3_zspan);
+    }
+    launched("dski gather (d=3 cell-line units, warp per unit)");
+    return;
+  }
   if (d == 3 && variant == 0 && g3_units.p && !(g_tuning.d3.load() & 1024)) {
     // RHS chunks of ≤ 17 columns (blockIdx.y): 64 RHS staged whole took
     // 166 KB per CTA (one CTA per SM)

@@ -53,7 +53,8 @@ struct Tuning {
   // d = 3 MVM A/B bitmask (0 = the measured default; each bit restores the variant it replaced):
   //   1 list-walk merge (k_scatter_merge3), 2 r-fastest gather tasks, 4 CTA-staged push for few RHS,
   //   8 non-persistent Toeplitz modes for M <= 48, 512 runtime RHS count in the gather, 1024 lean
-  //   gather, 2048 direct (unstaged) push for few RHS, 4096 one node column per merge CTA
+  //   gather, 2048 direct (unstaged) push for few RHS, 4096 one node column per merge CTA, 8192 32-column
+  //   Toeplitz tiles at small column counts, 16384 CTA-per-unit gather for few RHS
   std::atomic<int> d3{0};
   // D-SKIP Hadamard kernels: 0 = TMA-ring DMMA (v3, falling back to v2 for odd
   // sizes), 3 = cp.async DMMA (v2), 1 = first generation

@@ -266,7 +266,7 @@ def test_d3_unit_paths_bit_identical_and_match_oracle(nrhs, order):
     ref = r.mvm(V)
     default = g.mvm(V)
     assert rel(default, ref) <= TOL
-    prev = gk.set_tuning("d3", 1 | 4 | 512 | 1024 | 4096)
+    prev = gk.set_tuning("d3", 1 | 4 | 512 | 4096 | 16384)
     try:
         old = g.mvm(V)
     finally:
